@@ -1,0 +1,184 @@
+/*
+ * mrpt_cuda.h — C ABI of libmrpt_cuda.so, the sm_100a implementation of the
+ * MRPT (arXiv 1509.06957) batched index-build and k-NN query hot path.
+ *
+ * The reference plugs its hot kernels in at `mrpt._kernels`
+ * (pkg/src/mrpt/_kernels/__init__.py:71-88), one call per tree / per query,
+ * implemented by pkg/src/mrpt/_kernels/_cy.pyx:18-106.  Each entry point below
+ * replaces one of those kernels (or the numpy code around them) for a whole
+ * BATCH of trees or queries; the replaced interface is cited per function.
+ *
+ * Conventions (all functions):
+ *   - return an int32 status: MRPT_OK (0) or a negative MRPT_E* code; the
+ *     message for the calling thread is available from mrpt_last_error();
+ *   - every pointer argument is caller-owned DEVICE memory unless the comment
+ *     says "host"; the library never allocates or frees caller memory;
+ *   - work is enqueued on `stream` (a cudaStream_t, NULL = legacy default) and
+ *     the call returns without synchronising; host-side argument validation
+ *     fails fast before anything is enqueued;
+ *   - calls are reentrant: there is no global mutable state;
+ *   - leaf ids of tree t live at leaf_indices[t*n + off] (64-bit addressing,
+ *     T*n reaches 1e10 at the largest configuration).
+ * Status codes map onto the reference exception taxonomy
+ * (pkg/src/mrpt/exceptions.py:1-29) in the Python layer.
+ */
+#ifndef MRPT_CUDA_H
+#define MRPT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  MRPT_OK = 0,
+  MRPT_EPARAM = -1,     /* -> ParameterError  */
+  MRPT_ESHAPE = -2,     /* -> ShapeError      */
+  MRPT_EINTEGRITY = -3, /* -> IntegrityError  */
+  MRPT_EWORKSPACE = -4, /* workspace too small */
+  MRPT_ECUDA = -10,     /* CUDA launch / runtime failure */
+  MRPT_ENCCL = -11
+};
+
+/* Thread-local text of the last failing call on this thread ("" if none). */
+const char *mrpt_last_error(void);
+/* ABI version (major*100 + minor). */
+int32_t mrpt_abi_version(void);
+
+/* ------------------------------------------------------------------ K1 --
+ * Sparse projection with float64 accumulation in stored CSC order and one
+ * final rounding to float32; bit-identical to _cy.project
+ * (pkg/src/mrpt/_kernels/_cy.pyx:18-34) and to core.project_dataset /
+ * project_query (pkg/src/mrpt/core.py:235-260).
+ *   out[i*out_row_stride + c*out_col_stride] =
+ *       (float) sum_{s in [col_ptr[c], col_ptr[c+1])} (double)X[i*ldx+rows[s]] * (double)vals[s]
+ * A batch of trees is one call: concatenate their CSC columns (col_ptr holds
+ * global offsets).  Reference layout (m, ncols) row-major: row stride ncols,
+ * col stride 1; the build's level-major layout: row stride 1, col stride n. */
+int32_t mrpt_project(const float *X, int64_t m, int32_t d, int64_t ldx,
+                     const int64_t *col_ptr, const int32_t *rows,
+                     const float *vals, int32_t ncols, float *out,
+                     int64_t out_row_stride, int64_t out_col_stride,
+                     void *stream);
+
+/* ------------------------------------------------------------------ K2 --
+ * Heap descent: replaces _cy.route (pkg/src/mrpt/_kernels/_cy.pyx:37-54).
+ * proj (nrows, depth) row-major, splits (nrows, n_internal) row-major,
+ * out (nrows) int64 leaf ids; p <= split goes left. */
+int32_t mrpt_route(const float *proj, int64_t nrows, int32_t depth,
+                   const float *splits, int64_t n_internal, int64_t *out,
+                   void *stream);
+
+/* Fused query projection + descent over all T trees for nq queries:
+ * replaces search._route_all (pkg/src/mrpt/search.py:116-120), i.e. T calls
+ * of project_query (core.py:247-260) followed by _cy.route.
+ * Q (nq, d) with row stride ldq; CSC of all trees concatenated (tree t owns
+ * columns t*depth .. t*depth+depth-1); splits (T, 2^depth-1);
+ * leaves (nq, T) int32. */
+int32_t mrpt_query_route(const float *Q, int64_t nq, int32_t d, int64_t ldq,
+                         const int64_t *col_ptr, const int32_t *rows,
+                         const float *vals, const float *splits, int32_t T,
+                         int32_t depth, int32_t *leaves, void *stream);
+
+/* ------------------------------------------------------------------ K5 --
+ * Level-synchronous construction of Tb trees at once: per level, per node,
+ * the lower median (kth = (m+1)/2-1 smallest) of the node's projections by
+ * exact radix select, then a stable partition (value <= split goes left);
+ * replaces build_tree / median_split (pkg/src/mrpt/trees.py:33-98).
+ *   P:            (Tb, depth, n) float32, P[(t*depth+lev)*n + i]
+ *   splits:       (Tb, 2^depth-1) float32, heap order
+ *   leaf_offsets: (Tb, 2^depth+1) int64
+ *   leaf_indices: (Tb, n) int32 (leaf slices ascending point ids)
+ * Workspace: query its size first. */
+int32_t mrpt_build_workspace_size(int64_t n, int32_t Tb, int32_t depth,
+                                  size_t *bytes /* host */);
+int32_t mrpt_build_levels(const float *P, int64_t n, int32_t Tb,
+                          int32_t depth, float *splits, int64_t *leaf_offsets,
+                          int32_t *leaf_indices, void *ws, size_t ws_bytes,
+                          void *stream);
+
+/* ------------------------------------------------------------------ K3 --
+ * Vote counting for nq queries; replaces VoteAccumulator.accumulate +
+ * _cy.vote (pkg/src/mrpt/search.py:75-86, _kernels/_cy.pyx:57-78).
+ * Every occurrence of a point id in the query's T leaves counts one vote;
+ * cand[q*cap ..] receives the ids with >= v votes (unordered), ncand[q]
+ * their number.  leaves_sorted != 0 promises every leaf slice is ascending
+ * (true for indexes built by mrpt_build_levels) and enables the id-tiled
+ * sweep; max_count bounds any point's vote count (T for strictly ascending
+ * slices) and picks the counter width.  cap should bound the candidate count
+ * (min(n, sum of the query's leaf sizes / v) is always safe): ncand[q] is the
+ * true count, and when it exceeds cap only cap ids were stored -- the caller
+ * must treat that as an error (consumers clamp to cap). */
+int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_offsets,
+                  int64_t n, int32_t T, int32_t depth, const int32_t *leaves,
+                  int64_t nq, int32_t v, int32_t leaves_sorted,
+                  int64_t max_count, int32_t *cand, int64_t cap,
+                  int32_t *ncand, void *stream);
+
+/* Dense per-point vote counts for one query (VoteAccumulator.counts(),
+ * pkg/src/mrpt/search.py:68-73): counts (n) int32 is zeroed then filled. */
+int32_t mrpt_vote_counts(const int32_t *leaf_indices,
+                         const int64_t *leaf_offsets, int64_t n, int32_t T,
+                         int32_t depth, const int32_t *leaves, int32_t *counts,
+                         void *stream);
+
+/* Ordered compaction: out receives, ascending, the i with counts[i] >= v;
+ * *nout (device) their number.  (np.flatnonzero(counts >= v), _py.py:93) */
+int32_t mrpt_select_ge(const int32_t *counts, int64_t n, int32_t v,
+                       int32_t *out, int64_t *nout, void *stream);
+
+/* ------------------------------------------------------------------ K4 --
+ * Squared distances in float64 with the reference's sequential summation
+ * order: replaces _cy.scan (pkg/src/mrpt/_kernels/_cy.pyx:81-97).
+ * out[j] = sum_c ((double)X[cand[j]*ldx+c] - (double)q[c])^2, c ascending. */
+int32_t mrpt_scan(const float *X, int64_t n, int32_t d, int64_t ldx,
+                  const int64_t *cand, int64_t m, const float *q,
+                  double *out, void *stream);
+
+/* Exact k-NN over per-query candidate lists: replaces exact_knn_in_set's
+ * scan + lexsort + sqrt (pkg/src/mrpt/search.py:146-172) for nq queries.
+ * cand (nq, cap) int32 ids (unique per query), ncand (nq) int32, or
+ * cand == NULL to scan all n points (brute force, evaluation.py:28-47).
+ * Output per query, ascending (d^2, id): ids (nq, k) int64 padded with -1,
+ * dists (nq, k) float64 = sqrt(d^2) padded with +inf. */
+int32_t mrpt_scan_topk(const float *X, int64_t n, int32_t d, int64_t ldx,
+                       const float *Q, int64_t nq, int64_t ldq,
+                       const int32_t *cand, int64_t cap, const int32_t *ncand,
+                       int32_t k, int64_t *ids, double *dists, void *stream);
+
+/* Sorted de-duplication of arbitrary candidate ids (np.unique,
+ * search.py:157) through an n-bit bitmap.  ids outside [0, n) set
+ * *bad (device int32) to 1 (IntegrityError, search.py:158-162).
+ * bitmap: ceil(n/32) uint32 of workspace. */
+int32_t mrpt_unique_ids(const int64_t *cand, int64_t m, int64_t n,
+                        uint32_t *bitmap, int32_t *out, int64_t *nout,
+                        int32_t *bad, void *stream);
+
+/* ------------------------------------------------------------------ K6 --
+ * 64-bit FNV-1a over nbytes raw bytes (Dataset.checksum / _cy.fnv1a64,
+ * pkg/src/mrpt/core.py:77-82, _kernels/_cy.pyx:100-106), computed in
+ * parallel: per chunk a 256-entry table of (low-byte out, affine offset),
+ * composed in order.  *out (device uint64). */
+int32_t mrpt_fnv1a64_workspace_size(int64_t nbytes, size_t *bytes /* host */);
+int32_t mrpt_fnv1a64(const uint8_t *buf, int64_t nbytes, uint64_t *out,
+                     void *ws, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------- helpers --
+ * Dataset validation (core.py:63): *bad (device int32) = 1 if any element of
+ * X (m*d float32) is not finite. */
+int32_t mrpt_check_finite(const float *X, int64_t count, int32_t *bad,
+                          void *stream);
+
+/* Leaf-slice audit for indexes not built by mrpt_build_levels (hand-built or
+ * loaded): flags[0] = 1 if some slice is not strictly ascending, flags[1] =
+ * 1 if some id is outside [0, n).  flags: 2 int32, zeroed by the call. */
+int32_t mrpt_audit_leaves(const int32_t *leaf_indices,
+                          const int64_t *leaf_offsets, int64_t n, int32_t T,
+                          int32_t depth, int32_t *flags, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MRPT_CUDA_H */

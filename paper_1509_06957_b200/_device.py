@@ -1,0 +1,66 @@
+"""Device buffers and host<->device plumbing (torch is only the carrier)."""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+
+
+def torch_mod():
+    return _native.require_device()
+
+
+def device():
+    torch = torch_mod()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def is_tensor(x):
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor)
+
+
+def h2d(arr, dtype=None):
+    """Copy a host array to the current device (pinned staging for big arrays)."""
+    torch = torch_mod()
+    a = np.ascontiguousarray(arr if dtype is None else np.asarray(arr, dtype=dtype))
+    t = torch.from_numpy(a)
+    if a.nbytes >= (1 << 20):
+        t = t.pin_memory()
+        return t.to(device(), non_blocking=True)
+    return t.to(device())
+
+
+def d2h(t):
+    return t.detach().cpu().numpy()
+
+
+def empty(shape, dtype):
+    torch = torch_mod()
+    return torch.empty(shape, dtype=dtype, device=device())
+
+
+def concat_csc(matrices):
+    """Host CSC arrays of several SparseProjectionMatrix concatenated column-wise
+    with global offsets (tree t owns columns t*depth .. t*depth+depth-1)."""
+    ptrs, rows, vals = [np.zeros(1, np.int64)], [], []
+    base = 0
+    for R in matrices:
+        cp = np.asarray(R.col_ptr, dtype=np.int64)
+        ptrs.append(cp[1:] + base)
+        rows.append(np.asarray(R.row_idx, dtype=np.int32))
+        vals.append(np.asarray(R.values, dtype=np.float32))
+        base += int(cp[-1])
+    col_ptr = np.concatenate(ptrs)
+    row_idx = np.concatenate(rows) if base else np.zeros(1, np.int32)
+    values = np.concatenate(vals) if base else np.zeros(1, np.float32)
+    return col_ptr, row_idx, values
+
+
+def csc_device(matrices):
+    cp, r, v = concat_csc(matrices)
+    return h2d(cp), h2d(r), h2d(v)

@@ -1,0 +1,250 @@
+// K1 (sparse projection, fp64-exact) and K2 (routing / fused query descent).
+//
+// Parity contract (_cy.pyx:27-33, setup.py:37-39): every
+// output is a float64 sum of products (double)x * (double)r taken in stored
+// CSC order starting from +0.0, rounded once to float32.  A float*float
+// product is exact in float64 (24+24 < 53 mantissa bits), so one fused
+// multiply-add per term rounds exactly like the reference's separate
+// multiply and add -- the chain below is bit-identical to _cy.project.
+#include "common.cuh"
+
+namespace mrpt {
+
+// ---------------------------------------------------------------- K1 ------
+// One CTA owns a tile of `tp` points staged in shared memory (row stride
+// `stride`, odd, so lanes reading different points at the same coordinate
+// hit distinct banks).  Thread (pg, cg) computes points pg + j*npg for
+// j < PPT (independent fp64 chains hide DFMA latency) and columns
+// cg, cg+G, ...; consecutive lanes own consecutive points, so column-major
+// outputs (the build layout) are written coalesced.  The CSC entry of the
+// current column is uniform across the warp (broadcast load).
+template <int PPT>
+__global__ void __launch_bounds__(256)
+k_project_smem(const float *__restrict__ X, int64_t m, int d, int64_t ldx,
+               const int64_t *__restrict__ col_ptr, const int32_t *__restrict__ rows,
+               const float *__restrict__ vals, int ncols, float *__restrict__ out,
+               int64_t ors, int64_t ocs, int tp, int stride) {
+  extern __shared__ float xs[];
+  const int npg = tp / PPT;
+  const int G = blockDim.x / npg;
+  const int pg = threadIdx.x % npg, cg = threadIdx.x / npg;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  for (int64_t tile = blockIdx.x; tile * tp < m; tile += gridDim.x) {
+    const int64_t i0 = tile * tp;
+    const int here = (int)((m - i0) < tp ? (m - i0) : tp);
+    __syncthreads();
+    for (int r = warp; r < here; r += nwarps) {
+      const float *src = X + (i0 + r) * ldx;
+      float *dst = xs + r * stride;
+      for (int c = lane; c < d; c += 32) dst[c] = __ldg(src + c);
+    }
+    __syncthreads();
+    if (cg >= G) continue;
+    for (int c = cg; c < ncols; c += G) {
+      const int64_t s0 = __ldg(col_ptr + c), s1 = __ldg(col_ptr + c + 1);
+      double acc[PPT];
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) acc[j] = 0.0;
+      for (int64_t s = s0; s < s1; ++s) {
+        const int r = __ldg(rows + s);
+        const double v = (double)__ldg(vals + s);
+#pragma unroll
+        for (int j = 0; j < PPT; ++j)
+          acc[j] = __fma_rn((double)xs[(pg + j * npg) * stride + r], v, acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        const int p = pg + j * npg;
+        if (p < here) out[(i0 + p) * ors + (int64_t)c * ocs] = __double2float_rn(acc[j]);
+      }
+    }
+  }
+}
+
+// Fallback for rows too wide to stage (d beyond ~1.6K): one thread per
+// (point, column), coordinates read through the read-only path.
+__global__ void __launch_bounds__(256)
+k_project_global(const float *__restrict__ X, int64_t m, int64_t ldx,
+                 const int64_t *__restrict__ col_ptr, const int32_t *__restrict__ rows,
+                 const float *__restrict__ vals, int ncols, float *__restrict__ out,
+                 int64_t ors, int64_t ocs) {
+  const int64_t total = m * ncols;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(g / m);
+    const int64_t i = g - (int64_t)c * m;
+    const float *xr = X + i * ldx;
+    double acc = 0.0;
+    for (int64_t s = col_ptr[c]; s < col_ptr[c + 1]; ++s)
+      acc = __fma_rn((double)__ldg(xr + rows[s]), (double)vals[s], acc);
+    out[i * ors + (int64_t)c * ocs] = __double2float_rn(acc);
+  }
+}
+
+// ---------------------------------------------------------------- K2 ------
+// _cy.route: node = 2*node + 1 + (p > split); leaf = node - n_internal.
+__global__ void k_route(const float *__restrict__ proj, int64_t nrows, int depth,
+                        const float *__restrict__ splits, int64_t n_internal,
+                        int64_t *__restrict__ out) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t node = 0;
+    for (int lev = 0; lev < depth; ++lev) {
+      const float p = proj[r * depth + lev];
+      node = 2 * node + 1 + (p > splits[r * n_internal + node] ? 1 : 0);
+    }
+    out[r] = node - n_internal;
+  }
+}
+
+// Fused query projection + descent.  CTA = QB queries x 128 trees; the QB
+// query rows are staged in shared memory, each thread walks one tree for all
+// QB queries at once (QB independent fp64 chains, CSC entries loaded once).
+template <int QB, bool SMEM>
+__global__ void __launch_bounds__(128)
+k_query_route(const float *__restrict__ Q, int64_t nq, int d, int64_t ldq,
+              const int64_t *__restrict__ col_ptr, const int32_t *__restrict__ rows,
+              const float *__restrict__ vals, const float *__restrict__ splits, int T,
+              int depth, int32_t *__restrict__ leaves, int stride) {
+  extern __shared__ float qs[];
+  const int64_t q0 = (int64_t)blockIdx.y * QB;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nint = ((int64_t)1 << depth) - 1;
+  if (SMEM) {
+    for (int qi = 0; qi < QB; ++qi) {
+      const bool live = q0 + qi < nq;
+      const float *src = Q + (q0 + qi) * ldq;
+      for (int c = threadIdx.x; c < d; c += blockDim.x)
+        qs[qi * stride + c] = live ? __ldg(src + c) : 0.0f;
+    }
+    __syncthreads();
+  }
+  if (t >= T) return;
+  int64_t node[QB];
+#pragma unroll
+  for (int qi = 0; qi < QB; ++qi) node[qi] = 0;
+  const float *tsplit = splits + (int64_t)t * nint;
+  for (int lev = 0; lev < depth; ++lev) {
+    const int64_t c = (int64_t)t * depth + lev;
+    const int64_t s0 = __ldg(col_ptr + c), s1 = __ldg(col_ptr + c + 1);
+    double acc[QB];
+#pragma unroll
+    for (int qi = 0; qi < QB; ++qi) acc[qi] = 0.0;
+    for (int64_t s = s0; s < s1; ++s) {
+      const int r = __ldg(rows + s);
+      const double v = (double)__ldg(vals + s);
+#pragma unroll
+      for (int qi = 0; qi < QB; ++qi) {
+        float x;
+        if (SMEM) {
+          x = qs[qi * stride + r];
+        } else {
+          x = (q0 + qi < nq) ? __ldg(Q + (q0 + qi) * ldq + r) : 0.0f;
+        }
+        acc[qi] = __fma_rn((double)x, v, acc[qi]);
+      }
+    }
+#pragma unroll
+    for (int qi = 0; qi < QB; ++qi) {
+      const float p = __double2float_rn(acc[qi]);
+      node[qi] = 2 * node[qi] + 1 + (p > __ldg(tsplit + node[qi]) ? 1 : 0);
+    }
+  }
+#pragma unroll
+  for (int qi = 0; qi < QB; ++qi)
+    if (q0 + qi < nq) leaves[(q0 + qi) * T + t] = (int32_t)(node[qi] - nint);
+}
+
+}  // namespace mrpt
+
+using namespace mrpt;
+
+static const int kProjSmemBudget = 100 * 1024;  // two CTAs per SM
+
+extern "C" int32_t mrpt_project(const float *X, int64_t m, int32_t d, int64_t ldx,
+                                const int64_t *col_ptr, const int32_t *rows, const float *vals,
+                                int32_t ncols, float *out, int64_t out_row_stride,
+                                int64_t out_col_stride, void *stream) {
+  clear_error();
+  if (m < 0 || d < 1 || ldx < d || ncols < 0)
+    return fail(MRPT_ESHAPE, "mrpt_project: bad shape");
+  if (m == 0 || ncols == 0) return MRPT_OK;
+  if (!X || !col_ptr || !out) return fail(MRPT_EPARAM, "mrpt_project: null pointer");
+  cudaStream_t s = as_stream(stream);
+  const int stride = (d & 1) ? d : d + 1;
+  const int64_t row_bytes = (int64_t)stride * 4;
+  // tile of 256, 128 or 64 points (point groups must be a power-of-two
+  // multiple of the warp so every thread has a column group)
+  int tp = 256;
+  while (tp >= 64 && (int64_t)tp * row_bytes > kProjSmemBudget) tp >>= 1;
+  if (tp >= 64) {
+    const size_t smem = (size_t)tp * row_bytes;
+    const int64_t tiles = ceil_div<int64_t>(m, tp);
+    const int grid = (int)(tiles < (int64_t)num_sms() * 2 ? tiles : (int64_t)num_sms() * 2);
+    cudaFuncSetAttribute(k_project_smem<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_project_smem<2><<<grid, 256, smem, s>>>(X, m, d, ldx, col_ptr, rows, vals, ncols, out,
+                                               out_row_stride, out_col_stride, tp, stride);
+  } else if (32 * row_bytes <= 200 * 1024) {
+    tp = 32;
+    const size_t smem = (size_t)tp * row_bytes;
+    const int64_t tiles = ceil_div<int64_t>(m, tp);
+    const int grid = (int)(tiles < (int64_t)num_sms() ? tiles : (int64_t)num_sms());
+    cudaFuncSetAttribute(k_project_smem<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_project_smem<1><<<grid, 256, smem, s>>>(X, m, d, ldx, col_ptr, rows, vals, ncols, out,
+                                               out_row_stride, out_col_stride, tp, stride);
+  } else {
+    const int64_t total = m * ncols;
+    const int64_t blocks = ceil_div<int64_t>(total, 256);
+    const int grid = (int)(blocks < (int64_t)num_sms() * 8 ? blocks : (int64_t)num_sms() * 8);
+    k_project_global<<<grid, 256, 0, s>>>(X, m, ldx, col_ptr, rows, vals, ncols, out,
+                                          out_row_stride, out_col_stride);
+  }
+  return launch_status("mrpt_project");
+}
+
+extern "C" int32_t mrpt_route(const float *proj, int64_t nrows, int32_t depth, const float *splits,
+                              int64_t n_internal, int64_t *out, void *stream) {
+  clear_error();
+  if (nrows < 0 || depth < 0 || n_internal < 0) return fail(MRPT_ESHAPE, "mrpt_route: bad shape");
+  if (nrows == 0) return MRPT_OK;
+  cudaStream_t s = as_stream(stream);
+  const int64_t blocks = ceil_div<int64_t>(nrows, 128);
+  const int grid = (int)(blocks < 65535 ? blocks : 65535);
+  k_route<<<grid, 128, 0, s>>>(proj, nrows, depth, splits, n_internal, out);
+  return launch_status("mrpt_route");
+}
+
+extern "C" int32_t mrpt_query_route(const float *Q, int64_t nq, int32_t d, int64_t ldq,
+                                    const int64_t *col_ptr, const int32_t *rows,
+                                    const float *vals, const float *splits, int32_t T,
+                                    int32_t depth, int32_t *leaves, void *stream) {
+  clear_error();
+  if (nq < 0 || d < 1 || ldq < d || T < 1 || depth < 1 || depth > 30)
+    return fail(MRPT_ESHAPE, "mrpt_query_route: bad shape");
+  if (nq == 0) return MRPT_OK;
+  cudaStream_t s = as_stream(stream);
+  constexpr int QB = 4;
+  const int stride = (d & 1) ? d : d + 1;
+  const size_t smem = (size_t)QB * stride * sizeof(float);
+  const int64_t qblocks = ceil_div<int64_t>(nq, QB);
+  if (qblocks > 65535LL * 1024) return fail(MRPT_EPARAM, "mrpt_query_route: too many queries per call");
+  int64_t off = 0;
+  // gridDim.y is limited to 65535: split very large batches.
+  while (off < nq) {
+    const int64_t chunk_q = (nq - off) < 65535LL * QB ? (nq - off) : 65535LL * QB;
+    dim3 grid((unsigned)ceil_div<int>(T, 128), (unsigned)ceil_div<int64_t>(chunk_q, QB));
+    if (smem <= 160 * 1024) {
+      cudaFuncSetAttribute(k_query_route<QB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      k_query_route<QB, true><<<grid, 128, smem, s>>>(Q + off * ldq, chunk_q, d, ldq, col_ptr, rows,
+                                                      vals, splits, T, depth, leaves + off * T,
+                                                      stride);
+    } else {
+      k_query_route<QB, false><<<grid, 128, 0, s>>>(Q + off * ldq, chunk_q, d, ldq, col_ptr, rows,
+                                                    vals, splits, T, depth, leaves + off * T,
+                                                    stride);
+    }
+    off += chunk_q;
+  }
+  return launch_status("mrpt_query_route");
+}

@@ -1,0 +1,330 @@
+// K3: vote counting over the T leaves each query lands in
+// (replaces VoteAccumulator.accumulate + _cy.vote, search.py:75-86,
+// _kernels/_cy.pyx:57-78).
+//
+// One CTA per query.  Vote counters live in shared memory over a tile of W
+// point ids, packed 4 (u8), 2 (u16) or 1 (u32) per 32-bit word and bumped
+// with atomicAdd(word, 1 << lane_shift); the counter width is chosen so no
+// count can overflow into its neighbour.  When n > W the CTA sweeps the id
+// tiles in order with one cursor per tree: leaf slices built by K5 are
+// ascending, so the part of a slice inside the current tile is the next run
+// from the cursor.  A point is emitted exactly once, by the increment that
+// raises its count to v (the reference's `counts[idx] == v` test,
+// _cy.pyx:75-77).  Groups of G lanes share one tree slice (G ~ mean slice
+// length per tile) and each lane keeps U loads in flight.
+#include "common.cuh"
+
+namespace mrpt {
+
+struct VoteArgs {
+  const int32_t *leaf_indices;
+  const int64_t *leaf_offsets;
+  int64_t n;
+  int T, L;  // L = 2^depth leaves
+  const int32_t *leaves;
+  int64_t nq;
+  int v;
+  int32_t *cand;
+  int64_t cap;
+  int32_t *ncand;
+  int W, ntiles;
+};
+
+constexpr int kVoteNT = 512;
+constexpr int kVoteU = 4;
+
+template <int CW>
+__device__ __forceinline__ uint32_t bump(uint32_t *cnt, int local) {
+  if (CW == 1) {
+    const int sh = (local & 3) << 3;
+    const uint32_t old = atomicAdd(cnt + (local >> 2), 1u << sh);
+    return ((old >> sh) & 0xffu) + 1u;
+  } else if (CW == 2) {
+    const int sh = (local & 1) << 4;
+    const uint32_t old = atomicAdd(cnt + (local >> 1), 1u << sh);
+    return ((old >> sh) & 0xffffu) + 1u;
+  } else {
+    return atomicAdd(cnt + local, 1u) + 1u;
+  }
+}
+
+template <int CW, int G, bool SORTED>
+__global__ void __launch_bounds__(kVoteNT) k_vote(VoteArgs a) {
+  extern __shared__ uint4 vote_smem[];
+  uint32_t *cnt = reinterpret_cast<uint32_t *>(vote_smem);
+  const int cwords = a.W * CW / 4;  // W is a multiple of 64
+  int32_t *cur = reinterpret_cast<int32_t *>(cnt + cwords);
+  int32_t *endp = cur + a.T;
+  __shared__ int s_ncand;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int gl = lane & (G - 1);
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  const int gi = tid / G, ngroups = kVoteNT / G;
+  for (int64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
+    for (int t = tid; t < a.T; t += kVoteNT) {
+      const int leaf = a.leaves[q * a.T + t];
+      const int64_t *o = a.leaf_offsets + (int64_t)t * (a.L + 1);
+      cur[t] = (int32_t)o[leaf];
+      endp[t] = (int32_t)o[leaf + 1];
+    }
+    uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
+    for (int i = tid; i < cwords / 4; i += kVoteNT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (tid == 0) s_ncand = 0;
+    __syncthreads();
+    int32_t *qcand = a.cand + q * a.cap;
+    for (int tile = 0; tile < a.ntiles; ++tile) {
+      const int32_t lo = tile * a.W;
+      const int64_t hi64 = (int64_t)lo + a.W < a.n ? (int64_t)lo + a.W : a.n;
+      const int32_t hi = (int32_t)hi64;
+      for (int t = gi; t < a.T; t += ngroups) {
+        const int32_t *Lt = a.leaf_indices + (int64_t)t * a.n;
+        const int32_t e = endp[t];
+        if (SORTED) {
+          int32_t pos = cur[t];
+          while (pos < e) {
+            int32_t id[kVoteU];
+#pragma unroll
+            for (int u = 0; u < kVoteU; ++u) {
+              const int32_t idx = pos + gl + u * G;
+              id[u] = idx < e ? __ldg(Lt + idx) : 0x7fffffff;
+            }
+            int consumed = 0;
+#pragma unroll
+            for (int u = 0; u < kVoteU; ++u) {
+              const bool in = id[u] < hi;
+              if (in) {
+                if (bump<CW>(cnt, id[u] - lo) == (uint32_t)a.v) {
+                  const int slot = atomicAdd(&s_ncand, 1);
+                  if (slot < a.cap) qcand[slot] = id[u];
+                }
+              }
+              consumed += __popc(__ballot_sync(gmask, in) & gmask);
+            }
+            pos += consumed;
+            if (consumed < kVoteU * G) break;
+          }
+          if (gl == 0) cur[t] = pos;
+        } else {
+          // unsorted slices (foreign index): filter the whole slice per tile
+          for (int32_t idx = cur[t] + gl; idx < e; idx += G) {
+            const int32_t id = __ldg(Lt + idx);
+            if (id >= lo && id < hi) {
+              if (bump<CW>(cnt, id - lo) == (uint32_t)a.v) {
+                const int slot = atomicAdd(&s_ncand, 1);
+                if (slot < a.cap) qcand[slot] = id;
+              }
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (tile + 1 < a.ntiles) {
+        for (int i = tid; i < cwords / 4; i += kVoteNT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+      }
+    }
+    if (tid == 0) a.ncand[q] = s_ncand;  // > cap means only cap ids were stored
+    __syncthreads();
+  }
+}
+
+typedef void (*vote_fn)(VoteArgs);
+
+template <int CW, bool SORTED>
+static vote_fn pick_g(int G) {
+  switch (G) {
+    case 1: return k_vote<CW, 1, SORTED>;
+    case 2: return k_vote<CW, 2, SORTED>;
+    case 4: return k_vote<CW, 4, SORTED>;
+    case 8: return k_vote<CW, 8, SORTED>;
+    case 16: return k_vote<CW, 16, SORTED>;
+    default: return k_vote<CW, 32, SORTED>;
+  }
+}
+
+template <bool SORTED>
+static vote_fn pick_cw(int CW, int G) {
+  if (CW == 1) return pick_g<1, SORTED>(G);
+  if (CW == 2) return pick_g<2, SORTED>(G);
+  return pick_g<4, SORTED>(G);
+}
+
+// Dense counts for one query: one CTA per tree, global atomics.
+__global__ void k_vote_dense(const int32_t *__restrict__ leaf_indices,
+                             const int64_t *__restrict__ leaf_offsets, int64_t n, int L,
+                             const int32_t *__restrict__ leaves, int32_t *counts) {
+  const int t = blockIdx.x;
+  const int leaf = leaves[t];
+  const int64_t *o = leaf_offsets + (int64_t)t * (L + 1);
+  const int32_t *Lt = leaf_indices + (int64_t)t * n;
+  for (int64_t i = o[leaf] + threadIdx.x; i < o[leaf + 1]; i += blockDim.x) atomicAdd(counts + Lt[i], 1);
+}
+
+// Ordered compaction with one CTA of 1024 threads: rounds of 1024 elements,
+// ballot ranks, running base.
+__global__ void __launch_bounds__(1024) k_select_ge(const int32_t *__restrict__ counts, int64_t n,
+                                                    int v, int32_t *out, int64_t *nout) {
+  __shared__ int wcnt[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t base = 0;
+  for (int64_t r0 = 0; r0 < n; r0 += 1024) {
+    const int64_t i = r0 + threadIdx.x;
+    const bool f = i < n && counts[i] >= v;
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wcnt[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int w = 0; w < 32; ++w) {
+      before += w < warp ? wcnt[w] : 0;
+      tot += wcnt[w];
+    }
+    if (f) out[base + before + __popc(bal & lanemask_lt())] = (int32_t)i;
+    base += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *nout = base;
+}
+
+__global__ void k_mark_ids(const int64_t *__restrict__ cand, int64_t m, int64_t n, uint32_t *bitmap,
+                           int32_t *bad) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t id = cand[j];
+    if (id < 0 || id >= n) {
+      *bad = 1;
+    } else {
+      atomicOr(bitmap + (id >> 5), 1u << (id & 31));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_bitmap_compact(const uint32_t *__restrict__ bitmap,
+                                                         int64_t nwords, int32_t *out,
+                                                         int64_t *nout) {
+  __shared__ int wcnt[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t base = 0;
+  for (int64_t r0 = 0; r0 < nwords; r0 += 1024) {
+    const int64_t i = r0 + threadIdx.x;
+    uint32_t word = i < nwords ? bitmap[i] : 0u;
+    const int pc = __popc(word);
+    int incl = pc;
+    for (int o = 1; o < 32; o <<= 1) {
+      int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) wcnt[warp] = incl;
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int w = 0; w < 32; ++w) {
+      before += w < warp ? wcnt[w] : 0;
+      tot += wcnt[w];
+    }
+    int64_t pos = base + before + incl - pc;
+    while (word) {
+      const int b = __ffs(word) - 1;
+      out[pos++] = (int32_t)(i * 32 + b);
+      word &= word - 1;
+    }
+    base += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *nout = base;
+}
+
+}  // namespace mrpt
+
+using namespace mrpt;
+
+static const int kVoteSmemSingle = 110 * 1024;  // single tile: two CTAs per SM
+static const int kVoteSmemTiled = 200 * 1024;   // tiled sweep: one big CTA per SM
+
+extern "C" int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_offsets, int64_t n,
+                             int32_t T, int32_t depth, const int32_t *leaves, int64_t nq, int32_t v,
+                             int32_t leaves_sorted, int64_t max_count, int32_t *cand, int64_t cap,
+                             int32_t *ncand, void *stream) {
+  clear_error();
+  if (n < 1 || n >= (int64_t)1 << 31 || T < 1 || depth < 0 || depth > 30 || nq < 0)
+    return fail(MRPT_ESHAPE, "mrpt_vote: bad shape");
+  if (v < 1 || v > max_count) return fail(MRPT_EPARAM, "mrpt_vote: vote threshold out of range");
+  if (cap < 1) return fail(MRPT_EPARAM, "mrpt_vote: cap must be >= 1");
+  if (nq == 0) return MRPT_OK;
+  cudaStream_t s = as_stream(stream);
+  const int CW = max_count <= 255 ? 1 : (max_count <= 65535 ? 2 : 4);
+  const int64_t cursor_bytes = 8LL * T;
+  // widest tile that fits; a single tile if n fits the two-CTA budget
+  int64_t W;
+  int64_t budget = kVoteSmemSingle - cursor_bytes - 64;
+  if ((int64_t)ceil_div<int64_t>(n, 64) * 64 * CW <= budget) {
+    W = ceil_div<int64_t>(n, 64) * 64;
+  } else {
+    budget = kVoteSmemTiled - cursor_bytes - 64;
+    if (budget < 64 * CW) return fail(MRPT_EPARAM, "mrpt_vote: too many trees for shared cursors");
+    W = budget / CW / 64 * 64;
+  }
+  const int ntiles = (int)ceil_div<int64_t>(n, W);
+  const bool sorted = leaves_sorted != 0 || ntiles == 1;
+  // group size ~ mean slice length per tile (pow2 in [1, 32])
+  const double mean_leaf = (double)n / (double)((int64_t)1 << depth);
+  const double per_tile = mean_leaf / ntiles;
+  int G = 1;
+  while (G < 32 && G * kVoteU < per_tile) G <<= 1;
+  VoteArgs a;
+  a.leaf_indices = leaf_indices;
+  a.leaf_offsets = leaf_offsets;
+  a.n = n;
+  a.T = T;
+  a.L = 1 << depth;
+  a.leaves = leaves;
+  a.nq = nq;
+  a.v = v;
+  a.cand = cand;
+  a.cap = cap;
+  a.ncand = ncand;
+  a.W = (int)W;
+  a.ntiles = ntiles;
+  const size_t smem = (size_t)W * CW + (size_t)cursor_bytes;
+  vote_fn fn = sorted ? pick_cw<true>(CW, G) : pick_cw<false>(CW, G);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int per_sm = smem <= (size_t)kVoteSmemSingle ? 2 : 1;
+  const int64_t grid = nq < (int64_t)num_sms() * per_sm * 4 ? nq : (int64_t)num_sms() * per_sm * 4;
+  fn<<<(unsigned)grid, kVoteNT, smem, s>>>(a);
+  return launch_status("mrpt_vote");
+}
+
+extern "C" int32_t mrpt_vote_counts(const int32_t *leaf_indices, const int64_t *leaf_offsets,
+                                    int64_t n, int32_t T, int32_t depth, const int32_t *leaves,
+                                    int32_t *counts, void *stream) {
+  clear_error();
+  if (n < 1 || T < 1 || depth < 0 || depth > 30) return fail(MRPT_ESHAPE, "mrpt_vote_counts: bad shape");
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(counts, 0, sizeof(int32_t) * n, s);
+  k_vote_dense<<<T, 256, 0, s>>>(leaf_indices, leaf_offsets, n, 1 << depth, leaves, counts);
+  return launch_status("mrpt_vote_counts");
+}
+
+extern "C" int32_t mrpt_select_ge(const int32_t *counts, int64_t n, int32_t v, int32_t *out,
+                                  int64_t *nout, void *stream) {
+  clear_error();
+  if (n < 0) return fail(MRPT_ESHAPE, "mrpt_select_ge: bad shape");
+  cudaStream_t s = as_stream(stream);
+  k_select_ge<<<1, 1024, 0, s>>>(counts, n, v, out, nout);
+  return launch_status("mrpt_select_ge");
+}
+
+extern "C" int32_t mrpt_unique_ids(const int64_t *cand, int64_t m, int64_t n, uint32_t *bitmap,
+                                   int32_t *out, int64_t *nout, int32_t *bad, void *stream) {
+  clear_error();
+  if (m < 0 || n < 1 || n >= (int64_t)1 << 31) return fail(MRPT_ESHAPE, "mrpt_unique_ids: bad shape");
+  cudaStream_t s = as_stream(stream);
+  const int64_t nwords = ceil_div<int64_t>(n, 32);
+  cudaMemsetAsync(bitmap, 0, sizeof(uint32_t) * nwords, s);
+  cudaMemsetAsync(bad, 0, sizeof(int32_t), s);
+  if (m > 0) {
+    const int64_t blocks = ceil_div<int64_t>(m, 256);
+    const int grid = (int)(blocks < (int64_t)num_sms() * 8 ? blocks : (int64_t)num_sms() * 8);
+    k_mark_ids<<<grid, 256, 0, s>>>(cand, m, n, bitmap, bad);
+  }
+  k_bitmap_compact<<<1, 1024, 0, s>>>(bitmap, nwords, out, nout);
+  return launch_status("mrpt_unique_ids");
+}

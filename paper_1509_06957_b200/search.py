@@ -1,0 +1,308 @@
+"""Query phase on the GPU (mirrors pkg/src/mrpt/search.py).
+
+A query is projected onto every tree's matrix and descends to one leaf per
+tree (K2, ``mrpt_query_route``); points sharing its leaf in at least
+``votes`` trees are the candidates (K3, ``mrpt_vote``); the answer is the
+exact float64 k-NN among them (K4, ``mrpt_scan_topk``).  The batched entry
+point :func:`approximate_knn_batch` runs the three kernels over a whole
+query matrix; the single-query functions keep the reference's signatures,
+results and error order.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device, _native
+from .core import _record_macs, as_dataset
+from .exceptions import IntegrityError, ParameterError, ShapeError
+
+__all__ = [
+    "NeighborList",
+    "VoteAccumulator",
+    "approximate_knn",
+    "approximate_knn_batch",
+    "candidate_set",
+    "exact_knn_in_set",
+    "tree_query",
+]
+
+
+@dataclass(frozen=True)
+class NeighborList:
+    """Result of one query: ids by ascending distance, ties by ascending id
+    (search.py:28-47)."""
+
+    indices: np.ndarray  # int64
+    distances: np.ndarray  # float64
+    requested_k: int
+    candidate_count: int
+
+    def __len__(self):
+        return int(self.indices.shape[0])
+
+    @property
+    def shortfall(self):
+        return max(0, self.requested_k - len(self))
+
+
+class VoteAccumulator:
+    """Per-point vote counts of the last query (search.py:50-86), held on the GPU.
+
+    ``accumulate`` counts every occurrence of every id in the given leaves
+    (one per tree) and returns, ascending, the ids with at least ``votes``.
+    """
+
+    def __init__(self, n):
+        self.n = n
+        self._counts = None
+        self._epoch = 0
+
+    def begin(self):
+        self._epoch += 1
+        return self._epoch
+
+    def _buf(self):
+        if self._counts is None:
+            self._counts = _device.empty((self.n,), _device.torch_mod().int32)
+        return self._counts
+
+    def counts(self):
+        """Dense n-vector of the current query's votes (int64 copy)."""
+        if self._counts is None or self._epoch == 0:
+            return np.zeros(self.n, dtype=np.int64)
+        return _device.d2h(self._counts).astype(np.int64)
+
+    def count(self, i):
+        if self._counts is None or self._epoch == 0:
+            return 0
+        return int(self._counts[int(i)].item())
+
+    def accumulate(self, index, leaves, votes):
+        torch = _device.torch_mod()
+        self.begin()
+        D = index.device_index()
+        lv = leaves if _device.is_tensor(leaves) else _device.h2d(np.asarray(leaves, np.int32))
+        lv = lv.to(torch.int32)
+        counts = self._buf()
+        stream = _native.stream_ptr()
+        _native.call("mrpt_vote_counts", _native.ptr(D.indices), _native.ptr(D.offsets), D.n, D.T,
+                     D.depth, _native.ptr(lv), _native.ptr(counts), stream)
+        out = torch.empty(D.n, dtype=torch.int32, device=counts.device)
+        nout = torch.zeros(1, dtype=torch.int64, device=counts.device)
+        _native.call("mrpt_select_ge", _native.ptr(counts), D.n, int(votes), _native.ptr(out),
+                     _native.ptr(nout), stream)
+        return _device.d2h(out[:int(nout.item())]).astype(np.int64)
+
+
+def _query_vector(q, d):
+    arr = np.asarray(q)
+    if arr.ndim != 1:
+        raise ShapeError(f"query must be 1-D, got shape {arr.shape}")
+    if arr.shape[0] != d:
+        raise ShapeError(f"query has length {arr.shape[0]}, expected {d}")
+    return np.ascontiguousarray(arr, dtype=np.float32)
+
+
+def _route_device(Qd, D):
+    """(nq, T) int32 leaves of a device query block (K2)."""
+    torch = _device.torch_mod()
+    nq = int(Qd.shape[0])
+    leaves = torch.empty((nq, D.T), dtype=torch.int32, device=Qd.device)
+    _native.call("mrpt_query_route", _native.ptr(Qd), nq, D.d, int(Qd.stride(0)),
+                 _native.ptr(D.col_ptr), _native.ptr(D.rows), _native.ptr(D.vals),
+                 _native.ptr(D.splits), D.T, D.depth, _native.ptr(leaves), _native.stream_ptr())
+    return leaves
+
+
+def _route_tree(q, tree):
+    """Leaf id of ``q`` in one tree (search.py:100-102), on the device."""
+    from .core import _project_device
+
+    qd = _device.h2d(np.ascontiguousarray(q, dtype=np.float32).reshape(1, -1))
+    _record_macs(tree.random_matrix.nnz)
+    proj = _project_device(qd, tree.random_matrix)
+    torch = _device.torch_mod()
+    sp = _device.h2d(np.ascontiguousarray(tree.splits, dtype=np.float32).reshape(1, -1))
+    out = torch.empty(1, dtype=torch.int64, device=qd.device)
+    _native.call("mrpt_route", _native.ptr(proj), 1, tree.depth, _native.ptr(sp),
+                 int(sp.shape[1]), _native.ptr(out), _native.stream_ptr())
+    return int(out.item())
+
+
+def tree_query(q, tree):
+    """Point ids of the leaf ``q`` reaches in one tree (search.py:105-113)."""
+    q = _query_vector(q, tree.random_matrix.d)
+    return tree.leaf(_route_tree(q, tree))
+
+
+def _accumulator(index):
+    acc = getattr(index._local, "acc", None)
+    if acc is None or acc.n != index.n:
+        acc = index._local.acc = VoteAccumulator(index.n)
+    return acc
+
+
+def candidate_set(q, index, votes, accumulator=None):
+    """Points sharing a leaf with ``q`` in at least ``votes`` trees, ascending,
+    plus the accumulator holding all counts (search.py:130-143)."""
+    if not 1 <= votes <= index.n_trees:
+        raise ParameterError(f"vote threshold must lie in [1, {index.n_trees}], got {votes}")
+    q = _query_vector(q, index.d)
+    D = index.device_index()
+    for R in index.matrices:
+        _record_macs(R.nnz)
+    leaves = _route_device(_device.h2d(q.reshape(1, -1)), D)[0]
+    acc = accumulator if accumulator is not None else _accumulator(index)
+    return acc.accumulate(index, leaves, votes), acc
+
+
+def _topk_device(Xd, Qd, cand, cap, ncand, k):
+    torch = _device.torch_mod()
+    nq = int(Qd.shape[0])
+    ids = torch.empty((nq, k), dtype=torch.int64, device=Qd.device)
+    dists = torch.empty((nq, k), dtype=torch.float64, device=Qd.device)
+    _native.call("mrpt_scan_topk", _native.ptr(Xd), int(Xd.shape[0]), int(Xd.shape[1]),
+                 int(Xd.stride(0)), _native.ptr(Qd), nq, int(Qd.stride(0)), _native.ptr(cand),
+                 int(cap), _native.ptr(ncand), int(k), _native.ptr(ids), _native.ptr(dists),
+                 _native.stream_ptr())
+    return ids, dists
+
+
+def exact_knn_in_set(q, k, candidates, X):
+    """Exact k-NN of ``q`` among ``candidates`` of ``X`` (search.py:146-172):
+    duplicates collapsed, out-of-range ids rejected, float64 distances,
+    (distance, id) order."""
+    if k < 1:
+        raise ParameterError(f"k must be >= 1, got {k}")
+    X = as_dataset(X)
+    q = _query_vector(q, X.d)
+    torch = _device.torch_mod()
+    c = np.asarray(candidates, dtype=np.int64).ravel()
+    if c.shape[0] == 0:
+        return NeighborList(indices=np.empty(0, np.int64), distances=np.empty(0, np.float64),
+                            requested_k=k, candidate_count=0)
+    Xd = X.device()
+    cd = _device.h2d(c)
+    bitmap = torch.empty((X.n + 31) // 32, dtype=torch.int32, device=Xd.device)
+    uniq = torch.empty(min(X.n, c.shape[0]) + 1, dtype=torch.int32, device=Xd.device)
+    nout = torch.zeros(1, dtype=torch.int64, device=Xd.device)
+    bad = torch.zeros(1, dtype=torch.int32, device=Xd.device)
+    stream = _native.stream_ptr()
+    _native.call("mrpt_unique_ids", _native.ptr(cd), c.shape[0], X.n, _native.ptr(bitmap),
+                 _native.ptr(uniq), _native.ptr(nout), _native.ptr(bad), stream)
+    if int(bad.item()):
+        raise IntegrityError(f"candidate indices must lie in [0, {X.n}), got range "
+                             f"[{int(c.min())}, {int(c.max())}]")
+    ncand = nout.to(torch.int32)
+    m = int(nout.item())
+    ids, dists = _topk_device(Xd, _device.h2d(q.reshape(1, -1)), uniq, uniq.shape[0], ncand, k)
+    kept = min(k, m)
+    return NeighborList(indices=_device.d2h(ids[0, :kept]), distances=_device.d2h(dists[0, :kept]),
+                        requested_k=k, candidate_count=m)
+
+
+def _check_batch_args(k, index, votes):
+    if k < 1:
+        raise ParameterError(f"k must be >= 1, got {k}")
+    if not 1 <= votes <= index.n_trees:
+        raise ParameterError(f"vote threshold must lie in [1, {index.n_trees}], got {votes}")
+
+
+def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
+    """K2 -> K3 -> K4 over a device query block; returns device tensors
+    (ids (nq,k) int64, dists (nq,k) float64, candidate_count (nq,) int32).
+    ``timer``: optional list receiving (stage, start_event, end_event) per launch."""
+    torch = _device.torch_mod()
+
+    def stage(name, fn, *a):
+        if timer is None:
+            return fn(*a)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn(*a)
+        e1.record()
+        timer.append((name, e0, e1))
+
+    nq = int(Qd.shape[0])
+    dev = Qd.device
+    cap = D.cap(votes)
+    if out is None:
+        ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
+        dists = torch.empty((nq, k), dtype=torch.float64, device=dev)
+        counts = torch.empty(nq, dtype=torch.int32, device=dev)
+    else:
+        ids, dists, counts = out
+    if chunk is None:
+        per_q = 4 * (D.T + cap)
+        chunk = max(1, min(nq, (1 << 30) // per_q))
+    leaves = torch.empty((min(chunk, nq), D.T), dtype=torch.int32, device=dev)
+    cand = torch.empty((min(chunk, nq), cap), dtype=torch.int32, device=dev)
+    stream = _native.stream_ptr()
+    for s in range(0, nq, chunk):
+        e = min(nq, s + chunk)
+        qb = Qd[s:e]
+        stage("route", _native.call, "mrpt_query_route", _native.ptr(qb), e - s, D.d,
+              int(Qd.stride(0)), _native.ptr(D.col_ptr), _native.ptr(D.rows),
+              _native.ptr(D.vals), _native.ptr(D.splits), D.T, D.depth, _native.ptr(leaves),
+              stream)
+        stage("vote", _native.call, "mrpt_vote", _native.ptr(D.indices), _native.ptr(D.offsets),
+              D.n, D.T, D.depth, _native.ptr(leaves), e - s, int(votes), int(D.leaves_sorted),
+              int(D.max_count), _native.ptr(cand), int(cap), _native.ptr(counts[s:e]), stream)
+        stage("scan_topk", _native.call, "mrpt_scan_topk", _native.ptr(D.X), D.n, D.d,
+              int(D.X.stride(0)), _native.ptr(qb), e - s, int(Qd.stride(0)), _native.ptr(cand),
+              int(cap), _native.ptr(counts[s:e]), int(k), _native.ptr(ids[s:e]),
+              _native.ptr(dists[s:e]), stream)
+    return ids, dists, counts
+
+
+def approximate_knn_batch(Q, k, index, votes, chunk=None):
+    """Approximate k-NN for every row of ``Q`` in one batched GPU pass.
+
+    Returns (ids int64 (nq, k) padded with -1, dists float64 (nq, k) padded
+    with +inf, candidate_count int32 (nq,)).  Host input gives host arrays;
+    a CUDA tensor gives CUDA tensors and nothing is synchronised.
+    Row i equals ``approximate_knn(Q[i], k, index, votes)`` exactly.
+    """
+    _check_batch_args(k, index, votes)
+    on_device = _device.is_tensor(Q) and Q.is_cuda
+    torch = _device.torch_mod()
+    if _device.is_tensor(Q):
+        if Q.dim() != 2 or Q.shape[1] != index.d:
+            raise ShapeError(f"queries must be (nq, {index.d}), got {tuple(Q.shape)}")
+        # a pinned host tensor is copied asynchronously on the current stream
+        Qd = Q.to(device=_device.device(), dtype=torch.float32,
+                  non_blocking=True).contiguous()
+    else:
+        Qh = np.asarray(Q)
+        if Qh.ndim != 2 or Qh.shape[1] != index.d:
+            raise ShapeError(f"queries must be (nq, {index.d}), got {Qh.shape}")
+        Qd = _device.h2d(np.ascontiguousarray(Qh, dtype=np.float32))
+    D = index.device_index()
+    nq = int(Qd.shape[0])
+    nnz = sum(R.nnz for R in index.matrices)
+    _record_macs(nq * nnz)
+    if nq == 0:
+        z = (np.empty((0, k), np.int64), np.empty((0, k), np.float64), np.empty(0, np.int32))
+        return z
+    ids, dists, counts = query_device(D, Qd, k, votes, chunk=chunk)
+    if on_device:
+        return ids, dists, counts
+    return _device.d2h(ids), _device.d2h(dists), _device.d2h(counts)
+
+
+def approximate_knn(q, k, index, votes):
+    """Approximate k-NN of one query (search.py:175-184): vote-filtered
+    candidates, then the exact scan; ``shortfall`` reports a deficit."""
+    if k < 1:
+        raise ParameterError(f"k must be >= 1, got {k}")
+    if not 1 <= votes <= index.n_trees:
+        raise ParameterError(f"vote threshold must lie in [1, {index.n_trees}], got {votes}")
+    q = _query_vector(q, index.d)
+    ids, dists, counts = approximate_knn_batch(q.reshape(1, -1), k, index, votes)
+    m = int(counts[0])
+    kept = min(k, m)
+    return NeighborList(indices=ids[0, :kept].copy(), distances=dists[0, :kept].copy(),
+                        requested_k=k, candidate_count=m)

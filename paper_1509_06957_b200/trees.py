@@ -1,0 +1,370 @@
+"""Random projection tree construction on the GPU (mirrors pkg/src/mrpt/trees.py).
+
+``grow_trees`` keeps the reference's signature, validation and results:
+tree t uses the matrix drawn from (seed, t) (host numpy, bit-exact), the
+projections are computed by K1 (``mrpt_project``) into a level-major
+(Tb, depth, n) buffer, and K5 (``mrpt_build_levels``) splits every node of
+every tree in the batch level by level at the exact lower median with a
+stable partition -- the same splits, leaf offsets and leaf id order the
+reference produces (trees.py:54-98, 187-245).  The index stays on the
+device; the host arrays the reference exposes are materialised on demand.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import threading
+
+import numpy as np
+
+from . import _device, _native
+from .core import (
+    Dataset,
+    SparseProjectionMatrix,
+    _record_macs,
+    as_dataset,
+    default_sparsity,
+    sample_sparse_matrix,
+)
+from .exceptions import DepthError, IntegrityError, ParameterError
+
+__all__ = ["MRPTIndex", "RPTree", "build_tree", "grow_trees", "median_split"]
+
+
+def _as_f32_values(values):
+    """float32 copy of ``values``; the GPU compares in float32, so inputs whose
+    values float32 cannot hold exactly are rejected rather than silently
+    re-rounded."""
+    v = np.asarray(values)
+    f = np.ascontiguousarray(v, dtype=np.float32)
+    if v.dtype != np.float32:
+        with np.errstate(invalid="ignore", over="ignore"):
+            if not np.array_equal(f.astype(v.dtype), v, equal_nan=True):
+                raise ParameterError("projection values must be exactly representable in float32 "
+                                     "(the device split kernels compare in float32)")
+    return f
+
+
+def _build_device(Pdev, n, Tb, depth, splits, offsets, indices):
+    """Run K5 on a (Tb, depth, n) projection buffer into the given outputs."""
+    torch = _device.torch_mod()
+    sz = ctypes.c_size_t(0)
+    _native.call("mrpt_build_workspace_size", n, Tb, depth, ctypes.byref(sz))
+    ws = torch.empty(max(1, sz.value), dtype=torch.uint8, device=Pdev.device)
+    _native.call("mrpt_build_levels", _native.ptr(Pdev), n, Tb, depth, _native.ptr(splits),
+                 _native.ptr(offsets), _native.ptr(indices), _native.ptr(ws), sz.value,
+                 _native.stream_ptr())
+
+
+def _single_tree(P_rows_f32, depth):
+    """Build one tree over an (n, depth) host float32 matrix on the GPU."""
+    torch = _device.torch_mod()
+    n = P_rows_f32.shape[0]
+    Pd = _device.h2d(np.ascontiguousarray(P_rows_f32[:, :depth].T))  # level-major
+    splits = torch.empty((1, (1 << depth) - 1), dtype=torch.float32, device=Pd.device)
+    offsets = torch.empty((1, (1 << depth) + 1), dtype=torch.int64, device=Pd.device)
+    order = torch.empty((1, n), dtype=torch.int32, device=Pd.device)
+    _build_device(Pd, n, 1, depth, splits, offsets, order)
+    return _device.d2h(splits)[0], _device.d2h(offsets)[0], _device.d2h(order)[0]
+
+
+def median_split(values, indices):
+    """Split ``indices`` at the lower median of ``values`` (trees.py:33-51).
+
+    split = the ceil(m/2)-th smallest value; entries with value <= split go
+    left in their original order, the rest right.  Runs as a one-level build
+    on the device.
+    """
+    v = np.asarray(values)
+    idx = np.asarray(indices)
+    m = v.shape[0]
+    if m < 2:
+        raise ParameterError(f"median_split needs at least 2 entries, got {m}")
+    f = _as_f32_values(v)
+    splits, offsets, order = _single_tree(f.reshape(m, 1), 1)
+    nle = int(offsets[1])
+    split = v.dtype.type(splits[0]) if np.issubdtype(v.dtype, np.floating) else splits[0]
+    return split, idx[order[:nle]], idx[order[nle:]]
+
+
+def build_tree(P, depth, indices=None):
+    """Grow one tree from precomputed projections ``P`` (n x depth), trees.py:54-98.
+
+    Returns (splits f32[2^depth-1], leaf_offsets i64[2^depth+1], order i32).
+    With ``indices`` the tree is built over those rows of P in that order.
+    """
+    P = np.asarray(P)
+    if depth < 0 or P.ndim != 2 or P.shape[1] < depth:
+        raise ParameterError(f"projection matrix has {P.shape[1] if P.ndim == 2 else 0} levels, "
+                             f"need {depth}")
+    order0 = (np.arange(P.shape[0], dtype=np.int32) if indices is None
+              else np.array(indices, dtype=np.int32))
+    nleaf = 1 << depth
+    if depth == 0 or order0.shape[0] == 0:
+        splits = np.zeros(nleaf - 1, dtype=np.float32)
+        bounds = np.zeros(nleaf + 1, dtype=np.int64)
+        bounds[1:] = order0.shape[0]
+        if depth > 0:
+            bounds[:] = 0
+        return splits, bounds, order0
+    rows = P if indices is None else P[order0]
+    splits, offsets, pos = _single_tree(_as_f32_values(rows), depth)
+    order = pos if indices is None else order0[pos]
+    return splits, offsets, np.ascontiguousarray(order, dtype=np.int32)
+
+
+from dataclasses import dataclass  # noqa: E402
+
+
+@dataclass(frozen=True)
+class RPTree:
+    """One tree of an index: its matrix plus the flat tree arrays (trees.py:101-121)."""
+
+    random_matrix: SparseProjectionMatrix
+    depth: int
+    splits: np.ndarray  # float32 (2^depth - 1,)
+    leaf_offsets: np.ndarray  # int64 (2^depth + 1,)
+    leaf_indices: np.ndarray  # int32 (n,)
+
+    @property
+    def n_leaves(self):
+        return 2 ** self.depth
+
+    def leaf(self, leaf_id):
+        s, e = self.leaf_offsets[leaf_id], self.leaf_offsets[leaf_id + 1]
+        return self.leaf_indices[s:e].copy()
+
+    def leaf_sizes(self):
+        return np.diff(self.leaf_offsets)
+
+
+class _DeviceIndex:
+    """Device-resident copy of an index, as the query kernels consume it."""
+
+    def __init__(self, X, T, depth, splits, offsets, indices, col_ptr, rows, vals, leaves_sorted,
+                 max_count, max_leaf):
+        self.X = X
+        self.n, self.d = int(X.shape[0]), int(X.shape[1])
+        self.T, self.depth = T, depth
+        self.splits, self.offsets, self.indices = splits, offsets, indices
+        self.col_ptr, self.rows, self.vals = col_ptr, rows, vals
+        self.leaves_sorted = leaves_sorted
+        self.max_count = max_count
+        self.max_leaf = max_leaf
+
+    def cap(self, votes):
+        """Upper bound on any candidate set at this vote threshold."""
+        return max(1, min(self.n, (self.T * self.max_leaf) // votes))
+
+
+class MRPTIndex:
+    """T random projection trees over one dataset (trees.py:124-175).
+
+    Same constructor fields as the reference dataclass, so hand-assembled or
+    loaded indexes work; ``splits`` / ``leaf_offsets`` / ``leaf_indices`` may be
+    host arrays or CUDA tensors.  Host views are materialised lazily for
+    device-built indexes; the device copy is uploaded (and audited) lazily
+    for host-built ones.
+    """
+
+    def __init__(self, dataset, n_trees, depth, sparsity, seed, fixed_count, matrices, splits,
+                 leaf_offsets, leaf_indices, dataset_checksum, _local=None, _device_index=None):
+        self.dataset = dataset
+        self.n_trees = n_trees
+        self.depth = depth
+        self.sparsity = sparsity
+        self.seed = seed
+        self.fixed_count = fixed_count
+        self.matrices = matrices
+        self._arrays = {"splits": splits, "leaf_offsets": leaf_offsets,
+                        "leaf_indices": leaf_indices}
+        self.dataset_checksum = dataset_checksum
+        self._local = _local if _local is not None else threading.local()
+        self._dev = _device_index
+        self._dev_lock = threading.Lock()
+
+    def _host(self, name):
+        a = self._arrays[name]
+        if _device.is_tensor(a):
+            a = _device.d2h(a)
+            self._arrays[name] = a
+        return a
+
+    splits = property(lambda self: self._host("splits"),
+                      lambda self, v: self._set("splits", v))
+    leaf_offsets = property(lambda self: self._host("leaf_offsets"),
+                            lambda self, v: self._set("leaf_offsets", v))
+    leaf_indices = property(lambda self: self._host("leaf_indices"),
+                            lambda self, v: self._set("leaf_indices", v))
+
+    def _set(self, name, value):
+        self._arrays[name] = value
+        self._dev = None  # re-upload on next query
+
+    def tree(self, t):
+        return RPTree(random_matrix=self.matrices[t], depth=self.depth, splits=self.splits[t],
+                      leaf_offsets=self.leaf_offsets[t], leaf_indices=self.leaf_indices[t])
+
+    def __iter__(self):
+        return (self.tree(t) for t in range(self.n_trees))
+
+    @property
+    def n(self):
+        return self.dataset.n
+
+    @property
+    def d(self):
+        return self.dataset.d
+
+    def max_candidates(self):
+        """T * ceil(n / 2^depth), the reference's bound (trees.py:161-163)."""
+        return self.n_trees * math.ceil(self.n / 2 ** self.depth)
+
+    def memory_bytes(self):
+        nleaf = 1 << self.depth
+        total = (self.n_trees * (nleaf - 1) * 4 + self.n_trees * (nleaf + 1) * 8
+                 + self.n_trees * self.n * 4)
+        for R in self.matrices:
+            total += R.col_ptr.nbytes + R.row_idx.nbytes + R.values.nbytes
+        return total
+
+    def query(self, q, k, votes):
+        from .search import approximate_knn
+
+        return approximate_knn(q, k, self, votes)
+
+    def __repr__(self):
+        return (f"MRPTIndex(n={self.n}, d={self.d}, n_trees={self.n_trees}, depth={self.depth}, "
+                f"sparsity={self.sparsity}, seed={self.seed})")
+
+    # -- device side ---------------------------------------------------------
+    def device_index(self):
+        """The cached device copy (uploading and auditing it on first use)."""
+        if self._dev is not None:
+            return self._dev
+        with self._dev_lock:
+            if self._dev is None:
+                self._dev = self._upload()
+        return self._dev
+
+    def _upload(self):
+        torch = _device.torch_mod()
+        T, depth, n = self.n_trees, self.depth, self.n
+        nleaf = 1 << depth
+
+        def dev(name, dtype, shape):
+            a = self._arrays[name]
+            if _device.is_tensor(a):
+                t = a.to(device=_device.device(), dtype=dtype).contiguous()
+            else:
+                t = _device.h2d(np.asarray(a, dtype=np.dtype(str(dtype).split(".")[-1])))
+            return t.reshape(shape)
+
+        splits = dev("splits", torch.float32, (T, nleaf - 1))
+        offsets = dev("leaf_offsets", torch.int64, (T, nleaf + 1))
+        indices = dev("leaf_indices", torch.int32, (T, n))
+        host_off = self._host("leaf_offsets").reshape(T, nleaf + 1)
+        if (host_off[:, 0] != 0).any() or (host_off[:, -1] != n).any() or \
+                (np.diff(host_off, axis=1) < 0).any():
+            raise IntegrityError("leaf offsets must run from 0 to n without decreasing")
+        flags = torch.zeros(2, dtype=torch.int32, device=indices.device)
+        _native.call("mrpt_audit_leaves", _native.ptr(indices), _native.ptr(offsets), n, T, depth,
+                     _native.ptr(flags), _native.stream_ptr())
+        unsorted, out_of_range = (int(x) for x in _device.d2h(flags))
+        if out_of_range:
+            raise IntegrityError(f"leaf point ids must lie in [0, {n})")
+        max_leaf = int(np.diff(host_off, axis=1).max())
+        cp, rows, vals = _device.csc_device(self.matrices)
+        return _DeviceIndex(self.dataset.device(), T, depth, splits, offsets, indices, cp, rows,
+                            vals, leaves_sorted=not unsorted,
+                            max_count=T if not unsorted else T * max(1, max_leaf),
+                            max_leaf=max_leaf)
+
+
+def _resolve_threads(threads):
+    if threads is None:
+        env = os.environ.get("MRPT_THREADS", "").strip()
+        threads = int(env) if env else 1
+    if threads < 1:
+        raise ParameterError(f"thread count must be >= 1, got {threads}")
+    return threads
+
+
+def _batch_trees(n, d, depth, T, free_bytes):
+    """Trees per K1+K5 batch: projections (depth*n*4) + keys + scratch order
+    (8n) per tree, within half of the free memory."""
+    per_tree = n * (4 * depth + 8) + 4096
+    tb = max(1, int(0.5 * free_bytes) // per_tree)
+    tb = min(tb, T, 128)
+    while tb > 1 and tb * (1 << depth) >= (1 << 31):
+        tb //= 2
+    return tb
+
+
+def grow_trees(X, n_trees, depth, sparsity=None, seed=0, fixed_count=False, threads=None,
+               batch_trees=None):
+    """Build ``n_trees`` trees of the given depth over ``X`` (trees.py:187-245).
+
+    Same validation and errors as the reference.  ``threads`` (or
+    MRPT_THREADS) is validated for compatibility; the work itself runs as
+    batched GPU kernels.  ``batch_trees`` overrides the trees per launch.
+    """
+    X = as_dataset(X)
+    if n_trees < 1:
+        raise ParameterError(f"tree count must be >= 1, got {n_trees}")
+    if depth < 1:
+        raise DepthError(f"depth must be >= 1, got {depth}")
+    if 2 ** depth > X.n:
+        raise DepthError(f"depth {depth} gives {2 ** depth} leaves but the dataset has only "
+                         f"{X.n} points")
+    if sparsity is None:
+        sparsity = default_sparsity(X.d)
+    seed = int(seed)
+    if not 0 <= seed < 2 ** 64:
+        raise ParameterError(f"seed must be an unsigned 64-bit integer, got {seed}")
+    _resolve_threads(threads)
+    if not 0.0 < sparsity <= 1.0:
+        raise ParameterError(f"sparsity must lie in (0, 1], got {sparsity}")
+    torch = _device.torch_mod()
+    Xd = X.device()
+    n, d = X.n, X.d
+    nleaf = 1 << depth
+    dev = Xd.device
+    splits = torch.empty((n_trees, nleaf - 1), dtype=torch.float32, device=dev)
+    offsets = torch.empty((n_trees, nleaf + 1), dtype=torch.int64, device=dev)
+    indices = torch.empty((n_trees, n), dtype=torch.int32, device=dev)
+    free = torch.cuda.mem_get_info(dev)[0]
+    tb = batch_trees or _batch_trees(n, d, depth, n_trees, free)
+    sz = ctypes.c_size_t(0)
+    _native.call("mrpt_build_workspace_size", n, tb, depth, ctypes.byref(sz))
+    ws = torch.empty(max(1, sz.value), dtype=torch.uint8, device=dev)
+    P = torch.empty((tb, depth, n), dtype=torch.float32, device=dev)
+    matrices = []
+    stream = _native.stream_ptr()
+    for b0 in range(0, n_trees, tb):
+        b1 = min(n_trees, b0 + tb)
+        mats = [sample_sparse_matrix(d, depth, sparsity, seed=(seed, t), fixed_count=fixed_count)
+                for t in range(b0, b1)]
+        matrices.extend(mats)
+        for R in mats:
+            _record_macs(n * R.nnz)
+        cp, rows, vals = _device.csc_device(mats)
+        # P[(t*depth + lev)*n + i]: row stride 1, column stride n
+        _native.call("mrpt_project", _native.ptr(Xd), n, d, d, _native.ptr(cp), _native.ptr(rows),
+                     _native.ptr(vals), (b1 - b0) * depth, _native.ptr(P), 1, n, stream)
+        _native.call("mrpt_build_levels", _native.ptr(P), n, b1 - b0, depth,
+                     _native.ptr(splits[b0:]), _native.ptr(offsets[b0:]),
+                     _native.ptr(indices[b0:]), _native.ptr(ws), sz.value, stream)
+        del cp, rows, vals
+    del P, ws
+    sizes = offsets[:, 1:] - offsets[:, :-1]
+    max_leaf = int(sizes.max().item())
+    cp, rows, vals = _device.csc_device(matrices)
+    dindex = _DeviceIndex(Xd, n_trees, depth, splits, offsets, indices, cp, rows, vals,
+                          leaves_sorted=True, max_count=n_trees, max_leaf=max_leaf)
+    return MRPTIndex(dataset=X, n_trees=n_trees, depth=depth, sparsity=float(sparsity), seed=seed,
+                     fixed_count=fixed_count, matrices=matrices, splits=splits,
+                     leaf_offsets=offsets, leaf_indices=indices,
+                     dataset_checksum=X.checksum, _device_index=dindex)

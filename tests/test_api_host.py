@@ -1,0 +1,112 @@
+"""Host-side API behaviour that needs no GPU: validation order and error
+types match the reference (pkg/src/mrpt/core.py, trees.py, search.py), and
+host-side sampling is bit-identical to the reference's."""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_1509_06957_b200 as mrpt
+from conftest import gaussian, golden, golden_small_names, unpack_matrices
+
+
+def test_sample_sparse_matrix_matches_reference_streams():
+    for name in golden_small_names():
+        g = golden(name)
+        d = g["X"].shape[1]
+        for t, (cp, r, v) in enumerate(unpack_matrices(g)):
+            R = mrpt.sample_sparse_matrix(d, int(g["depth"]), float(g["sparsity"]),
+                                          seed=(int(g["seed"]), t),
+                                          fixed_count=bool(g["fixed_count"]))
+            assert np.array_equal(R.col_ptr, cp) and np.array_equal(R.row_idx, r)
+            assert R.values.tobytes() == v.tobytes()
+
+
+@pytest.mark.parametrize("bad_a", [1.5, 0.0, -0.25])
+def test_sparsity_out_of_range_rejected(bad_a):
+    with pytest.raises(mrpt.ParameterError):
+        mrpt.sample_sparse_matrix(4, 2, a=bad_a, seed=5)
+
+
+@pytest.mark.parametrize("d,depth", [(0, 2), (4, 0)])
+def test_degenerate_shape_rejected(d, depth):
+    with pytest.raises(mrpt.ParameterError):
+        mrpt.sample_sparse_matrix(d, depth, a=0.5, seed=5)
+
+
+def test_bad_seed_rejected():
+    with pytest.raises(mrpt.ParameterError):
+        mrpt.sample_sparse_matrix(4, 2, a=0.5, seed=-1)
+    with pytest.raises(mrpt.ParameterError):
+        mrpt.sample_sparse_matrix(4, 2, a=0.5, seed=(1, "x"))
+
+
+def test_fixed_count_columns():
+    R = mrpt.sample_sparse_matrix(37, 5, 0.21, seed=3, fixed_count=True)
+    assert (R.nonzeros_per_column() == math.ceil(0.21 * 37)).all()
+    for j in range(5):
+        assert (np.diff(R.row_idx[R.col_ptr[j]:R.col_ptr[j + 1]]) > 0).all()
+
+
+def test_dataset_validation_on_host():
+    with pytest.raises(mrpt.ParameterError):
+        mrpt.Dataset(np.array([[1.0, np.nan]], dtype=np.float32))
+    with pytest.raises(mrpt.ParameterError):
+        mrpt.Dataset(np.array([[np.inf, 1.0]], dtype=np.float32))
+    with pytest.raises(mrpt.ParameterError):
+        mrpt.Dataset(np.empty((0, 3), dtype=np.float32))
+    with pytest.raises(mrpt.ShapeError):
+        mrpt.Dataset(np.zeros(4, dtype=np.float32))
+    X = mrpt.Dataset(np.ones((3, 3)))
+    assert X.values.dtype == np.float32 and not X.values.flags.writeable
+
+
+def test_grow_trees_validation_precedes_device_work(rng):
+    X = gaussian(rng, 8, 5)
+    with pytest.raises(mrpt.ParameterError):
+        mrpt.grow_trees(X, n_trees=0, depth=2, seed=0)
+    with pytest.raises(mrpt.DepthError):
+        mrpt.grow_trees(X, n_trees=1, depth=4, seed=0)
+    with pytest.raises(mrpt.DepthError):
+        mrpt.grow_trees(X, n_trees=1, depth=0, seed=0)
+    with pytest.raises(mrpt.ParameterError):
+        mrpt.grow_trees(X, n_trees=1, depth=2, seed=-1)
+    with pytest.raises(mrpt.ParameterError):
+        mrpt.grow_trees(X, n_trees=1, depth=2, threads=0)
+
+
+def test_median_split_and_exact_scan_argument_errors():
+    with pytest.raises(mrpt.ParameterError):
+        mrpt.median_split(np.array([1.0]), np.array([0]))
+    with pytest.raises(mrpt.ParameterError):
+        mrpt.exact_knn_in_set(np.zeros(3), 0, np.arange(2), np.zeros((4, 3)))
+    with pytest.raises(mrpt.ShapeError):
+        mrpt.exact_knn_in_set(np.zeros(2), 1, np.arange(2), np.zeros((4, 3)))
+
+
+def test_euclidean_distance_host_helper():
+    assert mrpt.euclidean_distance([0.0, 0.0], [3.0, 4.0]) == 5.0
+    with pytest.raises(mrpt.ShapeError):
+        mrpt.euclidean_distance([1.0, 2.0], [1.0, 2.0, 3.0])
+
+
+def test_mac_counter_nesting():
+    from paper_1509_06957_b200.core import _record_macs
+
+    with mrpt.count_macs() as outer:
+        _record_macs(5)
+        with mrpt.count_macs() as inner:
+            _record_macs(7)
+    assert outer.macs == 12 and inner.macs == 7
+
+
+def test_workload_generators_are_deterministic():
+    from paper_1509_06957_b200 import workloads
+
+    for c in (1, 2, 3, 4, 5):
+        X1, Q1, p = workloads.generate(c, scale=0.0002 if c > 1 else 0.05)
+        X2, Q2, _ = workloads.generate(c, scale=0.0002 if c > 1 else 0.05)
+        assert X1.dtype == np.float32 and X1.shape[1] == p["d"]
+        assert np.array_equal(X1, X2) and np.array_equal(Q1, Q2)
+        assert 2 ** p["depth"] <= X1.shape[0]

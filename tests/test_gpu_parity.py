@@ -1,0 +1,193 @@
+"""GPU parity: the CUDA path against the reference's golden outputs and the
+oracle.  Bit-exact for splits, leaf offsets/ids, leaves, candidate sets,
+neighbour ids and distances (the kernels reproduce the reference's float64
+summation order exactly)."""
+
+import numpy as np
+import pytest
+
+import paper_1509_06957_b200 as mrpt
+from conftest import gaussian, golden, golden_small_names, unpack_matrices
+from oracle import oracle as O
+from paper_1509_06957_b200 import workloads
+from paper_1509_06957_b200.search import _route_device
+from paper_1509_06957_b200 import _device
+
+pytestmark = pytest.mark.gpu
+
+
+def _check_index(index, g):
+    for R, (cp, r, v) in zip(index.matrices, unpack_matrices(g)):
+        assert np.array_equal(R.col_ptr, cp) and np.array_equal(R.row_idx, r)
+        assert R.values.tobytes() == v.tobytes()
+    assert index.splits.tobytes() == g["splits"].tobytes()
+    assert np.array_equal(index.leaf_offsets, g["leaf_offsets"])
+    assert np.array_equal(index.leaf_indices, g["leaf_indices"])
+    assert index.dataset_checksum == int(g["checksum" if "checksum" in g else "x_checksum"])
+
+
+@pytest.mark.parametrize("name", golden_small_names())
+def test_build_and_query_match_reference(name):
+    g = golden(name)
+    index = mrpt.grow_trees(g["X"], int(g["n_trees"]), int(g["depth"]), float(g["sparsity"]),
+                            seed=int(g["seed"]), fixed_count=bool(g["fixed_count"]))
+    _check_index(index, g)
+    D = index.device_index()
+    leaves = _device.d2h(_route_device(_device.h2d(g["Q"]), D))
+    assert np.array_equal(leaves, g["leaves"])
+    k = int(g["k"])
+    for v in g["votes"]:
+        v = int(v)
+        ids, dists, counts = mrpt.approximate_knn_batch(g["Q"], k, index, v)
+        assert np.array_equal(counts.astype(np.int64), g[f"counts_v{v}"])
+        assert np.array_equal(ids, g[f"ids_v{v}"])
+        assert dists.tobytes() == g[f"dists_v{v}"].tobytes()
+        b = g[f"cand_bounds_v{v}"]
+        for i in range(min(len(b) - 1, 8)):
+            cands, acc = mrpt.candidate_set(g["Q"][i], index, v)
+            assert np.array_equal(cands, g[f"cand_v{v}"][b[i]:b[i + 1]])
+        r = mrpt.approximate_knn(g["Q"][0], k, index, v)
+        assert r.indices.tolist() == g[f"ids_v{v}"][0][:len(r)].tolist()
+        assert r.candidate_count == int(g[f"counts_v{v}"][0])
+
+
+def test_hand_assembled_index_from_golden_arrays():
+    """An index assembled from host arrays (as a loaded file would be) queries
+    exactly like the reference."""
+    g = golden("small_clustered_3000x96.npz")
+    mats = [mrpt.SparseProjectionMatrix(d=g["X"].shape[1], depth=int(g["depth"]),
+                                        a=float(g["sparsity"]), seed=(int(g["seed"]), t),
+                                        col_ptr=cp, row_idx=r, values=v)
+            for t, (cp, r, v) in enumerate(unpack_matrices(g))]
+    X = mrpt.Dataset(g["X"])
+    index = mrpt.MRPTIndex(dataset=X, n_trees=int(g["n_trees"]), depth=int(g["depth"]),
+                           sparsity=float(g["sparsity"]), seed=int(g["seed"]), fixed_count=False,
+                           matrices=mats, splits=g["splits"], leaf_offsets=g["leaf_offsets"],
+                           leaf_indices=g["leaf_indices"], dataset_checksum=int(g["checksum"]))
+    for v in g["votes"]:
+        ids, dists, counts = mrpt.approximate_knn_batch(g["Q"], int(g["k"]), index, int(v))
+        assert np.array_equal(ids, g[f"ids_v{int(v)}"])
+        assert np.array_equal(counts.astype(np.int64), g[f"counts_v{int(v)}"])
+
+
+def test_config1_full_matches_reference():
+    g = golden("config1.npz")
+    X, Q, p = workloads.generate(1)
+    index = mrpt.grow_trees(X, int(g["n_trees"]), int(g["depth"]), float(g["sparsity"]),
+                            seed=int(g["seed"]))
+    _check_index(index, g)
+    for v in (1, 2):
+        ids, dists, counts = mrpt.approximate_knn_batch(Q, int(g["k"]), index, v)
+        assert np.array_equal(counts.astype(np.int64), g[f"counts_v{v}"])
+        assert np.array_equal(ids, g[f"ids_v{v}"])
+        assert dists.tobytes() == g[f"dists_v{v}"].tobytes()
+
+
+# --- kernel-level differential tests against the oracle -----------------------
+@pytest.mark.parametrize("n,d,depth,a", [(777, 48, 6, 0.25), (3000, 784, 8, 1 / 28),
+                                         (200, 1100, 5, 0.05), (5, 3000, 4, 0.01)])
+def test_projection_bit_identical(rng, n, d, depth, a):
+    X = gaussian(rng, n, d)
+    R = mrpt.sample_sparse_matrix(d, depth, a, seed=(3, 1))
+    P = mrpt.project_dataset(X, R)
+    ref = O.project(X, R.col_ptr, R.row_idx, R.values)
+    assert P.tobytes() == ref.tobytes()
+    for i in (0, n // 2, n - 1):
+        assert mrpt.project_query(X[i], R).tobytes() == ref[i].tobytes()
+
+
+@pytest.mark.parametrize("n,d,T,depth,gen", [
+    (100_000, 64, 3, 10, "gauss"),       # big-path segments (> 8192) at the top levels
+    (60_000, 16, 2, 9, "ints"),          # heavy ties through the big path
+    (40_000, 8, 2, 6, "ones"),           # all keys equal in a big segment
+    (20_000, 32, 4, 12, "gauss"),        # tiny leaves (~5 points)
+])
+def test_build_matches_oracle_large(rng, n, d, T, depth, gen):
+    if gen == "gauss":
+        X = gaussian(rng, n, d)
+    elif gen == "ints":
+        X = rng.integers(0, 3, size=(n, d)).astype(np.float32)
+    else:
+        X = np.ones((n, d), dtype=np.float32)
+    index = mrpt.grow_trees(X, T, depth, seed=17)
+    for t in range(T):
+        R, (s, o, i) = O.build_one_tree(X, depth, 1 / np.sqrt(d), 17, t)
+        assert index.splits[t].tobytes() == s.tobytes(), t
+        assert np.array_equal(index.leaf_offsets[t], o), t
+        assert np.array_equal(index.leaf_indices[t], i), t
+
+
+def test_batched_build_equals_single_tree_batches(rng):
+    X = gaussian(rng, 5000, 20)
+    a = mrpt.grow_trees(X, 7, 6, seed=4, batch_trees=7)
+    b = mrpt.grow_trees(X, 7, 6, seed=4, batch_trees=2)
+    assert a.splits.tobytes() == b.splits.tobytes()
+    assert np.array_equal(a.leaf_indices, b.leaf_indices)
+
+
+@pytest.mark.parametrize("size", [1, 3, 4096, 4097, 1 << 20, 5_000_011])
+def test_fnv_matches_oracle(rng, size):
+    buf = rng.integers(0, 256, size=size).astype(np.uint8)
+    assert mrpt.fnv1a64(buf) == O.fnv1a64(buf.tobytes())
+
+
+def test_fnv_golden_vectors():
+    g = golden("fnv.npz")
+    blob = g["blob"].tobytes()
+    off = 0
+    for ln, h in zip(g["lens"], g["hashes"]):
+        assert mrpt.fnv1a64(blob[off:off + int(ln)]) == int(h)
+        off += int(ln)
+
+
+def test_scan_bit_identical(rng):
+    from paper_1509_06957_b200 import _native
+
+    X = gaussian(rng, 2000, 96)
+    q = gaussian(rng, 1, 96)[0]
+    cand = rng.choice(2000, size=700, replace=False).astype(np.int64)
+    torch = _device.torch_mod()
+    out = torch.empty(700, dtype=torch.float64, device="cuda")
+    Xd, cd, qd = _device.h2d(X), _device.h2d(cand), _device.h2d(q)
+    _native.call("mrpt_scan", _native.ptr(Xd), 2000, 96, 96, _native.ptr(cd), 700,
+                 _native.ptr(qd), _native.ptr(out), _native.stream_ptr())
+    assert _device.d2h(out).tobytes() == O.scan(X, cand, q).tobytes()
+
+
+def test_exact_knn_in_set_matches_oracle(rng):
+    X = gaussian(rng, 500, 13)
+    q = gaussian(rng, 1, 13)[0]
+    cand = rng.integers(0, 500, size=300)  # with duplicates
+    for k in (1, 7, 100, 400):
+        r = mrpt.exact_knn_in_set(q, k, cand, X)
+        ids, dists, cnt = O.exact_knn(X, q, k, cand)
+        assert r.indices.tolist() == ids.tolist()
+        assert r.distances.tobytes() == dists.tobytes()
+        assert r.candidate_count == cnt
+
+
+def test_large_k_multipass(rng):
+    X = gaussian(rng, 9000, 8)
+    q = gaussian(rng, 1, 8)[0]
+    r = mrpt.exact_knn_in_set(q, 7000, np.arange(9000), X)
+    ids, dists, cnt = O.exact_knn(X, q, 7000, np.arange(9000))
+    assert r.indices.tolist() == ids.tolist()
+    assert r.distances.tobytes() == dists.tobytes()
+
+
+@pytest.mark.parametrize("T,depth,n", [(300, 8, 50_000), (40, 12, 400_000)])
+def test_vote_tiled_and_wide_counters(rng, T, depth, n):
+    """u16 counters (T > 255) and the multi-tile id sweep (n > one tile)."""
+    c = 3.0 * rng.standard_normal((50, 16))
+    X = (c[rng.integers(0, 50, size=n + 64)] + rng.standard_normal((n + 64, 16))).astype(np.float32)
+    Xd, Q = X[:n], X[n:]
+    index = mrpt.grow_trees(Xd, T, depth, seed=2)
+    ref = dict(matrices=[(R.col_ptr, R.row_idx, R.values) for R in index.matrices],
+               splits=index.splits, leaf_offsets=index.leaf_offsets,
+               leaf_indices=index.leaf_indices, depth=depth)
+    for v in (1, 3, T // 2):
+        ids, dists, counts = mrpt.approximate_knn_batch(Q, 10, index, v)
+        rids, rd, rc = O.approximate_knn_batch(Xd, Q, 10, ref, v)
+        assert np.array_equal(counts.astype(np.int64), rc)
+        assert np.array_equal(ids, rids)
+        assert dists.tobytes() == rd.tobytes()
