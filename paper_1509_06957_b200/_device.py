@@ -28,6 +28,8 @@ def h2d(arr, dtype=None):
     """Copy a host array to the current device (pinned staging for big arrays)."""
     torch = torch_mod()
     a = np.ascontiguousarray(arr if dtype is None else np.asarray(arr, dtype=dtype))
+    if not a.flags.writeable:  # torch wants writable storage; the copy is read-only to us
+        a = a.copy()
     t = torch.from_numpy(a)
     if a.nbytes >= (1 << 20):
         t = t.pin_memory()

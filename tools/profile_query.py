@@ -1,0 +1,38 @@
+"""Run the query hot path on one configuration (no bench bookkeeping) so ncu
+can capture its kernels:  python tools/profile_query.py --config 2 --votes 1"""
+
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_1509_06957_b200 as mrpt  # noqa: E402
+from paper_1509_06957_b200 import workloads  # noqa: E402
+from paper_1509_06957_b200.search import query_device  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=2)
+ap.add_argument("--votes", type=int, default=None)
+ap.add_argument("--scale", type=float, default=1.0)
+ap.add_argument("--nq", type=int, default=None)
+ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--build-only", action="store_true")
+a = ap.parse_args()
+X, Q, p = workloads.generate(a.config, a.scale)
+if a.nq:
+    Q = Q[:a.nq]
+v = a.votes or p["headline_votes"]
+Xd = torch.from_numpy(X).cuda()
+index = mrpt.grow_trees(Xd, p["n_trees"], p["depth"], p["sparsity"], seed=p["seed"])
+torch.cuda.synchronize()
+if not a.build_only:
+    D = index.device_index()
+    Qd = torch.from_numpy(Q).cuda()
+    for _ in range(a.reps):
+        ids, dists, counts = query_device(D, Qd, p["k"], v)
+    torch.cuda.synchronize()
+    print("mean candidates", counts.double().mean().item())
