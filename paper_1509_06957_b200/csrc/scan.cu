@@ -38,6 +38,8 @@ struct TopkArgs {
   unsigned long long *lb_key;  // optional lower bound per query (multi-pass)
   int32_t *lb_id;
   bool vec4;
+  const int32_t *qlist;  // optional: process only these queries (count *qcount)
+  const int32_t *qcount;
 };
 
 __device__ __forceinline__ bool pair_less(unsigned long long ak, int ai, unsigned long long bk,
@@ -203,6 +205,445 @@ __global__ void __launch_bounds__(kScanNT) k_scan_topk(TopkArgs a) {
   }
 }
 
+// Coalesced variant (d % 4 == 0, 16-byte aligned rows).  Each warp scores 32
+// candidates at a time: rows are read in 128-byte chunks by 8 lanes each
+// (one LDG.128 instruction covers 4 rows), staged through a per-warp shared
+// tile with a 36-word row stride (conflict-free STS.128 / LDS.128), and each
+// lane then runs the reference's sequential float64 sum over its own row.
+// The next chunk's loads are in flight while the current one is summed.
+constexpr int kTileStride = 36;  // words per staged row (32 + 4 pad)
+
+template <int BUF>
+__global__ void __launch_bounds__(kScanNT, 3) k_scan_topk_tiled(TopkArgs a) {
+  extern __shared__ unsigned long long topk_smem[];
+  unsigned long long *bkey = topk_smem;                                   // BUF
+  int32_t *bid = reinterpret_cast<int32_t *>(bkey + BUF);                 // BUF
+  float *tiles = reinterpret_cast<float *>(bid + BUF);                    // 8 warps x 32 x 36
+  double *qd = reinterpret_cast<double *>(tiles + (kScanNT / 32) * 32 * kTileStride);  // d
+  __shared__ int s_cnt;
+  __shared__ unsigned long long s_tk;
+  __shared__ int s_ti;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float *tile = tiles + warp * 32 * kTileStride;
+  const int d = a.d;
+  const int nchunk = (d + 31) >> 5;
+  const int sub = lane & 7;   // float4 slot within a 128-byte chunk
+  const int rsub = lane >> 3; // row offset 0..3 within a load instruction
+  const int64_t nwork = a.qlist ? (int64_t)*a.qcount : a.nq;
+  for (int64_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const int64_t q = a.qlist ? (int64_t)a.qlist[w] : w;
+    for (int c = tid; c < d; c += kScanNT) qd[c] = (double)a.Q[q * a.ldq + c];
+    if (tid == 0) {
+      s_cnt = 0;
+      s_tk = ~0ull;
+      s_ti = 0x7fffffff;
+    }
+    const unsigned long long lbk = a.lb_key ? a.lb_key[q] : 0ull;
+    const int lbi = a.lb_key ? a.lb_id[q] : -1;
+    const bool use_lb = a.lb_key != nullptr;
+    __syncthreads();
+    int64_t m;
+    if (a.cand) {
+      const int64_t nc = a.ncand[q];
+      m = nc < a.cap ? nc : a.cap;
+    } else {
+      m = a.n;
+    }
+    const int32_t *qc = a.cand ? a.cand + q * a.cap : nullptr;
+    for (int64_t base = 0; base < m; base += kScanNT) {
+      const int64_t j = base + warp * 32 + lane;
+      const bool valid = j < m;
+      const int32_t myid = valid ? (qc ? qc[j] : (int32_t)j) : 0;
+      // row ids of the 8 rows this lane loads (rows rsub + 4i of the group)
+      int32_t rid[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rid[i] = __shfl_sync(0xffffffffu, myid, rsub + 4 * i);
+      const float *xb = a.X + 4 * sub;
+      const int64_t ldx = a.ldx;
+      float4 buf[8];
+      const bool full0 = 4 * sub < d;  // chunk 0 slot in range
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        buf[i] = full0 ? __ldg(reinterpret_cast<const float4 *>(xb + (int64_t)rid[i] * ldx))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      double acc = 0.0;
+      for (int ch = 0; ch < nchunk; ++ch) {
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          *reinterpret_cast<float4 *>(tile + (rsub + 4 * i) * kTileStride + 4 * sub) = buf[i];
+        __syncwarp();
+        if (ch + 1 < nchunk) {
+          const int off = (ch + 1) * 32;
+          const bool in = off + 4 * sub < d;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            buf[i] = in ? __ldg(reinterpret_cast<const float4 *>(xb + (int64_t)rid[i] * ldx + off))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        const int c0 = ch * 32;
+        const int cn = (d - c0) < 32 ? (d - c0) : 32;
+        const float *myrow = tile + lane * kTileStride;
+        if (cn == 32) {
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            const float4 x = *reinterpret_cast<const float4 *>(myrow + 4 * g);
+            const double2 q01 = *reinterpret_cast<const double2 *>(qd + c0 + 4 * g);
+            const double2 q23 = *reinterpret_cast<const double2 *>(qd + c0 + 4 * g + 2);
+            double t;
+            t = (double)x.x - q01.x;
+            acc = __dadd_rn(acc, __dmul_rn(t, t));
+            t = (double)x.y - q01.y;
+            acc = __dadd_rn(acc, __dmul_rn(t, t));
+            t = (double)x.z - q23.x;
+            acc = __dadd_rn(acc, __dmul_rn(t, t));
+            t = (double)x.w - q23.y;
+            acc = __dadd_rn(acc, __dmul_rn(t, t));
+          }
+        } else {
+          for (int c = 0; c < cn; ++c) {
+            const double t = (double)myrow[c] - qd[c0 + c];
+            acc = __dadd_rn(acc, __dmul_rn(t, t));
+          }
+        }
+      }
+      const unsigned long long tk = s_tk;
+      const int ti = s_ti;
+      const unsigned long long key = (unsigned long long)__double_as_longlong(acc);
+      if (valid && pair_less(key, myid, tk, ti) && (!use_lb || pair_less(lbk, lbi, key, myid))) {
+        const int slot = atomicAdd(&s_cnt, 1);
+        bkey[slot] = key;
+        bid[slot] = myid;
+      }
+      __syncthreads();
+      if (s_cnt > BUF - kScanNT) {
+        const int cnt = s_cnt;
+        for (int i = cnt + tid; i < BUF; i += kScanNT) {
+          bkey[i] = ~0ull;
+          bid[i] = 0x7fffffff;
+        }
+        __syncthreads();
+        bitonic_sort<BUF>(bkey, bid);
+        if (tid == 0) {
+          s_cnt = a.k;
+          s_tk = bkey[a.k - 1];
+          s_ti = bid[a.k - 1];
+        }
+        __syncthreads();
+      }
+    }
+    const int cnt = s_cnt;
+    for (int i = cnt + tid; i < BUF; i += kScanNT) {
+      bkey[i] = ~0ull;
+      bid[i] = 0x7fffffff;
+    }
+    __syncthreads();
+    bitonic_sort<BUF>(bkey, bid);
+    const int kept = cnt < a.k ? cnt : a.k;
+    for (int i = tid; i < a.k; i += kScanNT) {
+      if (i < kept) {
+        a.ids[q * a.kstride + i] = bid[i];
+        a.dists[q * a.kstride + i] = sqrt(__longlong_as_double((long long)bkey[i]));
+      } else {
+        a.ids[q * a.kstride + i] = -1;
+        a.dists[q * a.kstride + i] = __longlong_as_double(0x7ff0000000000000LL);
+      }
+    }
+    if (use_lb && tid == 0 && kept > 0) {
+      a.lb_key[q] = bkey[kept - 1];
+      a.lb_id[q] = bid[kept - 1];
+    }
+    __syncthreads();
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Filter-and-rerank top-k (d % 4 == 0, d <= 1024, k <= 120): bit-identical
+// results at streaming cost.
+//
+// Pass 1 scores every candidate in float32: one warp per group of kFU
+// candidates, lanes striding the coordinates with coalesced 16-byte loads,
+// FFMA partial sums and a butterfly reduction.  Its value A obeys
+// |A - E| <= eps*E + eta against the reference's float64 sum E (eps, eta
+// from the float32 error analysis of a sum of non-negative terms, with a
+// 2x safety factor).  Each warp keeps the candidates with
+//     A <= ((T_a + eta) * (1 + eps) / (1 - eps)) + eta,
+// T_a its k-th smallest A so far: if the k-th smallest E is E_k, the k
+// smallest-A candidates all have E <= (T_a + eta)/(1 - eps), so every member
+// of the exact top-k (ties included) satisfies the rule and survives.
+// Pass 2 recomputes E for the few survivors with the reference's sequential
+// float64 sum and orders them by (E, id).  A warp whose buffer cannot shrink
+// (masses of exact ties) sends its query to the exact tiled kernel.
+constexpr int kFU = 4;       // candidates per warp iteration
+constexpr int kFMaxJ = 8;    // d <= 128 * kFMaxJ
+
+__device__ __forceinline__ bool fpair_less(float ak, int ai, float bk, int bi) {
+  return ak < bk || (ak == bk && ai < bi);
+}
+
+// warp-level bitonic sort of n (pow2) (float, id) pairs in shared memory
+__device__ void warp_sort(float *k, int32_t *id, int n) {
+  const int lane = threadIdx.x & 31;
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = lane; i < n / 2; i += 32) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool asc = (lo & size) == 0;
+        const float ka = k[lo], kb = k[hi];
+        const int ia = id[lo], ib = id[hi];
+        if (fpair_less(kb, ib, ka, ia) == asc) {
+          k[lo] = kb;
+          k[hi] = ka;
+          id[lo] = ib;
+          id[hi] = ia;
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__device__ __forceinline__ double keep_bound(float ta, double eps, double eta) {
+  return ((double)ta + eta) * (1.0 + eps) / (1.0 - eps) + eta;
+}
+
+// sort the first cnt entries (padding to n), return how many satisfy the
+// keep rule for the current k-th value; *thr receives the bound.
+__device__ int warp_shrink(float *k, int32_t *id, int cnt, int n, int kk, double eps, double eta,
+                           double *thr) {
+  const int lane = threadIdx.x & 31;
+  for (int i = cnt + lane; i < n; i += 32) {
+    k[i] = __int_as_float(0x7f800000);
+    id[i] = 0x7fffffff;
+  }
+  __syncwarp();
+  warp_sort(k, id, n);
+  if (cnt < kk) {
+    *thr = __longlong_as_double(0x7ff0000000000000LL);
+    return cnt;
+  }
+  const double b = keep_bound(k[kk - 1], eps, eta);
+  int keep = 0;
+  for (int i0 = 0; i0 < cnt; i0 += 32) {
+    const int i = i0 + lane;
+    const bool in = i < cnt && (double)k[i] <= b;
+    keep += __popc(__ballot_sync(0xffffffffu, in));
+  }
+  *thr = b;
+  return keep;
+}
+
+template <int BUFW>
+__global__ void __launch_bounds__(kScanNT) k_scan_topk_filter(TopkArgs a, double eps, double eta,
+                                                              int32_t *fb_list, int32_t *fb_count) {
+  extern __shared__ unsigned long long topk_smem[];
+  constexpr int NWARP = kScanNT / 32;
+  float *wkey = reinterpret_cast<float *>(topk_smem);                 // NWARP * BUFW
+  int32_t *wid = reinterpret_cast<int32_t *>(wkey + NWARP * BUFW);    // NWARP * BUFW
+  unsigned long long *ckey = reinterpret_cast<unsigned long long *>(wid + NWARP * BUFW);  // NWARP*BUFW
+  int32_t *cid = reinterpret_cast<int32_t *>(ckey + NWARP * BUFW);    // NWARP * BUFW
+  float *ck = reinterpret_cast<float *>(cid + NWARP * BUFW);          // NWARP * BUFW (merge keys)
+  __shared__ int s_wcnt[NWARP];
+  __shared__ int s_bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float *mk = wkey + warp * BUFW;
+  int32_t *mi = wid + warp * BUFW;
+  const int d = a.d;
+  const int nj = (d + 127) >> 7;
+  const int kk = a.k;
+  for (int64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
+    const float *qrow = a.Q + q * a.ldq;
+    float4 qv[kFMaxJ];
+#pragma unroll
+    for (int j = 0; j < kFMaxJ; ++j) {
+      const int c = j * 128 + 4 * lane;
+      qv[j] = (j < nj && c < d) ? *reinterpret_cast<const float4 *>(qrow + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (tid == 0) s_bad = 0;
+    int64_t m;
+    if (a.cand) {
+      const int64_t nc = a.ncand[q];
+      m = nc < a.cap ? nc : a.cap;
+    } else {
+      m = a.n;
+    }
+    const int32_t *qc = a.cand ? a.cand + q * a.cap : nullptr;
+    int cnt = 0;
+    double thr = __longlong_as_double(0x7ff0000000000000LL);
+    bool bad = false;
+    for (int64_t g = (int64_t)warp * kFU; g < m; g += (int64_t)NWARP * kFU) {
+      int32_t cidv[kFU];
+      const float *row[kFU];
+#pragma unroll
+      for (int u = 0; u < kFU; ++u) {
+        const int64_t j = g + u;
+        cidv[u] = j < m ? (qc ? __ldg(qc + j) : (int32_t)j) : -1;
+        row[u] = a.X + (int64_t)(cidv[u] < 0 ? 0 : cidv[u]) * a.ldx;
+      }
+      float acc[kFU];
+#pragma unroll
+      for (int u = 0; u < kFU; ++u) acc[u] = 0.f;
+#pragma unroll
+      for (int j = 0; j < kFMaxJ; ++j) {
+        const int c = j * 128 + 4 * lane;
+        if (j < nj && c < d) {
+          float4 x[kFU];
+#pragma unroll
+          for (int u = 0; u < kFU; ++u) x[u] = __ldg(reinterpret_cast<const float4 *>(row[u] + c));
+#pragma unroll
+          for (int u = 0; u < kFU; ++u) {
+            float t;
+            t = x[u].x - qv[j].x;
+            acc[u] = __fmaf_rn(t, t, acc[u]);
+            t = x[u].y - qv[j].y;
+            acc[u] = __fmaf_rn(t, t, acc[u]);
+            t = x[u].z - qv[j].z;
+            acc[u] = __fmaf_rn(t, t, acc[u]);
+            t = x[u].w - qv[j].w;
+            acc[u] = __fmaf_rn(t, t, acc[u]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kFU; ++u) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+      }
+      // lane u decides for candidate u
+      float mine = acc[0];
+      int32_t myid = cidv[0];
+#pragma unroll
+      for (int u = 1; u < kFU; ++u)
+        if (lane == u) {
+          mine = acc[u];
+          myid = cidv[u];
+        }
+      const bool take = lane < kFU && myid >= 0 && (double)mine <= thr;
+      const unsigned tm = __ballot_sync(0xffffffffu, take);
+      if (take) {
+        const int slot = cnt + __popc(tm & lanemask_lt());
+        mk[slot] = mine;
+        mi[slot] = myid;
+      }
+      cnt += __popc(tm);
+      if (cnt > BUFW - kFU) {
+        __syncwarp();
+        cnt = warp_shrink(mk, mi, cnt, BUFW, kk, eps, eta, &thr);
+        if (cnt > BUFW - kFU) {  // cannot shrink: exact ties galore
+          bad = true;
+          cnt = 0;
+          break;
+        }
+      }
+    }
+    __syncwarp();
+    if (!bad) cnt = warp_shrink(mk, mi, cnt, BUFW, kk, eps, eta, &thr);
+    if (lane == 0) {
+      s_wcnt[warp] = cnt;
+      if (bad) s_bad = 1;
+    }
+    __syncthreads();
+    if (s_bad) {
+      if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = (int32_t)q;
+      __syncthreads();
+      continue;
+    }
+    // merge the warp survivors (each a sorted prefix) into ck/cid
+    int off = 0, total = 0;
+    for (int w = 0; w < NWARP; ++w) {
+      off += w < warp ? s_wcnt[w] : 0;
+      total += s_wcnt[w];
+    }
+    for (int i = lane; i < cnt; i += 32) {
+      ck[off + i] = mk[i];
+      cid[off + i] = mi[i];
+    }
+    int np2 = 32;
+    while (np2 < total) np2 <<= 1;
+    for (int i = total + tid; i < np2; i += kScanNT) {
+      ck[i] = __int_as_float(0x7f800000);
+      cid[i] = 0x7fffffff;
+    }
+    __syncthreads();
+    // CTA bitonic sort of np2 (approx, id)
+    for (int size = 2; size <= np2; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = tid; i < np2 / 2; i += kScanNT) {
+          const int lo = 2 * i - (i & (stride - 1));
+          const int hi = lo + stride;
+          const bool asc = (lo & size) == 0;
+          const float ka = ck[lo], kb = ck[hi];
+          const int ia = cid[lo], ib = cid[hi];
+          if (fpair_less(kb, ib, ka, ia) == asc) {
+            ck[lo] = kb;
+            ck[hi] = ka;
+            cid[lo] = ib;
+            cid[hi] = ia;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    const double b = total >= kk ? keep_bound(ck[kk - 1], eps, eta)
+                                 : __longlong_as_double(0x7ff0000000000000LL);
+    // survivors: sorted prefix with approx <= b; exact float64 rerank
+    int ns = 0;
+    for (int i = 0; i < total; ++i) {
+      if ((double)ck[i] <= b) ns = i + 1; else break;
+    }
+    int np3 = 1;
+    while (np3 < ns) np3 <<= 1;
+    for (int i = tid; i < np3; i += kScanNT) {
+      if (i < ns) {
+        const int32_t id = cid[i];
+        const float *xr = a.X + (int64_t)id * a.ldx;
+        double e = 0.0;
+        for (int c = 0; c < d; ++c) {
+          const double t = (double)__ldg(xr + c) - (double)__ldg(qrow + c);
+          e = __dadd_rn(e, __dmul_rn(t, t));
+        }
+        ckey[i] = (unsigned long long)__double_as_longlong(e);
+        wid[i] = id;
+      } else {
+        ckey[i] = ~0ull;
+        wid[i] = 0x7fffffff;
+      }
+    }
+    __syncthreads();
+    for (int size = 2; size <= np3; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = tid; i < np3 / 2; i += kScanNT) {
+          const int lo = 2 * i - (i & (stride - 1));
+          const int hi = lo + stride;
+          const bool asc = (lo & size) == 0;
+          const unsigned long long ka = ckey[lo], kb = ckey[hi];
+          const int ia = wid[lo], ib = wid[hi];
+          if (pair_less(kb, ib, ka, ia) == asc) {
+            ckey[lo] = kb;
+            ckey[hi] = ka;
+            wid[lo] = ib;
+            wid[hi] = ia;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    const int kept = ns < kk ? ns : kk;
+    for (int i = tid; i < kk; i += kScanNT) {
+      if (i < kept) {
+        a.ids[q * a.kstride + i] = wid[i];
+        a.dists[q * a.kstride + i] = sqrt(__longlong_as_double((long long)ckey[i]));
+      } else {
+        a.ids[q * a.kstride + i] = -1;
+        a.dists[q * a.kstride + i] = __longlong_as_double(0x7ff0000000000000LL);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(kScanNT)
 k_scan(const float *__restrict__ X, int64_t ldx, int d, const int64_t *__restrict__ cand, int64_t m,
        const float *__restrict__ q, double *out, bool vec4) {
@@ -251,6 +692,7 @@ extern "C" int32_t mrpt_scan(const float *X, int64_t n, int32_t d, int64_t ldx, 
 }
 
 typedef void (*topk_fn)(TopkArgs);
+typedef void (*topk_fn_f)(TopkArgs, double, double, int32_t *, int32_t *);
 
 extern "C" int32_t mrpt_scan_topk(const float *X, int64_t n, int32_t d, int64_t ldx, const float *Q,
                                   int64_t nq, int64_t ldq, const int32_t *cand, int64_t cap,
@@ -289,6 +731,40 @@ extern "C" int32_t mrpt_scan_topk(const float *X, int64_t n, int32_t d, int64_t 
     cudaMemsetAsync(a.lb_id, 0xff, sizeof(int32_t) * nq, s);
   }
   const int64_t grid = nq < (int64_t)num_sms() * 8 ? nq : (int64_t)num_sms() * 8;
+  a.qlist = nullptr;
+  a.qcount = nullptr;
+  const bool qvec4 = (ldq % 4 == 0) && aligned16(Q);
+  if (a.vec4 && qvec4 && d <= 128 * kFMaxJ && k <= 120) {
+    // filter (float32) + exact float64 rerank; exact-tie overflows go to the
+    // tiled exact kernel through a device-side query list.
+    const int bufw = (2 * k + 2 * kFU <= 64) ? 64 : ((2 * k + 2 * kFU <= 128) ? 128 : 256);
+    const size_t smem = (size_t)(kScanNT / 32) * bufw * (4 + 4 + 8 + 4 + 4);
+    int32_t *fb = nullptr;
+    if (cudaMallocAsync((void **)&fb, sizeof(int32_t) * (nq + 1), s) != cudaSuccess)
+      return fail(MRPT_ECUDA, "mrpt_scan_topk: scratch allocation failed");
+    cudaMemsetAsync(fb, 0, sizeof(int32_t), s);
+    const double u = 5.9604644775390625e-08;  // 2^-24
+    const double eps = 2.0 * (d + 16) * u;
+    const double eta = 2.0 * (d + 16) * 1.401298464324817e-45;  // subnormal float spacing
+    topk_fn_f ffn = bufw == 64 ? k_scan_topk_filter<64>
+                               : (bufw == 128 ? k_scan_topk_filter<128> : k_scan_topk_filter<256>);
+    cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    a.k = k;
+    a.ids = ids;
+    a.dists = dists;
+    ffn<<<(unsigned)grid, kScanNT, smem, s>>>(a, eps, eta, fb + 1, fb);
+    // fallback: exact tiled kernel over the listed queries
+    a.qlist = fb + 1;
+    a.qcount = fb;
+    const int buf = (k + kScanNT <= 1024) ? 1024 : 2048;
+    topk_fn tfn = buf == 1024 ? k_scan_topk_tiled<1024> : k_scan_topk_tiled<2048>;
+    const size_t tsmem = (size_t)buf * 12 + sizeof(float) * (kScanNT / 32) * 32 * kTileStride +
+                         sizeof(double) * (size_t)d;
+    cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+    tfn<<<(unsigned)(grid < 64 ? grid : 64), kScanNT, tsmem, s>>>(a);
+    cudaFreeAsync(fb, s);
+    return launch_status("mrpt_scan_topk");
+  }
   for (int p = 0; p < passes; ++p) {
     const int off = p * chunk_max;
     const int kk = (k - off) < chunk_max ? (k - off) : chunk_max;
@@ -297,14 +773,21 @@ extern "C" int32_t mrpt_scan_topk(const float *X, int64_t n, int32_t d, int64_t 
     a.dists = dists + off;
     topk_fn fn;
     int buf;
-    if (kk + kScanNT * kScanR <= 2048) {
+    size_t extra = 0;
+    if (a.vec4) {
+      // tiled kernel: one 256-candidate round between threshold updates
+      buf = (kk + kScanNT <= 1024) ? 1024 : ((kk + kScanNT <= 2048) ? 2048 : 4096);
+      fn = buf == 1024 ? k_scan_topk_tiled<1024>
+                       : (buf == 2048 ? k_scan_topk_tiled<2048> : k_scan_topk_tiled<4096>);
+      extra = sizeof(float) * (kScanNT / 32) * 32 * kTileStride;
+    } else if (kk + kScanNT * kScanR <= 2048) {
       fn = k_scan_topk<2048>;
       buf = 2048;
     } else {
       fn = k_scan_topk<4096>;
       buf = 4096;
     }
-    const size_t smem = (size_t)buf * 12 + sizeof(double) * (size_t)d;
+    const size_t smem = (size_t)buf * 12 + extra + sizeof(double) * (size_t)d;
     if (smem > 220 * 1024) return fail(MRPT_EPARAM, "mrpt_scan_topk: d too large");
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     fn<<<(unsigned)grid, kScanNT, smem, s>>>(a);

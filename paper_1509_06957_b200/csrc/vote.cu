@@ -8,10 +8,13 @@
 // count can overflow into its neighbour.  When n > W the CTA sweeps the id
 // tiles in order with one cursor per tree: leaf slices built by K5 are
 // ascending, so the part of a slice inside the current tile is the next run
-// from the cursor.  A point is emitted exactly once, by the increment that
-// raises its count to v (the reference's `counts[idx] == v` test,
-// _cy.pyx:75-77).  Groups of G lanes share one tree slice (G ~ mean slice
-// length per tile) and each lane keeps U loads in flight.
+// from the cursor.  The increment that raises a count to v (the reference's
+// `counts[idx] == v` test, _cy.pyx:75-77) sets the point's bit in a per-tile
+// bitmap; after the tile, the bitmap is compacted in id order, so every
+// candidate list comes out ascending (the order candidate_set returns, and
+// the order that lets concurrent queries sweep X through L2 together).
+// Groups of G lanes share one tree slice (G ~ mean slice length per tile)
+// and each lane keeps U loads in flight.
 #include "common.cuh"
 
 namespace mrpt {
@@ -48,14 +51,56 @@ __device__ __forceinline__ uint32_t bump(uint32_t *cnt, int local) {
   }
 }
 
+// Append, in id order, the ids whose bit is set in bits[0..nwords) (tile
+// origin lo) to out[base..]; returns the new base (block-uniform).  Clears
+// the bitmap as it goes.
+__device__ __forceinline__ int64_t emit_bitmap(uint32_t *bits, int nwords, int32_t lo, int32_t *out,
+                                               int64_t base, int64_t cap, int *wsum) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = kVoteNT / 32;
+  for (int r0 = 0; r0 < nwords; r0 += kVoteNT) {
+    const int i = r0 + threadIdx.x;
+    uint32_t word = i < nwords ? bits[i] : 0u;
+    if (i < nwords && word) bits[i] = 0u;
+    const int pc = __popc(word);
+    int incl = pc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int before = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const int c = wsum[w];
+      before += w < warp ? c : 0;
+      tot += c;
+    }
+    int64_t pos = base + before + incl - pc;
+    while (word) {
+      const int b = __ffs(word) - 1;
+      if (pos < cap) out[pos] = lo + i * 32 + b;
+      ++pos;
+      word &= word - 1u;
+    }
+    base += tot;
+    __syncthreads();
+  }
+  return base;
+}
+
 template <int CW, int G, bool SORTED>
 __global__ void __launch_bounds__(kVoteNT) k_vote(VoteArgs a) {
   extern __shared__ uint4 vote_smem[];
   uint32_t *cnt = reinterpret_cast<uint32_t *>(vote_smem);
   const int cwords = a.W * CW / 4;  // W is a multiple of 64
-  int32_t *cur = reinterpret_cast<int32_t *>(cnt + cwords);
+  uint32_t *bits = cnt + cwords;    // W/32 words: "reached v" flags
+  const int bwords = a.W / 32;
+  int32_t *cur = reinterpret_cast<int32_t *>(bits + bwords);
   int32_t *endp = cur + a.T;
-  __shared__ int s_ncand;
+  __shared__ int wsum[kVoteNT / 32];
   const int tid = threadIdx.x, lane = tid & 31;
   const int gl = lane & (G - 1);
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
@@ -69,9 +114,10 @@ __global__ void __launch_bounds__(kVoteNT) k_vote(VoteArgs a) {
     }
     uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
     for (int i = tid; i < cwords / 4; i += kVoteNT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
-    if (tid == 0) s_ncand = 0;
+    for (int i = tid; i < bwords; i += kVoteNT) bits[i] = 0u;
     __syncthreads();
     int32_t *qcand = a.cand + q * a.cap;
+    int64_t ncand = 0;
     for (int tile = 0; tile < a.ntiles; ++tile) {
       const int32_t lo = tile * a.W;
       const int64_t hi64 = (int64_t)lo + a.W < a.n ? (int64_t)lo + a.W : a.n;
@@ -93,10 +139,9 @@ __global__ void __launch_bounds__(kVoteNT) k_vote(VoteArgs a) {
             for (int u = 0; u < kVoteU; ++u) {
               const bool in = id[u] < hi;
               if (in) {
-                if (bump<CW>(cnt, id[u] - lo) == (uint32_t)a.v) {
-                  const int slot = atomicAdd(&s_ncand, 1);
-                  if (slot < a.cap) qcand[slot] = id[u];
-                }
+                const int local = id[u] - lo;
+                if (bump<CW>(cnt, local) == (uint32_t)a.v)
+                  atomicOr(bits + (local >> 5), 1u << (local & 31));
               }
               consumed += __popc(__ballot_sync(gmask, in) & gmask);
             }
@@ -109,21 +154,21 @@ __global__ void __launch_bounds__(kVoteNT) k_vote(VoteArgs a) {
           for (int32_t idx = cur[t] + gl; idx < e; idx += G) {
             const int32_t id = __ldg(Lt + idx);
             if (id >= lo && id < hi) {
-              if (bump<CW>(cnt, id - lo) == (uint32_t)a.v) {
-                const int slot = atomicAdd(&s_ncand, 1);
-                if (slot < a.cap) qcand[slot] = id;
-              }
+              const int local = id - lo;
+              if (bump<CW>(cnt, local) == (uint32_t)a.v)
+                atomicOr(bits + (local >> 5), 1u << (local & 31));
             }
           }
         }
       }
       __syncthreads();
+      ncand = emit_bitmap(bits, (int)((hi - lo + 31) >> 5), lo, qcand, ncand, a.cap, wsum);
       if (tile + 1 < a.ntiles) {
         for (int i = tid; i < cwords / 4; i += kVoteNT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
       }
     }
-    if (tid == 0) a.ncand[q] = s_ncand;  // > cap means only cap ids were stored
+    if (tid == 0) a.ncand[q] = (int32_t)ncand;  // > cap means only cap ids were stored
     __syncthreads();
   }
 }
@@ -255,12 +300,13 @@ extern "C" int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_of
   // widest tile that fits; a single tile if n fits the two-CTA budget
   int64_t W;
   int64_t budget = kVoteSmemSingle - cursor_bytes - 64;
-  if ((int64_t)ceil_div<int64_t>(n, 64) * 64 * CW <= budget) {
+  // per id of a tile: CW counter bytes + 1/8 byte of "reached v" bitmap
+  if ((int64_t)ceil_div<int64_t>(n, 64) * (64 * CW + 8) <= budget) {
     W = ceil_div<int64_t>(n, 64) * 64;
   } else {
     budget = kVoteSmemTiled - cursor_bytes - 64;
-    if (budget < 64 * CW) return fail(MRPT_EPARAM, "mrpt_vote: too many trees for shared cursors");
-    W = budget / CW / 64 * 64;
+    if (budget < 64 * CW + 8) return fail(MRPT_EPARAM, "mrpt_vote: too many trees for shared cursors");
+    W = budget / (64 * CW + 8) * 64;
   }
   const int ntiles = (int)ceil_div<int64_t>(n, W);
   const bool sorted = leaves_sorted != 0 || ntiles == 1;
@@ -283,7 +329,7 @@ extern "C" int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_of
   a.ncand = ncand;
   a.W = (int)W;
   a.ntiles = ntiles;
-  const size_t smem = (size_t)W * CW + (size_t)cursor_bytes;
+  const size_t smem = (size_t)W * CW + (size_t)W / 8 + (size_t)cursor_bytes;
   vote_fn fn = sorted ? pick_cw<true>(CW, G) : pick_cw<false>(CW, G);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int per_sm = smem <= (size_t)kVoteSmemSingle ? 2 : 1;
