@@ -13,6 +13,8 @@
 // running threshold; whenever it fills it is bitonic-sorted and truncated to
 // the k best, which tightens the threshold.  Ties on d^2 order by id, as
 // np.lexsort((S, d2)) does.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace mrpt {
@@ -375,7 +377,6 @@ __global__ void __launch_bounds__(kScanNT, 3) k_scan_topk_tiled(TopkArgs a) {
 // Pass 2 recomputes E for the few survivors with the reference's sequential
 // float64 sum and orders them by (E, id).  A warp whose buffer cannot shrink
 // (masses of exact ties) sends its query to the exact tiled kernel.
-constexpr int kFU = 4;       // candidates per warp iteration
 constexpr int kFMaxJ = 8;    // d <= 128 * kFMaxJ
 
 __device__ __forceinline__ bool fpair_less(float ak, int ai, float bk, int bi) {
@@ -435,12 +436,14 @@ __device__ int warp_shrink(float *k, int32_t *id, int cnt, int n, int kk, double
   return keep;
 }
 
-template <int BUFW>
-__global__ void __launch_bounds__(kScanNT) k_scan_topk_filter(TopkArgs a, double eps, double eta,
+template <int BUFW, int FU, int MINB>
+__global__ void __launch_bounds__(kScanNT, MINB) k_scan_topk_filter(TopkArgs a, double eps, double eta,
                                                               int32_t *fb_list, int32_t *fb_count) {
   extern __shared__ unsigned long long topk_smem[];
   constexpr int NWARP = kScanNT / 32;
-  float *wkey = reinterpret_cast<float *>(topk_smem);                 // NWARP * BUFW
+  constexpr int kFU = FU;
+  float *qs = reinterpret_cast<float *>(topk_smem);                   // 128 * kFMaxJ
+  float *wkey = qs + 128 * kFMaxJ;                                     // NWARP * BUFW
   int32_t *wid = reinterpret_cast<int32_t *>(wkey + NWARP * BUFW);    // NWARP * BUFW
   unsigned long long *ckey = reinterpret_cast<unsigned long long *>(wid + NWARP * BUFW);  // NWARP*BUFW
   int32_t *cid = reinterpret_cast<int32_t *>(ckey + NWARP * BUFW);    // NWARP * BUFW
@@ -455,13 +458,9 @@ __global__ void __launch_bounds__(kScanNT) k_scan_topk_filter(TopkArgs a, double
   const int kk = a.k;
   for (int64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
     const float *qrow = a.Q + q * a.ldq;
-    float4 qv[kFMaxJ];
-#pragma unroll
-    for (int j = 0; j < kFMaxJ; ++j) {
-      const int c = j * 128 + 4 * lane;
-      qv[j] = (j < nj && c < d) ? *reinterpret_cast<const float4 *>(qrow + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    for (int c = tid; c < 128 * kFMaxJ; c += kScanNT) qs[c] = c < d ? qrow[c] : 0.f;
     if (tid == 0) s_bad = 0;
+    __syncthreads();
     int64_t m;
     if (a.cand) {
       const int64_t nc = a.ncand[q];
@@ -489,19 +488,20 @@ __global__ void __launch_bounds__(kScanNT) k_scan_topk_filter(TopkArgs a, double
       for (int j = 0; j < kFMaxJ; ++j) {
         const int c = j * 128 + 4 * lane;
         if (j < nj && c < d) {
+          const float4 qj = *reinterpret_cast<const float4 *>(qs + c);
           float4 x[kFU];
 #pragma unroll
           for (int u = 0; u < kFU; ++u) x[u] = __ldg(reinterpret_cast<const float4 *>(row[u] + c));
 #pragma unroll
           for (int u = 0; u < kFU; ++u) {
             float t;
-            t = x[u].x - qv[j].x;
+            t = x[u].x - qj.x;
             acc[u] = __fmaf_rn(t, t, acc[u]);
-            t = x[u].y - qv[j].y;
+            t = x[u].y - qj.y;
             acc[u] = __fmaf_rn(t, t, acc[u]);
-            t = x[u].z - qv[j].z;
+            t = x[u].z - qj.z;
             acc[u] = __fmaf_rn(t, t, acc[u]);
-            t = x[u].w - qv[j].w;
+            t = x[u].w - qj.w;
             acc[u] = __fmaf_rn(t, t, acc[u]);
           }
         }
@@ -694,6 +694,20 @@ extern "C" int32_t mrpt_scan(const float *X, int64_t n, int32_t d, int64_t ldx, 
 typedef void (*topk_fn)(TopkArgs);
 typedef void (*topk_fn_f)(TopkArgs, double, double, int32_t *, int32_t *);
 
+template <int FU, int MINB>
+static topk_fn_f pick_filter_b(int bufw) {
+  return bufw == 64 ? k_scan_topk_filter<64, FU, MINB>
+                    : (bufw == 128 ? k_scan_topk_filter<128, FU, MINB> : k_scan_topk_filter<256, FU, MINB>);
+}
+
+static topk_fn_f pick_filter(int bufw, int fu, int minb) {
+  if (fu == 8) return minb >= 3 ? pick_filter_b<8, 3>(bufw) : pick_filter_b<8, 2>(bufw);
+  if (fu == 2) return pick_filter_b<2, 4>(bufw);
+  if (minb >= 5) return pick_filter_b<4, 5>(bufw);
+  if (minb == 3) return pick_filter_b<4, 3>(bufw);
+  return pick_filter_b<4, 4>(bufw);
+}
+
 extern "C" int32_t mrpt_scan_topk(const float *X, int64_t n, int32_t d, int64_t ldx, const float *Q,
                                   int64_t nq, int64_t ldq, const int32_t *cand, int64_t cap,
                                   const int32_t *ncand, int32_t k, int64_t *ids, double *dists,
@@ -737,8 +751,8 @@ extern "C" int32_t mrpt_scan_topk(const float *X, int64_t n, int32_t d, int64_t 
   if (a.vec4 && qvec4 && d <= 128 * kFMaxJ && k <= 120) {
     // filter (float32) + exact float64 rerank; exact-tie overflows go to the
     // tiled exact kernel through a device-side query list.
-    const int bufw = (2 * k + 2 * kFU <= 64) ? 64 : ((2 * k + 2 * kFU <= 128) ? 128 : 256);
-    const size_t smem = (size_t)(kScanNT / 32) * bufw * (4 + 4 + 8 + 4 + 4);
+    const int bufw = (2 * k + 16 <= 64) ? 64 : ((2 * k + 16 <= 128) ? 128 : 256);
+    const size_t smem = sizeof(float) * 128 * kFMaxJ + (size_t)(kScanNT / 32) * bufw * (4 + 4 + 8 + 4 + 4);
     int32_t *fb = nullptr;
     if (cudaMallocAsync((void **)&fb, sizeof(int32_t) * (nq + 1), s) != cudaSuccess)
       return fail(MRPT_ECUDA, "mrpt_scan_topk: scratch allocation failed");
@@ -746,8 +760,10 @@ extern "C" int32_t mrpt_scan_topk(const float *X, int64_t n, int32_t d, int64_t 
     const double u = 5.9604644775390625e-08;  // 2^-24
     const double eps = 2.0 * (d + 16) * u;
     const double eta = 2.0 * (d + 16) * 1.401298464324817e-45;  // subnormal float spacing
-    topk_fn_f ffn = bufw == 64 ? k_scan_topk_filter<64>
-                               : (bufw == 128 ? k_scan_topk_filter<128> : k_scan_topk_filter<256>);
+    const char *var = getenv("MRPT_SCAN_VARIANT");  // experiments: "FU,MINB"
+    int fu = 4, minb = 4;
+    if (var) sscanf(var, "%d,%d", &fu, &minb);
+    topk_fn_f ffn = pick_filter(bufw, fu, minb);
     cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     a.k = k;
     a.ids = ids;
