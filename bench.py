@@ -213,7 +213,12 @@ def run_ours(args):
     Xd = torch.from_numpy(X).cuda()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    index = mrpt.grow_trees(Xd, p["n_trees"], p["depth"], p["sparsity"], seed=p["seed"])
+    if world > 1:
+        from paper_1509_06957_b200.distributed import grow_trees_distributed
+
+        index = grow_trees_distributed(Xd, p["n_trees"], p["depth"], p["sparsity"], seed=p["seed"])
+    else:
+        index = mrpt.grow_trees(Xd, p["n_trees"], p["depth"], p["sparsity"], seed=p["seed"])
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0  # includes the GPU FNV checksum
     D = index.device_index()

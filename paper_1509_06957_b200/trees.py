@@ -303,14 +303,7 @@ def _batch_trees(n, d, depth, T, free_bytes):
     return tb
 
 
-def grow_trees(X, n_trees, depth, sparsity=None, seed=0, fixed_count=False, threads=None,
-               batch_trees=None):
-    """Build ``n_trees`` trees of the given depth over ``X`` (trees.py:187-245).
-
-    Same validation and errors as the reference.  ``threads`` (or
-    MRPT_THREADS) is validated for compatibility; the work itself runs as
-    batched GPU kernels.  ``batch_trees`` overrides the trees per launch.
-    """
+def _validate_grow(X, n_trees, depth, sparsity, seed, threads):
     X = as_dataset(X)
     if n_trees < 1:
         raise ParameterError(f"tree count must be >= 1, got {n_trees}")
@@ -327,38 +320,49 @@ def grow_trees(X, n_trees, depth, sparsity=None, seed=0, fixed_count=False, thre
     _resolve_threads(threads)
     if not 0.0 < sparsity <= 1.0:
         raise ParameterError(f"sparsity must lie in (0, 1], got {sparsity}")
+    return X, float(sparsity), seed
+
+
+def _grow_block(X, t_begin, t_end, depth, sparsity, seed, fixed_count, splits, offsets, indices,
+                batch_trees=None):
+    """Build trees [t_begin, t_end) of an index (tree t from seed (seed, t)) into
+    the device arrays ``splits/offsets/indices`` (rows 0 .. t_end-t_begin-1).
+    Returns the host matrices of those trees.  No host synchronisation."""
     torch = _device.torch_mod()
     Xd = X.device()
     n, d = X.n, X.d
-    nleaf = 1 << depth
     dev = Xd.device
-    splits = torch.empty((n_trees, nleaf - 1), dtype=torch.float32, device=dev)
-    offsets = torch.empty((n_trees, nleaf + 1), dtype=torch.int64, device=dev)
-    indices = torch.empty((n_trees, n), dtype=torch.int32, device=dev)
+    count = t_end - t_begin
     free = torch.cuda.mem_get_info(dev)[0]
-    tb = batch_trees or _batch_trees(n, d, depth, n_trees, free)
+    tb = min(count, batch_trees or _batch_trees(n, d, depth, count, free))
     sz = ctypes.c_size_t(0)
     _native.call("mrpt_build_workspace_size", n, tb, depth, ctypes.byref(sz))
     ws = torch.empty(max(1, sz.value), dtype=torch.uint8, device=dev)
     P = torch.empty((tb, depth, n), dtype=torch.float32, device=dev)
     matrices = []
     stream = _native.stream_ptr()
-    for b0 in range(0, n_trees, tb):
-        b1 = min(n_trees, b0 + tb)
-        mats = [sample_sparse_matrix(d, depth, sparsity, seed=(seed, t), fixed_count=fixed_count)
-                for t in range(b0, b1)]
+    for b0 in range(0, count, tb):
+        b1 = min(count, b0 + tb)
+        mats = [sample_sparse_matrix(d, depth, sparsity, seed=(seed, t_begin + t),
+                                     fixed_count=fixed_count) for t in range(b0, b1)]
         matrices.extend(mats)
         for R in mats:
             _record_macs(n * R.nnz)
         cp, rows, vals = _device.csc_device(mats)
-        # P[(t*depth + lev)*n + i]: row stride 1, column stride n
+        # K1: P[(t*depth + lev)*n + i] (row stride 1, column stride n)
         _native.call("mrpt_project", _native.ptr(Xd), n, d, d, _native.ptr(cp), _native.ptr(rows),
                      _native.ptr(vals), (b1 - b0) * depth, _native.ptr(P), 1, n, stream)
+        # K5: all levels of the batch
         _native.call("mrpt_build_levels", _native.ptr(P), n, b1 - b0, depth,
                      _native.ptr(splits[b0:]), _native.ptr(offsets[b0:]),
                      _native.ptr(indices[b0:]), _native.ptr(ws), sz.value, stream)
         del cp, rows, vals
-    del P, ws
+    return matrices
+
+
+def _finish_index(X, n_trees, depth, sparsity, seed, fixed_count, matrices, splits, offsets,
+                  indices):
+    Xd = X.device()
     sizes = offsets[:, 1:] - offsets[:, :-1]
     max_leaf = int(sizes.max().item())
     cp, rows, vals = _device.csc_device(matrices)
@@ -368,3 +372,27 @@ def grow_trees(X, n_trees, depth, sparsity=None, seed=0, fixed_count=False, thre
                      fixed_count=fixed_count, matrices=matrices, splits=splits,
                      leaf_offsets=offsets, leaf_indices=indices,
                      dataset_checksum=X.checksum, _device_index=dindex)
+
+
+def _alloc_index(n_trees, n, depth, dev):
+    torch = _device.torch_mod()
+    nleaf = 1 << depth
+    return (torch.empty((n_trees, nleaf - 1), dtype=torch.float32, device=dev),
+            torch.empty((n_trees, nleaf + 1), dtype=torch.int64, device=dev),
+            torch.empty((n_trees, n), dtype=torch.int32, device=dev))
+
+
+def grow_trees(X, n_trees, depth, sparsity=None, seed=0, fixed_count=False, threads=None,
+               batch_trees=None):
+    """Build ``n_trees`` trees of the given depth over ``X`` (trees.py:187-245).
+
+    Same validation and errors as the reference.  ``threads`` (or
+    MRPT_THREADS) is validated for compatibility; the work itself runs as
+    batched GPU kernels.  ``batch_trees`` overrides the trees per launch.
+    """
+    X, sparsity, seed = _validate_grow(X, n_trees, depth, sparsity, seed, threads)
+    splits, offsets, indices = _alloc_index(n_trees, X.n, depth, X.device().device)
+    matrices = _grow_block(X, 0, n_trees, depth, sparsity, seed, fixed_count, splits, offsets,
+                           indices, batch_trees)
+    return _finish_index(X, n_trees, depth, sparsity, seed, fixed_count, matrices, splits, offsets,
+                         indices)
