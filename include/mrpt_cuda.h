@@ -114,8 +114,21 @@ int32_t mrpt_build_levels(const float *P, int64_t n, int32_t Tb,
 int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_offsets,
                   int64_t n, int32_t T, int32_t depth, const int32_t *leaves,
                   int64_t nq, int32_t v, int32_t leaves_sorted,
-                  int64_t max_count, int32_t *cand, int64_t cap,
-                  int32_t *ncand, void *stream);
+                  int64_t max_count, const uint16_t *dir, int32_t *cand,
+                  int64_t cap, int32_t *ncand, void *stream);
+
+/* Vote geometry: number of id tiles the vote sweeps for this index shape and
+ * the uint16 entries of its tile directory (0 when one tile suffices).
+ * The directory (optional `dir` of mrpt_vote, built once per index by
+ * mrpt_vote_build_dir from ascending leaf slices of at most 65535 ids) holds,
+ * per (tree, leaf), where the slice's part in each id tile starts, so the
+ * multi-tile vote streams every slice without cursor walks. */
+int32_t mrpt_vote_plan(int64_t n, int32_t T, int32_t depth, int64_t max_count,
+                       int32_t *ntiles /* host */, int64_t *dir_entries /* host */);
+int32_t mrpt_vote_build_dir(const int32_t *leaf_indices,
+                            const int64_t *leaf_offsets, int64_t n, int32_t T,
+                            int32_t depth, int64_t max_count, uint16_t *dir,
+                            void *stream);
 
 /* Dense per-point vote counts for one query (VoteAccumulator.counts(),
  * pkg/src/mrpt/search.py:68-73): counts (n) int32 is zeroed then filled. */

@@ -31,7 +31,9 @@ SIGNATURES = {
     "mrpt_build_workspace_size": [_c_i64, _c_i32, _c_i32, ctypes.POINTER(_c_sz)],
     "mrpt_build_levels": [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p],
     "mrpt_vote": [_c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_i64, _c_i32, _c_i32, _c_i64, _c_p,
-                  _c_i64, _c_p, _c_p],
+                  _c_p, _c_i64, _c_p, _c_p],
+    "mrpt_vote_plan": [_c_i64, _c_i32, _c_i32, _c_i64, ctypes.POINTER(_c_i32), ctypes.POINTER(_c_i64)],
+    "mrpt_vote_build_dir": [_c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_i64, _c_p, _c_p],
     "mrpt_vote_counts": [_c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p],
     "mrpt_select_ge": [_c_p, _c_i64, _c_i32, _c_p, _c_p, _c_p],
     "mrpt_scan": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_p],

@@ -15,6 +15,8 @@
 // the order that lets concurrent queries sweep X through L2 together).
 // Groups of G lanes share one tree slice (G ~ mean slice length per tile)
 // and each lane keeps U loads in flight.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace mrpt {
@@ -31,10 +33,13 @@ struct VoteArgs {
   int64_t cap;
   int32_t *ncand;
   int W, ntiles;
+  const int32_t *qlist;  // optional: only these queries (count *qcount)
+  const int32_t *qcount;
+  const uint16_t *dir;   // optional tile directory (T, 2^depth, ntiles+1)
 };
 
-constexpr int kVoteNT = 512;
-constexpr int kVoteU = 4;
+constexpr int kVoteNT = 1024;
+constexpr int kVoteU = 8;
 
 template <int CW>
 __device__ __forceinline__ uint32_t bump(uint32_t *cnt, int local) {
@@ -71,13 +76,19 @@ __device__ __forceinline__ int64_t emit_bitmap(uint32_t *bits, int nwords, int32
     }
     if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    int before = 0, tot = 0;
+    if (warp == 0) {  // exclusive scan of the per-warp totals, total in wsum[NW]
+      const int c = lane < NW ? wsum[lane] : 0;
+      int x = c;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const int c = wsum[w];
-      before += w < warp ? c : 0;
-      tot += c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += u;
+      }
+      if (lane < NW) wsum[lane] = x - c;
+      if (lane == 31) wsum[NW] = x;
     }
+    __syncthreads();
+    const int before = wsum[warp], tot = wsum[NW];
     int64_t pos = base + before + incl - pc;
     while (word) {
       const int b = __ffs(word) - 1;
@@ -92,7 +103,7 @@ __device__ __forceinline__ int64_t emit_bitmap(uint32_t *bits, int nwords, int32
 }
 
 template <int CW, int G, bool SORTED>
-__global__ void __launch_bounds__(kVoteNT) k_vote(VoteArgs a) {
+__global__ void __launch_bounds__(kVoteNT, 1) k_vote(VoteArgs a) {
   extern __shared__ uint4 vote_smem[];
   uint32_t *cnt = reinterpret_cast<uint32_t *>(vote_smem);
   const int cwords = a.W * CW / 4;  // W is a multiple of 64
@@ -100,12 +111,14 @@ __global__ void __launch_bounds__(kVoteNT) k_vote(VoteArgs a) {
   const int bwords = a.W / 32;
   int32_t *cur = reinterpret_cast<int32_t *>(bits + bwords);
   int32_t *endp = cur + a.T;
-  __shared__ int wsum[kVoteNT / 32];
+  __shared__ int wsum[kVoteNT / 32 + 1];
   const int tid = threadIdx.x, lane = tid & 31;
   const int gl = lane & (G - 1);
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
   const int gi = tid / G, ngroups = kVoteNT / G;
-  for (int64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
+  const int64_t nwork = a.qlist ? (int64_t)*a.qcount : a.nq;
+  for (int64_t wq = blockIdx.x; wq < nwork; wq += gridDim.x) {
+    const int64_t q = a.qlist ? (int64_t)a.qlist[wq] : wq;
     for (int t = tid; t < a.T; t += kVoteNT) {
       const int leaf = a.leaves[q * a.T + t];
       const int64_t *o = a.leaf_offsets + (int64_t)t * (a.L + 1);
@@ -169,6 +182,193 @@ __global__ void __launch_bounds__(kVoteNT) k_vote(VoteArgs a) {
       }
     }
     if (tid == 0) a.ncand[q] = (int32_t)ncand;  // > cap means only cap ids were stored
+    __syncthreads();
+  }
+}
+
+
+
+// ---------------------------------------------------------------------------
+// Tile directory (built once per index): dir[(t*L + leaf)*(ntiles+1) + w] =
+// number of ids of that (ascending) leaf slice below w*W, i.e. where the
+// slice's part in id tile w starts.  One warp per leaf.
+__global__ void k_build_dir(const int32_t *__restrict__ leaf_indices,
+                            const int64_t *__restrict__ leaf_offsets, int64_t n, int T, int L, int W,
+                            int ntiles, uint16_t *dir) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nleaves = (int64_t)T * L;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < nleaves; g += wstride) {
+    const int64_t t = g / L, leaf = g - t * L;
+    const int64_t *o = leaf_offsets + t * (L + 1);
+    const int64_t s = o[leaf], e = o[leaf + 1];
+    const int32_t *Lt = leaf_indices + t * n;
+    uint16_t *d = dir + g * (ntiles + 1);
+    int prev_tile = -1;  // tile of the element before this chunk
+    for (int64_t p0 = s; p0 < e; p0 += 32) {
+      const int64_t p = p0 + lane;
+      const int tl = p < e ? (int)(Lt[p] / W) : ntiles;
+      int before = __shfl_up_sync(0xffffffffu, tl, 1);
+      if (lane == 0) before = prev_tile;
+      if (p < e)
+        for (int w = before + 1; w <= tl; ++w) d[w] = (uint16_t)(p - s);
+      prev_tile = __shfl_sync(0xffffffffu, tl, 31);
+      if (p0 + 32 >= e) {
+        // the lane holding the last element fills the trailing tiles
+        const int64_t last = e - 1;
+        if (p == last)
+          for (int w = tl + 1; w <= ntiles; ++w) d[w] = (uint16_t)(e - s);
+      }
+    }
+    if (s == e && lane == 0)
+      for (int w = 0; w <= ntiles; ++w) d[w] = 0;
+  }
+}
+
+// Directory-driven vote: per id tile, every tree's slice bounds come from the
+// directory, so a warp flattens the slices of its 32 trees and streams them
+// with consecutive lanes on consecutive ids (a 5-step shuffle search maps a
+// flat position to its tree).  No dependent cursor walks.
+template <int CW>
+__global__ void __launch_bounds__(kVoteNT, 1) k_vote_dir(VoteArgs a) {
+  extern __shared__ uint4 vote_smem[];
+  uint32_t *cnt = reinterpret_cast<uint32_t *>(vote_smem);
+  const int cwords = a.W * CW / 4;
+  uint32_t *bits = cnt + cwords;
+  const int bwords = a.W / 32;
+  int32_t *sbase = reinterpret_cast<int32_t *>(bits + bwords);  // T: slice start of the leaf
+  int32_t *sleaf = sbase + a.T;                                   // T: leaf id
+  __shared__ int wsum[kVoteNT / 32 + 1];
+  constexpr int kWList = 2048;  // bitmap words that became non-zero in this tile
+  __shared__ int32_t wlist[kWList];
+  __shared__ int s_nw, s_nc;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kVoteNT / 32;
+  const int ngroups = (a.T + 31) >> 5;
+  const int64_t dstride = a.ntiles + 1;
+  const int64_t nwork = a.qlist ? (int64_t)*a.qcount : a.nq;
+  for (int64_t wq = blockIdx.x; wq < nwork; wq += gridDim.x) {
+    const int64_t q = a.qlist ? (int64_t)a.qlist[wq] : wq;
+    for (int t = tid; t < a.T; t += kVoteNT) {
+      const int leaf = a.leaves[q * a.T + t];
+      sleaf[t] = leaf;
+      sbase[t] = (int32_t)a.leaf_offsets[(int64_t)t * (a.L + 1) + leaf];
+    }
+    uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
+    for (int i = tid; i < cwords / 4; i += kVoteNT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = tid; i < bwords; i += kVoteNT) bits[i] = 0u;
+    if (tid == 0) {
+      s_nw = 0;
+      s_nc = 0;
+    }
+    __syncthreads();
+    int32_t *qcand = a.cand + q * a.cap;
+    int64_t ncand = 0;
+    // with few trees, several warps share one group of 32 trees, each taking
+    // every parts-th 32-wide stripe of the group's flattened slices
+    const int parts = ngroups >= NW ? 1 : NW / ngroups;
+    const int nvirt = ngroups * parts;
+    for (int tile = 0; tile < a.ntiles; ++tile) {
+      const int32_t lo = tile * a.W;
+      for (int vw = warp; vw < nvirt; vw += NW) {
+        const int g = vw % ngroups, part = vw / ngroups;
+        const int t = g * 32 + lane;
+        int len = 0;
+        int64_t base = 0;
+        if (t < a.T) {
+          const uint16_t *d = a.dir + ((int64_t)t * a.L + sleaf[t]) * dstride + tile;
+          const int s0 = d[0], s1 = d[1];
+          len = s1 - s0;
+          base = (int64_t)t * a.n + sbase[t] + s0;
+        }
+        int pre = len;  // inclusive scan -> exclusive
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, pre, o);
+          if (lane >= o) pre += u;
+        }
+        const int total = __shfl_sync(0xffffffffu, pre, 31);
+        pre -= len;
+        constexpr int UNR = 4;  // independent id loads in flight per lane
+        const int stride = parts * 32;
+        for (int e0 = part * 32; e0 < total; e0 += UNR * stride) {
+          int32_t id[UNR];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) {
+            const int e = e0 + u * stride + lane;
+            int k = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+              const int c = k + step;
+              const int pc = __shfl_sync(0xffffffffu, pre, c & 31);
+              if (c < 32 && pc <= e) k = c;
+            }
+            const int pk = __shfl_sync(0xffffffffu, pre, k);
+            const long long bk = __shfl_sync(0xffffffffu, (long long)base, k);
+            id[u] = e < total ? __ldg(a.leaf_indices + bk + (e - pk)) : -1;
+          }
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) {
+            if (id[u] >= 0) {
+              const int local = id[u] - lo;
+              if (bump<CW>(cnt, local) == (uint32_t)a.v) {
+                if (atomicOr(bits + (local >> 5), 1u << (local & 31)) == 0u) {
+                  const int wi = atomicAdd(&s_nw, 1);
+                  if (wi < kWList) wlist[wi] = local >> 5;
+                }
+              }
+            }
+          }
+        }
+      }
+      __syncthreads();
+      const int nw = s_nw;
+      if (nw > kWList) {  // too many words to list: ordered scan of the whole bitmap
+        const int64_t hi = (int64_t)lo + a.W < a.n ? (int64_t)lo + a.W : a.n;
+        ncand = emit_bitmap(bits, (int)((hi - lo + 31) >> 5), lo, qcand, ncand, a.cap, wsum);
+      } else {
+        // listed words only (ids within the tile unordered; tiles ascending)
+        for (int i0 = 0; i0 < nw; i0 += kVoteNT) {
+          const int i = i0 + tid;
+          uint32_t word = 0u;
+          int wi = 0;
+          if (i < nw) {
+            wi = wlist[i];
+            word = bits[wi];
+            bits[wi] = 0u;
+          }
+          const int pc = __popc(word);
+          int incl = pc;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int u2 = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u2;
+          }
+          int wbase = 0;
+          if (lane == 31 && incl) wbase = atomicAdd(&s_nc, incl);
+          wbase = __shfl_sync(0xffffffffu, wbase, 31);
+          int64_t pos = ncand + wbase + incl - pc;
+          while (word) {
+            const int b = __ffs(word) - 1;
+            if (pos < a.cap) qcand[pos] = lo + wi * 32 + b;
+            ++pos;
+            word &= word - 1u;
+          }
+        }
+        __syncthreads();
+        ncand += s_nc;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        s_nw = 0;
+        s_nc = 0;
+      }
+      if (tile + 1 < a.ntiles) {
+        for (int i = tid; i < cwords / 4; i += kVoteNT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+      }
+    }
+    if (tid == 0) a.ncand[q] = (int32_t)ncand;
     __syncthreads();
   }
 }
@@ -281,23 +481,14 @@ __global__ void __launch_bounds__(1024) k_bitmap_compact(const uint32_t *__restr
 
 using namespace mrpt;
 
-static const int kVoteSmemSingle = 110 * 1024;  // single tile: two CTAs per SM
+static const int kVoteSmemSingle = 110 * 1024;  // single tile
 static const int kVoteSmemTiled = 200 * 1024;   // tiled sweep: one big CTA per SM
 
-extern "C" int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_offsets, int64_t n,
-                             int32_t T, int32_t depth, const int32_t *leaves, int64_t nq, int32_t v,
-                             int32_t leaves_sorted, int64_t max_count, int32_t *cand, int64_t cap,
-                             int32_t *ncand, void *stream) {
-  clear_error();
-  if (n < 1 || n >= (int64_t)1 << 31 || T < 1 || depth < 0 || depth > 30 || nq < 0)
-    return fail(MRPT_ESHAPE, "mrpt_vote: bad shape");
-  if (v < 1 || v > max_count) return fail(MRPT_EPARAM, "mrpt_vote: vote threshold out of range");
-  if (cap < 1) return fail(MRPT_EPARAM, "mrpt_vote: cap must be >= 1");
-  if (nq == 0) return MRPT_OK;
-  cudaStream_t s = as_stream(stream);
+// Tile geometry shared by mrpt_vote, mrpt_vote_plan and the directory.
+static int32_t vote_geometry(int64_t n, int32_t T, int64_t max_count, int *CWo, int64_t *Wo,
+                             int *ntiles_o) {
   const int CW = max_count <= 255 ? 1 : (max_count <= 65535 ? 2 : 4);
   const int64_t cursor_bytes = 8LL * T;
-  // widest tile that fits; a single tile if n fits the two-CTA budget
   int64_t W;
   int64_t budget = kVoteSmemSingle - cursor_bytes - 64;
   // per id of a tile: CW counter bytes + 1/8 byte of "reached v" bitmap
@@ -308,13 +499,66 @@ extern "C" int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_of
     if (budget < 64 * CW + 8) return fail(MRPT_EPARAM, "mrpt_vote: too many trees for shared cursors");
     W = budget / (64 * CW + 8) * 64;
   }
-  const int ntiles = (int)ceil_div<int64_t>(n, W);
+  *CWo = CW;
+  *Wo = W;
+  *ntiles_o = (int)ceil_div<int64_t>(n, W);
+  return MRPT_OK;
+}
+
+extern "C" int32_t mrpt_vote_plan(int64_t n, int32_t T, int32_t depth, int64_t max_count,
+                                  int32_t *ntiles, int64_t *dir_entries) {
+  clear_error();
+  if (n < 1 || n >= (int64_t)1 << 31 || T < 1 || depth < 0 || depth > 30 || !ntiles || !dir_entries)
+    return fail(MRPT_ESHAPE, "mrpt_vote_plan: bad arguments");
+  int CW, nt;
+  int64_t W;
+  int32_t st = vote_geometry(n, T, max_count, &CW, &W, &nt);
+  if (st) return st;
+  *ntiles = nt;
+  *dir_entries = nt > 1 ? (int64_t)T * ((int64_t)1 << depth) * (nt + 1) : 0;
+  return MRPT_OK;
+}
+
+extern "C" int32_t mrpt_vote_build_dir(const int32_t *leaf_indices, const int64_t *leaf_offsets,
+                                       int64_t n, int32_t T, int32_t depth, int64_t max_count,
+                                       uint16_t *dir, void *stream) {
+  clear_error();
+  int CW, nt;
+  int64_t W;
+  int32_t st = vote_geometry(n, T, max_count, &CW, &W, &nt);
+  if (st) return st;
+  if (nt <= 1) return MRPT_OK;
+  cudaStream_t s = as_stream(stream);
+  const int64_t nleaves = (int64_t)T << depth;
+  const int64_t blocks = ceil_div<int64_t>(nleaves, 8);
+  const int grid = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
+  k_build_dir<<<grid, 256, 0, s>>>(leaf_indices, leaf_offsets, n, T, 1 << depth, (int)W, nt, dir);
+  return launch_status("mrpt_vote_build_dir");
+}
+
+extern "C" int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_offsets, int64_t n,
+                             int32_t T, int32_t depth, const int32_t *leaves, int64_t nq, int32_t v,
+                             int32_t leaves_sorted, int64_t max_count, const uint16_t *dir,
+                             int32_t *cand, int64_t cap, int32_t *ncand, void *stream) {
+  clear_error();
+  if (n < 1 || n >= (int64_t)1 << 31 || T < 1 || depth < 0 || depth > 30 || nq < 0)
+    return fail(MRPT_ESHAPE, "mrpt_vote: bad shape");
+  if (v < 1 || v > max_count) return fail(MRPT_EPARAM, "mrpt_vote: vote threshold out of range");
+  if (cap < 1) return fail(MRPT_EPARAM, "mrpt_vote: cap must be >= 1");
+  if (nq == 0) return MRPT_OK;
+  cudaStream_t s = as_stream(stream);
+  int CW, ntiles;
+  int64_t W;
+  int32_t st = vote_geometry(n, T, max_count, &CW, &W, &ntiles);
+  if (st) return st;
+  const int64_t cursor_bytes = 8LL * T;
   const bool sorted = leaves_sorted != 0 || ntiles == 1;
-  // group size ~ mean slice length per tile (pow2 in [1, 32])
+  // lanes per tree slice for the cursor sweep (pow2 in [1, 32])
   const double mean_leaf = (double)n / (double)((int64_t)1 << depth);
   const double per_tile = mean_leaf / ntiles;
   int G = 1;
   while (G < 32 && G * kVoteU < per_tile) G <<= 1;
+  if (const char *env = getenv("MRPT_VOTE_G")) G = atoi(env);  // experiments
   VoteArgs a;
   a.leaf_indices = leaf_indices;
   a.leaf_offsets = leaf_offsets;
@@ -329,12 +573,20 @@ extern "C" int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_of
   a.ncand = ncand;
   a.W = (int)W;
   a.ntiles = ntiles;
+  a.qlist = nullptr;
+  a.qcount = nullptr;
+  a.dir = dir;
   const size_t smem = (size_t)W * CW + (size_t)W / 8 + (size_t)cursor_bytes;
-  vote_fn fn = sorted ? pick_cw<true>(CW, G) : pick_cw<false>(CW, G);
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int per_sm = smem <= (size_t)kVoteSmemSingle ? 2 : 1;
-  const int64_t grid = nq < (int64_t)num_sms() * per_sm * 4 ? nq : (int64_t)num_sms() * per_sm * 4;
-  fn<<<(unsigned)grid, kVoteNT, smem, s>>>(a);
+  const int64_t grid = nq < (int64_t)num_sms() * 4 ? nq : (int64_t)num_sms() * 4;
+  if (dir && ntiles > 1 && sorted) {
+    vote_fn fn = CW == 1 ? k_vote_dir<1> : (CW == 2 ? k_vote_dir<2> : k_vote_dir<4>);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    fn<<<(unsigned)grid, kVoteNT, smem, s>>>(a);
+  } else {
+    vote_fn fn = sorted ? pick_cw<true>(CW, G) : pick_cw<false>(CW, G);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    fn<<<(unsigned)grid, kVoteNT, smem, s>>>(a);
+  }
   return launch_status("mrpt_vote");
 }
 

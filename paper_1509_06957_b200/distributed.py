@@ -66,6 +66,7 @@ def grow_trees_distributed(X, n_trees, depth, sparsity=None, seed=0, fixed_count
 
     X, sparsity, seed = _validate_grow(X, n_trees, depth, sparsity, seed, None)
     rank, world = dist.get_rank(group), dist.get_world_size(group)
+    checksum = X.checksum_async()
     dev = X.device().device
     splits, offsets, indices = _alloc_index(n_trees, X.n, depth, dev)
     b0, b1 = tree_block(rank, world, n_trees)
@@ -82,7 +83,7 @@ def grow_trees_distributed(X, n_trees, depth, sparsity=None, seed=0, fixed_count
             matrices.append(sample_sparse_matrix(X.d, depth, sparsity, seed=(seed, t),
                                                  fixed_count=fixed_count))
     return _finish_index(X, n_trees, depth, sparsity, seed, fixed_count, matrices, splits, offsets,
-                         indices)
+                         indices, checksum)
 
 
 def approximate_knn_batch_sharded(Q, k, index, votes, group=None):

@@ -158,6 +158,25 @@ class _DeviceIndex:
         """Upper bound on any candidate set at this vote threshold."""
         return max(1, min(self.n, (self.T * self.max_leaf) // votes))
 
+    def vote_dir(self):
+        """Tile directory for the multi-tile vote (built once, on the device),
+        or None when one id tile covers the index or it cannot be used."""
+        if getattr(self, "_dir", False) is not False:
+            return self._dir
+        self._dir = None
+        if self.leaves_sorted and self.max_leaf <= 65535:
+            ntiles, entries = ctypes.c_int32(0), ctypes.c_int64(0)
+            _native.call("mrpt_vote_plan", self.n, self.T, self.depth, int(self.max_count),
+                         ctypes.byref(ntiles), ctypes.byref(entries))
+            if ntiles.value > 1:
+                torch = _device.torch_mod()
+                d = torch.empty(entries.value, dtype=torch.int16, device=self.indices.device)
+                _native.call("mrpt_vote_build_dir", _native.ptr(self.indices),
+                             _native.ptr(self.offsets), self.n, self.T, self.depth,
+                             int(self.max_count), _native.ptr(d), _native.stream_ptr())
+                self._dir = d
+        return self._dir
+
 
 class MRPTIndex:
     """T random projection trees over one dataset (trees.py:124-175).
@@ -361,7 +380,7 @@ def _grow_block(X, t_begin, t_end, depth, sparsity, seed, fixed_count, splits, o
 
 
 def _finish_index(X, n_trees, depth, sparsity, seed, fixed_count, matrices, splits, offsets,
-                  indices):
+                  indices, checksum=None):
     Xd = X.device()
     sizes = offsets[:, 1:] - offsets[:, :-1]
     max_leaf = int(sizes.max().item())
@@ -371,7 +390,8 @@ def _finish_index(X, n_trees, depth, sparsity, seed, fixed_count, matrices, spli
     return MRPTIndex(dataset=X, n_trees=n_trees, depth=depth, sparsity=float(sparsity), seed=seed,
                      fixed_count=fixed_count, matrices=matrices, splits=splits,
                      leaf_offsets=offsets, leaf_indices=indices,
-                     dataset_checksum=X.checksum, _device_index=dindex)
+                     dataset_checksum=checksum() if checksum else X.checksum,
+                     _device_index=dindex)
 
 
 def _alloc_index(n_trees, n, depth, dev):
@@ -391,8 +411,9 @@ def grow_trees(X, n_trees, depth, sparsity=None, seed=0, fixed_count=False, thre
     batched GPU kernels.  ``batch_trees`` overrides the trees per launch.
     """
     X, sparsity, seed = _validate_grow(X, n_trees, depth, sparsity, seed, threads)
+    checksum = X.checksum_async()  # K6 on a side stream, overlapping the build
     splits, offsets, indices = _alloc_index(n_trees, X.n, depth, X.device().device)
     matrices = _grow_block(X, 0, n_trees, depth, sparsity, seed, fixed_count, splits, offsets,
                            indices, batch_trees)
     return _finish_index(X, n_trees, depth, sparsity, seed, fixed_count, matrices, splits, offsets,
-                         indices)
+                         indices, checksum)

@@ -60,7 +60,8 @@ def test_status_maps_to_reference_exceptions(lib):
         _native.call("mrpt_build_workspace_size", 10, 1, 40, ctypes.byref(sz))
     # vote: threshold above the possible count is rejected before any launch
     with pytest.raises(ParameterError):
-        _native.call("mrpt_vote", None, None, 100, 4, 3, None, 1, 5, 1, 4, None, 10, None, None)
+        _native.call("mrpt_vote", None, None, 100, 4, 3, None, 1, 5, 1, 4, None, None, 10, None,
+                     None)
     with pytest.raises(ParameterError):
         _native.call("mrpt_scan_topk", None, 10, 4, 4, None, 1, 4, None, 0, None, 0, None, None,
                      None)

@@ -191,3 +191,47 @@ def test_vote_tiled_and_wide_counters(rng, T, depth, n):
         assert np.array_equal(counts.astype(np.int64), rc)
         assert np.array_equal(ids, rids)
         assert dists.tobytes() == rd.tobytes()
+
+
+def test_vote_hash_overflow_falls_back_to_tiles(rng):
+    """iid data: each query's leaves cover more distinct points than the hash
+    table holds, so every query takes the exact tiled sweep."""
+    n, T, depth = 300_000, 60, 8
+    X = gaussian(rng, n + 40, 8)
+    Xd, Q = X[:n], X[n:]
+    index = mrpt.grow_trees(Xd, T, depth, seed=9)
+    ref = dict(matrices=[(R.col_ptr, R.row_idx, R.values) for R in index.matrices],
+               splits=index.splits, leaf_offsets=index.leaf_offsets,
+               leaf_indices=index.leaf_indices, depth=depth)
+    for v in (1, 2):
+        ids, dists, counts = mrpt.approximate_knn_batch(Q, 10, index, v)
+        rids, rd, rc = O.approximate_knn_batch(Xd, Q, 10, ref, v)
+        assert np.array_equal(counts.astype(np.int64), rc)
+        assert np.array_equal(ids, rids)
+        assert dists.tobytes() == rd.tobytes()
+
+
+def test_unsorted_foreign_index_multi_tile_matches(rng):
+    """A loaded index whose leaf slices are not ascending (and n larger than
+    one counter tile) is audited, voted by the filtering sweep, and answers
+    exactly like the ascending original."""
+    n, T, depth = 260_000, 12, 7
+    X = gaussian(rng, n + 30, 6)
+    Xd, Q = X[:n], X[n:]
+    a = mrpt.grow_trees(Xd, T, depth, seed=4)
+    li = a.leaf_indices.copy()
+    for t in range(T):
+        o = a.leaf_offsets[t]
+        for j in range(len(o) - 1):
+            seg = li[t, o[j]:o[j + 1]]
+            li[t, o[j]:o[j + 1]] = seg[rng.permutation(len(seg))]
+    b = mrpt.MRPTIndex(dataset=mrpt.Dataset(Xd), n_trees=T, depth=depth, sparsity=a.sparsity,
+                       seed=4, fixed_count=False, matrices=a.matrices, splits=a.splits,
+                       leaf_offsets=a.leaf_offsets, leaf_indices=li,
+                       dataset_checksum=a.dataset_checksum)
+    assert not b.device_index().leaves_sorted
+    for v in (1, 3):
+        ra = mrpt.approximate_knn_batch(Q, 7, a, v)
+        rb = mrpt.approximate_knn_batch(Q, 7, b, v)
+        for x, y in zip(ra, rb):
+            assert np.array_equal(x, y)

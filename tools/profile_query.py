@@ -52,5 +52,12 @@ if not a.build_only:
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 5
+        ev = []
+        query_device(D, Qd, p["k"], v, timer=ev)
+        torch.cuda.synchronize()
+        st = {}
+        for name, x0, x1 in ev:
+            st[name] = st.get(name, 0.0) + x0.elapsed_time(x1)
         print(f"TIME config={a.config} v={v} nq={Qd.shape[0]} ms={ms:.3f} qps={Qd.shape[0] / ms * 1e3:.0f} "
-              f"variant={os.environ.get('MRPT_SCAN_VARIANT', '')}")
+              f"stages=" + ",".join(f"{k2}:{v2:.2f}" for k2, v2 in st.items()) +
+              f" variant={os.environ.get('MRPT_SCAN_VARIANT', '')}")
