@@ -130,6 +130,12 @@ def main():
         np.savez_compressed(os.path.join(HERE, f"small_{name}.npz"), **rec)
         print("wrote", name, file=sys.stderr)
 
+    # a reference-written index file (persistence.py:33-58), for byte-level checks
+    g = np.load(os.path.join(HERE, "small_gauss_400x24.npz"))
+    idx = mrpt.grow_trees(g["X"], n_trees=int(g["n_trees"]), depth=int(g["depth"]),
+                          seed=int(g["seed"]))
+    mrpt.save_index(idx, os.path.join(HERE, "index_gauss_400x24.mrpt"))
+
     # full BASELINE config 1 (regenerated from the pinned generator at test time)
     X, Q, p = workloads.generate(1)
     index = mrpt.grow_trees(X, p["n_trees"], p["depth"], p["sparsity"], seed=p["seed"])
