@@ -227,8 +227,11 @@ __global__ void k_build_dir(const int32_t *__restrict__ leaf_indices,
 
 // Directory-driven vote: per id tile, every tree's slice bounds come from the
 // directory, so a warp flattens the slices of its 32 trees and streams them
-// with consecutive lanes on consecutive ids (a 5-step shuffle search maps a
-// flat position to its tree).  No dependent cursor walks.
+// with consecutive lanes on consecutive ids.  A flat position is mapped to
+// its slice without searching: per 32-wide window one __reduce_or_sync
+// collects the slice starts inside the window, and the running count of
+// slice starts plus a popcount gives the slice's rank among the non-empty
+// slices, looked up in a 32-entry per-warp table.
 template <int CW>
 __global__ void __launch_bounds__(kVoteNT, 1) k_vote_dir(VoteArgs a) {
   extern __shared__ uint4 vote_smem[];
@@ -242,8 +245,10 @@ __global__ void __launch_bounds__(kVoteNT, 1) k_vote_dir(VoteArgs a) {
   constexpr int kWList = 2048;  // bitmap words that became non-zero in this tile
   __shared__ int32_t wlist[kWList];
   __shared__ int s_nw, s_nc;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = kVoteNT / 32;
+  __shared__ long long w_base[NW][32];  // per warp: global index of each non-empty slice (by rank)
+  __shared__ int w_pre[NW][32];         // per warp: flat start of each non-empty slice (by rank)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ngroups = (a.T + 31) >> 5;
   const int64_t dstride = a.ntiles + 1;
   const int64_t nwork = a.qlist ? (int64_t)*a.qcount : a.nq;
@@ -265,7 +270,7 @@ __global__ void __launch_bounds__(kVoteNT, 1) k_vote_dir(VoteArgs a) {
     int32_t *qcand = a.cand + q * a.cap;
     int64_t ncand = 0;
     // with few trees, several warps share one group of 32 trees, each taking
-    // every parts-th 32-wide stripe of the group's flattened slices
+    // every parts-th 32-wide window of the group's flattened slices
     const int parts = ngroups >= NW ? 1 : NW / ngroups;
     const int nvirt = ngroups * parts;
     for (int tile = 0; tile < a.ntiles; ++tile) {
@@ -274,14 +279,14 @@ __global__ void __launch_bounds__(kVoteNT, 1) k_vote_dir(VoteArgs a) {
         const int g = vw % ngroups, part = vw / ngroups;
         const int t = g * 32 + lane;
         int len = 0;
-        int64_t base = 0;
+        long long base = 0;
         if (t < a.T) {
           const uint16_t *d = a.dir + ((int64_t)t * a.L + sleaf[t]) * dstride + tile;
           const int s0 = d[0], s1 = d[1];
           len = s1 - s0;
-          base = (int64_t)t * a.n + sbase[t] + s0;
+          base = (long long)t * a.n + sbase[t] + s0;
         }
-        int pre = len;  // inclusive scan -> exclusive
+        int pre = len;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const int u = __shfl_up_sync(0xffffffffu, pre, o);
@@ -289,23 +294,35 @@ __global__ void __launch_bounds__(kVoteNT, 1) k_vote_dir(VoteArgs a) {
         }
         const int total = __shfl_sync(0xffffffffu, pre, 31);
         pre -= len;
-        constexpr int UNR = 4;  // independent id loads in flight per lane
+        // rank table of the non-empty slices
+        const unsigned ne = __ballot_sync(0xffffffffu, len > 0);
+        __syncwarp();
+        if (len > 0) {
+          const int r = __popc(ne & lanemask_lt());
+          w_base[warp][r] = base;
+          w_pre[warp][r] = pre;
+        }
+        __syncwarp();
+        constexpr int UNR = 4;
         const int stride = parts * 32;
         for (int e0 = part * 32; e0 < total; e0 += UNR * stride) {
           int32_t id[UNR];
 #pragma unroll
           for (int u = 0; u < UNR; ++u) {
-            const int e = e0 + u * stride + lane;
-            int k = 0;
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-              const int c = k + step;
-              const int pc = __shfl_sync(0xffffffffu, pre, c & 31);
-              if (c < 32 && pc <= e) k = c;
+            const int w0 = e0 + u * stride;
+            // slice starts inside [w0, w0+32) and before w0
+            const int rel = pre - w0;
+            const bool inwin = len > 0 && rel >= 0 && rel < 32;
+            const unsigned starts = __reduce_or_sync(0xffffffffu, inwin ? (1u << rel) : 0u);
+            const int before = __popc(__ballot_sync(0xffffffffu, len > 0 && rel < 0));
+            const int e = w0 + lane;
+            const int rank = before + __popc(starts & (0xffffffffu >> (31 - lane))) - 1;
+            id[u] = -1;
+            if (e < total) {
+              const long long bk = w_base[warp][rank];
+              const int pk = w_pre[warp][rank];
+              id[u] = __ldg(a.leaf_indices + bk + (e - pk));
             }
-            const int pk = __shfl_sync(0xffffffffu, pre, k);
-            const long long bk = __shfl_sync(0xffffffffu, (long long)base, k);
-            id[u] = e < total ? __ldg(a.leaf_indices + bk + (e - pk)) : -1;
           }
 #pragma unroll
           for (int u = 0; u < UNR; ++u) {
@@ -320,6 +337,7 @@ __global__ void __launch_bounds__(kVoteNT, 1) k_vote_dir(VoteArgs a) {
             }
           }
         }
+        __syncwarp();
       }
       __syncthreads();
       const int nw = s_nw;
@@ -482,7 +500,7 @@ __global__ void __launch_bounds__(1024) k_bitmap_compact(const uint32_t *__restr
 using namespace mrpt;
 
 static const int kVoteSmemSingle = 110 * 1024;  // single tile
-static const int kVoteSmemTiled = 200 * 1024;   // tiled sweep: one big CTA per SM
+static const int kVoteSmemTiled = 196 * 1024;   // tiled sweep: one big CTA per SM (+ static tables)
 
 // Tile geometry shared by mrpt_vote, mrpt_vote_plan and the directory.
 static int32_t vote_geometry(int64_t n, int32_t T, int64_t max_count, int *CWo, int64_t *Wo,
