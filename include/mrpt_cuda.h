@@ -161,6 +161,27 @@ int32_t mrpt_scan_topk(const float *X, int64_t n, int32_t d, int64_t ldx,
                        const int32_t *cand, int64_t cap, const int32_t *ncand,
                        int32_t k, int64_t *ids, double *dists, void *stream);
 
+/* fp16 shadow rows for the filter pass of mrpt_scan_topk_fp16: Xh (n, ldh)
+ * halves (ldh % 8 == 0, zero padded), radius[i] >= ||X_i - fp16(X_i)||_2.
+ * *bad (device int32) = 1 if some |x| exceeds the fp16 range. */
+int32_t mrpt_quantize_fp16(const float *X, int64_t n, int32_t d, int64_t ldx,
+                           void *Xh, int64_t ldh, float *radius, int32_t *bad,
+                           void *stream);
+
+/* mrpt_scan_topk with its float32 filter pass reading the fp16 shadow rows:
+ * per candidate the filter bounds the reference distance E within
+ * [(sqrt(D)-r)^2, (sqrt(D)+r)^2] (D the filter's value, r the row radius,
+ * plus float32 rounding terms) and keeps it while that lower bound is <= the
+ * running k-th smallest upper bound; survivors are reranked from X in float64
+ * exactly as mrpt_scan_topk, so results are identical.  Falls back to
+ * mrpt_scan_topk when Xh is NULL or the shape is unsupported. */
+int32_t mrpt_scan_topk_fp16(const float *X, int64_t n, int32_t d, int64_t ldx,
+                            const void *Xh, int64_t ldh, const float *radius,
+                            const float *Q, int64_t nq, int64_t ldq,
+                            const int32_t *cand, int64_t cap,
+                            const int32_t *ncand, int32_t k, int64_t *ids,
+                            double *dists, void *stream);
+
 /* Sorted de-duplication of arbitrary candidate ids (np.unique,
  * search.py:157) through an n-bit bitmap.  ids outside [0, n) set
  * *bad (device int32) to 1 (IntegrityError, search.py:158-162).

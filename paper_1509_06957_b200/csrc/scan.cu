@@ -13,6 +13,7 @@
 // running threshold; whenever it fills it is bitonic-sorted and truncated to
 // the k best, which tightens the threshold.  Ties on d^2 order by id, as
 // np.lexsort((S, d2)) does.
+#include <cuda_fp16.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -42,6 +43,9 @@ struct TopkArgs {
   bool vec4;
   const int32_t *qlist;  // optional: process only these queries (count *qcount)
   const int32_t *qcount;
+  const __half *Xh;      // optional fp16 shadow of X for the filter pass (row stride ldh)
+  int64_t ldh;
+  const float *radius;   // per row: upper bound of ||x - fp16(x)||_2
 };
 
 __device__ __forceinline__ bool pair_less(unsigned long long ak, int ai, unsigned long long bk,
@@ -644,6 +648,338 @@ __global__ void __launch_bounds__(kScanNT, MINB) k_scan_topk_filter(TopkArgs a, 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// fp16 shadow rows for the filter pass.  x~ = fp16(x) (round to nearest),
+// radius = ||x - x~||_2 rounded up.  For any query q the true distance then
+// lies within radius of ||x~ - q|| (triangle inequality), so the filter can
+// bound E from the fp16 row alone and the exact float64 rerank is unchanged.
+// Rows are padded to 8 halves (16-byte loads) with zeros.
+__global__ void k_quantize_fp16(const float *__restrict__ X, int64_t n, int d, int64_t ldx,
+                                __half *Xh, int64_t ldh, float *radius, int32_t *bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += wstride) {
+    const float *xr = X + i * ldx;
+    __half *hr = Xh + i * ldh;
+    double r2 = 0.0;
+    for (int c = lane; c < ldh; c += 32) {
+      float x = c < d ? xr[c] : 0.f;
+      if (fabsf(x) > 65504.f) *bad = 1;
+      const __half h = __float2half_rn(x);
+      hr[c] = h;
+      const double e = (double)x - (double)__half2float(h);
+      r2 = fma(e, e, r2);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+    if (lane == 0) radius[i] = __double2float_ru(__dsqrt_ru(r2 * (1.0 + 1e-12)));
+  }
+}
+
+// bounds of the reference distance E from the fp16-row filter value A and the
+// row radius r:  sqrt(E) in [sqrt(D) - r, sqrt(D) + r],  D = ||x~ - q||^2 with
+// |A - D| <= eps*D + eta (float32 arithmetic), E within 1e-12 relative of the
+// real value (float64 reference sum).
+__device__ __forceinline__ void dist_bounds(float A, float r, double eps, double eta, double &L,
+                                            double &U) {
+  const double a = (double)A;
+  const double dlo = fmax(0.0, (a - eta) / (1.0 + eps));
+  const double dhi = (a + eta) / (1.0 - eps);
+  const double slo = fmax(0.0, sqrt(dlo) - (double)r);
+  const double shi = sqrt(dhi) + (double)r;
+  L = slo * slo * (1.0 - 1e-12);
+  U = shi * shi * (1.0 + 1e-12);
+}
+
+// Filter on the fp16 shadow + exact rerank.  Per warp, a buffer of
+// (A, r, id).  At every shrink the buffer's bounds L_i <= E_i <= U_i are
+// evaluated in float64, U_k = k-th smallest U_i bounds the k-th smallest
+// reference distance, and entries with L_i > U_k are dropped.  Between
+// shrinks a candidate is admitted iff  A <= (1+eps)(sqrt(U_k) + r)^2 + eta,
+// evaluated with upward rounding -- a superset of L <= U_k -- so every exact
+// top-k member (ties included) survives to the float64 rerank.
+__device__ __forceinline__ bool admit(float A, float r, float su, float onepe) {
+  const float t = __fadd_ru(su, r);
+  const float rhs = __fadd_ru(__fmul_ru(__fmul_ru(t, t), onepe), 1.1754944e-38f);
+  return A <= rhs;
+}
+
+template <int BUFW>
+__device__ int shrink_bounds(float *ma, float *mr, int32_t *mi, int cnt, int kk, double eps,
+                             double eta, float *su_scr, int32_t *ix_scr, float *su_out) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < BUFW; i += 32) {
+    if (i < cnt) {
+      double L, U;
+      dist_bounds(ma[i], mr[i], eps, eta, L, U);
+      su_scr[i] = __double2float_ru(U);
+    } else {
+      su_scr[i] = __int_as_float(0x7f800000);
+    }
+    ix_scr[i] = i;
+  }
+  __syncwarp();
+  warp_sort(su_scr, ix_scr, BUFW);
+  const double uk = (double)su_scr[kk - 1];
+  int keep = 0;
+  for (int i0 = 0; i0 < cnt; i0 += 32) {
+    const int i = i0 + lane;
+    bool in = false;
+    float av = 0.f, rv = 0.f;
+    int32_t iv = 0;
+    if (i < cnt) {
+      av = ma[i];
+      rv = mr[i];
+      iv = mi[i];
+      double L, U;
+      dist_bounds(av, rv, eps, eta, L, U);
+      in = L <= uk;
+    }
+    const unsigned bm = __ballot_sync(0xffffffffu, in);
+    __syncwarp();
+    if (in) {
+      const int dst = keep + __popc(bm & lanemask_lt());
+      ma[dst] = av;
+      mr[dst] = rv;
+      mi[dst] = iv;
+    }
+    __syncwarp();
+    keep += __popc(bm);
+  }
+  *su_out = uk >= 3.0e38 ? __int_as_float(0x7f800000) : __double2float_ru(sqrt(uk));
+  return keep;
+}
+
+template <int BUFW>
+__global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_filter_h(TopkArgs a, double eps, double eta,
+                                                                  int32_t *fb_list, int32_t *fb_count) {
+  extern __shared__ unsigned long long topk_smem[];
+  constexpr int NWARP = kScanNT / 32;
+  constexpr int kFU = 4;
+  constexpr int kMaxJ = 4;  // ldh <= 256 * kMaxJ halves
+  float *qs = reinterpret_cast<float *>(topk_smem);                   // 256 * kMaxJ
+  float *wa = qs + 256 * kMaxJ;                                        // NWARP*BUFW filter values
+  float *wr = wa + NWARP * BUFW;                                       // NWARP*BUFW radii
+  int32_t *wid = reinterpret_cast<int32_t *>(wr + NWARP * BUFW);      // NWARP*BUFW
+  unsigned long long *ckey = reinterpret_cast<unsigned long long *>(wid + NWARP * BUFW);  // NWARP*BUFW
+  int32_t *cid = reinterpret_cast<int32_t *>(ckey + NWARP * BUFW);    // NWARP*BUFW
+  float *cu = reinterpret_cast<float *>(cid + NWARP * BUFW);          // NWARP*BUFW
+  float *cl = cu + NWARP * BUFW;                                       // NWARP*BUFW
+  __shared__ int s_wcnt[NWARP];
+  __shared__ int s_bad, s_ns;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float *ma = wa + warp * BUFW;
+  float *mr = wr + warp * BUFW;
+  int32_t *mi = wid + warp * BUFW;
+  const int d = a.d;
+  const int dpad = (int)a.ldh;
+  const int nj = (dpad + 255) >> 8;
+  const int kk = a.k;
+  const float onepe = __double2float_ru(1.0 + eps);
+  for (int64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
+    const float *qrow = a.Q + q * a.ldq;
+    for (int c = tid; c < 256 * kMaxJ; c += kScanNT) qs[c] = c < d ? qrow[c] : 0.f;
+    if (tid == 0) s_bad = 0;
+    __syncthreads();
+    int64_t m;
+    if (a.cand) {
+      const int64_t nc = a.ncand[q];
+      m = nc < a.cap ? nc : a.cap;
+    } else {
+      m = a.n;
+    }
+    const int32_t *qc = a.cand ? a.cand + q * a.cap : nullptr;
+    int cnt = 0;
+    float su = __int_as_float(0x7f800000);  // sqrt(U_k), +inf until the first shrink
+    bool bad = false;
+    for (int64_t g = (int64_t)warp * kFU; g < m; g += (int64_t)NWARP * kFU) {
+      int32_t cidv[kFU];
+      const __half *row[kFU];
+#pragma unroll
+      for (int u = 0; u < kFU; ++u) {
+        const int64_t j = g + u;
+        cidv[u] = j < m ? (qc ? __ldg(qc + j) : (int32_t)j) : -1;
+        row[u] = a.Xh + (int64_t)(cidv[u] < 0 ? 0 : cidv[u]) * a.ldh;
+      }
+      const float myr = (lane < kFU && cidv[lane < kFU ? lane : 0] >= 0)
+                            ? __ldg(a.radius + cidv[lane < kFU ? lane : 0]) : 0.f;
+      float acc[kFU];
+#pragma unroll
+      for (int u = 0; u < kFU; ++u) acc[u] = 0.f;
+#pragma unroll
+      for (int j = 0; j < kMaxJ; ++j) {
+        const int c = j * 256 + 8 * lane;
+        if (j < nj && c < dpad) {
+          const float4 q0 = *reinterpret_cast<const float4 *>(qs + c);
+          const float4 q1 = *reinterpret_cast<const float4 *>(qs + c + 4);
+          uint4 raw[kFU];
+#pragma unroll
+          for (int u = 0; u < kFU; ++u) raw[u] = __ldg(reinterpret_cast<const uint4 *>(row[u] + c));
+#pragma unroll
+          for (int u = 0; u < kFU; ++u) {
+            const __half2 *h2 = reinterpret_cast<const __half2 *>(&raw[u]);
+            float2 f;
+            float t;
+            f = __half22float2(h2[0]);
+            t = f.x - q0.x; acc[u] = __fmaf_rn(t, t, acc[u]);
+            t = f.y - q0.y; acc[u] = __fmaf_rn(t, t, acc[u]);
+            f = __half22float2(h2[1]);
+            t = f.x - q0.z; acc[u] = __fmaf_rn(t, t, acc[u]);
+            t = f.y - q0.w; acc[u] = __fmaf_rn(t, t, acc[u]);
+            f = __half22float2(h2[2]);
+            t = f.x - q1.x; acc[u] = __fmaf_rn(t, t, acc[u]);
+            t = f.y - q1.y; acc[u] = __fmaf_rn(t, t, acc[u]);
+            f = __half22float2(h2[3]);
+            t = f.x - q1.z; acc[u] = __fmaf_rn(t, t, acc[u]);
+            t = f.y - q1.w; acc[u] = __fmaf_rn(t, t, acc[u]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kFU; ++u) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+      }
+      float mine = acc[0];
+      int32_t myid = cidv[0];
+#pragma unroll
+      for (int u = 1; u < kFU; ++u)
+        if (lane == u) {
+          mine = acc[u];
+          myid = cidv[u];
+        }
+      const bool take = lane < kFU && myid >= 0 && admit(mine, myr, su, onepe);
+      const unsigned tm = __ballot_sync(0xffffffffu, take);
+      if (take) {
+        const int slot = cnt + __popc(tm & lanemask_lt());
+        ma[slot] = mine;
+        mr[slot] = myr;
+        mi[slot] = myid;
+      }
+      cnt += __popc(tm);
+      if (cnt > BUFW - kFU) {
+        __syncwarp();
+        cnt = shrink_bounds<BUFW>(ma, mr, mi, cnt, kk, eps, eta, cu + warp * BUFW,
+                                  cid + warp * BUFW, &su);
+        if (cnt > BUFW - kFU) {
+          bad = true;
+          cnt = 0;
+          break;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      s_wcnt[warp] = cnt;
+      if (bad) s_bad = 1;
+    }
+    __syncthreads();
+    if (s_bad) {
+      if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = (int32_t)q;
+      __syncthreads();
+      continue;
+    }
+    // merge every warp's buffer: bounds, global U_k, survivors L <= U_k
+    int off = 0, total = 0;
+    for (int w = 0; w < NWARP; ++w) {
+      off += w < warp ? s_wcnt[w] : 0;
+      total += s_wcnt[w];
+    }
+    for (int i = lane; i < cnt; i += 32) {
+      double L, U;
+      dist_bounds(ma[i], mr[i], eps, eta, L, U);
+      cu[off + i] = __double2float_ru(U);
+      cl[off + i] = __double2float_rd(L);
+      cid[off + i] = mi[i];
+    }
+    __syncthreads();
+    int np2 = 32;
+    while (np2 < total) np2 <<= 1;
+    float *su2 = wa;  // warp buffers are free now: sort scratch
+    int32_t *sx = wid;
+    for (int i = tid; i < np2; i += kScanNT) {
+      su2[i] = i < total ? cu[i] : __int_as_float(0x7f800000);
+      sx[i] = i;
+    }
+    __syncthreads();
+    for (int size = 2; size <= np2; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = tid; i < np2 / 2; i += kScanNT) {
+          const int lo = 2 * i - (i & (stride - 1));
+          const int hi = lo + stride;
+          const bool asc = (lo & size) == 0;
+          const float ka = su2[lo], kb = su2[hi];
+          const int ia = sx[lo], ib = sx[hi];
+          if (fpair_less(kb, ib, ka, ia) == asc) {
+            su2[lo] = kb;
+            su2[hi] = ka;
+            sx[lo] = ib;
+            sx[hi] = ia;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    const double uk = total >= kk ? (double)su2[kk - 1] : __longlong_as_double(0x7ff0000000000000LL);
+    if (tid == 0) s_ns = 0;
+    __syncthreads();
+    for (int i = tid; i < total; i += kScanNT) {
+      if ((double)cl[i] <= uk) sx[atomicAdd(&s_ns, 1)] = cid[i];
+    }
+    __syncthreads();
+    const int ns = s_ns;
+    int np3 = 1;
+    while (np3 < ns) np3 <<= 1;
+    for (int i = tid; i < np3; i += kScanNT) {
+      if (i < ns) {
+        const int32_t id = sx[i];
+        const float *xr = a.X + (int64_t)id * a.ldx;
+        double e = 0.0;
+        for (int c = 0; c < d; ++c) {
+          const double t = (double)__ldg(xr + c) - (double)__ldg(qrow + c);
+          e = __dadd_rn(e, __dmul_rn(t, t));
+        }
+        ckey[i] = (unsigned long long)__double_as_longlong(e);
+        cid[i] = id;
+      } else {
+        ckey[i] = ~0ull;
+        cid[i] = 0x7fffffff;
+      }
+    }
+    __syncthreads();
+    for (int size = 2; size <= np3; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = tid; i < np3 / 2; i += kScanNT) {
+          const int lo = 2 * i - (i & (stride - 1));
+          const int hi = lo + stride;
+          const bool asc = (lo & size) == 0;
+          const unsigned long long ka = ckey[lo], kb = ckey[hi];
+          const int ia = cid[lo], ib = cid[hi];
+          if (pair_less(kb, ib, ka, ia) == asc) {
+            ckey[lo] = kb;
+            ckey[hi] = ka;
+            cid[lo] = ib;
+            cid[hi] = ia;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    const int kept = ns < kk ? ns : kk;
+    for (int i = tid; i < kk; i += kScanNT) {
+      if (i < kept) {
+        a.ids[q * a.kstride + i] = cid[i];
+        a.dists[q * a.kstride + i] = sqrt(__longlong_as_double((long long)ckey[i]));
+      } else {
+        a.ids[q * a.kstride + i] = -1;
+        a.dists[q * a.kstride + i] = __longlong_as_double(0x7ff0000000000000LL);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(kScanNT)
 k_scan(const float *__restrict__ X, int64_t ldx, int d, const int64_t *__restrict__ cand, int64_t m,
        const float *__restrict__ q, double *out, bool vec4) {
@@ -813,4 +1149,85 @@ extern "C" int32_t mrpt_scan_topk(const float *X, int64_t n, int32_t d, int64_t 
     cudaFreeAsync(a.lb_id, s);
   }
   return launch_status("mrpt_scan_topk");
+}
+
+extern "C" int32_t mrpt_quantize_fp16(const float *X, int64_t n, int32_t d, int64_t ldx, void *Xh,
+                                      int64_t ldh, float *radius, int32_t *bad, void *stream) {
+  clear_error();
+  if (n < 1 || d < 1 || ldx < d || ldh < d || ldh % 8 != 0)
+    return fail(MRPT_ESHAPE, "mrpt_quantize_fp16: bad shape");
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(bad, 0, sizeof(int32_t), s);
+  const int64_t blocks = ceil_div<int64_t>(n, 8);
+  const int grid = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
+  k_quantize_fp16<<<grid, 256, 0, s>>>(X, n, d, ldx, reinterpret_cast<__half *>(Xh), ldh, radius, bad);
+  return launch_status("mrpt_quantize_fp16");
+}
+
+extern "C" int32_t mrpt_scan_topk_fp16(const float *X, int64_t n, int32_t d, int64_t ldx,
+                                       const void *Xh, int64_t ldh, const float *radius,
+                                       const float *Q, int64_t nq, int64_t ldq, const int32_t *cand,
+                                       int64_t cap, const int32_t *ncand, int32_t k, int64_t *ids,
+                                       double *dists, void *stream) {
+  clear_error();
+  if (!Xh || !radius || ldh % 8 != 0 || ldh < d || ldh > 1024 || k > 120 || k < 1 ||
+      (ldq % 4) != 0 || !aligned16(Q))
+    return mrpt_scan_topk(X, n, d, ldx, Q, nq, ldq, cand, cap, ncand, k, ids, dists, stream);
+  if (n < 1 || n >= (int64_t)1 << 31 || d < 1 || ldx < d || ldq < d || nq < 0)
+    return fail(MRPT_ESHAPE, "mrpt_scan_topk_fp16: bad shape");
+  if (cand && (cap < 1 || !ncand)) return fail(MRPT_EPARAM, "mrpt_scan_topk_fp16: bad candidate lists");
+  if (nq == 0) return MRPT_OK;
+  cudaStream_t s = as_stream(stream);
+  TopkArgs a;
+  a.X = X;
+  a.n = n;
+  a.d = d;
+  a.ldx = ldx;
+  a.Q = Q;
+  a.nq = nq;
+  a.ldq = ldq;
+  a.cand = cand;
+  a.cap = cap;
+  a.ncand = ncand;
+  a.k = k;
+  a.kstride = k;
+  a.ids = ids;
+  a.dists = dists;
+  a.lb_key = nullptr;
+  a.lb_id = nullptr;
+  a.vec4 = (d % 4 == 0) && (ldx % 4 == 0) && aligned16(X);
+  a.qlist = nullptr;
+  a.qcount = nullptr;
+  a.Xh = reinterpret_cast<const __half *>(Xh);
+  a.ldh = ldh;
+  a.radius = radius;
+  const int bufw = (2 * k + 16 <= 64) ? 64 : ((2 * k + 16 <= 128) ? 128 : 256);
+  const size_t smem = sizeof(float) * 256 * 4 + (size_t)(kScanNT / 32) * bufw * (4 + 4 + 4 + 8 + 4 + 4 + 4);
+  int32_t *fb = nullptr;
+  if (cudaMallocAsync((void **)&fb, sizeof(int32_t) * (nq + 1), s) != cudaSuccess)
+    return fail(MRPT_ECUDA, "mrpt_scan_topk_fp16: scratch allocation failed");
+  cudaMemsetAsync(fb, 0, sizeof(int32_t), s);
+  const double u = 5.9604644775390625e-08;  // 2^-24
+  const double eps = 2.0 * (ldh + 16) * u;
+  const double eta = 2.0 * (ldh + 16) * 1.401298464324817e-45;
+  topk_fn_f ffn = bufw == 64 ? k_scan_topk_filter_h<64>
+                             : (bufw == 128 ? k_scan_topk_filter_h<128> : k_scan_topk_filter_h<256>);
+  cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t grid = nq < (int64_t)num_sms() * 8 ? nq : (int64_t)num_sms() * 8;
+  ffn<<<(unsigned)grid, kScanNT, smem, s>>>(a, eps, eta, fb + 1, fb);
+  // fallback: exact tiled kernel over the listed queries
+  a.qlist = fb + 1;
+  a.qcount = fb;
+  if (a.vec4) {
+    const int buf = (k + kScanNT <= 1024) ? 1024 : 2048;
+    topk_fn tfn = buf == 1024 ? k_scan_topk_tiled<1024> : k_scan_topk_tiled<2048>;
+    const size_t tsmem = (size_t)buf * 12 + sizeof(float) * (kScanNT / 32) * 32 * kTileStride +
+                         sizeof(double) * (size_t)d;
+    cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+    tfn<<<(unsigned)(grid < 64 ? grid : 64), kScanNT, tsmem, s>>>(a);
+  } else {
+    return fail(MRPT_EPARAM, "mrpt_scan_topk_fp16: exact fallback needs 16-byte rows");
+  }
+  cudaFreeAsync(fb, s);
+  return launch_status("mrpt_scan_topk_fp16");
 }

@@ -41,12 +41,25 @@ struct VoteArgs {
 constexpr int kVoteNT = 1024;
 constexpr int kVoteU = 8;
 
+// Counter packing codes: 1 = 4 x 8-bit, 3 = 3 x 10-bit, 2 = 2 x 16-bit,
+// 4 = 1 x 32-bit lanes per 32-bit word.  A lane never carries into its
+// neighbour because the code is chosen from the largest possible count.
+template <int CW>
+__host__ __device__ __forceinline__ int counter_words(int W) {
+  return CW == 1 ? W / 4 : (CW == 2 ? W / 2 : (CW == 3 ? (W + 2) / 3 : W));
+}
+
 template <int CW>
 __device__ __forceinline__ uint32_t bump(uint32_t *cnt, int local) {
   if (CW == 1) {
     const int sh = (local & 3) << 3;
     const uint32_t old = atomicAdd(cnt + (local >> 2), 1u << sh);
     return ((old >> sh) & 0xffu) + 1u;
+  } else if (CW == 3) {
+    const int w = local / 3;
+    const int sh = (local - 3 * w) * 10;
+    const uint32_t old = atomicAdd(cnt + w, 1u << sh);
+    return ((old >> sh) & 0x3ffu) + 1u;
   } else if (CW == 2) {
     const int sh = (local & 1) << 4;
     const uint32_t old = atomicAdd(cnt + (local >> 1), 1u << sh);
@@ -106,7 +119,7 @@ template <int CW, int G, bool SORTED>
 __global__ void __launch_bounds__(kVoteNT, 1) k_vote(VoteArgs a) {
   extern __shared__ uint4 vote_smem[];
   uint32_t *cnt = reinterpret_cast<uint32_t *>(vote_smem);
-  const int cwords = a.W * CW / 4;  // W is a multiple of 64
+  const int cwords = (counter_words<CW>(a.W) + 3) & ~3;  // uint4-zeroable
   uint32_t *bits = cnt + cwords;    // W/32 words: "reached v" flags
   const int bwords = a.W / 32;
   int32_t *cur = reinterpret_cast<int32_t *>(bits + bwords);
@@ -236,7 +249,7 @@ template <int CW>
 __global__ void __launch_bounds__(kVoteNT, 1) k_vote_dir(VoteArgs a) {
   extern __shared__ uint4 vote_smem[];
   uint32_t *cnt = reinterpret_cast<uint32_t *>(vote_smem);
-  const int cwords = a.W * CW / 4;
+  const int cwords = (counter_words<CW>(a.W) + 3) & ~3;
   uint32_t *bits = cnt + cwords;
   const int bwords = a.W / 32;
   int32_t *sbase = reinterpret_cast<int32_t *>(bits + bwords);  // T: slice start of the leaf
@@ -409,6 +422,7 @@ template <bool SORTED>
 static vote_fn pick_cw(int CW, int G) {
   if (CW == 1) return pick_g<1, SORTED>(G);
   if (CW == 2) return pick_g<2, SORTED>(G);
+  if (CW == 3) return pick_g<3, SORTED>(G);
   return pick_g<4, SORTED>(G);
 }
 
@@ -503,19 +517,29 @@ static const int kVoteSmemSingle = 110 * 1024;  // single tile
 static const int kVoteSmemTiled = 196 * 1024;   // tiled sweep: one big CTA per SM (+ static tables)
 
 // Tile geometry shared by mrpt_vote, mrpt_vote_plan and the directory.
+// Smem per tile: the packed counters, a 1-bit "reached v" flag per id, and
+// 8 bytes per tree (cursors / slice bases).
+static size_t vote_smem_bytes(int CW, int64_t W, int32_t T) {
+  const int64_t words = CW == 1 ? W / 4 : (CW == 2 ? W / 2 : (CW == 3 ? (W + 2) / 3 : W));
+  return (size_t)((words + 3) & ~3LL) * 4 + (size_t)W / 8 + (size_t)8 * T;
+}
+
 static int32_t vote_geometry(int64_t n, int32_t T, int64_t max_count, int *CWo, int64_t *Wo,
                              int *ntiles_o) {
-  const int CW = max_count <= 255 ? 1 : (max_count <= 65535 ? 2 : 4);
-  const int64_t cursor_bytes = 8LL * T;
+  const int CW = max_count <= 255 ? 1 : (max_count <= 1023 ? 3 : (max_count <= 65535 ? 2 : 4));
+  const int64_t single = ceil_div<int64_t>(n, 192) * 192;
   int64_t W;
-  int64_t budget = kVoteSmemSingle - cursor_bytes - 64;
-  // per id of a tile: CW counter bytes + 1/8 byte of "reached v" bitmap
-  if ((int64_t)ceil_div<int64_t>(n, 64) * (64 * CW + 8) <= budget) {
-    W = ceil_div<int64_t>(n, 64) * 64;
+  if (vote_smem_bytes(CW, single, T) <= (size_t)kVoteSmemSingle) {
+    W = single;
   } else {
-    budget = kVoteSmemTiled - cursor_bytes - 64;
-    if (budget < 64 * CW + 8) return fail(MRPT_EPARAM, "mrpt_vote: too many trees for shared cursors");
-    W = budget / (64 * CW + 8) * 64;
+    // largest multiple of 192 ids (bitmap words x 10-bit triples) in budget
+    int64_t lo = 0, hi = single / 192;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) / 2;
+      if (vote_smem_bytes(CW, mid * 192, T) <= (size_t)kVoteSmemTiled) lo = mid; else hi = mid - 1;
+    }
+    if (lo == 0) return fail(MRPT_EPARAM, "mrpt_vote: too many trees for shared cursors");
+    W = lo * 192;
   }
   *CWo = CW;
   *Wo = W;
@@ -569,7 +593,6 @@ extern "C" int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_of
   int64_t W;
   int32_t st = vote_geometry(n, T, max_count, &CW, &W, &ntiles);
   if (st) return st;
-  const int64_t cursor_bytes = 8LL * T;
   const bool sorted = leaves_sorted != 0 || ntiles == 1;
   // lanes per tree slice for the cursor sweep (pow2 in [1, 32])
   const double mean_leaf = (double)n / (double)((int64_t)1 << depth);
@@ -594,10 +617,11 @@ extern "C" int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_of
   a.qlist = nullptr;
   a.qcount = nullptr;
   a.dir = dir;
-  const size_t smem = (size_t)W * CW + (size_t)W / 8 + (size_t)cursor_bytes;
+  const size_t smem = vote_smem_bytes(CW, W, T);
   const int64_t grid = nq < (int64_t)num_sms() * 4 ? nq : (int64_t)num_sms() * 4;
   if (dir && ntiles > 1 && sorted) {
-    vote_fn fn = CW == 1 ? k_vote_dir<1> : (CW == 2 ? k_vote_dir<2> : k_vote_dir<4>);
+    vote_fn fn = CW == 1 ? k_vote_dir<1>
+                         : (CW == 2 ? k_vote_dir<2> : (CW == 3 ? k_vote_dir<3> : k_vote_dir<4>));
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     fn<<<(unsigned)grid, kVoteNT, smem, s>>>(a);
   } else {

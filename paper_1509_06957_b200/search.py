@@ -239,6 +239,7 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
         per_q = 4 * (D.T + cap)
         chunk = max(1, min(nq, (1 << 30) // per_q))
     vdir = D.vote_dir()
+    shadow = D.shadow() if k <= 120 else None
     leaves = torch.empty((min(chunk, nq), D.T), dtype=torch.int32, device=dev)
     cand = torch.empty((min(chunk, nq), cap), dtype=torch.int32, device=dev)
     stream = _native.stream_ptr()
@@ -253,10 +254,17 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
               D.n, D.T, D.depth, _native.ptr(leaves), e - s, int(votes), int(D.leaves_sorted),
               int(D.max_count), _native.ptr(vdir), _native.ptr(cand), int(cap),
               _native.ptr(counts[s:e]), stream)
-        stage("scan_topk", _native.call, "mrpt_scan_topk", _native.ptr(D.X), D.n, D.d,
-              int(D.X.stride(0)), _native.ptr(qb), e - s, int(Qd.stride(0)), _native.ptr(cand),
-              int(cap), _native.ptr(counts[s:e]), int(k), _native.ptr(ids[s:e]),
-              _native.ptr(dists[s:e]), stream)
+        if shadow is not None:
+            stage("scan_topk", _native.call, "mrpt_scan_topk_fp16", _native.ptr(D.X), D.n, D.d,
+                  int(D.X.stride(0)), _native.ptr(shadow[0]), shadow[1], _native.ptr(shadow[2]),
+                  _native.ptr(qb), e - s, int(Qd.stride(0)), _native.ptr(cand), int(cap),
+                  _native.ptr(counts[s:e]), int(k), _native.ptr(ids[s:e]),
+                  _native.ptr(dists[s:e]), stream)
+        else:
+            stage("scan_topk", _native.call, "mrpt_scan_topk", _native.ptr(D.X), D.n, D.d,
+                  int(D.X.stride(0)), _native.ptr(qb), e - s, int(Qd.stride(0)),
+                  _native.ptr(cand), int(cap), _native.ptr(counts[s:e]), int(k),
+                  _native.ptr(ids[s:e]), _native.ptr(dists[s:e]), stream)
     return ids, dists, counts
 
 

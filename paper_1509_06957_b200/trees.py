@@ -158,6 +158,29 @@ class _DeviceIndex:
         """Upper bound on any candidate set at this vote threshold."""
         return max(1, min(self.n, (self.T * self.max_leaf) // votes))
 
+    def shadow(self):
+        """(fp16 rows, row stride, radius) for the scan filter, built once; None
+        when not worth it, or the rows do not fit the kernel or the fp16 range."""
+        if getattr(self, "_shadow", False) is not False:
+            return self._shadow
+        self._shadow = None
+        ldh = (self.d + 7) // 8 * 8
+        # worth it when the candidate rows stream from HBM (X well beyond L2)
+        # and a row fills whole warps; MRPT_FP16_FILTER=1/0 forces it on/off
+        mode = os.environ.get("MRPT_FP16_FILTER", "auto")
+        want = (mode == "1") or (mode == "auto" and self.d >= 256 and self.n * self.d * 4 > (256 << 20))
+        if want and ldh <= 1024 and self.d % 4 == 0:
+            torch = _device.torch_mod()
+            Xh = torch.empty((self.n, ldh), dtype=torch.float16, device=self.X.device)
+            rad = torch.empty(self.n, dtype=torch.float32, device=self.X.device)
+            bad = torch.zeros(1, dtype=torch.int32, device=self.X.device)
+            _native.call("mrpt_quantize_fp16", _native.ptr(self.X), self.n, self.d,
+                         int(self.X.stride(0)), _native.ptr(Xh), ldh, _native.ptr(rad),
+                         _native.ptr(bad), _native.stream_ptr())
+            if not int(bad.item()):
+                self._shadow = (Xh, ldh, rad)
+        return self._shadow
+
     def vote_dir(self):
         """Tile directory for the multi-tile vote (built once, on the device),
         or None when one id tile covers the index or it cannot be used."""
