@@ -63,6 +63,16 @@ def concat_csc(matrices):
     return col_ptr, row_idx, values
 
 
-def csc_device(matrices):
+def csc_device(matrices, pinned=False):
+    """Device copies of the concatenated CSC arrays.  ``pinned`` stages them in
+    page-locked memory and copies asynchronously, so the host can go on
+    sampling the next batch while the stream is still busy."""
     cp, r, v = concat_csc(matrices)
-    return h2d(cp), h2d(r), h2d(v)
+    if not pinned:
+        return h2d(cp), h2d(r), h2d(v)
+    torch = torch_mod()
+    out = []
+    for a in (cp, r, v):
+        t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        out.append(t.to(device(), non_blocking=True))
+    return tuple(out)

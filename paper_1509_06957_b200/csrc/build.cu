@@ -311,11 +311,26 @@ __global__ void __launch_bounds__(kNT) k_big_keys(LevelArgs a) {
     const int32_t *oin = a.order_in + (int64_t)t * a.n;
     uint32_t *kb = a.keys + (int64_t)t * a.n;
     uint32_t mn = 0xffffffffu, mx = 0u;
-    for (int64_t p = p0 + threadIdx.x; p < p1; p += kNT) {
-      const uint32_t k = f2key(__ldg(Pc + oin[p]));
-      kb[p] = k;
-      mn = k < mn ? k : mn;
-      mx = k > mx ? k : mx;
+    constexpr int U = 8;  // independent gathers in flight per thread
+    for (int64_t r0 = p0 + threadIdx.x; r0 < p1; r0 += (int64_t)U * kNT) {
+      int32_t id[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int64_t p = r0 + (int64_t)j * kNT;
+        id[j] = p < p1 ? __ldg(oin + p) : -1;
+      }
+      float v[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) v[j] = id[j] >= 0 ? __ldg(Pc + id[j]) : 0.f;
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        if (id[j] >= 0) {
+          const uint32_t k = f2key(v[j]);
+          kb[r0 + (int64_t)j * kNT] = k;
+          mn = k < mn ? k : mn;
+          mx = k > mx ? k : mx;
+        }
+      }
     }
     block_minmax(mn, mx, red_mn, red_mx);
     if (threadIdx.x == 0) {
@@ -360,9 +375,19 @@ __global__ void __launch_bounds__(kNT) k_big_hist(LevelArgs a) {
     const uint32_t *kb = a.keys + (int64_t)g->t * a.n;
     hist[threadIdx.x] = 0u;
     __syncthreads();
-    for (int64_t p = p0 + threadIdx.x; p < p1; p += kNT) {
-      const uint32_t k = kb[p];
-      if (prefix_match(k, prefix, nb)) atomicAdd(&hist[(k >> shift) & dmask], 1u);
+    constexpr int U = 8;
+    for (int64_t r0 = p0 + threadIdx.x; r0 < p1; r0 += (int64_t)U * kNT) {
+      uint32_t kk[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int64_t p = r0 + (int64_t)j * kNT;
+        kk[j] = p < p1 ? __ldg(kb + p) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int64_t p = r0 + (int64_t)j * kNT;
+        if (p < p1 && prefix_match(kk[j], prefix, nb)) atomicAdd(&hist[(kk[j] >> shift) & dmask], 1u);
+      }
     }
     __syncthreads();
     const uint32_t v = hist[threadIdx.x];
@@ -412,7 +437,20 @@ __global__ void __launch_bounds__(kNT) k_big_count(LevelArgs a) {
     const int64_t p1 = (p0 + kChunk) < g->e ? (p0 + kChunk) : g->e;
     const uint32_t *kb = a.keys + (int64_t)g->t * a.n;
     int cnt = 0;
-    for (int64_t p = p0 + threadIdx.x; p < p1; p += kNT) cnt += kb[p] <= K ? 1 : 0;
+    constexpr int U = 8;
+    for (int64_t r0 = p0 + threadIdx.x; r0 < p1; r0 += (int64_t)U * kNT) {
+      uint32_t kk[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int64_t p = r0 + (int64_t)j * kNT;
+        kk[j] = p < p1 ? __ldg(kb + p) : 0xffffffffu;
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int64_t p = r0 + (int64_t)j * kNT;
+        cnt += (p < p1 && kk[j] <= K) ? 1 : 0;
+      }
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cnt;
@@ -454,7 +492,9 @@ __global__ void k_big_scan(LevelArgs a) {
 }
 
 __global__ void __launch_bounds__(kNT) k_big_scatter(LevelArgs a) {
-  __shared__ int wcnt[kNT / 32];
+  constexpr int SR = 4;  // sub-rounds of kNT elements per barrier pair
+  constexpr int NW = kNT / 32;
+  __shared__ int wcnt[SR][NW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nch = a.ctl->nchunks;
   for (int64_t c = blockIdx.x; c < nch; c += gridDim.x) {
@@ -469,22 +509,47 @@ __global__ void __launch_bounds__(kNT) k_big_scatter(LevelArgs a) {
     const int32_t *oin = a.order_in + (int64_t)g->t * a.n;
     int32_t *oout = a.order_out + (int64_t)g->t * a.n;
     int64_t base_left = a.chunk_off[c];
-    for (int64_t r0 = p0; r0 < p1; r0 += kNT) {
-      const int64_t p = r0 + threadIdx.x;
-      const bool valid = p < p1;
-      const bool f = valid && kb[p] <= K;
-      const unsigned bal = __ballot_sync(0xffffffffu, f);
-      if (lane == 0) wcnt[warp] = __popc(bal);
-      __syncthreads();
-      int before = 0, tot = 0;
+    for (int64_t r0 = p0; r0 < p1; r0 += (int64_t)SR * kNT) {
+      uint32_t kk[SR];
+      int32_t id[SR];
+      bool f[SR];
+      unsigned bal[SR];
 #pragma unroll
-      for (int w2 = 0; w2 < kNT / 32; ++w2) {
-        const int cc = wcnt[w2];
-        before += w2 < warp ? cc : 0;
-        tot += cc;
+      for (int j = 0; j < SR; ++j) {
+        const int64_t p = r0 + (int64_t)j * kNT + threadIdx.x;
+        const bool valid = p < p1;
+        kk[j] = valid ? __ldg(kb + p) : 0xffffffffu;
+        id[j] = valid ? __ldg(oin + p) : 0;
       }
-      const int64_t lrank = base_left + before + __popc(bal & lanemask_lt());
-      if (valid) oout[f ? b + lrank : b + nle + ((p - b) - lrank)] = oin[p];
+#pragma unroll
+      for (int j = 0; j < SR; ++j) {
+        const int64_t p = r0 + (int64_t)j * kNT + threadIdx.x;
+        f[j] = p < p1 && kk[j] <= K;
+        bal[j] = __ballot_sync(0xffffffffu, f[j]);
+        if (lane == 0) wcnt[j][warp] = __popc(bal[j]);
+      }
+      __syncthreads();
+      int tot = 0;
+      int before[SR];
+#pragma unroll
+      for (int j = 0; j < SR; ++j) {
+        int bj = tot;
+#pragma unroll
+        for (int w2 = 0; w2 < NW; ++w2) {
+          const int cc = wcnt[j][w2];
+          bj += w2 < warp ? cc : 0;
+          tot += cc;
+        }
+        before[j] = bj;
+      }
+#pragma unroll
+      for (int j = 0; j < SR; ++j) {
+        const int64_t p = r0 + (int64_t)j * kNT + threadIdx.x;
+        if (p < p1) {
+          const int64_t lrank = base_left + before[j] + __popc(bal[j] & lanemask_lt());
+          oout[f[j] ? b + lrank : b + nle + ((p - b) - lrank)] = id[j];
+        }
+      }
       base_left += tot;
       __syncthreads();
     }

@@ -180,7 +180,11 @@ extern "C" int32_t mrpt_project(const float *X, int64_t m, int32_t d, int64_t ld
   if (tp >= 64) {
     const size_t smem = (size_t)tp * row_bytes;
     const int64_t tiles = ceil_div<int64_t>(m, tp);
-    const int grid = (int)(tiles < (int64_t)num_sms() * 2 ? tiles : (int64_t)num_sms() * 2);
+    // as many resident CTAs as shared memory allows (latency hiding)
+    int per_sm = (int)((220 * 1024) / (smem + 1024));
+    per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
+    const int64_t cap = (int64_t)num_sms() * per_sm;
+    const int grid = (int)(tiles < cap ? tiles : cap);
     cudaFuncSetAttribute(k_project_smem<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_project_smem<2><<<grid, 256, smem, s>>>(X, m, d, ldx, col_ptr, rows, vals, ncols, out,
                                                out_row_stride, out_col_stride, tp, stride);

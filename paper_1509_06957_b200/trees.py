@@ -390,7 +390,7 @@ def _grow_block(X, t_begin, t_end, depth, sparsity, seed, fixed_count, splits, o
         matrices.extend(mats)
         for R in mats:
             _record_macs(n * R.nnz)
-        cp, rows, vals = _device.csc_device(mats)
+        cp, rows, vals = _device.csc_device(mats, pinned=True)
         # K1: P[(t*depth + lev)*n + i] (row stride 1, column stride n)
         _native.call("mrpt_project", _native.ptr(Xd), n, d, d, _native.ptr(cp), _native.ptr(rows),
                      _native.ptr(vals), (b1 - b0) * depth, _native.ptr(P), 1, n, stream)
@@ -407,7 +407,7 @@ def _finish_index(X, n_trees, depth, sparsity, seed, fixed_count, matrices, spli
     Xd = X.device()
     sizes = offsets[:, 1:] - offsets[:, :-1]
     max_leaf = int(sizes.max().item())
-    cp, rows, vals = _device.csc_device(matrices)
+    cp, rows, vals = _device.csc_device(matrices, pinned=True)
     dindex = _DeviceIndex(Xd, n_trees, depth, splits, offsets, indices, cp, rows, vals,
                           leaves_sorted=True, max_count=n_trees, max_leaf=max_leaf)
     return MRPTIndex(dataset=X, n_trees=n_trees, depth=depth, sparsity=float(sparsity), seed=seed,
