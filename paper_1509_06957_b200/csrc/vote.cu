@@ -72,11 +72,12 @@ __device__ __forceinline__ uint32_t bump(uint32_t *cnt, int local) {
 // Append, in id order, the ids whose bit is set in bits[0..nwords) (tile
 // origin lo) to out[base..]; returns the new base (block-uniform).  Clears
 // the bitmap as it goes.
+template <int NT = kVoteNT>
 __device__ __forceinline__ int64_t emit_bitmap(uint32_t *bits, int nwords, int32_t lo, int32_t *out,
                                                int64_t base, int64_t cap, int *wsum) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int NW = kVoteNT / 32;
-  for (int r0 = 0; r0 < nwords; r0 += kVoteNT) {
+  constexpr int NW = NT / 32;
+  for (int r0 = 0; r0 < nwords; r0 += NT) {
     const int i = r0 + threadIdx.x;
     uint32_t word = i < nwords ? bits[i] : 0u;
     if (i < nwords && word) bits[i] = 0u;
@@ -245,8 +246,8 @@ __global__ void k_build_dir(const int32_t *__restrict__ leaf_indices,
 // collects the slice starts inside the window, and the running count of
 // slice starts plus a popcount gives the slice's rank among the non-empty
 // slices, looked up in a 32-entry per-warp table.
-template <int CW>
-__global__ void __launch_bounds__(kVoteNT, 1) k_vote_dir(VoteArgs a) {
+template <int CW, int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_vote_dir(VoteArgs a) {
   extern __shared__ uint4 vote_smem[];
   uint32_t *cnt = reinterpret_cast<uint32_t *>(vote_smem);
   const int cwords = (counter_words<CW>(a.W) + 3) & ~3;
@@ -254,11 +255,11 @@ __global__ void __launch_bounds__(kVoteNT, 1) k_vote_dir(VoteArgs a) {
   const int bwords = a.W / 32;
   int32_t *sbase = reinterpret_cast<int32_t *>(bits + bwords);  // T: slice start of the leaf
   int32_t *sleaf = sbase + a.T;                                   // T: leaf id
-  __shared__ int wsum[kVoteNT / 32 + 1];
+  __shared__ int wsum[NT / 32 + 1];
   constexpr int kWList = 2048;  // bitmap words that became non-zero in this tile
   __shared__ int32_t wlist[kWList];
   __shared__ int s_nw, s_nc;
-  constexpr int NW = kVoteNT / 32;
+  constexpr int NW = NT / 32;
   __shared__ long long w_base[NW][32];  // per warp: global index of each non-empty slice (by rank)
   __shared__ int w_pre[NW][32];         // per warp: flat start of each non-empty slice (by rank)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -267,14 +268,14 @@ __global__ void __launch_bounds__(kVoteNT, 1) k_vote_dir(VoteArgs a) {
   const int64_t nwork = a.qlist ? (int64_t)*a.qcount : a.nq;
   for (int64_t wq = blockIdx.x; wq < nwork; wq += gridDim.x) {
     const int64_t q = a.qlist ? (int64_t)a.qlist[wq] : wq;
-    for (int t = tid; t < a.T; t += kVoteNT) {
+    for (int t = tid; t < a.T; t += NT) {
       const int leaf = a.leaves[q * a.T + t];
       sleaf[t] = leaf;
       sbase[t] = (int32_t)a.leaf_offsets[(int64_t)t * (a.L + 1) + leaf];
     }
     uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
-    for (int i = tid; i < cwords / 4; i += kVoteNT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
-    for (int i = tid; i < bwords; i += kVoteNT) bits[i] = 0u;
+    for (int i = tid; i < cwords / 4; i += NT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = tid; i < bwords; i += NT) bits[i] = 0u;
     if (tid == 0) {
       s_nw = 0;
       s_nc = 0;
@@ -356,10 +357,10 @@ __global__ void __launch_bounds__(kVoteNT, 1) k_vote_dir(VoteArgs a) {
       const int nw = s_nw;
       if (nw > kWList) {  // too many words to list: ordered scan of the whole bitmap
         const int64_t hi = (int64_t)lo + a.W < a.n ? (int64_t)lo + a.W : a.n;
-        ncand = emit_bitmap(bits, (int)((hi - lo + 31) >> 5), lo, qcand, ncand, a.cap, wsum);
+        ncand = emit_bitmap<NT>(bits, (int)((hi - lo + 31) >> 5), lo, qcand, ncand, a.cap, wsum);
       } else {
         // listed words only (ids within the tile unordered; tiles ascending)
-        for (int i0 = 0; i0 < nw; i0 += kVoteNT) {
+        for (int i0 = 0; i0 < nw; i0 += NT) {
           const int i = i0 + tid;
           uint32_t word = 0u;
           int wi = 0;
@@ -395,7 +396,7 @@ __global__ void __launch_bounds__(kVoteNT, 1) k_vote_dir(VoteArgs a) {
         s_nc = 0;
       }
       if (tile + 1 < a.ntiles) {
-        for (int i = tid; i < cwords / 4; i += kVoteNT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+        for (int i = tid; i < cwords / 4; i += NT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
       }
     }
@@ -524,8 +525,14 @@ static size_t vote_smem_bytes(int CW, int64_t W, int32_t T) {
   return (size_t)((words + 3) & ~3LL) * 4 + (size_t)W / 8 + (size_t)8 * T;
 }
 
+static int vote_dir_threads() {
+  const char *e = getenv("MRPT_VOTE_NT");  // experiments: 512 = two CTAs per SM
+  return (e && atoi(e) == 512) ? 512 : 1024;
+}
+
 static int32_t vote_geometry(int64_t n, int32_t T, int64_t max_count, int *CWo, int64_t *Wo,
                              int *ntiles_o) {
+  const size_t tiled_budget = vote_dir_threads() == 512 ? 96 * 1024 : kVoteSmemTiled;
   const int CW = max_count <= 255 ? 1 : (max_count <= 1023 ? 3 : (max_count <= 65535 ? 2 : 4));
   const int64_t single = ceil_div<int64_t>(n, 192) * 192;
   int64_t W;
@@ -536,7 +543,7 @@ static int32_t vote_geometry(int64_t n, int32_t T, int64_t max_count, int *CWo, 
     int64_t lo = 0, hi = single / 192;
     while (lo < hi) {
       const int64_t mid = (lo + hi + 1) / 2;
-      if (vote_smem_bytes(CW, mid * 192, T) <= (size_t)kVoteSmemTiled) lo = mid; else hi = mid - 1;
+      if (vote_smem_bytes(CW, mid * 192, T) <= tiled_budget) lo = mid; else hi = mid - 1;
     }
     if (lo == 0) return fail(MRPT_EPARAM, "mrpt_vote: too many trees for shared cursors");
     W = lo * 192;
@@ -620,10 +627,17 @@ extern "C" int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_of
   const size_t smem = vote_smem_bytes(CW, W, T);
   const int64_t grid = nq < (int64_t)num_sms() * 4 ? nq : (int64_t)num_sms() * 4;
   if (dir && ntiles > 1 && sorted) {
-    vote_fn fn = CW == 1 ? k_vote_dir<1>
-                         : (CW == 2 ? k_vote_dir<2> : (CW == 3 ? k_vote_dir<3> : k_vote_dir<4>));
+    const int nt = vote_dir_threads();
+    vote_fn fn;
+    if (nt == 512)
+      fn = CW == 1 ? k_vote_dir<1, 512>
+                   : (CW == 2 ? k_vote_dir<2, 512> : (CW == 3 ? k_vote_dir<3, 512> : k_vote_dir<4, 512>));
+    else
+      fn = CW == 1 ? k_vote_dir<1, 1024>
+                   : (CW == 2 ? k_vote_dir<2, 1024> : (CW == 3 ? k_vote_dir<3, 1024> : k_vote_dir<4, 1024>));
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    fn<<<(unsigned)grid, kVoteNT, smem, s>>>(a);
+    const int64_t g2 = nt == 512 ? (nq < (int64_t)num_sms() * 8 ? nq : (int64_t)num_sms() * 8) : grid;
+    fn<<<(unsigned)g2, nt, smem, s>>>(a);
   } else {
     vote_fn fn = sorted ? pick_cw<true>(CW, G) : pick_cw<false>(CW, G);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
