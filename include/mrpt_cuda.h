@@ -182,6 +182,30 @@ int32_t mrpt_scan_topk_fp16(const float *X, int64_t n, int32_t d, int64_t ldx,
                             const int32_t *ncand, int32_t k, int64_t *ids,
                             double *dists, void *stream);
 
+/* u8 shadow rows for non-negative data: Xq (n, ldq) bytes (ldq % 16 == 0,
+ * <= 1024), X_i = rint(x_i / scale[i]) (scale = 1 when the whole dataset is
+ * integer-valued in [0, 255], which makes the shadow exact), norm[i] =
+ * sum X_i^2, radius[i] >= ||x_i - scale[i] X_i||_2.  flags (device, 2 int32):
+ * [0] = 1 if some x < 0 (nothing written), [1] = 1 if not integer-valued.
+ * Synchronises the stream once (index preparation, not the query path). */
+int32_t mrpt_quantize_u8(const float *X, int64_t n, int32_t d, int64_t ldx,
+                         void *Xq, int64_t ldq, float *scale, int32_t *norm,
+                         float *radius, int32_t *flags, void *stream);
+
+/* mrpt_scan_topk whose filter pass scores candidates on the u8 shadow with
+ * exact integer dot products (dp4a): D = s_x^2 N_x + s_q^2 N_q - 2 s_x s_q X.Q
+ * in float64, sqrt(E) within r_x + r_q of sqrt(D); kept while the lower bound
+ * is <= the running k-th smallest upper bound, then the same float64 rerank
+ * from X -- identical results.  Falls back to mrpt_scan_topk for unsupported
+ * shapes. */
+int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64_t ldx,
+                          const void *Xq, int64_t ldq, const float *scale,
+                          const int32_t *norm, const float *radius,
+                          const float *Q, int64_t nq, int64_t ldqq,
+                          const int32_t *cand, int64_t cap,
+                          const int32_t *ncand, int32_t k, int64_t *ids,
+                          double *dists, void *stream);
+
 /* Sorted de-duplication of arbitrary candidate ids (np.unique,
  * search.py:157) through an n-bit bitmap.  ids outside [0, n) set
  * *bad (device int32) to 1 (IntegrityError, search.py:158-162).

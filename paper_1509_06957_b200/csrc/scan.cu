@@ -980,6 +980,449 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_filter_h(TopkArgs a, d
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// u8 shadow rows (non-negative data): X_i = rint(x_i / s) in [0, 255] with a
+// per-row scale s (s = 1 when the whole dataset is integer-valued in
+// [0, 255], which makes the shadow exact), radius r >= ||x - s X||_2 and
+// N = sum X_i^2.  The filter then scores a candidate with exact integer dot
+// products (dp4a, int32 accumulate -- no rounding at all):
+//   D = s_x^2 N_x + s_q^2 N_q - 2 s_x s_q (X . Q)   (float64, |error| <= eta)
+// and sqrt(E) lies within r_x + r_q of sqrt(D) for the reference's E.
+__global__ void k_q8_flags(const float *__restrict__ X, int64_t n, int d, int64_t ldx, int32_t *flags) {
+  // flags[0]: some x < 0; flags[1]: some x not an integer in [0, 255]
+  bool neg = false, nonint = false;
+  const int64_t total = n * d;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = g / d, c = g - i * d;
+    const float x = X[i * ldx + c];
+    neg |= x < 0.f;
+    nonint |= !(x >= 0.f && x <= 255.f && rintf(x) == x);
+  }
+  if (__any_sync(0xffffffffu, neg) && (threadIdx.x & 31) == 0) flags[0] = 1;
+  if (__any_sync(0xffffffffu, nonint) && (threadIdx.x & 31) == 0) flags[1] = 1;
+}
+
+__global__ void k_quantize_u8(const float *__restrict__ X, int64_t n, int d, int64_t ldx,
+                              uint8_t *Xq, int64_t ldq, float *scale, int32_t *norm, float *radius,
+                              int integer_mode) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += wstride) {
+    const float *xr = X + i * ldx;
+    float mx = 0.f;
+    for (int c = lane; c < d; c += 32) mx = fmaxf(mx, xr[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float sc = integer_mode ? 1.f : (mx > 0.f ? mx / 255.f : 1.f);
+    double r2 = 0.0;
+    int nn = 0;
+    for (int c = lane; c < ldq; c += 32) {
+      const float x = c < d ? xr[c] : 0.f;
+      float qv = rintf(x / sc);
+      qv = fminf(fmaxf(qv, 0.f), 255.f);
+      const int qi = (int)qv;
+      Xq[i * ldq + c] = (uint8_t)qi;
+      const double e = (double)x - (double)sc * (double)qi;
+      r2 = fma(e, e, r2);
+      nn += qi * qi;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+      nn += __shfl_xor_sync(0xffffffffu, nn, o);
+    }
+    if (lane == 0) {
+      scale[i] = sc;
+      norm[i] = nn;
+      radius[i] = r2 == 0.0 ? 0.f : __double2float_ru(__dsqrt_ru(r2 * (1.0 + 1e-12)));
+    }
+  }
+}
+
+__device__ __forceinline__ void dist_bounds2(float A, float r, float eta, double &L, double &U) {
+  const double a = (double)A, e = (double)eta;
+  const double slo = fmax(0.0, sqrt(fmax(0.0, a - e)) - (double)r);
+  const double shi = sqrt(a + e) + (double)r;
+  L = slo * slo * (1.0 - 1e-12);
+  U = shi * shi * (1.0 + 1e-12);
+}
+
+// admitted iff A <= (sqrt(U_k) + r)^2 + eta, upward rounding: a superset of
+// "lower bound <= U_k"
+__device__ __forceinline__ bool admit2(float A, float r, float eta, float su) {
+  const float t = __fadd_ru(su, r);
+  const float rhs = __fadd_ru(__fmul_ru(t, t), __fadd_ru(eta, 1.1754944e-38f));
+  return A <= rhs;
+}
+
+template <int BUFW>
+__device__ int shrink_bounds2(float *ma, float *mr, float *me, int32_t *mi, int cnt, int kk,
+                              float *su_scr, int32_t *ix_scr, float *su_out) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < BUFW; i += 32) {
+    if (i < cnt) {
+      double L, U;
+      dist_bounds2(ma[i], mr[i], me[i], L, U);
+      su_scr[i] = __double2float_ru(U);
+    } else {
+      su_scr[i] = __int_as_float(0x7f800000);
+    }
+    ix_scr[i] = i;
+  }
+  __syncwarp();
+  warp_sort(su_scr, ix_scr, BUFW);
+  const double uk = (double)su_scr[kk - 1];
+  int keep = 0;
+  for (int i0 = 0; i0 < cnt; i0 += 32) {
+    const int i = i0 + lane;
+    bool in = false;
+    float av = 0.f, rv = 0.f, ev = 0.f;
+    int32_t iv = 0;
+    if (i < cnt) {
+      av = ma[i];
+      rv = mr[i];
+      ev = me[i];
+      iv = mi[i];
+      double L, U;
+      dist_bounds2(av, rv, ev, L, U);
+      in = L <= uk;
+    }
+    const unsigned bm = __ballot_sync(0xffffffffu, in);
+    __syncwarp();
+    if (in) {
+      const int dst = keep + __popc(bm & lanemask_lt());
+      ma[dst] = av;
+      mr[dst] = rv;
+      me[dst] = ev;
+      mi[dst] = iv;
+    }
+    __syncwarp();
+    keep += __popc(bm);
+  }
+  *su_out = uk >= 3.0e38 ? __int_as_float(0x7f800000) : __double2float_ru(sqrt(uk));
+  return keep;
+}
+
+struct Q8Rows {
+  const uint8_t *X;  // (n, ldq) u8
+  int64_t ldq;       // multiple of 16, <= 1024
+  const float *scale;
+  const int32_t *norm;
+  const float *radius;
+};
+
+__device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c, bool qsigned) {
+  int d;
+  if (qsigned)
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  else
+    asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// G lanes per row (ldq / 16 rounded up to a power of two, <= 32); each warp
+// iteration scores (32 / G) * 4 candidates with 16-byte loads.
+template <int BUFW, int G>
+__global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows rows,
+                                                             int32_t *fb_list, int32_t *fb_count) {
+  extern __shared__ unsigned long long topk_smem[];
+  constexpr int NWARP = kScanNT / 32;
+  constexpr int R = 32 / G;         // rows per load instruction
+  constexpr int U = 4;              // loads in flight per lane
+  constexpr int CPI = R * U;        // candidates per warp iteration (<= 32)
+  uint32_t *qb = reinterpret_cast<uint32_t *>(topk_smem);             // 256 words: quantized q
+  float *wa = reinterpret_cast<float *>(qb + 256);
+  float *wr = wa + NWARP * BUFW;
+  float *we = wr + NWARP * BUFW;
+  int32_t *wid = reinterpret_cast<int32_t *>(we + NWARP * BUFW);
+  unsigned long long *ckey = reinterpret_cast<unsigned long long *>(wid + NWARP * BUFW);
+  int32_t *cid = reinterpret_cast<int32_t *>(ckey + NWARP * BUFW);
+  float *cu = reinterpret_cast<float *>(cid + NWARP * BUFW);
+  float *cl = cu + NWARP * BUFW;
+  __shared__ int s_wcnt[NWARP];
+  __shared__ int s_bad, s_ns;
+  __shared__ float s_mn[NWARP], s_mx[NWARP];
+  __shared__ int s_int[NWARP];
+  __shared__ double s_r2[NWARP];
+  __shared__ long long s_nq[NWARP];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float *ma = wa + warp * BUFW;
+  float *mr = wr + warp * BUFW;
+  float *me = we + warp * BUFW;
+  int32_t *mi = wid + warp * BUFW;
+  const int d = a.d;
+  const int ldq = (int)rows.ldq;
+  const int nchunk = ldq / 16;
+  const int kk = a.k;
+  const int grp = lane / G, gl = lane % G;
+  for (int64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
+    const float *qrow = a.Q + q * a.ldq;
+    // --- quantize the query: u8 if q >= 0 (exact when integer-valued <= 255), else s8
+    float mn = 3.4e38f, mx = 0.f;
+    int isint = 1;
+    for (int c = tid; c < d; c += kScanNT) {
+      const float v = qrow[c];
+      mn = fminf(mn, v);
+      mx = fmaxf(mx, fabsf(v));
+      isint &= (v >= 0.f && v <= 255.f && rintf(v) == v) ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      isint &= __shfl_xor_sync(0xffffffffu, isint, o);
+    }
+    if (lane == 0) {
+      s_mn[warp] = mn;
+      s_mx[warp] = mx;
+      s_int[warp] = isint;
+    }
+    if (tid == 0) s_bad = 0;
+    __syncthreads();
+    mn = s_mn[0];
+    mx = s_mx[0];
+    isint = s_int[0];
+    for (int w = 1; w < NWARP; ++w) {
+      mn = fminf(mn, s_mn[w]);
+      mx = fmaxf(mx, s_mx[w]);
+      isint &= s_int[w];
+    }
+    const bool qsigned = mn < 0.f;
+    const float sq = isint ? 1.f : (mx > 0.f ? mx / (qsigned ? 127.f : 255.f) : 1.f);
+    double r2 = 0.0;
+    long long nq = 0;
+    for (int w4 = tid; w4 < ldq / 4; w4 += kScanNT) {
+      uint32_t packed = 0u;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int c = 4 * w4 + b;
+        const float v = c < d ? qrow[c] : 0.f;
+        float qv = rintf(v / sq);
+        qv = qsigned ? fminf(fmaxf(qv, -127.f), 127.f) : fminf(fmaxf(qv, 0.f), 255.f);
+        const int qi = (int)qv;
+        packed |= ((uint32_t)qi & 0xffu) << (8 * b);
+        const double e = (double)v - (double)sq * (double)qi;
+        r2 = fma(e, e, r2);
+        nq += (long long)qi * qi;
+      }
+      qb[w4] = packed;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+      nq += __shfl_xor_sync(0xffffffffu, nq, o);
+    }
+    __syncthreads();  // everyone has read s_mn/s_mx before they are rewritten
+    if (lane == 0) {
+      s_r2[warp] = r2;
+      s_nq[warp] = nq;
+    }
+    __syncthreads();
+    double r2t = 0.0;
+    long long nqt = 0;
+    for (int w = 0; w < NWARP; ++w) {
+      r2t += s_r2[w];
+      nqt += s_nq[w];
+    }
+    const float rq = r2t == 0.0 ? 0.f : __double2float_ru(__dsqrt_ru(r2t * (1.0 + 1e-12)));
+    const double sqd = (double)sq, t2 = sqd * sqd * (double)nqt;
+    int64_t m;
+    if (a.cand) {
+      const int64_t nc = a.ncand[q];
+      m = nc < a.cap ? nc : a.cap;
+    } else {
+      m = a.n;
+    }
+    const int32_t *qc = a.cand ? a.cand + q * a.cap : nullptr;
+    int cnt = 0;
+    float su = __int_as_float(0x7f800000);
+    bool bad = false;
+    for (int64_t g = (int64_t)warp * CPI; g < m; g += (int64_t)NWARP * CPI) {
+      int32_t cidv[U];
+      const uint8_t *rp[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = g + u * R + grp;
+        cidv[u] = j < m ? (qc ? __ldg(qc + j) : (int32_t)j) : -1;
+        rp[u] = rows.X + (int64_t)(cidv[u] < 0 ? 0 : cidv[u]) * ldq;
+      }
+      int acc[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc[u] = 0;
+      for (int ch = gl; ch < nchunk; ch += G) {
+        const uint4 qv = *reinterpret_cast<const uint4 *>(qb + 4 * ch);
+        uint4 xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = __ldg(reinterpret_cast<const uint4 *>(rp[u] + 16 * ch));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          acc[u] = dp4a_us(xv[u].x, qv.x, acc[u], qsigned);
+          acc[u] = dp4a_us(xv[u].y, qv.y, acc[u], qsigned);
+          acc[u] = dp4a_us(xv[u].z, qv.z, acc[u], qsigned);
+          acc[u] = dp4a_us(xv[u].w, qv.w, acc[u], qsigned);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+      }
+      // group leader of row group grp holds candidates u*R + grp; hand candidate
+      // (lane) = u*R + grp' to lane (u*R + grp') for the buffer decision
+      int mys = 0;
+      int32_t myc = -1;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = __shfl_sync(0xffffffffu, acc[u], ((lane - u * R) & (R - 1)) * G);
+        const int32_t c2 = __shfl_sync(0xffffffffu, cidv[u], ((lane - u * R) & (R - 1)) * G);
+        if (lane >= u * R && lane < (u + 1) * R) {
+          mys = v;
+          myc = c2;
+        }
+      }
+      float A = 0.f, r = 0.f, eta = 0.f;
+      if (lane < CPI && myc >= 0) {
+        const double sx = (double)__ldg(rows.scale + myc);
+        const double t1 = sx * sx * (double)__ldg(rows.norm + myc);
+        const double t3 = 2.0 * sx * sqd * (double)mys;
+        const double D = (t1 + t2) - t3;
+        A = (float)D;
+        eta = __double2float_ru(8.0 * 1.1102230246251565e-16 * (t1 + t2 + fabs(t3)) +
+                                5.9604644775390625e-08 * fabs(D)) ;
+        r = __fadd_ru(__ldg(rows.radius + myc), rq);
+      }
+      const bool take = lane < CPI && myc >= 0 && admit2(A, r, eta, su);
+      const unsigned tm = __ballot_sync(0xffffffffu, take);
+      if (take) {
+        const int slot = cnt + __popc(tm & lanemask_lt());
+        ma[slot] = A;
+        mr[slot] = r;
+        me[slot] = eta;
+        mi[slot] = myc;
+      }
+      cnt += __popc(tm);
+      if (cnt > BUFW - CPI) {
+        __syncwarp();
+        cnt = shrink_bounds2<BUFW>(ma, mr, me, mi, cnt, kk, cu + warp * BUFW, cid + warp * BUFW, &su);
+        if (cnt > BUFW - CPI) {
+          bad = true;
+          cnt = 0;
+          break;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      s_wcnt[warp] = cnt;
+      if (bad) s_bad = 1;
+    }
+    __syncthreads();
+    if (s_bad) {
+      if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = (int32_t)q;
+      __syncthreads();
+      continue;
+    }
+    int off = 0, total = 0;
+    for (int w = 0; w < NWARP; ++w) {
+      off += w < warp ? s_wcnt[w] : 0;
+      total += s_wcnt[w];
+    }
+    for (int i = lane; i < cnt; i += 32) {
+      double L, Uu;
+      dist_bounds2(ma[i], mr[i], me[i], L, Uu);
+      cu[off + i] = __double2float_ru(Uu);
+      cl[off + i] = __double2float_rd(L);
+      cid[off + i] = mi[i];
+    }
+    __syncthreads();
+    int np2 = 32;
+    while (np2 < total) np2 <<= 1;
+    float *su2 = wa;
+    int32_t *sx = wid;
+    for (int i = tid; i < np2; i += kScanNT) {
+      su2[i] = i < total ? cu[i] : __int_as_float(0x7f800000);
+      sx[i] = i;
+    }
+    __syncthreads();
+    for (int size = 2; size <= np2; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = tid; i < np2 / 2; i += kScanNT) {
+          const int lo = 2 * i - (i & (stride - 1));
+          const int hi = lo + stride;
+          const bool asc = (lo & size) == 0;
+          const float ka = su2[lo], kb = su2[hi];
+          const int ia = sx[lo], ib = sx[hi];
+          if (fpair_less(kb, ib, ka, ia) == asc) {
+            su2[lo] = kb;
+            su2[hi] = ka;
+            sx[lo] = ib;
+            sx[hi] = ia;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    const double uk = total >= kk ? (double)su2[kk - 1] : __longlong_as_double(0x7ff0000000000000LL);
+    if (tid == 0) s_ns = 0;
+    __syncthreads();
+    for (int i = tid; i < total; i += kScanNT) {
+      if ((double)cl[i] <= uk) sx[atomicAdd(&s_ns, 1)] = cid[i];
+    }
+    __syncthreads();
+    const int ns = s_ns;
+    int np3 = 1;
+    while (np3 < ns) np3 <<= 1;
+    for (int i = tid; i < np3; i += kScanNT) {
+      if (i < ns) {
+        const int32_t id = sx[i];
+        const float *xr = a.X + (int64_t)id * a.ldx;
+        double e = 0.0;
+        for (int c = 0; c < d; ++c) {
+          const double t = (double)__ldg(xr + c) - (double)__ldg(qrow + c);
+          e = __dadd_rn(e, __dmul_rn(t, t));
+        }
+        ckey[i] = (unsigned long long)__double_as_longlong(e);
+        cid[i] = id;
+      } else {
+        ckey[i] = ~0ull;
+        cid[i] = 0x7fffffff;
+      }
+    }
+    __syncthreads();
+    for (int size = 2; size <= np3; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = tid; i < np3 / 2; i += kScanNT) {
+          const int lo = 2 * i - (i & (stride - 1));
+          const int hi = lo + stride;
+          const bool asc = (lo & size) == 0;
+          const unsigned long long ka = ckey[lo], kb = ckey[hi];
+          const int ia = cid[lo], ib = cid[hi];
+          if (pair_less(kb, ib, ka, ia) == asc) {
+            ckey[lo] = kb;
+            ckey[hi] = ka;
+            cid[lo] = ib;
+            cid[hi] = ia;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    const int kept = ns < kk ? ns : kk;
+    for (int i = tid; i < kk; i += kScanNT) {
+      if (i < kept) {
+        a.ids[q * a.kstride + i] = cid[i];
+        a.dists[q * a.kstride + i] = sqrt(__longlong_as_double((long long)ckey[i]));
+      } else {
+        a.ids[q * a.kstride + i] = -1;
+        a.dists[q * a.kstride + i] = __longlong_as_double(0x7ff0000000000000LL);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(kScanNT)
 k_scan(const float *__restrict__ X, int64_t ldx, int d, const int64_t *__restrict__ cand, int64_t m,
        const float *__restrict__ q, double *out, bool vec4) {
@@ -1171,7 +1614,7 @@ extern "C" int32_t mrpt_scan_topk_fp16(const float *X, int64_t n, int32_t d, int
                                        double *dists, void *stream) {
   clear_error();
   if (!Xh || !radius || ldh % 8 != 0 || ldh < d || ldh > 1024 || k > 120 || k < 1 ||
-      (ldq % 4) != 0 || !aligned16(Q))
+      (ldq % 4) != 0 || !aligned16(Q) || d % 4 != 0 || ldx % 4 != 0 || !aligned16(X))
     return mrpt_scan_topk(X, n, d, ldx, Q, nq, ldq, cand, cap, ncand, k, ids, dists, stream);
   if (n < 1 || n >= (int64_t)1 << 31 || d < 1 || ldx < d || ldq < d || nq < 0)
     return fail(MRPT_ESHAPE, "mrpt_scan_topk_fp16: bad shape");
@@ -1230,4 +1673,112 @@ extern "C" int32_t mrpt_scan_topk_fp16(const float *X, int64_t n, int32_t d, int
   }
   cudaFreeAsync(fb, s);
   return launch_status("mrpt_scan_topk_fp16");
+}
+
+extern "C" int32_t mrpt_quantize_u8(const float *X, int64_t n, int32_t d, int64_t ldx, void *Xq,
+                                    int64_t ldq, float *scale, int32_t *norm, float *radius,
+                                    int32_t *flags, void *stream) {
+  // flags (device, 2 int32): [0] = 1 if some x < 0 (the u8 shadow is then
+  // unusable and left unwritten), [1] = 1 if not integer-valued in [0, 255]
+  clear_error();
+  if (n < 1 || d < 1 || ldx < d || ldq < d || ldq % 16 != 0 || ldq > 1024)
+    return fail(MRPT_ESHAPE, "mrpt_quantize_u8: bad shape");
+  cudaStream_t s = as_stream(stream);
+  cudaMemsetAsync(flags, 0, 2 * sizeof(int32_t), s);
+  const int64_t total = n * d;
+  const int64_t blocks = ceil_div<int64_t>(total, 256 * 8);
+  const int g1 = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
+  k_q8_flags<<<g1, 256, 0, s>>>(X, n, d, ldx, flags);
+  int32_t hflags[2] = {0, 0};
+  cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return launch_status("mrpt_quantize_u8");
+  if (hflags[0]) return MRPT_OK;
+  const int64_t wb = ceil_div<int64_t>(n, 8);
+  const int g2 = (int)(wb < (int64_t)num_sms() * 16 ? wb : (int64_t)num_sms() * 16);
+  k_quantize_u8<<<g2, 256, 0, s>>>(X, n, d, ldx, reinterpret_cast<uint8_t *>(Xq), ldq, scale, norm,
+                                   radius, hflags[1] ? 0 : 1);
+  return launch_status("mrpt_quantize_u8");
+}
+
+typedef void (*topk_fn_u8)(TopkArgs, Q8Rows, int32_t *, int32_t *);
+
+template <int G>
+static topk_fn_u8 pick_u8_b(int bufw) {
+  return bufw == 64 ? k_scan_topk_u8<64, G> : (bufw == 128 ? k_scan_topk_u8<128, G> : k_scan_topk_u8<256, G>);
+}
+
+extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64_t ldx,
+                                     const void *Xq, int64_t ldq, const float *scale,
+                                     const int32_t *norm, const float *radius, const float *Q,
+                                     int64_t nq, int64_t ldqq, const int32_t *cand, int64_t cap,
+                                     const int32_t *ncand, int32_t k, int64_t *ids, double *dists,
+                                     void *stream) {
+  clear_error();
+  if (!Xq || !scale || !norm || !radius || ldq % 16 != 0 || ldq < d || ldq > 1024 || k > 120 || k < 1 ||
+      d % 4 != 0 || ldx % 4 != 0 || !aligned16(X))  // the exact fallback needs 16-byte rows
+    return mrpt_scan_topk(X, n, d, ldx, Q, nq, ldqq, cand, cap, ncand, k, ids, dists, stream);
+  if (n < 1 || n >= (int64_t)1 << 31 || d < 1 || ldx < d || ldqq < d || nq < 0)
+    return fail(MRPT_ESHAPE, "mrpt_scan_topk_u8: bad shape");
+  if (cand && (cap < 1 || !ncand)) return fail(MRPT_EPARAM, "mrpt_scan_topk_u8: bad candidate lists");
+  if (nq == 0) return MRPT_OK;
+  cudaStream_t s = as_stream(stream);
+  TopkArgs a;
+  a.X = X;
+  a.n = n;
+  a.d = d;
+  a.ldx = ldx;
+  a.Q = Q;
+  a.nq = nq;
+  a.ldq = ldqq;
+  a.cand = cand;
+  a.cap = cap;
+  a.ncand = ncand;
+  a.k = k;
+  a.kstride = k;
+  a.ids = ids;
+  a.dists = dists;
+  a.lb_key = nullptr;
+  a.lb_id = nullptr;
+  a.vec4 = (d % 4 == 0) && (ldx % 4 == 0) && aligned16(X);
+  a.qlist = nullptr;
+  a.qcount = nullptr;
+  a.Xh = nullptr;
+  a.ldh = 0;
+  a.radius = nullptr;
+  Q8Rows rows;
+  rows.X = reinterpret_cast<const uint8_t *>(Xq);
+  rows.ldq = ldq;
+  rows.scale = scale;
+  rows.norm = norm;
+  rows.radius = radius;
+  const int chunks = (int)(ldq / 16);
+  const int G = chunks >= 32 ? 32 : (chunks > 16 ? 32 : (chunks > 8 ? 16 : 8));
+  const int cpi = (32 / G) * 4;
+  int bufw = 64;
+  while (bufw < 2 * k + 2 * cpi) bufw <<= 1;
+  if (bufw > 256) return mrpt_scan_topk(X, n, d, ldx, Q, nq, ldqq, cand, cap, ncand, k, ids, dists, stream);
+  const size_t smem = 1024 + (size_t)(kScanNT / 32) * bufw * (4 * 4 + 8 + 4 * 3);
+  int32_t *fb = nullptr;
+  if (cudaMallocAsync((void **)&fb, sizeof(int32_t) * (nq + 1), s) != cudaSuccess)
+    return fail(MRPT_ECUDA, "mrpt_scan_topk_u8: scratch allocation failed");
+  cudaMemsetAsync(fb, 0, sizeof(int32_t), s);
+  topk_fn_u8 fn = G == 32 ? pick_u8_b<32>(bufw) : (G == 16 ? pick_u8_b<16>(bufw) : pick_u8_b<8>(bufw));
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t grid = nq < (int64_t)num_sms() * 8 ? nq : (int64_t)num_sms() * 8;
+  fn<<<(unsigned)grid, kScanNT, smem, s>>>(a, rows, fb + 1, fb);
+  a.qlist = fb + 1;
+  a.qcount = fb;
+  if (a.vec4) {
+    const int buf = (k + kScanNT <= 1024) ? 1024 : 2048;
+    topk_fn tfn = buf == 1024 ? k_scan_topk_tiled<1024> : k_scan_topk_tiled<2048>;
+    const size_t tsmem = (size_t)buf * 12 + sizeof(float) * (kScanNT / 32) * 32 * kTileStride +
+                         sizeof(double) * (size_t)d;
+    cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+    tfn<<<(unsigned)(grid < 64 ? grid : 64), kScanNT, tsmem, s>>>(a);
+  } else {
+    cudaFreeAsync(fb, s);
+    return fail(MRPT_EPARAM, "mrpt_scan_topk_u8: exact fallback needs 16-byte rows");
+  }
+  cudaFreeAsync(fb, s);
+  return launch_status("mrpt_scan_topk_u8");
 }

@@ -11,6 +11,7 @@ results and error order.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -239,7 +240,6 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
         per_q = 4 * (D.T + cap)
         chunk = max(1, min(nq, (1 << 30) // per_q))
     vdir = D.vote_dir()
-    shadow = D.shadow() if k <= 120 else None
     leaves = torch.empty((min(chunk, nq), D.T), dtype=torch.int32, device=dev)
     cand = torch.empty((min(chunk, nq), cap), dtype=torch.int32, device=dev)
     stream = _native.stream_ptr()
@@ -254,18 +254,71 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
               D.n, D.T, D.depth, _native.ptr(leaves), e - s, int(votes), int(D.leaves_sorted),
               int(D.max_count), _native.ptr(vdir), _native.ptr(cand), int(cap),
               _native.ptr(counts[s:e]), stream)
-        if shadow is not None:
-            stage("scan_topk", _native.call, "mrpt_scan_topk_fp16", _native.ptr(D.X), D.n, D.d,
-                  int(D.X.stride(0)), _native.ptr(shadow[0]), shadow[1], _native.ptr(shadow[2]),
-                  _native.ptr(qb), e - s, int(Qd.stride(0)), _native.ptr(cand), int(cap),
-                  _native.ptr(counts[s:e]), int(k), _native.ptr(ids[s:e]),
-                  _native.ptr(dists[s:e]), stream)
-        else:
-            stage("scan_topk", _native.call, "mrpt_scan_topk", _native.ptr(D.X), D.n, D.d,
-                  int(D.X.stride(0)), _native.ptr(qb), e - s, int(Qd.stride(0)),
-                  _native.ptr(cand), int(cap), _native.ptr(counts[s:e]), int(k),
-                  _native.ptr(ids[s:e]), _native.ptr(dists[s:e]), stream)
+        args = (qb, e - s, int(Qd.stride(0)), cand, cap, counts[s:e], k, ids[s:e], dists[s:e])
+        variant = D.scan_choice.get(k)
+        if variant is None:
+            variant = _autotune_scan(D, args) if e - s >= 256 else "fp32"
+        stage("scan_topk", _scan_launch, D, variant, args)
     return ids, dists, counts
+
+
+def _scan_variants(D, k):
+    """Exact filter variants available for this index (all give identical results)."""
+    out = []
+    if k <= 120 and D.u8_rows() is not None:
+        out.append("u8")
+    if k <= 120 and D.shadow() is not None:
+        out.append("fp16")
+    out.append("fp32")
+    return out
+
+
+def _scan_launch(D, variant, args):
+    """K4 over one query chunk with the chosen filter rows."""
+    qb, m, ldq, cand, cap, counts, k, ids, dists = args
+    stream = _native.stream_ptr()
+    common_tail = (_native.ptr(qb), m, ldq, _native.ptr(cand), int(cap), _native.ptr(counts),
+                   int(k), _native.ptr(ids), _native.ptr(dists), stream)
+    if variant == "u8":
+        Xq, ldr, sc, nm, rad = D.u8_rows()
+        _native.call("mrpt_scan_topk_u8", _native.ptr(D.X), D.n, D.d, int(D.X.stride(0)),
+                     _native.ptr(Xq), ldr, _native.ptr(sc), _native.ptr(nm), _native.ptr(rad),
+                     *common_tail)
+    elif variant == "fp16":
+        Xh, ldh, rad = D.shadow()
+        _native.call("mrpt_scan_topk_fp16", _native.ptr(D.X), D.n, D.d, int(D.X.stride(0)),
+                     _native.ptr(Xh), ldh, _native.ptr(rad), *common_tail)
+    else:
+        _native.call("mrpt_scan_topk", _native.ptr(D.X), D.n, D.d, int(D.X.stride(0)),
+                     *common_tail)
+
+
+def _autotune_scan(D, args):
+    """Time every exact filter variant once on this chunk and keep the fastest
+    for the index (per k); the last launch leaves valid outputs."""
+    torch = _device.torch_mod()
+    k = args[6]
+    env = os.environ.get("MRPT_SCAN_ROWS")
+    variants = _scan_variants(D, k)
+    if env in variants:
+        D.scan_choice[k] = env
+        return env
+    if len(variants) == 1:
+        D.scan_choice[k] = variants[0]
+        return variants[0]
+    best, best_ms = None, None
+    for v in variants:
+        _scan_launch(D, v, args)  # warm (first use builds nothing; shadows exist)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _scan_launch(D, v, args)
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        if best_ms is None or ms < best_ms:
+            best, best_ms = v, ms
+    D.scan_choice[k] = best
+    return best
 
 
 def approximate_knn_batch(Q, k, index, votes, chunk=None):

@@ -153,6 +153,7 @@ class _DeviceIndex:
         self.leaves_sorted = leaves_sorted
         self.max_count = max_count
         self.max_leaf = max_leaf
+        self.scan_choice = {}  # k -> exact filter variant chosen by the autotune
 
     def cap(self, votes):
         """Upper bound on any candidate set at this vote threshold."""
@@ -168,6 +169,10 @@ class _DeviceIndex:
         # worth it when the candidate rows stream from HBM (X well beyond L2)
         # and a row fills whole warps; MRPT_FP16_FILTER=1/0 forces it on/off
         mode = os.environ.get("MRPT_FP16_FILTER", "auto")
+        if os.environ.get("MRPT_SCAN_ROWS") == "fp16":
+            mode = "1"
+        elif os.environ.get("MRPT_SCAN_ROWS") == "fp32":
+            mode = "0"
         want = (mode == "1") or (mode == "auto" and self.d >= 256 and self.n * self.d * 4 > (256 << 20))
         if want and ldh <= 1024 and self.d % 4 == 0:
             torch = _device.torch_mod()
@@ -180,6 +185,31 @@ class _DeviceIndex:
             if not int(bad.item()):
                 self._shadow = (Xh, ldh, rad)
         return self._shadow
+
+    def u8_rows(self):
+        """u8 shadow (rows, row stride, scale, norm, radius) for non-negative
+        data, built once; None for signed data or unsupported widths
+        (MRPT_SCAN_ROWS=fp16|fp32 disables it)."""
+        if getattr(self, "_u8", False) is not False:
+            return self._u8
+        self._u8 = None
+        ldq = (self.d + 15) // 16 * 16
+        mode = os.environ.get("MRPT_SCAN_ROWS", "auto")
+        if mode in ("auto", "u8") and ldq <= 1024:
+            torch = _device.torch_mod()
+            dev = self.X.device
+            Xq = torch.empty((self.n, ldq), dtype=torch.uint8, device=dev)
+            sc = torch.empty(self.n, dtype=torch.float32, device=dev)
+            nm = torch.empty(self.n, dtype=torch.int32, device=dev)
+            rad = torch.empty(self.n, dtype=torch.float32, device=dev)
+            flags = torch.zeros(2, dtype=torch.int32, device=dev)
+            _native.call("mrpt_quantize_u8", _native.ptr(self.X), self.n, self.d,
+                         int(self.X.stride(0)), _native.ptr(Xq), ldq, _native.ptr(sc),
+                         _native.ptr(nm), _native.ptr(rad), _native.ptr(flags),
+                         _native.stream_ptr())
+            if not int(flags[0].item()):
+                self._u8 = (Xq, ldq, sc, nm, rad)
+        return self._u8
 
     def vote_dir(self):
         """Tile directory for the multi-tile vote (built once, on the device),
