@@ -30,6 +30,22 @@ inline int32_t launch_status(const char *where) {
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Small stream-ordered scratch (fallback lists) comes from the device's
+// default memory pool; keep freed blocks cached in the pool instead of
+// returning them to the driver at every synchronisation, so per-call scratch
+// never costs a host-side remap.  Idempotent, per device.
+inline void keep_pool_warm() {
+  static int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = 64ull << 20;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done_dev = dev;
+}
+
 inline int num_sms() {
   static int sms = 0;  // benign race: every thread computes the same value
   if (sms == 0) {

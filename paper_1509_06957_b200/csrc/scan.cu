@@ -1516,7 +1516,8 @@ extern "C" int32_t mrpt_scan_topk(const float *X, int64_t n, int32_t d, int64_t 
   const int chunk_max = 4096 - kScanNT * kScanR;  // 3072 entries per pass
   const int passes = (k + chunk_max - 1) / chunk_max;
   if (passes > 1) {
-    if (cudaMallocAsync((void **)&a.lb_key, sizeof(unsigned long long) * nq, s) != cudaSuccess ||
+    keep_pool_warm();
+  if (cudaMallocAsync((void **)&a.lb_key, sizeof(unsigned long long) * nq, s) != cudaSuccess ||
         cudaMallocAsync((void **)&a.lb_id, sizeof(int32_t) * nq, s) != cudaSuccess)
       return fail(MRPT_ECUDA, "mrpt_scan_topk: scratch allocation failed");
     // lower bound below every key: (0, -1)
@@ -1533,7 +1534,8 @@ extern "C" int32_t mrpt_scan_topk(const float *X, int64_t n, int32_t d, int64_t 
     const int bufw = (2 * k + 16 <= 64) ? 64 : ((2 * k + 16 <= 128) ? 128 : 256);
     const size_t smem = sizeof(float) * 128 * kFMaxJ + (size_t)(kScanNT / 32) * bufw * (4 + 4 + 8 + 4 + 4);
     int32_t *fb = nullptr;
-    if (cudaMallocAsync((void **)&fb, sizeof(int32_t) * (nq + 1), s) != cudaSuccess)
+    keep_pool_warm();
+  if (cudaMallocAsync((void **)&fb, sizeof(int32_t) * (nq + 1), s) != cudaSuccess)
       return fail(MRPT_ECUDA, "mrpt_scan_topk: scratch allocation failed");
     cudaMemsetAsync(fb, 0, sizeof(int32_t), s);
     const double u = 5.9604644775390625e-08;  // 2^-24
@@ -1647,6 +1649,7 @@ extern "C" int32_t mrpt_scan_topk_fp16(const float *X, int64_t n, int32_t d, int
   const int bufw = (2 * k + 16 <= 64) ? 64 : ((2 * k + 16 <= 128) ? 128 : 256);
   const size_t smem = sizeof(float) * 256 * 4 + (size_t)(kScanNT / 32) * bufw * (4 + 4 + 4 + 8 + 4 + 4 + 4);
   int32_t *fb = nullptr;
+  keep_pool_warm();
   if (cudaMallocAsync((void **)&fb, sizeof(int32_t) * (nq + 1), s) != cudaSuccess)
     return fail(MRPT_ECUDA, "mrpt_scan_topk_fp16: scratch allocation failed");
   cudaMemsetAsync(fb, 0, sizeof(int32_t), s);
@@ -1759,6 +1762,7 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
   if (bufw > 256) return mrpt_scan_topk(X, n, d, ldx, Q, nq, ldqq, cand, cap, ncand, k, ids, dists, stream);
   const size_t smem = 1024 + (size_t)(kScanNT / 32) * bufw * (4 * 4 + 8 + 4 * 3);
   int32_t *fb = nullptr;
+  keep_pool_warm();
   if (cudaMallocAsync((void **)&fb, sizeof(int32_t) * (nq + 1), s) != cudaSuccess)
     return fail(MRPT_ECUDA, "mrpt_scan_topk_u8: scratch allocation failed");
   cudaMemsetAsync(fb, 0, sizeof(int32_t), s);
