@@ -283,18 +283,23 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_vote_dir(VoteArgs a) {
     __syncthreads();
     int32_t *qcand = a.cand + q * a.cap;
     int64_t ncand = 0;
-    // with few trees, several warps share one group of 32 trees, each taking
-    // every parts-th 32-wide window of the group's flattened slices
-    const int parts = ngroups >= NW ? 1 : NW / ngroups;
-    const int nvirt = ngroups * parts;
+    // Work split per tile: with NW <= T <= 32*NW every warp owns a balanced
+    // contiguous range of <= 32 trees; with fewer trees several warps share
+    // one group, each taking every parts-th 32-wide window; with more, warps
+    // loop over 32-tree groups.
+    const bool ranged = a.T >= NW && a.T <= 32 * NW;
+    const int parts = ranged || ngroups >= NW ? 1 : NW / ngroups;
+    const int nvirt = ranged ? NW : ngroups * parts;
     for (int tile = 0; tile < a.ntiles; ++tile) {
       const int32_t lo = tile * a.W;
       for (int vw = warp; vw < nvirt; vw += NW) {
-        const int g = vw % ngroups, part = vw / ngroups;
-        const int t = g * 32 + lane;
+        const int g = ranged ? 0 : vw % ngroups, part = ranged ? 0 : vw / ngroups;
+        const int t_lo = ranged ? (int)(((int64_t)vw * a.T) / NW) : g * 32;
+        const int t_hi = ranged ? (int)(((int64_t)(vw + 1) * a.T) / NW) : (g * 32 + 32 < a.T ? g * 32 + 32 : a.T);
+        const int t = t_lo + lane;
         int len = 0;
         long long base = 0;
-        if (t < a.T) {
+        if (t < t_hi) {
           const uint16_t *d = a.dir + ((int64_t)t * a.L + sleaf[t]) * dstride + tile;
           const int s0 = d[0], s1 = d[1];
           len = s1 - s0;
@@ -317,7 +322,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_vote_dir(VoteArgs a) {
           w_pre[warp][r] = pre;
         }
         __syncwarp();
-        constexpr int UNR = 4;
+        constexpr int UNR = 8;
         const int stride = parts * 32;
         for (int e0 = part * 32; e0 < total; e0 += UNR * stride) {
           int32_t id[UNR];
