@@ -1227,7 +1227,7 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
       nqt += s_nq[w];
     }
     const float rq = r2t == 0.0 ? 0.f : __double2float_ru(__dsqrt_ru(r2t * (1.0 + 1e-12)));
-    const double sqd = (double)sq, t2 = sqd * sqd * (double)nqt;
+    const float sqf = sq, t2f = sq * sq * (float)nqt;
     int64_t m;
     if (a.cand) {
       const int64_t nc = a.ncand[q];
@@ -1282,15 +1282,15 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
           myc = c2;
         }
       }
+      // float32 evaluation: each of t1, t2, t3 carries <= 3 roundings and the
+      // sum two more, so |A - D| <= 8 * 2^-24 * (t1 + t2 + |t3|)
       float A = 0.f, r = 0.f, eta = 0.f;
       if (lane < CPI && myc >= 0) {
-        const double sx = (double)__ldg(rows.scale + myc);
-        const double t1 = sx * sx * (double)__ldg(rows.norm + myc);
-        const double t3 = 2.0 * sx * sqd * (double)mys;
-        const double D = (t1 + t2) - t3;
-        A = (float)D;
-        eta = __double2float_ru(8.0 * 1.1102230246251565e-16 * (t1 + t2 + fabs(t3)) +
-                                5.9604644775390625e-08 * fabs(D)) ;
+        const float sx = __ldg(rows.scale + myc);
+        const float t1 = sx * sx * (float)__ldg(rows.norm + myc);
+        const float t3 = 2.0f * sx * sqf * (float)mys;
+        A = (t1 + t2f) - t3;
+        eta = __fmul_ru(4.76837158203125e-07f, __fadd_ru(__fadd_ru(t1, t2f), fabsf(t3)));
         r = __fadd_ru(__ldg(rows.radius + myc), rq);
       }
       const bool take = lane < CPI && myc >= 0 && admit2(A, r, eta, su);
@@ -1754,8 +1754,9 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
   rows.scale = scale;
   rows.norm = norm;
   rows.radius = radius;
-  const int chunks = (int)(ldq / 16);
-  const int G = chunks >= 32 ? 32 : (chunks > 16 ? 32 : (chunks > 8 ? 16 : 8));
+  // 8 lanes per row: 16 candidates per warp iteration, 3 shuffle levels per
+  // reduction, several chunk loads in flight per lane even for wide rows
+  const int G = 8;
   const int cpi = (32 / G) * 4;
   int bufw = 64;
   while (bufw < 2 * k + 2 * cpi) bufw <<= 1;
