@@ -245,28 +245,41 @@ def run_ours(args):
     def timed_step(events):
         return query_device(D, Qd, k, v, timer=events)
 
+    # L2 is flushed between timed steps (a 2x-L2 write outside each step's events):
+    # within a step, the index and data rows are re-read by many queries, which is
+    # the workload; across steps nothing stays warm.  Warm-up runs the identical
+    # sequence (flush, events, stage timers) so no first-use cost lands in the
+    # timed region.
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(args.warmup):
-        query_device(D, Qd, k, v)
+        flush.fill_(1)
+        w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0.record(stream)
+        timed_step([])
+        w1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     evs = []
+    step_ev = []
     with Clocks(local) as clk:
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        start = torch.cuda.Event(enable_timing=True)
-        end = torch.cuda.Event(enable_timing=True)
-        start.record(stream)
         for _ in range(args.steps):
+            flush.fill_(1)
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
             ev = []
             timed_step(ev)
+            s1.record(stream)
             evs.append(ev)
-        end.record(stream)
+            step_ev.append((s0, s1))
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-    elapsed_ms = start.elapsed_time(end)
+    elapsed_ms = sum(a.elapsed_time(b) for a, b in step_ev)
     for ev in evs:
         for name, a, b in ev:
             stage_ms[name] += a.elapsed_time(b)
@@ -318,6 +331,18 @@ def run_ours(args):
             traffic = json.load(open(tpath)).get(dominant)
         except Exception:
             traffic = None
+    # bytes the chosen filter variant actually reads per candidate (its row
+    # format + per-row side data + the candidate id); survivors reranked in fp32
+    # are not included
+    variant = D.scan_choice.get(k, "fp32")
+    if variant == "u8":
+        row_b, filt_mb = D.u8_rows()[1] + 12, D.n * D.u8_rows()[1] / 1e6
+    elif variant == "fp16":
+        row_b, filt_mb = 2 * D.shadow()[1] + 4, D.n * 2 * D.shadow()[1] / 1e6
+    else:
+        row_b, filt_mb = 4 * p["d"], X.nbytes / 1e6
+    filter_bytes = float(cand.sum().item()) * (row_b + 4)
+    filter_gbs = filter_bytes / (stage_ms["scan_topk"] / steps / 1000.0) / 1e9
     stage_gbs = (vote_bytes + scan_bytes) / ((stage_ms["vote"] + stage_ms["scan_topk"]) / steps / 1000.0) / 1e9
 
     line = {
@@ -328,8 +353,9 @@ def run_ours(args):
         "config": {"workload": p["name"], "n": p["n"], "d": p["d"], "nq_per_gpu": p["nq"],
                    "n_trees": p["n_trees"], "depth": p["depth"], "k": k, "votes": v,
                    "sparsity": p["sparsity"], "generator": p["generator"],
-                   "l2": "inputs larger than L2 (X %.0f MB, leaf ids %.0f MB)" % (
-                       X.nbytes / 1e6, 4.0 * p["n_trees"] * p["n"] / 1e6),
+                   "l2": "L2 flushed between timed steps (256 MB write outside the step "
+                         "events); X %.0f MB, leaf ids %.0f MB, scan filter rows %.0f MB" % (
+                       X.nbytes / 1e6, 4.0 * p["n_trees"] * p["n"] / 1e6, filt_mb),
                    "parallelism": f"replicated index, queries sharded by batch x{world}"},
         "recall_at_k": recall,
         "mean_candidates": float(cand.mean().item()),
@@ -339,7 +365,15 @@ def run_ours(args):
                      "traffic": traffic,
                      "stage_vote_plus_scan_gbs": stage_gbs,
                      "stage_frac": stage_gbs / peak,
-                     "bytes_per_query": (vote_bytes + scan_bytes) / p["nq"]},
+                     "bytes_per_query": (vote_bytes + scan_bytes) / p["nq"],
+                     "scan_variant": variant,
+                     "scan_filter_bytes_per_query": filter_bytes / p["nq"],
+                     "scan_filter_gbs": filter_gbs,
+                     "note": "achieved/frac use SURVEY 8(d) algorithmic bytes (4 B per leaf id "
+                             "+ 4*d B per candidate row); frac > 1 is possible because the "
+                             "exact scan filters on %s rows (%d B/candidate) and the per-step "
+                             "working set can sit in the 126 MB L2; traffic = ncu DRAM bytes "
+                             "of the kernel per launch" % (variant, row_b + 4)},
         "stage_ms_per_step": {k2: v2 / steps for k2, v2 in stage_ms.items()},
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
