@@ -1113,13 +1113,35 @@ struct Q8Rows {
   const float *radius;
 };
 
-__device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c, bool qsigned) {
+template <bool QS>
+__device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
   int d;
-  if (qsigned)
+  if (QS)
     asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
   else
     asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
   return d;
+}
+
+// U rows' partial dot products over this lane's 16-byte chunks.  The query's
+// signedness is a template parameter: a runtime flag here puts a branch
+// around every dp4a (inline asm cannot be predicated).
+template <int U, int G, bool QS>
+__device__ __forceinline__ void dot_rows_u8(const uint8_t *(&rp)[U], const uint32_t *qb,
+                                            int gl, int nchunk, int (&acc)[U]) {
+  for (int ch = gl; ch < nchunk; ch += G) {
+    const uint4 qv = *reinterpret_cast<const uint4 *>(qb + 4 * ch);
+    uint4 xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = __ldg(reinterpret_cast<const uint4 *>(rp[u] + 16 * ch));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      acc[u] = dp4a_us<QS>(xv[u].x, qv.x, acc[u]);
+      acc[u] = dp4a_us<QS>(xv[u].y, qv.y, acc[u]);
+      acc[u] = dp4a_us<QS>(xv[u].z, qv.z, acc[u]);
+      acc[u] = dp4a_us<QS>(xv[u].w, qv.w, acc[u]);
+    }
+  }
 }
 
 // G lanes per row (ldq / 16 rounded up to a power of two, <= 32); each warp
@@ -1251,19 +1273,10 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
       int acc[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) acc[u] = 0;
-      for (int ch = gl; ch < nchunk; ch += G) {
-        const uint4 qv = *reinterpret_cast<const uint4 *>(qb + 4 * ch);
-        uint4 xv[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) xv[u] = __ldg(reinterpret_cast<const uint4 *>(rp[u] + 16 * ch));
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          acc[u] = dp4a_us(xv[u].x, qv.x, acc[u], qsigned);
-          acc[u] = dp4a_us(xv[u].y, qv.y, acc[u], qsigned);
-          acc[u] = dp4a_us(xv[u].z, qv.z, acc[u], qsigned);
-          acc[u] = dp4a_us(xv[u].w, qv.w, acc[u], qsigned);
-        }
-      }
+      if (qsigned)
+        dot_rows_u8<U, G, true>(rp, qb, gl, nchunk, acc);
+      else
+        dot_rows_u8<U, G, false>(rp, qb, gl, nchunk, acc);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
 #pragma unroll
@@ -1754,9 +1767,17 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
   rows.scale = scale;
   rows.norm = norm;
   rows.radius = radius;
-  // 8 lanes per row: 16 candidates per warp iteration, 3 shuffle levels per
-  // reduction, several chunk loads in flight per lane even for wide rows
-  const int G = 8;
+  // G lanes per row: 8 for wide rows (16 candidates per warp iteration, several
+  // chunk loads in flight per lane); 4 for rows of <= 256 bytes (two or more
+  // chunks per lane, 32 candidates per iteration, one shuffle level less).
+  // MRPT_U8_G overrides (4, 8, 16, 32).
+  static int g_env = -1;
+  if (g_env < 0) {
+    const char *e = getenv("MRPT_U8_G");
+    g_env = e ? atoi(e) : 0;
+  }
+  const int G = (g_env == 4 || g_env == 8 || g_env == 16 || g_env == 32) ? g_env
+                                                                         : (ldq <= 256 ? 4 : 8);
   const int cpi = (32 / G) * 4;
   int bufw = 64;
   while (bufw < 2 * k + 2 * cpi) bufw <<= 1;
@@ -1767,7 +1788,8 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
   if (cudaMallocAsync((void **)&fb, sizeof(int32_t) * (nq + 1), s) != cudaSuccess)
     return fail(MRPT_ECUDA, "mrpt_scan_topk_u8: scratch allocation failed");
   cudaMemsetAsync(fb, 0, sizeof(int32_t), s);
-  topk_fn_u8 fn = G == 32 ? pick_u8_b<32>(bufw) : (G == 16 ? pick_u8_b<16>(bufw) : pick_u8_b<8>(bufw));
+  topk_fn_u8 fn = G == 32 ? pick_u8_b<32>(bufw)
+                  : (G == 16 ? pick_u8_b<16>(bufw) : (G == 8 ? pick_u8_b<8>(bufw) : pick_u8_b<4>(bufw)));
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t grid = nq < (int64_t)num_sms() * 8 ? nq : (int64_t)num_sms() * 8;
   fn<<<(unsigned)grid, kScanNT, smem, s>>>(a, rows, fb + 1, fb);

@@ -410,7 +410,151 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_vote_dir(VoteArgs a) {
   }
 }
 
+// Ordered compaction of a bitmap into out[base..], four words per thread per
+// round, clearing it on the way.  Each warp stages its ids in shared memory
+// (kUnionStage per warp, in windows if a round yields more) and copies them
+// out with consecutive lanes on consecutive positions, so the stores are
+// coalesced instead of one 32-byte sector per 4-byte id.
+constexpr int kUnionStage = 512;
+
+template <int NT>
+__device__ __forceinline__ int64_t emit_bitmap_staged(uint4 *bits4, int nwords4, int32_t *out,
+                                                      int64_t cap, int *wsum, int32_t *stage) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = NT / 32;
+  const int capi = cap < 0x7fffffff ? (int)cap : 0x7fffffff;
+  int64_t total = 0;
+  for (int r0 = 0; r0 < nwords4; r0 += NT) {
+    const int i = r0 + threadIdx.x;
+    uint4 w4 = i < nwords4 ? bits4[i] : make_uint4(0u, 0u, 0u, 0u);
+    const int pc = __popc(w4.x) + __popc(w4.y) + __popc(w4.z) + __popc(w4.w);
+    if (pc) bits4[i] = make_uint4(0u, 0u, 0u, 0u);
+    int incl = pc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const int c = lane < NW ? wsum[lane] : 0;
+      int x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += u;
+      }
+      if (lane < NW) wsum[lane] = x - c;
+      if (lane == 31) wsum[NW] = x;
+    }
+    __syncthreads();
+    const int tot = wsum[NW];
+    const int64_t gbase = total + wsum[warp];  // this warp's first output position
+    const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+    const int pos0 = incl - pc;  // warp-local
+    const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+    for (int c0 = 0; c0 < wtot && gbase + c0 < capi; c0 += kUnionStage) {
+      if (pc && pos0 < c0 + kUnionStage && incl > c0) {
+        if (pos0 >= c0 && incl <= c0 + kUnionStage) {
+          // common case: all of this thread's ids land in the window
+          int p = pos0 - c0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t word = wv[j];
+            const int32_t id0 = (i * 4 + j) * 32;
+            while (word) {
+              stage[p++] = id0 + __ffs(word) - 1;
+              word &= word - 1u;
+            }
+          }
+        } else {
+          int p = pos0 - c0;  // may start below the window
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t word = wv[j];
+            const int32_t id0 = (i * 4 + j) * 32;
+            while (word) {
+              if (p >= 0 && p < kUnionStage) stage[p] = id0 + __ffs(word) - 1;
+              ++p;
+              word &= word - 1u;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      const int cnt = wtot - c0 < kUnionStage ? wtot - c0 : kUnionStage;
+      for (int k = lane; k < cnt; k += 32) {
+        const int64_t gp = gbase + c0 + k;
+        if (gp < capi) out[gp] = stage[k];
+      }
+      __syncwarp();
+    }
+    total += tot;
+    __syncthreads();
+  }
+  return total;
+}
+
+// v == 1: the candidate set is the union of the T leaves, so one bit per id
+// replaces the counters and the whole id range fits one shared-memory bitmap
+// (n <= ~1.3M).  Slices need not be sorted.  The T slice bounds are fetched
+// into shared memory in one round trip; groups of G lanes then walk whole
+// leaf slices (contiguous runs of leaf_indices) with UNR loads in flight and
+// set bits with shared atomicOr; the bitmap is compacted in id order
+// (ascending candidate lists, like the counting path) and cleared on the way.
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k_vote_union(VoteArgs a, int G) {
+  extern __shared__ uint4 vote_smem[];
+  uint32_t *bits = reinterpret_cast<uint32_t *>(vote_smem);
+  const int nwords4 = (int)((a.n + 127) >> 7);
+  int32_t *stage = reinterpret_cast<int32_t *>(vote_smem + nwords4);  // NW * kUnionStage
+  int64_t *s_start = reinterpret_cast<int64_t *>(stage + (NT / 32) * kUnionStage);  // T
+  int32_t *s_len = reinterpret_cast<int32_t *>(s_start + a.T);                      // T
+  __shared__ int wsum[NT / 32 + 1];
+  const int tid = threadIdx.x;
+  const int gl = tid & (G - 1), ngroups = NT / G;
+  int32_t *my_stage = stage + (tid >> 5) * kUnionStage;
+  for (int i = tid; i < nwords4; i += NT) vote_smem[i] = make_uint4(0u, 0u, 0u, 0u);
+  const int64_t nwork = a.qlist ? (int64_t)*a.qcount : a.nq;
+  for (int64_t wq = blockIdx.x; wq < nwork; wq += gridDim.x) {
+    const int64_t q = a.qlist ? (int64_t)a.qlist[wq] : wq;
+    for (int t = tid; t < a.T; t += NT) {
+      const int leaf = a.leaves[q * a.T + t];
+      const int64_t *o = a.leaf_offsets + (int64_t)t * (a.L + 1) + leaf;
+      const int64_t s0 = o[0];
+      s_start[t] = (int64_t)t * a.n + s0;
+      s_len[t] = (int)(o[1] - s0);
+    }
+    __syncthreads();
+    for (int t = tid / G; t < a.T; t += ngroups) {
+      const int len = s_len[t];
+      const int32_t *Lt = a.leaf_indices + s_start[t];
+      constexpr int UNR = 8;
+      for (int p0 = gl; p0 < len; p0 += UNR * G) {
+        int32_t id[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const int p = p0 + u * G;
+          id[u] = p < len ? __ldg(Lt + p) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+          if (id[u] >= 0) atomicOr(bits + (id[u] >> 5), 1u << (id[u] & 31));
+      }
+    }
+    __syncthreads();
+    const int64_t nc = emit_bitmap_staged<NT>(vote_smem, nwords4, a.cand + q * a.cap, a.cap, wsum, my_stage);
+    if (tid == 0) a.ncand[q] = (int32_t)nc;  // > cap means only cap ids were stored
+  }
+}
+
 typedef void (*vote_fn)(VoteArgs);
+typedef void (*union_fn)(VoteArgs, int);
+static inline void k_vote_union_launch(union_fn fn, unsigned grid, int nt, size_t smem, cudaStream_t s,
+                                       const VoteArgs &a, int G) {
+  fn<<<grid, nt, smem, s>>>(a, G);
+}
 
 template <int CW, bool SORTED>
 static vote_fn pick_g(int G) {
@@ -521,6 +665,7 @@ using namespace mrpt;
 
 static const int kVoteSmemSingle = 110 * 1024;  // single tile
 static const int kVoteSmemTiled = 196 * 1024;   // tiled sweep: one big CTA per SM (+ static tables)
+static const int kVoteSmemUnion = 222 * 1024;   // v == 1 bitmap over all ids + staging
 
 // Tile geometry shared by mrpt_vote, mrpt_vote_plan and the directory.
 // Smem per tile: the packed counters, a 1-bit "reached v" flag per id, and
@@ -631,6 +776,32 @@ extern "C" int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_of
   a.dir = dir;
   const size_t smem = vote_smem_bytes(CW, W, T);
   const int64_t grid = nq < (int64_t)num_sms() * 4 ? nq : (int64_t)num_sms() * 4;
+  // v == 1: bitmap + per-warp staging + slice table
+  const size_t ubits = (size_t)((n + 127) >> 7) * 16;
+  const size_t usmem512 = ubits + 16 * kUnionStage * 4 + (size_t)12 * T;
+  const size_t usmem1024 = ubits + 32 * kUnionStage * 4 + (size_t)12 * T;
+  // (only where the counting path needs several id tiles: with one tile the
+  // counting kernel is as fast)
+  const char *uenv = getenv("MRPT_VOTE_UNION");  // "0": never, "1": whenever it fits
+  const bool want_union = uenv ? atoi(uenv) != 0 : ntiles > 1;
+  if (v == 1 && want_union && usmem1024 <= (size_t)kVoteSmemUnion && !getenv("MRPT_VOTE_NO_UNION")) {
+    // NT=512 when two CTAs fit per SM (one query's compaction overlaps the
+    // other's atomics), else one CTA of 1024 threads
+    const bool two = usmem512 + 4 * 1024 <= (size_t)kVoteSmemUnion / 2;
+    const size_t usmem = two ? usmem512 : usmem1024;
+    union_fn fn = two ? k_vote_union<512> : k_vote_union<1024>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usmem);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, two ? 512 : 1024, usmem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t g = (int64_t)num_sms() * per_sm;
+    // lanes per leaf slice: enough for UNR=8 loads each over a mean slice
+    const double mean_slice = (double)n / (double)((int64_t)1 << depth);
+    int Gu = 4;
+    while (Gu < 32 && Gu * 8 < mean_slice) Gu <<= 1;
+    k_vote_union_launch(fn, (unsigned)(nq < g ? nq : g), two ? 512 : 1024, usmem, s, a, Gu);
+    return launch_status("mrpt_vote");
+  }
   if (dir && ntiles > 1 && sorted) {
     const int nt = vote_dir_threads();
     vote_fn fn;

@@ -235,3 +235,65 @@ def test_unsorted_foreign_index_multi_tile_matches(rng):
         rb = mrpt.approximate_knn_batch(Q, 7, b, v)
         for x, y in zip(ra, rb):
             assert np.array_equal(x, y)
+
+
+def _vote_lists(index, Q, v):
+    """Raw K2+K3 output (candidate lists, counts) through the C ABI."""
+    import torch
+
+    from paper_1509_06957_b200 import _native
+    from paper_1509_06957_b200.search import _route_device
+
+    D = index.device_index()
+    Qd = torch.from_numpy(np.ascontiguousarray(Q)).cuda()
+    leaves = _route_device(Qd, D)
+    cap = D.cap(v)
+    cand = torch.full((Q.shape[0], cap), -7, dtype=torch.int32, device="cuda")
+    counts = torch.empty(Q.shape[0], dtype=torch.int32, device="cuda")
+    _native.call("mrpt_vote", _native.ptr(D.indices), _native.ptr(D.offsets), D.n, D.T, D.depth,
+                 _native.ptr(leaves), Q.shape[0], int(v), int(D.leaves_sorted), int(D.max_count),
+                 _native.ptr(D.vote_dir()), _native.ptr(cand), int(cap), _native.ptr(counts),
+                 _native.stream_ptr())
+    c = counts.cpu().numpy()
+    lists = [row[:m] for row, m in zip(cand.cpu().numpy(), c)]
+    return lists, c
+
+
+@pytest.mark.parametrize("T,depth,n,shuffle", [(40, 6, 20_000, False), (1100, 5, 3_000, False),
+                                               (600, 6, 30_000, True), (6, 10, 900_000, False)])
+def test_vote_union_v1_matches_counting_path(rng, monkeypatch, T, depth, n, shuffle):
+    """v = 1 runs the bitmap-union kernel (512 or 1024 threads, ranged or
+    32-tree-group warps, sorted or shuffled slices); its candidate lists are
+    identical, element for element, to the counting kernels' and the
+    oracle's."""
+    X = gaussian(rng, n + 24, 6)
+    Xd, Q = X[:n], X[n:]
+    index = mrpt.grow_trees(Xd, T, depth, seed=5)
+    if shuffle:
+        li = index.leaf_indices.copy()
+        for t in range(T):
+            o = index.leaf_offsets[t]
+            for j in range(len(o) - 1):
+                li[t, o[j]:o[j + 1]] = li[t, o[j]:o[j + 1]][rng.permutation(o[j + 1] - o[j])]
+        index = mrpt.MRPTIndex(dataset=mrpt.Dataset(Xd), n_trees=T, depth=depth,
+                               sparsity=index.sparsity, seed=5, fixed_count=False,
+                               matrices=index.matrices, splits=index.splits,
+                               leaf_offsets=index.leaf_offsets, leaf_indices=li,
+                               dataset_checksum=index.dataset_checksum)
+    monkeypatch.setenv("MRPT_VOTE_UNION", "1")
+    got, gc = _vote_lists(index, Q, 1)
+    monkeypatch.setenv("MRPT_VOTE_UNION", "0")
+    want, wc = _vote_lists(index, Q, 1)
+    assert np.array_equal(gc, wc)
+    for a, b in zip(got, want):
+        assert np.array_equal(a, np.sort(b))
+        assert np.all(np.diff(a) > 0)
+    monkeypatch.setenv("MRPT_VOTE_UNION", "1")
+    ref = dict(matrices=[(R.col_ptr, R.row_idx, R.values) for R in index.matrices],
+               splits=index.splits, leaf_offsets=index.leaf_offsets,
+               leaf_indices=index.leaf_indices, depth=depth)
+    ids, dists, counts = mrpt.approximate_knn_batch(Q, 10, index, 1)
+    rids, rd, rc = O.approximate_knn_batch(Xd, Q, 10, ref, 1)
+    assert np.array_equal(counts.astype(np.int64), rc)
+    assert np.array_equal(ids, rids)
+    assert dists.tobytes() == rd.tobytes()
