@@ -12,11 +12,14 @@
  *   - return an int32 status: MRPT_OK (0) or a negative MRPT_E* code; the
  *     message for the calling thread is available from mrpt_last_error();
  *   - every pointer argument is caller-owned DEVICE memory unless the comment
- *     says "host"; the library never allocates or frees caller memory;
+ *     says "host"; the library never allocates or frees caller memory (its
+ *     own scratch: small stream-ordered pool allocations, and one 32 MB
+ *     cuBLASLt workspace per device for mrpt_scan_topk_u8gemm);
  *   - work is enqueued on `stream` (a cudaStream_t, NULL = legacy default) and
  *     the call returns without synchronising; host-side argument validation
  *     fails fast before anything is enqueued;
- *   - calls are reentrant: there is no global mutable state;
+ *   - calls are reentrant; the only global state is the per-device cuBLASLt
+ *     handle and GEMM plan cache of mrpt_scan_topk_u8gemm (mutex-guarded);
  *   - leaf ids of tree t live at leaf_indices[t*n + off] (64-bit addressing,
  *     T*n reaches 1e10 at the largest configuration).
  * Status codes map onto the reference exception taxonomy
@@ -205,6 +208,35 @@ int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64_t ldx,
                           const int32_t *cand, int64_t cap,
                           const int32_t *ncand, int32_t k, int64_t *ids,
                           double *dists, void *stream);
+
+/* GEMM operands of the u8 shadow for mrpt_scan_topk_u8gemm: Xs = Xq ^ 0x80
+ * (s8, same (n, ldq) layout) and info (n x 16 bytes, 16-byte aligned): per
+ * row {scale (f32), norm (s32), radius (f32), sum of the u8 entries (s32)}. */
+int32_t mrpt_u8_gemm_rows(const void *Xq, int64_t n, int64_t ldq, const float *scale,
+                          const int32_t *norm, const float *radius, void *Xs,
+                          void *info, void *stream);
+
+/* Workspace bytes mrpt_scan_topk_u8gemm needs for nq queries (it runs
+ * queries in chunks whose dot-product matrix is <= 1 GiB). */
+int32_t mrpt_scan_topk_u8gemm_workspace_size(int64_t n, int64_t ldq, int64_t nq,
+                                             int64_t *bytes);
+
+/* mrpt_scan_topk_u8 with the filter's integer dot products for every
+ * (query, row) pair computed by one int8 tensor-core GEMM per query chunk
+ * (D = Qop . Xs^T, cuBLASLt IMMA; exact in int32).  The filter then reads 4
+ * bytes per candidate instead of a row: x.q = D + 128 sum(q) (+ 128 sum(x)
+ * - 16384 ldq for u8 queries).  Same bounds, same float64 rerank, identical
+ * results; pays when candidate sets cover a large share of the rows.
+ * workspace: 256-byte aligned, >= one query's share of
+ * mrpt_scan_topk_u8gemm_workspace_size (smaller workspaces run smaller
+ * chunks).  Falls back to mrpt_scan_topk for unsupported shapes. */
+int32_t mrpt_scan_topk_u8gemm(const float *X, int64_t n, int32_t d, int64_t ldx,
+                              const void *Xs, int64_t ldq, const void *info,
+                              const float *Q, int64_t nq, int64_t ldqq,
+                              const int32_t *cand, int64_t cap,
+                              const int32_t *ncand, int32_t k, int64_t *ids,
+                              double *dists, void *workspace, int64_t ws_bytes,
+                              void *stream);
 
 /* Sorted de-duplication of arbitrary candidate ids (np.unique,
  * search.py:157) through an n-bit bitmap.  ids outside [0, n) set

@@ -53,6 +53,47 @@ __device__ __forceinline__ bool pair_less(unsigned long long ak, int ai, unsigne
   return ak < bk || (ak == bk && ai < bi);
 }
 
+// Exact squared distance of one row, summed in coordinate order exactly as
+// the reference's float64 loop (_cy.pyx:81-97): one thread per row, but with
+// 8 float4 loads (32 coordinates) in flight ahead of each run of dependent
+// additions instead of one load round trip per coordinate.
+__device__ __forceinline__ bool aligned16_dev(const void *p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
+
+__device__ __forceinline__ double exact_dist2(const float *__restrict__ xr, const float *__restrict__ q, int d,
+                                              bool vec4) {
+  double e = 0.0;
+  int c = 0;
+  if (vec4) {
+    for (; c + 32 <= d; c += 32) {
+      float4 xv[8], qv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        xv[u] = __ldg(reinterpret_cast<const float4 *>(xr + c) + u);
+        qv[u] = __ldg(reinterpret_cast<const float4 *>(q + c) + u);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        double t;
+        t = (double)xv[u].x - (double)qv[u].x;
+        e = __dadd_rn(e, __dmul_rn(t, t));
+        t = (double)xv[u].y - (double)qv[u].y;
+        e = __dadd_rn(e, __dmul_rn(t, t));
+        t = (double)xv[u].z - (double)qv[u].z;
+        e = __dadd_rn(e, __dmul_rn(t, t));
+        t = (double)xv[u].w - (double)qv[u].w;
+        e = __dadd_rn(e, __dmul_rn(t, t));
+      }
+    }
+  }
+  for (; c < d; ++c) {
+    const double t = (double)__ldg(xr + c) - (double)__ldg(q + c);
+    e = __dadd_rn(e, __dmul_rn(t, t));
+  }
+  return e;
+}
+
 template <int R>
 __device__ __forceinline__ void dist_rows(const float *__restrict__ X, int64_t ldx, const int32_t *id,
                                           const double *qd, int d, bool vec4, double *acc) {
@@ -603,11 +644,7 @@ __global__ void __launch_bounds__(kScanNT, MINB) k_scan_topk_filter(TopkArgs a, 
       if (i < ns) {
         const int32_t id = cid[i];
         const float *xr = a.X + (int64_t)id * a.ldx;
-        double e = 0.0;
-        for (int c = 0; c < d; ++c) {
-          const double t = (double)__ldg(xr + c) - (double)__ldg(qrow + c);
-          e = __dadd_rn(e, __dmul_rn(t, t));
-        }
+        const double e = exact_dist2(xr, qrow, d, a.vec4 && aligned16_dev(qrow));
         ckey[i] = (unsigned long long)__double_as_longlong(e);
         wid[i] = id;
       } else {
@@ -935,11 +972,7 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_filter_h(TopkArgs a, d
       if (i < ns) {
         const int32_t id = sx[i];
         const float *xr = a.X + (int64_t)id * a.ldx;
-        double e = 0.0;
-        for (int c = 0; c < d; ++c) {
-          const double t = (double)__ldg(xr + c) - (double)__ldg(qrow + c);
-          e = __dadd_rn(e, __dmul_rn(t, t));
-        }
+        const double e = exact_dist2(xr, qrow, d, a.vec4 && aligned16_dev(qrow));
         ckey[i] = (unsigned long long)__double_as_longlong(e);
         cid[i] = id;
       } else {
@@ -1105,12 +1138,19 @@ __device__ int shrink_bounds2(float *ma, float *mr, float *me, int32_t *mi, int 
   return keep;
 }
 
+struct QParams;
+
 struct Q8Rows {
   const uint8_t *X;  // (n, ldq) u8
   int64_t ldq;       // multiple of 16, <= 1024
   const float *scale;
   const int32_t *norm;
   const float *radius;
+  // precomputed-dot mode (tensor-core GEMM over all rows):
+  const int32_t *D;    // (nq, ldD) s32: (x ^ 0x80) . qop for every row x
+  int64_t ldD;
+  const uint4 *info;   // per row {scale (f32), norm (s32), radius (f32), sum of u8 entries (s32)}
+  const QParams *qp;   // per query (the quantisation that produced qop)
 };
 
 template <bool QS>
@@ -1144,16 +1184,127 @@ __device__ __forceinline__ void dot_rows_u8(const uint8_t *(&rp)[U], const uint3
   }
 }
 
+// Per-query quantisation parameters of the u8 filter.
+struct QParams {
+  float sq;     // query scale (1 for integer-valued queries in [0, 255])
+  float rq;     // L2 norm of the query's quantisation error, rounded up
+  float t2f;    // sq^2 * ||qq||^2 in float32 (the filter's t2 term)
+  int qsigned;  // 1: s8 entries (the query has negatives), 0: u8
+  int qsum;     // sum of the quantised entries over ldq (pads are 0)
+  int pad;
+};
+
+template <int NW>
+struct QScratch {
+  float mn[NW], mx[NW];
+  int isint[NW];
+  double r2[NW];
+  long long nq[NW];
+  int qs[NW];
+};
+
+// Block-wide quantisation of one query row into qb (ldq/4 packed words):
+// u8 when q >= 0 (exact for integer values <= 255), else s8 with scale
+// max|q|/127.  Every thread returns the same parameters.
+template <int NT>
+__device__ __forceinline__ QParams quantize_query_u8(const float *qrow, int d, int ldq, uint32_t *qb,
+                                                     QScratch<NT / 32> &sc) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float mn = 3.4e38f, mx = 0.f;
+  int isint = 1;
+  for (int c = tid; c < d; c += NT) {
+    const float v = qrow[c];
+    mn = fminf(mn, v);
+    mx = fmaxf(mx, fabsf(v));
+    isint &= (v >= 0.f && v <= 255.f && rintf(v) == v) ? 1 : 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    isint &= __shfl_xor_sync(0xffffffffu, isint, o);
+  }
+  if (lane == 0) {
+    sc.mn[warp] = mn;
+    sc.mx[warp] = mx;
+    sc.isint[warp] = isint;
+  }
+  __syncthreads();
+  mn = sc.mn[0];
+  mx = sc.mx[0];
+  isint = sc.isint[0];
+  for (int w = 1; w < NW; ++w) {
+    mn = fminf(mn, sc.mn[w]);
+    mx = fmaxf(mx, sc.mx[w]);
+    isint &= sc.isint[w];
+  }
+  const bool qsigned = mn < 0.f;
+  const float sq = isint ? 1.f : (mx > 0.f ? mx / (qsigned ? 127.f : 255.f) : 1.f);
+  double r2 = 0.0;
+  long long nq = 0;
+  int qs = 0;
+  for (int w4 = tid; w4 < ldq / 4; w4 += NT) {
+    uint32_t packed = 0u;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int c = 4 * w4 + b;
+      const float v = c < d ? qrow[c] : 0.f;
+      float qv = rintf(v / sq);
+      qv = qsigned ? fminf(fmaxf(qv, -127.f), 127.f) : fminf(fmaxf(qv, 0.f), 255.f);
+      const int qi = (int)qv;
+      packed |= ((uint32_t)qi & 0xffu) << (8 * b);
+      const double e = (double)v - (double)sq * (double)qi;
+      r2 = fma(e, e, r2);
+      nq += (long long)qi * qi;
+      qs += qi;
+    }
+    qb[w4] = packed;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+    nq += __shfl_xor_sync(0xffffffffu, nq, o);
+    qs += __shfl_xor_sync(0xffffffffu, qs, o);
+  }
+  __syncthreads();  // everyone has read sc.mn/mx before the next query rewrites them
+  if (lane == 0) {
+    sc.r2[warp] = r2;
+    sc.nq[warp] = nq;
+    sc.qs[warp] = qs;
+  }
+  __syncthreads();
+  double r2t = 0.0;
+  long long nqt = 0;
+  int qst = 0;
+  for (int w = 0; w < NW; ++w) {
+    r2t += sc.r2[w];
+    nqt += sc.nq[w];
+    qst += sc.qs[w];
+  }
+  QParams P;
+  P.rq = r2t == 0.0 ? 0.f : __double2float_ru(__dsqrt_ru(r2t * (1.0 + 1e-12)));
+  P.sq = sq;
+  P.t2f = sq * sq * (float)nqt;
+  P.qsigned = qsigned ? 1 : 0;
+  P.qsum = qst;
+  P.pad = 0;
+  return P;
+}
+
 // G lanes per row (ldq / 16 rounded up to a power of two, <= 32); each warp
-// iteration scores (32 / G) * 4 candidates with 16-byte loads.
-template <int BUFW, int G>
+// iteration scores (32 / G) * 4 candidates with 16-byte loads.  DM: the dot
+// products come precomputed from the tensor-core GEMM (rows.D, one candidate
+// per lane, 4 bytes per candidate instead of a row); the bounds, buffer and
+// exact re-rank are the same code.
+template <int BUFW, int G, bool DM>
 __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows rows,
                                                              int32_t *fb_list, int32_t *fb_count) {
   extern __shared__ unsigned long long topk_smem[];
   constexpr int NWARP = kScanNT / 32;
-  constexpr int R = 32 / G;         // rows per load instruction
-  constexpr int U = 4;              // loads in flight per lane
-  constexpr int CPI = R * U;        // candidates per warp iteration (<= 32)
+  constexpr int R = 32 / G;             // rows per load instruction
+  constexpr int U = 4;                  // loads in flight per lane
+  constexpr int CPI = DM ? 32 : R * U;  // candidates per warp iteration (<= 32)
   uint32_t *qb = reinterpret_cast<uint32_t *>(topk_smem);             // 256 words: quantized q
   float *wa = reinterpret_cast<float *>(qb + 256);
   float *wr = wa + NWARP * BUFW;
@@ -1165,10 +1316,7 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
   float *cl = cu + NWARP * BUFW;
   __shared__ int s_wcnt[NWARP];
   __shared__ int s_bad, s_ns;
-  __shared__ float s_mn[NWARP], s_mx[NWARP];
-  __shared__ int s_int[NWARP];
-  __shared__ double s_r2[NWARP];
-  __shared__ long long s_nq[NWARP];
+  __shared__ QScratch<NWARP> qscr;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float *ma = wa + warp * BUFW;
   float *mr = wr + warp * BUFW;
@@ -1181,75 +1329,20 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
   const int grp = lane / G, gl = lane % G;
   for (int64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
     const float *qrow = a.Q + q * a.ldq;
-    // --- quantize the query: u8 if q >= 0 (exact when integer-valued <= 255), else s8
-    float mn = 3.4e38f, mx = 0.f;
-    int isint = 1;
-    for (int c = tid; c < d; c += kScanNT) {
-      const float v = qrow[c];
-      mn = fminf(mn, v);
-      mx = fmaxf(mx, fabsf(v));
-      isint &= (v >= 0.f && v <= 255.f && rintf(v) == v) ? 1 : 0;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      isint &= __shfl_xor_sync(0xffffffffu, isint, o);
-    }
-    if (lane == 0) {
-      s_mn[warp] = mn;
-      s_mx[warp] = mx;
-      s_int[warp] = isint;
-    }
     if (tid == 0) s_bad = 0;
-    __syncthreads();
-    mn = s_mn[0];
-    mx = s_mx[0];
-    isint = s_int[0];
-    for (int w = 1; w < NWARP; ++w) {
-      mn = fminf(mn, s_mn[w]);
-      mx = fmaxf(mx, s_mx[w]);
-      isint &= s_int[w];
+    QParams P;
+    if (DM) {
+      P = rows.qp[q];
+      __syncthreads();
+    } else {
+      P = quantize_query_u8<kScanNT>(qrow, d, ldq, qb, qscr);
     }
-    const bool qsigned = mn < 0.f;
-    const float sq = isint ? 1.f : (mx > 0.f ? mx / (qsigned ? 127.f : 255.f) : 1.f);
-    double r2 = 0.0;
-    long long nq = 0;
-    for (int w4 = tid; w4 < ldq / 4; w4 += kScanNT) {
-      uint32_t packed = 0u;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int c = 4 * w4 + b;
-        const float v = c < d ? qrow[c] : 0.f;
-        float qv = rintf(v / sq);
-        qv = qsigned ? fminf(fmaxf(qv, -127.f), 127.f) : fminf(fmaxf(qv, 0.f), 255.f);
-        const int qi = (int)qv;
-        packed |= ((uint32_t)qi & 0xffu) << (8 * b);
-        const double e = (double)v - (double)sq * (double)qi;
-        r2 = fma(e, e, r2);
-        nq += (long long)qi * qi;
-      }
-      qb[w4] = packed;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      r2 += __shfl_xor_sync(0xffffffffu, r2, o);
-      nq += __shfl_xor_sync(0xffffffffu, nq, o);
-    }
-    __syncthreads();  // everyone has read s_mn/s_mx before they are rewritten
-    if (lane == 0) {
-      s_r2[warp] = r2;
-      s_nq[warp] = nq;
-    }
-    __syncthreads();
-    double r2t = 0.0;
-    long long nqt = 0;
-    for (int w = 0; w < NWARP; ++w) {
-      r2t += s_r2[w];
-      nqt += s_nq[w];
-    }
-    const float rq = r2t == 0.0 ? 0.f : __double2float_ru(__dsqrt_ru(r2t * (1.0 + 1e-12)));
-    const float sqf = sq, t2f = sq * sq * (float)nqt;
+    const bool qsigned = P.qsigned != 0;
+    const float rq = P.rq;
+    const float sqf = P.sq, t2f = P.t2f;
+    // DM: x.qq = D + 128*sum(qq) (+ 128*sum(x) - 16384*ldq when the GEMM used qq - 128)
+    const int corr_q = 128 * P.qsum - (qsigned ? 0 : 16384 * ldq);
+    const int32_t *Drow = DM ? rows.D + q * rows.ldD : nullptr;
     int64_t m;
     if (a.cand) {
       const int64_t nc = a.ncand[q];
@@ -1261,7 +1354,71 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
     int cnt = 0;
     float su = __int_as_float(0x7f800000);
     bool bad = false;
+    // One candidate per lane: bound it, admit it into the warp's buffer, shrink
+    // the buffer when full; false when the buffer cannot shrink (-> fallback).
+    auto admit_lane = [&](int32_t myc, int mys, float sx, int nrm, float rad) -> bool {
+      // float32 evaluation: each of t1, t2, t3 carries <= 3 roundings and the
+      // sum two more, so |A - D| <= 8 * 2^-24 * (t1 + t2 + |t3|)
+      float A = 0.f, r = 0.f, eta = 0.f;
+      if (myc >= 0) {
+        const float t1 = sx * sx * (float)nrm;
+        const float t3 = 2.0f * sx * sqf * (float)mys;
+        A = (t1 + t2f) - t3;
+        eta = __fmul_ru(4.76837158203125e-07f, __fadd_ru(__fadd_ru(t1, t2f), fabsf(t3)));
+        r = __fadd_ru(rad, rq);
+      }
+      const bool take = myc >= 0 && admit2(A, r, eta, su);
+      const unsigned tm = __ballot_sync(0xffffffffu, take);
+      if (take) {
+        const int slot = cnt + __popc(tm & lanemask_lt());
+        ma[slot] = A;
+        mr[slot] = r;
+        me[slot] = eta;
+        mi[slot] = myc;
+      }
+      cnt += __popc(tm);
+      if (cnt > BUFW - CPI) {
+        __syncwarp();
+        cnt = shrink_bounds2<BUFW>(ma, mr, me, mi, cnt, kk, cu + warp * BUFW, cid + warp * BUFW, &su);
+        if (cnt > BUFW - CPI) return false;
+      }
+      return true;
+    };
+    if (DM) {
+      // UDM candidates per lane in flight: ids, then their dot products and row info
+      constexpr int UDM = 4;
+      for (int64_t g = (int64_t)warp * 32 * UDM; g < m && !bad; g += (int64_t)NWARP * 32 * UDM) {
+        int32_t cj[UDM];
+#pragma unroll
+        for (int u = 0; u < UDM; ++u) {
+          const int64_t j = g + u * 32 + lane;
+          cj[u] = j < m ? (qc ? __ldg(qc + j) : (int32_t)j) : -1;
+        }
+        int dv[UDM];
+        uint4 inf[UDM];
+#pragma unroll
+        for (int u = 0; u < UDM; ++u) {
+          dv[u] = 0;
+          inf[u] = make_uint4(0u, 0u, 0u, 0u);
+          if (cj[u] >= 0) {
+            dv[u] = __ldg(Drow + cj[u]);
+            inf[u] = __ldg(rows.info + cj[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UDM; ++u) {
+          const int mys = dv[u] + corr_q + (qsigned ? 0 : 128 * (int)inf[u].w);
+          if (!admit_lane(cj[u], mys, __uint_as_float(inf[u].x), (int)inf[u].y, __uint_as_float(inf[u].z))) {
+            bad = true;
+            cnt = 0;
+            break;
+          }
+        }
+      }
+    } else {
     for (int64_t g = (int64_t)warp * CPI; g < m; g += (int64_t)NWARP * CPI) {
+      int mys = 0;
+      int32_t myc = -1;
       int32_t cidv[U];
       const uint8_t *rp[U];
 #pragma unroll
@@ -1284,8 +1441,6 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
       }
       // group leader of row group grp holds candidates u*R + grp; hand candidate
       // (lane) = u*R + grp' to lane (u*R + grp') for the buffer decision
-      int mys = 0;
-      int32_t myc = -1;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int v = __shfl_sync(0xffffffffu, acc[u], ((lane - u * R) & (R - 1)) * G);
@@ -1295,36 +1450,20 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
           myc = c2;
         }
       }
-      // float32 evaluation: each of t1, t2, t3 carries <= 3 roundings and the
-      // sum two more, so |A - D| <= 8 * 2^-24 * (t1 + t2 + |t3|)
-      float A = 0.f, r = 0.f, eta = 0.f;
-      if (lane < CPI && myc >= 0) {
-        const float sx = __ldg(rows.scale + myc);
-        const float t1 = sx * sx * (float)__ldg(rows.norm + myc);
-        const float t3 = 2.0f * sx * sqf * (float)mys;
-        A = (t1 + t2f) - t3;
-        eta = __fmul_ru(4.76837158203125e-07f, __fadd_ru(__fadd_ru(t1, t2f), fabsf(t3)));
-        r = __fadd_ru(__ldg(rows.radius + myc), rq);
+      float sx = 0.f, rad = 0.f;
+      int nrm = 0;
+      if (lane >= CPI) myc = -1;
+      if (myc >= 0) {
+        sx = __ldg(rows.scale + myc);
+        nrm = __ldg(rows.norm + myc);
+        rad = __ldg(rows.radius + myc);
       }
-      const bool take = lane < CPI && myc >= 0 && admit2(A, r, eta, su);
-      const unsigned tm = __ballot_sync(0xffffffffu, take);
-      if (take) {
-        const int slot = cnt + __popc(tm & lanemask_lt());
-        ma[slot] = A;
-        mr[slot] = r;
-        me[slot] = eta;
-        mi[slot] = myc;
+      if (!admit_lane(myc, mys, sx, nrm, rad)) {
+        bad = true;
+        cnt = 0;
+        break;
       }
-      cnt += __popc(tm);
-      if (cnt > BUFW - CPI) {
-        __syncwarp();
-        cnt = shrink_bounds2<BUFW>(ma, mr, me, mi, cnt, kk, cu + warp * BUFW, cid + warp * BUFW, &su);
-        if (cnt > BUFW - CPI) {
-          bad = true;
-          cnt = 0;
-          break;
-        }
-      }
+    }
     }
     __syncwarp();
     if (lane == 0) {
@@ -1391,11 +1530,7 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
       if (i < ns) {
         const int32_t id = sx[i];
         const float *xr = a.X + (int64_t)id * a.ldx;
-        double e = 0.0;
-        for (int c = 0; c < d; ++c) {
-          const double t = (double)__ldg(xr + c) - (double)__ldg(qrow + c);
-          e = __dadd_rn(e, __dmul_rn(t, t));
-        }
+        const double e = exact_dist2(xr, qrow, d, a.vec4 && aligned16_dev(qrow));
         ckey[i] = (unsigned long long)__double_as_longlong(e);
         cid[i] = id;
       } else {
@@ -1433,6 +1568,48 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
       }
     }
     __syncthreads();
+  }
+}
+
+// GEMM operand of each query: the filter's own quantisation (u8 or s8),
+// stored as s8 (u8 entries shifted by -128, i.e. byte ^ 0x80), and its
+// parameters.  One CTA per query.
+__global__ void __launch_bounds__(kScanNT) k_quantize_q8(const float *__restrict__ Q, int64_t ldqq, int d,
+                                                         int ldq, int64_t nq, int8_t *__restrict__ qop,
+                                                         QParams *__restrict__ qp) {
+  __shared__ uint32_t qb[256];
+  __shared__ QScratch<kScanNT / 32> qscr;
+  for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
+    const QParams P = quantize_query_u8<kScanNT>(Q + q * ldqq, d, ldq, qb, qscr);
+    const uint32_t flip = P.qsigned ? 0u : 0x80808080u;
+    uint32_t *dst = reinterpret_cast<uint32_t *>(qop + q * (int64_t)ldq);
+    for (int w = threadIdx.x; w < ldq / 4; w += kScanNT) dst[w] = qb[w] ^ flip;
+    if (threadIdx.x == 0) qp[q] = P;
+    __syncthreads();  // qb is rewritten by the next query
+  }
+}
+
+// s8 copy of the u8 filter rows (byte ^ 0x80) -- the GEMM's row operand --
+// and one 16-byte record per row for the filter: {scale, norm, radius, sum of
+// the u8 entries (the GEMM's offset correction)}.  One warp per row.
+__global__ void k_u8_gemm_rows(const uint8_t *__restrict__ Xq, int64_t n, int ldq, const float *__restrict__ scale,
+                               const int32_t *__restrict__ norm, const float *__restrict__ radius,
+                               int8_t *__restrict__ Xs, uint4 *__restrict__ info) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += wstride) {
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(Xq + r * ldq);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(Xs + r * ldq);
+    int sum = 0;
+    for (int w = lane; w < ldq / 4; w += 32) {
+      const uint32_t v = src[w];
+      dst[w] = v ^ 0x80808080u;
+      sum += (int)(v & 0xffu) + (int)((v >> 8) & 0xffu) + (int)((v >> 16) & 0xffu) + (int)(v >> 24);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0)
+      info[r] = make_uint4(__float_as_uint(scale[r]), (uint32_t)norm[r], __float_as_uint(radius[r]), (uint32_t)sum);
   }
 }
 
@@ -1718,9 +1895,15 @@ extern "C" int32_t mrpt_quantize_u8(const float *X, int64_t n, int32_t d, int64_
 
 typedef void (*topk_fn_u8)(TopkArgs, Q8Rows, int32_t *, int32_t *);
 
-template <int G>
+template <int G, bool DM = false>
 static topk_fn_u8 pick_u8_b(int bufw) {
-  return bufw == 64 ? k_scan_topk_u8<64, G> : (bufw == 128 ? k_scan_topk_u8<128, G> : k_scan_topk_u8<256, G>);
+  return bufw == 64 ? k_scan_topk_u8<64, G, DM>
+                    : (bufw == 128 ? k_scan_topk_u8<128, G, DM> : k_scan_topk_u8<256, G, DM>);
+}
+
+namespace mrpt {
+int32_t igemm_rows_tn(const int8_t *Xs, int64_t n, const int8_t *Qop, int64_t m, int64_t k, int32_t *D,
+                      int64_t ldD, cudaStream_t s);
 }
 
 extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64_t ldx,
@@ -1767,6 +1950,10 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
   rows.scale = scale;
   rows.norm = norm;
   rows.radius = radius;
+  rows.D = nullptr;
+  rows.ldD = 0;
+  rows.info = nullptr;
+  rows.qp = nullptr;
   // G lanes per row: 8 for wide rows (16 candidates per warp iteration, several
   // chunk loads in flight per lane); 4 for rows of <= 256 bytes (two or more
   // chunks per lane, 32 candidates per iteration, one shuffle level less).
@@ -1808,4 +1995,136 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
   }
   cudaFreeAsync(fb, s);
   return launch_status("mrpt_scan_topk_u8");
+}
+
+extern "C" int32_t mrpt_u8_gemm_rows(const void *Xq, int64_t n, int64_t ldq, const float *scale,
+                                     const int32_t *norm, const float *radius, void *Xs, void *info,
+                                     void *stream) {
+  clear_error();
+  if (!Xq || !Xs || !info || !scale || !norm || !radius || n < 1 || ldq < 16 || ldq % 16 != 0 || ldq > 1024)
+    return fail(MRPT_ESHAPE, "mrpt_u8_gemm_rows: bad shape");
+  if (reinterpret_cast<uintptr_t>(info) & 15u) return fail(MRPT_EPARAM, "mrpt_u8_gemm_rows: info must be 16-byte aligned");
+  const int64_t blocks = ceil_div<int64_t>(n, 8);
+  const int grid = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
+  k_u8_gemm_rows<<<grid, 256, 0, as_stream(stream)>>>(reinterpret_cast<const uint8_t *>(Xq), n, (int)ldq,
+                                                       scale, norm, radius, reinterpret_cast<int8_t *>(Xs),
+                                                       reinterpret_cast<uint4 *>(info));
+  return launch_status("mrpt_u8_gemm_rows");
+}
+
+// Workspace of the GEMM filter for a chunk of mc queries: D (mc x ldD s32),
+// the query operands, their parameters and the fallback list.
+static int64_t u8gemm_bytes(int64_t n, int64_t ldq, int64_t mc, int64_t *off_qop, int64_t *off_qp,
+                            int64_t *off_fb) {
+  auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
+  const int64_t ldD = (n + 3) & ~(int64_t)3;
+  int64_t o = al(mc * ldD * 4);
+  if (off_qop) *off_qop = o;
+  o = al(o + mc * ldq);
+  if (off_qp) *off_qp = o;
+  o = al(o + mc * (int64_t)sizeof(QParams));
+  if (off_fb) *off_fb = o;
+  return al(o + (mc + 1) * 4);
+}
+
+static const int64_t kGemmChunkD = (int64_t)1 << 30;  // D bytes per query chunk
+
+extern "C" int32_t mrpt_scan_topk_u8gemm_workspace_size(int64_t n, int64_t ldq, int64_t nq, int64_t *bytes) {
+  clear_error();
+  if (n < 1 || ldq < 16 || nq < 0 || !bytes) return fail(MRPT_ESHAPE, "mrpt_scan_topk_u8gemm_workspace_size");
+  const int64_t ldD = (n + 3) & ~(int64_t)3;
+  int64_t mc = kGemmChunkD / (4 * ldD);
+  if (mc > nq) mc = nq;
+  if (mc < 1) mc = 1;
+  *bytes = u8gemm_bytes(n, ldq, mc, nullptr, nullptr, nullptr);
+  return MRPT_OK;
+}
+
+extern "C" int32_t mrpt_scan_topk_u8gemm(const float *X, int64_t n, int32_t d, int64_t ldx, const void *Xs,
+                                         int64_t ldq, const void *info, const float *Q, int64_t nq,
+                                         int64_t ldqq, const int32_t *cand, int64_t cap, const int32_t *ncand,
+                                         int32_t k, int64_t *ids, double *dists, void *workspace,
+                                         int64_t ws_bytes, void *stream) {
+  clear_error();
+  if (!Xs || !info || ldq % 16 != 0 || ldq < d || ldq > 1024 ||
+      k > 120 || k < 1 || d % 4 != 0 || ldx % 4 != 0 || !aligned16(X))
+    return mrpt_scan_topk(X, n, d, ldx, Q, nq, ldqq, cand, cap, ncand, k, ids, dists, stream);
+  if (n < 1 || n >= (int64_t)1 << 31 || d < 1 || ldx < d || ldqq < d || nq < 0)
+    return fail(MRPT_ESHAPE, "mrpt_scan_topk_u8gemm: bad shape");
+  if (cand && (cap < 1 || !ncand)) return fail(MRPT_EPARAM, "mrpt_scan_topk_u8gemm: bad candidate lists");
+  if (nq == 0) return MRPT_OK;
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255u))
+    return fail(MRPT_EWORKSPACE, "mrpt_scan_topk_u8gemm: workspace must be 256-byte aligned");
+  // largest query chunk whose workspace fits
+  const int64_t ldD = (n + 3) & ~(int64_t)3;
+  int64_t mc = ws_bytes / (4 * ldD + ldq + (int64_t)sizeof(QParams) + 4);
+  if (mc > nq) mc = nq;
+  while (mc > 0 && u8gemm_bytes(n, ldq, mc, nullptr, nullptr, nullptr) > ws_bytes) --mc;
+  if (mc < 1) return fail(MRPT_EWORKSPACE, "mrpt_scan_topk_u8gemm: workspace too small for one query");
+  int64_t off_qop, off_qp, off_fb;
+  u8gemm_bytes(n, ldq, mc, &off_qop, &off_qp, &off_fb);
+  char *w = reinterpret_cast<char *>(workspace);
+  int32_t *D = reinterpret_cast<int32_t *>(w);
+  int8_t *qop = reinterpret_cast<int8_t *>(w + off_qop);
+  QParams *qp = reinterpret_cast<QParams *>(w + off_qp);
+  int32_t *fb = reinterpret_cast<int32_t *>(w + off_fb);
+  cudaStream_t s = as_stream(stream);
+  int bufw = 64;
+  while (bufw < 2 * k + 2 * 32) bufw <<= 1;
+  if (bufw > 256) return mrpt_scan_topk(X, n, d, ldx, Q, nq, ldqq, cand, cap, ncand, k, ids, dists, stream);
+  const size_t smem = 1024 + (size_t)(kScanNT / 32) * bufw * (4 * 4 + 8 + 4 * 3);
+  topk_fn_u8 fn = pick_u8_b<8, true>(bufw);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int buf = (k + kScanNT <= 1024) ? 1024 : 2048;
+  topk_fn tfn = buf == 1024 ? k_scan_topk_tiled<1024> : k_scan_topk_tiled<2048>;
+  const size_t tsmem =
+      (size_t)buf * 12 + sizeof(float) * (kScanNT / 32) * 32 * kTileStride + sizeof(double) * (size_t)d;
+  cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+  Q8Rows rows;
+  rows.X = nullptr;
+  rows.ldq = ldq;
+  rows.scale = nullptr;
+  rows.norm = nullptr;
+  rows.radius = nullptr;
+  rows.D = D;
+  rows.ldD = ldD;
+  rows.info = reinterpret_cast<const uint4 *>(info);
+  rows.qp = qp;
+  for (int64_t q0 = 0; q0 < nq; q0 += mc) {
+    const int64_t m = nq - q0 < mc ? nq - q0 : mc;
+    const int64_t g1 = m < (int64_t)num_sms() * 8 ? m : (int64_t)num_sms() * 8;
+    k_quantize_q8<<<(unsigned)g1, kScanNT, 0, s>>>(Q + q0 * ldqq, ldqq, d, (int)ldq, m, qop, qp);
+    int32_t st = igemm_rows_tn(reinterpret_cast<const int8_t *>(Xs), n, qop, m, ldq, D, ldD, s);
+    if (st) return st;
+    TopkArgs a;
+    a.X = X;
+    a.n = n;
+    a.d = d;
+    a.ldx = ldx;
+    a.Q = Q + q0 * ldqq;
+    a.nq = m;
+    a.ldq = ldqq;
+    a.cand = cand ? cand + q0 * cap : nullptr;
+    a.cap = cap;
+    a.ncand = cand ? ncand + q0 : nullptr;
+    a.k = k;
+    a.kstride = k;
+    a.ids = ids + q0 * k;
+    a.dists = dists + q0 * k;
+    a.lb_key = nullptr;
+    a.lb_id = nullptr;
+    a.vec4 = true;
+    a.qlist = nullptr;
+    a.qcount = nullptr;
+    a.Xh = nullptr;
+    a.ldh = 0;
+    a.radius = nullptr;
+    cudaMemsetAsync(fb, 0, sizeof(int32_t), s);
+    const int64_t grid = m < (int64_t)num_sms() * 8 ? m : (int64_t)num_sms() * 8;
+    fn<<<(unsigned)grid, kScanNT, smem, s>>>(a, rows, fb + 1, fb);
+    a.qlist = fb + 1;
+    a.qcount = fb;
+    tfn<<<(unsigned)(grid < 64 ? grid : 64), kScanNT, tsmem, s>>>(a);
+  }
+  return launch_status("mrpt_scan_topk_u8gemm");
 }

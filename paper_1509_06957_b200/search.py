@@ -267,6 +267,10 @@ def _scan_variants(D, k):
     out = []
     if k <= 120 and D.u8_rows() is not None:
         out.append("u8")
+        # tensor-core dot products for every (query, row) pair: only where the
+        # dot-product matrix of a useful query chunk fits (n <= 4M rows)
+        if D.n <= (4 << 20):
+            out.append("u8gemm")
     if k <= 120 and D.shadow() is not None:
         out.append("fp16")
     out.append("fp32")
@@ -284,6 +288,13 @@ def _scan_launch(D, variant, args):
         _native.call("mrpt_scan_topk_u8", _native.ptr(D.X), D.n, D.d, int(D.X.stride(0)),
                      _native.ptr(Xq), ldr, _native.ptr(sc), _native.ptr(nm), _native.ptr(rad),
                      *common_tail)
+    elif variant == "u8gemm":
+        ldr = D.u8_rows()[1]
+        Xs, info, ws = D.u8_gemm(m)
+        _native.call("mrpt_scan_topk_u8gemm", _native.ptr(D.X), D.n, D.d, int(D.X.stride(0)),
+                     _native.ptr(Xs), ldr, _native.ptr(info), _native.ptr(qb), m, ldq,
+                     _native.ptr(cand), int(cap), _native.ptr(counts), int(k), _native.ptr(ids),
+                     _native.ptr(dists), _native.ptr(ws), int(ws.numel()), stream)
     elif variant == "fp16":
         Xh, ldh, rad = D.shadow()
         _native.call("mrpt_scan_topk_fp16", _native.ptr(D.X), D.n, D.d, int(D.X.stride(0)),

@@ -195,7 +195,7 @@ class _DeviceIndex:
         self._u8 = None
         ldq = (self.d + 15) // 16 * 16
         mode = os.environ.get("MRPT_SCAN_ROWS", "auto")
-        if mode in ("auto", "u8") and ldq <= 1024:
+        if mode in ("auto", "u8", "u8gemm") and ldq <= 1024:
             torch = _device.torch_mod()
             dev = self.X.device
             Xq = torch.empty((self.n, ldq), dtype=torch.uint8, device=dev)
@@ -210,6 +210,30 @@ class _DeviceIndex:
             if not int(flags[0].item()):
                 self._u8 = (Xq, ldq, sc, nm, rad)
         return self._u8
+
+    def u8_gemm(self, nq):
+        """(s8 rows, per-row records, workspace) for the tensor-core GEMM filter over
+        the u8 shadow; rows built once, workspace sized for nq queries (kept,
+        grown on demand).  None without a u8 shadow."""
+        u8 = self.u8_rows()
+        if u8 is None:
+            return None
+        torch = _device.torch_mod()
+        Xq, ldq = u8[0], u8[1]
+        if getattr(self, "_u8g", None) is None:
+            Xs = torch.empty_like(Xq)
+            info = torch.empty((self.n, 4), dtype=torch.int32, device=Xq.device)
+            _native.call("mrpt_u8_gemm_rows", _native.ptr(Xq), self.n, ldq, _native.ptr(u8[2]),
+                         _native.ptr(u8[3]), _native.ptr(u8[4]), _native.ptr(Xs),
+                         _native.ptr(info), _native.stream_ptr())
+            self._u8g = (Xs, info)
+            self._u8g_ws = None
+        need = ctypes.c_int64(0)
+        _native.call("mrpt_scan_topk_u8gemm_workspace_size", self.n, ldq, int(nq),
+                     ctypes.byref(need))
+        if self._u8g_ws is None or self._u8g_ws.numel() < need.value:
+            self._u8g_ws = torch.empty(need.value, dtype=torch.uint8, device=Xq.device)
+        return self._u8g[0], self._u8g[1], self._u8g_ws
 
     def vote_dir(self):
         """Tile directory for the multi-tile vote (built once, on the device),

@@ -36,7 +36,7 @@ def _data(kind, rng, n, d):
     return x.astype(np.float32)
 
 
-@pytest.mark.parametrize("variant", ["u8", "fp16", "fp32"])
+@pytest.mark.parametrize("variant", ["u8", "u8gemm", "fp16", "fp32"])
 @pytest.mark.parametrize("kind,d,k,v", [("pixels", 96, 10, 1), ("ints", 128, 10, 2),
                                          ("clusters01", 256, 10, 2), ("signed", 64, 7, 1),
                                          ("dups", 32, 20, 1), ("pixels", 200, 100, 1)])
@@ -64,3 +64,56 @@ def test_large_k_batch_multipass(rng):
     ids, dists, counts = mrpt.approximate_knn_batch(X[2700:2710], 500, index, 1)
     rids, rd, rc = _oracle(index, X[:2700], X[2700:2710], 500, 1)
     assert np.array_equal(ids, rids) and dists.tobytes() == rd.tobytes()
+
+
+@pytest.mark.parametrize("kind,signed", [("ints", False), ("pixels", True), ("clusters01", False)])
+def test_u8gemm_small_workspace_chunks(rng, kind, signed):
+    """The GEMM filter run through the C ABI with a workspace that holds only
+    a few queries (many query chunks, a ragged last one) returns exactly what
+    the dp4a filter returns, for u8 and s8 queries."""
+    import ctypes
+
+    import torch
+
+    from paper_1509_06957_b200 import _native
+    from paper_1509_06957_b200.search import query_device
+
+    n, d, nq, k = 3000, 72, 203, 9
+    X = _data(kind, rng, n + nq, d)
+    Xd, Q = X[:n], X[n:]
+    if signed:
+        Q = Q - 0.05
+    index = mrpt.grow_trees(Xd, 5, 5, seed=7)
+    D = index.device_index()
+    Qd = torch.from_numpy(np.ascontiguousarray(Q)).cuda()
+    D.scan_choice[k] = "u8"
+    want = [t.cpu().numpy() for t in query_device(D, Qd, k, 1)]
+    ldq = D.u8_rows()[1]
+    Xs, info, _ = D.u8_gemm(nq)
+    per_q = ctypes.c_int64(0)
+    _native.call("mrpt_scan_topk_u8gemm_workspace_size", n, ldq, 1, ctypes.byref(per_q))
+    ws = torch.empty(per_q.value * 11 // 2, dtype=torch.uint8, device="cuda")  # ~5 queries
+    from paper_1509_06957_b200.search import _route_device
+
+    leaves = _route_device(Qd, D)
+    cap = D.cap(1)
+    cand = torch.empty((nq, cap), dtype=torch.int32, device="cuda")
+    counts = torch.empty(nq, dtype=torch.int32, device="cuda")
+    _native.call("mrpt_vote", _native.ptr(D.indices), _native.ptr(D.offsets), D.n, D.T, D.depth,
+                 _native.ptr(leaves), nq, 1, int(D.leaves_sorted), int(D.max_count),
+                 _native.ptr(D.vote_dir()), _native.ptr(cand), int(cap), _native.ptr(counts),
+                 _native.stream_ptr())
+    ids = torch.empty((nq, k), dtype=torch.int64, device="cuda")
+    dists = torch.empty((nq, k), dtype=torch.float64, device="cuda")
+    _native.call("mrpt_scan_topk_u8gemm", _native.ptr(D.X), n, d, int(D.X.stride(0)),
+                 _native.ptr(Xs), ldq, _native.ptr(info), _native.ptr(Qd), nq, d, _native.ptr(cand),
+                 int(cap), _native.ptr(counts), k, _native.ptr(ids), _native.ptr(dists),
+                 _native.ptr(ws), int(ws.numel()), _native.stream_ptr())
+    assert np.array_equal(ids.cpu().numpy(), want[0])
+    assert dists.cpu().numpy().tobytes() == want[1].tobytes()
+    # a workspace too small for one query is refused
+    with pytest.raises(mrpt.MRPTError):
+        _native.call("mrpt_scan_topk_u8gemm", _native.ptr(D.X), n, d, int(D.X.stride(0)),
+                     _native.ptr(Xs), ldq, _native.ptr(info), _native.ptr(Qd), nq, d,
+                     _native.ptr(cand), int(cap), _native.ptr(counts), k, _native.ptr(ids),
+                     _native.ptr(dists), _native.ptr(ws), 1024, _native.stream_ptr())
