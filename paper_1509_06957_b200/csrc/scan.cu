@@ -46,7 +46,11 @@ struct TopkArgs {
   const __half *Xh;      // optional fp16 shadow of X for the filter pass (row stride ldh)
   int64_t ldh;
   const float *radius;   // per row: upper bound of ||x - fp16(x)||_2
+  int32_t *surv;         // optional (u8 filter): survivors per query, kSurvCap each, for k_rerank
+  int32_t *nsurv;        // survivors per query, -1 when the query was finished in the filter kernel
 };
+
+constexpr int kSurvCap = 64;
 
 __device__ __forceinline__ bool pair_less(unsigned long long ak, int ai, unsigned long long bk,
                                           int bi) {
@@ -1472,7 +1476,10 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
     }
     __syncthreads();
     if (s_bad) {
-      if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = (int32_t)q;
+      if (tid == 0) {
+        fb_list[atomicAdd(fb_count, 1)] = (int32_t)q;
+        if (a.surv) a.nsurv[q] = -1;
+      }
       __syncthreads();
       continue;
     }
@@ -1524,6 +1531,17 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
     }
     __syncthreads();
     const int ns = s_ns;
+    if (a.surv) {
+      // hand the survivors to k_rerank (many queries' exact distances in
+      // flight at once) unless there are too many
+      if (ns <= kSurvCap) {
+        for (int i = tid; i < ns; i += kScanNT) a.surv[q * kSurvCap + i] = sx[i];
+        if (tid == 0) a.nsurv[q] = ns;
+        __syncthreads();
+        continue;
+      }
+      if (tid == 0) a.nsurv[q] = -1;
+    }
     int np3 = 1;
     while (np3 < ns) np3 <<= 1;
     for (int i = tid; i < np3; i += kScanNT) {
@@ -1568,6 +1586,62 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
       }
     }
     __syncthreads();
+  }
+}
+
+// Exact re-rank of the survivors the u8 filter handed over (a.surv /
+// a.nsurv): one warp per query, one lane per survivor (two when > 32), each
+// lane summing its row's float64 distance in coordinate order
+// (exact_dist2); the (distance, id) order is a rank count over the warp.
+// Many queries' rows are in flight at once, instead of a few threads per
+// filter CTA waiting out one row each.
+__global__ void __launch_bounds__(256) k_rerank(TopkArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < a.nq; q += nw) {
+    const int ns = a.nsurv[q];
+    if (ns < 0) continue;
+    const float *qrow = a.Q + q * a.ldq;
+    const bool v4 = a.vec4 && aligned16_dev(qrow);
+    unsigned long long k0 = ~0ull, k1 = ~0ull;
+    int i0 = 0x7fffffff, i1 = 0x7fffffff;
+    if (lane < ns) {
+      i0 = a.surv[q * kSurvCap + lane];
+      k0 = (unsigned long long)__double_as_longlong(exact_dist2(a.X + (int64_t)i0 * a.ldx, qrow, a.d, v4));
+    }
+    if (lane + 32 < ns) {
+      i1 = a.surv[q * kSurvCap + 32 + lane];
+      k1 = (unsigned long long)__double_as_longlong(exact_dist2(a.X + (int64_t)i1 * a.ldx, qrow, a.d, v4));
+    }
+    int r0 = 0, r1 = 0;
+    for (int j = 0; j < 32; ++j) {
+      const unsigned long long kj = __shfl_sync(0xffffffffu, k0, j);
+      const int ij = __shfl_sync(0xffffffffu, i0, j);
+      r0 += pair_less(kj, ij, k0, i0) ? 1 : 0;
+      r1 += pair_less(kj, ij, k1, i1) ? 1 : 0;
+    }
+    if (ns > 32) {
+      for (int j = 0; j < 32; ++j) {
+        const unsigned long long kj = __shfl_sync(0xffffffffu, k1, j);
+        const int ij = __shfl_sync(0xffffffffu, i1, j);
+        r0 += pair_less(kj, ij, k0, i0) ? 1 : 0;
+        r1 += pair_less(kj, ij, k1, i1) ? 1 : 0;
+      }
+    }
+    int64_t *oid = a.ids + q * a.kstride;
+    double *od = a.dists + q * a.kstride;
+    if (lane < ns && r0 < a.k) {
+      oid[r0] = i0;
+      od[r0] = sqrt(__longlong_as_double((long long)k0));
+    }
+    if (lane + 32 < ns && r1 < a.k) {
+      oid[r1] = i1;
+      od[r1] = sqrt(__longlong_as_double((long long)k1));
+    }
+    for (int i = ns + lane; i < a.k; i += 32) {
+      oid[i] = -1;
+      od[i] = __longlong_as_double(0x7ff0000000000000LL);
+    }
   }
 }
 
@@ -1688,7 +1762,7 @@ extern "C" int32_t mrpt_scan_topk(const float *X, int64_t n, int32_t d, int64_t 
   if (cand && (cap < 1 || !ncand)) return fail(MRPT_EPARAM, "mrpt_scan_topk: bad candidate lists");
   if (nq == 0) return MRPT_OK;
   cudaStream_t s = as_stream(stream);
-  TopkArgs a;
+  TopkArgs a = {};
   a.X = X;
   a.n = n;
   a.d = d;
@@ -1813,7 +1887,7 @@ extern "C" int32_t mrpt_scan_topk_fp16(const float *X, int64_t n, int32_t d, int
   if (cand && (cap < 1 || !ncand)) return fail(MRPT_EPARAM, "mrpt_scan_topk_fp16: bad candidate lists");
   if (nq == 0) return MRPT_OK;
   cudaStream_t s = as_stream(stream);
-  TopkArgs a;
+  TopkArgs a = {};
   a.X = X;
   a.n = n;
   a.d = d;
@@ -1906,6 +1980,12 @@ int32_t igemm_rows_tn(const int8_t *Xs, int64_t n, const int8_t *Qop, int64_t m,
                       int64_t ldD, cudaStream_t s);
 }
 
+static void launch_rerank(const TopkArgs &a, cudaStream_t s) {
+  const int64_t blocks = ceil_div<int64_t>(a.nq, 8);
+  const int64_t cap = (int64_t)num_sms() * 16;
+  k_rerank<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, s>>>(a);
+}
+
 extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64_t ldx,
                                      const void *Xq, int64_t ldq, const float *scale,
                                      const int32_t *norm, const float *radius, const float *Q,
@@ -1921,7 +2001,7 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
   if (cand && (cap < 1 || !ncand)) return fail(MRPT_EPARAM, "mrpt_scan_topk_u8: bad candidate lists");
   if (nq == 0) return MRPT_OK;
   cudaStream_t s = as_stream(stream);
-  TopkArgs a;
+  TopkArgs a = {};
   a.X = X;
   a.n = n;
   a.d = d;
@@ -1944,6 +2024,8 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
   a.Xh = nullptr;
   a.ldh = 0;
   a.radius = nullptr;
+  a.surv = nullptr;
+  a.nsurv = nullptr;
   Q8Rows rows;
   rows.X = reinterpret_cast<const uint8_t *>(Xq);
   rows.ldq = ldq;
@@ -1972,9 +2054,12 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
   const size_t smem = 1024 + (size_t)(kScanNT / 32) * bufw * (4 * 4 + 8 + 4 * 3);
   int32_t *fb = nullptr;
   keep_pool_warm();
-  if (cudaMallocAsync((void **)&fb, sizeof(int32_t) * (nq + 1), s) != cudaSuccess)
+  // scratch: fallback count + list, survivor counts, survivor lists
+  if (cudaMallocAsync((void **)&fb, sizeof(int32_t) * ((nq + 1) + nq * (kSurvCap + 1)), s) != cudaSuccess)
     return fail(MRPT_ECUDA, "mrpt_scan_topk_u8: scratch allocation failed");
   cudaMemsetAsync(fb, 0, sizeof(int32_t), s);
+  a.nsurv = fb + 1 + nq;
+  a.surv = a.nsurv + nq;
   topk_fn_u8 fn = G == 32 ? pick_u8_b<32>(bufw)
                   : (G == 16 ? pick_u8_b<16>(bufw) : (G == 8 ? pick_u8_b<8>(bufw) : pick_u8_b<4>(bufw)));
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1993,6 +2078,7 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
     cudaFreeAsync(fb, s);
     return fail(MRPT_EPARAM, "mrpt_scan_topk_u8: exact fallback needs 16-byte rows");
   }
+  launch_rerank(a, s);
   cudaFreeAsync(fb, s);
   return launch_status("mrpt_scan_topk_u8");
 }
@@ -2023,8 +2109,8 @@ static int64_t u8gemm_bytes(int64_t n, int64_t ldq, int64_t mc, int64_t *off_qop
   o = al(o + mc * ldq);
   if (off_qp) *off_qp = o;
   o = al(o + mc * (int64_t)sizeof(QParams));
-  if (off_fb) *off_fb = o;
-  return al(o + (mc + 1) * 4);
+  if (off_fb) *off_fb = o;  // fallback count + list, survivor counts, survivor lists
+  return al(o + ((mc + 1) + mc * (kSurvCap + 1)) * 4);
 }
 
 static const int64_t kGemmChunkD = (int64_t)1 << 30;  // D bytes per query chunk
@@ -2057,7 +2143,7 @@ extern "C" int32_t mrpt_scan_topk_u8gemm(const float *X, int64_t n, int32_t d, i
     return fail(MRPT_EWORKSPACE, "mrpt_scan_topk_u8gemm: workspace must be 256-byte aligned");
   // largest query chunk whose workspace fits
   const int64_t ldD = (n + 3) & ~(int64_t)3;
-  int64_t mc = ws_bytes / (4 * ldD + ldq + (int64_t)sizeof(QParams) + 4);
+  int64_t mc = ws_bytes / (4 * ldD + ldq + (int64_t)sizeof(QParams) + 4 * (kSurvCap + 2));
   if (mc > nq) mc = nq;
   while (mc > 0 && u8gemm_bytes(n, ldq, mc, nullptr, nullptr, nullptr) > ws_bytes) --mc;
   if (mc < 1) return fail(MRPT_EWORKSPACE, "mrpt_scan_topk_u8gemm: workspace too small for one query");
@@ -2096,7 +2182,7 @@ extern "C" int32_t mrpt_scan_topk_u8gemm(const float *X, int64_t n, int32_t d, i
     k_quantize_q8<<<(unsigned)g1, kScanNT, 0, s>>>(Q + q0 * ldqq, ldqq, d, (int)ldq, m, qop, qp);
     int32_t st = igemm_rows_tn(reinterpret_cast<const int8_t *>(Xs), n, qop, m, ldq, D, ldD, s);
     if (st) return st;
-    TopkArgs a;
+    TopkArgs a = {};
     a.X = X;
     a.n = n;
     a.d = d;
@@ -2119,12 +2205,15 @@ extern "C" int32_t mrpt_scan_topk_u8gemm(const float *X, int64_t n, int32_t d, i
     a.Xh = nullptr;
     a.ldh = 0;
     a.radius = nullptr;
+    a.nsurv = fb + 1 + mc;
+    a.surv = a.nsurv + mc;
     cudaMemsetAsync(fb, 0, sizeof(int32_t), s);
     const int64_t grid = m < (int64_t)num_sms() * 8 ? m : (int64_t)num_sms() * 8;
     fn<<<(unsigned)grid, kScanNT, smem, s>>>(a, rows, fb + 1, fb);
     a.qlist = fb + 1;
     a.qcount = fb;
     tfn<<<(unsigned)(grid < 64 ? grid : 64), kScanNT, tsmem, s>>>(a);
+    launch_rerank(a, s);
   }
   return launch_status("mrpt_scan_topk_u8gemm");
 }
