@@ -24,6 +24,18 @@ def is_tensor(x):
     return isinstance(x, torch.Tensor)
 
 
+_SIDE = {}
+
+
+def side_streams():
+    """Two CUDA streams per device (upload, download) for overlapped batches."""
+    torch = torch_mod()
+    dev = torch.cuda.current_device()
+    if dev not in _SIDE:
+        _SIDE[dev] = (torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev))
+    return _SIDE[dev]
+
+
 def h2d(arr, dtype=None):
     """Copy a host array to the current device (pinned staging for big arrays)."""
     torch = torch_mod()

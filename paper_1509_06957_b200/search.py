@@ -343,6 +343,14 @@ def approximate_knn_batch(Q, k, index, votes, chunk=None):
     _check_batch_args(k, index, votes)
     on_device = _device.is_tensor(Q) and Q.is_cuda
     torch = _device.torch_mod()
+    if not on_device and chunk is None:
+        Qc = Q if _device.is_tensor(Q) else None
+        if Qc is None:
+            Qh = np.asarray(Q)
+            if Qh.ndim == 2 and Qh.shape[1] == index.d and Qh.shape[0] >= 2 * _PIPE_MIN:
+                Qc = torch.from_numpy(np.ascontiguousarray(Qh, dtype=np.float32))
+        if Qc is not None and Qc.dim() == 2 and Qc.shape[1] == index.d and Qc.shape[0] >= 2 * _PIPE_MIN:
+            return _knn_batch_pipelined(Qc, k, index, votes)
     if _device.is_tensor(Q):
         if Q.dim() != 2 or Q.shape[1] != index.d:
             raise ShapeError(f"queries must be (nq, {index.d}), got {tuple(Q.shape)}")
@@ -365,6 +373,53 @@ def approximate_knn_batch(Q, k, index, votes, chunk=None):
     if on_device:
         return ids, dists, counts
     return _device.d2h(ids), _device.d2h(dists), _device.d2h(counts)
+
+
+_PIPE_MIN = 2048  # queries per pipelined piece (at least)
+
+
+def _knn_batch_pipelined(Qc, k, index, votes):
+    """Host queries in, host results out, with the transfers overlapped: the
+    batch is cut into up to 4 pieces; piece i's upload (copy stream), its
+    route/vote/scan (compute stream, after the upload's event) and its
+    results' download into pinned host memory (a third stream, after the
+    compute event) are enqueued in that order, so uploads of later pieces and
+    downloads of earlier ones run under the compute of the others.  Results
+    are identical to the unpipelined path."""
+    torch = _device.torch_mod()
+    D = index.device_index()
+    nq = int(Qc.shape[0])
+    Qc = Qc.to(dtype=torch.float32).contiguous()
+    _record_macs(nq * sum(R.nnz for R in index.matrices))
+    pieces = max(1, min(4, nq // _PIPE_MIN))
+    bounds = [nq * i // pieces for i in range(pieces + 1)]
+    dev = _device.device()
+    Qd = torch.empty((nq, index.d), dtype=torch.float32, device=dev)
+    ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
+    dists = torch.empty((nq, k), dtype=torch.float64, device=dev)
+    counts = torch.empty(nq, dtype=torch.int32, device=dev)
+    hid = torch.empty((nq, k), dtype=torch.int64, pin_memory=True)
+    hdist = torch.empty((nq, k), dtype=torch.float64, pin_memory=True)
+    hcnt = torch.empty(nq, dtype=torch.int32, pin_memory=True)
+    compute = torch.cuda.current_stream()
+    up, down = _device.side_streams()
+    for i in range(pieces):
+        s, e = bounds[i], bounds[i + 1]
+        with torch.cuda.stream(up):
+            Qd[s:e].copy_(Qc[s:e], non_blocking=True)
+            ev_up = torch.cuda.Event()
+            ev_up.record(up)
+        compute.wait_event(ev_up)
+        query_device(D, Qd[s:e], k, votes, out=(ids[s:e], dists[s:e], counts[s:e]))
+        ev_done = torch.cuda.Event()
+        ev_done.record(compute)
+        with torch.cuda.stream(down):
+            down.wait_event(ev_done)
+            hid[s:e].copy_(ids[s:e], non_blocking=True)
+            hdist[s:e].copy_(dists[s:e], non_blocking=True)
+            hcnt[s:e].copy_(counts[s:e], non_blocking=True)
+    down.synchronize()  # after every piece's compute and upload, too
+    return hid.numpy(), hdist.numpy(), hcnt.numpy()
 
 
 def approximate_knn(q, k, index, votes):

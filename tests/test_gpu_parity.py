@@ -297,3 +297,30 @@ def test_vote_union_v1_matches_counting_path(rng, monkeypatch, T, depth, n, shuf
     assert np.array_equal(counts.astype(np.int64), rc)
     assert np.array_equal(ids, rids)
     assert dists.tobytes() == rd.tobytes()
+
+
+def test_pipelined_host_batch_matches(rng):
+    """Large host batches take the overlapped upload/compute/download path
+    (numpy, pinned and pageable tensors); results equal the one-shot device
+    path and the oracle."""
+    import torch
+
+    n, d = 20_000, 16
+    X = gaussian(rng, n + 9000, d)
+    Xd, Q = X[:n], X[n:]
+    index = mrpt.grow_trees(Xd, 8, 6, seed=12)
+    want = mrpt.approximate_knn_batch(Q, 6, index, 2, chunk=len(Q))  # unpipelined
+    got_np = mrpt.approximate_knn_batch(Q, 6, index, 2)
+    got_pin = mrpt.approximate_knn_batch(torch.from_numpy(Q).pin_memory(), 6, index, 2)
+    got_page = mrpt.approximate_knn_batch(torch.from_numpy(Q.copy()), 6, index, 2)
+    for got in (got_np, got_pin, got_page):
+        for a, b in zip(got, want):
+            assert isinstance(a, np.ndarray)
+            assert np.array_equal(a, b)
+    ref = dict(matrices=[(R.col_ptr, R.row_idx, R.values) for R in index.matrices],
+               splits=index.splits, leaf_offsets=index.leaf_offsets,
+               leaf_indices=index.leaf_indices, depth=6)
+    rids, rd, rc = O.approximate_knn_batch(Xd, Q[:60], 6, ref, 2)
+    assert np.array_equal(got_np[0][:60], rids)
+    assert got_np[1][:60].tobytes() == rd.tobytes()
+    assert np.array_equal(got_np[2][:60].astype(np.int64), rc)
