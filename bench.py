@@ -334,14 +334,20 @@ def run_ours(args):
     # bytes the chosen filter variant actually reads per candidate (its row
     # format + per-row side data + the candidate id); survivors reranked in fp32
     # are not included
-    variant = D.scan_choice.get(k, "fp32")
-    if variant == "u8":
+    variant = D.scan_choice.get((k, v), "fp32")
+    if variant.startswith("u8gemm"):
+        # per candidate: its dot product (4 B) + row record (16 B) (+ its id in
+        # list mode); per query: the GEMM's n dot products written and read
+        row_b, filt_mb = 16 if variant == "u8gemm_bits" else 20, D.n * D.u8_rows()[1] / 1e6
+    elif variant == "u8":
         row_b, filt_mb = D.u8_rows()[1] + 12, D.n * D.u8_rows()[1] / 1e6
     elif variant == "fp16":
         row_b, filt_mb = 2 * D.shadow()[1] + 4, D.n * 2 * D.shadow()[1] / 1e6
     else:
         row_b, filt_mb = 4 * p["d"], X.nbytes / 1e6
     filter_bytes = float(cand.sum().item()) * (row_b + 4)
+    if variant.startswith("u8gemm"):
+        filter_bytes += 8.0 * D.n * p["nq"]
     filter_gbs = filter_bytes / (stage_ms["scan_topk"] / steps / 1000.0) / 1e9
     stage_gbs = (vote_bytes + scan_bytes) / ((stage_ms["vote"] + stage_ms["scan_topk"]) / steps / 1000.0) / 1e9
 

@@ -120,6 +120,16 @@ int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_offsets,
                   int64_t max_count, const uint16_t *dir, int32_t *cand,
                   int64_t cap, int32_t *ncand, void *stream);
 
+/* mrpt_vote with the candidates returned as bitmaps instead of lists:
+ * bits (nq, bstride) uint32, bit i of query q set iff point i has >= v votes
+ * (bstride >= ceil(n/32)); ncand[q] = number of set bits.  No ordered
+ * compaction: pays when candidate sets are a sizeable share of the points. */
+int32_t mrpt_vote_bitmap(const int32_t *leaf_indices, const int64_t *leaf_offsets,
+                         int64_t n, int32_t T, int32_t depth, const int32_t *leaves,
+                         int64_t nq, int32_t v, int32_t leaves_sorted,
+                         int64_t max_count, const uint16_t *dir, uint32_t *bits,
+                         int64_t bstride, int32_t *ncand, void *stream);
+
 /* Vote geometry: number of id tiles the vote sweeps for this index shape and
  * the uint16 entries of its tile directory (0 when one tile suffices).
  * The directory (optional `dir` of mrpt_vote, built once per index by
@@ -237,6 +247,16 @@ int32_t mrpt_scan_topk_u8gemm(const float *X, int64_t n, int32_t d, int64_t ldx,
                               const int32_t *ncand, int32_t k, int64_t *ids,
                               double *dists, void *workspace, int64_t ws_bytes,
                               void *stream);
+
+/* mrpt_scan_topk_u8gemm over candidate bitmaps (mrpt_vote_bitmap) instead of
+ * lists: each warp walks its query's bitmap words, reading the dot products
+ * of a word's 32 ids in one coalesced access.  k <= 96.  Same results. */
+int32_t mrpt_scan_topk_u8gemm_bits(const float *X, int64_t n, int32_t d, int64_t ldx,
+                                   const void *Xs, int64_t ldq, const void *info,
+                                   const float *Q, int64_t nq, int64_t ldqq,
+                                   const uint32_t *cbits, int64_t bstride, int32_t k,
+                                   int64_t *ids, double *dists, void *workspace,
+                                   int64_t ws_bytes, void *stream);
 
 /* Sorted de-duplication of arbitrary candidate ids (np.unique,
  * search.py:157) through an n-bit bitmap.  ids outside [0, n) set

@@ -48,6 +48,8 @@ struct TopkArgs {
   const float *radius;   // per row: upper bound of ||x - fp16(x)||_2
   int32_t *surv;         // optional (u8 filter): survivors per query, kSurvCap each, for k_rerank
   int32_t *nsurv;        // survivors per query, -1 when the query was finished in the filter kernel
+  const uint32_t *cbits; // optional: candidate bitmaps (nq, bstride words) instead of cand lists
+  int64_t bstride;
 };
 
 constexpr int kSurvCap = 64;
@@ -301,9 +303,10 @@ __global__ void __launch_bounds__(kScanNT, 3) k_scan_topk_tiled(TopkArgs a) {
       m = a.n;
     }
     const int32_t *qc = a.cand ? a.cand + q * a.cap : nullptr;
+    const uint32_t *qbits = a.cbits ? a.cbits + q * a.bstride : nullptr;
     for (int64_t base = 0; base < m; base += kScanNT) {
       const int64_t j = base + warp * 32 + lane;
-      const bool valid = j < m;
+      const bool valid = j < m && (!qbits || ((__ldg(qbits + (j >> 5)) >> (j & 31)) & 1u));
       const int32_t myid = valid ? (qc ? qc[j] : (int32_t)j) : 0;
       // row ids of the 8 rows this lane loads (rows rsub + 4i of the group)
       int32_t rid[8];
@@ -1155,6 +1158,8 @@ struct Q8Rows {
   int64_t ldD;
   const uint4 *info;   // per row {scale (f32), norm (s32), radius (f32), sum of u8 entries (s32)}
   const QParams *qp;   // per query (the quantisation that produced qop)
+  const uint32_t *cbits;  // optional: candidate bitmaps (nq, bstride words) instead of lists
+  int64_t bstride;
 };
 
 template <bool QS>
@@ -1388,7 +1393,72 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
       }
       return true;
     };
-    if (DM) {
+    if (DM && rows.cbits) {
+      // candidate bitmap: each lane loads one of 32 consecutive words; the
+      // warp's set bits are then dealt out 32 per batch (lane r takes the
+      // r-th set bit: binary search over the words' prefix counts, then a
+      // popcount select inside the word), so every admission round is full
+      constexpr int UB = 2;
+      const uint32_t *qbits = rows.cbits + q * rows.bstride;
+      const int nwords = (int)((a.n + 31) >> 5);
+      for (int w0 = warp * 32; w0 < nwords && !bad; w0 += NWARP * 32) {
+        const uint32_t word = w0 + lane < nwords ? __ldg(qbits + w0 + lane) : 0u;
+        const int pc = __popc(word);
+        int incl = pc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += u;
+        }
+        const int excl = incl - pc;
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        for (int b0 = 0; b0 < total && !bad; b0 += 32 * UB) {
+          int32_t cj[UB];
+          int dv[UB];
+          uint4 inf[UB];
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            const int r = b0 + 32 * u + lane;
+            int src = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+              const int e = __shfl_sync(0xffffffffu, excl, src + step);
+              if (e <= r) src += step;
+            }
+            int rr = r - __shfl_sync(0xffffffffu, excl, src);
+            uint32_t wd = __shfl_sync(0xffffffffu, word, src);
+            int bit = 0;
+#pragma unroll
+            for (int half = 16; half > 0; half >>= 1) {
+              const int c = __popc(wd & ((1u << half) - 1u));
+              if (rr >= c) {
+                rr -= c;
+                wd >>= half;
+                bit += half;
+              }
+            }
+            cj[u] = -1;
+            dv[u] = 0;
+            inf[u] = make_uint4(0u, 0u, 0u, 0u);
+            if (r < total) {
+              cj[u] = (w0 + src) * 32 + bit;
+              dv[u] = __ldg(Drow + cj[u]);
+              inf[u] = __ldg(rows.info + cj[u]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            if (b0 + 32 * u >= total) break;  // warp-uniform
+            const int mys = dv[u] + corr_q + (qsigned ? 0 : 128 * (int)inf[u].w);
+            if (!admit_lane(cj[u], mys, __uint_as_float(inf[u].x), (int)inf[u].y, __uint_as_float(inf[u].z))) {
+              bad = true;
+              cnt = 0;
+              break;
+            }
+          }
+        }
+      }
+    } else if (DM) {
       // UDM candidates per lane in flight: ids, then their dot products and row info
       constexpr int UDM = 4;
       for (int64_t g = (int64_t)warp * 32 * UDM; g < m && !bad; g += (int64_t)NWARP * 32 * UDM) {
@@ -2036,6 +2106,8 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
   rows.ldD = 0;
   rows.info = nullptr;
   rows.qp = nullptr;
+  rows.cbits = nullptr;
+  rows.bstride = 0;
   // G lanes per row: 8 for wide rows (16 candidates per warp iteration, several
   // chunk loads in flight per lane); 4 for rows of <= 256 bytes (two or more
   // chunks per lane, 32 candidates per iteration, one shuffle level less).
@@ -2126,12 +2198,15 @@ extern "C" int32_t mrpt_scan_topk_u8gemm_workspace_size(int64_t n, int64_t ldq, 
   return MRPT_OK;
 }
 
-extern "C" int32_t mrpt_scan_topk_u8gemm(const float *X, int64_t n, int32_t d, int64_t ldx, const void *Xs,
-                                         int64_t ldq, const void *info, const float *Q, int64_t nq,
-                                         int64_t ldqq, const int32_t *cand, int64_t cap, const int32_t *ncand,
-                                         int32_t k, int64_t *ids, double *dists, void *workspace,
-                                         int64_t ws_bytes, void *stream) {
-  clear_error();
+static int32_t u8gemm_impl(const float *X, int64_t n, int32_t d, int64_t ldx, const void *Xs, int64_t ldq,
+                           const void *info, const float *Q, int64_t nq, int64_t ldqq, const int32_t *cand,
+                           int64_t cap, const int32_t *ncand, const uint32_t *cbits, int64_t bstride, int32_t k,
+                           int64_t *ids, double *dists, void *workspace, int64_t ws_bytes, void *stream) {
+  if (cbits && (bstride < (n + 31) / 32 || cand))
+    return fail(MRPT_EPARAM, "mrpt_scan_topk_u8gemm_bits: bad candidate bitmaps");
+  if (cbits && (!Xs || !info || ldq % 16 != 0 || ldq < d || ldq > 1024 || k > 96 || k < 1 || d % 4 != 0 ||
+                ldx % 4 != 0 || !aligned16(X)))
+    return fail(MRPT_EPARAM, "mrpt_scan_topk_u8gemm_bits: unsupported shape");
   if (!Xs || !info || ldq % 16 != 0 || ldq < d || ldq > 1024 ||
       k > 120 || k < 1 || d % 4 != 0 || ldx % 4 != 0 || !aligned16(X))
     return mrpt_scan_topk(X, n, d, ldx, Q, nq, ldqq, cand, cap, ncand, k, ids, dists, stream);
@@ -2176,6 +2251,8 @@ extern "C" int32_t mrpt_scan_topk_u8gemm(const float *X, int64_t n, int32_t d, i
   rows.ldD = ldD;
   rows.info = reinterpret_cast<const uint4 *>(info);
   rows.qp = qp;
+  rows.cbits = nullptr;
+  rows.bstride = 0;
   for (int64_t q0 = 0; q0 < nq; q0 += mc) {
     const int64_t m = nq - q0 < mc ? nq - q0 : mc;
     const int64_t g1 = m < (int64_t)num_sms() * 8 ? m : (int64_t)num_sms() * 8;
@@ -2193,6 +2270,10 @@ extern "C" int32_t mrpt_scan_topk_u8gemm(const float *X, int64_t n, int32_t d, i
     a.cand = cand ? cand + q0 * cap : nullptr;
     a.cap = cap;
     a.ncand = cand ? ncand + q0 : nullptr;
+    a.cbits = cbits ? cbits + q0 * bstride : nullptr;
+    a.bstride = bstride;
+    rows.cbits = a.cbits;
+    rows.bstride = bstride;
     a.k = k;
     a.kstride = k;
     a.ids = ids + q0 * k;
@@ -2216,4 +2297,25 @@ extern "C" int32_t mrpt_scan_topk_u8gemm(const float *X, int64_t n, int32_t d, i
     launch_rerank(a, s);
   }
   return launch_status("mrpt_scan_topk_u8gemm");
+}
+
+extern "C" int32_t mrpt_scan_topk_u8gemm(const float *X, int64_t n, int32_t d, int64_t ldx, const void *Xs,
+                                         int64_t ldq, const void *info, const float *Q, int64_t nq,
+                                         int64_t ldqq, const int32_t *cand, int64_t cap, const int32_t *ncand,
+                                         int32_t k, int64_t *ids, double *dists, void *workspace,
+                                         int64_t ws_bytes, void *stream) {
+  clear_error();
+  return u8gemm_impl(X, n, d, ldx, Xs, ldq, info, Q, nq, ldqq, cand, cap, ncand, nullptr, 0, k, ids, dists,
+                     workspace, ws_bytes, stream);
+}
+
+extern "C" int32_t mrpt_scan_topk_u8gemm_bits(const float *X, int64_t n, int32_t d, int64_t ldx,
+                                              const void *Xs, int64_t ldq, const void *info, const float *Q,
+                                              int64_t nq, int64_t ldqq, const uint32_t *cbits, int64_t bstride,
+                                              int32_t k, int64_t *ids, double *dists, void *workspace,
+                                              int64_t ws_bytes, void *stream) {
+  clear_error();
+  if (!cbits) return fail(MRPT_EPARAM, "mrpt_scan_topk_u8gemm_bits: cbits is NULL");
+  return u8gemm_impl(X, n, d, ldx, Xs, ldq, info, Q, nq, ldqq, nullptr, 0, nullptr, cbits, bstride, k, ids,
+                     dists, workspace, ws_bytes, stream);
 }

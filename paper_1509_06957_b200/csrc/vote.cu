@@ -36,6 +36,8 @@ struct VoteArgs {
   const int32_t *qlist;  // optional: only these queries (count *qcount)
   const int32_t *qcount;
   const uint16_t *dir;   // optional tile directory (T, 2^depth, ntiles+1)
+  uint32_t *bits_out;    // optional: candidate bitmap per query instead of lists
+  int64_t bstride;       // words per query in bits_out
 };
 
 constexpr int kVoteNT = 1024;
@@ -116,6 +118,29 @@ __device__ __forceinline__ int64_t emit_bitmap(uint32_t *bits, int nwords, int32
   return base;
 }
 
+// Bitmap output: copy the tile's "reached v" words to dst (coalesced),
+// clearing them; returns their popcount (block-uniform).
+template <int NT = kVoteNT>
+__device__ __forceinline__ int64_t store_bits(uint32_t *bits, int nwords, uint32_t *dst, int *wsum) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = NT / 32;
+  int c = 0;
+  for (int i = threadIdx.x; i < nwords; i += NT) {
+    const uint32_t w = bits[i];
+    dst[i] = w;
+    if (w) bits[i] = 0u;
+    c += __popc(w);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) wsum[warp] = c;
+  __syncthreads();
+  int64_t tot = 0;
+  for (int w = 0; w < NW; ++w) tot += wsum[w];
+  __syncthreads();
+  return tot;
+}
+
 template <int CW, int G, bool SORTED>
 __global__ void __launch_bounds__(kVoteNT, 1) k_vote(VoteArgs a) {
   extern __shared__ uint4 vote_smem[];
@@ -189,7 +214,10 @@ __global__ void __launch_bounds__(kVoteNT, 1) k_vote(VoteArgs a) {
         }
       }
       __syncthreads();
-      ncand = emit_bitmap(bits, (int)((hi - lo + 31) >> 5), lo, qcand, ncand, a.cap, wsum);
+      if (a.bits_out)
+        ncand += store_bits(bits, (int)((hi - lo + 31) >> 5), a.bits_out + q * a.bstride + (lo >> 5), wsum);
+      else
+        ncand = emit_bitmap(bits, (int)((hi - lo + 31) >> 5), lo, qcand, ncand, a.cap, wsum);
       if (tile + 1 < a.ntiles) {
         for (int i = tid; i < cwords / 4; i += kVoteNT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
@@ -360,7 +388,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_vote_dir(VoteArgs a) {
       }
       __syncthreads();
       const int nw = s_nw;
-      if (nw > kWList) {  // too many words to list: ordered scan of the whole bitmap
+      if (a.bits_out) {
+        const int64_t hi = (int64_t)lo + a.W < a.n ? (int64_t)lo + a.W : a.n;
+        ncand += store_bits<NT>(bits, (int)((hi - lo + 31) >> 5), a.bits_out + q * a.bstride + (lo >> 5), wsum);
+      } else if (nw > kWList) {  // too many words to list: ordered scan of the whole bitmap
         const int64_t hi = (int64_t)lo + a.W < a.n ? (int64_t)lo + a.W : a.n;
         ncand = emit_bitmap<NT>(bits, (int)((hi - lo + 31) >> 5), lo, qcand, ncand, a.cap, wsum);
       } else {
@@ -544,7 +575,9 @@ __global__ void __launch_bounds__(NT, 1) k_vote_union(VoteArgs a, int G) {
       }
     }
     __syncthreads();
-    const int64_t nc = emit_bitmap_staged<NT>(vote_smem, nwords4, a.cand + q * a.cap, a.cap, wsum, my_stage);
+    const int64_t nc = a.bits_out
+        ? store_bits<NT>(bits, (int)((a.n + 31) >> 5), a.bits_out + q * a.bstride, wsum)
+        : emit_bitmap_staged<NT>(vote_smem, nwords4, a.cand + q * a.cap, a.cap, wsum, my_stage);
     if (tid == 0) a.ncand[q] = (int32_t)nc;  // > cap means only cap ids were stored
   }
 }
@@ -735,15 +768,15 @@ extern "C" int32_t mrpt_vote_build_dir(const int32_t *leaf_indices, const int64_
   return launch_status("mrpt_vote_build_dir");
 }
 
-extern "C" int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_offsets, int64_t n,
-                             int32_t T, int32_t depth, const int32_t *leaves, int64_t nq, int32_t v,
-                             int32_t leaves_sorted, int64_t max_count, const uint16_t *dir,
-                             int32_t *cand, int64_t cap, int32_t *ncand, void *stream) {
-  clear_error();
+static int32_t vote_impl(const int32_t *leaf_indices, const int64_t *leaf_offsets, int64_t n, int32_t T,
+                         int32_t depth, const int32_t *leaves, int64_t nq, int32_t v, int32_t leaves_sorted,
+                         int64_t max_count, const uint16_t *dir, int32_t *cand, int64_t cap,
+                         uint32_t *bits_out, int64_t bstride, int32_t *ncand, void *stream) {
   if (n < 1 || n >= (int64_t)1 << 31 || T < 1 || depth < 0 || depth > 30 || nq < 0)
     return fail(MRPT_ESHAPE, "mrpt_vote: bad shape");
   if (v < 1 || v > max_count) return fail(MRPT_EPARAM, "mrpt_vote: vote threshold out of range");
-  if (cap < 1) return fail(MRPT_EPARAM, "mrpt_vote: cap must be >= 1");
+  if (!bits_out && cap < 1) return fail(MRPT_EPARAM, "mrpt_vote: cap must be >= 1");
+  if (bits_out && bstride < (n + 31) / 32) return fail(MRPT_EPARAM, "mrpt_vote_bitmap: bstride < ceil(n/32)");
   if (nq == 0) return MRPT_OK;
   cudaStream_t s = as_stream(stream);
   int CW, ntiles;
@@ -757,7 +790,7 @@ extern "C" int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_of
   int G = 1;
   while (G < 32 && G * kVoteU < per_tile) G <<= 1;
   if (const char *env = getenv("MRPT_VOTE_G")) G = atoi(env);  // experiments
-  VoteArgs a;
+  VoteArgs a = {};
   a.leaf_indices = leaf_indices;
   a.leaf_offsets = leaf_offsets;
   a.n = n;
@@ -774,6 +807,8 @@ extern "C" int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_of
   a.qlist = nullptr;
   a.qcount = nullptr;
   a.dir = dir;
+  a.bits_out = bits_out;
+  a.bstride = bstride;
   const size_t smem = vote_smem_bytes(CW, W, T);
   const int64_t grid = nq < (int64_t)num_sms() * 4 ? nq : (int64_t)num_sms() * 4;
   // v == 1: bitmap + per-warp staging + slice table
@@ -820,6 +855,25 @@ extern "C" int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_of
     fn<<<(unsigned)grid, kVoteNT, smem, s>>>(a);
   }
   return launch_status("mrpt_vote");
+}
+
+extern "C" int32_t mrpt_vote(const int32_t *leaf_indices, const int64_t *leaf_offsets, int64_t n,
+                             int32_t T, int32_t depth, const int32_t *leaves, int64_t nq, int32_t v,
+                             int32_t leaves_sorted, int64_t max_count, const uint16_t *dir,
+                             int32_t *cand, int64_t cap, int32_t *ncand, void *stream) {
+  clear_error();
+  return vote_impl(leaf_indices, leaf_offsets, n, T, depth, leaves, nq, v, leaves_sorted, max_count, dir, cand,
+                   cap, nullptr, 0, ncand, stream);
+}
+
+extern "C" int32_t mrpt_vote_bitmap(const int32_t *leaf_indices, const int64_t *leaf_offsets, int64_t n,
+                                    int32_t T, int32_t depth, const int32_t *leaves, int64_t nq, int32_t v,
+                                    int32_t leaves_sorted, int64_t max_count, const uint16_t *dir,
+                                    uint32_t *bits, int64_t bstride, int32_t *ncand, void *stream) {
+  clear_error();
+  if (!bits) return fail(MRPT_EPARAM, "mrpt_vote_bitmap: bits is NULL");
+  return vote_impl(leaf_indices, leaf_offsets, n, T, depth, leaves, nq, v, leaves_sorted, max_count, dir,
+                   nullptr, 1, bits, bstride, ncand, stream);
 }
 
 extern "C" int32_t mrpt_vote_counts(const int32_t *leaf_indices, const int64_t *leaf_offsets,

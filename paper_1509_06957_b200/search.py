@@ -215,7 +215,9 @@ def _check_batch_args(k, index, votes):
 def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
     """K2 -> K3 -> K4 over a device query block; returns device tensors
     (ids (nq,k) int64, dists (nq,k) float64, candidate_count (nq,) int32).
-    ``timer``: optional list receiving (stage, start_event, end_event) per launch."""
+    ``timer``: optional list receiving (stage, start_event, end_event) per launch.
+    The candidate hand-over is a list per query, or a bitmap per query for
+    the GEMM filter when the autotune found that faster (both exact)."""
     torch = _device.torch_mod()
 
     def stage(name, fn, *a):
@@ -236,12 +238,17 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
         counts = torch.empty(nq, dtype=torch.int32, device=dev)
     else:
         ids, dists, counts = out
+    bstride = _bstride(D)
+    choice = D.scan_choice.get((k, votes))
+    bits_mode = choice == "u8gemm_bits"
     if chunk is None:
-        per_q = 4 * (D.T + cap)
+        per_q = 4 * (D.T + (bstride if bits_mode else cap))
         chunk = max(1, min(nq, (1 << 30) // per_q))
     vdir = D.vote_dir()
-    leaves = torch.empty((min(chunk, nq), D.T), dtype=torch.int32, device=dev)
-    cand = torch.empty((min(chunk, nq), cap), dtype=torch.int32, device=dev)
+    m0 = min(chunk, nq)
+    leaves = torch.empty((m0, D.T), dtype=torch.int32, device=dev)
+    cand = None
+    bits = torch.empty((m0, bstride), dtype=torch.int32, device=dev) if bits_mode else None
     stream = _native.stream_ptr()
     for s in range(0, nq, chunk):
         e = min(nq, s + chunk)
@@ -250,16 +257,51 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
               int(Qd.stride(0)), _native.ptr(D.col_ptr), _native.ptr(D.rows),
               _native.ptr(D.vals), _native.ptr(D.splits), D.T, D.depth, _native.ptr(leaves),
               stream)
-        stage("vote", _native.call, "mrpt_vote", _native.ptr(D.indices), _native.ptr(D.offsets),
-              D.n, D.T, D.depth, _native.ptr(leaves), e - s, int(votes), int(D.leaves_sorted),
-              int(D.max_count), _native.ptr(vdir), _native.ptr(cand), int(cap),
-              _native.ptr(counts[s:e]), stream)
+        if choice is None and e - s >= 256:
+            # the autotune's last run leaves this chunk's outputs
+            choice = _autotune(D, qb, e - s, int(Qd.stride(0)), leaves, votes, vdir, cap,
+                               counts[s:e], k, ids[s:e], dists[s:e])
+            continue
+        if bits_mode:
+            stage("vote", _vote_bitmap, D, leaves, e - s, votes, vdir, bits, bstride, counts[s:e])
+            stage("scan_topk", _scan_bits, D, qb, e - s, int(Qd.stride(0)), bits, bstride, k,
+                  ids[s:e], dists[s:e])
+            continue
+        if cand is None:
+            cand = torch.empty((m0, cap), dtype=torch.int32, device=dev)
+        stage("vote", _vote_list, D, leaves, e - s, votes, vdir, cand, cap, counts[s:e])
         args = (qb, e - s, int(Qd.stride(0)), cand, cap, counts[s:e], k, ids[s:e], dists[s:e])
-        variant = D.scan_choice.get(k)
-        if variant is None:
-            variant = _autotune_scan(D, args) if e - s >= 256 else "fp32"
+        variant = choice if choice not in (None, "u8gemm_bits") else "fp32"
         stage("scan_topk", _scan_launch, D, variant, args)
     return ids, dists, counts
+
+
+def _bstride(D):
+    """Words per query of a candidate bitmap (16-byte rows)."""
+    return (D.n + 127) // 128 * 4
+
+
+def _vote_list(D, leaves, m, votes, vdir, cand, cap, counts):
+    _native.call("mrpt_vote", _native.ptr(D.indices), _native.ptr(D.offsets), D.n, D.T, D.depth,
+                 _native.ptr(leaves), m, int(votes), int(D.leaves_sorted), int(D.max_count),
+                 _native.ptr(vdir), _native.ptr(cand), int(cap), _native.ptr(counts),
+                 _native.stream_ptr())
+
+
+def _vote_bitmap(D, leaves, m, votes, vdir, bits, bstride, counts):
+    _native.call("mrpt_vote_bitmap", _native.ptr(D.indices), _native.ptr(D.offsets), D.n, D.T,
+                 D.depth, _native.ptr(leaves), m, int(votes), int(D.leaves_sorted),
+                 int(D.max_count), _native.ptr(vdir), _native.ptr(bits), int(bstride),
+                 _native.ptr(counts), _native.stream_ptr())
+
+
+def _scan_bits(D, qb, m, ldq, bits, bstride, k, ids, dists):
+    ldr = D.u8_rows()[1]
+    Xs, info, ws = D.u8_gemm(m)
+    _native.call("mrpt_scan_topk_u8gemm_bits", _native.ptr(D.X), D.n, D.d, int(D.X.stride(0)),
+                 _native.ptr(Xs), ldr, _native.ptr(info), _native.ptr(qb), m, ldq,
+                 _native.ptr(bits), int(bstride), int(k), _native.ptr(ids), _native.ptr(dists),
+                 _native.ptr(ws), int(ws.numel()), _native.stream_ptr())
 
 
 def _scan_variants(D, k):
@@ -271,6 +313,8 @@ def _scan_variants(D, k):
         # dot-product matrix of a useful query chunk fits (n <= 4M rows)
         if D.n <= (4 << 20):
             out.append("u8gemm")
+            if k <= 96:
+                out.append("u8gemm_bits")  # same filter, candidate bitmaps from K3
     if k <= 120 and D.shadow() is not None:
         out.append("fp16")
     out.append("fp32")
@@ -304,31 +348,42 @@ def _scan_launch(D, variant, args):
                      *common_tail)
 
 
-def _autotune_scan(D, args):
-    """Time every exact filter variant once on this chunk and keep the fastest
-    for the index (per k); the last launch leaves valid outputs."""
+def _autotune(D, qb, m, ldq, leaves, votes, vdir, cap, counts, k, ids, dists):
+    """Time every exact route for this chunk -- list vote + each list filter,
+    bitmap vote + the bitmap GEMM filter -- and keep the fastest for the index
+    (per k and vote threshold); the last run leaves valid outputs (all routes
+    give identical results).  MRPT_SCAN_ROWS forces a variant."""
     torch = _device.torch_mod()
-    k = args[6]
-    env = os.environ.get("MRPT_SCAN_ROWS")
     variants = _scan_variants(D, k)
+    env = os.environ.get("MRPT_SCAN_ROWS")
     if env in variants:
-        D.scan_choice[k] = env
-        return env
-    if len(variants) == 1:
-        D.scan_choice[k] = variants[0]
-        return variants[0]
-    best, best_ms = None, None
-    for v in variants:
-        _scan_launch(D, v, args)  # warm (first use builds nothing; shadows exist)
+        variants = [env]
+    dev = qb.device
+    list_vars = [v for v in variants if v != "u8gemm_bits"]
+    times = {}
+
+    def timed(fn, *a):
+        fn(*a)  # warm (first use builds the filter rows)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        _scan_launch(D, v, args)
+        fn(*a)
         e1.record()
         e1.synchronize()
-        ms = e0.elapsed_time(e1)
-        if best_ms is None or ms < best_ms:
-            best, best_ms = v, ms
-    D.scan_choice[k] = best
+        return e0.elapsed_time(e1)
+
+    if "u8gemm_bits" in variants:
+        bstride = _bstride(D)
+        bits = torch.empty((m, bstride), dtype=torch.int32, device=dev)
+        tv = timed(_vote_bitmap, D, leaves, m, votes, vdir, bits, bstride, counts)
+        times["u8gemm_bits"] = tv + timed(_scan_bits, D, qb, m, ldq, bits, bstride, k, ids, dists)
+    if list_vars:
+        cand = torch.empty((m, cap), dtype=torch.int32, device=dev)
+        tv = timed(_vote_list, D, leaves, m, votes, vdir, cand, cap, counts)
+        args = (qb, m, ldq, cand, cap, counts, k, ids, dists)
+        for v in list_vars:
+            times[v] = tv + timed(_scan_launch, D, v, args)
+    best = min(times, key=times.get)
+    D.scan_choice[(k, votes)] = best
     return best
 
 

@@ -153,7 +153,7 @@ class _DeviceIndex:
         self.leaves_sorted = leaves_sorted
         self.max_count = max_count
         self.max_leaf = max_leaf
-        self.scan_choice = {}  # k -> exact filter variant chosen by the autotune
+        self.scan_choice = {}  # (k, votes) -> exact route chosen by the autotune
 
     def cap(self, votes):
         """Upper bound on any candidate set at this vote threshold."""
@@ -195,7 +195,7 @@ class _DeviceIndex:
         self._u8 = None
         ldq = (self.d + 15) // 16 * 16
         mode = os.environ.get("MRPT_SCAN_ROWS", "auto")
-        if mode in ("auto", "u8", "u8gemm") and ldq <= 1024:
+        if mode in ("auto", "u8", "u8gemm", "u8gemm_bits") and ldq <= 1024:
             torch = _device.torch_mod()
             dev = self.X.device
             Xq = torch.empty((self.n, ldq), dtype=torch.uint8, device=dev)

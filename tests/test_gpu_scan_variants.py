@@ -36,11 +36,13 @@ def _data(kind, rng, n, d):
     return x.astype(np.float32)
 
 
-@pytest.mark.parametrize("variant", ["u8", "u8gemm", "fp16", "fp32"])
+@pytest.mark.parametrize("variant", ["u8", "u8gemm", "u8gemm_bits", "fp16", "fp32"])
 @pytest.mark.parametrize("kind,d,k,v", [("pixels", 96, 10, 1), ("ints", 128, 10, 2),
                                          ("clusters01", 256, 10, 2), ("signed", 64, 7, 1),
                                          ("dups", 32, 20, 1), ("pixels", 200, 100, 1)])
 def test_variant_parity(monkeypatch, rng, variant, kind, d, k, v):
+    if variant == "u8gemm_bits" and k > 96:
+        pytest.skip("the bitmap GEMM filter takes k <= 96")
     monkeypatch.setenv("MRPT_SCAN_ROWS", variant)
     if variant == "fp16":
         monkeypatch.setenv("MRPT_FP16_FILTER", "1")
@@ -51,7 +53,7 @@ def test_variant_parity(monkeypatch, rng, variant, kind, d, k, v):
         Q = Q - 0.05  # negative query coordinates: s8 query quantisation
     index = mrpt.grow_trees(Xd, 6, 6, seed=3)
     ids, dists, counts = mrpt.approximate_knn_batch(Q, k, index, v)
-    assert index.device_index().scan_choice.get(k) in (variant, "fp32")
+    assert index.device_index().scan_choice.get((k, v)) in (variant, "fp32")
     rids, rd, rc = _oracle(index, Xd, Q, k, v)
     assert np.array_equal(counts.astype(np.int64), rc)
     assert np.array_equal(ids, rids)
@@ -86,7 +88,7 @@ def test_u8gemm_small_workspace_chunks(rng, kind, signed):
     index = mrpt.grow_trees(Xd, 5, 5, seed=7)
     D = index.device_index()
     Qd = torch.from_numpy(np.ascontiguousarray(Q)).cuda()
-    D.scan_choice[k] = "u8"
+    D.scan_choice[(k, 1)] = "u8"
     want = [t.cpu().numpy() for t in query_device(D, Qd, k, 1)]
     ldq = D.u8_rows()[1]
     Xs, info, _ = D.u8_gemm(nq)
@@ -108,6 +110,27 @@ def test_u8gemm_small_workspace_chunks(rng, kind, signed):
     _native.call("mrpt_scan_topk_u8gemm", _native.ptr(D.X), n, d, int(D.X.stride(0)),
                  _native.ptr(Xs), ldq, _native.ptr(info), _native.ptr(Qd), nq, d, _native.ptr(cand),
                  int(cap), _native.ptr(counts), k, _native.ptr(ids), _native.ptr(dists),
+                 _native.ptr(ws), int(ws.numel()), _native.stream_ptr())
+    assert np.array_equal(ids.cpu().numpy(), want[0])
+    assert dists.cpu().numpy().tobytes() == want[1].tobytes()
+    # the same through candidate bitmaps
+    bstride = (n + 127) // 128 * 4
+    bits = torch.empty((nq, bstride), dtype=torch.int32, device="cuda")
+    bcounts = torch.empty(nq, dtype=torch.int32, device="cuda")
+    _native.call("mrpt_vote_bitmap", _native.ptr(D.indices), _native.ptr(D.offsets), D.n, D.T,
+                 D.depth, _native.ptr(leaves), nq, 1, int(D.leaves_sorted), int(D.max_count),
+                 _native.ptr(D.vote_dir()), _native.ptr(bits), bstride, _native.ptr(bcounts),
+                 _native.stream_ptr())
+    assert np.array_equal(bcounts.cpu().numpy(), counts.cpu().numpy())
+    bl = bits.cpu().numpy().view(np.uint32)
+    for qi in range(0, nq, 17):
+        setbits = np.flatnonzero(np.unpackbits(bl[qi].view(np.uint8), bitorder="little"))
+        setbits = setbits[setbits < n]  # words past ceil(n/32) are padding, never written
+        assert np.array_equal(setbits, np.sort(cand[qi, :int(counts[qi])].cpu().numpy()))
+    ids.fill_(-5)
+    _native.call("mrpt_scan_topk_u8gemm_bits", _native.ptr(D.X), n, d, int(D.X.stride(0)),
+                 _native.ptr(Xs), ldq, _native.ptr(info), _native.ptr(Qd), nq, d,
+                 _native.ptr(bits), bstride, k, _native.ptr(ids), _native.ptr(dists),
                  _native.ptr(ws), int(ws.numel()), _native.stream_ptr())
     assert np.array_equal(ids.cpu().numpy(), want[0])
     assert dists.cpu().numpy().tobytes() == want[1].tobytes()

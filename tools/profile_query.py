@@ -60,4 +60,4 @@ if not a.build_only:
             st[name] = st.get(name, 0.0) + x0.elapsed_time(x1)
         print(f"TIME config={a.config} v={v} nq={Qd.shape[0]} ms={ms:.3f} qps={Qd.shape[0] / ms * 1e3:.0f} "
               f"stages=" + ",".join(f"{k2}:{v2:.2f}" for k2, v2 in st.items()) +
-              f" variant={os.environ.get('MRPT_SCAN_VARIANT', '')}")
+              f" variant={D.scan_choice.get((p['k'], v))}")
