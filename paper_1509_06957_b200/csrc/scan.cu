@@ -1301,6 +1301,41 @@ __device__ __forceinline__ QParams quantize_query_u8(const float *qrow, int d, i
   return P;
 }
 
+// One candidate per lane of the u8 filter: float32 bounds of its distance
+// (each of t1, t2, t3 carries <= 3 roundings and the sum two more, so
+// |A - D| <= 8 * 2^-24 * (t1 + t2 + |t3|)), admission against the warp's
+// running k-th upper bound, buffer append, and a shrink when the buffer is
+// full; false when it cannot shrink (-> exact fallback).
+template <int BUFW, int CPI>
+__device__ __forceinline__ bool admit_lane_u8(int32_t myc, int mys, float sx, int nrm, float rad, float sqf,
+                                              float t2f, float rq, float &su, int &cnt, float *ma, float *mr,
+                                              float *me, int32_t *mi, int kk, float *cu_w, int32_t *cid_w) {
+  float A = 0.f, r = 0.f, eta = 0.f;
+  if (myc >= 0) {
+    const float t1 = sx * sx * (float)nrm;
+    const float t3 = 2.0f * sx * sqf * (float)mys;
+    A = (t1 + t2f) - t3;
+    eta = __fmul_ru(4.76837158203125e-07f, __fadd_ru(__fadd_ru(t1, t2f), fabsf(t3)));
+    r = __fadd_ru(rad, rq);
+  }
+  const bool take = myc >= 0 && admit2(A, r, eta, su);
+  const unsigned tm = __ballot_sync(0xffffffffu, take);
+  if (take) {
+    const int slot = cnt + __popc(tm & lanemask_lt());
+    ma[slot] = A;
+    mr[slot] = r;
+    me[slot] = eta;
+    mi[slot] = myc;
+  }
+  cnt += __popc(tm);
+  if (cnt > BUFW - CPI) {
+    __syncwarp();
+    cnt = shrink_bounds2<BUFW>(ma, mr, me, mi, cnt, kk, cu_w, cid_w, &su);
+    if (cnt > BUFW - CPI) return false;
+  }
+  return true;
+}
+
 // G lanes per row (ldq / 16 rounded up to a power of two, <= 32); each warp
 // iteration scores (32 / G) * 4 candidates with 16-byte loads.  DM: the dot
 // products come precomputed from the tensor-core GEMM (rows.D, one candidate
@@ -1323,6 +1358,7 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
   int32_t *cid = reinterpret_cast<int32_t *>(ckey + NWARP * BUFW);
   float *cu = reinterpret_cast<float *>(cid + NWARP * BUFW);
   float *cl = cu + NWARP * BUFW;
+  int32_t *wq_base = reinterpret_cast<int32_t *>(cl + NWARP * BUFW);  // DM bitmap mode: 512 ids per warp
   __shared__ int s_wcnt[NWARP];
   __shared__ int s_bad, s_ns;
   __shared__ QScratch<NWARP> qscr;
@@ -1365,44 +1401,21 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
     bool bad = false;
     // One candidate per lane: bound it, admit it into the warp's buffer, shrink
     // the buffer when full; false when the buffer cannot shrink (-> fallback).
-    auto admit_lane = [&](int32_t myc, int mys, float sx, int nrm, float rad) -> bool {
-      // float32 evaluation: each of t1, t2, t3 carries <= 3 roundings and the
-      // sum two more, so |A - D| <= 8 * 2^-24 * (t1 + t2 + |t3|)
-      float A = 0.f, r = 0.f, eta = 0.f;
-      if (myc >= 0) {
-        const float t1 = sx * sx * (float)nrm;
-        const float t3 = 2.0f * sx * sqf * (float)mys;
-        A = (t1 + t2f) - t3;
-        eta = __fmul_ru(4.76837158203125e-07f, __fadd_ru(__fadd_ru(t1, t2f), fabsf(t3)));
-        r = __fadd_ru(rad, rq);
-      }
-      const bool take = myc >= 0 && admit2(A, r, eta, su);
-      const unsigned tm = __ballot_sync(0xffffffffu, take);
-      if (take) {
-        const int slot = cnt + __popc(tm & lanemask_lt());
-        ma[slot] = A;
-        mr[slot] = r;
-        me[slot] = eta;
-        mi[slot] = myc;
-      }
-      cnt += __popc(tm);
-      if (cnt > BUFW - CPI) {
-        __syncwarp();
-        cnt = shrink_bounds2<BUFW>(ma, mr, me, mi, cnt, kk, cu + warp * BUFW, cid + warp * BUFW, &su);
-        if (cnt > BUFW - CPI) return false;
-      }
-      return true;
-    };
+    float *cu_w = cu + warp * BUFW;
+    int32_t *cid_w = cid + warp * BUFW;
+#define ADMIT_LANE(MYC, MYS, SX, NRM, RAD) \
+  admit_lane_u8<BUFW, CPI>((MYC), (MYS), (SX), (NRM), (RAD), sqf, t2f, rq, su, cnt, ma, mr, me, mi, kk, cu_w, cid_w)
     if (DM && rows.cbits) {
-      // candidate bitmap: each lane loads one of 32 consecutive words; the
-      // warp's set bits are then dealt out 32 per batch (lane r takes the
-      // r-th set bit: binary search over the words' prefix counts, then a
-      // popcount select inside the word), so every admission round is full
+      // candidate bitmap: lanes 0..15 each load one of 16 consecutive words
+      // and write their set bits' ids, in id order, to the warp's queue at
+      // the word's prefix offset; the queue is then consumed 32 ids per
+      // admission round (2 rounds in flight)
       constexpr int UB = 2;
       const uint32_t *qbits = rows.cbits + q * rows.bstride;
       const int nwords = (int)((a.n + 31) >> 5);
-      for (int w0 = warp * 32; w0 < nwords && !bad; w0 += NWARP * 32) {
-        const uint32_t word = w0 + lane < nwords ? __ldg(qbits + w0 + lane) : 0u;
+      int32_t *queue = wq_base + warp * (16 * 32);
+      for (int w0 = warp * 16; w0 < nwords && !bad; w0 += NWARP * 16) {
+        const uint32_t word = (lane < 16 && w0 + lane < nwords) ? __ldg(qbits + w0 + lane) : 0u;
         const int pc = __popc(word);
         int incl = pc;
 #pragma unroll
@@ -1410,8 +1423,17 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
           const int u = __shfl_up_sync(0xffffffffu, incl, o);
           if (lane >= o) incl += u;
         }
-        const int excl = incl - pc;
         const int total = __shfl_sync(0xffffffffu, incl, 31);
+        {
+          int p = incl - pc;
+          uint32_t wd = word;
+          const int32_t id0 = (w0 + lane) * 32;
+          while (wd) {
+            queue[p++] = id0 + __ffs(wd) - 1;
+            wd &= wd - 1u;
+          }
+        }
+        __syncwarp();
         for (int b0 = 0; b0 < total && !bad; b0 += 32 * UB) {
           int32_t cj[UB];
           int dv[UB];
@@ -1419,29 +1441,10 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
 #pragma unroll
           for (int u = 0; u < UB; ++u) {
             const int r = b0 + 32 * u + lane;
-            int src = 0;
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-              const int e = __shfl_sync(0xffffffffu, excl, src + step);
-              if (e <= r) src += step;
-            }
-            int rr = r - __shfl_sync(0xffffffffu, excl, src);
-            uint32_t wd = __shfl_sync(0xffffffffu, word, src);
-            int bit = 0;
-#pragma unroll
-            for (int half = 16; half > 0; half >>= 1) {
-              const int c = __popc(wd & ((1u << half) - 1u));
-              if (rr >= c) {
-                rr -= c;
-                wd >>= half;
-                bit += half;
-              }
-            }
-            cj[u] = -1;
+            cj[u] = r < total ? queue[r] : -1;
             dv[u] = 0;
             inf[u] = make_uint4(0u, 0u, 0u, 0u);
-            if (r < total) {
-              cj[u] = (w0 + src) * 32 + bit;
+            if (cj[u] >= 0) {
               dv[u] = __ldg(Drow + cj[u]);
               inf[u] = __ldg(rows.info + cj[u]);
             }
@@ -1450,13 +1453,14 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
           for (int u = 0; u < UB; ++u) {
             if (b0 + 32 * u >= total) break;  // warp-uniform
             const int mys = dv[u] + corr_q + (qsigned ? 0 : 128 * (int)inf[u].w);
-            if (!admit_lane(cj[u], mys, __uint_as_float(inf[u].x), (int)inf[u].y, __uint_as_float(inf[u].z))) {
+            if (!ADMIT_LANE(cj[u], mys, __uint_as_float(inf[u].x), (int)inf[u].y, __uint_as_float(inf[u].z))) {
               bad = true;
               cnt = 0;
               break;
             }
           }
         }
+        __syncwarp();  // the queue is rewritten by the next 16 words
       }
     } else if (DM) {
       // UDM candidates per lane in flight: ids, then their dot products and row info
@@ -1482,7 +1486,7 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
 #pragma unroll
         for (int u = 0; u < UDM; ++u) {
           const int mys = dv[u] + corr_q + (qsigned ? 0 : 128 * (int)inf[u].w);
-          if (!admit_lane(cj[u], mys, __uint_as_float(inf[u].x), (int)inf[u].y, __uint_as_float(inf[u].z))) {
+          if (!ADMIT_LANE(cj[u], mys, __uint_as_float(inf[u].x), (int)inf[u].y, __uint_as_float(inf[u].z))) {
             bad = true;
             cnt = 0;
             break;
@@ -1532,7 +1536,7 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
         nrm = __ldg(rows.norm + myc);
         rad = __ldg(rows.radius + myc);
       }
-      if (!admit_lane(myc, mys, sx, nrm, rad)) {
+      if (!ADMIT_LANE(myc, mys, sx, nrm, rad)) {
         bad = true;
         cnt = 0;
         break;
@@ -2233,7 +2237,8 @@ static int32_t u8gemm_impl(const float *X, int64_t n, int32_t d, int64_t ldx, co
   int bufw = 64;
   while (bufw < 2 * k + 2 * 32) bufw <<= 1;
   if (bufw > 256) return mrpt_scan_topk(X, n, d, ldx, Q, nq, ldqq, cand, cap, ncand, k, ids, dists, stream);
-  const size_t smem = 1024 + (size_t)(kScanNT / 32) * bufw * (4 * 4 + 8 + 4 * 3);
+  const size_t smem = 1024 + (size_t)(kScanNT / 32) * bufw * (4 * 4 + 8 + 4 * 3) +
+                      (cbits ? (size_t)(kScanNT / 32) * 16 * 32 * 4 : 0);
   topk_fn_u8 fn = pick_u8_b<8, true>(bufw);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int buf = (k + kScanNT <= 1024) ? 1024 : 2048;
