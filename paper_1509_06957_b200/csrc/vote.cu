@@ -318,8 +318,22 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_vote_dir(VoteArgs a) {
     const bool ranged = a.T >= NW && a.T <= 32 * NW;
     const int parts = ranged || ngroups >= NW ? 1 : NW / ngroups;
     const int nvirt = ranged ? NW : ngroups * parts;
+    // ranged: each lane owns one tree for the whole query, so its directory
+    // entries for the current and next tile stay in registers and the one
+    // after is fetched while the current tile is processed
+    const uint16_t *dlane = nullptr;
+    int dcur = 0, dnxt = 0;
+    if (ranged) {
+      const int t = (int)(((int64_t)warp * a.T) / NW) + lane;
+      if (t < (int)(((int64_t)(warp + 1) * a.T) / NW)) {
+        dlane = a.dir + ((int64_t)t * a.L + sleaf[t]) * dstride;
+        dcur = dlane[0];
+        dnxt = dlane[1];
+      }
+    }
     for (int tile = 0; tile < a.ntiles; ++tile) {
       const int32_t lo = tile * a.W;
+      const int dnn = (dlane && tile + 2 <= a.ntiles) ? (int)__ldg(dlane + tile + 2) : 0;
       for (int vw = warp; vw < nvirt; vw += NW) {
         const int g = ranged ? 0 : vw % ngroups, part = ranged ? 0 : vw / ngroups;
         const int t_lo = ranged ? (int)(((int64_t)vw * a.T) / NW) : g * 32;
@@ -328,8 +342,15 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_vote_dir(VoteArgs a) {
         int len = 0;
         long long base = 0;
         if (t < t_hi) {
-          const uint16_t *d = a.dir + ((int64_t)t * a.L + sleaf[t]) * dstride + tile;
-          const int s0 = d[0], s1 = d[1];
+          int s0, s1;
+          if (ranged) {
+            s0 = dcur;
+            s1 = dnxt;
+          } else {
+            const uint16_t *d = a.dir + ((int64_t)t * a.L + sleaf[t]) * dstride + tile;
+            s0 = d[0];
+            s1 = d[1];
+          }
           len = s1 - s0;
           base = (long long)t * a.n + sbase[t] + s0;
         }
@@ -431,6 +452,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_vote_dir(VoteArgs a) {
         s_nw = 0;
         s_nc = 0;
       }
+      dcur = dnxt;
+      dnxt = dnn;
       if (tile + 1 < a.ntiles) {
         for (int i = tid; i < cwords / 4; i += NT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
