@@ -49,6 +49,9 @@ enum {
 const char *mrpt_last_error(void);
 /* ABI version (major*100 + minor). */
 int32_t mrpt_abi_version(void);
+/* Kernels this library has launched so far (process-wide; library GEMMs of
+ * cuBLASLt are not counted). */
+int64_t mrpt_launch_count(void);
 
 /* ------------------------------------------------------------------ K1 --
  * Sparse projection with float64 accumulation in stored CSC order and one

@@ -24,6 +24,7 @@ _c_i32, _c_i64, _c_p, _c_sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, c
 SIGNATURES = {
     "mrpt_last_error": [],
     "mrpt_abi_version": [],
+    "mrpt_launch_count": [],
     "mrpt_project": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_i32, _c_p, _c_i64, _c_i64, _c_p],
     "mrpt_route": [_c_p, _c_i64, _c_i32, _c_p, _c_i64, _c_p, _c_p],
     "mrpt_query_route": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_i32, _c_i32, _c_p,
@@ -59,7 +60,7 @@ SIGNATURES = {
     "mrpt_check_finite": [_c_p, _c_i64, _c_p, _c_p],
     "mrpt_audit_leaves": [_c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p],
 }
-_RESTYPE = {"mrpt_last_error": ctypes.c_char_p}
+_RESTYPE = {"mrpt_last_error": ctypes.c_char_p, "mrpt_launch_count": _c_i64}
 
 MRPT_OK, MRPT_EPARAM, MRPT_ESHAPE, MRPT_EINTEGRITY, MRPT_EWORKSPACE = 0, -1, -2, -3, -4
 MRPT_ECUDA, MRPT_ENCCL = -10, -11

@@ -1,6 +1,8 @@
 // Error plumbing and small validation kernels of libmrpt_cuda.so.
 #include <stdarg.h>
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace mrpt {
@@ -15,6 +17,10 @@ void set_error(const char *fmt, ...) {
 }
 
 void clear_error() { g_err[0] = 0; }
+
+static std::atomic<long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 // core.py:63 -- np.isfinite(arr).all()
 __global__ void k_check_finite(const float *__restrict__ X, int64_t count, int32_t *bad) {
@@ -58,7 +64,9 @@ using namespace mrpt;
 
 extern "C" const char *mrpt_last_error(void) { return g_err; }
 
-extern "C" int32_t mrpt_abi_version(void) { return 100; }
+extern "C" int32_t mrpt_abi_version(void) { return 101; }
+
+extern "C" int64_t mrpt_launch_count(void) { return mrpt::g_launches.load(std::memory_order_relaxed); }
 
 extern "C" int32_t mrpt_check_finite(const float *X, int64_t count, int32_t *bad, void *stream) {
   clear_error();
@@ -68,7 +76,7 @@ extern "C" int32_t mrpt_check_finite(const float *X, int64_t count, int32_t *bad
   if (count == 0) return launch_status("mrpt_check_finite");
   int64_t blocks = ceil_div<int64_t>(count, 256 * 8);
   int grid = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
-  k_check_finite<<<grid, 256, 0, s>>>(X, count, bad);
+  (count_launch(), k_check_finite<<<grid, 256, 0, s>>>(X, count, bad));
   return launch_status("mrpt_check_finite");
 }
 
@@ -83,6 +91,6 @@ extern "C" int32_t mrpt_audit_leaves(const int32_t *leaf_indices, const int64_t 
   int64_t total = (int64_t)T * n;
   int64_t blocks = ceil_div<int64_t>(total, 256);
   int grid = (int)(blocks < (int64_t)num_sms() * 32 ? blocks : (int64_t)num_sms() * 32);
-  k_audit_leaves<<<grid, 256, 0, s>>>(leaf_indices, leaf_offsets, n, T, 1 << depth, flags);
+  (count_launch(), k_audit_leaves<<<grid, 256, 0, s>>>(leaf_indices, leaf_offsets, n, T, 1 << depth, flags));
   return launch_status("mrpt_audit_leaves");
 }

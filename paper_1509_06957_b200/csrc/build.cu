@@ -631,7 +631,7 @@ extern "C" int32_t mrpt_build_levels(const float *P, int64_t n, int32_t Tb, int3
     const int64_t total = (int64_t)Tb * n;
     const int64_t blocks = ceil_div<int64_t>(total, 256);
     const int grid = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
-    k_build_init<<<grid, 256, 0, s>>>(obuf[0], bbuf[0], n, Tb, bstride);
+    (count_launch(), k_build_init<<<grid, 256, 0, s>>>(obuf[0], bbuf[0], n, Tb, bstride));
   }
   const int sms = num_sms();
   cudaFuncSetAttribute(k_seg_small<kMidMax>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMidMax * 8);
@@ -660,27 +660,27 @@ extern "C" int32_t mrpt_build_levels(const float *P, int64_t n, int32_t Tb, int3
     a.chunk_off = reinterpret_cast<int32_t *>(w + L.coff);
     cudaMemsetAsync(a.ctl, 0, sizeof(LevelCtl), s);
     const int64_t nsegs = (int64_t)Tb << lev;
-    k_level_plan<<<(unsigned)ceil_div<int64_t>(nsegs, 256), 256, 0, s>>>(a);
+    (count_launch(), k_level_plan<<<(unsigned)ceil_div<int64_t>(nsegs, 256), 256, 0, s>>>(a));
     // expected per-segment size decides how many CTAs the small paths get
     const int64_t est = n >> lev;
     const int64_t tiny_grid = nsegs < (int64_t)sms * 8 ? nsegs : (int64_t)sms * 8;
-    k_seg_small<kTinyMax><<<(unsigned)(est <= kTinyMax ? tiny_grid : (tiny_grid < sms ? tiny_grid : sms)),
-                             kNT, kTinyMax * 8, s>>>(a, 0);
+    (count_launch(), k_seg_small<kTinyMax><<<(unsigned)(est <= kTinyMax ? tiny_grid : (tiny_grid < sms ? tiny_grid : sms)),
+                             kNT, kTinyMax * 8, s>>>(a, 0));
     const int64_t mid_grid = nsegs < (int64_t)sms * 3 ? nsegs : (int64_t)sms * 3;
-    k_seg_small<kMidMax><<<(unsigned)mid_grid, kNT, kMidMax * 8, s>>>(a, 1);
+    (count_launch(), k_seg_small<kMidMax><<<(unsigned)mid_grid, kNT, kMidMax * 8, s>>>(a, 1));
     if (est > kMidMax || lev > 0) {
       // the big path may have work whenever a segment can exceed kMidMax;
       // after level 0 ties can make any segment large, so always launch.
       const int big_grid = sms * 4;
-      k_big_keys<<<big_grid, kNT, 0, s>>>(a);
-      k_big_init<<<ceil_div<int>(sms, 1), 256, 0, s>>>(a);
+      (count_launch(), k_big_keys<<<big_grid, kNT, 0, s>>>(a));
+      (count_launch(), k_big_init<<<ceil_div<int>(sms, 1), 256, 0, s>>>(a));
       for (int pass = 0; pass < 4; ++pass) {
-        k_big_hist<<<big_grid, kNT, 0, s>>>(a);
-        k_big_pick<<<sms, 256, 0, s>>>(a);
+        (count_launch(), k_big_hist<<<big_grid, kNT, 0, s>>>(a));
+        (count_launch(), k_big_pick<<<sms, 256, 0, s>>>(a));
       }
-      k_big_count<<<big_grid, kNT, 0, s>>>(a);
-      k_big_scan<<<sms, 256, 0, s>>>(a);
-      k_big_scatter<<<big_grid, kNT, 0, s>>>(a);
+      (count_launch(), k_big_count<<<big_grid, kNT, 0, s>>>(a));
+      (count_launch(), k_big_scan<<<sms, 256, 0, s>>>(a));
+      (count_launch(), k_big_scatter<<<big_grid, kNT, 0, s>>>(a));
     }
   }
   return launch_status("mrpt_build_levels");

@@ -18,6 +18,10 @@ inline int32_t fail(int32_t code, const char *what) {
   return code;
 }
 
+// Kernels this library has launched (all devices, all threads): the bench's
+// gpu_launches evidence, read through mrpt_launch_count().
+void count_launch();
+
 // Report the launch status of the kernels just enqueued.
 inline int32_t launch_status(const char *where) {
   cudaError_t e = cudaGetLastError();

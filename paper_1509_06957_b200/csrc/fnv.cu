@@ -172,7 +172,7 @@ extern "C" int32_t mrpt_fnv1a64(const uint8_t *buf, int64_t nbytes, uint64_t *ou
   cudaStream_t s = as_stream(stream);
   unsigned long long *o = reinterpret_cast<unsigned long long *>(out);
   if (nbytes == 0) {  // empty input hashes to the offset basis
-    k_fnv_combine<<<1, 32, 0, s>>>(nullptr, 0, 1ull, 1ull, o);
+    (count_launch(), k_fnv_combine<<<1, 32, 0, s>>>(nullptr, 0, 1ull, 1ull, o));
     return launch_status("mrpt_fnv1a64");
   }
   const int64_t chunk = fnv_chunk(nbytes);
@@ -183,11 +183,11 @@ extern "C" int32_t mrpt_fnv1a64(const uint8_t *buf, int64_t nbytes, uint64_t *ou
   uint8_t *starts = perm + (size_t)nch * 256;
   unsigned long long *coff = reinterpret_cast<unsigned long long *>(
       (reinterpret_cast<uintptr_t>(starts + nch) + 15) & ~uintptr_t(15));
-  k_fnv_perm<<<(unsigned)nch, 256, 0, s>>>(buf, nbytes, chunk, perm);
-  k_fnv_starts<<<1, 256, 0, s>>>(perm, nch, starts);
-  k_fnv_offsets<<<(unsigned)ceil_div<int64_t>(nch, 128), 128, 0, s>>>(buf, nbytes, chunk, nch, starts,
-                                                                      coff);
+  (count_launch(), k_fnv_perm<<<(unsigned)nch, 256, 0, s>>>(buf, nbytes, chunk, perm));
+  (count_launch(), k_fnv_starts<<<1, 256, 0, s>>>(perm, nch, starts));
+  (count_launch(), k_fnv_offsets<<<(unsigned)ceil_div<int64_t>(nch, 128), 128, 0, s>>>(buf, nbytes, chunk, nch, starts,
+                                                                      coff));
   const int64_t last = nbytes - (nch - 1) * chunk;
-  k_fnv_combine<<<1, 32, 0, s>>>(coff, nch, pow_mod64(kFnvPrime, chunk), pow_mod64(kFnvPrime, last), o);
+  (count_launch(), k_fnv_combine<<<1, 32, 0, s>>>(coff, nch, pow_mod64(kFnvPrime, chunk), pow_mod64(kFnvPrime, last), o));
   return launch_status("mrpt_fnv1a64");
 }

@@ -186,22 +186,22 @@ extern "C" int32_t mrpt_project(const float *X, int64_t m, int32_t d, int64_t ld
     const int64_t cap = (int64_t)num_sms() * per_sm;
     const int grid = (int)(tiles < cap ? tiles : cap);
     cudaFuncSetAttribute(k_project_smem<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_project_smem<2><<<grid, 256, smem, s>>>(X, m, d, ldx, col_ptr, rows, vals, ncols, out,
-                                               out_row_stride, out_col_stride, tp, stride);
+    (count_launch(), k_project_smem<2><<<grid, 256, smem, s>>>(X, m, d, ldx, col_ptr, rows, vals, ncols, out,
+                                               out_row_stride, out_col_stride, tp, stride));
   } else if (32 * row_bytes <= 200 * 1024) {
     tp = 32;
     const size_t smem = (size_t)tp * row_bytes;
     const int64_t tiles = ceil_div<int64_t>(m, tp);
     const int grid = (int)(tiles < (int64_t)num_sms() ? tiles : (int64_t)num_sms());
     cudaFuncSetAttribute(k_project_smem<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_project_smem<1><<<grid, 256, smem, s>>>(X, m, d, ldx, col_ptr, rows, vals, ncols, out,
-                                               out_row_stride, out_col_stride, tp, stride);
+    (count_launch(), k_project_smem<1><<<grid, 256, smem, s>>>(X, m, d, ldx, col_ptr, rows, vals, ncols, out,
+                                               out_row_stride, out_col_stride, tp, stride));
   } else {
     const int64_t total = m * ncols;
     const int64_t blocks = ceil_div<int64_t>(total, 256);
     const int grid = (int)(blocks < (int64_t)num_sms() * 8 ? blocks : (int64_t)num_sms() * 8);
-    k_project_global<<<grid, 256, 0, s>>>(X, m, ldx, col_ptr, rows, vals, ncols, out,
-                                          out_row_stride, out_col_stride);
+    (count_launch(), k_project_global<<<grid, 256, 0, s>>>(X, m, ldx, col_ptr, rows, vals, ncols, out,
+                                          out_row_stride, out_col_stride));
   }
   return launch_status("mrpt_project");
 }
@@ -214,7 +214,7 @@ extern "C" int32_t mrpt_route(const float *proj, int64_t nrows, int32_t depth, c
   cudaStream_t s = as_stream(stream);
   const int64_t blocks = ceil_div<int64_t>(nrows, 128);
   const int grid = (int)(blocks < 65535 ? blocks : 65535);
-  k_route<<<grid, 128, 0, s>>>(proj, nrows, depth, splits, n_internal, out);
+  (count_launch(), k_route<<<grid, 128, 0, s>>>(proj, nrows, depth, splits, n_internal, out));
   return launch_status("mrpt_route");
 }
 
@@ -240,13 +240,13 @@ extern "C" int32_t mrpt_query_route(const float *Q, int64_t nq, int32_t d, int64
     if (smem <= 160 * 1024) {
       cudaFuncSetAttribute(k_query_route<QB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem);
-      k_query_route<QB, true><<<grid, 128, smem, s>>>(Q + off * ldq, chunk_q, d, ldq, col_ptr, rows,
+      (count_launch(), k_query_route<QB, true><<<grid, 128, smem, s>>>(Q + off * ldq, chunk_q, d, ldq, col_ptr, rows,
                                                       vals, splits, T, depth, leaves + off * T,
-                                                      stride);
+                                                      stride));
     } else {
-      k_query_route<QB, false><<<grid, 128, 0, s>>>(Q + off * ldq, chunk_q, d, ldq, col_ptr, rows,
+      (count_launch(), k_query_route<QB, false><<<grid, 128, 0, s>>>(Q + off * ldq, chunk_q, d, ldq, col_ptr, rows,
                                                     vals, splits, T, depth, leaves + off * T,
-                                                    stride);
+                                                    stride));
     }
     off += chunk_q;
   }

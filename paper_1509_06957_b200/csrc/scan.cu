@@ -1804,7 +1804,7 @@ extern "C" int32_t mrpt_scan(const float *X, int64_t n, int32_t d, int64_t ldx, 
   cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t blocks = ceil_div<int64_t>(m, kScanNT * kScanR);
   const int grid = (int)(blocks < (int64_t)num_sms() * 8 ? blocks : (int64_t)num_sms() * 8);
-  k_scan<<<grid, kScanNT, smem, s>>>(X, ldx, d, cand, m, q, out, vec4);
+  (count_launch(), k_scan<<<grid, kScanNT, smem, s>>>(X, ldx, d, cand, m, q, out, vec4));
   return launch_status("mrpt_scan");
 }
 
@@ -1887,7 +1887,7 @@ extern "C" int32_t mrpt_scan_topk(const float *X, int64_t n, int32_t d, int64_t 
     a.k = k;
     a.ids = ids;
     a.dists = dists;
-    ffn<<<(unsigned)grid, kScanNT, smem, s>>>(a, eps, eta, fb + 1, fb);
+    (count_launch(), ffn<<<(unsigned)grid, kScanNT, smem, s>>>(a, eps, eta, fb + 1, fb));
     // fallback: exact tiled kernel over the listed queries
     a.qlist = fb + 1;
     a.qcount = fb;
@@ -1896,7 +1896,7 @@ extern "C" int32_t mrpt_scan_topk(const float *X, int64_t n, int32_t d, int64_t 
     const size_t tsmem = (size_t)buf * 12 + sizeof(float) * (kScanNT / 32) * 32 * kTileStride +
                          sizeof(double) * (size_t)d;
     cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-    tfn<<<(unsigned)(grid < 64 ? grid : 64), kScanNT, tsmem, s>>>(a);
+    (count_launch(), tfn<<<(unsigned)(grid < 64 ? grid : 64), kScanNT, tsmem, s>>>(a));
     cudaFreeAsync(fb, s);
     return launch_status("mrpt_scan_topk");
   }
@@ -1925,7 +1925,7 @@ extern "C" int32_t mrpt_scan_topk(const float *X, int64_t n, int32_t d, int64_t 
     const size_t smem = (size_t)buf * 12 + extra + sizeof(double) * (size_t)d;
     if (smem > 220 * 1024) return fail(MRPT_EPARAM, "mrpt_scan_topk: d too large");
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    fn<<<(unsigned)grid, kScanNT, smem, s>>>(a);
+    (count_launch(), fn<<<(unsigned)grid, kScanNT, smem, s>>>(a));
   }
   if (passes > 1) {
     cudaFreeAsync(a.lb_key, s);
@@ -1943,7 +1943,7 @@ extern "C" int32_t mrpt_quantize_fp16(const float *X, int64_t n, int32_t d, int6
   cudaMemsetAsync(bad, 0, sizeof(int32_t), s);
   const int64_t blocks = ceil_div<int64_t>(n, 8);
   const int grid = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
-  k_quantize_fp16<<<grid, 256, 0, s>>>(X, n, d, ldx, reinterpret_cast<__half *>(Xh), ldh, radius, bad);
+  (count_launch(), k_quantize_fp16<<<grid, 256, 0, s>>>(X, n, d, ldx, reinterpret_cast<__half *>(Xh), ldh, radius, bad));
   return launch_status("mrpt_quantize_fp16");
 }
 
@@ -1998,7 +1998,7 @@ extern "C" int32_t mrpt_scan_topk_fp16(const float *X, int64_t n, int32_t d, int
                              : (bufw == 128 ? k_scan_topk_filter_h<128> : k_scan_topk_filter_h<256>);
   cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t grid = nq < (int64_t)num_sms() * 8 ? nq : (int64_t)num_sms() * 8;
-  ffn<<<(unsigned)grid, kScanNT, smem, s>>>(a, eps, eta, fb + 1, fb);
+  (count_launch(), ffn<<<(unsigned)grid, kScanNT, smem, s>>>(a, eps, eta, fb + 1, fb));
   // fallback: exact tiled kernel over the listed queries
   a.qlist = fb + 1;
   a.qcount = fb;
@@ -2008,7 +2008,7 @@ extern "C" int32_t mrpt_scan_topk_fp16(const float *X, int64_t n, int32_t d, int
     const size_t tsmem = (size_t)buf * 12 + sizeof(float) * (kScanNT / 32) * 32 * kTileStride +
                          sizeof(double) * (size_t)d;
     cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-    tfn<<<(unsigned)(grid < 64 ? grid : 64), kScanNT, tsmem, s>>>(a);
+    (count_launch(), tfn<<<(unsigned)(grid < 64 ? grid : 64), kScanNT, tsmem, s>>>(a));
   } else {
     return fail(MRPT_EPARAM, "mrpt_scan_topk_fp16: exact fallback needs 16-byte rows");
   }
@@ -2029,15 +2029,15 @@ extern "C" int32_t mrpt_quantize_u8(const float *X, int64_t n, int32_t d, int64_
   const int64_t total = n * d;
   const int64_t blocks = ceil_div<int64_t>(total, 256 * 8);
   const int g1 = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
-  k_q8_flags<<<g1, 256, 0, s>>>(X, n, d, ldx, flags);
+  (count_launch(), k_q8_flags<<<g1, 256, 0, s>>>(X, n, d, ldx, flags));
   int32_t hflags[2] = {0, 0};
   cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return launch_status("mrpt_quantize_u8");
   if (hflags[0]) return MRPT_OK;
   const int64_t wb = ceil_div<int64_t>(n, 8);
   const int g2 = (int)(wb < (int64_t)num_sms() * 16 ? wb : (int64_t)num_sms() * 16);
-  k_quantize_u8<<<g2, 256, 0, s>>>(X, n, d, ldx, reinterpret_cast<uint8_t *>(Xq), ldq, scale, norm,
-                                   radius, hflags[1] ? 0 : 1);
+  (count_launch(), k_quantize_u8<<<g2, 256, 0, s>>>(X, n, d, ldx, reinterpret_cast<uint8_t *>(Xq), ldq, scale, norm,
+                                   radius, hflags[1] ? 0 : 1));
   return launch_status("mrpt_quantize_u8");
 }
 
@@ -2057,7 +2057,7 @@ int32_t igemm_rows_tn(const int8_t *Xs, int64_t n, const int8_t *Qop, int64_t m,
 static void launch_rerank(const TopkArgs &a, cudaStream_t s) {
   const int64_t blocks = ceil_div<int64_t>(a.nq, 8);
   const int64_t cap = (int64_t)num_sms() * 16;
-  k_rerank<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, s>>>(a);
+  (count_launch(), k_rerank<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, s>>>(a));
 }
 
 extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64_t ldx,
@@ -2140,7 +2140,7 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
                   : (G == 16 ? pick_u8_b<16>(bufw) : (G == 8 ? pick_u8_b<8>(bufw) : pick_u8_b<4>(bufw)));
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t grid = nq < (int64_t)num_sms() * 8 ? nq : (int64_t)num_sms() * 8;
-  fn<<<(unsigned)grid, kScanNT, smem, s>>>(a, rows, fb + 1, fb);
+  (count_launch(), fn<<<(unsigned)grid, kScanNT, smem, s>>>(a, rows, fb + 1, fb));
   a.qlist = fb + 1;
   a.qcount = fb;
   if (a.vec4) {
@@ -2149,7 +2149,7 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
     const size_t tsmem = (size_t)buf * 12 + sizeof(float) * (kScanNT / 32) * 32 * kTileStride +
                          sizeof(double) * (size_t)d;
     cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-    tfn<<<(unsigned)(grid < 64 ? grid : 64), kScanNT, tsmem, s>>>(a);
+    (count_launch(), tfn<<<(unsigned)(grid < 64 ? grid : 64), kScanNT, tsmem, s>>>(a));
   } else {
     cudaFreeAsync(fb, s);
     return fail(MRPT_EPARAM, "mrpt_scan_topk_u8: exact fallback needs 16-byte rows");
@@ -2168,9 +2168,9 @@ extern "C" int32_t mrpt_u8_gemm_rows(const void *Xq, int64_t n, int64_t ldq, con
   if (reinterpret_cast<uintptr_t>(info) & 15u) return fail(MRPT_EPARAM, "mrpt_u8_gemm_rows: info must be 16-byte aligned");
   const int64_t blocks = ceil_div<int64_t>(n, 8);
   const int grid = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
-  k_u8_gemm_rows<<<grid, 256, 0, as_stream(stream)>>>(reinterpret_cast<const uint8_t *>(Xq), n, (int)ldq,
+  (count_launch(), k_u8_gemm_rows<<<grid, 256, 0, as_stream(stream)>>>(reinterpret_cast<const uint8_t *>(Xq), n, (int)ldq,
                                                        scale, norm, radius, reinterpret_cast<int8_t *>(Xs),
-                                                       reinterpret_cast<uint4 *>(info));
+                                                       reinterpret_cast<uint4 *>(info)));
   return launch_status("mrpt_u8_gemm_rows");
 }
 
@@ -2261,7 +2261,7 @@ static int32_t u8gemm_impl(const float *X, int64_t n, int32_t d, int64_t ldx, co
   for (int64_t q0 = 0; q0 < nq; q0 += mc) {
     const int64_t m = nq - q0 < mc ? nq - q0 : mc;
     const int64_t g1 = m < (int64_t)num_sms() * 8 ? m : (int64_t)num_sms() * 8;
-    k_quantize_q8<<<(unsigned)g1, kScanNT, 0, s>>>(Q + q0 * ldqq, ldqq, d, (int)ldq, m, qop, qp);
+    (count_launch(), k_quantize_q8<<<(unsigned)g1, kScanNT, 0, s>>>(Q + q0 * ldqq, ldqq, d, (int)ldq, m, qop, qp));
     int32_t st = igemm_rows_tn(reinterpret_cast<const int8_t *>(Xs), n, qop, m, ldq, D, ldD, s);
     if (st) return st;
     TopkArgs a = {};
@@ -2295,10 +2295,10 @@ static int32_t u8gemm_impl(const float *X, int64_t n, int32_t d, int64_t ldx, co
     a.surv = a.nsurv + mc;
     cudaMemsetAsync(fb, 0, sizeof(int32_t), s);
     const int64_t grid = m < (int64_t)num_sms() * 8 ? m : (int64_t)num_sms() * 8;
-    fn<<<(unsigned)grid, kScanNT, smem, s>>>(a, rows, fb + 1, fb);
+    (count_launch(), fn<<<(unsigned)grid, kScanNT, smem, s>>>(a, rows, fb + 1, fb));
     a.qlist = fb + 1;
     a.qcount = fb;
-    tfn<<<(unsigned)(grid < 64 ? grid : 64), kScanNT, tsmem, s>>>(a);
+    (count_launch(), tfn<<<(unsigned)(grid < 64 ? grid : 64), kScanNT, tsmem, s>>>(a));
     launch_rerank(a, s);
   }
   return launch_status("mrpt_scan_topk_u8gemm");

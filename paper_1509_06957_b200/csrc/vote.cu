@@ -609,7 +609,7 @@ typedef void (*vote_fn)(VoteArgs);
 typedef void (*union_fn)(VoteArgs, int);
 static inline void k_vote_union_launch(union_fn fn, unsigned grid, int nt, size_t smem, cudaStream_t s,
                                        const VoteArgs &a, int G) {
-  fn<<<grid, nt, smem, s>>>(a, G);
+  (count_launch(), fn<<<grid, nt, smem, s>>>(a, G));
 }
 
 template <int CW, bool SORTED>
@@ -787,7 +787,7 @@ extern "C" int32_t mrpt_vote_build_dir(const int32_t *leaf_indices, const int64_
   const int64_t nleaves = (int64_t)T << depth;
   const int64_t blocks = ceil_div<int64_t>(nleaves, 8);
   const int grid = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
-  k_build_dir<<<grid, 256, 0, s>>>(leaf_indices, leaf_offsets, n, T, 1 << depth, (int)W, nt, dir);
+  (count_launch(), k_build_dir<<<grid, 256, 0, s>>>(leaf_indices, leaf_offsets, n, T, 1 << depth, (int)W, nt, dir));
   return launch_status("mrpt_vote_build_dir");
 }
 
@@ -871,11 +871,11 @@ static int32_t vote_impl(const int32_t *leaf_indices, const int64_t *leaf_offset
                    : (CW == 2 ? k_vote_dir<2, 1024> : (CW == 3 ? k_vote_dir<3, 1024> : k_vote_dir<4, 1024>));
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int64_t g2 = nt == 512 ? (nq < (int64_t)num_sms() * 8 ? nq : (int64_t)num_sms() * 8) : grid;
-    fn<<<(unsigned)g2, nt, smem, s>>>(a);
+    (count_launch(), fn<<<(unsigned)g2, nt, smem, s>>>(a));
   } else {
     vote_fn fn = sorted ? pick_cw<true>(CW, G) : pick_cw<false>(CW, G);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    fn<<<(unsigned)grid, kVoteNT, smem, s>>>(a);
+    (count_launch(), fn<<<(unsigned)grid, kVoteNT, smem, s>>>(a));
   }
   return launch_status("mrpt_vote");
 }
@@ -906,7 +906,7 @@ extern "C" int32_t mrpt_vote_counts(const int32_t *leaf_indices, const int64_t *
   if (n < 1 || T < 1 || depth < 0 || depth > 30) return fail(MRPT_ESHAPE, "mrpt_vote_counts: bad shape");
   cudaStream_t s = as_stream(stream);
   cudaMemsetAsync(counts, 0, sizeof(int32_t) * n, s);
-  k_vote_dense<<<T, 256, 0, s>>>(leaf_indices, leaf_offsets, n, 1 << depth, leaves, counts);
+  (count_launch(), k_vote_dense<<<T, 256, 0, s>>>(leaf_indices, leaf_offsets, n, 1 << depth, leaves, counts));
   return launch_status("mrpt_vote_counts");
 }
 
@@ -915,7 +915,7 @@ extern "C" int32_t mrpt_select_ge(const int32_t *counts, int64_t n, int32_t v, i
   clear_error();
   if (n < 0) return fail(MRPT_ESHAPE, "mrpt_select_ge: bad shape");
   cudaStream_t s = as_stream(stream);
-  k_select_ge<<<1, 1024, 0, s>>>(counts, n, v, out, nout);
+  (count_launch(), k_select_ge<<<1, 1024, 0, s>>>(counts, n, v, out, nout));
   return launch_status("mrpt_select_ge");
 }
 
@@ -930,8 +930,8 @@ extern "C" int32_t mrpt_unique_ids(const int64_t *cand, int64_t m, int64_t n, ui
   if (m > 0) {
     const int64_t blocks = ceil_div<int64_t>(m, 256);
     const int grid = (int)(blocks < (int64_t)num_sms() * 8 ? blocks : (int64_t)num_sms() * 8);
-    k_mark_ids<<<grid, 256, 0, s>>>(cand, m, n, bitmap, bad);
+    (count_launch(), k_mark_ids<<<grid, 256, 0, s>>>(cand, m, n, bitmap, bad));
   }
-  k_bitmap_compact<<<1, 1024, 0, s>>>(bitmap, nwords, out, nout);
+  (count_launch(), k_bitmap_compact<<<1, 1024, 0, s>>>(bitmap, nwords, out, nout));
   return launch_status("mrpt_unique_ids");
 }

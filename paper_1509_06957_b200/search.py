@@ -258,10 +258,13 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
               _native.ptr(D.vals), _native.ptr(D.splits), D.T, D.depth, _native.ptr(leaves),
               stream)
         if choice is None and e - s >= 256:
-            # the autotune's last run leaves this chunk's outputs
-            choice = _autotune(D, qb, e - s, int(Qd.stride(0)), leaves, votes, vdir, cap,
-                               counts[s:e], k, ids[s:e], dists[s:e])
-            continue
+            # the autotune's last run leaves this chunk's outputs; the rest of
+            # the batch runs the chosen route (its own chunking)
+            _autotune(D, qb, e - s, int(Qd.stride(0)), leaves, votes, vdir, cap, counts[s:e], k,
+                      ids[s:e], dists[s:e])
+            if e < nq:
+                query_device(D, Qd[e:], k, votes, out=(ids[e:], dists[e:], counts[e:]), timer=timer)
+            return ids, dists, counts
         if bits_mode:
             stage("vote", _vote_bitmap, D, leaves, e - s, votes, vdir, bits, bstride, counts[s:e])
             stage("scan_topk", _scan_bits, D, qb, e - s, int(Qd.stride(0)), bits, bstride, k,

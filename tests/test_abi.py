@@ -39,7 +39,8 @@ def test_every_declared_symbol_is_exported(lib):
 
 
 def test_version_and_error_text(lib):
-    assert lib.mrpt_abi_version() == 100
+    assert lib.mrpt_abi_version() == 101
+    assert lib.mrpt_launch_count() == 0  # nothing launched in this CPU-only process
     sz = ctypes.c_size_t(0)
     st = lib.mrpt_build_workspace_size(0, 1, 3, ctypes.byref(sz))
     assert st == _native.MRPT_ESHAPE
