@@ -60,6 +60,8 @@ struct LevelArgs {
   uint32_t *ghist;  // (maxbig, 256)
   int2 *chunks;
   int32_t *chunk_left, *chunk_off;
+  int32_t *tree_nch;   // (Tb) big-path chunks per tree this level
+  int64_t *tree_base;  // (Tb) first chunk of each tree (tree-major chunk order)
 };
 
 __device__ __forceinline__ void write_node(const LevelArgs &a, int t, int s, int64_t b, int64_t e,
@@ -170,7 +172,10 @@ __global__ void k_level_plan(LevelArgs a) {
   } else {
     const int slot = atomicAdd(&a.ctl->nbig, 1);
     const int nch = (int)ceil_div<int64_t>(m, kChunk);
-    const int64_t cb = (int64_t)atomicAdd((unsigned long long *)&a.ctl->nchunks, (unsigned long long)nch);
+    // chunk position within its tree; k_chunk_layout adds the tree's base so
+    // the chunk table is tree-major (concurrent CTAs gather from the same
+    // tree's projection column, which then stays in L2)
+    const int64_t cb = (int64_t)atomicAdd(&a.tree_nch[t], nch);
     BigSeg g;
     g.b = b;
     g.e = e;
@@ -188,9 +193,57 @@ __global__ void k_level_plan(LevelArgs a) {
     g.cnt_last = 0;
     g.nle = 0;
     a.big[slot] = g;
-    for (int c = 0; c < nch; ++c) a.chunks[cb + c] = make_int2(slot, c);
     uint32_t *h = a.ghist + (int64_t)slot * 256;
     for (int i = 0; i < 256; ++i) h[i] = 0u;
+  }
+}
+
+// Tree-major chunk table: exclusive scan of the per-tree chunk counts (one
+// CTA), then one warp per big segment rebases its chunks and writes them.
+__global__ void __launch_bounds__(1024) k_chunk_layout(LevelArgs a) {
+  __shared__ int64_t wsum[33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t carry = 0;
+  for (int t0 = 0; t0 < a.Tb; t0 += 1024) {
+    const int t = t0 + threadIdx.x;
+    const int64_t v = t < a.Tb ? a.tree_nch[t] : 0;
+    int64_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const int64_t c = wsum[lane];
+      int64_t x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t u = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += u;
+      }
+      wsum[lane] = x - c;
+      if (lane == 31) wsum[32] = x;
+    }
+    __syncthreads();
+    if (t < a.Tb) a.tree_base[t] = carry + wsum[warp] + incl - v;
+    carry += wsum[32];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.ctl->nchunks = carry;
+}
+
+__global__ void k_chunk_fill(LevelArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int nbig = a.ctl->nbig;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < nbig; i += wstride) {
+    BigSeg *g = a.big + i;
+    const int64_t cb = g->chunk_base + a.tree_base[g->t];
+    __syncwarp();
+    if (lane == 0) g->chunk_base = cb;
+    for (int c = lane; c < g->nchunks; c += 32) a.chunks[cb + c] = make_int2((int)i, c);
   }
 }
 
@@ -558,7 +611,7 @@ __global__ void __launch_bounds__(kNT) k_big_scatter(LevelArgs a) {
 
 // ---------------------------------------------------------------------------
 struct WsLayout {
-  size_t order_tmp, bounds_tmp, keys, ctl, tiny, mid, big, ghist, chunks, cleft, coff, total;
+  size_t order_tmp, bounds_tmp, keys, ctl, tiny, mid, big, ghist, chunks, cleft, coff, tnch, tbase, total;
 };
 
 static size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -583,6 +636,8 @@ static WsLayout layout(int64_t n, int Tb, int depth) {
   L.chunks = off; off = align_up(off + sizeof(int2) * (size_t)maxchunks);
   L.cleft = off; off = align_up(off + sizeof(int32_t) * (size_t)maxchunks);
   L.coff = off; off = align_up(off + sizeof(int32_t) * (size_t)maxchunks);
+  L.tnch = off; off = align_up(off + sizeof(int32_t) * (size_t)Tb);
+  L.tbase = off; off = align_up(off + sizeof(int64_t) * (size_t)Tb);
   L.total = off;
   return L;
 }
@@ -658,7 +713,10 @@ extern "C" int32_t mrpt_build_levels(const float *P, int64_t n, int32_t Tb, int3
     a.chunks = reinterpret_cast<int2 *>(w + L.chunks);
     a.chunk_left = reinterpret_cast<int32_t *>(w + L.cleft);
     a.chunk_off = reinterpret_cast<int32_t *>(w + L.coff);
+    a.tree_nch = reinterpret_cast<int32_t *>(w + L.tnch);
+    a.tree_base = reinterpret_cast<int64_t *>(w + L.tbase);
     cudaMemsetAsync(a.ctl, 0, sizeof(LevelCtl), s);
+    cudaMemsetAsync(a.tree_nch, 0, sizeof(int32_t) * (size_t)Tb, s);
     const int64_t nsegs = (int64_t)Tb << lev;
     (count_launch(), k_level_plan<<<(unsigned)ceil_div<int64_t>(nsegs, 256), 256, 0, s>>>(a));
     // expected per-segment size decides how many CTAs the small paths get
@@ -672,6 +730,8 @@ extern "C" int32_t mrpt_build_levels(const float *P, int64_t n, int32_t Tb, int3
       // the big path may have work whenever a segment can exceed kMidMax;
       // after level 0 ties can make any segment large, so always launch.
       const int big_grid = sms * 4;
+      (count_launch(), k_chunk_layout<<<1, 1024, 0, s>>>(a));
+      (count_launch(), k_chunk_fill<<<sms * 2, 256, 0, s>>>(a));
       (count_launch(), k_big_keys<<<big_grid, kNT, 0, s>>>(a));
       (count_launch(), k_big_init<<<ceil_div<int>(sms, 1), 256, 0, s>>>(a));
       for (int pass = 0; pass < 4; ++pass) {
