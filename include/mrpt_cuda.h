@@ -230,7 +230,7 @@ int32_t mrpt_u8_gemm_rows(const void *Xq, int64_t n, int64_t ldq, const float *s
                           void *info, void *stream);
 
 /* Workspace bytes mrpt_scan_topk_u8gemm needs for nq queries (it runs
- * queries in chunks whose dot-product matrix is <= 1 GiB). */
+ * queries in chunks whose dot-product matrix is <= 4 GiB). */
 int32_t mrpt_scan_topk_u8gemm_workspace_size(int64_t n, int64_t ldq, int64_t nq,
                                              int64_t *bytes);
 
@@ -252,14 +252,16 @@ int32_t mrpt_scan_topk_u8gemm(const float *X, int64_t n, int32_t d, int64_t ldx,
                               void *stream);
 
 /* mrpt_scan_topk_u8gemm over candidate bitmaps (mrpt_vote_bitmap) instead of
- * lists: each warp walks its query's bitmap words, reading the dot products
- * of a word's 32 ids in one coalesced access.  k <= 96.  Same results. */
+ * lists: each warp takes its query's bitmap 16 words at a time and admits
+ * the set ids 32 per round.  k <= 96.  Same results.  wait_event (a
+ * cudaEvent_t, or NULL): the filter waits for it after the first chunk's
+ * GEMM, so the bitmaps may be produced on another stream while the GEMM runs. */
 int32_t mrpt_scan_topk_u8gemm_bits(const float *X, int64_t n, int32_t d, int64_t ldx,
                                    const void *Xs, int64_t ldq, const void *info,
                                    const float *Q, int64_t nq, int64_t ldqq,
                                    const uint32_t *cbits, int64_t bstride, int32_t k,
                                    int64_t *ids, double *dists, void *workspace,
-                                   int64_t ws_bytes, void *stream);
+                                   int64_t ws_bytes, void *wait_event, void *stream);
 
 /* Sorted de-duplication of arbitrary candidate ids (np.unique,
  * search.py:157) through an n-bit bitmap.  ids outside [0, n) set

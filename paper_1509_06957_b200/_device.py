@@ -36,6 +36,18 @@ def side_streams():
     return _SIDE[dev]
 
 
+_VOTE = {}
+
+
+def vote_stream():
+    """A CUDA stream per device for K3 running beside K4's GEMM."""
+    torch = torch_mod()
+    dev = torch.cuda.current_device()
+    if dev not in _VOTE:
+        _VOTE[dev] = torch.cuda.Stream(device=dev)
+    return _VOTE[dev]
+
+
 def h2d(arr, dtype=None):
     """Copy a host array to the current device (pinned staging for big arrays)."""
     torch = torch_mod()

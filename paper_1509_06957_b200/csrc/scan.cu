@@ -2189,7 +2189,7 @@ static int64_t u8gemm_bytes(int64_t n, int64_t ldq, int64_t mc, int64_t *off_qop
   return al(o + ((mc + 1) + mc * (kSurvCap + 1)) * 4);
 }
 
-static const int64_t kGemmChunkD = (int64_t)1 << 30;  // D bytes per query chunk
+static const int64_t kGemmChunkD = (int64_t)1 << 32;  // D bytes per query chunk
 
 extern "C" int32_t mrpt_scan_topk_u8gemm_workspace_size(int64_t n, int64_t ldq, int64_t nq, int64_t *bytes) {
   clear_error();
@@ -2205,7 +2205,8 @@ extern "C" int32_t mrpt_scan_topk_u8gemm_workspace_size(int64_t n, int64_t ldq, 
 static int32_t u8gemm_impl(const float *X, int64_t n, int32_t d, int64_t ldx, const void *Xs, int64_t ldq,
                            const void *info, const float *Q, int64_t nq, int64_t ldqq, const int32_t *cand,
                            int64_t cap, const int32_t *ncand, const uint32_t *cbits, int64_t bstride, int32_t k,
-                           int64_t *ids, double *dists, void *workspace, int64_t ws_bytes, void *stream) {
+                           int64_t *ids, double *dists, void *workspace, int64_t ws_bytes, void *stream,
+                           void *wait_event) {
   if (cbits && (bstride < (n + 31) / 32 || cand))
     return fail(MRPT_EPARAM, "mrpt_scan_topk_u8gemm_bits: bad candidate bitmaps");
   if (cbits && (!Xs || !info || ldq % 16 != 0 || ldq < d || ldq > 1024 || k > 96 || k < 1 || d % 4 != 0 ||
@@ -2264,6 +2265,8 @@ static int32_t u8gemm_impl(const float *X, int64_t n, int32_t d, int64_t ldx, co
     (count_launch(), k_quantize_q8<<<(unsigned)g1, kScanNT, 0, s>>>(Q + q0 * ldqq, ldqq, d, (int)ldq, m, qop, qp));
     int32_t st = igemm_rows_tn(reinterpret_cast<const int8_t *>(Xs), n, qop, m, ldq, D, ldD, s);
     if (st) return st;
+    // candidates produced on another stream (the vote runs beside the GEMM)
+    if (wait_event && q0 == 0) cudaStreamWaitEvent(s, reinterpret_cast<cudaEvent_t>(wait_event), 0);
     TopkArgs a = {};
     a.X = X;
     a.n = n;
@@ -2311,16 +2314,16 @@ extern "C" int32_t mrpt_scan_topk_u8gemm(const float *X, int64_t n, int32_t d, i
                                          int64_t ws_bytes, void *stream) {
   clear_error();
   return u8gemm_impl(X, n, d, ldx, Xs, ldq, info, Q, nq, ldqq, cand, cap, ncand, nullptr, 0, k, ids, dists,
-                     workspace, ws_bytes, stream);
+                     workspace, ws_bytes, stream, nullptr);
 }
 
 extern "C" int32_t mrpt_scan_topk_u8gemm_bits(const float *X, int64_t n, int32_t d, int64_t ldx,
                                               const void *Xs, int64_t ldq, const void *info, const float *Q,
                                               int64_t nq, int64_t ldqq, const uint32_t *cbits, int64_t bstride,
                                               int32_t k, int64_t *ids, double *dists, void *workspace,
-                                              int64_t ws_bytes, void *stream) {
+                                              int64_t ws_bytes, void *wait_event, void *stream) {
   clear_error();
   if (!cbits) return fail(MRPT_EPARAM, "mrpt_scan_topk_u8gemm_bits: cbits is NULL");
   return u8gemm_impl(X, n, d, ldx, Xs, ldq, info, Q, nq, ldqq, nullptr, 0, nullptr, cbits, bstride, k, ids,
-                     dists, workspace, ws_bytes, stream);
+                     dists, workspace, ws_bytes, stream, wait_event);
 }

@@ -266,9 +266,21 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
                 query_device(D, Qd[e:], k, votes, out=(ids[e:], dists[e:], counts[e:]), timer=timer)
             return ids, dists, counts
         if bits_mode:
-            stage("vote", _vote_bitmap, D, leaves, e - s, votes, vdir, bits, bstride, counts[s:e])
+            # the vote (K3) runs on its own stream beside the query quantisation
+            # and tensor-core GEMM of K4; the filter waits for it
+            vs = _device.vote_stream()
+            ev_route = torch.cuda.Event()
+            ev_route.record()
+            with torch.cuda.stream(vs):
+                vs.wait_event(ev_route)
+                stage("vote", _vote_bitmap, D, leaves, e - s, votes, vdir, bits, bstride,
+                      counts[s:e])
+                ev_vote = torch.cuda.Event()
+                ev_vote.record(vs)
             stage("scan_topk", _scan_bits, D, qb, e - s, int(Qd.stride(0)), bits, bstride, k,
-                  ids[s:e], dists[s:e])
+                  ids[s:e], dists[s:e], ev_vote)
+            if e < nq:
+                torch.cuda.current_stream().wait_event(ev_vote)  # leaves/bits are reused
             continue
         if cand is None:
             cand = torch.empty((m0, cap), dtype=torch.int32, device=dev)
@@ -298,13 +310,14 @@ def _vote_bitmap(D, leaves, m, votes, vdir, bits, bstride, counts):
                  _native.ptr(counts), _native.stream_ptr())
 
 
-def _scan_bits(D, qb, m, ldq, bits, bstride, k, ids, dists):
+def _scan_bits(D, qb, m, ldq, bits, bstride, k, ids, dists, wait=None):
     ldr = D.u8_rows()[1]
     Xs, info, ws = D.u8_gemm(m)
     _native.call("mrpt_scan_topk_u8gemm_bits", _native.ptr(D.X), D.n, D.d, int(D.X.stride(0)),
                  _native.ptr(Xs), ldr, _native.ptr(info), _native.ptr(qb), m, ldq,
                  _native.ptr(bits), int(bstride), int(k), _native.ptr(ids), _native.ptr(dists),
-                 _native.ptr(ws), int(ws.numel()), _native.stream_ptr())
+                 _native.ptr(ws), int(ws.numel()), None if wait is None else wait.cuda_event,
+                 _native.stream_ptr())
 
 
 def _scan_variants(D, k):

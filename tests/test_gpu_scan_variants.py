@@ -131,7 +131,7 @@ def test_u8gemm_small_workspace_chunks(rng, kind, signed):
     _native.call("mrpt_scan_topk_u8gemm_bits", _native.ptr(D.X), n, d, int(D.X.stride(0)),
                  _native.ptr(Xs), ldq, _native.ptr(info), _native.ptr(Qd), nq, d,
                  _native.ptr(bits), bstride, k, _native.ptr(ids), _native.ptr(dists),
-                 _native.ptr(ws), int(ws.numel()), _native.stream_ptr())
+                 _native.ptr(ws), int(ws.numel()), None, _native.stream_ptr())
     assert np.array_equal(ids.cpu().numpy(), want[0])
     assert dists.cpu().numpy().tobytes() == want[1].tobytes()
     # a workspace too small for one query is refused
