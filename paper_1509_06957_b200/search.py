@@ -249,14 +249,28 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
     leaves = torch.empty((m0, D.T), dtype=torch.int32, device=dev)
     cand = None
     bits = torch.empty((m0, bstride), dtype=torch.int32, device=dev) if bits_mode else None
-    stream = _native.stream_ptr()
     for s in range(0, nq, chunk):
         e = min(nq, s + chunk)
         qb = Qd[s:e]
-        stage("route", _native.call, "mrpt_query_route", _native.ptr(qb), e - s, D.d,
-              int(Qd.stride(0)), _native.ptr(D.col_ptr), _native.ptr(D.rows),
-              _native.ptr(D.vals), _native.ptr(D.splits), D.T, D.depth, _native.ptr(leaves),
-              stream)
+        if bits_mode:
+            # K2 + K3 run on their own stream beside K4's query quantisation and
+            # tensor-core GEMM (which need only the queries); the filter waits
+            # for the candidate bitmaps
+            vs = _device.vote_stream()
+            ev_start = torch.cuda.Event()
+            ev_start.record()
+            with torch.cuda.stream(vs):
+                vs.wait_event(ev_start)
+                stage("route", _route_launch, D, qb, e - s, int(Qd.stride(0)), leaves)
+                stage("vote", _vote_bitmap, D, leaves, e - s, votes, vdir, bits, bstride,
+                      counts[s:e])
+                ev_vote = torch.cuda.Event()
+                ev_vote.record(vs)
+            stage("scan_topk", _scan_bits, D, qb, e - s, int(Qd.stride(0)), bits, bstride, k,
+                  ids[s:e], dists[s:e], ev_vote)
+            torch.cuda.current_stream().wait_event(ev_vote)  # leaves/bits are reused
+            continue
+        stage("route", _route_launch, D, qb, e - s, int(Qd.stride(0)), leaves)
         if choice is None and e - s >= 256:
             # the autotune's last run leaves this chunk's outputs; the rest of
             # the batch runs the chosen route (its own chunking)
@@ -265,23 +279,6 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
             if e < nq:
                 query_device(D, Qd[e:], k, votes, out=(ids[e:], dists[e:], counts[e:]), timer=timer)
             return ids, dists, counts
-        if bits_mode:
-            # the vote (K3) runs on its own stream beside the query quantisation
-            # and tensor-core GEMM of K4; the filter waits for it
-            vs = _device.vote_stream()
-            ev_route = torch.cuda.Event()
-            ev_route.record()
-            with torch.cuda.stream(vs):
-                vs.wait_event(ev_route)
-                stage("vote", _vote_bitmap, D, leaves, e - s, votes, vdir, bits, bstride,
-                      counts[s:e])
-                ev_vote = torch.cuda.Event()
-                ev_vote.record(vs)
-            stage("scan_topk", _scan_bits, D, qb, e - s, int(Qd.stride(0)), bits, bstride, k,
-                  ids[s:e], dists[s:e], ev_vote)
-            if e < nq:
-                torch.cuda.current_stream().wait_event(ev_vote)  # leaves/bits are reused
-            continue
         if cand is None:
             cand = torch.empty((m0, cap), dtype=torch.int32, device=dev)
         stage("vote", _vote_list, D, leaves, e - s, votes, vdir, cand, cap, counts[s:e])
@@ -294,6 +291,12 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
 def _bstride(D):
     """Words per query of a candidate bitmap (16-byte rows)."""
     return (D.n + 127) // 128 * 4
+
+
+def _route_launch(D, qb, m, ldq, leaves):
+    _native.call("mrpt_query_route", _native.ptr(qb), m, D.d, int(ldq), _native.ptr(D.col_ptr),
+                 _native.ptr(D.rows), _native.ptr(D.vals), _native.ptr(D.splits), D.T, D.depth,
+                 _native.ptr(leaves), _native.stream_ptr())
 
 
 def _vote_list(D, leaves, m, votes, vdir, cand, cap, counts):
