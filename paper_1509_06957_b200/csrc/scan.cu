@@ -1306,10 +1306,15 @@ __device__ __forceinline__ QParams quantize_query_u8(const float *qrow, int d, i
 // |A - D| <= 8 * 2^-24 * (t1 + t2 + |t3|)), admission against the warp's
 // running k-th upper bound, buffer append, and a shrink when the buffer is
 // full; false when it cannot shrink (-> exact fallback).
+// su_cta: the smallest sqrt(k-th upper bound) any warp of the CTA has
+// established for this query (float bits; every warp's k-th bound bounds the
+// query's k-th, so each warp may filter with the smallest).
 template <int BUFW, int CPI>
 __device__ __forceinline__ bool admit_lane_u8(int32_t myc, int mys, float sx, int nrm, float rad, float sqf,
                                               float t2f, float rq, float &su, int &cnt, float *ma, float *mr,
-                                              float *me, int32_t *mi, int kk, float *cu_w, int32_t *cid_w) {
+                                              float *me, int32_t *mi, int kk, float *cu_w, int32_t *cid_w,
+                                              unsigned *su_cta) {
+  su = fminf(su, __uint_as_float(*reinterpret_cast<volatile unsigned *>(su_cta)));
   float A = 0.f, r = 0.f, eta = 0.f;
   if (myc >= 0) {
     const float t1 = sx * sx * (float)nrm;
@@ -1331,6 +1336,7 @@ __device__ __forceinline__ bool admit_lane_u8(int32_t myc, int mys, float sx, in
   if (cnt > BUFW - CPI) {
     __syncwarp();
     cnt = shrink_bounds2<BUFW>(ma, mr, me, mi, cnt, kk, cu_w, cid_w, &su);
+    if ((threadIdx.x & 31) == 0) atomicMin(su_cta, __float_as_uint(su));
     if (cnt > BUFW - CPI) return false;
   }
   return true;
@@ -1361,6 +1367,7 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
   int32_t *wq_base = reinterpret_cast<int32_t *>(cl + NWARP * BUFW);  // DM bitmap mode: 512 ids per warp
   __shared__ int s_wcnt[NWARP];
   __shared__ int s_bad, s_ns;
+  __shared__ unsigned s_su_cta;
   __shared__ QScratch<NWARP> qscr;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float *ma = wa + warp * BUFW;
@@ -1374,7 +1381,10 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
   const int grp = lane / G, gl = lane % G;
   for (int64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
     const float *qrow = a.Q + q * a.ldq;
-    if (tid == 0) s_bad = 0;
+    if (tid == 0) {
+      s_bad = 0;
+      s_su_cta = 0x7f800000u;  // +inf
+    }
     QParams P;
     if (DM) {
       P = rows.qp[q];
@@ -1404,7 +1414,8 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
     float *cu_w = cu + warp * BUFW;
     int32_t *cid_w = cid + warp * BUFW;
 #define ADMIT_LANE(MYC, MYS, SX, NRM, RAD) \
-  admit_lane_u8<BUFW, CPI>((MYC), (MYS), (SX), (NRM), (RAD), sqf, t2f, rq, su, cnt, ma, mr, me, mi, kk, cu_w, cid_w)
+  admit_lane_u8<BUFW, CPI>((MYC), (MYS), (SX), (NRM), (RAD), sqf, t2f, rq, su, cnt, ma, mr, me, mi, kk, cu_w, cid_w, \
+                           &s_su_cta)
     if (DM && rows.cbits) {
       // candidate bitmap: lanes 0..15 each load one of 16 consecutive words
       // and write their set bits' ids, in id order, to the warp's queue at
