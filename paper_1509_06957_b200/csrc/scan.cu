@@ -1436,9 +1436,16 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
         }
         const int total = __shfl_sync(0xffffffffu, incl, 31);
         {
-          int p = incl - pc;
-          uint32_t wd = word;
-          const int32_t id0 = (w0 + lane) * 32;
+          // lane l writes the low 16 bits of word l, lane l+16 its high 16 bits
+          const int src = lane & 15;
+          const uint32_t w = __shfl_sync(0xffffffffu, word, src);
+          int p = __shfl_sync(0xffffffffu, incl - pc, src);
+          uint32_t wd = w & 0xffffu;
+          if (lane >= 16) {
+            p += __popc(wd);
+            wd = w & 0xffff0000u;
+          }
+          const int32_t id0 = (w0 + src) * 32;
           while (wd) {
             queue[p++] = id0 + __ffs(wd) - 1;
             wd &= wd - 1u;
