@@ -223,8 +223,9 @@ int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64_t ldx,
                           double *dists, void *stream);
 
 /* GEMM operands of the u8 shadow for mrpt_scan_topk_u8gemm: Xs = Xq ^ 0x80
- * (s8, same (n, ldq) layout) and info (n x 16 bytes, 16-byte aligned): per
- * row {scale (f32), norm (s32), radius (f32), sum of the u8 entries (s32)}. */
+ * (s8, row stride ldq, room for round_up(n, 16) rows -- the rows past n are
+ * zeroed here) and info (n x 16 bytes, 16-byte aligned): per row {scale
+ * (f32), norm (s32), radius (f32), sum of the u8 entries (s32)}. */
 int32_t mrpt_u8_gemm_rows(const void *Xq, int64_t n, int64_t ldq, const float *scale,
                           const int32_t *norm, const float *radius, void *Xs,
                           void *info, void *stream);

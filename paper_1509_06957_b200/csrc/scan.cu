@@ -2180,6 +2180,11 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
 extern "C" int32_t mrpt_u8_gemm_rows(const void *Xq, int64_t n, int64_t ldq, const float *scale,
                                      const int32_t *norm, const float *radius, void *Xs, void *info,
                                      void *stream) {
+  // Xs holds round_up(n, 16) rows: the GEMM runs over whole 16-row groups
+  // (cuBLASLt's int8 kernels want the row count a multiple of 4); pad rows are 0
+  const int64_t n16 = (n + 15) & ~(int64_t)15;
+  if (Xs && n16 > n)
+    cudaMemsetAsync(reinterpret_cast<int8_t *>(Xs) + n * ldq, 0, (size_t)((n16 - n) * ldq), as_stream(stream));
   clear_error();
   if (!Xq || !Xs || !info || !scale || !norm || !radius || n < 1 || ldq < 16 || ldq % 16 != 0 || ldq > 1024)
     return fail(MRPT_ESHAPE, "mrpt_u8_gemm_rows: bad shape");
@@ -2197,7 +2202,7 @@ extern "C" int32_t mrpt_u8_gemm_rows(const void *Xq, int64_t n, int64_t ldq, con
 static int64_t u8gemm_bytes(int64_t n, int64_t ldq, int64_t mc, int64_t *off_qop, int64_t *off_qp,
                             int64_t *off_fb) {
   auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
-  const int64_t ldD = (n + 3) & ~(int64_t)3;
+  const int64_t ldD = (n + 15) & ~(int64_t)15;
   int64_t o = al(mc * ldD * 4);
   if (off_qop) *off_qop = o;
   o = al(o + mc * ldq);
@@ -2212,7 +2217,7 @@ static const int64_t kGemmChunkD = (int64_t)1 << 32;  // D bytes per query chunk
 extern "C" int32_t mrpt_scan_topk_u8gemm_workspace_size(int64_t n, int64_t ldq, int64_t nq, int64_t *bytes) {
   clear_error();
   if (n < 1 || ldq < 16 || nq < 0 || !bytes) return fail(MRPT_ESHAPE, "mrpt_scan_topk_u8gemm_workspace_size");
-  const int64_t ldD = (n + 3) & ~(int64_t)3;
+  const int64_t ldD = (n + 15) & ~(int64_t)15;
   int64_t mc = kGemmChunkD / (4 * ldD);
   if (mc > nq) mc = nq;
   if (mc < 1) mc = 1;
@@ -2239,8 +2244,8 @@ static int32_t u8gemm_impl(const float *X, int64_t n, int32_t d, int64_t ldx, co
   if (nq == 0) return MRPT_OK;
   if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255u))
     return fail(MRPT_EWORKSPACE, "mrpt_scan_topk_u8gemm: workspace must be 256-byte aligned");
-  // largest query chunk whose workspace fits
-  const int64_t ldD = (n + 3) & ~(int64_t)3;
+  // largest query chunk whose workspace fits; the GEMM covers n16 rows
+  const int64_t ldD = (n + 15) & ~(int64_t)15;
   int64_t mc = ws_bytes / (4 * ldD + ldq + (int64_t)sizeof(QParams) + 4 * (kSurvCap + 2));
   if (mc > nq) mc = nq;
   while (mc > 0 && u8gemm_bytes(n, ldq, mc, nullptr, nullptr, nullptr) > ws_bytes) --mc;
@@ -2281,7 +2286,7 @@ static int32_t u8gemm_impl(const float *X, int64_t n, int32_t d, int64_t ldx, co
     const int64_t m = nq - q0 < mc ? nq - q0 : mc;
     const int64_t g1 = m < (int64_t)num_sms() * 8 ? m : (int64_t)num_sms() * 8;
     (count_launch(), k_quantize_q8<<<(unsigned)g1, kScanNT, 0, s>>>(Q + q0 * ldqq, ldqq, d, (int)ldq, m, qop, qp));
-    int32_t st = igemm_rows_tn(reinterpret_cast<const int8_t *>(Xs), n, qop, m, ldq, D, ldD, s);
+    int32_t st = igemm_rows_tn(reinterpret_cast<const int8_t *>(Xs), ldD, qop, m, ldq, D, ldD, s);
     if (st) return st;
     // candidates produced on another stream (the vote runs beside the GEMM)
     if (wait_event && q0 == 0) cudaStreamWaitEvent(s, reinterpret_cast<cudaEvent_t>(wait_event), 0);

@@ -221,7 +221,7 @@ class _DeviceIndex:
         torch = _device.torch_mod()
         Xq, ldq = u8[0], u8[1]
         if getattr(self, "_u8g", None) is None:
-            Xs = torch.empty_like(Xq)
+            Xs = torch.empty(((self.n + 15) // 16 * 16, ldq), dtype=torch.uint8, device=Xq.device)
             info = torch.empty((self.n, 4), dtype=torch.int32, device=Xq.device)
             _native.call("mrpt_u8_gemm_rows", _native.ptr(Xq), self.n, ldq, _native.ptr(u8[2]),
                          _native.ptr(u8[3]), _native.ptr(u8[4]), _native.ptr(Xs),

@@ -140,3 +140,32 @@ def test_u8gemm_small_workspace_chunks(rng, kind, signed):
                      _native.ptr(Xs), ldq, _native.ptr(info), _native.ptr(Qd), nq, d,
                      _native.ptr(cand), int(cap), _native.ptr(counts), k, _native.ptr(ids),
                      _native.ptr(dists), _native.ptr(ws), 1024, _native.stream_ptr())
+
+
+@pytest.mark.parametrize("v,k", [(6, 8), (5, 40), (1, 96)])
+def test_bitmap_route_edges(monkeypatch, rng, v, k):
+    """The bitmap hand-over + GEMM filter at the edges: v = T (mostly empty
+    candidate sets), k larger than most candidate sets (-1 / inf padding),
+    k at its limit; a foreign index with unsorted leaf slices; n not a
+    multiple of 32."""
+    monkeypatch.setenv("MRPT_SCAN_ROWS", "u8gemm_bits")
+    n, d, nq = 3001, 40, 300
+    X = _data("ints", rng, n + nq, d)
+    Xd, Q = X[:n], X[n:]
+    a = mrpt.grow_trees(Xd, 6, 6, seed=21)
+    li = a.leaf_indices.copy()
+    for t in range(6):
+        o = a.leaf_offsets[t]
+        for j in range(len(o) - 1):
+            li[t, o[j]:o[j + 1]] = li[t, o[j]:o[j + 1]][rng.permutation(o[j + 1] - o[j])]
+    b = mrpt.MRPTIndex(dataset=mrpt.Dataset(Xd), n_trees=6, depth=6, sparsity=a.sparsity, seed=21,
+                       fixed_count=False, matrices=a.matrices, splits=a.splits,
+                       leaf_offsets=a.leaf_offsets, leaf_indices=li,
+                       dataset_checksum=a.dataset_checksum)
+    for index in (a, b):
+        ids, dists, counts = mrpt.approximate_knn_batch(Q, k, index, v)
+        assert index.device_index().scan_choice.get((k, v)) == "u8gemm_bits"
+        rids, rd, rc = _oracle(index, Xd, Q, k, v)
+        assert np.array_equal(counts.astype(np.int64), rc)
+        assert np.array_equal(ids, rids)
+        assert dists.tobytes() == rd.tobytes()
