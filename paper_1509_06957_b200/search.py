@@ -332,8 +332,11 @@ def _scan_variants(D, k):
         # dot-product matrix of a useful query chunk fits (n <= 4M rows)
         if D.n <= (4 << 20):
             out.append("u8gemm")
-            if k <= 96:
-                out.append("u8gemm_bits")  # same filter, candidate bitmaps from K3
+            # same filter over K3's bitmaps; it has no list to fall back on, so
+            # only where the exact fallback's 16-byte rows exist
+            aligned = D.d % 4 == 0 and int(D.X.stride(0)) % 4 == 0 and D.X.data_ptr() % 16 == 0
+            if k <= 96 and aligned:
+                out.append("u8gemm_bits")
     if k <= 120 and D.shadow() is not None:
         out.append("fp16")
     out.append("fp32")

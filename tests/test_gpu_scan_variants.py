@@ -169,3 +169,19 @@ def test_bitmap_route_edges(monkeypatch, rng, v, k):
         assert np.array_equal(counts.astype(np.int64), rc)
         assert np.array_equal(ids, rids)
         assert dists.tobytes() == rd.tobytes()
+
+
+@pytest.mark.parametrize("variant", ["u8", "u8gemm", "u8gemm_bits"])
+def test_u8_routes_odd_width(monkeypatch, rng, variant):
+    """d not a multiple of 4: the u8 list routes fall back to the float32
+    filter inside the library, the bitmap route is not offered; answers stay
+    exact."""
+    monkeypatch.setenv("MRPT_SCAN_ROWS", variant)
+    n, d, nq = 2500, 37, 280
+    X = _data("ints", rng, n + nq, d)
+    Xd, Q = X[:n], X[n:]
+    index = mrpt.grow_trees(Xd, 5, 5, seed=2)
+    ids, dists, counts = mrpt.approximate_knn_batch(Q, 9, index, 1)
+    rids, rd, rc = _oracle(index, Xd, Q, 9, 1)
+    assert np.array_equal(ids, rids)
+    assert dists.tobytes() == rd.tobytes()
