@@ -468,8 +468,17 @@ def _knn_batch_pipelined(Qc, k, index, votes):
     nq = int(Qc.shape[0])
     Qc = Qc.to(dtype=torch.float32).contiguous()
     _record_macs(nq * sum(R.nnz for R in index.matrices))
-    pieces = max(1, min(4, nq // _PIPE_MIN))
-    bounds = [nq * i // pieces for i in range(pieces + 1)]
+    # a small first piece (its upload is the only one not hidden), then
+    # larger ones (fewer, fuller filter launches); MRPT_PIPE=equal: 4 equal pieces
+    if os.environ.get("MRPT_PIPE") == "equal":
+        pieces = max(1, min(4, nq // _PIPE_MIN))
+        bounds = [nq * i // pieces for i in range(pieces + 1)]
+    else:
+        first = max(256, nq // 8)
+        rest = nq - first
+        pieces = max(1, min(3, rest // _PIPE_MIN))
+        bounds = [0] + [first + rest * i // pieces for i in range(pieces + 1)]
+        pieces = len(bounds) - 1
     dev = _device.device()
     Qd = torch.empty((nq, index.d), dtype=torch.float32, device=dev)
     ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
