@@ -455,6 +455,19 @@ def approximate_knn_batch(Q, k, index, votes, chunk=None):
 _PIPE_MIN = 2048  # queries per pipelined piece (at least)
 
 
+def _pipe_bounds(nq, mode=""):
+    """Piece boundaries of a pipelined host batch: a small first piece (its
+    upload is the only one not hidden under compute), then up to 3 larger
+    ones (fewer, fuller filter launches).  mode "equal": up to 4 equal pieces."""
+    if mode == "equal":
+        pieces = max(1, min(4, nq // _PIPE_MIN))
+        return [nq * i // pieces for i in range(pieces + 1)]
+    first = min(nq, max(256, nq // 8))
+    rest = nq - first
+    pieces = max(1, min(3, rest // _PIPE_MIN))
+    return [0] + [first + rest * i // pieces for i in range(pieces + 1)]
+
+
 def _knn_batch_pipelined(Qc, k, index, votes):
     """Host queries in, host results out, with the transfers overlapped: the
     batch is cut into up to 4 pieces; piece i's upload (copy stream), its
@@ -468,17 +481,8 @@ def _knn_batch_pipelined(Qc, k, index, votes):
     nq = int(Qc.shape[0])
     Qc = Qc.to(dtype=torch.float32).contiguous()
     _record_macs(nq * sum(R.nnz for R in index.matrices))
-    # a small first piece (its upload is the only one not hidden), then
-    # larger ones (fewer, fuller filter launches); MRPT_PIPE=equal: 4 equal pieces
-    if os.environ.get("MRPT_PIPE") == "equal":
-        pieces = max(1, min(4, nq // _PIPE_MIN))
-        bounds = [nq * i // pieces for i in range(pieces + 1)]
-    else:
-        first = max(256, nq // 8)
-        rest = nq - first
-        pieces = max(1, min(3, rest // _PIPE_MIN))
-        bounds = [0] + [first + rest * i // pieces for i in range(pieces + 1)]
-        pieces = len(bounds) - 1
+    bounds = _pipe_bounds(nq, os.environ.get("MRPT_PIPE", ""))
+    pieces = len(bounds) - 1
     dev = _device.device()
     Qd = torch.empty((nq, index.d), dtype=torch.float32, device=dev)
     ids = torch.empty((nq, k), dtype=torch.int64, device=dev)

@@ -110,3 +110,56 @@ def test_workload_generators_are_deterministic():
         assert X1.dtype == np.float32 and X1.shape[1] == p["d"]
         assert np.array_equal(X1, X2) and np.array_equal(Q1, Q2)
         assert 2 ** p["depth"] <= X1.shape[0]
+
+
+@pytest.mark.parametrize("nq", [4096, 4097, 5000, 10000, 10001, 65536])
+@pytest.mark.parametrize("mode", ["", "equal"])
+def test_pipelined_piece_bounds_partition_the_batch(nq, mode):
+    """The overlapped host path cuts a batch into ascending pieces that cover
+    every query exactly once, with a small first piece by default."""
+    from paper_1509_06957_b200.search import _pipe_bounds
+
+    b = _pipe_bounds(nq, mode)
+    assert b[0] == 0 and b[-1] == nq
+    assert all(x < y for x, y in zip(b, b[1:]))
+    assert 1 <= len(b) - 1 <= 4
+    if mode == "":
+        assert b[1] - b[0] <= max(256, nq // 8)
+
+
+class _FakeRows:
+    def __init__(self, stride):
+        self._s = stride
+
+    def stride(self, i):
+        return self._s
+
+    def data_ptr(self):
+        return 1 << 20
+
+
+class _FakeIndex:
+    def __init__(self, n, d, u8=True, fp16=False, stride=None):
+        self.n, self.d = n, d
+        self.X = _FakeRows(stride if stride is not None else d)
+        self._u8, self._h = u8, fp16
+
+    def u8_rows(self):
+        return object() if self._u8 else None
+
+    def shadow(self):
+        return object() if self._h else None
+
+
+@pytest.mark.parametrize("n,d,k,u8,want", [
+    (60_000, 784, 10, True, ["u8", "u8gemm", "u8gemm_bits", "fp32"]),
+    (60_000, 784, 100, True, ["u8", "u8gemm", "fp32"]),          # bitmap filter: k <= 96
+    (60_000, 37, 10, True, ["u8", "u8gemm", "fp32"]),            # no 16-byte rows
+    (5_000_000, 128, 10, True, ["u8", "fp32"]),                   # dot-product matrix too big
+    (60_000, 784, 121, True, ["fp32"]),                           # filters take k <= 120
+    (60_000, 784, 10, False, ["fp32"]),                           # signed data: no u8 shadow
+])
+def test_scan_route_availability(n, d, k, u8, want):
+    from paper_1509_06957_b200.search import _scan_variants
+
+    assert _scan_variants(_FakeIndex(n, d, u8), k) == want
