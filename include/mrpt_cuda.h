@@ -133,6 +133,24 @@ int32_t mrpt_vote_bitmap(const int32_t *leaf_indices, const int64_t *leaf_offset
                          int64_t max_count, const uint16_t *dir, uint32_t *bits,
                          int64_t bstride, int32_t *ncand, void *stream);
 
+/* mrpt_vote that also stores each listed candidate's vote count
+ * (cand_counts (nq, cap) uint16, saturated at 65535): one K2/K3 pass at the
+ * smallest threshold of a sweep serves every larger v through
+ * mrpt_filter_counts (vote counts do not depend on v). */
+int32_t mrpt_vote_counted(const int32_t *leaf_indices, const int64_t *leaf_offsets,
+                          int64_t n, int32_t T, int32_t depth, const int32_t *leaves,
+                          int64_t nq, int32_t v, int32_t leaves_sorted,
+                          int64_t max_count, const uint16_t *dir, int32_t *cand,
+                          uint16_t *cand_counts, int64_t cap, int32_t *ncand,
+                          void *stream);
+
+/* Keep, per query and in list order, the candidates of a counted vote whose
+ * count is >= v: cand_out (nq, cap_out), ncand_out (nq) (true count). */
+int32_t mrpt_filter_counts(const int32_t *cand, const uint16_t *cand_counts,
+                           int64_t cap, const int32_t *ncand, int64_t nq, int32_t v,
+                           int32_t *cand_out, int64_t cap_out, int32_t *ncand_out,
+                           void *stream);
+
 /* Vote geometry: number of id tiles the vote sweeps for this index shape and
  * the uint16 entries of its tile directory (0 when one tile suffices).
  * The directory (optional `dir` of mrpt_vote, built once per index by

@@ -50,6 +50,9 @@ SIGNATURES = {
     "mrpt_scan_topk_u8gemm_workspace_size": [_c_i64, _c_i64, _c_i64, ctypes.POINTER(_c_i64)],
     "mrpt_scan_topk_u8gemm": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_i64, _c_i64,
                               _c_p, _c_i64, _c_p, _c_i32, _c_p, _c_p, _c_p, _c_i64, _c_p],
+    "mrpt_vote_counted": [_c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_i64, _c_i32, _c_i32, _c_i64,
+                          _c_p, _c_p, _c_p, _c_i64, _c_p, _c_p],
+    "mrpt_filter_counts": [_c_p, _c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_p, _c_i64, _c_p, _c_p],
     "mrpt_vote_bitmap": [_c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_i64, _c_i32, _c_i32, _c_i64,
                          _c_p, _c_p, _c_i64, _c_p, _c_p],
     "mrpt_scan_topk_u8gemm_bits": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_i64,

@@ -38,7 +38,19 @@ struct VoteArgs {
   const uint16_t *dir;   // optional tile directory (T, 2^depth, ntiles+1)
   uint32_t *bits_out;    // optional: candidate bitmap per query instead of lists
   int64_t bstride;       // words per query in bits_out
+  uint16_t *cnt_out;     // optional: each listed candidate's vote count (saturated), beside cand
 };
+
+// Vote count of tile-local id `local` in the packed counters (code cw).
+__device__ __forceinline__ uint32_t counter_read(const uint32_t *cnt, int cw, int local) {
+  if (cw == 1) return (cnt[local >> 2] >> ((local & 3) << 3)) & 0xffu;
+  if (cw == 3) {
+    const int w = local / 3;
+    return (cnt[w] >> ((local - 3 * w) * 10)) & 0x3ffu;
+  }
+  if (cw == 2) return (cnt[local >> 1] >> ((local & 1) << 4)) & 0xffffu;
+  return cnt[local];
+}
 
 constexpr int kVoteNT = 1024;
 constexpr int kVoteU = 8;
@@ -76,7 +88,9 @@ __device__ __forceinline__ uint32_t bump(uint32_t *cnt, int local) {
 // the bitmap as it goes.
 template <int NT = kVoteNT>
 __device__ __forceinline__ int64_t emit_bitmap(uint32_t *bits, int nwords, int32_t lo, int32_t *out,
-                                               int64_t base, int64_t cap, int *wsum) {
+                                               int64_t base, int64_t cap, int *wsum,
+                                               const uint32_t *cntw = nullptr, int cw = 0,
+                                               uint16_t *cout = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = NT / 32;
   for (int r0 = 0; r0 < nwords; r0 += NT) {
@@ -108,7 +122,13 @@ __device__ __forceinline__ int64_t emit_bitmap(uint32_t *bits, int nwords, int32
     int64_t pos = base + before + incl - pc;
     while (word) {
       const int b = __ffs(word) - 1;
-      if (pos < cap) out[pos] = lo + i * 32 + b;
+      if (pos < cap) {
+        out[pos] = lo + i * 32 + b;
+        if (cout) {
+          const uint32_t c = counter_read(cntw, cw, i * 32 + b);
+          cout[pos] = (uint16_t)(c < 65535u ? c : 65535u);
+        }
+      }
       ++pos;
       word &= word - 1u;
     }
@@ -217,7 +237,8 @@ __global__ void __launch_bounds__(kVoteNT, 1) k_vote(VoteArgs a) {
       if (a.bits_out)
         ncand += store_bits(bits, (int)((hi - lo + 31) >> 5), a.bits_out + q * a.bstride + (lo >> 5), wsum);
       else
-        ncand = emit_bitmap(bits, (int)((hi - lo + 31) >> 5), lo, qcand, ncand, a.cap, wsum);
+        ncand = emit_bitmap(bits, (int)((hi - lo + 31) >> 5), lo, qcand, ncand, a.cap, wsum, cnt, CW,
+                            a.cnt_out ? a.cnt_out + q * a.cap : nullptr);
       if (tile + 1 < a.ntiles) {
         for (int i = tid; i < cwords / 4; i += kVoteNT) c4[i] = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
@@ -414,7 +435,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_vote_dir(VoteArgs a) {
         ncand += store_bits<NT>(bits, (int)((hi - lo + 31) >> 5), a.bits_out + q * a.bstride + (lo >> 5), wsum);
       } else if (nw > kWList) {  // too many words to list: ordered scan of the whole bitmap
         const int64_t hi = (int64_t)lo + a.W < a.n ? (int64_t)lo + a.W : a.n;
-        ncand = emit_bitmap<NT>(bits, (int)((hi - lo + 31) >> 5), lo, qcand, ncand, a.cap, wsum);
+        ncand = emit_bitmap<NT>(bits, (int)((hi - lo + 31) >> 5), lo, qcand, ncand, a.cap, wsum, cnt, CW,
+                                a.cnt_out ? a.cnt_out + q * a.cap : nullptr);
       } else {
         // listed words only (ids within the tile unordered; tiles ascending)
         for (int i0 = 0; i0 < nw; i0 += NT) {
@@ -439,7 +461,13 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_vote_dir(VoteArgs a) {
           int64_t pos = ncand + wbase + incl - pc;
           while (word) {
             const int b = __ffs(word) - 1;
-            if (pos < a.cap) qcand[pos] = lo + wi * 32 + b;
+            if (pos < a.cap) {
+              qcand[pos] = lo + wi * 32 + b;
+              if (a.cnt_out) {
+                const uint32_t c = counter_read(cnt, CW, wi * 32 + b);
+                a.cnt_out[q * a.cap + pos] = (uint16_t)(c < 65535u ? c : 65535u);
+              }
+            }
             ++pos;
             word &= word - 1u;
           }
@@ -794,7 +822,8 @@ extern "C" int32_t mrpt_vote_build_dir(const int32_t *leaf_indices, const int64_
 static int32_t vote_impl(const int32_t *leaf_indices, const int64_t *leaf_offsets, int64_t n, int32_t T,
                          int32_t depth, const int32_t *leaves, int64_t nq, int32_t v, int32_t leaves_sorted,
                          int64_t max_count, const uint16_t *dir, int32_t *cand, int64_t cap,
-                         uint32_t *bits_out, int64_t bstride, int32_t *ncand, void *stream) {
+                         uint32_t *bits_out, int64_t bstride, int32_t *ncand, void *stream,
+                         uint16_t *cnt_out = nullptr) {
   if (n < 1 || n >= (int64_t)1 << 31 || T < 1 || depth < 0 || depth > 30 || nq < 0)
     return fail(MRPT_ESHAPE, "mrpt_vote: bad shape");
   if (v < 1 || v > max_count) return fail(MRPT_EPARAM, "mrpt_vote: vote threshold out of range");
@@ -832,6 +861,7 @@ static int32_t vote_impl(const int32_t *leaf_indices, const int64_t *leaf_offset
   a.dir = dir;
   a.bits_out = bits_out;
   a.bstride = bstride;
+  a.cnt_out = cnt_out;
   const size_t smem = vote_smem_bytes(CW, W, T);
   const int64_t grid = nq < (int64_t)num_sms() * 4 ? nq : (int64_t)num_sms() * 4;
   // v == 1: bitmap + per-warp staging + slice table
@@ -842,7 +872,7 @@ static int32_t vote_impl(const int32_t *leaf_indices, const int64_t *leaf_offset
   // counting kernel is as fast)
   const char *uenv = getenv("MRPT_VOTE_UNION");  // "0": never, "1": whenever it fits
   const bool want_union = uenv ? atoi(uenv) != 0 : ntiles > 1;
-  if (v == 1 && want_union && usmem1024 <= (size_t)kVoteSmemUnion && !getenv("MRPT_VOTE_NO_UNION")) {
+  if (v == 1 && want_union && !cnt_out && usmem1024 <= (size_t)kVoteSmemUnion && !getenv("MRPT_VOTE_NO_UNION")) {
     // NT=512 when two CTAs fit per SM (one query's compaction overlaps the
     // other's atomics), else one CTA of 1024 threads
     const bool two = usmem512 + 4 * 1024 <= (size_t)kVoteSmemUnion / 2;
@@ -897,6 +927,57 @@ extern "C" int32_t mrpt_vote_bitmap(const int32_t *leaf_indices, const int64_t *
   if (!bits) return fail(MRPT_EPARAM, "mrpt_vote_bitmap: bits is NULL");
   return vote_impl(leaf_indices, leaf_offsets, n, T, depth, leaves, nq, v, leaves_sorted, max_count, dir,
                    nullptr, 1, bits, bstride, ncand, stream);
+}
+
+extern "C" int32_t mrpt_vote_counted(const int32_t *leaf_indices, const int64_t *leaf_offsets, int64_t n,
+                                     int32_t T, int32_t depth, const int32_t *leaves, int64_t nq, int32_t v,
+                                     int32_t leaves_sorted, int64_t max_count, const uint16_t *dir,
+                                     int32_t *cand, uint16_t *cand_counts, int64_t cap, int32_t *ncand,
+                                     void *stream) {
+  clear_error();
+  if (!cand_counts) return fail(MRPT_EPARAM, "mrpt_vote_counted: cand_counts is NULL");
+  return vote_impl(leaf_indices, leaf_offsets, n, T, depth, leaves, nq, v, leaves_sorted, max_count, dir, cand,
+                   cap, nullptr, 0, ncand, stream, cand_counts);
+}
+
+// One warp per query: keep the listed candidates whose count is >= v, in
+// list order (ballot compaction).
+__global__ void k_filter_counts(const int32_t *__restrict__ cand, const uint16_t *__restrict__ cnts, int64_t cap,
+                                const int32_t *__restrict__ ncand, int64_t nq, int32_t v, int32_t *cand_out,
+                                int64_t cap_out, int32_t *ncand_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < nq; q += nw) {
+    const int64_t m = ncand[q] < cap ? ncand[q] : cap;
+    const int32_t *c = cand + q * cap;
+    const uint16_t *k = cnts + q * cap;
+    int32_t *o = cand_out + q * cap_out;
+    int64_t outn = 0;
+    for (int64_t i0 = 0; i0 < m; i0 += 32) {
+      const int64_t i = i0 + lane;
+      const bool keep = i < m && (int32_t)k[i] >= v;
+      const unsigned bm = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const int64_t pos = outn + __popc(bm & lanemask_lt());
+        if (pos < cap_out) o[pos] = c[i];
+      }
+      outn += __popc(bm);
+    }
+    if (lane == 0) ncand_out[q] = (int32_t)outn;
+  }
+}
+
+extern "C" int32_t mrpt_filter_counts(const int32_t *cand, const uint16_t *cand_counts, int64_t cap,
+                                      const int32_t *ncand, int64_t nq, int32_t v, int32_t *cand_out,
+                                      int64_t cap_out, int32_t *ncand_out, void *stream) {
+  clear_error();
+  if (cap < 1 || cap_out < 1 || nq < 0 || v < 1) return fail(MRPT_EPARAM, "mrpt_filter_counts: bad arguments");
+  if (nq == 0) return MRPT_OK;
+  const int64_t blocks = ceil_div<int64_t>(nq, 8);
+  const int64_t capb = (int64_t)num_sms() * 16;
+  (count_launch(), k_filter_counts<<<(unsigned)(blocks < capb ? blocks : capb), 256, 0, as_stream(stream)>>>(
+      cand, cand_counts, cap, ncand, nq, v, cand_out, cap_out, ncand_out));
+  return launch_status("mrpt_filter_counts");
 }
 
 extern "C" int32_t mrpt_vote_counts(const int32_t *leaf_indices, const int64_t *leaf_offsets,

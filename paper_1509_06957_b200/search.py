@@ -512,6 +512,69 @@ def _knn_batch_pipelined(Qc, k, index, votes):
     return hid.numpy(), hdist.numpy(), hcnt.numpy()
 
 
+def approximate_knn_sweep(Q, k, index, votes):
+    """approximate_knn_batch for several vote thresholds from ONE route and
+    ONE vote pass (the reference's sweeps loop queries and
+    thresholds one at a time, evaluation.py:163-215): the vote at the smallest
+    threshold also records each candidate's count, every larger threshold
+    filters that list (counts do not depend on v), and each threshold's
+    candidates go through the exact scan.  Returns {v: (ids, dists, counts)}
+    with host arrays for host input, CUDA tensors for a CUDA tensor; each
+    entry equals approximate_knn_batch(Q, k, index, v)."""
+    vs = sorted({int(v) for v in votes})
+    if not vs:
+        return {}
+    for v in vs:
+        _check_batch_args(k, index, v)
+    torch = _device.torch_mod()
+    on_device = _device.is_tensor(Q) and Q.is_cuda
+    if _device.is_tensor(Q):
+        Qd = Q.to(device=_device.device(), dtype=torch.float32).contiguous()
+    else:
+        Qd = _device.h2d(np.ascontiguousarray(np.asarray(Q), dtype=np.float32))
+    if Qd.dim() != 2 or Qd.shape[1] != index.d:
+        raise ShapeError(f"queries must be (nq, {index.d}), got {tuple(Qd.shape)}")
+    D = index.device_index()
+    nq = int(Qd.shape[0])
+    dev = Qd.device
+    _record_macs(nq * sum(R.nnz for R in index.matrices) * len(vs))
+    cap0 = D.cap(vs[0])
+    leaves = torch.empty((max(1, nq), D.T), dtype=torch.int32, device=dev)
+    cand0 = torch.empty((max(1, nq), cap0), dtype=torch.int32, device=dev)
+    cnt0 = torch.empty((max(1, nq), cap0), dtype=torch.int16, device=dev)
+    n0 = torch.empty(max(1, nq), dtype=torch.int32, device=dev)
+    out = {}
+    if nq:
+        _route_launch(D, Qd, nq, int(Qd.stride(0)), leaves)
+        _native.call("mrpt_vote_counted", _native.ptr(D.indices), _native.ptr(D.offsets), D.n, D.T,
+                     D.depth, _native.ptr(leaves), nq, vs[0], int(D.leaves_sorted),
+                     int(D.max_count), _native.ptr(D.vote_dir()), _native.ptr(cand0),
+                     _native.ptr(cnt0), int(cap0), _native.ptr(n0), _native.stream_ptr())
+    for v in vs:
+        ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
+        dists = torch.empty((nq, k), dtype=torch.float64, device=dev)
+        if v == vs[0]:
+            cand, cap, counts = cand0, cap0, n0[:nq]
+        else:
+            cap = D.cap(v)
+            cand = torch.empty((max(1, nq), cap), dtype=torch.int32, device=dev)
+            counts = torch.empty(nq, dtype=torch.int32, device=dev)
+            if nq:
+                _native.call("mrpt_filter_counts", _native.ptr(cand0), _native.ptr(cnt0), int(cap0),
+                             _native.ptr(n0), nq, v, _native.ptr(cand), int(cap),
+                             _native.ptr(counts), _native.stream_ptr())
+        if nq:
+            variant = D.scan_choice.get((k, v))
+            if variant in (None, "u8gemm_bits"):
+                avail = [x for x in _scan_variants(D, k) if x != "u8gemm_bits"]
+                variant = "u8gemm" if variant == "u8gemm_bits" else avail[0]
+            args = (Qd, nq, int(Qd.stride(0)), cand, cap, counts, k, ids, dists)
+            _scan_launch(D, variant, args)
+        res = (ids, dists, counts.clone())
+        out[v] = res if on_device else tuple(_device.d2h(t) for t in res)
+    return out
+
+
 def approximate_knn(q, k, index, votes):
     """Approximate k-NN of one query (search.py:175-184): vote-filtered
     candidates, then the exact scan; ``shortfall`` reports a deficit."""

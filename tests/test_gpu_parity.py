@@ -324,3 +324,29 @@ def test_pipelined_host_batch_matches(rng):
     assert np.array_equal(got_np[0][:60], rids)
     assert got_np[1][:60].tobytes() == rd.tobytes()
     assert np.array_equal(got_np[2][:60].astype(np.int64), rc)
+
+
+@pytest.mark.parametrize("n,T,depth,votes", [(20_000, 12, 7, (1, 2, 4)),
+                                             (300_000, 40, 9, (1, 3, 6)),
+                                             (8_000, 300, 5, (2, 10, 40))])
+def test_vote_sweep_one_pass_matches_per_threshold(rng, n, T, depth, votes):
+    """approximate_knn_sweep (one route + one counted vote, filtered per
+    threshold) answers every threshold exactly like approximate_knn_batch
+    and like the oracle."""
+    X = gaussian(rng, n + 40, 10)
+    Xd, Q = X[:n], X[n:]
+    index = mrpt.grow_trees(Xd, T, depth, seed=17)
+    sweep = mrpt.approximate_knn_sweep(Q, 7, index, votes)
+    assert sorted(sweep) == sorted(votes)
+    ref = dict(matrices=[(R.col_ptr, R.row_idx, R.values) for R in index.matrices],
+               splits=index.splits, leaf_offsets=index.leaf_offsets,
+               leaf_indices=index.leaf_indices, depth=depth)
+    for v in votes:
+        ids, dists, counts = sweep[v]
+        bids, bd, bc = mrpt.approximate_knn_batch(Q, 7, index, v)
+        assert np.array_equal(ids, bids) and dists.tobytes() == bd.tobytes()
+        assert np.array_equal(counts, bc)
+        rids, rd, rc = O.approximate_knn_batch(Xd, Q, 7, ref, v)
+        assert np.array_equal(ids, rids)
+        assert dists.tobytes() == rd.tobytes()
+        assert np.array_equal(counts.astype(np.int64), rc)
