@@ -416,6 +416,20 @@ def run_ours(args):
             sw[str(vv)] = {"qps": p["nq"] * 3 / (s.elapsed_time(e) / 1000.0), "recall": rc,
                            "mean_candidates": float(r[2].double().mean().item())}
         line["sweep"] = sw
+        # the same thresholds from one route + one counted vote (f4)
+        for _ in range(2):
+            mrpt.approximate_knn_sweep(Qd, k, index, p["votes"])
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for _ in range(3):
+            mrpt.approximate_knn_sweep(Qd, k, index, p["votes"])
+        e.record(stream)
+        torch.cuda.synchronize()
+        one = s.elapsed_time(e) / 3
+        line["sweep_one_pass"] = {
+            "votes": list(p["votes"]), "ms_all_thresholds": one,
+            "ms_sum_separate": sum(p["nq"] / x["qps"] * 1e3 for x in sw.values())}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, X, Q, p, v, index)
     line["clocks"] = clk.summary()
