@@ -240,6 +240,24 @@ int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64_t ldx,
                           const int32_t *ncand, int32_t k, int64_t *ids,
                           double *dists, void *stream);
 
+/* Signed 8-bit shadow rows for data with negative values: per row scale
+ * s = max|x| / 127, Xq = clamp(rint(x / s), -127, 127) (s8, (n, ldq)),
+ * norm = sum Xq^2, radius >= ||x - s Xq||_2.  Used by mrpt_scan_topk_s8. */
+int32_t mrpt_quantize_s8(const float *X, int64_t n, int32_t d, int64_t ldx,
+                         void *Xq, int64_t ldq, float *scale, int32_t *norm,
+                         float *radius, void *stream);
+
+/* mrpt_scan_topk_u8 over signed (s8) shadow rows: the same exact integer
+ * dot-product filter (dp4a with signed rows) and float64 rerank; identical
+ * results.  Falls back to mrpt_scan_topk for unsupported shapes. */
+int32_t mrpt_scan_topk_s8(const float *X, int64_t n, int32_t d, int64_t ldx,
+                          const void *Xq, int64_t ldq, const float *scale,
+                          const int32_t *norm, const float *radius,
+                          const float *Q, int64_t nq, int64_t ldqq,
+                          const int32_t *cand, int64_t cap,
+                          const int32_t *ncand, int32_t k, int64_t *ids,
+                          double *dists, void *stream);
+
 /* GEMM operands of the u8 shadow for mrpt_scan_topk_u8gemm: Xs = Xq ^ 0x80
  * (s8, row stride ldq, room for round_up(n, 16) rows -- the rows past n are
  * zeroed here) and info (n x 16 bytes, 16-byte aligned): per row {scale

@@ -46,6 +46,9 @@ SIGNATURES = {
     "mrpt_quantize_u8": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p],
     "mrpt_scan_topk_u8": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_p,
                           _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i32, _c_p, _c_p, _c_p],
+    "mrpt_quantize_s8": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_p],
+    "mrpt_scan_topk_s8": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_p,
+                          _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i32, _c_p, _c_p, _c_p],
     "mrpt_u8_gemm_rows": [_c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p],
     "mrpt_scan_topk_u8gemm_workspace_size": [_c_i64, _c_i64, _c_i64, ctypes.POINTER(_c_i64)],
     "mrpt_scan_topk_u8gemm": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_i64, _c_i64,

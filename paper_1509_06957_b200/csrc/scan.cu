@@ -1081,6 +1081,44 @@ __global__ void k_quantize_u8(const float *__restrict__ X, int64_t n, int d, int
   }
 }
 
+// Signed 8-bit shadow rows for data with negative values: per row scale
+// sx = max|x| / 127, X_i = clamp(rint(x / sx), -127, 127) (one warp per row).
+__global__ void k_quantize_s8(const float *__restrict__ X, int64_t n, int d, int64_t ldx, int8_t *Xq, int64_t ldq,
+                              float *scale, int32_t *norm, float *radius) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += wstride) {
+    const float *xr = X + i * ldx;
+    float mx = 0.f;
+    for (int c = lane; c < d; c += 32) mx = fmaxf(mx, fabsf(xr[c]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float sc = mx > 0.f ? mx / 127.f : 1.f;
+    double r2 = 0.0;
+    int nn = 0;
+    for (int c = lane; c < ldq; c += 32) {
+      const float x = c < d ? xr[c] : 0.f;
+      float qv = rintf(x / sc);
+      qv = fminf(fmaxf(qv, -127.f), 127.f);
+      const int qi = (int)qv;
+      Xq[i * ldq + c] = (int8_t)qi;
+      const double e = (double)x - (double)sc * (double)qi;
+      r2 = fma(e, e, r2);
+      nn += qi * qi;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+      nn += __shfl_xor_sync(0xffffffffu, nn, o);
+    }
+    if (lane == 0) {
+      scale[i] = sc;
+      norm[i] = nn;
+      radius[i] = r2 == 0.0 ? 0.f : __double2float_ru(__dsqrt_ru(r2 * (1.0 + 1e-12)));
+    }
+  }
+}
+
 __device__ __forceinline__ void dist_bounds2(float A, float r, float eta, double &L, double &U) {
   const double a = (double)A, e = (double)eta;
   const double slo = fmax(0.0, sqrt(fmax(0.0, a - e)) - (double)r);
@@ -1162,10 +1200,15 @@ struct Q8Rows {
   int64_t bstride;
 };
 
-template <bool QS>
+// a: 4 row bytes (u8, or s8 when RS), b: 4 query bytes (s8 when QS, else u8)
+template <bool QS, bool RS = false>
 __device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
   int d;
-  if (QS)
+  if (RS && QS)
+    asm("dp4a.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  else if (RS)
+    asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  else if (QS)
     asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
   else
     asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
@@ -1175,7 +1218,7 @@ __device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
 // U rows' partial dot products over this lane's 16-byte chunks.  The query's
 // signedness is a template parameter: a runtime flag here puts a branch
 // around every dp4a (inline asm cannot be predicated).
-template <int U, int G, bool QS>
+template <int U, int G, bool QS, bool RS = false>
 __device__ __forceinline__ void dot_rows_u8(const uint8_t *(&rp)[U], const uint32_t *qb,
                                             int gl, int nchunk, int (&acc)[U]) {
   for (int ch = gl; ch < nchunk; ch += G) {
@@ -1185,10 +1228,10 @@ __device__ __forceinline__ void dot_rows_u8(const uint8_t *(&rp)[U], const uint3
     for (int u = 0; u < U; ++u) xv[u] = __ldg(reinterpret_cast<const uint4 *>(rp[u] + 16 * ch));
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      acc[u] = dp4a_us<QS>(xv[u].x, qv.x, acc[u]);
-      acc[u] = dp4a_us<QS>(xv[u].y, qv.y, acc[u]);
-      acc[u] = dp4a_us<QS>(xv[u].z, qv.z, acc[u]);
-      acc[u] = dp4a_us<QS>(xv[u].w, qv.w, acc[u]);
+      acc[u] = dp4a_us<QS, RS>(xv[u].x, qv.x, acc[u]);
+      acc[u] = dp4a_us<QS, RS>(xv[u].y, qv.y, acc[u]);
+      acc[u] = dp4a_us<QS, RS>(xv[u].z, qv.z, acc[u]);
+      acc[u] = dp4a_us<QS, RS>(xv[u].w, qv.w, acc[u]);
     }
   }
 }
@@ -1347,7 +1390,7 @@ __device__ __forceinline__ bool admit_lane_u8(int32_t myc, int mys, float sx, in
 // products come precomputed from the tensor-core GEMM (rows.D, one candidate
 // per lane, 4 bytes per candidate instead of a row); the bounds, buffer and
 // exact re-rank are the same code.
-template <int BUFW, int G, bool DM>
+template <int BUFW, int G, bool DM, bool RS = false>
 __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows rows,
                                                              int32_t *fb_list, int32_t *fb_count) {
   extern __shared__ unsigned long long topk_smem[];
@@ -1527,9 +1570,9 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
 #pragma unroll
       for (int u = 0; u < U; ++u) acc[u] = 0;
       if (qsigned)
-        dot_rows_u8<U, G, true>(rp, qb, gl, nchunk, acc);
+        dot_rows_u8<U, G, true, RS>(rp, qb, gl, nchunk, acc);
       else
-        dot_rows_u8<U, G, false>(rp, qb, gl, nchunk, acc);
+        dot_rows_u8<U, G, false, RS>(rp, qb, gl, nchunk, acc);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
 #pragma unroll
@@ -2059,12 +2102,24 @@ extern "C" int32_t mrpt_quantize_u8(const float *X, int64_t n, int32_t d, int64_
   return launch_status("mrpt_quantize_u8");
 }
 
+extern "C" int32_t mrpt_quantize_s8(const float *X, int64_t n, int32_t d, int64_t ldx, void *Xq, int64_t ldq,
+                                    float *scale, int32_t *norm, float *radius, void *stream) {
+  clear_error();
+  if (n < 1 || d < 1 || ldx < d || ldq < d || ldq % 16 != 0 || ldq > 1024)
+    return fail(MRPT_ESHAPE, "mrpt_quantize_s8: bad shape");
+  const int64_t wb = ceil_div<int64_t>(n, 8);
+  const int g = (int)(wb < (int64_t)num_sms() * 16 ? wb : (int64_t)num_sms() * 16);
+  (count_launch(), k_quantize_s8<<<g, 256, 0, as_stream(stream)>>>(X, n, d, ldx, reinterpret_cast<int8_t *>(Xq),
+                                                                   ldq, scale, norm, radius));
+  return launch_status("mrpt_quantize_s8");
+}
+
 typedef void (*topk_fn_u8)(TopkArgs, Q8Rows, int32_t *, int32_t *);
 
-template <int G, bool DM = false>
+template <int G, bool DM = false, bool RS = false>
 static topk_fn_u8 pick_u8_b(int bufw) {
-  return bufw == 64 ? k_scan_topk_u8<64, G, DM>
-                    : (bufw == 128 ? k_scan_topk_u8<128, G, DM> : k_scan_topk_u8<256, G, DM>);
+  return bufw == 64 ? k_scan_topk_u8<64, G, DM, RS>
+                    : (bufw == 128 ? k_scan_topk_u8<128, G, DM, RS> : k_scan_topk_u8<256, G, DM, RS>);
 }
 
 namespace mrpt {
@@ -2078,13 +2133,10 @@ static void launch_rerank(const TopkArgs &a, cudaStream_t s) {
   (count_launch(), k_rerank<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, s>>>(a));
 }
 
-extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64_t ldx,
-                                     const void *Xq, int64_t ldq, const float *scale,
-                                     const int32_t *norm, const float *radius, const float *Q,
-                                     int64_t nq, int64_t ldqq, const int32_t *cand, int64_t cap,
-                                     const int32_t *ncand, int32_t k, int64_t *ids, double *dists,
-                                     void *stream) {
-  clear_error();
+static int32_t scan_u8_impl(const float *X, int64_t n, int32_t d, int64_t ldx, const void *Xq, int64_t ldq,
+                            const float *scale, const int32_t *norm, const float *radius, const float *Q,
+                            int64_t nq, int64_t ldqq, const int32_t *cand, int64_t cap, const int32_t *ncand,
+                            int32_t k, int64_t *ids, double *dists, void *stream, bool rs) {
   if (!Xq || !scale || !norm || !radius || ldq % 16 != 0 || ldq < d || ldq > 1024 || k > 120 || k < 1 ||
       d % 4 != 0 || ldx % 4 != 0 || !aligned16(X))  // the exact fallback needs 16-byte rows
     return mrpt_scan_topk(X, n, d, ldx, Q, nq, ldqq, cand, cap, ncand, k, ids, dists, stream);
@@ -2139,8 +2191,8 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
     const char *e = getenv("MRPT_U8_G");
     g_env = e ? atoi(e) : 0;
   }
-  const int G = (g_env == 4 || g_env == 8 || g_env == 16 || g_env == 32) ? g_env
-                                                                         : (ldq <= 256 ? 4 : 8);
+  int G = (g_env == 4 || g_env == 8 || g_env == 16 || g_env == 32) ? g_env : (ldq <= 256 ? 4 : 8);
+  if (rs && G > 8) G = 8;  // signed rows are instantiated for 4 and 8 lanes per row
   const int cpi = (32 / G) * 4;
   int bufw = 64;
   while (bufw < 2 * k + 2 * cpi) bufw <<= 1;
@@ -2154,8 +2206,9 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
   cudaMemsetAsync(fb, 0, sizeof(int32_t), s);
   a.nsurv = fb + 1 + nq;
   a.surv = a.nsurv + nq;
-  topk_fn_u8 fn = G == 32 ? pick_u8_b<32>(bufw)
-                  : (G == 16 ? pick_u8_b<16>(bufw) : (G == 8 ? pick_u8_b<8>(bufw) : pick_u8_b<4>(bufw)));
+  topk_fn_u8 fn = rs ? (G == 4 ? pick_u8_b<4, false, true>(bufw) : pick_u8_b<8, false, true>(bufw))
+                     : (G == 32 ? pick_u8_b<32>(bufw)
+                                : (G == 16 ? pick_u8_b<16>(bufw) : (G == 8 ? pick_u8_b<8>(bufw) : pick_u8_b<4>(bufw))));
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t grid = nq < (int64_t)num_sms() * 8 ? nq : (int64_t)num_sms() * 8;
   (count_launch(), fn<<<(unsigned)grid, kScanNT, smem, s>>>(a, rows, fb + 1, fb));
@@ -2175,6 +2228,28 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
   launch_rerank(a, s);
   cudaFreeAsync(fb, s);
   return launch_status("mrpt_scan_topk_u8");
+}
+
+extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64_t ldx,
+                                     const void *Xq, int64_t ldq, const float *scale,
+                                     const int32_t *norm, const float *radius, const float *Q,
+                                     int64_t nq, int64_t ldqq, const int32_t *cand, int64_t cap,
+                                     const int32_t *ncand, int32_t k, int64_t *ids, double *dists,
+                                     void *stream) {
+  clear_error();
+  return scan_u8_impl(X, n, d, ldx, Xq, ldq, scale, norm, radius, Q, nq, ldqq, cand, cap, ncand, k, ids, dists,
+                      stream, false);
+}
+
+extern "C" int32_t mrpt_scan_topk_s8(const float *X, int64_t n, int32_t d, int64_t ldx,
+                                     const void *Xq, int64_t ldq, const float *scale,
+                                     const int32_t *norm, const float *radius, const float *Q,
+                                     int64_t nq, int64_t ldqq, const int32_t *cand, int64_t cap,
+                                     const int32_t *ncand, int32_t k, int64_t *ids, double *dists,
+                                     void *stream) {
+  clear_error();
+  return scan_u8_impl(X, n, d, ldx, Xq, ldq, scale, norm, radius, Q, nq, ldqq, cand, cap, ncand, k, ids, dists,
+                      stream, true);
 }
 
 extern "C" int32_t mrpt_u8_gemm_rows(const void *Xq, int64_t n, int64_t ldq, const float *scale,

@@ -337,6 +337,8 @@ def _scan_variants(D, k):
             aligned = D.d % 4 == 0 and int(D.X.stride(0)) % 4 == 0 and D.X.data_ptr() % 16 == 0
             if k <= 96 and aligned:
                 out.append("u8gemm_bits")
+    elif k <= 120 and D.s8_rows() is not None:
+        out.append("s8")
     if k <= 120 and D.shadow() is not None:
         out.append("fp16")
     out.append("fp32")
@@ -361,6 +363,11 @@ def _scan_launch(D, variant, args):
                      _native.ptr(Xs), ldr, _native.ptr(info), _native.ptr(qb), m, ldq,
                      _native.ptr(cand), int(cap), _native.ptr(counts), int(k), _native.ptr(ids),
                      _native.ptr(dists), _native.ptr(ws), int(ws.numel()), stream)
+    elif variant == "s8":
+        Xq, ldr, sc, nm, rad = D.s8_rows()
+        _native.call("mrpt_scan_topk_s8", _native.ptr(D.X), D.n, D.d, int(D.X.stride(0)),
+                     _native.ptr(Xq), ldr, _native.ptr(sc), _native.ptr(nm), _native.ptr(rad),
+                     *common_tail)
     elif variant == "fp16":
         Xh, ldh, rad = D.shadow()
         _native.call("mrpt_scan_topk_fp16", _native.ptr(D.X), D.n, D.d, int(D.X.stride(0)),

@@ -211,6 +211,28 @@ class _DeviceIndex:
                 self._u8 = (Xq, ldq, sc, nm, rad)
         return self._u8
 
+    def s8_rows(self):
+        """s8 shadow (rows, row stride, scale, norm, radius) for data with
+        negative values (where u8_rows() is None), built once; None otherwise
+        (MRPT_SCAN_ROWS=fp16|fp32 disables it)."""
+        if getattr(self, "_s8", False) is not False:
+            return self._s8
+        self._s8 = None
+        ldq = (self.d + 15) // 16 * 16
+        mode = os.environ.get("MRPT_SCAN_ROWS", "auto")
+        if mode in ("auto", "s8") and ldq <= 1024 and self.u8_rows() is None:
+            torch = _device.torch_mod()
+            dev = self.X.device
+            Xq = torch.empty((self.n, ldq), dtype=torch.int8, device=dev)
+            sc = torch.empty(self.n, dtype=torch.float32, device=dev)
+            nm = torch.empty(self.n, dtype=torch.int32, device=dev)
+            rad = torch.empty(self.n, dtype=torch.float32, device=dev)
+            _native.call("mrpt_quantize_s8", _native.ptr(self.X), self.n, self.d,
+                         int(self.X.stride(0)), _native.ptr(Xq), ldq, _native.ptr(sc),
+                         _native.ptr(nm), _native.ptr(rad), _native.stream_ptr())
+            self._s8 = (Xq, ldq, sc, nm, rad)
+        return self._s8
+
     def u8_gemm(self, nq):
         """(s8 rows, per-row records, workspace) for the tensor-core GEMM filter over
         the u8 shadow; rows built once, workspace sized for nq queries (kept,

@@ -150,6 +150,9 @@ class _FakeIndex:
     def shadow(self):
         return object() if self._h else None
 
+    def s8_rows(self):
+        return None if self._u8 else object()
+
 
 @pytest.mark.parametrize("n,d,k,u8,want", [
     (60_000, 784, 10, True, ["u8", "u8gemm", "u8gemm_bits", "fp32"]),
@@ -157,7 +160,7 @@ class _FakeIndex:
     (60_000, 37, 10, True, ["u8", "u8gemm", "fp32"]),            # no 16-byte rows
     (5_000_000, 128, 10, True, ["u8", "fp32"]),                   # dot-product matrix too big
     (60_000, 784, 121, True, ["fp32"]),                           # filters take k <= 120
-    (60_000, 784, 10, False, ["fp32"]),                           # signed data: no u8 shadow
+    (60_000, 784, 10, False, ["s8", "fp32"]),                     # signed data: s8 shadow
 ])
 def test_scan_route_availability(n, d, k, u8, want):
     from paper_1509_06957_b200.search import _scan_variants

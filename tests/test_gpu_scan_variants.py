@@ -36,13 +36,15 @@ def _data(kind, rng, n, d):
     return x.astype(np.float32)
 
 
-@pytest.mark.parametrize("variant", ["u8", "u8gemm", "u8gemm_bits", "fp16", "fp32"])
+@pytest.mark.parametrize("variant", ["u8", "u8gemm", "u8gemm_bits", "s8", "fp16", "fp32"])
 @pytest.mark.parametrize("kind,d,k,v", [("pixels", 96, 10, 1), ("ints", 128, 10, 2),
                                          ("clusters01", 256, 10, 2), ("signed", 64, 7, 1),
                                          ("dups", 32, 20, 1), ("pixels", 200, 100, 1)])
 def test_variant_parity(monkeypatch, rng, variant, kind, d, k, v):
     if variant == "u8gemm_bits" and k > 96:
         pytest.skip("the bitmap GEMM filter takes k <= 96")
+    if variant == "s8" and kind != "signed":
+        pytest.skip("the s8 shadow is for data with negative values")
     monkeypatch.setenv("MRPT_SCAN_ROWS", variant)
     if variant == "fp16":
         monkeypatch.setenv("MRPT_FP16_FILTER", "1")
@@ -53,7 +55,8 @@ def test_variant_parity(monkeypatch, rng, variant, kind, d, k, v):
         Q = Q - 0.05  # negative query coordinates: s8 query quantisation
     index = mrpt.grow_trees(Xd, 6, 6, seed=3)
     ids, dists, counts = mrpt.approximate_knn_batch(Q, k, index, v)
-    assert index.device_index().scan_choice.get((k, v)) in (variant, "fp32")
+    allowed = (variant, "fp32", "s8") if kind == "signed" else (variant, "fp32")
+    assert index.device_index().scan_choice.get((k, v)) in allowed
     rids, rd, rc = _oracle(index, Xd, Q, k, v)
     assert np.array_equal(counts.astype(np.int64), rc)
     assert np.array_equal(ids, rids)
@@ -183,5 +186,23 @@ def test_u8_routes_odd_width(monkeypatch, rng, variant):
     index = mrpt.grow_trees(Xd, 5, 5, seed=2)
     ids, dists, counts = mrpt.approximate_knn_batch(Q, 9, index, 1)
     rids, rd, rc = _oracle(index, Xd, Q, 9, 1)
+    assert np.array_equal(ids, rids)
+    assert dists.tobytes() == rd.tobytes()
+
+
+@pytest.mark.parametrize("d,k,v", [(64, 10, 1), (256, 25, 2), (37, 9, 1), (200, 100, 1)])
+def test_s8_route_signed_data(monkeypatch, rng, d, k, v):
+    """Signed data through the s8 shadow (dp4a with signed rows and signed
+    queries): exactly the oracle's answers, including odd widths (library
+    fallback) and k near the filter's limit."""
+    monkeypatch.setenv("MRPT_SCAN_ROWS", "s8")
+    n, nq = 4000, 290
+    X = _data("signed", rng, n + nq, d)
+    Xd, Q = X[:n], X[n:]
+    index = mrpt.grow_trees(Xd, 6, 5, seed=9)
+    ids, dists, counts = mrpt.approximate_knn_batch(Q, k, index, v)
+    assert index.device_index().scan_choice.get((k, v)) == "s8"
+    rids, rd, rc = _oracle(index, Xd, Q, k, v)
+    assert np.array_equal(counts.astype(np.int64), rc)
     assert np.array_equal(ids, rids)
     assert dists.tobytes() == rd.tobytes()
