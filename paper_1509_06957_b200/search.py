@@ -284,6 +284,10 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
         stage("vote", _vote_list, D, leaves, e - s, votes, vdir, cand, cap, counts[s:e])
         args = (qb, e - s, int(Qd.stride(0)), cand, cap, counts[s:e], k, ids[s:e], dists[s:e])
         variant = choice if choice not in (None, "u8gemm_bits") else "fp32"
+        if choice is None:  # small batch, no autotune: a forced list route still applies
+            env = os.environ.get("MRPT_SCAN_ROWS")
+            if env and env != "u8gemm_bits" and env in _scan_variants(D, k):
+                variant = env
         stage("scan_topk", _scan_launch, D, variant, args)
     return ids, dists, counts
 
