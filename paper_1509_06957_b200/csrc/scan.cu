@@ -1724,6 +1724,55 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
   }
 }
 
+// exact_dist2 with the query in shared memory and 16 float4 row loads (64
+// coordinates) in flight ahead of each run of additions; same terms in the
+// same order.
+__device__ __forceinline__ double exact_dist2_sq(const float *__restrict__ xr, const float *qs, int d,
+                                                 bool vec4) {
+  double e = 0.0;
+  int c = 0;
+  if (vec4) {
+    for (; c + 64 <= d; c += 64) {
+      float4 xv[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) xv[u] = __ldg(reinterpret_cast<const float4 *>(xr + c) + u);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const float4 qv = *reinterpret_cast<const float4 *>(qs + c + 4 * u);
+        double t;
+        t = (double)xv[u].x - (double)qv.x;
+        e = __dadd_rn(e, __dmul_rn(t, t));
+        t = (double)xv[u].y - (double)qv.y;
+        e = __dadd_rn(e, __dmul_rn(t, t));
+        t = (double)xv[u].z - (double)qv.z;
+        e = __dadd_rn(e, __dmul_rn(t, t));
+        t = (double)xv[u].w - (double)qv.w;
+        e = __dadd_rn(e, __dmul_rn(t, t));
+      }
+    }
+    for (; c + 4 <= d; c += 4) {
+      const float4 xv = __ldg(reinterpret_cast<const float4 *>(xr + c));
+      const float4 qv = *reinterpret_cast<const float4 *>(qs + c);
+      double t;
+      t = (double)xv.x - (double)qv.x;
+      e = __dadd_rn(e, __dmul_rn(t, t));
+      t = (double)xv.y - (double)qv.y;
+      e = __dadd_rn(e, __dmul_rn(t, t));
+      t = (double)xv.z - (double)qv.z;
+      e = __dadd_rn(e, __dmul_rn(t, t));
+      t = (double)xv.w - (double)qv.w;
+      e = __dadd_rn(e, __dmul_rn(t, t));
+    }
+  }
+  for (; c < d; ++c) {
+    const double t = (double)__ldg(xr + c) - (double)qs[c];
+    e = __dadd_rn(e, __dmul_rn(t, t));
+  }
+  return e;
+}
+
+constexpr int kRerankSmemD = 2048;  // query staged in shared memory up to this width
+
 // Exact re-rank of the survivors the u8 filter handed over (a.surv /
 // a.nsurv): one warp per query, one lane per survivor (two when > 32), each
 // lane summing its row's float64 distance in coordinate order
@@ -1731,22 +1780,34 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
 // Many queries' rows are in flight at once, instead of a few threads per
 // filter CTA waiting out one row each.
 __global__ void __launch_bounds__(256) k_rerank(TopkArgs a) {
+  extern __shared__ float rr_smem[];
   const int lane = threadIdx.x & 31;
+  const bool staged = a.d <= kRerankSmemD;
+  float *qs = rr_smem + (threadIdx.x >> 5) * ((a.d + 3) & ~3);
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < a.nq; q += nw) {
     const int ns = a.nsurv[q];
     if (ns < 0) continue;
     const float *qrow = a.Q + q * a.ldq;
+    if (staged) {
+      __syncwarp();
+      for (int c = lane; c < a.d; c += 32) qs[c] = __ldg(qrow + c);
+      __syncwarp();
+    }
     const bool v4 = a.vec4 && aligned16_dev(qrow);
     unsigned long long k0 = ~0ull, k1 = ~0ull;
     int i0 = 0x7fffffff, i1 = 0x7fffffff;
     if (lane < ns) {
       i0 = a.surv[q * kSurvCap + lane];
-      k0 = (unsigned long long)__double_as_longlong(exact_dist2(a.X + (int64_t)i0 * a.ldx, qrow, a.d, v4));
+      const float *xr = a.X + (int64_t)i0 * a.ldx;
+      k0 = (unsigned long long)__double_as_longlong(staged ? exact_dist2_sq(xr, qs, a.d, a.vec4)
+                                                           : exact_dist2(xr, qrow, a.d, v4));
     }
     if (lane + 32 < ns) {
       i1 = a.surv[q * kSurvCap + 32 + lane];
-      k1 = (unsigned long long)__double_as_longlong(exact_dist2(a.X + (int64_t)i1 * a.ldx, qrow, a.d, v4));
+      const float *xr = a.X + (int64_t)i1 * a.ldx;
+      k1 = (unsigned long long)__double_as_longlong(staged ? exact_dist2_sq(xr, qs, a.d, a.vec4)
+                                                           : exact_dist2(xr, qrow, a.d, v4));
     }
     int r0 = 0, r1 = 0;
     for (int j = 0; j < 32; ++j) {
@@ -2130,7 +2191,9 @@ int32_t igemm_rows_tn(const int8_t *Xs, int64_t n, const int8_t *Qop, int64_t m,
 static void launch_rerank(const TopkArgs &a, cudaStream_t s) {
   const int64_t blocks = ceil_div<int64_t>(a.nq, 8);
   const int64_t cap = (int64_t)num_sms() * 16;
-  (count_launch(), k_rerank<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, s>>>(a));
+  const size_t smem = a.d <= kRerankSmemD ? (size_t)8 * ((a.d + 3) & ~3) * sizeof(float) : 0;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_rerank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  (count_launch(), k_rerank<<<(unsigned)(blocks < cap ? blocks : cap), 256, smem, s>>>(a));
 }
 
 static int32_t scan_u8_impl(const float *X, int64_t n, int32_t d, int64_t ldx, const void *Xq, int64_t ldq,
