@@ -253,22 +253,8 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
         e = min(nq, s + chunk)
         qb = Qd[s:e]
         if bits_mode:
-            # K2 + K3 run on their own stream beside K4's query quantisation and
-            # tensor-core GEMM (which need only the queries); the filter waits
-            # for the candidate bitmaps
-            vs = _device.vote_stream()
-            ev_start = torch.cuda.Event()
-            ev_start.record()
-            with torch.cuda.stream(vs):
-                vs.wait_event(ev_start)
-                stage("route", _route_launch, D, qb, e - s, int(Qd.stride(0)), leaves)
-                stage("vote", _vote_bitmap, D, leaves, e - s, votes, vdir, bits, bstride,
-                      counts[s:e])
-                ev_vote = torch.cuda.Event()
-                ev_vote.record(vs)
-            stage("scan_topk", _scan_bits, D, qb, e - s, int(Qd.stride(0)), bits, bstride, k,
-                  ids[s:e], dists[s:e], ev_vote)
-            torch.cuda.current_stream().wait_event(ev_vote)  # leaves/bits are reused
+            _run_bits(D, qb, e - s, int(Qd.stride(0)), leaves, votes, vdir, bits, bstride,
+                      counts[s:e], k, ids[s:e], dists[s:e], stage)
             continue
         stage("route", _route_launch, D, qb, e - s, int(Qd.stride(0)), leaves)
         if choice is None and e - s >= 256:
@@ -290,6 +276,27 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
                 variant = env
         stage("scan_topk", _scan_launch, D, variant, args)
     return ids, dists, counts
+
+
+def _run_bits(D, qb, m, ldq, leaves, votes, vdir, bits, bstride, counts, k, ids, dists, stage=None):
+    """The bitmap route: K2 + K3 on their own stream beside K4's query
+    quantisation and tensor-core GEMM (which need only the queries); the
+    filter waits for the candidate bitmaps."""
+    torch = _device.torch_mod()
+    if stage is None:
+        def stage(name, fn, *a):
+            fn(*a)
+    vs = _device.vote_stream()
+    ev_start = torch.cuda.Event()
+    ev_start.record()
+    with torch.cuda.stream(vs):
+        vs.wait_event(ev_start)
+        stage("route", _route_launch, D, qb, m, ldq, leaves)
+        stage("vote", _vote_bitmap, D, leaves, m, votes, vdir, bits, bstride, counts)
+        ev_vote = torch.cuda.Event()
+        ev_vote.record(vs)
+    stage("scan_topk", _scan_bits, D, qb, m, ldq, bits, bstride, k, ids, dists, ev_vote)
+    torch.cuda.current_stream().wait_event(ev_vote)  # leaves/bits are reused
 
 
 def _bstride(D):
@@ -404,14 +411,16 @@ def _autotune(D, qb, m, ldq, leaves, votes, vdir, cap, counts, k, ids, dists):
         e1.synchronize()
         return e0.elapsed_time(e1)
 
+    tr = timed(_route_launch, D, qb, m, ldq, leaves)
     if "u8gemm_bits" in variants:
+        # timed as it runs: route + vote beside the GEMM, then the filter
         bstride = _bstride(D)
         bits = torch.empty((m, bstride), dtype=torch.int32, device=dev)
-        tv = timed(_vote_bitmap, D, leaves, m, votes, vdir, bits, bstride, counts)
-        times["u8gemm_bits"] = tv + timed(_scan_bits, D, qb, m, ldq, bits, bstride, k, ids, dists)
+        times["u8gemm_bits"] = timed(_run_bits, D, qb, m, ldq, leaves, votes, vdir, bits, bstride,
+                                     counts, k, ids, dists)
     if list_vars:
         cand = torch.empty((m, cap), dtype=torch.int32, device=dev)
-        tv = timed(_vote_list, D, leaves, m, votes, vdir, cand, cap, counts)
+        tv = tr + timed(_vote_list, D, leaves, m, votes, vdir, cand, cap, counts)
         args = (qb, m, ldq, cand, cap, counts, k, ids, dists)
         for v in list_vars:
             times[v] = tv + timed(_scan_launch, D, v, args)
