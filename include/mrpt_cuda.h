@@ -300,6 +300,26 @@ int32_t mrpt_scan_topk_u8gemm_bits(const float *X, int64_t n, int32_t d, int64_t
                                    int64_t *ids, double *dists, void *workspace,
                                    int64_t ws_bytes, void *wait_event, void *stream);
 
+/* The u8 filter over candidate bitmaps fused onto the tcgen05 tensor cores
+ * (replaces the _cy.scan + lexsort step of exact_knn_in_set,
+ * pkg/src/mrpt/search.py:146-172, like every K4 route): a persistent kernel
+ * streams the s8 shadow rows Xs (mrpt_u8_gemm_rows) through TMA into
+ * shared memory, forms each 128-query x 256-row block of dot products with
+ * tcgen05.mma.kind::i8 into TMEM and bounds every candidate straight out of
+ * TMEM (no dot-product matrix in HBM); survivors get the exact float64
+ * re-rank.  Same arguments and results as mrpt_scan_topk_u8gemm_bits.
+ * 128 <= ldq <= 896, k <= 32.  workspace: 256-byte aligned, sized by
+ * mrpt_scan_topk_u8tc_workspace_size (smaller workspaces run smaller query
+ * chunks). */
+int32_t mrpt_scan_topk_u8tc_workspace_size(int64_t n, int64_t ldq, int64_t nq,
+                                           int64_t *bytes);
+int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d, int64_t ldx,
+                                 const void *Xs, int64_t ldq, const void *info,
+                                 const float *Q, int64_t nq, int64_t ldqq,
+                                 const uint32_t *cbits, int64_t bstride, int32_t k,
+                                 int64_t *ids, double *dists, void *workspace,
+                                 int64_t ws_bytes, void *wait_event, void *stream);
+
 /* Sorted de-duplication of arbitrary candidate ids (np.unique,
  * search.py:157) through an n-bit bitmap.  ids outside [0, n) set
  * *bad (device int32) to 1 (IntegrityError, search.py:158-162).

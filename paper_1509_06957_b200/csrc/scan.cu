@@ -17,6 +17,7 @@
 #include <stdlib.h>
 
 #include "common.cuh"
+#include <cudaTypedefs.h>
 
 namespace mrpt {
 
@@ -1909,6 +1910,8 @@ k_scan(const float *__restrict__ X, int64_t ldx, int d, const int64_t *__restric
 
 }  // namespace mrpt
 
+#include "tc_filter.cuh"
+
 using namespace mrpt;
 
 static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -2487,4 +2490,227 @@ extern "C" int32_t mrpt_scan_topk_u8gemm_bits(const float *X, int64_t n, int32_t
   if (!cbits) return fail(MRPT_EPARAM, "mrpt_scan_topk_u8gemm_bits: cbits is NULL");
   return u8gemm_impl(X, n, d, ldx, Xs, ldq, info, Q, nq, ldqq, nullptr, 0, nullptr, cbits, bstride, k, ids,
                      dists, workspace, ws_bytes, stream, wait_event);
+}
+
+// ------------------------------------------------------------ K4 tc route --
+// The u8 filter fused onto tcgen05 (tc_filter.cuh): no dot-product matrix in
+// HBM.  Workspace per query chunk of mc queries: quantised queries, their
+// parameters, the row records, per-query entry lists and counts, and the
+// survivor / fallback lists the re-rank and the exact fallback read.
+static const int kTcCap = tc::kSelCap;
+static const int kTcKb = 256;  // per query: the streams' k smallest bounds
+
+static int64_t u8tc_bytes(int64_t n, int64_t ldq, int64_t mc, int64_t *off) {
+  auto al = [](int64_t x) { return (x + 1023) & ~(int64_t)1023; };
+  int64_t o = 0;
+  off[0] = o;  // qop (mc x ldq s8)
+  o = al(o + mc * ldq);
+  off[1] = o;  // qp
+  o = al(o + mc * (int64_t)sizeof(QParams));
+  off[2] = o;  // rinfo (n x 16 B)
+  o = al(o + n * 16);
+  off[3] = o;  // entries (mc x cap x 16 B)
+  o = al(o + mc * kTcCap * 16);
+  off[4] = o;  // entry counts (mc), shared k-th bounds (mc), bound counts (mc), bounds (mc x kTcKb)
+  o = al(o + mc * 12 + mc * kTcKb * 4);
+  off[5] = o;  // fallback count + list, survivor counts, survivor lists
+  return al(o + ((mc + 1) + mc * (kSurvCap + 1)) * 4) + 1024;  // + base alignment
+}
+
+static const int64_t kTcChunk = 16384;  // queries per chunk (entry lists: 8 KB per query)
+
+extern "C" int32_t mrpt_scan_topk_u8tc_workspace_size(int64_t n, int64_t ldq, int64_t nq, int64_t *bytes) {
+  clear_error();
+  if (n < 1 || ldq < 16 || nq < 0 || !bytes) return fail(MRPT_ESHAPE, "mrpt_scan_topk_u8tc_workspace_size");
+  int64_t mc = nq < kTcChunk ? nq : kTcChunk;
+  if (mc < 1) mc = 1;
+  int64_t off[6];
+  *bytes = u8tc_bytes(n, ldq, mc, off);
+  return MRPT_OK;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    tried = true;
+  }
+  return fn;
+}
+
+// 2-D u8 tensor map (rows x ldq bytes), boxes of 128 bytes x box_rows rows,
+// 128-B swizzle (the UMMA K-major canonical layout); reads past the edges
+// fill zeros.
+static bool tc_map(CUtensorMap *m, const void *base, int64_t rows, int64_t ldq, int box_rows) {
+  PFN_cuTensorMapEncodeTiled_v12000 fn = tc_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)ldq, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ldq};
+  cuuint32_t box[2] = {(cuuint32_t)tc::kKB, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d, int64_t ldx, const void *Xs,
+                                            int64_t ldq, const void *info, const float *Q, int64_t nq,
+                                            int64_t ldqq, const uint32_t *cbits, int64_t bstride, int32_t k,
+                                            int64_t *ids, double *dists, void *workspace, int64_t ws_bytes,
+                                            void *wait_event, void *stream) {
+  clear_error();
+  if (!cbits || bstride < (n + 31) / 32) return fail(MRPT_EPARAM, "mrpt_scan_topk_u8tc_bits: bad candidate bitmaps");
+  if (!X || !Xs || !info || !Q || n < 1 || n >= (int64_t)1 << 31 || d < 1 || ldx < d || ldqq < d || nq < 0)
+    return fail(MRPT_ESHAPE, "mrpt_scan_topk_u8tc_bits: bad shape");
+  if (ldq % 16 != 0 || ldq < d || ldq < tc::kKB || ldq > tc::kMaxKB * tc::kKB || k < 1 || k > 32 || d % 4 != 0 ||
+      ldx % 4 != 0 || !aligned16(X) || !aligned16(Xs) || (reinterpret_cast<uintptr_t>(info) & 15u))
+    return fail(MRPT_EPARAM, "mrpt_scan_topk_u8tc_bits: unsupported shape");
+  if (nq == 0) return MRPT_OK;
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255u))
+    return fail(MRPT_EWORKSPACE, "mrpt_scan_topk_u8tc_bits: workspace must be 256-byte aligned");
+  int64_t off[6];
+  int64_t mc = nq < kTcChunk ? nq : kTcChunk;
+  while (mc > 0 && u8tc_bytes(n, ldq, mc, off) > ws_bytes) mc = mc > 128 ? mc - 128 : mc - 1;
+  if (mc < 1) return fail(MRPT_EWORKSPACE, "mrpt_scan_topk_u8tc_bits: workspace too small for one query");
+  u8tc_bytes(n, ldq, mc, off);
+  char *w = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(workspace) + 1023) & ~(uintptr_t)1023);
+  int8_t *qop = reinterpret_cast<int8_t *>(w + off[0]);
+  QParams *qp = reinterpret_cast<QParams *>(w + off[1]);
+  uint4 *rinfo = reinterpret_cast<uint4 *>(w + off[2]);
+  uint4 *ent = reinterpret_cast<uint4 *>(w + off[3]);
+  int32_t *ent_cnt = reinterpret_cast<int32_t *>(w + off[4]);
+  int32_t *fb = reinterpret_cast<int32_t *>(w + off[5]);
+  cudaStream_t s = as_stream(stream);
+  CUtensorMap tmB;
+  if (!tc_map(&tmB, Xs, n, ldq, tc::kN)) return fail(MRPT_ECUDA, "mrpt_scan_topk_u8tc_bits: tensor map (rows)");
+  {
+    const int64_t g = ceil_div<int64_t>(n, 256);
+    (count_launch(), tc::k_tc_rows<<<(unsigned)(g < 4096 ? g : 4096), 256, 0, s>>>(
+                         reinterpret_cast<const uint4 *>(info), n, rinfo));
+  }
+  const char *cge = getenv("MRPT_TC_CG");
+  const int cg = cge ? atoi(cge) : 4;
+  void (*fk)(const CUtensorMap, const CUtensorMap, tc::TcArgs);
+  int fthreads;
+  if (cg >= 4) {
+    fk = k <= 16 ? tc::k_tc_filter<16, 4> : tc::k_tc_filter<32, 4>;
+    fthreads = tc::threads_for<4>();
+  } else if (cg == 2) {
+    fk = k <= 16 ? tc::k_tc_filter<16, 2> : tc::k_tc_filter<32, 2>;
+    fthreads = tc::threads_for<2>();
+  } else {
+    fk = k <= 16 ? tc::k_tc_filter<16, 1> : tc::k_tc_filter<32, 1>;
+    fthreads = tc::threads_for<1>();
+  }
+  cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
+  const int sel_smem = 8 * 4 * tc::kSelCap;
+  cudaFuncSetAttribute(tc::k_tc_select, cudaFuncAttributeMaxDynamicSharedMemorySize, sel_smem);
+  const int buf = (k + kScanNT <= 1024) ? 1024 : 2048;
+  topk_fn tfn = buf == 1024 ? k_scan_topk_tiled<1024> : k_scan_topk_tiled<2048>;
+  const size_t tsmem =
+      (size_t)buf * 12 + sizeof(float) * (kScanNT / 32) * 32 * kTileStride + sizeof(double) * (size_t)d;
+  cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+  const int ntiles = (int)ceil_div<int64_t>(n, tc::kN);
+  for (int64_t q0 = 0; q0 < nq; q0 += mc) {
+    const int64_t m = nq - q0 < mc ? nq - q0 : mc;
+    const int64_t g1 = m < (int64_t)num_sms() * 8 ? m : (int64_t)num_sms() * 8;
+    (count_launch(), k_quantize_q8<<<(unsigned)g1, kScanNT, 0, s>>>(Q + q0 * ldqq, ldqq, d, (int)ldq, m, qop, qp));
+    CUtensorMap tmA;
+    if (!tc_map(&tmA, qop, m, ldq, tc::kM)) return fail(MRPT_ECUDA, "mrpt_scan_topk_u8tc_bits: tensor map (queries)");
+    cudaMemsetAsync(ent_cnt, 0, (size_t)m * 4, s);
+    cudaMemsetAsync(ent_cnt + mc, 0x7f, (size_t)m * 4, s);  // 3.4e38: no bound yet
+    cudaMemsetAsync(ent_cnt + 2 * mc, 0, (size_t)m * 4, s);
+    cudaMemsetAsync(fb, 0, sizeof(int32_t), s);
+    if (wait_event && q0 == 0) cudaStreamWaitEvent(s, reinterpret_cast<cudaEvent_t>(wait_event), 0);
+    tc::TcArgs ta;
+    ta.n = n;
+    ta.m = m;
+    ta.ntiles = ntiles;
+    ta.nqb = (int)ceil_div<int64_t>(m, tc::kM);
+    ta.kblocks = (int)ceil_div<int64_t>(ldq, tc::kKB);
+    ta.k = k;
+    ta.ldq = (int)ldq;
+    ta.rinfo = rinfo;
+    ta.qp = qp;
+    ta.cbits = cbits + q0 * bstride;
+    ta.bstride = bstride;
+    ta.ent = ent;
+    ta.ent_cnt = ent_cnt;
+    ta.cap = kTcCap;
+    ta.su_g = reinterpret_cast<unsigned *>(ent_cnt + mc);
+    ta.kb_cnt = ent_cnt + 2 * mc;
+    ta.kb = reinterpret_cast<float *>(ent_cnt + 3 * mc);
+    ta.kbcap = kTcKb;
+    const int64_t items = (int64_t)ta.nqb * ntiles;
+    const int grid = (int)(items < num_sms() ? items : num_sms());
+    ta.dbgD = nullptr;
+    ta.noepi = getenv("MRPT_TC_NOEPI") ? atoi(getenv("MRPT_TC_NOEPI")) : 0;
+    const bool dbg = getenv("MRPT_TC_DEBUG") != nullptr;
+    int32_t *D1 = nullptr, *D2 = nullptr;
+    if (dbg) {
+      cudaMalloc(&D1, (size_t)m * n * 4);
+      cudaMalloc(&D2, (size_t)m * ((n + 15) & ~15) * 4 + 64);
+      ta.dbgD = D1;
+    }
+    (count_launch(), fk<<<grid, fthreads, tc::kSmemBytes, s>>>(tmA, tmB, ta));
+    if (dbg) {
+      const int64_t ldD = (n + 15) & ~(int64_t)15;
+      int32_t st = igemm_rows_tn(reinterpret_cast<const int8_t *>(Xs), ldD, qop, m, ldq, D2, ldD, s);
+      // compact D2 rows to n columns
+      for (int64_t r = 0; r < m && ldD != n; ++r) cudaMemcpyAsync(D2 + r * n, D2 + r * ldD, n * 4, cudaMemcpyDeviceToDevice, s);
+      unsigned long long *o = nullptr;
+      cudaMalloc(&o, 24);
+      cudaMemsetAsync(o, 0, 24, s);
+      tc::k_tc_debug<<<1024, 256, 0, s>>>(D1, D2, m * n, ent_cnt, m, o);
+      unsigned long long h[3];
+      cudaMemcpyAsync(h, o, 24, cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      int32_t fbc = 0;
+      fprintf(stderr, "[tc debug] m=%lld n=%lld gemm_st=%d D mismatches=%llu entries total=%llu max=%llu (cap %d)\n",
+              (long long)m, (long long)n, st, h[0], h[1], h[2], kTcCap);
+      (void)fbc;
+      cudaFree(o);
+      cudaFree(D1);
+      cudaFree(D2);
+    }
+    TopkArgs a = {};
+    a.X = X;
+    a.n = n;
+    a.d = d;
+    a.ldx = ldx;
+    a.Q = Q + q0 * ldqq;
+    a.nq = m;
+    a.ldq = ldqq;
+    a.cbits = ta.cbits;
+    a.bstride = bstride;
+    a.k = k;
+    a.kstride = k;
+    a.ids = ids + q0 * k;
+    a.dists = dists + q0 * k;
+    a.vec4 = true;
+    a.nsurv = fb + 1 + mc;
+    a.surv = a.nsurv + mc;
+    {
+      const int64_t g = ceil_div<int64_t>(m, 4);
+      (count_launch(), tc::k_tc_select<<<(unsigned)(g < 4096 ? g : 4096), 128, sel_smem, s>>>(
+                           ent, ent_cnt, ta.kb, ta.kb_cnt, kTcKb, kTcCap, m, k, a.surv, a.nsurv, fb + 1, fb));
+    }
+    if (getenv("MRPT_TC_DEBUG")) {
+      int32_t fbc = 0;
+      cudaMemcpyAsync(&fbc, fb, 4, cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      fprintf(stderr, "[tc debug] fallback queries %d of %lld\n", fbc, (long long)m);
+    }
+    a.qlist = fb + 1;
+    a.qcount = fb;
+    const int64_t tg = m < 64 ? m : 64;
+    (count_launch(), tfn<<<(unsigned)tg, kScanNT, tsmem, s>>>(a));
+    launch_rerank(a, s);
+  }
+  return launch_status("mrpt_scan_topk_u8tc_bits");
 }

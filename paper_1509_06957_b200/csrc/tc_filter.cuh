@@ -1,0 +1,628 @@
+// K4 "tc" route: the u8 filter fused onto the 5th-generation tensor cores.
+//
+// Included by scan.cu (it shares QParams, dist_bounds2, admit2, warp_sort and
+// the survivor hand-over with the other u8 routes).
+//
+// The GEMM route (gemm.cu + k_scan_topk_u8<DM>) forms every (query, row)
+// dot product of the u8 shadow with a library int8 GEMM, writes the s32
+// matrix D to HBM and reads it back in a separate filter pass (config 2:
+// 2.4 GB written + 2.4 GB read per 10k queries).  This kernel never
+// materialises D:
+//
+//   * a persistent CTA per SM walks a contiguous range of (query block,
+//     row tile) items: 128 queries x 256 rows;
+//   * the query block's quantised rows (A, s8, K-major, <= 7 x 128 B) are
+//     loaded once by TMA and stay resident in shared memory; row tiles of the
+//     s8 shadow (B) stream through a 3-stage TMA ring (128-B swizzle);
+//   * one thread issues tcgen05.mma.kind::i8 (s8 x s8 -> s32, M=128,
+//     N=256, K=32 per instruction) into a double-buffered TMEM accumulator
+//     (2 x 256 columns);
+//   * 16 epilogue warps read the accumulator with tcgen05.ld (one TMEM lane
+//     = one query, 4 warps per lane quarter split the tile's columns) and
+//     apply the u8 filter's admission rule to every column whose bit is set
+//     in the query's candidate bitmap (K3's output): the same float32 bound
+//     (t1 + t2 - t3, eta, radius) as k_scan_topk_u8, against the query's
+//     running k-th upper bound kept in registers (sorted, k <= KT) and
+//     shared through shared memory between the query's 4 column warps;
+//   * admitted candidates go to a per-query entry list {L, U, id} in global
+//     memory (rare after warm-up); k_tc_select takes the k-th smallest U per
+//     query and hands the survivors (L <= U_k) to k_rerank, the exact float64
+//     re-rank every u8 route shares.
+//
+// D values are the same exact int32 dot products as the library GEMM's, so
+// the admitted sets are supersets of the exact top-k exactly as before and
+// the results are bit-identical to the reference's.
+#pragma once
+#include <cuda.h>
+
+namespace mrpt {
+namespace tc {
+
+constexpr int kM = 128;         // queries per block = TMEM lanes
+constexpr int kN = 256;         // rows per tile = TMEM columns per accumulator
+constexpr int kKB = 128;        // K bytes per block (one 128-B swizzle row)
+constexpr int kMaxKB = 7;       // resident query block: ldq <= 896
+constexpr int kStages = 3;      // row-tile ring
+// epilogue: 4 lane quarters x CG column groups (template); + TMA + MMA warps
+template <int CG>
+constexpr int threads_for() {
+  return (4 * CG + 2) * 32;
+}
+constexpr uint32_t kABytes = kM * kKB;    // 16 KB per K block
+constexpr uint32_t kBBytes = kN * kKB;    // 32 KB per stage
+constexpr uint32_t kInfoBytes = kN * 16;  // 4 KB of row records per tile
+
+// shared-memory carve-up (offsets from a 1024-B aligned base)
+constexpr uint32_t kOffA = 0;
+constexpr uint32_t kOffB = kOffA + kMaxKB * kABytes;
+constexpr uint32_t kOffInfo = kOffB + kStages * kBBytes;
+constexpr uint32_t kOffBar = kOffInfo + 2 * kInfoBytes;
+// barriers: fullB[3], emptyB[3], fullA, emptyA, tmem_full[2], epi_empty[2], info_full[2]
+constexpr int kNumBars = 2 * kStages + 2 + 6;
+constexpr uint32_t kOffTmemSlot = kOffBar + 8 * kNumBars;
+constexpr uint32_t kOffSu = kOffTmemSlot + 16;
+constexpr uint32_t kSmemBytes = kOffSu + 4 * kM + 1024;  // + alignment slack
+
+struct TcArgs {
+  int64_t n;            // data rows
+  int64_t m;            // queries of this chunk
+  int ntiles;           // ceil(n / kN)
+  int nqb;              // ceil(m / kM)
+  int kblocks;          // ceil(ldq / kKB)
+  int k;                // neighbours
+  int ldq;              // shadow row bytes (the unsigned-query offset term)
+  const uint4 *rinfo;   // per row {t1 = sx^2 * nrm (f32), 2 sx (f32), radius (f32), 128 * sum(u8) (s32)}
+  const QParams *qp;    // per query of the chunk
+  const uint32_t *cbits;
+  int64_t bstride;
+  uint4 *ent;           // (m, cap) entries {L (f32, rounded down), U (f32, rounded up), id, 0}
+  int32_t *ent_cnt;     // (m) entries appended (may exceed cap: overflow -> exact fallback)
+  int cap;
+  unsigned *su_g;       // (m) per-query sqrt(k-th upper bound) as float bits, shared by all CTAs
+  float *kb;            // (m, kbcap) every stream's k smallest upper bounds (their union holds the query's k smallest)
+  int32_t *kb_cnt;      // (m) values appended to kb
+  int kbcap;
+  int32_t *dbgD;        // optional (MRPT_TC_DEBUG): every dot product, (m, n)
+  int noepi;            // experiment (MRPT_TC_NOEPI): skip the epilogue work (MMA + TMA pipeline only)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// Producer / MMA waits: back off between polls so a single-thread role
+// spinning on a barrier does not take issue slots from the epilogue warps
+// that share its scheduler.
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(64);
+  }
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major, 128-B swizzle (8 rows x 128 B
+// atoms, 1024 B apart), Blackwell descriptor version 1.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
+  uint64_t d = (uint64_t)((addr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;            // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // stride byte offset: next 8-row group
+  d |= (uint64_t)1 << 46;            // version
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: s8 x s8 -> s32, K-major A and B, M=128, N=256
+constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kN >> 3) << 17) |
+                            ((uint32_t)(kM >> 4) << 24);
+
+__device__ __forceinline__ void mma_i8(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(dtmem), "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+        "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+        "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Per-query state of one epilogue thread.
+template <int KT>
+struct EpiState {
+  float topU[KT];  // the k smallest upper bounds so far (unsorted; +inf until filled, -inf fillers past k)
+  float umax;      // max of topU (the k-th smallest bound) and its slot
+  int imax;
+  float su;        // sqrt(k-th smallest U) rounded up (+inf until k bounds exist)
+  int base, left;  // current block of reserved entry slots: next = base + (kEntBlock - left)
+};
+
+constexpr int kEntBlock = 32;  // entry slots a thread reserves at a time (one atomic per block)
+
+// End of a stream (one thread's share of a query): publish its k smallest
+// upper bounds and mark the unused tail of its reserved block (L = NaN: never
+// a survivor).
+template <int KT>
+__device__ __forceinline__ void tc_flush(EpiState<KT> &st, int64_t q, const TcArgs &a) {
+  if (st.umax < __int_as_float(0x7f800000) || st.left < kEntBlock || st.base > 0) {
+    const int o = atomicAdd(a.kb_cnt + q, a.k);
+#pragma unroll
+    for (int i = 0; i < KT; ++i)
+      if (i < a.k && o + i < a.kbcap) a.kb[q * a.kbcap + o + i] = st.topU[i];
+  }
+  for (; st.left > 0; --st.left) {
+    const int slot = st.base + (kEntBlock - st.left);
+    if (slot < a.cap) a.ent[q * a.cap + slot] = make_uint4(0x7fc00000u, 0x7f800000u, 0u, 0u);
+  }
+}
+
+// Rigorous float32 bounds of the exact squared distance from the filter's
+// (A, r, eta) (same quantities as dist_bounds2, every operation rounded
+// toward the safe side instead of float64 plus a relative margin).
+__device__ __forceinline__ void dist_bounds_f(float A, float r, float eta, float &L, float &U) {
+  const float slo = fmaxf(0.f, __fsub_rd(__fsqrt_rd(fmaxf(0.f, __fsub_rd(A, eta))), r));
+  const float shi = __fadd_ru(__fsqrt_ru(__fadd_ru(A, eta)), r);
+  L = __fmul_rd(slo, slo);
+  U = __fmul_ru(shi, shi);
+}
+
+template <int KT>
+__device__ __forceinline__ void tc_admit(EpiState<KT> &st, float A, float r, float eta, int32_t col, int64_t q,
+                                      const TcArgs &a, unsigned *su_slot) {
+  float Lf, Uf;
+  dist_bounds_f(A, r, eta, Lf, Uf);
+  if (st.left == 0) {
+    st.base = atomicAdd(a.ent_cnt + q, kEntBlock);
+    st.left = kEntBlock;
+  }
+  const int slot = st.base + (kEntBlock - st.left--);
+  if (slot < a.cap)
+    a.ent[q * a.cap + slot] = make_uint4(__float_as_uint(Lf), __float_as_uint(Uf), (uint32_t)col, 0u);
+  if (Uf < st.umax) {
+    // replace the largest of the k bounds, then find the new largest (a
+    // depth-log2(KT) tree instead of a KT-deep insertion chain)
+#pragma unroll
+    for (int i = 0; i < KT; ++i) st.topU[i] = i == st.imax ? Uf : st.topU[i];
+    float mv[KT];
+    int mi[KT];
+#pragma unroll
+    for (int i = 0; i < KT; ++i) {
+      mv[i] = st.topU[i];
+      mi[i] = i;
+    }
+#pragma unroll
+    for (int w = KT / 2; w >= 1; w >>= 1) {
+#pragma unroll
+      for (int i = 0; i < w; ++i) {
+        const bool gt = mv[i + w] > mv[i];
+        mv[i] = gt ? mv[i + w] : mv[i];
+        mi[i] = gt ? mi[i + w] : mi[i];
+      }
+    }
+    st.umax = mv[0];
+    st.imax = mi[0];
+    const float uk = st.umax;
+    if (uk < 3.0e38f) {
+      const float s = __fsqrt_ru(uk);
+      if (s < st.su) {
+        st.su = s;
+        atomicMin(su_slot, __float_as_uint(s));
+        atomicMin(a.su_g + q, __float_as_uint(s));
+      }
+    }
+  }
+}
+
+template <int KT, int CG>
+__global__ void __launch_bounds__(threads_for<CG>(), 1)
+    k_tc_filter(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~(uintptr_t)1023);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t sA = sbase + kOffA, sB = sbase + kOffB, sInfo = sbase + kOffInfo;
+  const uint32_t bar0 = sbase + kOffBar;
+  auto fullB = [&](int s) { return bar0 + 8u * s; };
+  auto emptyB = [&](int s) { return bar0 + 8u * (kStages + s); };
+  const uint32_t fullA = bar0 + 8u * (2 * kStages), emptyA = fullA + 8u;
+  auto tmemFull = [&](int b) { return bar0 + 8u * (2 * kStages + 2 + b); };
+  auto epiEmpty = [&](int b) { return bar0 + 8u * (2 * kStages + 4 + b); };
+  auto infoFull = [&](int b) { return bar0 + 8u * (2 * kStages + 6 + b); };
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + kOffTmemSlot);
+  unsigned *su_s = reinterpret_cast<unsigned *>(smem + kOffSu);
+
+  constexpr int kEpiWarps = 4 * CG, kColsPerWarp = kN / CG;
+  constexpr int kProdWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t W = (int64_t)a.nqb * a.ntiles;
+  const int64_t it0 = W * blockIdx.x / gridDim.x, it1 = W * (blockIdx.x + 1) / gridDim.x;
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(fullB(s), 1);
+      mbar_init(emptyB(s), 1);
+    }
+    mbar_init(fullA, 1);
+    mbar_init(emptyA, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tmemFull(b), 1);
+      mbar_init(epiEmpty(b), kEpiWarps);
+      mbar_init(infoFull(b), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == kProdWarp && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (tid < kM) su_s[tid] = 0x7f800000u;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == kProdWarp) {
+    if (lane == 0) {
+      int64_t cur_qb = -1;
+      uint32_t nA = 0, g = 0;
+      for (int64_t it = it0; it < it1; ++it) {
+        const int qb = (int)(it / a.ntiles), tile = (int)(it % a.ntiles);
+        if (qb != cur_qb) {
+          mbar_wait_sleep(emptyA, (nA & 1u) ^ 1u);
+          mbar_expect_tx(fullA, (uint32_t)a.kblocks * kABytes);
+          for (int kb = 0; kb < a.kblocks; ++kb) tma_load_2d(sA + kb * kABytes, &tmA, fullA, kb * kKB, qb * kM);
+          ++nA;
+          cur_qb = qb;
+        }
+        for (int kb = 0; kb < a.kblocks; ++kb, ++g) {
+          const int s = (int)(g % kStages);
+          mbar_wait_sleep(emptyB(s), ((g / kStages) & 1u) ^ 1u);
+          mbar_expect_tx(fullB(s), kBBytes);
+          tma_load_2d(sB + s * kBBytes, &tmB, fullB(s), kb * kKB, tile * kN);
+        }
+        const uint32_t li = (uint32_t)(it - it0), b = li & 1u;
+        mbar_wait_sleep(epiEmpty(b), ((li >> 1) & 1u) ^ 1u);
+        const int64_t rows = a.n - (int64_t)tile * kN < kN ? a.n - (int64_t)tile * kN : kN;
+        mbar_expect_tx(infoFull(b), (uint32_t)rows * 16u);
+        bulk_load(sInfo + b * kInfoBytes, a.rinfo + (int64_t)tile * kN, (uint32_t)rows * 16u, infoFull(b));
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    if (lane == 0) {
+      int64_t cur_qb = -1;
+      uint32_t nA = 0, g = 0;
+      for (int64_t it = it0; it < it1; ++it) {
+        const int qb = (int)(it / a.ntiles);
+        if (qb != cur_qb) {
+          mbar_wait_sleep(fullA, nA & 1u);
+          ++nA;
+          cur_qb = qb;
+        }
+        const uint32_t li = (uint32_t)(it - it0), b = li & 1u;
+        mbar_wait_sleep(epiEmpty(b), ((li >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t dt = tmem_base + b * kN;
+        for (int kb = 0; kb < a.kblocks; ++kb, ++g) {
+          const int s = (int)(g % kStages);
+          mbar_wait_sleep(fullB(s), (g / kStages) & 1u);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < kKB / 32; ++kk) {
+            const uint64_t ad = sw128_desc(sA + kb * kABytes + kk * 32);
+            const uint64_t bd = sw128_desc(sB + s * kBBytes + kk * 32);
+            mma_i8(dt, ad, bd, (kb | kk) != 0 ? 1u : 0u);
+          }
+          mma_commit(emptyB(s));
+        }
+        mma_commit(tmemFull(b));
+        const bool last_of_qb = it + 1 >= it1 || (int)((it + 1) / a.ntiles) != qb;
+        if (last_of_qb) mma_commit(emptyA);
+      }
+    }
+  } else {
+    // ---------------- epilogue warps ----------------
+    const int lq = warp & 3, cg = warp >> 2;
+    const int qloc = lq * 32 + lane;
+    const uint32_t trow = tmem_base + ((uint32_t)(lq * 32) << 16);
+    const float4 *info4 = reinterpret_cast<const float4 *>(smem + kOffInfo);
+    EpiState<KT> st;
+    int64_t cur_qb = -1, q = 0;
+    bool valid = false;
+    float sqf = 0.f, t2f = 0.f, rq = 0.f;
+    int corr = 0, sel = 0;
+    // candidate words of item itx for this warp's columns
+    constexpr int NWD = kColsPerWarp / 32;
+    auto load_words = [&](int64_t itx, uint32_t (&w)[NWD]) {
+      const int qbx = (int)(itx / a.ntiles), tilex = (int)(itx % a.ntiles);
+      const int64_t qx = (int64_t)qbx * kM + qloc;
+#pragma unroll
+      for (int c = 0; c < NWD; ++c) {
+        const int64_t col0 = (int64_t)tilex * kN + cg * kColsPerWarp + c * 32;
+        uint32_t x = 0u;
+        if (qx < a.m && col0 < a.n) {
+          x = __ldg(a.cbits + qx * a.bstride + (col0 >> 5));
+          if (a.n - col0 < 32) x &= (1u << (a.n - col0)) - 1u;
+        }
+        w[c] = x;
+      }
+    };
+    uint32_t wnext[NWD];
+    if (it0 < it1) load_words(it0, wnext);
+    for (int64_t it = it0; it < it1; ++it) {
+      const int qb = (int)(it / a.ntiles), tile = (int)(it % a.ntiles);
+      uint32_t wd[NWD];
+#pragma unroll
+      for (int c = 0; c < NWD; ++c) wd[c] = wnext[c];
+      if (it + 1 < it1) load_words(it + 1, wnext);  // in flight while this tile is filtered
+      if (qb != cur_qb) {
+        if (valid) tc_flush<KT>(st, q, a);
+        // new query block: every epilogue warp is past the old one before
+        // the shared k-th bounds are reset
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        if (cg == 0) su_s[qloc] = 0x7f800000u;
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        cur_qb = qb;
+        q = (int64_t)qb * kM + qloc;
+        valid = q < a.m;
+#pragma unroll
+        for (int i = 0; i < KT; ++i) st.topU[i] = i < a.k ? __int_as_float(0x7f800000) : -__int_as_float(0x7f800000);
+        st.umax = __int_as_float(0x7f800000);
+        st.imax = 0;
+        st.su = __int_as_float(0x7f800000);
+        st.left = 0;
+        st.base = 0;
+        if (valid) {
+          const QParams P = a.qp[q];
+          sqf = P.sq;
+          t2f = P.t2f;
+          rq = P.rq;
+          // x.qq = D + 128 sum(qq) (+ 128 sum(x) - 16384 ldq for u8 queries), as k_scan_topk_u8
+          corr = 128 * P.qsum - (P.qsigned ? 0 : 16384 * a.ldq);
+          sel = P.qsigned ? 0 : 1;
+        }
+      }
+      if (valid) st.su = fminf(st.su, __uint_as_float(__ldcg(a.su_g + q)));
+      const uint32_t li = (uint32_t)(it - it0), b = li & 1u;
+      mbar_wait(infoFull(b), (li >> 1) & 1u);
+      mbar_wait(tmemFull(b), (li >> 1) & 1u);
+      tc_fence_after();
+      if (a.noepi == 1) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(epiEmpty(b));
+        continue;
+      }
+      // 16 columns per TMEM load (register budget: 18 warps per SM)
+#pragma unroll 1
+      for (int c = 0; c < kColsPerWarp / 16; ++c) {
+        uint32_t v[16];
+        const int cofs = cg * kColsPerWarp + c * 16;
+        tmem_ld16(trow + b * kN + cofs, v);
+        tmem_wait_ld();
+        const uint32_t wc = (wd[c >> 1] >> (16 * (c & 1))) & 0xffffu;
+        if (a.dbgD && valid) {
+          for (int j = 0; j < 16; ++j) {
+            const int64_t col = (int64_t)tile * kN + cofs + j;
+            if (col < a.n) a.dbgD[q * a.n + col] = (int32_t)v[j];
+          }
+        }
+        if (__any_sync(0xffffffffu, wc != 0u)) {
+          st.su = fminf(st.su, __uint_as_float(*reinterpret_cast<volatile unsigned *>(su_s + qloc)));
+          const float4 *ri = info4 + b * kN + cofs;
+          const int32_t colb = tile * kN + cofs;
+          // bound every column; the (rare after warm-up) admissions run
+          // once per set bit outside the unrolled loop
+          uint32_t take = 0u;
+          // superset of admit2 in plain float arithmetic: A <= (su + rad +
+          // rq)^2 * (1 + 2^-16) + 1e-6 (T + |t3|) covers every directed
+          // rounding of admit2 and its eta (<= 4.8e-7 (T + |t3|)); the exact
+          // rule runs below only for columns that pass
+          const float srq = st.su + rq;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float4 r4 = ri[j];
+            const int mys = (int)v[j] + corr + sel * __float_as_int(r4.w);
+            const float T = r4.x + t2f;
+            const float t3 = (r4.y * sqf) * (float)mys;
+            const float A = T - t3;
+            const float sr = srq + r4.z;
+            const float G = fmaf(sr * 1.0000153f, sr, fmaf(1.0e-6f, T + fabsf(t3), 2.4e-38f));
+            take |= (A <= G ? 1u : 0u) << j;
+          }
+          take &= wc;
+          if (a.noepi == 2) take = 0u;  // experiment: bounds without admissions
+          while (take) {
+            const int j = __ffs(take) - 1;
+            take &= take - 1u;
+            // v[j] by a depth-4 select tree
+            int d8[8], d4[4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) d8[i] = (j & 1) ? (int)v[2 * i + 1] : (int)v[2 * i];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) d4[i] = (j & 2) ? d8[2 * i + 1] : d8[2 * i];
+            const int d2a = (j & 4) ? d4[1] : d4[0], d2b = (j & 4) ? d4[3] : d4[2];
+            const int dv = (j & 8) ? d2b : d2a;
+            const float4 r4 = ri[j];
+            const int mys = dv + corr + sel * __float_as_int(r4.w);
+            const float t1 = r4.x;
+            const float t3 = (r4.y * sqf) * (float)mys;
+            const float A = (t1 + t2f) - t3;
+            const float eta = __fmul_ru(4.76837158203125e-07f, __fadd_ru(__fadd_ru(t1, t2f), fabsf(t3)));
+            const float r = __fadd_ru(r4.z, rq);
+            if (admit2(A, r, eta, st.su)) tc_admit<KT>(st, A, r, eta, colb + j, q, a, su_s + qloc);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(epiEmpty(b));
+    }
+    if (valid) tc_flush<KT>(st, q, a);
+  }
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
+// Row records of the fused filter, from the GEMM route's {scale, norm,
+// radius, sum}: t1 = scale^2 * norm exactly as k_scan_topk_u8 forms it,
+// 2 * scale, radius, 128 * sum (the unsigned-query offset term).
+__global__ void k_tc_rows(const uint4 *__restrict__ info, int64_t n, uint4 *__restrict__ rinfo) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 v = info[i];
+    const float sx = __uint_as_float(v.x);
+    const float t1 = sx * sx * (float)(int)v.y;
+    rinfo[i] = make_uint4(__float_as_uint(t1), __float_as_uint(2.0f * sx), v.z, (uint32_t)(128 * (int)v.w));
+  }
+}
+
+// Per query (one warp): k-th smallest U over the entries, survivors L <= U_k
+// to k_rerank's lists; list overflow or too many survivors -> exact fallback.
+constexpr int kSelCap = 1024;
+__global__ void __launch_bounds__(128) k_tc_select(const uint4 *__restrict__ ent, const int32_t *__restrict__ ent_cnt,
+                                                   const float *__restrict__ kb, const int32_t *__restrict__ kb_cnt,
+                                                   int kbcap, int cap, int64_t m, int k, int32_t *surv, int32_t *nsurv,
+                                                   int32_t *fb_list, int32_t *fb_count) {
+  extern __shared__ float sel_smem[];
+  float (*sk)[kSelCap] = reinterpret_cast<float (*)[kSelCap]>(sel_smem);
+  int32_t (*si)[kSelCap] = reinterpret_cast<int32_t (*)[kSelCap]>(sel_smem + 4 * kSelCap);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float *kk = sk[w];
+  int32_t *ii = si[w];
+  for (int64_t q = (int64_t)blockIdx.x * 4 + w; q < m; q += (int64_t)gridDim.x * 4) {
+    const int cnt = ent_cnt[q];
+    const uint4 *e = ent + q * cap;
+    if (cnt > cap || cnt > kSelCap) {
+      if (lane == 0) {
+        nsurv[q] = -1;
+        fb_list[atomicAdd(fb_count, 1)] = (int32_t)q;
+      }
+      continue;
+    }
+    // the query's k-th smallest upper bound: the union of the streams' k
+    // smallest bounds holds it (a short sort); with too many streams, sort
+    // every entry's bound instead
+    const int nb = kb_cnt[q];
+    const bool from_kb = nb <= kbcap;
+    const int nsrt = from_kb ? nb : cnt;
+    int np2 = 32;
+    while (np2 < nsrt) np2 <<= 1;
+    for (int i = lane; i < np2; i += 32) {
+      kk[i] = i < nsrt ? (from_kb ? kb[q * kbcap + i] : __uint_as_float(e[i].y)) : __int_as_float(0x7f800000);
+      ii[i] = i;
+    }
+    __syncwarp();
+    warp_sort(kk, ii, np2);
+    const double uk = nsrt >= k ? (double)kk[k - 1] : __longlong_as_double(0x7ff0000000000000LL);
+    __syncwarp();
+    int ns = 0;
+    for (int i0 = 0; i0 < cnt; i0 += 32) {
+      const int i = i0 + lane;
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      const bool in = i < cnt && (double)__uint_as_float((v = e[i]).x) <= uk;
+      const unsigned bm = __ballot_sync(0xffffffffu, in);
+      const int dst = ns + __popc(bm & lanemask_lt());
+      if (in && dst < kSurvCap) surv[q * kSurvCap + dst] = (int32_t)v.z;
+      ns += __popc(bm);
+    }
+    if (lane == 0) {
+      if (ns <= kSurvCap) {
+        nsurv[q] = ns;
+      } else {
+        nsurv[q] = -1;
+        fb_list[atomicAdd(fb_count, 1)] = (int32_t)q;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace tc
+}  // namespace mrpt
+
+namespace mrpt {
+namespace tc {
+// debug: compare two (m, n) s32 matrices, count mismatches; entry stats
+__global__ void k_tc_debug(const int32_t *A, const int32_t *B, int64_t count, const int32_t *ent_cnt, int64_t m,
+                           unsigned long long *out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    if (A[i] != B[i]) atomicAdd(out, 1ull);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    atomicAdd(out + 1, (unsigned long long)ent_cnt[i]);
+    atomicMax(out + 2, (unsigned long long)ent_cnt[i]);
+  }
+}
+}  // namespace tc
+}  // namespace mrpt

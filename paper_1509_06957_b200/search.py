@@ -240,7 +240,7 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
         ids, dists, counts = out
     bstride = _bstride(D)
     choice = D.scan_choice.get((k, votes))
-    bits_mode = choice == "u8gemm_bits"
+    bits_mode = choice in _BITS_ROUTES
     if chunk is None:
         per_q = 4 * (D.T + (bstride if bits_mode else cap))
         chunk = max(1, min(nq, (1 << 30) // per_q))
@@ -254,7 +254,7 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
         qb = Qd[s:e]
         if bits_mode:
             _run_bits(D, qb, e - s, int(Qd.stride(0)), leaves, votes, vdir, bits, bstride,
-                      counts[s:e], k, ids[s:e], dists[s:e], stage)
+                      counts[s:e], k, ids[s:e], dists[s:e], stage, route=choice)
             continue
         stage("route", _route_launch, D, qb, e - s, int(Qd.stride(0)), leaves)
         if choice is None and e - s >= 256:
@@ -269,19 +269,24 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
             cand = torch.empty((m0, cap), dtype=torch.int32, device=dev)
         stage("vote", _vote_list, D, leaves, e - s, votes, vdir, cand, cap, counts[s:e])
         args = (qb, e - s, int(Qd.stride(0)), cand, cap, counts[s:e], k, ids[s:e], dists[s:e])
-        variant = choice if choice not in (None, "u8gemm_bits") else "fp32"
+        variant = choice if choice is not None and choice not in _BITS_ROUTES else "fp32"
         if choice is None:  # small batch, no autotune: a forced list route still applies
             env = os.environ.get("MRPT_SCAN_ROWS")
-            if env and env != "u8gemm_bits" and env in _scan_variants(D, k):
+            if env and env not in _BITS_ROUTES and env in _scan_variants(D, k):
                 variant = env
         stage("scan_topk", _scan_launch, D, variant, args)
     return ids, dists, counts
 
 
-def _run_bits(D, qb, m, ldq, leaves, votes, vdir, bits, bstride, counts, k, ids, dists, stage=None):
-    """The bitmap route: K2 + K3 on their own stream beside K4's query
-    quantisation and tensor-core GEMM (which need only the queries); the
-    filter waits for the candidate bitmaps."""
+_BITS_ROUTES = ("u8gemm_bits", "u8tc_bits")
+
+
+def _run_bits(D, qb, m, ldq, leaves, votes, vdir, bits, bstride, counts, k, ids, dists, stage=None,
+              route="u8gemm_bits"):
+    """A bitmap route: K2 + K3 on their own stream beside K4's query
+    quantisation (and, for u8gemm_bits, the library GEMM), which need only
+    the queries; the filter waits for the candidate bitmaps.  u8tc_bits is
+    the fused tcgen05 filter (no dot-product matrix)."""
     torch = _device.torch_mod()
     if stage is None:
         def stage(name, fn, *a):
@@ -295,7 +300,8 @@ def _run_bits(D, qb, m, ldq, leaves, votes, vdir, bits, bstride, counts, k, ids,
         stage("vote", _vote_bitmap, D, leaves, m, votes, vdir, bits, bstride, counts)
         ev_vote = torch.cuda.Event()
         ev_vote.record(vs)
-    stage("scan_topk", _scan_bits, D, qb, m, ldq, bits, bstride, k, ids, dists, ev_vote)
+    scan = _scan_tc if route == "u8tc_bits" else _scan_bits
+    stage("scan_topk", scan, D, qb, m, ldq, bits, bstride, k, ids, dists, ev_vote)
     torch.cuda.current_stream().wait_event(ev_vote)  # leaves/bits are reused
 
 
@@ -334,6 +340,16 @@ def _scan_bits(D, qb, m, ldq, bits, bstride, k, ids, dists, wait=None):
                  _native.stream_ptr())
 
 
+def _scan_tc(D, qb, m, ldq, bits, bstride, k, ids, dists, wait=None):
+    ldr = D.u8_rows()[1]
+    Xs, info, ws = D.u8_tc(m)
+    _native.call("mrpt_scan_topk_u8tc_bits", _native.ptr(D.X), D.n, D.d, int(D.X.stride(0)),
+                 _native.ptr(Xs), ldr, _native.ptr(info), _native.ptr(qb), m, ldq,
+                 _native.ptr(bits), int(bstride), int(k), _native.ptr(ids), _native.ptr(dists),
+                 _native.ptr(ws), int(ws.numel()), None if wait is None else wait.cuda_event,
+                 _native.stream_ptr())
+
+
 def _scan_variants(D, k):
     """Exact filter variants available for this index (all give identical results)."""
     out = []
@@ -348,6 +364,10 @@ def _scan_variants(D, k):
             aligned = D.d % 4 == 0 and int(D.X.stride(0)) % 4 == 0 and D.X.data_ptr() % 16 == 0
             if k <= 96 and aligned:
                 out.append("u8gemm_bits")
+            # the fused tcgen05 filter: resident query block (ldq <= 896),
+            # k-th bound kept in registers (k <= 32)
+            if k <= 32 and aligned and 128 <= D.u8_rows()[1] <= 896:
+                out.append("u8tc_bits")
     elif k <= 120 and D.s8_rows() is not None:
         out.append("s8")
     if k <= 120 and D.shadow() is not None:
@@ -399,7 +419,7 @@ def _autotune(D, qb, m, ldq, leaves, votes, vdir, cap, counts, k, ids, dists):
     if env in variants:
         variants = [env]
     dev = qb.device
-    list_vars = [v for v in variants if v != "u8gemm_bits"]
+    list_vars = [v for v in variants if v not in _BITS_ROUTES]
     times = {}
 
     def timed(fn, *a):
@@ -412,12 +432,15 @@ def _autotune(D, qb, m, ldq, leaves, votes, vdir, cap, counts, k, ids, dists):
         return e0.elapsed_time(e1)
 
     tr = timed(_route_launch, D, qb, m, ldq, leaves)
-    if "u8gemm_bits" in variants:
-        # timed as it runs: route + vote beside the GEMM, then the filter
+    for route in _BITS_ROUTES:
+        if route not in variants:
+            continue
+        # timed as it runs: route + vote beside the quantisation (and GEMM),
+        # then the filter
         bstride = _bstride(D)
         bits = torch.empty((m, bstride), dtype=torch.int32, device=dev)
-        times["u8gemm_bits"] = timed(_run_bits, D, qb, m, ldq, leaves, votes, vdir, bits, bstride,
-                                     counts, k, ids, dists)
+        times[route] = timed(_run_bits, D, qb, m, ldq, leaves, votes, vdir, bits, bstride,
+                             counts, k, ids, dists, None, route)
     if list_vars:
         cand = torch.empty((m, cap), dtype=torch.int32, device=dev)
         tv = tr + timed(_vote_list, D, leaves, m, votes, vdir, cand, cap, counts)
@@ -585,9 +608,9 @@ def approximate_knn_sweep(Q, k, index, votes):
                              _native.ptr(counts), _native.stream_ptr())
         if nq:
             variant = D.scan_choice.get((k, v))
-            if variant in (None, "u8gemm_bits"):
-                avail = [x for x in _scan_variants(D, k) if x != "u8gemm_bits"]
-                variant = "u8gemm" if variant == "u8gemm_bits" else avail[0]
+            if variant is None or variant in _BITS_ROUTES:
+                avail = [x for x in _scan_variants(D, k) if x not in _BITS_ROUTES]
+                variant = "u8gemm" if variant in _BITS_ROUTES else avail[0]
             args = (Qd, nq, int(Qd.stride(0)), cand, cap, counts, k, ids, dists)
             _scan_launch(D, variant, args)
         res = (ids, dists, counts.clone())

@@ -195,7 +195,7 @@ class _DeviceIndex:
         self._u8 = None
         ldq = (self.d + 15) // 16 * 16
         mode = os.environ.get("MRPT_SCAN_ROWS", "auto")
-        if mode in ("auto", "u8", "u8gemm", "u8gemm_bits") and ldq <= 1024:
+        if mode in ("auto", "u8", "u8gemm", "u8gemm_bits", "u8tc_bits") and ldq <= 1024:
             torch = _device.torch_mod()
             dev = self.X.device
             Xq = torch.empty((self.n, ldq), dtype=torch.uint8, device=dev)
@@ -256,6 +256,22 @@ class _DeviceIndex:
         if self._u8g_ws is None or self._u8g_ws.numel() < need.value:
             self._u8g_ws = torch.empty(need.value, dtype=torch.uint8, device=Xq.device)
         return self._u8g[0], self._u8g[1], self._u8g_ws
+
+    def u8_tc(self, nq):
+        """(s8 rows, per-row records, workspace) for the fused tcgen05 filter
+        (mrpt_scan_topk_u8tc_bits): the GEMM route's rows, its own workspace
+        sized for nq queries (kept, grown on demand)."""
+        g = self.u8_gemm(1)
+        if g is None:
+            return None
+        torch = _device.torch_mod()
+        need = ctypes.c_int64(0)
+        _native.call("mrpt_scan_topk_u8tc_workspace_size", self.n, self.u8_rows()[1], int(nq),
+                     ctypes.byref(need))
+        ws = getattr(self, "_u8tc_ws", None)
+        if ws is None or ws.numel() < need.value:
+            ws = self._u8tc_ws = torch.empty(need.value, dtype=torch.uint8, device=g[0].device)
+        return g[0], g[1], ws
 
     def vote_dir(self):
         """Tile directory for the multi-tile vote (built once, on the device),

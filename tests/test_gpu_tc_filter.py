@@ -1,0 +1,74 @@
+"""The fused tcgen05 filter route (u8tc_bits: TMA-fed tcgen05.mma.kind::i8
+into TMEM, bounds applied straight out of TMEM) returns exactly the oracle's
+candidate counts, neighbour ids and float64 distances: several row tiles and
+query blocks with ragged ends, K blocks ragged against the 128-byte TMA box,
+u8 and s8 query quantisation, exact-tie masses (entry-list overflow -> exact
+fallback), k at its limit, sparse and dense candidate bitmaps."""
+
+import numpy as np
+import pytest
+
+import paper_1509_06957_b200 as mrpt
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle(index, X, Q, k, v):
+    ref = dict(matrices=[(R.col_ptr, R.row_idx, R.values) for R in index.matrices],
+               splits=index.splits, leaf_offsets=index.leaf_offsets,
+               leaf_indices=index.leaf_indices, depth=index.depth)
+    return O.approximate_knn_batch(X, Q, k, ref, v)
+
+
+def _data(kind, rng, n, d):
+    if kind == "pixels":
+        x = np.where(rng.random((n, d)) < 0.2, rng.random((n, d)), 0.0)
+    elif kind == "ints":
+        x = np.minimum(255, np.floor(rng.exponential(20.0, size=(n, d))))
+    elif kind == "clusters01":
+        c = rng.uniform(0, 0.5, size=(20, d))
+        x = np.clip(c[rng.integers(0, 20, n)] + 0.05 * rng.standard_normal((n, d)), 0, 1)
+    else:  # heavy duplicates
+        base = rng.integers(0, 3, size=(40, d)).astype(np.float64)
+        x = base[rng.integers(0, 40, n)]
+    return x.astype(np.float32)
+
+
+CASES = [
+    # kind, n, d, nq, T, depth, k, v, shift
+    ("pixels", 5000, 784, 300, 8, 5, 10, 1, 0.0),     # config-2 width: 7 K blocks (last ragged)
+    ("pixels", 5000, 200, 260, 8, 5, 10, 1, -0.05),   # s8 queries, 2 K blocks
+    ("ints", 4100, 128, 390, 10, 6, 10, 2, 0.0),      # exact u8 rows, one K block
+    ("clusters01", 3000, 256, 385, 6, 4, 32, 1, 0.0), # k at the limit, ragged query block
+    ("dups", 2000, 128, 300, 6, 5, 20, 1, 0.0),       # exact-tie masses: fallback path
+    ("ints", 700, 160, 300, 5, 3, 1, 3, 0.0),         # k = 1, v > 1, n < 3 tiles
+    ("pixels", 200, 256, 300, 3, 2, 10, 1, 0.0),      # n < one row tile
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}-n{c[1]}-d{c[2]}-k{c[6]}-v{c[7]}")
+def test_tc_route_parity(monkeypatch, rng, case):
+    kind, n, d, nq, T, depth, k, v, shift = case
+    monkeypatch.setenv("MRPT_SCAN_ROWS", "u8tc_bits")
+    X = _data(kind, rng, n + nq, d)
+    Xd, Q = X[:n], X[n:] + np.float32(shift)
+    index = mrpt.grow_trees(Xd, T, depth, seed=5)
+    ids, dists, counts = mrpt.approximate_knn_batch(Q, k, index, v)
+    assert index.device_index().scan_choice.get((k, v)) == "u8tc_bits"
+    rids, rd, rc = _oracle(index, Xd, Q, k, v)
+    assert np.array_equal(counts.astype(np.int64), rc)
+    assert np.array_equal(ids, rids)
+    assert dists.tobytes() == rd.tobytes()
+
+
+def test_tc_route_not_offered_outside_limits(rng):
+    from paper_1509_06957_b200.search import _scan_variants
+
+    X = _data("ints", rng, 3000, 64)          # ldq 64 < one 128-byte K block
+    D = mrpt.grow_trees(X, 4, 4, seed=1).device_index()
+    assert "u8tc_bits" not in _scan_variants(D, 10)
+    X = _data("ints", rng, 3000, 128)
+    D = mrpt.grow_trees(X, 4, 4, seed=1).device_index()
+    assert "u8tc_bits" in _scan_variants(D, 32)
+    assert "u8tc_bits" not in _scan_variants(D, 33)   # k-th bound in registers: k <= 32
