@@ -145,7 +145,8 @@ class _FakeIndex:
         self._u8, self._h = u8, fp16
 
     def u8_rows(self):
-        return object() if self._u8 else None
+        # (rows, row stride, ...): the stride is the shadow width round_up(d, 16)
+        return (None, (self.d + 15) // 16 * 16) if self._u8 else None
 
     def shadow(self):
         return object() if self._h else None
@@ -155,7 +156,10 @@ class _FakeIndex:
 
 
 @pytest.mark.parametrize("n,d,k,u8,want", [
-    (60_000, 784, 10, True, ["u8", "u8gemm", "u8gemm_bits", "fp32"]),
+    (60_000, 784, 10, True, ["u8", "u8gemm", "u8gemm_bits", "u8tc_bits", "fp32"]),
+    (60_000, 784, 33, True, ["u8", "u8gemm", "u8gemm_bits", "fp32"]),  # tcgen05 filter: k <= 32
+    (60_000, 1000, 10, True, ["u8", "u8gemm", "u8gemm_bits", "fp32"]),  # tcgen05 filter: ldq <= 896
+    (60_000, 100, 10, True, ["u8", "u8gemm", "u8gemm_bits", "fp32"]),   # tcgen05 filter: ldq >= 128
     (60_000, 784, 100, True, ["u8", "u8gemm", "fp32"]),          # bitmap filter: k <= 96
     (60_000, 37, 10, True, ["u8", "u8gemm", "fp32"]),            # no 16-byte rows
     (5_000_000, 128, 10, True, ["u8", "fp32"]),                   # dot-product matrix too big
