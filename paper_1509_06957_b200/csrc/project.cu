@@ -6,6 +6,8 @@
 // product is exact in float64 (24+24 < 53 mantissa bits), so one fused
 // multiply-add per term rounds exactly like the reference's separate
 // multiply and add -- the chain below is bit-identical to _cy.project.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace mrpt {
