@@ -13,6 +13,7 @@ k=10) at its highest-recall vote threshold.  Prints ONE JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
@@ -43,6 +44,16 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--sweep", action="store_true", help="also time every v of the config")
     return ap.parse_args()
+
+
+def tensor_peak_i8():
+    """int8 tensor peak for the fused filter's roofline: 2x the measured dense
+    bf16 rate (MEASURED_PEAKS.json burst), else 2x the recipe's fallback."""
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return 2.0 * float(mp["bf16_tflops"]), "2x measured bf16 dense (int8 not measured)"
+    except Exception:
+        return 2.0 * 1590.0, "2x fallback bf16 dense (B200_PROFILING.md)"
 
 
 def hbm_peak():
@@ -266,6 +277,7 @@ def run_ours(args):
 
     lib = native.load()
     launches0 = int(lib.mrpt_launch_count())
+    lib.mrpt_kernel_timer(1)  # events around the fused filter launches (roofline)
     with Clocks(local) as clk:
         torch.cuda.synchronize()
         if world > 1:
@@ -288,6 +300,9 @@ def run_ours(args):
         for name, a, b in ev:
             stage_ms[name] += a.elapsed_time(b)
     launches = int(lib.mrpt_launch_count()) - launches0  # this library's kernels, timed steps only
+    kt_ms, kt_n = ctypes.c_double(0.0), ctypes.c_int64(0)
+    native.call("mrpt_kernel_timer_read", ctypes.byref(kt_ms), ctypes.byref(kt_n))
+    lib.mrpt_kernel_timer(0)
     stage_launches = {name: sum(1 for ev in evs for (nm, _, _) in ev if nm == name) for name in stage_ms}
     if world > 1:
         t = torch.tensor([elapsed_ms], device="cuda")
@@ -341,8 +356,15 @@ def run_ours(args):
     # bytes the chosen filter variant actually reads per candidate (its row
     # format + per-row side data + the candidate id); survivors reranked in fp32
     # are not included
-    variant = D.scan_choice.get((k, v), "fp32")
-    if variant.startswith("u8gemm"):
+    from paper_1509_06957_b200.search import _size_class
+
+    variant = (D.scan_pin.get((k, v)) or D.scan_choice_by_size.get((k, v, _size_class(p["nq"])))
+               or D.scan_choice.get((k, v), "fp32"))
+    if variant == "u8tc_bits":
+        # fused tcgen05 filter: no dot-product matrix; per candidate its bit
+        # (read once per (query, row)) and, per row tile, 16-B row records
+        row_b, filt_mb = 0, D.n * D.u8_rows()[1] / 1e6
+    elif variant.startswith("u8gemm"):
         # per candidate: its dot product (4 B) + row record (16 B) (+ its id in
         # list mode); per query: the GEMM's n dot products written and read
         row_b, filt_mb = 16 if variant == "u8gemm_bits" else 20, D.n * D.u8_rows()[1] / 1e6
@@ -355,9 +377,43 @@ def run_ours(args):
     filter_bytes = float(cand.sum().item()) * (row_b + 4)
     if variant.startswith("u8gemm"):
         filter_bytes += 8.0 * D.n * p["nq"]
+    if variant == "u8tc_bits":
+        filter_bytes = D.n * p["nq"] / 8.0 + 16.0 * D.n * math.ceil(p["nq"] / 128)
     filter_gbs = filter_bytes / (stage_ms["scan_topk"] / steps / 1000.0) / 1e9
     stage_gbs = (vote_bytes + scan_bytes) / ((stage_ms["vote"] + stage_ms["scan_topk"]) / steps / 1000.0) / 1e9
 
+    roof = None
+    if variant == "u8tc_bits" and kt_n.value > 0:
+        # the fused filter is a tensor-core kernel: int8 ops of the (query,
+        # row) dot products it forms (2*nq*n*d per step), live CUDA-event
+        # duration of its launches; peak = 2x the measured dense bf16 rate
+        # (the nominal int8:bf16 ratio; int8 is not in MEASURED_PEAKS.json)
+        per_ms = kt_ms.value / kt_n.value
+        launches_per_step = kt_n.value / steps
+        ops = 2.0 * p["nq"] * D.n * p["d"] / launches_per_step
+        tops = ops / (per_ms / 1000.0) / 1e12
+        tpeak, tkind = tensor_peak_i8()
+        ttraffic = None
+        if os.path.exists(tpath):
+            try:
+                ttraffic = json.load(open(tpath)).get("k_tc_filter")
+            except Exception:
+                ttraffic = None
+        roof = {"bound": "tensor", "kernel": "k_tc_filter (fused tcgen05 int8 filter)",
+                "achieved": tops, "peak": tpeak, "peak_kind": tkind, "unit": "TOP/s",
+                "frac": tops / tpeak, "traffic": ttraffic,
+                "kernel_ms_per_launch": per_ms, "kernel_launches_per_step": launches_per_step,
+                "hbm_algorithmic": {"kernel": dominant, "achieved_gbs": achieved, "peak": peak,
+                                    "frac": achieved / peak,
+                                    "note": "SURVEY 8(d) algorithmic bytes (4*d B per candidate row) "
+                                            "over the scan stage; the fused filter never reads "
+                                            "float32 rows"},
+                "stage_vote_plus_scan_gbs": stage_gbs, "stage_frac": stage_gbs / peak,
+                "bytes_per_query": (vote_bytes + scan_bytes) / p["nq"], "scan_variant": variant,
+                "scan_filter_bytes_per_query": filter_bytes / p["nq"],
+                "note": ("ops = 2*nq*n*d int8 multiply-adds of the dot products the kernel forms "
+                         "(tcgen05.mma.kind::i8, K padded to 128-B blocks not counted); traffic "
+                         "= ncu DRAM bytes per launch (profiles/traffic_*.json)")}
     line = {
         "metric": "queries/sec (approximate k-NN, batched queries)",
         "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
@@ -374,7 +430,7 @@ def run_ours(args):
         "recall_queries": n_gt,
         "mean_candidates": float(cand.mean().item()),
         "build_s": build_s,
-        "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
+        "roofline": roof if roof is not None else {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic,
                      "stage_vote_plus_scan_gbs": stage_gbs,

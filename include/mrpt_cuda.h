@@ -320,6 +320,14 @@ int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d, int64_t l
                                  int64_t *ids, double *dists, void *workspace,
                                  int64_t ws_bytes, void *wait_event, void *stream);
 
+/* Measurement support (not part of the reference interface): when enabled,
+ * the fused filter launch of mrpt_scan_topk_u8tc_bits is bracketed by CUDA
+ * events on its stream; _read synchronises them and returns the summed
+ * milliseconds and the number of bracketed launches.  Enabling (or
+ * disabling) clears the record. */
+int32_t mrpt_kernel_timer(int32_t enable);
+int32_t mrpt_kernel_timer_read(double *ms, int64_t *launches);
+
 /* Sorted de-duplication of arbitrary candidate ids (np.unique,
  * search.py:157) through an n-bit bitmap.  ids outside [0, n) set
  * *bad (device int32) to 1 (IntegrityError, search.py:158-162).

@@ -63,6 +63,8 @@ SIGNATURES = {
     "mrpt_scan_topk_u8tc_workspace_size": [_c_i64, _c_i64, _c_i64, ctypes.POINTER(_c_i64)],
     "mrpt_scan_topk_u8tc_bits": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_i64,
                                  _c_i64, _c_p, _c_i64, _c_i32, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_p],
+    "mrpt_kernel_timer": [_c_i32],
+    "mrpt_kernel_timer_read": [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_c_i64)],
     "mrpt_unique_ids": [_c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p],
     "mrpt_fnv1a64_workspace_size": [_c_i64, ctypes.POINTER(_c_sz)],
     "mrpt_fnv1a64": [_c_p, _c_i64, _c_p, _c_p, _c_sz, _c_p],

@@ -3,6 +3,10 @@
 
 #include <atomic>
 
+#include <mutex>
+#include <utility>
+#include <vector>
+
 #include "common.cuh"
 
 namespace mrpt {
@@ -67,6 +71,58 @@ extern "C" const char *mrpt_last_error(void) { return g_err; }
 extern "C" int32_t mrpt_abi_version(void) { return 101; }
 
 extern "C" int64_t mrpt_launch_count(void) { return mrpt::g_launches.load(std::memory_order_relaxed); }
+
+// ---- event timer around the dominant kernel (bench roofline evidence) ----
+namespace mrpt {
+static std::mutex g_kt_mu;
+static bool g_kt_on = false;
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_kt;
+
+void ktimer_begin(cudaStream_t s, cudaEvent_t *e0) {
+  *e0 = nullptr;
+  std::lock_guard<std::mutex> lock(g_kt_mu);
+  if (!g_kt_on) return;
+  if (cudaEventCreate(e0) != cudaSuccess) {
+    *e0 = nullptr;
+    return;
+  }
+  cudaEventRecord(*e0, s);
+}
+
+void ktimer_end(cudaStream_t s, cudaEvent_t e0) {
+  if (!e0) return;
+  cudaEvent_t e1;
+  if (cudaEventCreate(&e1) != cudaSuccess) return;
+  cudaEventRecord(e1, s);
+  std::lock_guard<std::mutex> lock(g_kt_mu);
+  g_kt.emplace_back(e0, e1);
+}
+}  // namespace mrpt
+
+extern "C" int32_t mrpt_kernel_timer(int32_t enable) {
+  std::lock_guard<std::mutex> lock(mrpt::g_kt_mu);
+  mrpt::g_kt_on = enable != 0;
+  for (auto &p : mrpt::g_kt) {
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+  mrpt::g_kt.clear();
+  return MRPT_OK;
+}
+
+extern "C" int32_t mrpt_kernel_timer_read(double *ms, int64_t *launches) {
+  std::lock_guard<std::mutex> lock(mrpt::g_kt_mu);
+  double tot = 0.0;
+  for (auto &p : mrpt::g_kt) {
+    float x = 0.f;
+    if (cudaEventSynchronize(p.second) != cudaSuccess || cudaEventElapsedTime(&x, p.first, p.second) != cudaSuccess)
+      return mrpt::fail(MRPT_ECUDA, "mrpt_kernel_timer_read: event");
+    tot += x;
+  }
+  if (ms) *ms = tot;
+  if (launches) *launches = (int64_t)mrpt::g_kt.size();
+  return MRPT_OK;
+}
 
 extern "C" int32_t mrpt_check_finite(const float *X, int64_t count, int32_t *bad, void *stream) {
   clear_error();

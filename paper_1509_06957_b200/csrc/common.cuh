@@ -22,6 +22,12 @@ inline int32_t fail(int32_t code, const char *what) {
 // gpu_launches evidence, read through mrpt_launch_count().
 void count_launch();
 
+// Optional CUDA-event bracket around the dominant kernel of a call (the
+// fused tcgen05 filter), read by mrpt_kernel_timer_read: the bench's live
+// per-launch duration for the roofline.  No-ops unless mrpt_kernel_timer(1).
+void ktimer_begin(cudaStream_t s, cudaEvent_t *e0);
+void ktimer_end(cudaStream_t s, cudaEvent_t e0);
+
 // Report the launch status of the kernels just enqueued.
 inline int32_t launch_status(const char *where) {
   cudaError_t e = cudaGetLastError();

@@ -2593,21 +2593,20 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
     (count_launch(), tc::k_tc_rows<<<(unsigned)(g < 4096 ? g : 4096), 256, 0, s>>>(
                          reinterpret_cast<const uint4 *>(info), n, rinfo));
   }
-  const char *cge = getenv("MRPT_TC_CG");
-  const int cg = cge ? atoi(cge) : 4;
-  void (*fk)(const CUtensorMap, const CUtensorMap, tc::TcArgs);
-  int fthreads;
-  if (cg >= 4) {
-    fk = k <= 16 ? tc::k_tc_filter<16, 4> : tc::k_tc_filter<32, 4>;
-    fthreads = tc::threads_for<4>();
-  } else if (cg == 2) {
-    fk = k <= 16 ? tc::k_tc_filter<16, 2> : tc::k_tc_filter<32, 2>;
-    fthreads = tc::threads_for<2>();
-  } else {
-    fk = k <= 16 ? tc::k_tc_filter<16, 1> : tc::k_tc_filter<32, 1>;
-    fthreads = tc::threads_for<1>();
-  }
-  cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
+  // kernel variant per chunk (below): CG column-group warps per query
+  typedef void (*tc_fn)(const CUtensorMap, const CUtensorMap, tc::TcArgs);
+  auto pick_tc = [&](int cg, int *threads) -> tc_fn {
+    if (cg >= 4) {
+      *threads = tc::threads_for<4>();
+      return k <= 16 ? tc::k_tc_filter<16, 4> : tc::k_tc_filter<32, 4>;
+    }
+    if (cg == 2) {
+      *threads = tc::threads_for<2>();
+      return k <= 16 ? tc::k_tc_filter<16, 2> : tc::k_tc_filter<32, 2>;
+    }
+    *threads = tc::threads_for<1>();
+    return k <= 16 ? tc::k_tc_filter<16, 1> : tc::k_tc_filter<32, 1>;
+  };
   const int sel_smem = 8 * 4 * tc::kSelCap;
   cudaFuncSetAttribute(tc::k_tc_select, cudaFuncAttributeMaxDynamicSharedMemorySize, sel_smem);
   const int buf = (k + kScanNT <= 1024) ? 1024 : 2048;
@@ -2646,8 +2645,20 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
     ta.kb_cnt = ent_cnt + 2 * mc;
     ta.kb = reinterpret_cast<float *>(ent_cnt + 3 * mc);
     ta.kbcap = kTcKb;
+    // Every (CTA, column group) that touches a query is a "stream" with its
+    // own k-th bound warm-up (>= k admissions each): few query blocks per
+    // CTA (small chunks) means many streams per query.  Fewer column groups
+    // there, and at most 8 CTAs per query block.
     const int64_t items = (int64_t)ta.nqb * ntiles;
-    const int grid = (int)(items < num_sms() ? items : num_sms());
+    int grid = (int)(items < num_sms() ? items : num_sms());
+    auto cpq = [&](int g) { return (int)ceil_div<int64_t>((int64_t)ntiles * g, items) + 1; };
+    int cg = cpq(grid) <= 3 ? 4 : (cpq(grid) <= 6 ? 2 : 1);
+    if (cg == 1)
+      while (grid > 1 && cpq(grid) > 8) --grid;
+    if (const char *cge = getenv("MRPT_TC_CG")) cg = atoi(cge);
+    int fthreads = 0;
+    const tc_fn fk = pick_tc(cg, &fthreads);
+    cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
     ta.dbgD = nullptr;
     ta.noepi = getenv("MRPT_TC_NOEPI") ? atoi(getenv("MRPT_TC_NOEPI")) : 0;
     const bool dbg = getenv("MRPT_TC_DEBUG") != nullptr;
@@ -2657,7 +2668,10 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
       cudaMalloc(&D2, (size_t)m * ((n + 15) & ~15) * 4 + 64);
       ta.dbgD = D1;
     }
+    cudaEvent_t kt0;
+    ktimer_begin(s, &kt0);
     (count_launch(), fk<<<grid, fthreads, tc::kSmemBytes, s>>>(tmA, tmB, ta));
+    ktimer_end(s, kt0);
     if (dbg) {
       const int64_t ldD = (n + 15) & ~(int64_t)15;
       int32_t st = igemm_rows_tn(reinterpret_cast<const int8_t *>(Xs), ldD, qop, m, ldq, D2, ldD, s);

@@ -550,7 +550,7 @@ __global__ void k_tc_rows(const uint4 *__restrict__ info, int64_t n, uint4 *__re
 
 // Per query (one warp): k-th smallest U over the entries, survivors L <= U_k
 // to k_rerank's lists; list overflow or too many survivors -> exact fallback.
-constexpr int kSelCap = 1024;
+constexpr int kSelCap = 2048;
 __global__ void __launch_bounds__(128) k_tc_select(const uint4 *__restrict__ ent, const int32_t *__restrict__ ent_cnt,
                                                    const float *__restrict__ kb, const int32_t *__restrict__ kb_cnt,
                                                    int kbcap, int cap, int64_t m, int k, int32_t *surv, int32_t *nsurv,

@@ -239,7 +239,7 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
     else:
         ids, dists, counts = out
     bstride = _bstride(D)
-    choice = D.scan_choice.get((k, votes))
+    choice = D.scan_pin.get((k, votes)) or D.scan_choice_by_size.get((k, votes, _size_class(int(Qd.shape[0]))))
     bits_mode = choice in _BITS_ROUTES
     if chunk is None:
         per_q = 4 * (D.T + (bstride if bits_mode else cap))
@@ -449,7 +449,18 @@ def _autotune(D, qb, m, ldq, leaves, votes, vdir, cap, counts, k, ids, dists):
             times[v] = tv + timed(_scan_launch, D, v, args)
     best = min(times, key=times.get)
     D.scan_choice[(k, votes)] = best
+    D.scan_choice_by_size[(k, votes, _size_class(m))] = best
     return best
+
+
+def _size_class(m):
+    """Batch-size class of the per-index route autotune: the routes' relative
+    speed depends on how many queries share one launch (the fused tcgen05
+    filter needs many query blocks per CTA)."""
+    c = 0
+    while c < 3 and m >= (2048 << c):
+        c += 1
+    return c
 
 
 def approximate_knn_batch(Q, k, index, votes, chunk=None):
@@ -500,14 +511,15 @@ _PIPE_MIN = 2048  # queries per pipelined piece (at least)
 
 def _pipe_bounds(nq, mode=""):
     """Piece boundaries of a pipelined host batch: a small first piece (its
-    upload is the only one not hidden under compute), then up to 3 larger
-    ones (fewer, fuller filter launches).  mode "equal": up to 4 equal pieces."""
+    upload is the only one not hidden under compute), then a larger
+    one (MRPT_PIPE_REST pieces, default 1: the fused filter wants full
+    launches).  mode "equal": up to 4 equal pieces."""
     if mode == "equal":
         pieces = max(1, min(4, nq // _PIPE_MIN))
         return [nq * i // pieces for i in range(pieces + 1)]
     first = min(nq, max(256, nq // 8))
     rest = nq - first
-    pieces = max(1, min(3, rest // _PIPE_MIN))
+    pieces = max(1, min(int(os.environ.get("MRPT_PIPE_REST", "1")), rest // _PIPE_MIN))
     return [0] + [first + rest * i // pieces for i in range(pieces + 1)]
 
 

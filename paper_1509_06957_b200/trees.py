@@ -154,6 +154,8 @@ class _DeviceIndex:
         self.max_count = max_count
         self.max_leaf = max_leaf
         self.scan_choice = {}  # (k, votes) -> exact route chosen by the autotune
+        self.scan_choice_by_size = {}  # (k, votes, batch-size class) -> route
+        self.scan_pin = {}  # (k, votes) -> route forced for every batch size (pin_route)
 
     def cap(self, votes):
         """Upper bound on any candidate set at this vote threshold."""
@@ -256,6 +258,15 @@ class _DeviceIndex:
         if self._u8g_ws is None or self._u8g_ws.numel() < need.value:
             self._u8g_ws = torch.empty(need.value, dtype=torch.uint8, device=Xq.device)
         return self._u8g[0], self._u8g[1], self._u8g_ws
+
+    def pin_route(self, k, votes, route):
+        """Force the exact K4 route for (k, votes) at every batch size (tools,
+        tests); None unpins (the autotune decides again)."""
+        if route is None:
+            self.scan_pin.pop((k, votes), None)
+        else:
+            self.scan_pin[(k, votes)] = route
+            self.scan_choice[(k, votes)] = route
 
     def u8_tc(self, nq):
         """(s8 rows, per-row records, workspace) for the fused tcgen05 filter

@@ -91,7 +91,7 @@ def test_u8gemm_small_workspace_chunks(rng, kind, signed):
     index = mrpt.grow_trees(Xd, 5, 5, seed=7)
     D = index.device_index()
     Qd = torch.from_numpy(np.ascontiguousarray(Q)).cuda()
-    D.scan_choice[(k, 1)] = "u8"
+    D.pin_route(k, 1, "u8")
     want = [t.cpu().numpy() for t in query_device(D, Qd, k, 1)]
     ldq = D.u8_rows()[1]
     Xs, info, _ = D.u8_gemm(nq)

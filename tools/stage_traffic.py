@@ -45,7 +45,8 @@ for l in last:
     elif "k_vote" in l["name"]:
         stages["vote"].append(l)
         seen_vote = True
-    elif seen_vote and ("mrpt::" in l["name"] or "cutlass" in l["name"] or "gemm" in l["name"]):
+    elif seen_vote and ("mrpt::" in l["name"] or "tc::" in l["name"] or "cutlass" in l["name"]
+                        or "gemm" in l["name"]):
         stages["scan_topk"].append(l)  # (torch kernels of the calling tool are not the path)
 out = {"source": src, "unit": "DRAM bytes (read + write) per stage call of the last query pass",
        "kernels": {}}
@@ -53,5 +54,8 @@ for st, ls in stages.items():
     out[st] = sum(l.get("dram__bytes_read.sum", 0) + l.get("dram__bytes_write.sum", 0) for l in ls)
     out["kernels"][st] = [[l["name"][:70], l.get("dram__bytes_read.sum", 0) + l.get("dram__bytes_write.sum", 0),
                            l.get("gpu__time_duration.sum", 0)] for l in ls]
+tcf = [l for l in stages["scan_topk"] if "k_tc_filter" in l["name"]]
+if tcf:  # the fused filter kernel alone (bench roofline.traffic of the tc route)
+    out["k_tc_filter"] = sum(l.get("dram__bytes_read.sum", 0) + l.get("dram__bytes_write.sum", 0) for l in tcf)
 json.dump(out, open(dst, "w"), indent=1)
 print(json.dumps({k: v for k, v in out.items() if k != "kernels"}, indent=1))

@@ -32,7 +32,7 @@ def main():
             search.query_device(D, Qd, k, v)
             torch.cuda.synchronize()
             del os.environ["MRPT_TC_DEBUG"]
-        D.scan_choice[(k, v)] = route
+        D.pin_route(k, v, route)
         out = search.query_device(D, Qd, k, v)
         torch.cuda.synchronize()
         ts = []
