@@ -132,7 +132,32 @@ k_query_route(const float *__restrict__ Q, int64_t nq, int d, int64_t ldq,
     double acc[QB];
 #pragma unroll
     for (int qi = 0; qi < QB; ++qi) acc[qi] = 0.0;
-    for (int64_t s = s0; s < s1; ++s) {
+    // CSC entries 8 at a time: their loads are independent of the FMA chain,
+    // so all 8 (and the query loads they index) are in flight together
+    int64_t s = s0;
+    for (; s + 8 <= s1; s += 8) {
+      int r[8];
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        r[u] = __ldg(rows + s + u);
+        v[u] = __ldg(vals + s + u);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+#pragma unroll
+        for (int qi = 0; qi < QB; ++qi) {
+          float x;
+          if (SMEM) {
+            x = qs[qi * stride + r[u]];
+          } else {
+            x = (q0 + qi < nq) ? __ldg(Q + (q0 + qi) * ldq + r[u]) : 0.0f;
+          }
+          acc[qi] = __fma_rn((double)x, (double)v[u], acc[qi]);
+        }
+      }
+    }
+    for (; s < s1; ++s) {
       const int r = __ldg(rows + s);
       const double v = (double)__ldg(vals + s);
 #pragma unroll

@@ -15,6 +15,7 @@
 // np.lexsort((S, d2)) does.
 #include <cuda_fp16.h>
 #include <stdlib.h>
+#include <vector>
 
 #include "common.cuh"
 #include <cudaTypedefs.h>
@@ -2509,6 +2510,8 @@ static int64_t u8tc_bytes(int64_t n, int64_t ldq, int64_t mc, int64_t *off) {
   o = al(o + mc * (int64_t)sizeof(QParams));
   off[2] = o;  // rinfo (n x 16 B)
   o = al(o + n * 16);
+  off[6] = o;  // row t1 terms (n floats, 16-B padded)
+  o = al(o + n * 4 + 16);
   off[3] = o;  // entries (mc x cap x 16 B)
   o = al(o + mc * kTcCap * 16);
   off[4] = o;  // entry counts (mc), shared k-th bounds (mc), bound counts (mc), bounds (mc x kTcKb)
@@ -2524,7 +2527,7 @@ extern "C" int32_t mrpt_scan_topk_u8tc_workspace_size(int64_t n, int64_t ldq, in
   if (n < 1 || ldq < 16 || nq < 0 || !bytes) return fail(MRPT_ESHAPE, "mrpt_scan_topk_u8tc_workspace_size");
   int64_t mc = nq < kTcChunk ? nq : kTcChunk;
   if (mc < 1) mc = 1;
-  int64_t off[6];
+  int64_t off[7];
   *bytes = u8tc_bytes(n, ldq, mc, off);
   return MRPT_OK;
 }
@@ -2573,7 +2576,7 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
   if (nq == 0) return MRPT_OK;
   if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255u))
     return fail(MRPT_EWORKSPACE, "mrpt_scan_topk_u8tc_bits: workspace must be 256-byte aligned");
-  int64_t off[6];
+  int64_t off[7];
   int64_t mc = nq < kTcChunk ? nq : kTcChunk;
   while (mc > 0 && u8tc_bytes(n, ldq, mc, off) > ws_bytes) mc = mc > 128 ? mc - 128 : mc - 1;
   if (mc < 1) return fail(MRPT_EWORKSPACE, "mrpt_scan_topk_u8tc_bits: workspace too small for one query");
@@ -2582,6 +2585,7 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
   int8_t *qop = reinterpret_cast<int8_t *>(w + off[0]);
   QParams *qp = reinterpret_cast<QParams *>(w + off[1]);
   uint4 *rinfo = reinterpret_cast<uint4 *>(w + off[2]);
+  float *rt1 = reinterpret_cast<float *>(w + off[6]);
   uint4 *ent = reinterpret_cast<uint4 *>(w + off[3]);
   int32_t *ent_cnt = reinterpret_cast<int32_t *>(w + off[4]);
   int32_t *fb = reinterpret_cast<int32_t *>(w + off[5]);
@@ -2591,7 +2595,7 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
   {
     const int64_t g = ceil_div<int64_t>(n, 256);
     (count_launch(), tc::k_tc_rows<<<(unsigned)(g < 4096 ? g : 4096), 256, 0, s>>>(
-                         reinterpret_cast<const uint4 *>(info), n, rinfo));
+                         reinterpret_cast<const uint4 *>(info), n, rinfo, rt1));
   }
   // kernel variant per chunk (below): CG column-group warps per query
   typedef void (*tc_fn)(const CUtensorMap, const CUtensorMap, tc::TcArgs);
@@ -2635,6 +2639,7 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
     ta.k = k;
     ta.ldq = (int)ldq;
     ta.rinfo = rinfo;
+    ta.rt1 = rt1;
     ta.qp = qp;
     ta.cbits = cbits + q0 * bstride;
     ta.bstride = bstride;
@@ -2717,8 +2722,17 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
     if (getenv("MRPT_TC_DEBUG")) {
       int32_t fbc = 0;
       cudaMemcpyAsync(&fbc, fb, 4, cudaMemcpyDeviceToHost, s);
+      std::vector<int32_t> hs((size_t)m), he((size_t)m);
+      cudaMemcpyAsync(hs.data(), a.nsurv, (size_t)m * 4, cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(he.data(), ent_cnt, (size_t)m * 4, cudaMemcpyDeviceToHost, s);
       cudaStreamSynchronize(s);
-      fprintf(stderr, "[tc debug] fallback queries %d of %lld\n", fbc, (long long)m);
+      long long ss = 0, se = 0;
+      for (int64_t i = 0; i < m; ++i) {
+        ss += hs[i] > 0 ? hs[i] : 0;
+        se += he[i];
+      }
+      fprintf(stderr, "[tc debug] cg=%d grid=%d fallback queries %d of %lld, mean entry slots %.1f, mean survivors %.1f\n",
+              cg, grid, fbc, (long long)m, (double)se / m, (double)ss / m);
     }
     a.qlist = fb + 1;
     a.qcount = fb;

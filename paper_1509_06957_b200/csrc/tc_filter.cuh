@@ -42,7 +42,8 @@ constexpr int kM = 128;         // queries per block = TMEM lanes
 constexpr int kN = 256;         // rows per tile = TMEM columns per accumulator
 constexpr int kKB = 128;        // K bytes per block (one 128-B swizzle row)
 constexpr int kMaxKB = 7;       // resident query block: ldq <= 896
-constexpr int kStages = 3;      // row-tile ring
+constexpr int kStages = 2;      // row-tile ring (the epilogue, not the MMA feed, bounds the kernel)
+constexpr int kTopMax = 32;     // k <= 32: a query's k smallest upper bounds in shared memory
 // epilogue: 4 lane quarters x CG column groups (template); + TMA + MMA warps
 template <int CG>
 constexpr int threads_for() {
@@ -50,7 +51,7 @@ constexpr int threads_for() {
 }
 constexpr uint32_t kABytes = kM * kKB;    // 16 KB per K block
 constexpr uint32_t kBBytes = kN * kKB;    // 32 KB per stage
-constexpr uint32_t kInfoBytes = kN * 16;  // 4 KB of row records per tile
+constexpr uint32_t kInfoBytes = kN * 20;  // per tile: 256 x 16-B pre-test records + 256 x t1 (5 KB)
 
 // shared-memory carve-up (offsets from a 1024-B aligned base)
 constexpr uint32_t kOffA = 0;
@@ -61,7 +62,13 @@ constexpr uint32_t kOffBar = kOffInfo + 2 * kInfoBytes;
 constexpr int kNumBars = 2 * kStages + 2 + 6;
 constexpr uint32_t kOffTmemSlot = kOffBar + 8 * kNumBars;
 constexpr uint32_t kOffSu = kOffTmemSlot + 16;
-constexpr uint32_t kSmemBytes = kOffSu + 4 * kM + 1024;  // + alignment slack
+// per query of the block: the k smallest upper bounds its column-group warps
+// have found (unsorted, -inf fillers past k), their max and its slot, a lock
+constexpr uint32_t kOffTop = kOffSu + 4 * kM;
+constexpr uint32_t kOffTopMax = kOffTop + 4 * kM * kTopMax;
+constexpr uint32_t kOffTopIdx = kOffTopMax + 4 * kM;
+constexpr uint32_t kOffLock = kOffTopIdx + 4 * kM;
+constexpr uint32_t kSmemBytes = kOffLock + 4 * kM + 1024;  // + alignment slack
 
 struct TcArgs {
   int64_t n;            // data rows
@@ -71,7 +78,8 @@ struct TcArgs {
   int kblocks;          // ceil(ldq / kKB)
   int k;                // neighbours
   int ldq;              // shadow row bytes (the unsigned-query offset term)
-  const uint4 *rinfo;   // per row {t1 = sx^2 * nrm (f32), 2 sx (f32), radius (f32), 128 * sum(u8) (s32)}
+  const uint4 *rinfo;   // per row {P (f32), 2 sx (f32), radius (f32), 128 * sum(u8) (s32)}, see k_tc_rows
+  const float *rt1;     // per row t1 = sx^2 * nrm (the exact admission rule's row term)
   const QParams *qp;    // per query of the chunk
   const uint32_t *cbits;
   int64_t bstride;
@@ -196,29 +204,58 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 // Per-query state of one epilogue thread.
 template <int KT>
 struct EpiState {
-  float topU[KT];  // the k smallest upper bounds so far (unsorted; +inf until filled, -inf fillers past k)
-  float umax;      // max of topU (the k-th smallest bound) and its slot
-  int imax;
   float su;        // sqrt(k-th smallest U) rounded up (+inf until k bounds exist)
   int base, left;  // current block of reserved entry slots: next = base + (kEntBlock - left)
 };
 
+// The query's shared k smallest upper bounds (one set per CTA and query,
+// merged over its column-group warps): replace the largest under the
+// query's lock, find the new largest.  Returns the new k-th bound.
+template <int KT>
+__device__ __forceinline__ float top_insert(float *top, float *tmax, int *tidx, int *lock, float U) {
+  while (atomicCAS(lock, 0, 1) != 0) {
+  }
+  __threadfence_block();
+  float m = *reinterpret_cast<volatile float *>(tmax);
+  if (U < m) {
+    const int ix = *reinterpret_cast<volatile int *>(tidx);
+    reinterpret_cast<volatile float *>(top)[ix] = U;
+    float mv[KT];
+    int mi[KT];
+#pragma unroll
+    for (int i = 0; i < KT; i += 4) {
+      asm volatile("ld.volatile.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(mv[i]), "=f"(mv[i + 1]), "=f"(mv[i + 2]), "=f"(mv[i + 3])
+                   : "r"(smem_u32(top + i)));
+      mi[i] = i, mi[i + 1] = i + 1, mi[i + 2] = i + 2, mi[i + 3] = i + 3;
+    }
+#pragma unroll
+    for (int w = KT / 2; w >= 1; w >>= 1) {
+#pragma unroll
+      for (int i = 0; i < w; ++i) {
+        const bool gt = mv[i + w] > mv[i];
+        mv[i] = gt ? mv[i + w] : mv[i];
+        mi[i] = gt ? mi[i + w] : mi[i];
+      }
+    }
+    m = mv[0];
+    *reinterpret_cast<volatile float *>(tmax) = m;
+    *reinterpret_cast<volatile int *>(tidx) = mi[0];
+  }
+  __threadfence_block();
+  atomicExch(lock, 0);
+  return m;
+}
+
 constexpr int kEntBlock = 32;  // entry slots a thread reserves at a time (one atomic per block)
 
-// End of a stream (one thread's share of a query): publish its k smallest
-// upper bounds and mark the unused tail of its reserved block (L = NaN: never
-// a survivor).
+// End of a thread's share of a query: mark the unused tail of its reserved
+// block (A = NaN: never a survivor).
 template <int KT>
 __device__ __forceinline__ void tc_flush(EpiState<KT> &st, int64_t q, const TcArgs &a) {
-  if (st.umax < __int_as_float(0x7f800000) || st.left < kEntBlock || st.base > 0) {
-    const int o = atomicAdd(a.kb_cnt + q, a.k);
-#pragma unroll
-    for (int i = 0; i < KT; ++i)
-      if (i < a.k && o + i < a.kbcap) a.kb[q * a.kbcap + o + i] = st.topU[i];
-  }
   for (; st.left > 0; --st.left) {
     const int slot = st.base + (kEntBlock - st.left);
-    if (slot < a.cap) a.ent[q * a.cap + slot] = make_uint4(0x7fc00000u, 0x7f800000u, 0u, 0u);
+    if (slot < a.cap) a.ent[q * a.cap + slot] = make_uint4(0x7fc00000u, 0u, 0u, 0u);  // A = NaN: no entry
   }
 }
 
@@ -232,42 +269,26 @@ __device__ __forceinline__ void dist_bounds_f(float A, float r, float eta, float
   U = __fmul_ru(shi, shi);
 }
 
+// An admitted candidate: its raw (A, r, eta) go to the entry list (k_tc_select
+// turns them into bounds); only a candidate that can enter the k smallest
+// upper bounds (U >= A, so A < umax is necessary) pays for its bound here.
 template <int KT>
 __device__ __forceinline__ void tc_admit(EpiState<KT> &st, float A, float r, float eta, int32_t col, int64_t q,
-                                      const TcArgs &a, unsigned *su_slot) {
-  float Lf, Uf;
-  dist_bounds_f(A, r, eta, Lf, Uf);
+                                      const TcArgs &a, unsigned *su_slot, float *top, float *tmax, int *tidx,
+                                      int *lock) {
   if (st.left == 0) {
     st.base = atomicAdd(a.ent_cnt + q, kEntBlock);
     st.left = kEntBlock;
   }
   const int slot = st.base + (kEntBlock - st.left--);
   if (slot < a.cap)
-    a.ent[q * a.cap + slot] = make_uint4(__float_as_uint(Lf), __float_as_uint(Uf), (uint32_t)col, 0u);
-  if (Uf < st.umax) {
-    // replace the largest of the k bounds, then find the new largest (a
-    // depth-log2(KT) tree instead of a KT-deep insertion chain)
-#pragma unroll
-    for (int i = 0; i < KT; ++i) st.topU[i] = i == st.imax ? Uf : st.topU[i];
-    float mv[KT];
-    int mi[KT];
-#pragma unroll
-    for (int i = 0; i < KT; ++i) {
-      mv[i] = st.topU[i];
-      mi[i] = i;
-    }
-#pragma unroll
-    for (int w = KT / 2; w >= 1; w >>= 1) {
-#pragma unroll
-      for (int i = 0; i < w; ++i) {
-        const bool gt = mv[i + w] > mv[i];
-        mv[i] = gt ? mv[i + w] : mv[i];
-        mi[i] = gt ? mi[i + w] : mi[i];
-      }
-    }
-    st.umax = mv[0];
-    st.imax = mi[0];
-    const float uk = st.umax;
+    a.ent[q * a.cap + slot] =
+        make_uint4(__float_as_uint(A), __float_as_uint(r), __float_as_uint(eta), (uint32_t)col);
+  if (A >= *reinterpret_cast<volatile float *>(tmax)) return;
+  float Lf, Uf;
+  dist_bounds_f(A, r, eta, Lf, Uf);
+  if (Uf < *reinterpret_cast<volatile float *>(tmax)) {
+    const float uk = top_insert<KT>(top, tmax, tidx, lock, Uf);
     if (uk < 3.0e38f) {
       const float s = __fsqrt_ru(uk);
       if (s < st.su) {
@@ -353,8 +374,10 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
         const uint32_t li = (uint32_t)(it - it0), b = li & 1u;
         mbar_wait_sleep(epiEmpty(b), ((li >> 1) & 1u) ^ 1u);
         const int64_t rows = a.n - (int64_t)tile * kN < kN ? a.n - (int64_t)tile * kN : kN;
-        mbar_expect_tx(infoFull(b), (uint32_t)rows * 16u);
+        const uint32_t t1b = ((uint32_t)rows * 4u + 15u) & ~15u;  // (rt1 is padded to 16 B)
+        mbar_expect_tx(infoFull(b), (uint32_t)rows * 16u + t1b);
         bulk_load(sInfo + b * kInfoBytes, a.rinfo + (int64_t)tile * kN, (uint32_t)rows * 16u, infoFull(b));
+        bulk_load(sInfo + b * kInfoBytes + kN * 16, a.rt1 + (int64_t)tile * kN, t1b, infoFull(b));
       }
     }
   } else if (warp == kMmaWarp) {
@@ -394,50 +417,63 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
     const int lq = warp & 3, cg = warp >> 2;
     const int qloc = lq * 32 + lane;
     const uint32_t trow = tmem_base + ((uint32_t)(lq * 32) << 16);
-    const float4 *info4 = reinterpret_cast<const float4 *>(smem + kOffInfo);
+    const float4 *info4 = reinterpret_cast<const float4 *>(smem + kOffInfo);  // [2][kInfoBytes / 16]
+    float *top = reinterpret_cast<float *>(smem + kOffTop) + qloc * kTopMax;
+    float *tmax = reinterpret_cast<float *>(smem + kOffTopMax) + qloc;
+    int *tidx = reinterpret_cast<int *>(smem + kOffTopIdx) + qloc;
+    int *tlock = reinterpret_cast<int *>(smem + kOffLock) + qloc;
     EpiState<KT> st;
     int64_t cur_qb = -1, q = 0;
     bool valid = false;
     float sqf = 0.f, t2f = 0.f, rq = 0.f;
     int corr = 0, sel = 0;
+    // the CTA's k smallest bounds of its query go to the query's bound list
+    // (their union over CTAs holds the query's k smallest)
+    auto publish = [&]() {
+      const int o = atomicAdd(a.kb_cnt + q, a.k);
+      for (int i = 0; i < a.k; ++i)
+        if (o + i < a.kbcap) a.kb[q * a.kbcap + o + i] = top[i];
+    };
     // candidate words of item itx for this warp's columns
     constexpr int NWD = kColsPerWarp / 32;
-    auto load_words = [&](int64_t itx, uint32_t (&w)[NWD]) {
+    // (the tail mask is kept apart and applied when the words are used, a
+    // tile later, so nothing waits on the loads here)
+    auto load_words = [&](int64_t itx, uint32_t (&w)[NWD], uint32_t (&mk)[NWD]) {
       const int qbx = (int)(itx / a.ntiles), tilex = (int)(itx % a.ntiles);
       const int64_t qx = (int64_t)qbx * kM + qloc;
 #pragma unroll
       for (int c = 0; c < NWD; ++c) {
         const int64_t col0 = (int64_t)tilex * kN + cg * kColsPerWarp + c * 32;
-        uint32_t x = 0u;
-        if (qx < a.m && col0 < a.n) {
-          x = __ldg(a.cbits + qx * a.bstride + (col0 >> 5));
-          if (a.n - col0 < 32) x &= (1u << (a.n - col0)) - 1u;
-        }
-        w[c] = x;
+        const bool in = qx < a.m && col0 < a.n;
+        w[c] = in ? __ldg(a.cbits + qx * a.bstride + (col0 >> 5)) : 0u;
+        mk[c] = !in ? 0u : (a.n - col0 < 32 ? (1u << (a.n - col0)) - 1u : 0xffffffffu);
       }
     };
-    uint32_t wnext[NWD];
-    if (it0 < it1) load_words(it0, wnext);
+    uint32_t wnext[NWD], mnext[NWD];
+    if (it0 < it1) load_words(it0, wnext, mnext);
     for (int64_t it = it0; it < it1; ++it) {
       const int qb = (int)(it / a.ntiles), tile = (int)(it % a.ntiles);
       uint32_t wd[NWD];
 #pragma unroll
-      for (int c = 0; c < NWD; ++c) wd[c] = wnext[c];
-      if (it + 1 < it1) load_words(it + 1, wnext);  // in flight while this tile is filtered
+      for (int c = 0; c < NWD; ++c) wd[c] = wnext[c] & mnext[c];
+      if (it + 1 < it1) load_words(it + 1, wnext, mnext);  // in flight while this tile is filtered
       if (qb != cur_qb) {
         if (valid) tc_flush<KT>(st, q, a);
         // new query block: every epilogue warp is past the old one before
         // the shared k-th bounds are reset
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
-        if (cg == 0) su_s[qloc] = 0x7f800000u;
+        if (cg == 0) {
+          if (valid) publish();
+          su_s[qloc] = 0x7f800000u;
+          for (int i = 0; i < KT; ++i) top[i] = i < a.k ? __int_as_float(0x7f800000) : -__int_as_float(0x7f800000);
+          *tmax = __int_as_float(0x7f800000);
+          *tidx = 0;
+          *tlock = 0;
+        }
         asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
         cur_qb = qb;
         q = (int64_t)qb * kM + qloc;
         valid = q < a.m;
-#pragma unroll
-        for (int i = 0; i < KT; ++i) st.topU[i] = i < a.k ? __int_as_float(0x7f800000) : -__int_as_float(0x7f800000);
-        st.umax = __int_as_float(0x7f800000);
-        st.imax = 0;
         st.su = __int_as_float(0x7f800000);
         st.left = 0;
         st.base = 0;
@@ -478,26 +514,39 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
         }
         if (__any_sync(0xffffffffu, wc != 0u)) {
           st.su = fminf(st.su, __uint_as_float(*reinterpret_cast<volatile unsigned *>(su_s + qloc)));
-          const float4 *ri = info4 + b * kN + cofs;
+          const float4 *ri = info4 + b * (kInfoBytes / 16) + cofs;
+          const float *rt = reinterpret_cast<const float *>(info4 + b * (kInfoBytes / 16) + kN) + cofs;
           const int32_t colb = tile * kN + cofs;
-          // bound every column; the (rare after warm-up) admissions run
-          // once per set bit outside the unrolled loop
+          // Pre-test, a superset of admit2: admit2 implies
+          //   t3 + 2 S (1+2^-16) rad >= [t1 (1-k) - rad^2 (1+2^-16)] + [t2 (1-k) - S^2 (1+2^-16)]
+          // with S = su + rq, k = 2^-18 (|t3| <= T, admit2's eta <= 4.8e-7
+          // (T + |t3|), and every rounding of both forms is far inside the
+          // margins): per column one row record (P = the first bracket) and
+          // three float ops.  Columns that pass run the exact rule below
+          // (their admissions are rare after the warm-up).
+          float s2e = 0.f, nqq = 3.4028235e38f;  // no k-th bound yet: everything passes
+          if (st.su < 1.0e18f) {
+            const float S = __fadd_ru(st.su, rq);
+            s2e = __fmul_ru(2.0f * S, 1.0000153f);
+            nqq = -__fsub_rd(__fmul_rd(t2f, 0.99999619f), __fmul_ru(__fmul_ru(S, S), 1.0000153f));
+          }
           uint32_t take = 0u;
-          // superset of admit2 in plain float arithmetic: A <= (su + rad +
-          // rq)^2 * (1 + 2^-16) + 1e-6 (T + |t3|) covers every directed
-          // rounding of admit2 and its eta (<= 4.8e-7 (T + |t3|)); the exact
-          // rule runs below only for columns that pass
-          const float srq = st.su + rq;
+          if (__all_sync(0xffffffffu, sel == 1)) {  // unsigned queries (the common case)
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float4 r4 = ri[j];
-            const int mys = (int)v[j] + corr + sel * __float_as_int(r4.w);
-            const float T = r4.x + t2f;
-            const float t3 = (r4.y * sqf) * (float)mys;
-            const float A = T - t3;
-            const float sr = srq + r4.z;
-            const float G = fmaf(sr * 1.0000153f, sr, fmaf(1.0e-6f, T + fabsf(t3), 2.4e-38f));
-            take |= (A <= G ? 1u : 0u) << j;
+            for (int j = 0; j < 16; ++j) {
+              const float4 r4 = ri[j];
+              const float f = (float)((int)v[j] + __float_as_int(r4.w) + corr);
+              const float lhs = fmaf(r4.y * sqf, f, fmaf(s2e, r4.z, nqq));
+              take |= (lhs >= r4.x ? 1u : 0u) << j;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float4 r4 = ri[j];
+              const float f = (float)((int)v[j] + sel * __float_as_int(r4.w) + corr);
+              const float lhs = fmaf(r4.y * sqf, f, fmaf(s2e, r4.z, nqq));
+              take |= (lhs >= r4.x ? 1u : 0u) << j;
+            }
           }
           take &= wc;
           if (a.noepi == 2) take = 0u;  // experiment: bounds without admissions
@@ -514,12 +563,12 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
             const int dv = (j & 8) ? d2b : d2a;
             const float4 r4 = ri[j];
             const int mys = dv + corr + sel * __float_as_int(r4.w);
-            const float t1 = r4.x;
+            const float t1 = rt[j];
             const float t3 = (r4.y * sqf) * (float)mys;
             const float A = (t1 + t2f) - t3;
             const float eta = __fmul_ru(4.76837158203125e-07f, __fadd_ru(__fadd_ru(t1, t2f), fabsf(t3)));
             const float r = __fadd_ru(r4.z, rq);
-            if (admit2(A, r, eta, st.su)) tc_admit<KT>(st, A, r, eta, colb + j, q, a, su_s + qloc);
+            tc_admit<KT>(st, A, r, eta, colb + j, q, a, su_s + qloc, top, tmax, tidx, tlock);
           }
         }
       }
@@ -528,6 +577,8 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
       if (lane == 0) mbar_arrive(epiEmpty(b));
     }
     if (valid) tc_flush<KT>(st, q, a);
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+    if (cg == 0 && valid) publish();
   }
   __syncthreads();
   if (warp == kMmaWarp) {
@@ -539,17 +590,22 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
 // Row records of the fused filter, from the GEMM route's {scale, norm,
 // radius, sum}: t1 = scale^2 * norm exactly as k_scan_topk_u8 forms it,
 // 2 * scale, radius, 128 * sum (the unsigned-query offset term).
-__global__ void k_tc_rows(const uint4 *__restrict__ info, int64_t n, uint4 *__restrict__ rinfo) {
+__global__ void k_tc_rows(const uint4 *__restrict__ info, int64_t n, uint4 *__restrict__ rinfo, float *rt1) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint4 v = info[i];
     const float sx = __uint_as_float(v.x);
     const float t1 = sx * sx * (float)(int)v.y;
-    rinfo[i] = make_uint4(__float_as_uint(t1), __float_as_uint(2.0f * sx), v.z, (uint32_t)(128 * (int)v.w));
+    const float rad = __uint_as_float(v.z);
+    // pre-test row term P = t1 (1 - 2^-18) - rad^2 (1 + 2^-16), rounded down
+    const float P = __fsub_rd(__fmul_rd(t1, 0.99999619f), __fmul_ru(__fmul_ru(rad, rad), 1.0000153f));
+    rinfo[i] = make_uint4(__float_as_uint(P), __float_as_uint(2.0f * sx), v.z, (uint32_t)(128 * (int)v.w));
+    rt1[i] = t1;
   }
 }
 
-// Per query (one warp): k-th smallest U over the entries, survivors L <= U_k
-// to k_rerank's lists; list overflow or too many survivors -> exact fallback.
+// Per query (one warp): bounds of the entries' (A, r, eta), the k-th smallest
+// upper bound U_k, survivors L <= U_k to k_rerank's lists; list overflow or
+// too many survivors -> exact fallback.
 constexpr int kSelCap = 2048;
 __global__ void __launch_bounds__(128) k_tc_select(const uint4 *__restrict__ ent, const int32_t *__restrict__ ent_cnt,
                                                    const float *__restrict__ kb, const int32_t *__restrict__ kb_cnt,
@@ -580,7 +636,18 @@ __global__ void __launch_bounds__(128) k_tc_select(const uint4 *__restrict__ ent
     int np2 = 32;
     while (np2 < nsrt) np2 <<= 1;
     for (int i = lane; i < np2; i += 32) {
-      kk[i] = i < nsrt ? (from_kb ? kb[q * kbcap + i] : __uint_as_float(e[i].y)) : __int_as_float(0x7f800000);
+      float u = __int_as_float(0x7f800000);
+      if (i < nsrt) {
+        if (from_kb) {
+          u = kb[q * kbcap + i];
+        } else {
+          const uint4 v = e[i];
+          float L;
+          dist_bounds_f(__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), L, u);
+          if (u != u) u = __int_as_float(0x7f800000);  // no entry
+        }
+      }
+      kk[i] = u;
       ii[i] = i;
     }
     __syncwarp();
@@ -591,10 +658,17 @@ __global__ void __launch_bounds__(128) k_tc_select(const uint4 *__restrict__ ent
     for (int i0 = 0; i0 < cnt; i0 += 32) {
       const int i = i0 + lane;
       uint4 v = make_uint4(0u, 0u, 0u, 0u);
-      const bool in = i < cnt && (double)__uint_as_float((v = e[i]).x) <= uk;
+      bool in = false;
+      if (i < cnt) {
+        v = e[i];
+        float L, U;
+        dist_bounds_f(__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), L, U);
+        const float A = __uint_as_float(v.x);
+        in = A == A && (double)L <= uk;  // an empty slot holds A = NaN
+      }
       const unsigned bm = __ballot_sync(0xffffffffu, in);
       const int dst = ns + __popc(bm & lanemask_lt());
-      if (in && dst < kSurvCap) surv[q * kSurvCap + dst] = (int32_t)v.z;
+      if (in && dst < kSurvCap) surv[q * kSurvCap + dst] = (int32_t)v.w;
       ns += __popc(bm);
     }
     if (lane == 0) {

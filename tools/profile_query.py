@@ -39,6 +39,8 @@ print(f"BUILD config={a.config} n={X.shape[0]} T={p['n_trees']} depth={p['depth'
 if not a.build_only:
     D = index.device_index()
     Qd = torch.from_numpy(Q).cuda()
+    if os.environ.get("MRPT_PIN"):  # route pinned for every batch size (no autotune runs under ncu)
+        D.pin_route(p["k"], v, os.environ["MRPT_PIN"])
     vs = [v] if a.votes else [v]
     for _ in range(a.reps):
         ids, dists, counts = query_device(D, Qd, p["k"], v)
