@@ -212,7 +212,7 @@ def _check_batch_args(k, index, votes):
         raise ParameterError(f"vote threshold must lie in [1, {index.n_trees}], got {votes}")
 
 
-def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
+def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None, size_class=None):
     """K2 -> K3 -> K4 over a device query block; returns device tensors
     (ids (nq,k) int64, dists (nq,k) float64, candidate_count (nq,) int32).
     ``timer``: optional list receiving (stage, start_event, end_event) per launch.
@@ -239,7 +239,10 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
     else:
         ids, dists, counts = out
     bstride = _bstride(D)
-    choice = D.scan_pin.get((k, votes)) or D.scan_choice_by_size.get((k, votes, _size_class(int(Qd.shape[0]))))
+    # the route is chosen per batch-size class of this call (the caller's
+    # class when this is the rest of an autotuned batch)
+    sc = _size_class(int(Qd.shape[0])) if size_class is None else size_class
+    choice = D.scan_pin.get((k, votes)) or D.scan_choice_by_size.get((k, votes, sc))
     bits_mode = choice in _BITS_ROUTES
     if chunk is None:
         per_q = 4 * (D.T + (bstride if bits_mode else cap))
@@ -260,10 +263,11 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None):
         if choice is None and e - s >= 256:
             # the autotune's last run leaves this chunk's outputs; the rest of
             # the batch runs the chosen route (its own chunking)
-            _autotune(D, qb, e - s, int(Qd.stride(0)), leaves, votes, vdir, cap, counts[s:e], k,
+            _autotune(D, qb, e - s, int(Qd.stride(0)), leaves, votes, vdir, cap, counts[s:e], k, sc,
                       ids[s:e], dists[s:e])
             if e < nq:
-                query_device(D, Qd[e:], k, votes, out=(ids[e:], dists[e:], counts[e:]), timer=timer)
+                query_device(D, Qd[e:], k, votes, out=(ids[e:], dists[e:], counts[e:]), timer=timer,
+                             size_class=sc)
             return ids, dists, counts
         if cand is None:
             cand = torch.empty((m0, cap), dtype=torch.int32, device=dev)
@@ -408,7 +412,7 @@ def _scan_launch(D, variant, args):
                      *common_tail)
 
 
-def _autotune(D, qb, m, ldq, leaves, votes, vdir, cap, counts, k, ids, dists):
+def _autotune(D, qb, m, ldq, leaves, votes, vdir, cap, counts, k, sc, ids, dists):
     """Time every exact route for this chunk -- list vote + each list filter,
     bitmap vote + the bitmap GEMM filter -- and keep the fastest for the index
     (per k and vote threshold); the last run leaves valid outputs (all routes
@@ -449,7 +453,7 @@ def _autotune(D, qb, m, ldq, leaves, votes, vdir, cap, counts, k, ids, dists):
             times[v] = tv + timed(_scan_launch, D, v, args)
     best = min(times, key=times.get)
     D.scan_choice[(k, votes)] = best
-    D.scan_choice_by_size[(k, votes, _size_class(m))] = best
+    D.scan_choice_by_size[(k, votes, sc)] = best
     return best
 
 

@@ -1,4 +1,1 @@
-export MRPT_PIN=u8tc_bits
-for qb in 4 8; do MRPT_ROUTE_QB=$qb python tools/profile_query.py --config 2 --reps 2 --time 2>&1 | grep TIME | sed "s/^/qb=$qb /"; done
-MRPT_ROUTE_QB=0 python tools/profile_query.py --config 2 --reps 2 --time 2>&1 | grep TIME | sed "s/^/old /"
-for c in 3 4; do MRPT_ROUTE_QB=8 python tools/profile_query.py --config $c --reps 2 --time --nq 2000 2>&1 | grep TIME | sed "s/^/qb=8 /"; MRPT_ROUTE_QB=0 python tools/profile_query.py --config $c --reps 2 --time --nq 2000 2>&1 | grep TIME | sed "s/^/old /"; done
+for r in u8tc_bits u8gemm_bits u8; do MRPT_PIN=$r MRPT_TC_DEBUG=1 python tools/profile_query.py --config 3 --votes 1 --reps 1 --time 2>&1 | grep -E "TIME|tc debug\] cg" | sed "s/^/$r /"; done
