@@ -521,6 +521,11 @@ def _pipe_bounds(nq, mode=""):
     if mode == "equal":
         pieces = max(1, min(4, nq // _PIPE_MIN))
         return [nq * i // pieces for i in range(pieces + 1)]
+    if mode == "one":
+        return [0, nq]
+    if mode.startswith("first"):  # "firstN": a first piece of N queries, then the rest
+        first = min(nq, max(1, int(mode[5:])))
+        return [0, first, nq] if first < nq else [0, nq]
     first = min(nq, max(256, nq // 8))
     rest = nq - first
     pieces = max(1, min(int(os.environ.get("MRPT_PIPE_REST", "1")), rest // _PIPE_MIN))
@@ -540,6 +545,10 @@ def _knn_batch_pipelined(Qc, k, index, votes):
     nq = int(Qc.shape[0])
     Qc = Qc.to(dtype=torch.float32).contiguous()
     _record_macs(nq * sum(R.nnz for R in index.matrices))
+    route = D.scan_pin.get((k, votes)) or D.scan_choice_by_size.get((k, votes, _size_class(nq)))
+    if route in _BITS_ROUTES and not os.environ.get("MRPT_PIPE") and \
+            4 * nq * (D.T + _bstride(D)) <= (1 << 30):
+        return _knn_batch_pipelined_bits(Qc, k, index, votes, route)
     bounds = _pipe_bounds(nq, os.environ.get("MRPT_PIPE", ""))
     pieces = len(bounds) - 1
     dev = _device.device()
@@ -568,6 +577,49 @@ def _knn_batch_pipelined(Qc, k, index, votes):
             hdist[s:e].copy_(dists[s:e], non_blocking=True)
             hcnt[s:e].copy_(counts[s:e], non_blocking=True)
     down.synchronize()  # after every piece's compute and upload, too
+    return hid.numpy(), hdist.numpy(), hcnt.numpy()
+
+
+def _knn_batch_pipelined_bits(Qc, k, index, votes, route):
+    """Host batch over a bitmap route: the upload is cut into pieces and each
+    piece's route + vote (K2 + K3, bitmaps into one batch-wide buffer) runs
+    as soon as it lands, under the next piece's upload; then ONE filter
+    launch covers the whole batch (the fused filter wants full launches), and
+    the results come back in one download.  Results are identical."""
+    torch = _device.torch_mod()
+    D = index.device_index()
+    nq = int(Qc.shape[0])
+    dev = _device.device()
+    bstride = _bstride(D)
+    Qd = torch.empty((nq, index.d), dtype=torch.float32, device=dev)
+    leaves = torch.empty((nq, D.T), dtype=torch.int32, device=dev)
+    bits = torch.empty((nq, bstride), dtype=torch.int32, device=dev)
+    ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
+    dists = torch.empty((nq, k), dtype=torch.float64, device=dev)
+    counts = torch.empty(nq, dtype=torch.int32, device=dev)
+    hid = torch.empty((nq, k), dtype=torch.int64, pin_memory=True)
+    hdist = torch.empty((nq, k), dtype=torch.float64, pin_memory=True)
+    hcnt = torch.empty(nq, dtype=torch.int32, pin_memory=True)
+    compute = torch.cuda.current_stream()
+    up, _ = _device.side_streams()
+    vdir = D.vote_dir()
+    pieces = max(1, min(4, nq // _PIPE_MIN))
+    bounds = [nq * i // pieces for i in range(pieces + 1)]
+    for i in range(pieces):
+        s, e = bounds[i], bounds[i + 1]
+        with torch.cuda.stream(up):
+            Qd[s:e].copy_(Qc[s:e], non_blocking=True)
+            ev_up = torch.cuda.Event()
+            ev_up.record(up)
+        compute.wait_event(ev_up)
+        _route_launch(D, Qd[s:e], e - s, int(Qd.stride(0)), leaves[s:e])
+        _vote_bitmap(D, leaves[s:e], e - s, votes, vdir, bits[s:e], bstride, counts[s:e])
+    scan = _scan_tc if route == "u8tc_bits" else _scan_bits
+    scan(D, Qd, nq, int(Qd.stride(0)), bits, bstride, k, ids, dists)
+    hid.copy_(ids, non_blocking=True)
+    hdist.copy_(dists, non_blocking=True)
+    hcnt.copy_(counts, non_blocking=True)
+    compute.synchronize()
     return hid.numpy(), hdist.numpy(), hcnt.numpy()
 
 

@@ -72,3 +72,21 @@ def test_tc_route_not_offered_outside_limits(rng):
     D = mrpt.grow_trees(X, 4, 4, seed=1).device_index()
     assert "u8tc_bits" in _scan_variants(D, 32)
     assert "u8tc_bits" not in _scan_variants(D, 33)   # k-th bound in registers: k <= 32
+
+
+@pytest.mark.parametrize("route", ["u8tc_bits", "u8gemm_bits", "u8"])
+def test_host_batch_pipelined_paths(rng, route):
+    """Host batches >= 4096 queries take the overlapped paths: bitmap routes
+    upload in pieces, route + vote each piece as it lands and run one
+    filter over the whole batch; list routes pipeline whole pieces.  Same
+    answers as the oracle either way."""
+    n, d, nq, k, v = 3000, 136, 4500, 10, 1
+    X = _data("ints", rng, n + nq, d)
+    Xd, Q = X[:n], X[n:]
+    index = mrpt.grow_trees(Xd, 6, 5, seed=13)
+    index.device_index().pin_route(k, v, route)
+    ids, dists, counts = mrpt.approximate_knn_batch(Q, k, index, v)
+    rids, rd, rc = _oracle(index, Xd, Q, k, v)
+    assert np.array_equal(counts.astype(np.int64), rc)
+    assert np.array_equal(ids, rids)
+    assert dists.tobytes() == rd.tobytes()
