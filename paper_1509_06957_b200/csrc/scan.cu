@@ -2561,13 +2561,29 @@ static bool tc_map(CUtensorMap *m, const void *base, int64_t rows, int64_t ldq, 
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 2-D u32 tensor map of the candidate bitmaps (rows x bstride words), boxes
+// of one row tile's 8 words x 128 queries, no swizzle.
+static bool tc_map_words(CUtensorMap *m, const void *base, int64_t rows, int64_t bstride) {
+  PFN_cuTensorMapEncodeTiled_v12000 fn = tc_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)bstride, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)bstride * 4};
+  cuuint32_t box[2] = {(cuuint32_t)(tc::kN / 32), (cuuint32_t)tc::kM};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void *>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d, int64_t ldx, const void *Xs,
                                             int64_t ldq, const void *info, const float *Q, int64_t nq,
                                             int64_t ldqq, const uint32_t *cbits, int64_t bstride, int32_t k,
                                             int64_t *ids, double *dists, void *workspace, int64_t ws_bytes,
                                             void *wait_event, void *stream) {
   clear_error();
-  if (!cbits || bstride < (n + 31) / 32) return fail(MRPT_EPARAM, "mrpt_scan_topk_u8tc_bits: bad candidate bitmaps");
+  if (!cbits || bstride < (n + 31) / 32 || bstride % 4 != 0 || !aligned16(cbits))
+    return fail(MRPT_EPARAM, "mrpt_scan_topk_u8tc_bits: bad candidate bitmaps (bstride a multiple of 4 words, "
+                             "16-byte aligned)");
   if (!X || !Xs || !info || !Q || n < 1 || n >= (int64_t)1 << 31 || d < 1 || ldx < d || ldqq < d || nq < 0)
     return fail(MRPT_ESHAPE, "mrpt_scan_topk_u8tc_bits: bad shape");
   if (ldq % 16 != 0 || ldq < d || ldq < tc::kKB || ldq > tc::kMaxKB * tc::kKB || k < 1 || k > 32 || d % 4 != 0 ||
@@ -2598,7 +2614,7 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
                          reinterpret_cast<const uint4 *>(info), n, rinfo, rt1));
   }
   // kernel variant per chunk (below): CG column-group warps per query
-  typedef void (*tc_fn)(const CUtensorMap, const CUtensorMap, tc::TcArgs);
+  typedef void (*tc_fn)(const CUtensorMap, const CUtensorMap, const CUtensorMap, tc::TcArgs);
   auto pick_tc = [&](int cg, int *threads) -> tc_fn {
     if (cg >= 4) {
       *threads = tc::threads_for<4>();
@@ -2623,8 +2639,10 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
     const int64_t m = nq - q0 < mc ? nq - q0 : mc;
     const int64_t g1 = m < (int64_t)num_sms() * 8 ? m : (int64_t)num_sms() * 8;
     (count_launch(), k_quantize_q8<<<(unsigned)g1, kScanNT, 0, s>>>(Q + q0 * ldqq, ldqq, d, (int)ldq, m, qop, qp));
-    CUtensorMap tmA;
+    CUtensorMap tmA, tmC;
     if (!tc_map(&tmA, qop, m, ldq, tc::kM)) return fail(MRPT_ECUDA, "mrpt_scan_topk_u8tc_bits: tensor map (queries)");
+    if (!tc_map_words(&tmC, cbits + q0 * bstride, m, bstride))
+      return fail(MRPT_ECUDA, "mrpt_scan_topk_u8tc_bits: tensor map (candidate bitmaps)");
     cudaMemsetAsync(ent_cnt, 0, (size_t)m * 4, s);
     cudaMemsetAsync(ent_cnt + mc, 0x7f, (size_t)m * 4, s);  // 3.4e38: no bound yet
     cudaMemsetAsync(ent_cnt + 2 * mc, 0, (size_t)m * 4, s);
@@ -2675,7 +2693,7 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
     }
     cudaEvent_t kt0;
     ktimer_begin(s, &kt0);
-    (count_launch(), fk<<<grid, fthreads, tc::kSmemBytes, s>>>(tmA, tmB, ta));
+    (count_launch(), fk<<<grid, fthreads, tc::kSmemBytes, s>>>(tmA, tmB, tmC, ta));
     ktimer_end(s, kt0);
     if (dbg) {
       const int64_t ldD = (n + 15) & ~(int64_t)15;

@@ -57,7 +57,9 @@ constexpr uint32_t kInfoBytes = kN * 20;  // per tile: 256 x 16-B pre-test recor
 constexpr uint32_t kOffA = 0;
 constexpr uint32_t kOffB = kOffA + kMaxKB * kABytes;
 constexpr uint32_t kOffInfo = kOffB + kStages * kBBytes;
-constexpr uint32_t kOffBar = kOffInfo + 2 * kInfoBytes;
+constexpr uint32_t kBitsBytes = kM * (kN / 32) * 4;  // the block's candidate words of one tile (4 KB)
+constexpr uint32_t kOffBits = kOffInfo + 2 * kInfoBytes;
+constexpr uint32_t kOffBar = kOffBits + 2 * kBitsBytes;
 // barriers: fullB[3], emptyB[3], fullA, emptyA, tmem_full[2], epi_empty[2], info_full[2]
 constexpr int kNumBars = 2 * kStages + 2 + 6;
 constexpr uint32_t kOffTmemSlot = kOffBar + 8 * kNumBars;
@@ -302,11 +304,12 @@ __device__ __forceinline__ void tc_admit(EpiState<KT> &st, float A, float r, flo
 
 template <int KT, int CG>
 __global__ void __launch_bounds__(threads_for<CG>(), 1)
-    k_tc_filter(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+    k_tc_filter(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmC, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t sA = sbase + kOffA, sB = sbase + kOffB, sInfo = sbase + kOffInfo;
+  const uint32_t sA = sbase + kOffA, sB = sbase + kOffB, sInfo = sbase + kOffInfo, sBits = sbase + kOffBits;
   const uint32_t bar0 = sbase + kOffBar;
   auto fullB = [&](int s) { return bar0 + 8u * s; };
   auto emptyB = [&](int s) { return bar0 + 8u * (kStages + s); };
@@ -345,6 +348,7 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
   if (warp == kProdWarp && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmC)) : "memory");
   }
   if (tid < kM) su_s[tid] = 0x7f800000u;
   tc_fence_before();
@@ -356,8 +360,12 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
     if (lane == 0) {
       int64_t cur_qb = -1;
       uint32_t nA = 0, g = 0;
-      for (int64_t it = it0; it < it1; ++it) {
-        const int qb = (int)(it / a.ntiles), tile = (int)(it % a.ntiles);
+      int qb = (int)(it0 / a.ntiles), tile = (int)(it0 % a.ntiles);
+      for (int64_t it = it0; it < it1; ++it, ++tile) {
+        if (tile == a.ntiles) {
+          tile = 0;
+          ++qb;
+        }
         if (qb != cur_qb) {
           mbar_wait_sleep(emptyA, (nA & 1u) ^ 1u);
           mbar_expect_tx(fullA, (uint32_t)a.kblocks * kABytes);
@@ -375,17 +383,23 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
         mbar_wait_sleep(epiEmpty(b), ((li >> 1) & 1u) ^ 1u);
         const int64_t rows = a.n - (int64_t)tile * kN < kN ? a.n - (int64_t)tile * kN : kN;
         const uint32_t t1b = ((uint32_t)rows * 4u + 15u) & ~15u;  // (rt1 is padded to 16 B)
-        mbar_expect_tx(infoFull(b), (uint32_t)rows * 16u + t1b);
+        mbar_expect_tx(infoFull(b), (uint32_t)rows * 16u + t1b + kBitsBytes);
         bulk_load(sInfo + b * kInfoBytes, a.rinfo + (int64_t)tile * kN, (uint32_t)rows * 16u, infoFull(b));
         bulk_load(sInfo + b * kInfoBytes + kN * 16, a.rt1 + (int64_t)tile * kN, t1b, infoFull(b));
+        // the block's candidate words for this tile: 128 queries x 8 words
+        tma_load_2d(sBits + b * kBitsBytes, &tmC, infoFull(b), tile * (kN / 32), qb * kM);
       }
     }
   } else if (warp == kMmaWarp) {
     if (lane == 0) {
       int64_t cur_qb = -1;
       uint32_t nA = 0, g = 0;
-      for (int64_t it = it0; it < it1; ++it) {
-        const int qb = (int)(it / a.ntiles);
+      int qb = (int)(it0 / a.ntiles), tile = (int)(it0 % a.ntiles);
+      for (int64_t it = it0; it < it1; ++it, ++tile) {
+        if (tile == a.ntiles) {
+          tile = 0;
+          ++qb;
+        }
         if (qb != cur_qb) {
           mbar_wait_sleep(fullA, nA & 1u);
           ++nA;
@@ -408,7 +422,7 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
           mma_commit(emptyB(s));
         }
         mma_commit(tmemFull(b));
-        const bool last_of_qb = it + 1 >= it1 || (int)((it + 1) / a.ntiles) != qb;
+        const bool last_of_qb = it + 1 >= it1 || tile + 1 == a.ntiles;
         if (last_of_qb) mma_commit(emptyA);
       }
     }
@@ -434,29 +448,15 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
       for (int i = 0; i < a.k; ++i)
         if (o + i < a.kbcap) a.kb[q * a.kbcap + o + i] = top[i];
     };
-    // candidate words of item itx for this warp's columns
     constexpr int NWD = kColsPerWarp / 32;
-    // (the tail mask is kept apart and applied when the words are used, a
-    // tile later, so nothing waits on the loads here)
-    auto load_words = [&](int64_t itx, uint32_t (&w)[NWD], uint32_t (&mk)[NWD]) {
-      const int qbx = (int)(itx / a.ntiles), tilex = (int)(itx % a.ntiles);
-      const int64_t qx = (int64_t)qbx * kM + qloc;
-#pragma unroll
-      for (int c = 0; c < NWD; ++c) {
-        const int64_t col0 = (int64_t)tilex * kN + cg * kColsPerWarp + c * 32;
-        const bool in = qx < a.m && col0 < a.n;
-        w[c] = in ? __ldg(a.cbits + qx * a.bstride + (col0 >> 5)) : 0u;
-        mk[c] = !in ? 0u : (a.n - col0 < 32 ? (1u << (a.n - col0)) - 1u : 0xffffffffu);
-      }
-    };
-    uint32_t wnext[NWD], mnext[NWD];
-    if (it0 < it1) load_words(it0, wnext, mnext);
+    const uint32_t *bits_s = reinterpret_cast<const uint32_t *>(smem + kOffBits);  // [2][kM][8]
+    int qb = (int)(it0 / a.ntiles), tile = (int)(it0 % a.ntiles) - 1;
+    float sunext = __int_as_float(0x7f800000);
     for (int64_t it = it0; it < it1; ++it) {
-      const int qb = (int)(it / a.ntiles), tile = (int)(it % a.ntiles);
-      uint32_t wd[NWD];
-#pragma unroll
-      for (int c = 0; c < NWD; ++c) wd[c] = wnext[c] & mnext[c];
-      if (it + 1 < it1) load_words(it + 1, wnext, mnext);  // in flight while this tile is filtered
+      if (++tile == a.ntiles) {
+        tile = 0;
+        ++qb;
+      }
       if (qb != cur_qb) {
         if (valid) tc_flush<KT>(st, q, a);
         // new query block: every epilogue warp is past the old one before
@@ -475,6 +475,7 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
         q = (int64_t)qb * kM + qloc;
         valid = q < a.m;
         st.su = __int_as_float(0x7f800000);
+        sunext = __int_as_float(0x7f800000);  // (a bound of the previous query)
         st.left = 0;
         st.base = 0;
         if (valid) {
@@ -487,11 +488,21 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
           sel = P.qsigned ? 0 : 1;
         }
       }
-      if (valid) st.su = fminf(st.su, __uint_as_float(__ldcg(a.su_g + q)));
+      // the other CTAs' bound for this query, loaded a tile earlier
+      st.su = fminf(st.su, sunext);
+      if (valid) sunext = __uint_as_float(__ldcg(a.su_g + q));
       const uint32_t li = (uint32_t)(it - it0), b = li & 1u;
       mbar_wait(infoFull(b), (li >> 1) & 1u);
       mbar_wait(tmemFull(b), (li >> 1) & 1u);
       tc_fence_after();
+      // candidate words of this warp's columns (TMA-staged with the row records)
+      uint32_t wd[NWD];
+#pragma unroll
+      for (int c = 0; c < NWD; ++c) {
+        wd[c] = bits_s[(b * kM + qloc) * (kN / 32) + cg * NWD + c];
+        const int64_t col0 = (int64_t)tile * kN + cg * kColsPerWarp + c * 32;
+        if (a.n - col0 < 32) wd[c] &= a.n - col0 <= 0 ? 0u : (1u << (a.n - col0)) - 1u;
+      }
       if (a.noepi == 1) {
         tc_fence_before();
         __syncwarp();

@@ -1,1 +1,3 @@
-for r in u8tc_bits u8gemm_bits u8; do MRPT_PIN=$r MRPT_TC_DEBUG=1 python tools/profile_query.py --config 3 --votes 1 --reps 1 --time 2>&1 | grep -E "TIME|tc debug\] cg" | sed "s/^/$r /"; done
+export MRPT_PIN=u8tc_bits
+python tools/profile_query.py --config 2 --reps 2 --time 2>&1 | grep TIME | sed "s/^/pinned /"
+MRPT_TC_NOEPI=2 python tools/profile_query.py --config 2 --reps 2 --time 2>&1 | grep TIME | sed "s/^/NOADMIT /"
