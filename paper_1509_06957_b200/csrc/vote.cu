@@ -609,20 +609,40 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 4 : 1) k_vote_union(VoteArgs a
       s_len[t] = (int)(o[1] - s0);
     }
     __syncthreads();
+    // 16-byte loads: a slice [s, s + len) is covered by the aligned int4
+    // groups from s & ~3; lanes keep the components that fall inside it
     for (int t = tid / G; t < a.T; t += ngroups) {
+      const int64_t s0 = s_start[t];
       const int len = s_len[t];
-      const int32_t *Lt = a.leaf_indices + s_start[t];
+      const int64_t a0 = s0 & ~(int64_t)3;
+      const int lo = (int)(s0 - a0), hi = lo + len;  // element range within the aligned run
+      const int4 *L4 = reinterpret_cast<const int4 *>(a.leaf_indices + a0);
+      const int n4 = (hi + 3) >> 2;
       constexpr int UNR = 8;
-      for (int p0 = gl; p0 < len; p0 += UNR * G) {
-        int32_t id[UNR];
+      for (int p0 = gl; p0 < n4; p0 += UNR * G) {
+        int4 v[UNR];
+        const int64_t total = (int64_t)a.T * a.n;  // no 16-byte load past the array
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
           const int p = p0 + u * G;
-          id[u] = p < len ? __ldg(Lt + p) : -1;
+          if (p < n4 && a0 + 4 * (int64_t)p + 4 <= total) {
+            v[u] = __ldg(L4 + p);
+          } else {
+            int w[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              w[c] = p < n4 && a0 + 4 * (int64_t)p + c < total ? __ldg(a.leaf_indices + a0 + 4 * p + c) : -1;
+            v[u] = make_int4(w[0], w[1], w[2], w[3]);
+          }
         }
 #pragma unroll
-        for (int u = 0; u < UNR; ++u)
-          if (id[u] >= 0) atomicOr(bits + (id[u] >> 5), 1u << (id[u] & 31));
+        for (int u = 0; u < UNR; ++u) {
+          const int e = 4 * (p0 + u * G);
+          const int ids[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (e + c >= lo && e + c < hi) atomicOr(bits + (ids[c] >> 5), 1u << (ids[c] & 31));
+        }
       }
     }
     __syncthreads();
@@ -892,8 +912,9 @@ static int32_t vote_impl(const int32_t *leaf_indices, const int64_t *leaf_offset
     const int64_t g = (int64_t)num_sms() * per_sm;
     // lanes per leaf slice: enough for UNR=8 loads each over a mean slice
     const double mean_slice = (double)n / (double)((int64_t)1 << depth);
-    int Gu = 4;
-    while (Gu < 32 && Gu * 8 < mean_slice) Gu <<= 1;
+    int Gu = 4;  // lanes per slice: enough for 8 int4 loads each over a mean slice
+    while (Gu < 32 && Gu * 32 < mean_slice) Gu <<= 1;
+    if (const char *ge = getenv("MRPT_VOTE_GU")) Gu = atoi(ge);
     k_vote_union_launch(fn, (unsigned)(nq < g ? nq : g), nt, usmem, s, a, Gu);
     return launch_status("mrpt_vote");
   }
