@@ -102,13 +102,14 @@ __global__ void k_route(const float *__restrict__ proj, int64_t nrows, int depth
 // Fused query projection + descent.  CTA = QB queries x 128 trees; the QB
 // query rows are staged in shared memory, each thread walks one tree for all
 // QB queries at once (QB independent fp64 chains, CSC entries loaded once).
-template <int QB, bool SMEM>
+template <int QB, bool SMEM, typename QT = float>
 __global__ void __launch_bounds__(128)
 k_query_route(const float *__restrict__ Q, int64_t nq, int d, int64_t ldq,
               const int64_t *__restrict__ col_ptr, const int32_t *__restrict__ rows,
               const float *__restrict__ vals, const float *__restrict__ splits, int T,
               int depth, int32_t *__restrict__ leaves, int stride) {
-  extern __shared__ float qs[];
+  extern __shared__ __align__(16) unsigned char qs_raw[];
+  QT *qs = reinterpret_cast<QT *>(qs_raw);
   const int64_t q0 = (int64_t)blockIdx.y * QB;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nint = ((int64_t)1 << depth) - 1;
@@ -117,7 +118,7 @@ k_query_route(const float *__restrict__ Q, int64_t nq, int d, int64_t ldq,
       const bool live = q0 + qi < nq;
       const float *src = Q + (q0 + qi) * ldq;
       for (int c = threadIdx.x; c < d; c += blockDim.x)
-        qs[qi * stride + c] = live ? __ldg(src + c) : 0.0f;
+        qs[qi * stride + c] = (QT)(live ? __ldg(src + c) : 0.0f);
     }
     __syncthreads();
   }
@@ -147,7 +148,7 @@ k_query_route(const float *__restrict__ Q, int64_t nq, int d, int64_t ldq,
       for (int u = 0; u < 8; ++u) {
 #pragma unroll
         for (int qi = 0; qi < QB; ++qi) {
-          float x;
+          QT x;
           if (SMEM) {
             x = qs[qi * stride + r[u]];
           } else {
@@ -162,7 +163,7 @@ k_query_route(const float *__restrict__ Q, int64_t nq, int d, int64_t ldq,
       const double v = (double)__ldg(vals + s);
 #pragma unroll
       for (int qi = 0; qi < QB; ++qi) {
-        float x;
+        QT x;
         if (SMEM) {
           x = qs[qi * stride + r];
         } else {
@@ -245,6 +246,34 @@ extern "C" int32_t mrpt_route(const float *proj, int64_t nrows, int32_t depth, c
   return launch_status("mrpt_route");
 }
 
+template <int QB, typename QT = float>
+static int32_t query_route_launch(const float *Q, int64_t nq, int32_t d, int64_t ldq, const int64_t *col_ptr,
+                                  const int32_t *rows, const float *vals, const float *splits, int32_t T,
+                                  int32_t depth, int32_t *leaves, cudaStream_t s) {
+  const int stride = (d & 1) ? d : d + 1;
+  const size_t smem = (size_t)QB * stride * sizeof(QT);
+  const int64_t qblocks = ceil_div<int64_t>(nq, QB);
+  if (qblocks > 65535LL * 1024) return fail(MRPT_EPARAM, "mrpt_query_route: too many queries per call");
+  int64_t off = 0;
+  // gridDim.y is limited to 65535: split very large batches.
+  while (off < nq) {
+    const int64_t chunk_q = (nq - off) < 65535LL * QB ? (nq - off) : 65535LL * QB;
+    dim3 grid((unsigned)ceil_div<int>(T, 128), (unsigned)ceil_div<int64_t>(chunk_q, QB));
+    if (smem <= 160 * 1024) {
+      cudaFuncSetAttribute(k_query_route<QB, true, QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      (count_launch(), k_query_route<QB, true, QT><<<grid, 128, smem, s>>>(Q + off * ldq, chunk_q, d, ldq, col_ptr,
+                                                                       rows, vals, splits, T, depth,
+                                                                       leaves + off * T, stride));
+    } else {
+      (count_launch(), k_query_route<QB, false><<<grid, 128, 0, s>>>(Q + off * ldq, chunk_q, d, ldq, col_ptr,
+                                                                     rows, vals, splits, T, depth,
+                                                                     leaves + off * T, stride));
+    }
+    off += chunk_q;
+  }
+  return MRPT_OK;
+}
+
 extern "C" int32_t mrpt_query_route(const float *Q, int64_t nq, int32_t d, int64_t ldq,
                                     const int64_t *col_ptr, const int32_t *rows,
                                     const float *vals, const float *splits, int32_t T,
@@ -254,28 +283,15 @@ extern "C" int32_t mrpt_query_route(const float *Q, int64_t nq, int32_t d, int64
     return fail(MRPT_ESHAPE, "mrpt_query_route: bad shape");
   if (nq == 0) return MRPT_OK;
   cudaStream_t s = as_stream(stream);
-  constexpr int QB = 4;
-  const int stride = (d & 1) ? d : d + 1;
-  const size_t smem = (size_t)QB * stride * sizeof(float);
-  const int64_t qblocks = ceil_div<int64_t>(nq, QB);
-  if (qblocks > 65535LL * 1024) return fail(MRPT_EPARAM, "mrpt_query_route: too many queries per call");
-  int64_t off = 0;
-  // gridDim.y is limited to 65535: split very large batches.
-  while (off < nq) {
-    const int64_t chunk_q = (nq - off) < 65535LL * QB ? (nq - off) : 65535LL * QB;
-    dim3 grid((unsigned)ceil_div<int>(T, 128), (unsigned)ceil_div<int64_t>(chunk_q, QB));
-    if (smem <= 160 * 1024) {
-      cudaFuncSetAttribute(k_query_route<QB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      (count_launch(), k_query_route<QB, true><<<grid, 128, smem, s>>>(Q + off * ldq, chunk_q, d, ldq, col_ptr, rows,
-                                                      vals, splits, T, depth, leaves + off * T,
-                                                      stride));
-    } else {
-      (count_launch(), k_query_route<QB, false><<<grid, 128, 0, s>>>(Q + off * ldq, chunk_q, d, ldq, col_ptr, rows,
-                                                    vals, splits, T, depth, leaves + off * T,
-                                                    stride));
-    }
-    off += chunk_q;
-  }
+  const char *qe = getenv("MRPT_ROUTE_QB");
+  const int qbs = qe ? atoi(qe) : 8;
+  // 8 queries per thread (8 independent float64 chains per CSC entry load);
+  // measured at config 2: 0.27 ms vs 0.30 (4) and 0.46 (2).  A float64 copy
+  // of the query rows in shared memory was slower (0.47 ms: 8-byte loads at
+  // random coordinates conflict twice as often).
+  const int32_t st = qbs == 4
+      ? query_route_launch<4>(Q, nq, d, ldq, col_ptr, rows, vals, splits, T, depth, leaves, s)
+      : query_route_launch<8>(Q, nq, d, ldq, col_ptr, rows, vals, splits, T, depth, leaves, s);
+  if (st) return st;
   return launch_status("mrpt_query_route");
 }

@@ -1,5 +1,3 @@
 export MRPT_PIN=u8tc_bits
-python tools/profile_query.py --config 2 --reps 2 --time 2>&1 | grep TIME | sed "s/^/pinned /"
-for gu in 4 16; do MRPT_VOTE_GU=$gu python tools/profile_query.py --config 2 --reps 2 --time 2>&1 | grep TIME | sed "s/^/gu=$gu /"; done
-unset MRPT_PIN
-python tools/profile_query.py --config 3 --reps 2 --time 2>&1 | grep TIME | sed "s/^/c3 /"
+for qb in 4 8; do MRPT_ROUTE_QB=$qb python tools/profile_query.py --config 2 --reps 2 --time 2>&1 | grep TIME | sed "s/^/dbl qb=$qb /"; done
+MRPT_ROUTE_F32=1 python tools/profile_query.py --config 2 --reps 2 --time 2>&1 | grep TIME | sed "s/^/f32 qb=8 /"
