@@ -639,9 +639,14 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 4 : 1) k_vote_union(VoteArgs a
         for (int u = 0; u < UNR; ++u) {
           const int e = 4 * (p0 + u * G);
           const int ids[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+          if (e >= lo && e + 4 <= hi) {  // interior group: no per-id range checks
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (e + c >= lo && e + c < hi) atomicOr(bits + (ids[c] >> 5), 1u << (ids[c] & 31));
+            for (int c = 0; c < 4; ++c) atomicOr(bits + (ids[c] >> 5), 1u << (ids[c] & 31));
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (e + c >= lo && e + c < hi) atomicOr(bits + (ids[c] >> 5), 1u << (ids[c] & 31));
+          }
         }
       }
     }
