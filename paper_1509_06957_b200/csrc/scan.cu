@@ -1843,6 +1843,7 @@ __global__ void __launch_bounds__(256) k_rerank(TopkArgs a) {
   }
 }
 
+
 // GEMM operand of each query: the filter's own quantisation (u8 or s8),
 // stored as s8 (u8 entries shifted by -128, i.e. byte ^ 0x80), and its
 // parameters.  One CTA per query.
@@ -2499,7 +2500,7 @@ extern "C" int32_t mrpt_scan_topk_u8gemm_bits(const float *X, int64_t n, int32_t
 // parameters, the row records, per-query entry lists and counts, and the
 // survivor / fallback lists the re-rank and the exact fallback read.
 static const int kTcCap = tc::kSelCap;
-static const int kTcKb = 256;  // per query: the streams' k smallest bounds
+static const int kTcKb = tc::kKbSort;  // per query: the CTAs' k smallest bounds
 
 static int64_t u8tc_bytes(int64_t n, int64_t ldq, int64_t mc, int64_t *off) {
   auto al = [](int64_t x) { return (x + 1023) & ~(int64_t)1023; };
@@ -2627,8 +2628,7 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
     *threads = tc::threads_for<1>();
     return k <= 16 ? tc::k_tc_filter<16, 1> : tc::k_tc_filter<32, 1>;
   };
-  const int sel_smem = 8 * 4 * tc::kSelCap;
-  cudaFuncSetAttribute(tc::k_tc_select, cudaFuncAttributeMaxDynamicSharedMemorySize, sel_smem);
+
   const int buf = (k + kScanNT <= 1024) ? 1024 : 2048;
   topk_fn tfn = buf == 1024 ? k_scan_topk_tiled<1024> : k_scan_topk_tiled<2048>;
   const size_t tsmem =
@@ -2734,7 +2734,7 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
     a.surv = a.nsurv + mc;
     {
       const int64_t g = ceil_div<int64_t>(m, 4);
-      (count_launch(), tc::k_tc_select<<<(unsigned)(g < 4096 ? g : 4096), 128, sel_smem, s>>>(
+      (count_launch(), tc::k_tc_select<<<(unsigned)(g < 4096 ? g : 4096), 128, 0, s>>>(
                            ent, ent_cnt, ta.kb, ta.kb_cnt, kTcKb, kTcCap, m, k, a.surv, a.nsurv, fb + 1, fb));
     }
     if (getenv("MRPT_TC_DEBUG")) {

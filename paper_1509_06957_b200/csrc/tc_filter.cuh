@@ -617,53 +617,41 @@ __global__ void k_tc_rows(const uint4 *__restrict__ info, int64_t n, uint4 *__re
 // Per query (one warp): bounds of the entries' (A, r, eta), the k-th smallest
 // upper bound U_k, survivors L <= U_k to k_rerank's lists; list overflow or
 // too many survivors -> exact fallback.
-constexpr int kSelCap = 2048;
+constexpr int kSelCap = 2048;  // entry slots per query
+constexpr int kKbSort = 256;   // bounds per query in the union of the CTAs' k smallest (kTcKb)
 __global__ void __launch_bounds__(128) k_tc_select(const uint4 *__restrict__ ent, const int32_t *__restrict__ ent_cnt,
                                                    const float *__restrict__ kb, const int32_t *__restrict__ kb_cnt,
                                                    int kbcap, int cap, int64_t m, int k, int32_t *surv, int32_t *nsurv,
                                                    int32_t *fb_list, int32_t *fb_count) {
-  extern __shared__ float sel_smem[];
-  float (*sk)[kSelCap] = reinterpret_cast<float (*)[kSelCap]>(sel_smem);
-  int32_t (*si)[kSelCap] = reinterpret_cast<int32_t (*)[kSelCap]>(sel_smem + 4 * kSelCap);
+  __shared__ float sk[4][kKbSort];
+  __shared__ int32_t si[4][kKbSort];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float *kk = sk[w];
   int32_t *ii = si[w];
   for (int64_t q = (int64_t)blockIdx.x * 4 + w; q < m; q += (int64_t)gridDim.x * 4) {
     const int cnt = ent_cnt[q];
     const uint4 *e = ent + q * cap;
-    if (cnt > cap || cnt > kSelCap) {
+    const int nb = kb_cnt[q];
+    // overflowing entry or bound lists (not reached with <= 8 CTAs per query
+    // block): the exact fallback
+    if (cnt > cap || nb > kbcap || nb > kKbSort) {
       if (lane == 0) {
         nsurv[q] = -1;
         fb_list[atomicAdd(fb_count, 1)] = (int32_t)q;
       }
       continue;
     }
-    // the query's k-th smallest upper bound: the union of the streams' k
-    // smallest bounds holds it (a short sort); with too many streams, sort
-    // every entry's bound instead
-    const int nb = kb_cnt[q];
-    const bool from_kb = nb <= kbcap;
-    const int nsrt = from_kb ? nb : cnt;
+    // the query's k-th smallest upper bound: the union of the CTAs' k
+    // smallest bounds holds it (a short sort)
     int np2 = 32;
-    while (np2 < nsrt) np2 <<= 1;
+    while (np2 < nb) np2 <<= 1;
     for (int i = lane; i < np2; i += 32) {
-      float u = __int_as_float(0x7f800000);
-      if (i < nsrt) {
-        if (from_kb) {
-          u = kb[q * kbcap + i];
-        } else {
-          const uint4 v = e[i];
-          float L;
-          dist_bounds_f(__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), L, u);
-          if (u != u) u = __int_as_float(0x7f800000);  // no entry
-        }
-      }
-      kk[i] = u;
+      kk[i] = i < nb ? kb[q * kbcap + i] : __int_as_float(0x7f800000);
       ii[i] = i;
     }
     __syncwarp();
     warp_sort(kk, ii, np2);
-    const double uk = nsrt >= k ? (double)kk[k - 1] : __longlong_as_double(0x7ff0000000000000LL);
+    const double uk = nb >= k ? (double)kk[k - 1] : __longlong_as_double(0x7ff0000000000000LL);
     __syncwarp();
     int ns = 0;
     for (int i0 = 0; i0 < cnt; i0 += 32) {
