@@ -308,7 +308,7 @@ int32_t mrpt_scan_topk_u8gemm_bits(const float *X, int64_t n, int32_t d, int64_t
  * tcgen05.mma.kind::i8 into TMEM and bounds every candidate straight out of
  * TMEM (no dot-product matrix in HBM); survivors get the exact float64
  * re-rank.  Same arguments and results as mrpt_scan_topk_u8gemm_bits.
- * 128 <= ldq <= 896, k <= 32; bstride a multiple of 4 words (the bitmaps are
+ * 128 <= ldq <= 1024, k <= 16; bstride a multiple of 4 words (the bitmaps are
  * TMA-staged per row tile).  workspace: 256-byte aligned, sized by
  * mrpt_scan_topk_u8tc_workspace_size (smaller workspaces run smaller query
  * chunks). */

@@ -2587,7 +2587,7 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
                              "16-byte aligned)");
   if (!X || !Xs || !info || !Q || n < 1 || n >= (int64_t)1 << 31 || d < 1 || ldx < d || ldqq < d || nq < 0)
     return fail(MRPT_ESHAPE, "mrpt_scan_topk_u8tc_bits: bad shape");
-  if (ldq % 16 != 0 || ldq < d || ldq < tc::kKB || ldq > tc::kMaxKB * tc::kKB || k < 1 || k > 32 || d % 4 != 0 ||
+  if (ldq % 16 != 0 || ldq < d || ldq < tc::kKB || ldq > tc::kMaxKB * tc::kKB || k < 1 || k > tc::kTopMax || d % 4 != 0 ||
       ldx % 4 != 0 || !aligned16(X) || !aligned16(Xs) || (reinterpret_cast<uintptr_t>(info) & 15u))
     return fail(MRPT_EPARAM, "mrpt_scan_topk_u8tc_bits: unsupported shape");
   if (nq == 0) return MRPT_OK;
@@ -2608,25 +2608,28 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
   int32_t *fb = reinterpret_cast<int32_t *>(w + off[5]);
   cudaStream_t s = as_stream(stream);
   CUtensorMap tmB;
-  if (!tc_map(&tmB, Xs, n, ldq, tc::kN)) return fail(MRPT_ECUDA, "mrpt_scan_topk_u8tc_bits: tensor map (rows)");
+  const int mcast = getenv("MRPT_TC_MC") ? (atoi(getenv("MRPT_TC_MC")) == 2 ? 2 : 1) : 2;
+  // (a cluster pair loads half a row tile per CTA and multicasts it)
+  if (!tc_map(&tmB, Xs, n, ldq, tc::kN / mcast)) return fail(MRPT_ECUDA, "mrpt_scan_topk_u8tc_bits: tensor map (rows)");
   {
     const int64_t g = ceil_div<int64_t>(n, 256);
     (count_launch(), tc::k_tc_rows<<<(unsigned)(g < 4096 ? g : 4096), 256, 0, s>>>(
                          reinterpret_cast<const uint4 *>(info), n, rinfo, rt1));
   }
-  // kernel variant per chunk (below): CG column-group warps per query
+  // kernel variant per chunk (below): CG column-group warps per query, MC
+  // CTAs per cluster sharing the row tiles (multicast)
   typedef void (*tc_fn)(const CUtensorMap, const CUtensorMap, const CUtensorMap, tc::TcArgs);
-  auto pick_tc = [&](int cg, int *threads) -> tc_fn {
+  auto pick_tc = [&](int cg, int mc, int *threads) -> tc_fn {
     if (cg >= 4) {
       *threads = tc::threads_for<4>();
-      return k <= 16 ? tc::k_tc_filter<16, 4> : tc::k_tc_filter<32, 4>;
+      return mc == 2 ? tc::k_tc_filter<16, 4, 2> : tc::k_tc_filter<16, 4, 1>;
     }
     if (cg == 2) {
       *threads = tc::threads_for<2>();
-      return k <= 16 ? tc::k_tc_filter<16, 2> : tc::k_tc_filter<32, 2>;
+      return mc == 2 ? tc::k_tc_filter<16, 2, 2> : tc::k_tc_filter<16, 2, 1>;
     }
     *threads = tc::threads_for<1>();
-    return k <= 16 ? tc::k_tc_filter<16, 1> : tc::k_tc_filter<32, 1>;
+    return mc == 2 ? tc::k_tc_filter<16, 1, 2> : tc::k_tc_filter<16, 1, 1>;
   };
 
   const int buf = (k + kScanNT <= 1024) ? 1024 : 2048;
@@ -2672,15 +2675,19 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
     // own k-th bound warm-up (>= k admissions each): few query blocks per
     // CTA (small chunks) means many streams per query.  Fewer column groups
     // there, and at most 8 CTAs per query block.
-    const int64_t items = (int64_t)ta.nqb * ntiles;
-    int grid = (int)(items < num_sms() ? items : num_sms());
+    // (units: query blocks, or query-block pairs for a cluster pair; groups:
+    // CTAs, or clusters)
+    const int64_t items = ceil_div<int64_t>(ta.nqb, mcast) * ntiles;
+    const int64_t maxg = num_sms() / mcast;
+    int groups = (int)(items < maxg ? items : maxg);
     auto cpq = [&](int g) { return (int)ceil_div<int64_t>((int64_t)ntiles * g, items) + 1; };
-    int cg = cpq(grid) <= 3 ? 4 : (cpq(grid) <= 6 ? 2 : 1);
+    int cg = cpq(groups) <= 3 ? 4 : (cpq(groups) <= 6 ? 2 : 1);
     if (cg == 1)
-      while (grid > 1 && cpq(grid) > 8) --grid;
+      while (groups > 1 && cpq(groups) > 8) --groups;
     if (const char *cge = getenv("MRPT_TC_CG")) cg = atoi(cge);
+    const int grid = groups * mcast;
     int fthreads = 0;
-    const tc_fn fk = pick_tc(cg, &fthreads);
+    const tc_fn fk = pick_tc(cg, mcast, &fthreads);
     cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::kSmemBytes);
     ta.dbgD = nullptr;
     ta.noepi = getenv("MRPT_TC_NOEPI") ? atoi(getenv("MRPT_TC_NOEPI")) : 0;
@@ -2693,7 +2700,24 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
     }
     cudaEvent_t kt0;
     ktimer_begin(s, &kt0);
-    (count_launch(), fk<<<grid, fthreads, tc::kSmemBytes, s>>>(tmA, tmB, tmC, ta));
+    if (mcast == 2) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)grid);
+      cfg.blockDim = dim3((unsigned)fthreads);
+      cfg.dynamicSmemBytes = tc::kSmemBytes;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      count_launch();
+      cudaLaunchKernelEx(&cfg, fk, tmA, tmB, tmC, ta);
+    } else {
+      (count_launch(), fk<<<grid, fthreads, tc::kSmemBytes, s>>>(tmA, tmB, tmC, ta));
+    }
     ktimer_end(s, kt0);
     if (dbg) {
       const int64_t ldD = (n + 15) & ~(int64_t)15;

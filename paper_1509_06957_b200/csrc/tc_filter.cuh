@@ -41,9 +41,9 @@ namespace tc {
 constexpr int kM = 128;         // queries per block = TMEM lanes
 constexpr int kN = 256;         // rows per tile = TMEM columns per accumulator
 constexpr int kKB = 128;        // K bytes per block (one 128-B swizzle row)
-constexpr int kMaxKB = 7;       // resident query block: ldq <= 896
-constexpr int kStages = 2;      // row-tile ring (the epilogue, not the MMA feed, bounds the kernel)
-constexpr int kTopMax = 32;     // k <= 32: a query's k smallest upper bounds in shared memory
+constexpr int kMaxKB = 8;       // ldq <= 1024 (the route's u8 shadow limit)
+constexpr int kStages = 4;      // ring of (query block, row tile) K-block pairs: 192 KB in flight per SM
+constexpr int kTopMax = 16;     // k <= 16: a query's k smallest upper bounds in shared memory
 // epilogue: 4 lane quarters x CG column groups (template); + TMA + MMA warps
 template <int CG>
 constexpr int threads_for() {
@@ -54,13 +54,16 @@ constexpr uint32_t kBBytes = kN * kKB;    // 32 KB per stage
 constexpr uint32_t kInfoBytes = kN * 20;  // per tile: 256 x 16-B pre-test records + 256 x t1 (5 KB)
 
 // shared-memory carve-up (offsets from a 1024-B aligned base)
-constexpr uint32_t kOffA = 0;
-constexpr uint32_t kOffB = kOffA + kMaxKB * kABytes;
-constexpr uint32_t kOffInfo = kOffB + kStages * kBBytes;
+// stage s: the query block's K block (16 KB) then the row tile's (32 KB);
+// both streamed by TMA (the queries re-read from L2 every tile: more bytes in
+// flight beats a resident query block, the feed is latency-bound)
+constexpr uint32_t kStageBytes = kABytes + kBBytes;
+constexpr uint32_t kOffStage = 0;
+constexpr uint32_t kOffInfo = kOffStage + kStages * kStageBytes;
 constexpr uint32_t kBitsBytes = kM * (kN / 32) * 4;  // the block's candidate words of one tile (4 KB)
 constexpr uint32_t kOffBits = kOffInfo + 2 * kInfoBytes;
 constexpr uint32_t kOffBar = kOffBits + 2 * kBitsBytes;
-// barriers: fullB[3], emptyB[3], fullA, emptyA, tmem_full[2], epi_empty[2], info_full[2]
+// barriers: fullB[kStages], emptyB[kStages], (2 unused), tmem_full[2], epi_empty[2], info_full[2]
 constexpr int kNumBars = 2 * kStages + 2 + 6;
 constexpr uint32_t kOffTmemSlot = kOffBar + 8 * kNumBars;
 constexpr uint32_t kOffSu = kOffTmemSlot + 16;
@@ -146,6 +149,25 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
       ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
       : "memory");
 }
+// B-tile half loaded once and written to both CTAs of a cluster pair (same
+// shared-memory offset, each CTA's barrier at that offset gets the bytes)
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap *map, uint32_t bar, int x, int y,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
@@ -176,6 +198,12 @@ __device__ __forceinline__ void mma_i8(uint32_t dtmem, uint64_t adesc, uint64_t 
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
       ::"r"(dtmem), "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accum));
+}
+// commit arriving on the barrier at this offset in every CTA of the mask
+__device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(bar), "h"(mask)
+               : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
@@ -302,14 +330,19 @@ __device__ __forceinline__ void tc_admit(EpiState<KT> &st, float A, float r, flo
   }
 }
 
-template <int KT, int CG>
+// MC = 2: launched as clusters of 2 CTAs working on two query blocks over
+// the same row tiles in lockstep; each CTA TMA-loads half of every B tile and
+// multicasts it to both, so each SM pulls half the row bytes from L2 (the
+// MMA feed, not HBM, is the floor of this kernel).  A stage is refilled only
+// after both CTAs' MMAs committed it (multicast commits, count-2 barriers).
+template <int KT, int CG, int MC>
 __global__ void __launch_bounds__(threads_for<CG>(), 1)
     k_tc_filter(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t sA = sbase + kOffA, sB = sbase + kOffB, sInfo = sbase + kOffInfo, sBits = sbase + kOffBits;
+  const uint32_t sStage = sbase + kOffStage, sInfo = sbase + kOffInfo, sBits = sbase + kOffBits;
   const uint32_t bar0 = sbase + kOffBar;
   auto fullB = [&](int s) { return bar0 + 8u * s; };
   auto emptyB = [&](int s) { return bar0 + 8u * (kStages + s); };
@@ -323,13 +356,18 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
   constexpr int kEpiWarps = 4 * CG, kColsPerWarp = kN / CG;
   constexpr int kProdWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t W = (int64_t)a.nqb * a.ntiles;
-  const int64_t it0 = W * blockIdx.x / gridDim.x, it1 = W * (blockIdx.x + 1) / gridDim.x;
+  // work units: query blocks (MC = 1) or query-block pairs (MC = 2, one per
+  // cluster); each CTA (cluster) walks a contiguous range of (unit, tile)
+  const int rank = MC > 1 ? (int)cluster_rank() : 0;
+  const int64_t units = (a.nqb + MC - 1) / MC;
+  const int64_t W = units * a.ntiles;
+  const int64_t grp = blockIdx.x / MC, ngrp = gridDim.x / MC;
+  const int64_t it0 = W * grp / ngrp, it1 = W * (grp + 1) / ngrp;
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(fullB(s), 1);
-      mbar_init(emptyB(s), 1);
+      mbar_init(emptyB(s), MC);
     }
     mbar_init(fullA, 1);
     mbar_init(emptyA, 1);
@@ -353,31 +391,30 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
   if (tid < kM) su_s[tid] = 0x7f800000u;
   tc_fence_before();
   __syncthreads();
+  if (MC > 1) cluster_sync_all();  // the partner's barriers exist before any multicast
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == kProdWarp) {
     if (lane == 0) {
-      int64_t cur_qb = -1;
-      uint32_t nA = 0, g = 0;
-      int qb = (int)(it0 / a.ntiles), tile = (int)(it0 % a.ntiles);
+      uint32_t g = 0;
+      int qb = (int)(it0 / a.ntiles) * MC + rank, tile = (int)(it0 % a.ntiles);
       for (int64_t it = it0; it < it1; ++it, ++tile) {
         if (tile == a.ntiles) {
           tile = 0;
-          ++qb;
-        }
-        if (qb != cur_qb) {
-          mbar_wait_sleep(emptyA, (nA & 1u) ^ 1u);
-          mbar_expect_tx(fullA, (uint32_t)a.kblocks * kABytes);
-          for (int kb = 0; kb < a.kblocks; ++kb) tma_load_2d(sA + kb * kABytes, &tmA, fullA, kb * kKB, qb * kM);
-          ++nA;
-          cur_qb = qb;
+          qb += MC;
         }
         for (int kb = 0; kb < a.kblocks; ++kb, ++g) {
           const int s = (int)(g % kStages);
           mbar_wait_sleep(emptyB(s), ((g / kStages) & 1u) ^ 1u);
-          mbar_expect_tx(fullB(s), kBBytes);
-          tma_load_2d(sB + s * kBBytes, &tmB, fullB(s), kb * kKB, tile * kN);
+          mbar_expect_tx(fullB(s), kStageBytes);
+          const uint32_t st = sStage + s * kStageBytes;
+          tma_load_2d(st, &tmA, fullB(s), kb * kKB, qb * kM);
+          if (MC > 1)
+            tma_load_2d_mc(st + kABytes + rank * (kBBytes / 2), &tmB, fullB(s), kb * kKB,
+                           tile * kN + rank * (kN / 2), (uint16_t)0x3);
+          else
+            tma_load_2d(st + kABytes, &tmB, fullB(s), kb * kKB, tile * kN);
         }
         const uint32_t li = (uint32_t)(it - it0), b = li & 1u;
         mbar_wait_sleep(epiEmpty(b), ((li >> 1) & 1u) ^ 1u);
@@ -389,21 +426,21 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
         // the block's candidate words for this tile: 128 queries x 8 words
         tma_load_2d(sBits + b * kBitsBytes, &tmC, infoFull(b), tile * (kN / 32), qb * kM);
       }
+      if (MC > 1) {
+        // both CTAs' last commits of every stage have arrived here before the
+        // cluster may exit (so the partner's commits into this CTA are done)
+        for (uint32_t gg = g > (uint32_t)kStages ? g - kStages : 0; gg < g; ++gg)
+          mbar_wait_sleep(emptyB((int)(gg % kStages)), (gg / kStages) & 1u);
+      }
     }
   } else if (warp == kMmaWarp) {
     if (lane == 0) {
-      int64_t cur_qb = -1;
-      uint32_t nA = 0, g = 0;
-      int qb = (int)(it0 / a.ntiles), tile = (int)(it0 % a.ntiles);
+      uint32_t g = 0;
+      int qb = (int)(it0 / a.ntiles) * MC + rank, tile = (int)(it0 % a.ntiles);
       for (int64_t it = it0; it < it1; ++it, ++tile) {
         if (tile == a.ntiles) {
           tile = 0;
-          ++qb;
-        }
-        if (qb != cur_qb) {
-          mbar_wait_sleep(fullA, nA & 1u);
-          ++nA;
-          cur_qb = qb;
+          qb += MC;
         }
         const uint32_t li = (uint32_t)(it - it0), b = li & 1u;
         mbar_wait_sleep(epiEmpty(b), ((li >> 1) & 1u) ^ 1u);
@@ -415,15 +452,17 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < kKB / 32; ++kk) {
-            const uint64_t ad = sw128_desc(sA + kb * kABytes + kk * 32);
-            const uint64_t bd = sw128_desc(sB + s * kBBytes + kk * 32);
+            const uint64_t ad = sw128_desc(sStage + s * kStageBytes + kk * 32);
+            const uint64_t bd = sw128_desc(sStage + s * kStageBytes + kABytes + kk * 32);
             mma_i8(dt, ad, bd, (kb | kk) != 0 ? 1u : 0u);
           }
-          mma_commit(emptyB(s));
+          if (MC > 1)
+            mma_commit_mc(emptyB(s), (uint16_t)0x3);
+          else
+            mma_commit(emptyB(s));
         }
         mma_commit(tmemFull(b));
-        const bool last_of_qb = it + 1 >= it1 || tile + 1 == a.ntiles;
-        if (last_of_qb) mma_commit(emptyA);
+
       }
     }
   } else {
@@ -450,12 +489,12 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
     };
     constexpr int NWD = kColsPerWarp / 32;
     const uint32_t *bits_s = reinterpret_cast<const uint32_t *>(smem + kOffBits);  // [2][kM][8]
-    int qb = (int)(it0 / a.ntiles), tile = (int)(it0 % a.ntiles) - 1;
+    int qb = (int)(it0 / a.ntiles) * MC + rank, tile = (int)(it0 % a.ntiles) - 1;
     float sunext = __int_as_float(0x7f800000);
     for (int64_t it = it0; it < it1; ++it) {
       if (++tile == a.ntiles) {
         tile = 0;
-        ++qb;
+        qb += MC;
       }
       if (qb != cur_qb) {
         if (valid) tc_flush<KT>(st, q, a);
@@ -592,6 +631,7 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
     if (cg == 0 && valid) publish();
   }
   __syncthreads();
+  if (MC > 1) cluster_sync_all();
   if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));

@@ -368,9 +368,9 @@ def _scan_variants(D, k):
             aligned = D.d % 4 == 0 and int(D.X.stride(0)) % 4 == 0 and D.X.data_ptr() % 16 == 0
             if k <= 96 and aligned:
                 out.append("u8gemm_bits")
-            # the fused tcgen05 filter: resident query block (ldq <= 896),
-            # k-th bound kept in registers (k <= 32)
-            if k <= 32 and aligned and 128 <= D.u8_rows()[1] <= 896:
+            # the fused tcgen05 filter: one 128-B K block at least, the
+            # queries' k smallest bounds in shared memory (k <= 16)
+            if k <= 16 and aligned and 128 <= D.u8_rows()[1] <= 1024:
                 out.append("u8tc_bits")
     elif k <= 120 and D.s8_rows() is not None:
         out.append("s8")

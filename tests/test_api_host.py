@@ -157,8 +157,8 @@ class _FakeIndex:
 
 @pytest.mark.parametrize("n,d,k,u8,want", [
     (60_000, 784, 10, True, ["u8", "u8gemm", "u8gemm_bits", "u8tc_bits", "fp32"]),
-    (60_000, 784, 33, True, ["u8", "u8gemm", "u8gemm_bits", "fp32"]),  # tcgen05 filter: k <= 32
-    (60_000, 1000, 10, True, ["u8", "u8gemm", "u8gemm_bits", "fp32"]),  # tcgen05 filter: ldq <= 896
+    (60_000, 784, 17, True, ["u8", "u8gemm", "u8gemm_bits", "fp32"]),  # tcgen05 filter: k <= 16
+    (60_000, 1000, 10, True, ["u8", "u8gemm", "u8gemm_bits", "u8tc_bits", "fp32"]),  # ldq 1008
     (60_000, 100, 10, True, ["u8", "u8gemm", "u8gemm_bits", "fp32"]),   # tcgen05 filter: ldq >= 128
     (60_000, 784, 100, True, ["u8", "u8gemm", "fp32"]),          # bitmap filter: k <= 96
     (60_000, 37, 10, True, ["u8", "u8gemm", "fp32"]),            # no 16-byte rows

@@ -40,8 +40,9 @@ CASES = [
     ("pixels", 5000, 784, 300, 8, 5, 10, 1, 0.0),     # config-2 width: 7 K blocks (last ragged)
     ("pixels", 5000, 200, 260, 8, 5, 10, 1, -0.05),   # s8 queries, 2 K blocks
     ("ints", 4100, 128, 390, 10, 6, 10, 2, 0.0),      # exact u8 rows, one K block
-    ("clusters01", 3000, 256, 385, 6, 4, 32, 1, 0.0), # k at the limit, ragged query block
-    ("dups", 2000, 128, 300, 6, 5, 20, 1, 0.0),       # exact-tie masses: fallback path
+    ("clusters01", 3000, 256, 385, 6, 4, 16, 1, 0.0), # k at the limit, ragged query block
+    ("pixels", 2500, 1000, 300, 6, 4, 10, 1, 0.0),    # widest rows: 8 K blocks (ldq 1008)
+    ("dups", 2000, 128, 300, 6, 5, 16, 1, 0.0),       # exact-tie masses: fallback path
     ("ints", 700, 160, 300, 5, 3, 1, 3, 0.0),         # k = 1, v > 1, n < 3 tiles
     ("pixels", 200, 256, 300, 3, 2, 10, 1, 0.0),      # n < one row tile
 ]
@@ -70,8 +71,8 @@ def test_tc_route_not_offered_outside_limits(rng):
     assert "u8tc_bits" not in _scan_variants(D, 10)
     X = _data("ints", rng, 3000, 128)
     D = mrpt.grow_trees(X, 4, 4, seed=1).device_index()
-    assert "u8tc_bits" in _scan_variants(D, 32)
-    assert "u8tc_bits" not in _scan_variants(D, 33)   # k-th bound in registers: k <= 32
+    assert "u8tc_bits" in _scan_variants(D, 16)
+    assert "u8tc_bits" not in _scan_variants(D, 17)   # k smallest bounds in shared memory: k <= 16
 
 
 @pytest.mark.parametrize("route", ["u8tc_bits", "u8gemm_bits", "u8"])
