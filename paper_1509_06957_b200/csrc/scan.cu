@@ -2671,19 +2671,18 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
     ta.kb_cnt = ent_cnt + 2 * mc;
     ta.kb = reinterpret_cast<float *>(ent_cnt + 3 * mc);
     ta.kbcap = kTcKb;
-    // Every (CTA, column group) that touches a query is a "stream" with its
-    // own k-th bound warm-up (>= k admissions each): few query blocks per
-    // CTA (small chunks) means many streams per query.  Fewer column groups
-    // there, and at most 8 CTAs per query block.
+    // Every CTA that touches a query runs its own warm-up of the query's
+    // k-th bound (>= k admissions; the CTA's column-group warps share one):
+    // few query blocks per CTA (small chunks) means many CTAs per query, so
+    // at most 8 CTAs per query block (fewer CTAs for tiny chunks).
     // (units: query blocks, or query-block pairs for a cluster pair; groups:
     // CTAs, or clusters)
     const int64_t items = ceil_div<int64_t>(ta.nqb, mcast) * ntiles;
     const int64_t maxg = num_sms() / mcast;
     int groups = (int)(items < maxg ? items : maxg);
     auto cpq = [&](int g) { return (int)ceil_div<int64_t>((int64_t)ntiles * g, items) + 1; };
-    int cg = cpq(groups) <= 3 ? 4 : (cpq(groups) <= 6 ? 2 : 1);
-    if (cg == 1)
-      while (groups > 1 && cpq(groups) > 8) --groups;
+    int cg = 4;
+    while (groups > 1 && cpq(groups) > 8) --groups;
     if (const char *cge = getenv("MRPT_TC_CG")) cg = atoi(cge);
     const int grid = groups * mcast;
     int fthreads = 0;
