@@ -2721,12 +2721,10 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
     if (dbg) {
       const int64_t ldD = (n + 15) & ~(int64_t)15;
       int32_t st = igemm_rows_tn(reinterpret_cast<const int8_t *>(Xs), ldD, qop, m, ldq, D2, ldD, s);
-      // compact D2 rows to n columns
-      for (int64_t r = 0; r < m && ldD != n; ++r) cudaMemcpyAsync(D2 + r * n, D2 + r * ldD, n * 4, cudaMemcpyDeviceToDevice, s);
       unsigned long long *o = nullptr;
       cudaMalloc(&o, 24);
       cudaMemsetAsync(o, 0, 24, s);
-      tc::k_tc_debug<<<1024, 256, 0, s>>>(D1, D2, m * n, ent_cnt, m, o);
+      tc::k_tc_debug<<<1024, 256, 0, s>>>(D1, D2, n, ldD, ent_cnt, m, o);
       unsigned long long h[3];
       cudaMemcpyAsync(h, o, 24, cudaMemcpyDeviceToHost, s);
       cudaStreamSynchronize(s);

@@ -728,10 +728,11 @@ __global__ void __launch_bounds__(128) k_tc_select(const uint4 *__restrict__ ent
 namespace mrpt {
 namespace tc {
 // debug: compare two (m, n) s32 matrices, count mismatches; entry stats
-__global__ void k_tc_debug(const int32_t *A, const int32_t *B, int64_t count, const int32_t *ent_cnt, int64_t m,
-                           unsigned long long *out) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
-    if (A[i] != B[i]) atomicAdd(out, 1ull);
+__global__ void k_tc_debug(const int32_t *A, const int32_t *B, int64_t n, int64_t ldb, const int32_t *ent_cnt,
+                           int64_t m, unsigned long long *out) {
+  // A: (m, n) dense; B: (m, ldb) library GEMM output
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m * n; i += (int64_t)gridDim.x * blockDim.x)
+    if (A[i] != B[(i / n) * ldb + i % n]) atomicAdd(out, 1ull);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
     atomicAdd(out + 1, (unsigned long long)ent_cnt[i]);
     atomicMax(out + 2, (unsigned long long)ent_cnt[i]);

@@ -91,3 +91,36 @@ def test_host_batch_pipelined_paths(rng, route):
     assert np.array_equal(counts.astype(np.int64), rc)
     assert np.array_equal(ids, rids)
     assert dists.tobytes() == rd.tobytes()
+
+
+def test_tc_dot_products_equal_library_gemm(tmp_path):
+    """Debug mode of the fused kernel (MRPT_TC_DEBUG): every (query, row)
+    int32 dot product it reads out of TMEM is compared on the device with the
+    cuBLASLt int8 GEMM of the same operands -- they must agree exactly (the
+    admission rule's bounds rest on that)."""
+    import os
+    import subprocess
+    import sys
+    import textwrap
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = textwrap.dedent("""
+        import numpy as np, sys
+        sys.path.insert(0, %r)
+        import paper_1509_06957_b200 as mrpt
+        rng = np.random.default_rng(3)
+        X = np.where(rng.random((3500, 300)) < 0.3, rng.random((3500, 300)), 0).astype(np.float32)
+        Q = X[3000:] - np.float32(0.02)   # signed queries too
+        index = mrpt.grow_trees(X[:3000], 5, 4, seed=1)
+        index.device_index().pin_route(10, 1, "u8tc_bits")
+        mrpt.approximate_knn_batch(Q, 10, index, 1)
+        index2 = mrpt.grow_trees(X[:3000], 5, 4, seed=2)
+        index2.device_index().pin_route(10, 1, "u8tc_bits")
+        mrpt.approximate_knn_batch(np.abs(X[3000:]), 10, index2, 1)
+    """ % root)
+    env = dict(os.environ, MRPT_TC_DEBUG="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stderr.splitlines() if "D mismatches=" in l]
+    assert len(lines) >= 2
+    assert all("D mismatches=0 " in l for l in lines), lines
