@@ -603,7 +603,7 @@ def _knn_batch_pipelined_bits(Qc, k, index, votes, route):
     compute = torch.cuda.current_stream()
     up, _ = _device.side_streams()
     vdir = D.vote_dir()
-    pieces = max(1, min(4, nq // _PIPE_MIN))
+    pieces = max(1, min(int(os.environ.get("MRPT_PIPE_PIECES", "4")), nq // 1024))
     bounds = [nq * i // pieces for i in range(pieces + 1)]
     for i in range(pieces):
         s, e = bounds[i], bounds[i + 1]

@@ -13,8 +13,8 @@ from paper_1509_06957_b200 import workloads  # noqa: E402
 X, Q, p = workloads.generate(2)
 index = mrpt.grow_trees(X, p["n_trees"], p["depth"], sparsity=p["sparsity"], seed=0)
 Qp = torch.from_numpy(Q).pin_memory()
-for mode in ("", "one", "first512"):
-    os.environ["MRPT_PIPE"] = mode
+for mode in ("p2", "p4", "p6", "p8"):
+    os.environ["MRPT_PIPE_PIECES"] = mode[1:]
     for _ in range(3):
         mrpt.approximate_knn_batch(Qp, p["k"], index, 1)
     torch.cuda.synchronize()
