@@ -70,3 +70,42 @@ def test_fuzz_matches_oracle(monkeypatch, case):
     assert np.array_equal(counts.astype(np.int64), rc)
     assert np.array_equal(ids, rids)
     assert dists.tobytes() == rd.tobytes()
+
+
+def _tc_cases():
+    rng = np.random.default_rng(2048)
+    out = []
+    for i in range(12):
+        n = int(rng.integers(100, 9000))
+        d = int(rng.choice([128, 132, 200, 256, 384, 520, 784, 1000, 1024]))
+        T = int(rng.integers(1, 24))
+        depth = int(rng.integers(1, max(2, min(8, int(np.log2(n))) + 1)))
+        v = int(rng.integers(1, min(T, 3) + 1))
+        k = int(rng.integers(1, 17))
+        kind = str(rng.choice(["ints", "nonneg", "dups", "shifted"]))
+        out.append((i, n, d, T, depth, v, k, kind))
+    return out
+
+
+@pytest.mark.parametrize("case", _tc_cases(), ids=lambda c: f"tc{c[0]}-n{c[1]}-d{c[2]}-k{c[6]}")
+def test_fuzz_tc_route(case):
+    """Seeded fuzz of the fused tcgen05 filter route (pinned): ragged row
+    tiles and query blocks (odd cluster pairs), every K-block count, k up to
+    its limit, signed (shifted) queries, duplicate masses."""
+    i, n, d, T, depth, v, k, kind = case
+    rng = np.random.default_rng(5000 + i)
+    nq = int(rng.integers(256, 900))
+    X = _data("nonneg" if kind == "shifted" else kind, rng, n + nq, d)
+    Xd, Q = X[:n], X[n:]
+    if kind == "shifted":
+        Q = Q - np.float32(0.1)
+    index = mrpt.grow_trees(Xd, T, depth, seed=i)
+    index.device_index().pin_route(k, v, "u8tc_bits")
+    ids, dists, counts = mrpt.approximate_knn_batch(Q, k, index, v)
+    ref = dict(matrices=[(R.col_ptr, R.row_idx, R.values) for R in index.matrices],
+               splits=index.splits, leaf_offsets=index.leaf_offsets,
+               leaf_indices=index.leaf_indices, depth=depth)
+    rids, rd, rc = O.approximate_knn_batch(Xd, Q, k, ref, v)
+    assert np.array_equal(counts.astype(np.int64), rc)
+    assert np.array_equal(ids, rids)
+    assert dists.tobytes() == rd.tobytes()
