@@ -9,29 +9,31 @@
 // 2.4 GB written + 2.4 GB read per 10k queries).  This kernel never
 // materialises D:
 //
-//   * a persistent CTA per SM walks a contiguous range of (query block,
-//     row tile) items: 128 queries x 256 rows;
-//   * the query block's quantised rows (A, s8, K-major, <= 7 x 128 B) are
-//     loaded once by TMA and stay resident in shared memory; row tiles of the
-//     s8 shadow (B) stream through a 3-stage TMA ring (128-B swizzle);
-//   * one thread issues tcgen05.mma.kind::i8 (s8 x s8 -> s32, M=128,
-//     N=256, K=32 per instruction) into a double-buffered TMEM accumulator
-//     (2 x 256 columns);
+//   * clusters of 2 persistent CTAs (one per SM) walk contiguous ranges of
+//     (pair of 128-query blocks, 256-row tile) items in lockstep;
+//   * a 4-stage TMA ring (128-B swizzle, 48 KB per stage) streams each
+//     CTA's query-block K block (A, s8, K-major) and the row tile's K block
+//     (B, the s8 shadow): each CTA loads half of B and multicasts it to both
+//     CTAs of the pair; a stage is refilled once both CTAs' MMAs committed it;
+//   * one thread issues tcgen05.mma.cta_group::1.kind::i8 (s8 x s8 -> s32,
+//     M=128, N=256, K=32 per instruction) into a double-buffered TMEM
+//     accumulator (2 x 256 columns);
 //   * 16 epilogue warps read the accumulator with tcgen05.ld (one TMEM lane
-//     = one query, 4 warps per lane quarter split the tile's columns) and
-//     apply the u8 filter's admission rule to every column whose bit is set
-//     in the query's candidate bitmap (K3's output): the same float32 bound
-//     (t1 + t2 - t3, eta, radius) as k_scan_topk_u8, against the query's
-//     running k-th upper bound kept in registers (sorted, k <= KT) and
-//     shared through shared memory between the query's 4 column warps;
-//   * admitted candidates go to a per-query entry list {L, U, id} in global
-//     memory (rare after warm-up); k_tc_select takes the k-th smallest U per
-//     query and hands the survivors (L <= U_k) to k_rerank, the exact float64
-//     re-rank every u8 route shares.
+//     = one query, 4 column-group warps per lane quarter) and run a 3-op
+//     pre-test (a superset of the u8 filter's admission rule) on every
+//     column; columns whose candidate bit (K3's bitmap, TMA-staged per tile)
+//     is set and that pass are admitted: their raw bound terms go to the
+//     query's entry list in global memory, and the query's k smallest upper
+//     bounds (shared in shared memory by its 4 column-group warps, across
+//     CTAs through a global atomicMin of the k-th) tighten the pre-test;
+//   * k_tc_select takes the k-th smallest upper bound from the union of the
+//     CTAs' k smallest and hands the survivors (L <= U_k) to k_rerank, the
+//     exact float64 re-rank every u8 route shares.
 //
-// D values are the same exact int32 dot products as the library GEMM's, so
-// the admitted sets are supersets of the exact top-k exactly as before and
-// the results are bit-identical to the reference's.
+// D values are the same exact int32 dot products as the library GEMM's
+// (MRPT_TC_DEBUG compares them element for element), so the admitted sets
+// are supersets of the exact top-k and the results are bit-identical to the
+// reference's.
 #pragma once
 #include <cuda.h>
 
