@@ -418,6 +418,23 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
           else
             tma_load_2d(st + kABytes, &tmB, fullB(s), kb * kKB, tile * kN);
         }
+      }
+      if (MC > 1) {
+        // both CTAs' last commits of every stage have arrived here before the
+        // cluster may exit (so the partner's commits into this CTA are done)
+        for (uint32_t gg = g > (uint32_t)kStages ? g - kStages : 0; gg < g; ++gg)
+          mbar_wait_sleep(emptyB((int)(gg % kStages)), (gg / kStages) & 1u);
+      }
+    } else if (lane == 1) {
+      // the tile's row records and candidate words, on their own thread: a
+      // buffer is refilled as soon as the epilogue released it, not after the
+      // row-tile loads of the item (which wait for the MMA)
+      int qb = (int)(it0 / a.ntiles) * MC + rank, tile = (int)(it0 % a.ntiles);
+      for (int64_t it = it0; it < it1; ++it, ++tile) {
+        if (tile == a.ntiles) {
+          tile = 0;
+          qb += MC;
+        }
         const uint32_t li = (uint32_t)(it - it0), b = li & 1u;
         mbar_wait_sleep(epiEmpty(b), ((li >> 1) & 1u) ^ 1u);
         const int64_t rows = a.n - (int64_t)tile * kN < kN ? a.n - (int64_t)tile * kN : kN;
@@ -427,12 +444,6 @@ __global__ void __launch_bounds__(threads_for<CG>(), 1)
         bulk_load(sInfo + b * kInfoBytes + kN * 16, a.rt1 + (int64_t)tile * kN, t1b, infoFull(b));
         // the block's candidate words for this tile: 128 queries x 8 words
         tma_load_2d(sBits + b * kBitsBytes, &tmC, infoFull(b), tile * (kN / 32), qb * kM);
-      }
-      if (MC > 1) {
-        // both CTAs' last commits of every stage have arrived here before the
-        // cluster may exit (so the partner's commits into this CTA are done)
-        for (uint32_t gg = g > (uint32_t)kStages ? g - kStages : 0; gg < g; ++gg)
-          mbar_wait_sleep(emptyB((int)(gg % kStages)), (gg / kStages) & 1u);
       }
     }
   } else if (warp == kMmaWarp) {
