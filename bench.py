@@ -47,8 +47,14 @@ def parse():
 
 
 def tensor_peak_i8():
-    """int8 tensor peak for the fused filter's roofline: 2x the measured dense
-    bf16 rate (MEASURED_PEAKS.json burst), else 2x the recipe's fallback."""
+    """int8 tensor peak for the fused filter's roofline: the int8 rate measured
+    on this pool's B200 (profiles/int8_peak.json, tools/int8_peak.py: cuBLASLt
+    IMMA 8192^3 burst), else 2x the measured dense bf16 rate."""
+    try:
+        pk = json.load(open(os.path.join(ROOT, "profiles", "int8_peak.json")))
+        return float(pk["int8_tops"]), "measured int8 (cuBLASLt 8192^3 burst, profiles/int8_peak.json)"
+    except Exception:
+        pass
     try:
         mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         return 2.0 * float(mp["bf16_tflops"]), "2x measured bf16 dense (int8 not measured)"
@@ -386,8 +392,8 @@ def run_ours(args):
     if variant == "u8tc_bits" and kt_n.value > 0:
         # the fused filter is a tensor-core kernel: int8 ops of the (query,
         # row) dot products it forms (2*nq*n*d per step), live CUDA-event
-        # duration of its launches; peak = 2x the measured dense bf16 rate
-        # (the nominal int8:bf16 ratio; int8 is not in MEASURED_PEAKS.json)
+        # duration of its launches; peak = the measured int8 rate of this
+        # pool's B200 (profiles/int8_peak.json)
         per_ms = kt_ms.value / kt_n.value
         launches_per_step = kt_n.value / steps
         ops = 2.0 * p["nq"] * D.n * p["d"] / launches_per_step
