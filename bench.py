@@ -319,14 +319,19 @@ def run_ours(args):
 
     # --- e2e through the public API: pinned host queries in, host results out ------
     Qpin = torch.from_numpy(Q).pin_memory()
-    for _ in range(2):
+    for _ in range(5):
         mrpt.approximate_knn_batch(Qpin, k, index, v)
     torch.cuda.synchronize()
+    # three runs of e2e_steps calls each, the median run reported: a host-side
+    # stall (the box's CPU is shared) in one run does not decide the number
     e2e_steps = max(3, min(args.steps, 10))
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        out = mrpt.approximate_knn_batch(Qpin, k, index, v)
-    e2e_s = (time.perf_counter() - t0)
+    runs = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            out = mrpt.approximate_knn_batch(Qpin, k, index, v)
+        runs.append(time.perf_counter() - t0)
+    e2e_s = float(np.median(runs))
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -458,7 +463,10 @@ def run_ours(args):
                               "DRAM bytes of the stage per call (profiles/traffic_*.json)")},
         "stage_ms_per_step": {k2: v2 / steps for k2, v2 in stage_ms.items()},
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h)},
+                "d2h_bytes_per_step": int(d2h),
+                "method": f"approximate_knn_batch on pinned host queries, wall clock; median of 3 runs "
+                          f"of {e2e_steps} calls (run means: "
+                          + ", ".join(f"{p['nq'] * e2e_steps / r:.0f}" for r in runs) + " queries/s)"},
         "gpu_launches": int(launches),
     }
     if args.sweep:
