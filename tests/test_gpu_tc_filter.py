@@ -124,3 +124,24 @@ def test_tc_dot_products_equal_library_gemm(tmp_path):
     lines = [l for l in r.stderr.splitlines() if "D mismatches=" in l]
     assert len(lines) >= 2
     assert all("D mismatches=0 " in l for l in lines), lines
+
+
+def test_tc_route_several_query_chunks(rng):
+    """More queries than one fused-filter chunk (16384): the per-chunk
+    bookkeeping (entry lists, shared bounds, bound lists) is reset and
+    offset per chunk; answers equal the oracle's."""
+    import torch
+
+    from paper_1509_06957_b200.search import query_device
+
+    n, d, nq, k, v = 1500, 128, 20000, 5, 1
+    X = _data("ints", rng, n + nq, d)
+    Xd, Q = X[:n], X[n:]
+    index = mrpt.grow_trees(Xd, 4, 4, seed=17)
+    D = index.device_index()
+    D.pin_route(k, v, "u8tc_bits")
+    ids, dists, counts = (t.cpu().numpy() for t in query_device(D, torch.from_numpy(Q).cuda(), k, v))
+    rids, rd, rc = _oracle(index, Xd, Q, k, v)
+    assert np.array_equal(counts.astype(np.int64), rc)
+    assert np.array_equal(ids, rids)
+    assert dists.tobytes() == rd.tobytes()
