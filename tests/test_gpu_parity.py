@@ -259,6 +259,33 @@ def _vote_lists(index, Q, v):
     return lists, c
 
 
+@pytest.mark.parametrize("T,depth,n,votes", [(12, 7, 260_000, (2, 3)),      # fewer trees than warps, u8
+                                             (300, 6, 200_000, (1, 2, 9)),  # ranged warps, 10-bit counters
+                                             (1000, 9, 150_000, (3, 10)),   # ranged, 31-32 trees per warp
+                                             (1100, 5, 140_000, (2, 40))])  # 32-tree groups, u16
+def test_vote_multi_tile_matches_oracle(rng, monkeypatch, T, depth, n, votes):
+    """Several id tiles (fewer trees than warps, ranged warps, 32-tree
+    groups; u8 / 10-bit / u16 counters): the directory-driven vote gives the
+    oracle's candidate counts, neighbour ids and distances."""
+    X = gaussian(rng, n + 40, 5)
+    Xd, Q = X[:n], X[n:]
+    index = mrpt.grow_trees(Xd, T, depth, seed=6)
+    D = index.device_index()
+    assert D.vote_dir() is not None and D.vote_dir().numel() > 0
+    ref = dict(matrices=[(R.col_ptr, R.row_idx, R.values) for R in index.matrices],
+               splits=index.splits, leaf_offsets=index.leaf_offsets,
+               leaf_indices=index.leaf_indices, depth=depth)
+    monkeypatch.setenv("MRPT_VOTE_UNION", "0")
+    for v in votes:
+        got, gc = _vote_lists(index, Q, v)
+        ids, dists, counts = mrpt.approximate_knn_batch(Q, 10, index, v)
+        rids, rd, rc = O.approximate_knn_batch(Xd, Q, 10, ref, v)
+        assert np.array_equal(gc.astype(np.int64), rc)
+        assert np.array_equal(counts.astype(np.int64), rc)
+        assert np.array_equal(ids, rids)
+        assert dists.tobytes() == rd.tobytes()
+
+
 @pytest.mark.parametrize("T,depth,n,shuffle", [(40, 6, 20_000, False), (1100, 5, 3_000, False),
                                                (600, 6, 30_000, True), (6, 10, 900_000, False)])
 def test_vote_union_v1_matches_counting_path(rng, monkeypatch, T, depth, n, shuffle):
