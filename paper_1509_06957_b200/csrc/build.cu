@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // K5: level-synchronous random-projection-tree construction for a batch of
 // trees (replaces build_tree / median_split, pkg/src/mrpt/trees.py:33-98).
 //
@@ -411,6 +412,40 @@ __global__ void k_big_init(LevelArgs a) {
   }
 }
 
+// Calls f(key) for every element of kb[p0, p1) (one chunk, <= kChunk
+// elements): the 16-byte-aligned body as uint4 loads, all of a thread's
+// loads issued before any key is used (one memory round trip per chunk);
+// the unaligned head and tail (< 4 elements each) element-wise.
+template <typename F>
+__device__ __forceinline__ void for_chunk_keys(const uint32_t *__restrict__ kb, int64_t p0, int64_t p1, F f) {
+  const int64_t mis = (int64_t)(((uintptr_t)(kb + p0) >> 2) & 3);
+  int64_t a0 = p0 + ((4 - mis) & 3);
+  if (a0 > p1) a0 = p1;
+  const int64_t a1 = a0 + ((p1 - a0) & ~3LL);
+  if (p0 + threadIdx.x < a0) f(__ldg(kb + p0 + threadIdx.x));
+  if (a1 + threadIdx.x < p1) f(__ldg(kb + a1 + threadIdx.x));
+  const uint4 *k4 = reinterpret_cast<const uint4 *>(kb + a0);
+  const int nv = (int)((a1 - a0) >> 2);
+  constexpr int U = kChunk / 4 / kNT;
+  for (int v0 = threadIdx.x; v0 < nv; v0 += U * kNT) {
+    uint4 r[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int i = v0 + j * kNT;
+      r[j] = i < nv ? __ldg(k4 + i) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      if (v0 + j * kNT < nv) {
+        f(r[j].x);
+        f(r[j].y);
+        f(r[j].z);
+        f(r[j].w);
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kNT) k_big_hist(LevelArgs a) {
   __shared__ uint32_t hist[256];
   const int64_t nch = a.ctl->nchunks;
@@ -428,20 +463,9 @@ __global__ void __launch_bounds__(kNT) k_big_hist(LevelArgs a) {
     const uint32_t *kb = a.keys + (int64_t)g->t * a.n;
     hist[threadIdx.x] = 0u;
     __syncthreads();
-    constexpr int U = 8;
-    for (int64_t r0 = p0 + threadIdx.x; r0 < p1; r0 += (int64_t)U * kNT) {
-      uint32_t kk[U];
-#pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const int64_t p = r0 + (int64_t)j * kNT;
-        kk[j] = p < p1 ? __ldg(kb + p) : 0u;
-      }
-#pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const int64_t p = r0 + (int64_t)j * kNT;
-        if (p < p1 && prefix_match(kk[j], prefix, nb)) atomicAdd(&hist[(kk[j] >> shift) & dmask], 1u);
-      }
-    }
+    for_chunk_keys(kb, p0, p1, [&](uint32_t k) {
+      if (prefix_match(k, prefix, nb)) atomicAdd(&hist[(k >> shift) & dmask], 1u);
+    });
     __syncthreads();
     const uint32_t v = hist[threadIdx.x];
     if (v) atomicAdd(a.ghist + (int64_t)ch.x * 256 + threadIdx.x, v);
@@ -490,20 +514,7 @@ __global__ void __launch_bounds__(kNT) k_big_count(LevelArgs a) {
     const int64_t p1 = (p0 + kChunk) < g->e ? (p0 + kChunk) : g->e;
     const uint32_t *kb = a.keys + (int64_t)g->t * a.n;
     int cnt = 0;
-    constexpr int U = 8;
-    for (int64_t r0 = p0 + threadIdx.x; r0 < p1; r0 += (int64_t)U * kNT) {
-      uint32_t kk[U];
-#pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const int64_t p = r0 + (int64_t)j * kNT;
-        kk[j] = p < p1 ? __ldg(kb + p) : 0xffffffffu;
-      }
-#pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const int64_t p = r0 + (int64_t)j * kNT;
-        cnt += (p < p1 && kk[j] <= K) ? 1 : 0;
-      }
-    }
+    for_chunk_keys(kb, p0, p1, [&](uint32_t k) { cnt += k <= K ? 1 : 0; });
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cnt;
@@ -545,7 +556,9 @@ __global__ void k_big_scan(LevelArgs a) {
 }
 
 __global__ void __launch_bounds__(kNT) k_big_scatter(LevelArgs a) {
-  constexpr int SR = 4;  // sub-rounds of kNT elements per barrier pair
+  // sub-rounds of kNT elements per barrier pair (8 or 16 measured slower:
+  // 140 / 242 registers leave one CTA per SM)
+  constexpr int SR = 4;
   constexpr int NW = kNT / 32;
   __shared__ int wcnt[SR][NW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -729,7 +742,12 @@ extern "C" int32_t mrpt_build_levels(const float *P, int64_t n, int32_t Tb, int3
     if (est > kMidMax || lev > 0) {
       // the big path may have work whenever a segment can exceed kMidMax;
       // after level 0 ties can make any segment large, so always launch.
-      const int big_grid = sms * 4;
+      static const int big_per_sm = [] {
+        const char *e = getenv("MRPT_BUILD_CTAS_PER_SM");  // experiments
+        const int v = e ? atoi(e) : 4;
+        return v < 1 ? 1 : (v > 8 ? 8 : v);
+      }();
+      const int big_grid = sms * big_per_sm;
       (count_launch(), k_chunk_layout<<<1, 1024, 0, s>>>(a));
       (count_launch(), k_chunk_fill<<<sms * 2, 256, 0, s>>>(a));
       (count_launch(), k_big_keys<<<big_grid, kNT, 0, s>>>(a));

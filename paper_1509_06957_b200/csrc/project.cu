@@ -213,9 +213,18 @@ extern "C" int32_t mrpt_project(const float *X, int64_t m, int32_t d, int64_t ld
     per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
     const int64_t cap = (int64_t)num_sms() * per_sm;
     const int grid = (int)(tiles < cap ? tiles : cap);
-    cudaFuncSetAttribute(k_project_smem<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    (count_launch(), k_project_smem<2><<<grid, 256, smem, s>>>(X, m, d, ldx, col_ptr, rows, vals, ncols, out,
-                                               out_row_stride, out_col_stride, tp, stride));
+    // points per thread: each CSC entry (two warp-uniform loads and a
+    // conversion) is shared by PPT independent fp64 chains
+    const char *pe = getenv("MRPT_PROJ_PPT");
+    int ppt = pe ? atoi(pe) : 4;
+    if (ppt != 2 && ppt != 4 && ppt != 8) ppt = 2;
+    while (ppt > 2 && tp / ppt < 8) ppt >>= 1;  // >= 8 consecutive points per column write
+    void (*fn)(const float *, int64_t, int, int64_t, const int64_t *, const int32_t *, const float *, int,
+               float *, int64_t, int64_t, int, int) =
+        ppt == 8 ? k_project_smem<8> : (ppt == 4 ? k_project_smem<4> : k_project_smem<2>);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    (count_launch(), fn<<<grid, 256, smem, s>>>(X, m, d, ldx, col_ptr, rows, vals, ncols, out,
+                                                out_row_stride, out_col_stride, tp, stride));
   } else if (32 * row_bytes <= 200 * 1024) {
     tp = 32;
     const size_t smem = (size_t)tp * row_bytes;

@@ -84,9 +84,13 @@ def test_config1_full_matches_reference():
 
 
 # --- kernel-level differential tests against the oracle -----------------------
+@pytest.mark.parametrize("ppt", ["2", "4", "8"])
 @pytest.mark.parametrize("n,d,depth,a", [(777, 48, 6, 0.25), (3000, 784, 8, 1 / 28),
-                                         (200, 1100, 5, 0.05), (5, 3000, 4, 0.01)])
-def test_projection_bit_identical(rng, n, d, depth, a):
+                                         (200, 1100, 5, 0.05), (5, 3000, 4, 0.01),
+                                         (1000, 256, 13, 1 / 16), (2049, 128, 11, 0.09)])
+def test_projection_bit_identical(rng, monkeypatch, n, d, depth, a, ppt):
+    """K1 with 2, 4 or 8 points per thread is bit-identical to _cy.project."""
+    monkeypatch.setenv("MRPT_PROJ_PPT", ppt)
     X = gaussian(rng, n, d)
     R = mrpt.sample_sparse_matrix(d, depth, a, seed=(3, 1))
     P = mrpt.project_dataset(X, R)
