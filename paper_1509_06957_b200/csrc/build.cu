@@ -473,6 +473,90 @@ __global__ void __launch_bounds__(kNT) k_big_hist(LevelArgs a) {
   }
 }
 
+// Stable partition of one chunk with 16-byte loads: thread i of a round
+// owns the four consecutive positions of 16-byte group i (groups aligned on
+// the address, positions outside [p0, p1) masked), so positions are in
+// thread order and a warp scan of the per-thread left counts gives every
+// element's rank -- the same ranks as the element-wise k_big_scatter.
+__global__ void __launch_bounds__(kNT) k_big_scatter4(LevelArgs a) {
+  constexpr int NW = kNT / 32;
+  constexpr int SR = 2;  // rounds of kNT groups per barrier pair
+  __shared__ int wcnt[SR][NW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nch = a.ctl->nchunks;
+  for (int64_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    const int2 ch = a.chunks[c];
+    const BigSeg *g = a.big + ch.x;
+    const uint32_t K = g->prefix;
+    const int64_t b = g->b;
+    const int64_t p0 = b + (int64_t)ch.y * kChunk;
+    const int64_t p1 = (p0 + kChunk) < g->e ? (p0 + kChunk) : g->e;
+    const int64_t nle = g->nle;
+    const uint32_t *kb = a.keys + (int64_t)g->t * a.n;
+    const int32_t *oin = a.order_in + (int64_t)g->t * a.n;
+    int32_t *oout = a.order_out + (int64_t)g->t * a.n;
+    const int64_t pa = p0 - (int64_t)(((uintptr_t)(kb + p0) >> 2) & 3);  // first group's position
+    int64_t base_left = a.chunk_off[c];
+    for (int64_t r0 = pa; r0 < p1; r0 += (int64_t)SR * kNT * 4) {
+      uint4 kk[SR];
+      int4 id[SR];
+      int fl[SR], cl[SR], incl[SR];
+#pragma unroll
+      for (int j = 0; j < SR; ++j) {
+        const int64_t q = r0 + ((int64_t)j * kNT + threadIdx.x) * 4;  // group start position
+        const bool any = q < p1;
+        kk[j] = any ? __ldg(reinterpret_cast<const uint4 *>(kb + q)) : make_uint4(0u, 0u, 0u, 0u);
+        id[j] = any ? __ldg(reinterpret_cast<const int4 *>(oin + q)) : make_int4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int j = 0; j < SR; ++j) {
+        const int64_t q = r0 + ((int64_t)j * kNT + threadIdx.x) * 4;
+        const uint32_t kv[4] = {kk[j].x, kk[j].y, kk[j].z, kk[j].w};
+        int f = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (q + e >= p0 && q + e < p1 && kv[e] <= K) f |= 1 << e;
+        fl[j] = f;
+        cl[j] = __popc(f);
+        int x = cl[j];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += u;
+        }
+        incl[j] = x;
+        if (lane == 31) wcnt[j][warp] = x;
+      }
+      __syncthreads();
+      int tot = 0;
+#pragma unroll
+      for (int j = 0; j < SR; ++j) {
+        int bj = tot;
+#pragma unroll
+        for (int w2 = 0; w2 < NW; ++w2) {
+          const int cc = wcnt[j][w2];
+          bj += w2 < warp ? cc : 0;
+          tot += cc;
+        }
+        const int64_t q = r0 + ((int64_t)j * kNT + threadIdx.x) * 4;
+        int64_t lrank = base_left + bj + incl[j] - cl[j];
+        const int iv[4] = {id[j].x, id[j].y, id[j].z, id[j].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int64_t p = q + e;
+          if (p >= p0 && p < p1) {
+            const bool left = (fl[j] >> e) & 1;
+            oout[left ? b + lrank : b + nle + ((p - b) - lrank)] = iv[e];
+            lrank += left ? 1 : 0;
+          }
+        }
+      }
+      base_left += tot;
+      __syncthreads();
+    }
+  }
+}
+
 // One warp per big segment.
 __global__ void k_big_pick(LevelArgs a) {
   const int nbig = a.ctl->nbig;
@@ -758,7 +842,14 @@ extern "C" int32_t mrpt_build_levels(const float *P, int64_t n, int32_t Tb, int3
       }
       (count_launch(), k_big_count<<<big_grid, kNT, 0, s>>>(a));
       (count_launch(), k_big_scan<<<sms, 256, 0, s>>>(a));
-      (count_launch(), k_big_scatter<<<big_grid, kNT, 0, s>>>(a));
+      static const bool scatter4 = [] {
+        const char *e = getenv("MRPT_BUILD_SCATTER4");  // "0": the element-wise scatter
+        return !(e && atoi(e) == 0);
+      }();
+      if (scatter4 && (((uintptr_t)a.keys | (uintptr_t)a.order_in) & 15) == 0)
+        (count_launch(), k_big_scatter4<<<big_grid, kNT, 0, s>>>(a));
+      else
+        (count_launch(), k_big_scatter<<<big_grid, kNT, 0, s>>>(a));
     }
   }
   return launch_status("mrpt_build_levels");
