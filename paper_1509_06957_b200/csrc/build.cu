@@ -819,9 +819,16 @@ extern "C" int32_t mrpt_build_levels(const float *P, int64_t n, int32_t Tb, int3
     // expected per-segment size decides how many CTAs the small paths get
     const int64_t est = n >> lev;
     const int64_t tiny_grid = nsegs < (int64_t)sms * 8 ? nsegs : (int64_t)sms * 8;
-    (count_launch(), k_seg_small<kTinyMax><<<(unsigned)(est <= kTinyMax ? tiny_grid : (tiny_grid < sms ? tiny_grid : sms)),
+    // one CTA per segment for the same L2 locality of the projection gathers
+    static const bool small_flat = [] {
+      const char *e = getenv("MRPT_BUILD_SMALL_FLAT");  // "0": grid-stride loop
+      return !(e && atoi(e) == 0);
+    }();
+    const unsigned flat_grid = (unsigned)(nsegs < 0x7fffffff ? nsegs : 0x7fffffff);
+    (count_launch(), k_seg_small<kTinyMax><<<small_flat ? flat_grid
+                                                        : (unsigned)(est <= kTinyMax ? tiny_grid : (tiny_grid < sms ? tiny_grid : sms)),
                              kNT, kTinyMax * 8, s>>>(a, 0));
-    const int64_t mid_grid = nsegs < (int64_t)sms * 3 ? nsegs : (int64_t)sms * 3;
+    const int64_t mid_grid = small_flat ? (int64_t)flat_grid : (nsegs < (int64_t)sms * 3 ? nsegs : (int64_t)sms * 3);
     (count_launch(), k_seg_small<kMidMax><<<(unsigned)mid_grid, kNT, kMidMax * 8, s>>>(a, 1));
     if (est > kMidMax || lev > 0) {
       // the big path may have work whenever a segment can exceed kMidMax;
@@ -834,7 +841,20 @@ extern "C" int32_t mrpt_build_levels(const float *P, int64_t n, int32_t Tb, int3
       const int big_grid = sms * big_per_sm;
       (count_launch(), k_chunk_layout<<<1, 1024, 0, s>>>(a));
       (count_launch(), k_chunk_fill<<<sms * 2, 256, 0, s>>>(a));
-      (count_launch(), k_big_keys<<<big_grid, kNT, 0, s>>>(a));
+      // The gather P[t][lev][order[i]] re-reads a tree's projection column
+      // once per segment; with one CTA per chunk (in-order dispatch keeps the
+      // resident chunks within about one tree) those re-reads hit L2 -- a
+      // grid-stride loop let CTAs drift over several trees and read DRAM ~2x
+      // (config 5 half scale: 1099 -> 602 GB, 229 -> 155 ms).
+      static const bool keys_flat = [] {
+        const char *e = getenv("MRPT_BUILD_KEYS_FLAT");  // "0": grid-stride loop
+        return !(e && atoi(e) == 0);
+      }();
+      // chunk count bound (device-side count unknown here): big segments hold
+      // > kChunk points each, so chunks <= 2 * n * Tb / kChunk
+      const int64_t chunk_bound = 2 * ceil_div<int64_t>(a.n * (int64_t)a.Tb, kChunk);
+      const int keys_grid = keys_flat ? (int)(chunk_bound < 0x7fffffff ? chunk_bound : 0x7fffffff) : big_grid;
+      (count_launch(), k_big_keys<<<keys_grid, kNT, 0, s>>>(a));
       (count_launch(), k_big_init<<<ceil_div<int>(sms, 1), 256, 0, s>>>(a));
       for (int pass = 0; pass < 4; ++pass) {
         (count_launch(), k_big_hist<<<big_grid, kNT, 0, s>>>(a));
