@@ -295,7 +295,7 @@ __global__ void k_build_dir(const int32_t *__restrict__ leaf_indices,
 // collects the slice starts inside the window, and the running count of
 // slice starts plus a popcount gives the slice's rank among the non-empty
 // slices, looked up in a 32-entry per-warp table.
-template <int CW, int NT>
+template <int CW, int NT, bool OFF32 = false>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_vote_dir(VoteArgs a) {
   extern __shared__ uint4 vote_smem[];
   uint32_t *cnt = reinterpret_cast<uint32_t *>(vote_smem);
@@ -309,7 +309,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_vote_dir(VoteArgs a) {
   __shared__ int32_t wlist[kWList];
   __shared__ int s_nw, s_nc;
   constexpr int NW = NT / 32;
-  __shared__ long long w_base[NW][32];  // per warp: global index of each non-empty slice (by rank)
+  // per warp: where each non-empty slice (by rank) starts -- a global index,
+  // or (OFF32, 32 * n < 2^31) an offset from the warp's first tree's row
+  __shared__ long long w_base[NW][OFF32 ? 1 : 32];
+  __shared__ int32_t w_off[NW][OFF32 ? 32 : 1];
   __shared__ int w_pre[NW][32];         // per warp: flat start of each non-empty slice (by rank)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ngroups = (a.T + 31) >> 5;
@@ -360,6 +363,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_vote_dir(VoteArgs a) {
         const int t_lo = ranged ? (int)(((int64_t)vw * a.T) / NW) : g * 32;
         const int t_hi = ranged ? (int)(((int64_t)(vw + 1) * a.T) / NW) : (g * 32 + 32 < a.T ? g * 32 + 32 : a.T);
         const int t = t_lo + lane;
+        const int32_t *wrow = a.leaf_indices + (int64_t)t_lo * a.n;  // OFF32 origin
         int len = 0;
         long long base = 0;
         if (t < t_hi) {
@@ -373,7 +377,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_vote_dir(VoteArgs a) {
             s1 = d[1];
           }
           len = s1 - s0;
-          base = (long long)t * a.n + sbase[t] + s0;
+          base = OFF32 ? (long long)(t - t_lo) * a.n + sbase[t] + s0 : (long long)t * a.n + sbase[t] + s0;
         }
         int pre = len;
 #pragma unroll
@@ -388,7 +392,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_vote_dir(VoteArgs a) {
         __syncwarp();
         if (len > 0) {
           const int r = __popc(ne & lanemask_lt());
-          w_base[warp][r] = base;
+          if (OFF32)
+            w_off[warp][r] = (int32_t)base;
+          else
+            w_base[warp][r] = base;
           w_pre[warp][r] = pre;
         }
         __syncwarp();
@@ -408,9 +415,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_vote_dir(VoteArgs a) {
             const int rank = before + __popc(starts & (0xffffffffu >> (31 - lane))) - 1;
             id[u] = -1;
             if (e < total) {
-              const long long bk = w_base[warp][rank];
               const int pk = w_pre[warp][rank];
-              id[u] = __ldg(a.leaf_indices + bk + (e - pk));
+              if (OFF32)
+                id[u] = __ldg(wrow + (w_off[warp][rank] + (e - pk)));
+              else
+                id[u] = __ldg(a.leaf_indices + w_base[warp][rank] + (e - pk));
             }
           }
 #pragma unroll
@@ -929,6 +938,11 @@ static int32_t vote_impl(const int32_t *leaf_indices, const int64_t *leaf_offset
     if (nt == 512)
       fn = CW == 1 ? k_vote_dir<1, 512>
                    : (CW == 2 ? k_vote_dir<2, 512> : (CW == 3 ? k_vote_dir<3, 512> : k_vote_dir<4, 512>));
+    else if (n * 32 < (1LL << 31) && !(getenv("MRPT_VOTE_OFF32") && atoi(getenv("MRPT_VOTE_OFF32")) == 0))
+      // 32-bit slice offsets from each warp's first tree (<= 32 trees per warp)
+      fn = CW == 1 ? k_vote_dir<1, 1024, true>
+                   : (CW == 2 ? k_vote_dir<2, 1024, true>
+                              : (CW == 3 ? k_vote_dir<3, 1024, true> : k_vote_dir<4, 1024, true>));
     else
       fn = CW == 1 ? k_vote_dir<1, 1024>
                    : (CW == 2 ? k_vote_dir<2, 1024> : (CW == 3 ? k_vote_dir<3, 1024> : k_vote_dir<4, 1024>));
