@@ -1,10 +1,14 @@
-"""Benchmark: batched MRPT k-NN queries on B200 (BASELINE.json metric).
+"""Benchmark: batched MRPT k-NN queries and index build on B200 (BASELINE.json metric).
 
 One step = one batched pass of the hot path (project+route K2 -> vote K3 ->
 exact scan+top-k K4) over the configuration's whole query batch, with the
-index and the queries resident in HBM.  Default workload: BASELINE config 2
-(configs[1], image-pixel-shaped, n=60k, d=784, 10k queries, T=100, l=8,
-k=10) at its highest-recall vote threshold.  Prints ONE JSON line on rank 0.
+index and the queries resident in HBM.  Default workload: BASELINE config 5
+(configs[4], the largest configuration that fits one B200: n=10M, d=256,
+100k queries, T=1000, l=13, a=1/16, k=100, v=10).  Prints ONE JSON line on
+rank 0 carrying, besides the contract keys, the index build time, recall@k
+against the package's exact ground truth, a ``parity`` block (oracle rebuilds
+of sampled trees, the unmodified reference's answers on a query sample) and
+the reference CPU baseline.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--votes V]
     python bench.py --impl reference ...   # the reference CPU package, same workload
@@ -19,7 +23,9 @@ import math
 import os
 import subprocess
 import sys
+import tempfile
 import time
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -29,6 +35,11 @@ sys.path.insert(0, ROOT)
 from paper_1509_06957_b200 import workloads  # noqa: E402
 
 PEAKS_FALLBACK_GBS = 6650.0
+METRIC = "queries/sec (approximate k-NN, batched queries)"
+# the reference arm builds its whole index when the build fits a few minutes
+# on the host; above this many (point, tree) pairs it builds 2 x cores trees
+# and extrapolates (trees are i.i.d. in cost, trees.py:217-224)
+REF_FULL_BUILD_MAX = 2.5e8
 
 
 def parse():
@@ -37,22 +48,33 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--votes", type=int, default=None)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--parity-trees", type=int, default=4)
+    ap.add_argument("--gt-queries", type=int, default=2000,
+                    help="ground-truth query sample above 2e10 (point, query) pairs")
     ap.add_argument("--sweep", action="store_true", help="also time every v of the config")
+    ap.add_argument("--export-index", default=None, help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return PEAKS_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
 def tensor_peak_i8():
-    """int8 tensor peak for the fused filter's roofline: the int8 rate measured
-    on this pool's B200 (profiles/int8_peak.json, tools/int8_peak.py: cuBLASLt
-    IMMA 8192^3 burst), else 2x the measured dense bf16 rate."""
+    """int8 tensor peak (side field of the fused-filter route): the rate measured
+    on this pool's B200 (profiles/int8_peak.json), else 2x the measured bf16."""
     try:
         pk = json.load(open(os.path.join(ROOT, "profiles", "int8_peak.json")))
-        return float(pk["int8_tops"]), "measured int8 (cuBLASLt 8192^3 burst, profiles/int8_peak.json)"
+        return float(pk["int8_tops"]), "measured int8 (profiles/int8_peak.json)"
     except Exception:
         pass
     try:
@@ -62,12 +84,15 @@ def tensor_peak_i8():
         return 2.0 * 1590.0, "2x fallback bf16 dense (B200_PROFILING.md)"
 
 
-def hbm_peak():
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            return float(json.load(fh)["hbm_gbs"]), "measured"
-    except Exception:
-        return PEAKS_FALLBACK_GBS, "fallback"
+def config_dict(p, v, world):
+    """The workload description both arms print (key-identical)."""
+    return {"workload": p["name"], "n": p["n"], "d": p["d"], "nq_per_gpu": p["nq"],
+            "n_trees": p["n_trees"], "depth": p["depth"], "k": p["k"], "votes": v,
+            "sparsity": p["sparsity"], "generator": p["generator"],
+            "l2": "device steps: L2 flushed between timed steps (256 MB write outside the step "
+                  "events); inputs far above L2 (X %.0f MB, leaf ids %.0f MB)" % (
+                      4.0 * p["n"] * p["d"] / 1e6, 4.0 * p["n_trees"] * p["n"] / 1e6),
+            "parallelism": f"replicated index, queries sharded by batch x{world}"}
 
 
 class Clocks:
@@ -130,36 +155,49 @@ _POOL_STATE = {}
 
 
 def _ref_worker(args):
+    """Reference approximate_knn, one query per call (evaluation.py:199-205);
+    returns the answers padded like the batch API, for the parity check."""
     lo, hi = args
     mrpt = _ref_import()
     st = _POOL_STATE
+    k = st["k"]
+    ids = np.full((hi - lo, k), -1, np.int64)
+    dists = np.full((hi - lo, k), np.inf)
+    cnt = np.zeros(hi - lo, np.int64)
     for i in range(lo, hi):
-        mrpt.approximate_knn(st["Q"][i], st["k"], st["index"], st["v"])
-    return hi - lo
+        r = mrpt.approximate_knn(st["Q"][i], k, st["index"], st["v"])
+        ids[i - lo, :len(r)] = r.indices
+        dists[i - lo, :len(r)] = r.distances
+        cnt[i - lo] = r.candidate_count
+    return lo, ids, dists, cnt
 
 
-def ref_query_rate(index, Q, k, v, seconds, cores):
-    """Reference approximate_knn (single query per call, search.py:175-184) over a
-    bounded query sample, one forked worker per core sharing the index."""
+def ref_query_rate(index, Q, k, v, seconds, cores, start=0):
+    """Reference approximate_knn over a bounded query sample (rows start..),
+    one forked worker per core sharing the index.  Returns
+    (qps, done, seconds, (ids, dists, counts) of the sampled rows)."""
     import multiprocessing as mp
 
     mrpt = _ref_import()
     t0 = time.perf_counter()
-    mrpt.approximate_knn(Q[0], k, index, v)
+    mrpt.approximate_knn(Q[start], k, index, v)
     one = max(1e-5, time.perf_counter() - t0)
-    sample = int(min(len(Q), max(cores, seconds / one * cores)))
+    sample = int(min(len(Q) - start, max(cores, seconds / one * cores)))
     _POOL_STATE.update(Q=Q, k=k, v=v, index=index)
-    bounds = np.linspace(0, sample, cores + 1).astype(int)
+    bounds = start + np.linspace(0, sample, cores + 1).astype(int)
     jobs = [(int(bounds[i]), int(bounds[i + 1])) for i in range(cores) if bounds[i + 1] > bounds[i]]
     ctx = mp.get_context("fork")
     with ctx.Pool(len(jobs)) as pool:
         t0 = time.perf_counter()
-        done = sum(pool.map(_ref_worker, jobs))
+        parts = pool.map(_ref_worker, jobs)
         dt = time.perf_counter() - t0
-    return done / dt, done, dt
+    parts.sort(key=lambda x: x[0])
+    ans = tuple(np.concatenate([p[j] for p in parts]) for j in (1, 2, 3))
+    return sample / dt, sample, dt, ans
 
 
 def ref_index_from_arrays(X, p, matrices, splits, offsets, indices, checksum):
+    """The reference's own MRPTIndex (trees.py:124-175) over given arrays."""
     mrpt = _ref_import()
     mats = [mrpt.SparseProjectionMatrix(d=R.d, depth=R.depth, a=R.a, seed=R.seed, col_ptr=R.col_ptr,
                                         row_idx=R.row_idx, values=R.values,
@@ -170,6 +208,53 @@ def ref_index_from_arrays(X, p, matrices, splits, offsets, indices, checksum):
                           dataset_checksum=checksum)
 
 
+def _export_index(args):
+    """Helper process of the reference arm (configs whose full reference build
+    does not fit the run): build the index with this repo's GPU path and write
+    splits / leaf offsets / leaf ids / checksum as .npy files into the
+    directory given, so the reference process (which never loads this
+    repo's library) can assemble the reference's own MRPTIndex over them."""
+    import torch
+
+    import paper_1509_06957_b200 as ours
+
+    torch.cuda.set_device(0)
+    X, _, p = workloads.generate(args.config, args.scale)
+    index = ours.grow_trees(torch.from_numpy(X).cuda(), p["n_trees"], p["depth"], p["sparsity"],
+                            seed=p["seed"])
+    out = args.export_index
+    D = index.device_index()
+    np.save(os.path.join(out, "splits.npy"), D.splits.cpu().numpy())
+    np.save(os.path.join(out, "leaf_offsets.npy"), D.offsets.cpu().numpy())
+    mm = np.lib.format.open_memmap(os.path.join(out, "leaf_indices.npy"), mode="w+", dtype=np.int32,
+                                   shape=(p["n_trees"], p["n"]))
+    step = max(1, (1 << 30) // (4 * p["n"]))
+    for t in range(0, p["n_trees"], step):
+        mm[t:t + step] = D.indices[t:t + step].cpu().numpy()
+    mm.flush()
+    del mm
+    with open(os.path.join(out, "checksum.json"), "w") as fh:
+        json.dump({"checksum": int(index.dataset_checksum)}, fh)
+
+
+def _ref_build_sample(mrpt, X, p, trees, cores):
+    """Time the reference's per-tree build (trees.py:217-224: sample_sparse_matrix,
+    project_dataset, build_tree) for trees 0..trees-1 on a pool of `cores`
+    threads; returns (seconds, splits, offsets, indices) of those trees."""
+    Xd = mrpt.Dataset(X)
+    out = [None] * trees
+
+    def one(t):
+        R = mrpt.sample_sparse_matrix(Xd.d, p["depth"], p["sparsity"], seed=(p["seed"], t))
+        P = mrpt.project_dataset(Xd, R)
+        out[t] = mrpt.build_tree(P, p["depth"])
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=min(cores, trees)) as pool:
+        list(pool.map(one, range(trees)))
+    return time.perf_counter() - t0, out
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -177,43 +262,115 @@ def run_reference(args):
     mrpt = _ref_import()
     X, Q, p = workloads.generate(args.config, args.scale)
     v = args.votes or p["headline_votes"]
+    k = p["k"]
     cores = len(os.sched_getaffinity(0))
-    t0 = time.perf_counter()
-    index = mrpt.grow_trees(X, p["n_trees"], p["depth"], p["sparsity"], seed=p["seed"],
-                            threads=cores)
-    build_s = time.perf_counter() - t0
+    full = p["n"] * p["n_trees"] <= REF_FULL_BUILD_MAX
+    build = {"cores": cores}
+    parity = {}
+    if full:
+        t0 = time.perf_counter()
+        index = mrpt.grow_trees(X, p["n_trees"], p["depth"], p["sparsity"], seed=p["seed"],
+                                threads=cores)
+        build_s = time.perf_counter() - t0
+        build.update(kind="full reference grow_trees (threads=cores), FNV checksum included")
+        index_note = "built by the reference's grow_trees in this run"
+    else:
+        # the reference's own per-tree build on 2 x cores trees, extrapolated
+        # linearly in T, plus its serial FNV checksum (trees.py:244) measured once
+        sample_trees = min(p["n_trees"], 2 * cores)
+        t_trees, built = _ref_build_sample(mrpt, X, p, sample_trees, cores)
+        t0 = time.perf_counter()
+        checksum = mrpt.Dataset(X).checksum
+        t_cs = time.perf_counter() - t0
+        build_s = t_trees * p["n_trees"] / sample_trees + t_cs
+        build.update(kind="extrapolated", trees_built=sample_trees, trees_s=t_trees,
+                     checksum_s=t_cs,
+                     formula="trees_s * n_trees / trees_built + checksum_s (trees i.i.d., "
+                             "trees.py:217-224)")
+        # the full index for the query measurement: exported by a helper
+        # process running this repo's GPU build; its trees are checked here
+        # against the reference's own trees built above
+        tmp_root = "/dev/shm" if os.path.isdir("/dev/shm") and \
+            os.statvfs("/dev/shm").f_bavail * os.statvfs("/dev/shm").f_frsize > \
+            4.4 * p["n"] * p["n_trees"] + (8 << 30) else None
+        with tempfile.TemporaryDirectory(dir=tmp_root) as tmp:
+            subprocess.check_call([sys.executable, os.path.abspath(__file__), "--config",
+                                   str(args.config), "--scale", str(args.scale), "--export-index", tmp],
+                                  env={k2: v2 for k2, v2 in os.environ.items()
+                                       if k2 not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")})
+            splits = np.load(os.path.join(tmp, "splits.npy"))
+            offsets = np.load(os.path.join(tmp, "leaf_offsets.npy"))
+            indices = np.load(os.path.join(tmp, "leaf_indices.npy"), mmap_mode="r")
+            exp_cs = json.load(open(os.path.join(tmp, "checksum.json")))["checksum"]
+            bad = 0
+            for t, (s_, o_, i_) in enumerate(built):
+                bad += int(s_.tobytes() != splits[t].tobytes() or not np.array_equal(o_, offsets[t])
+                           or not np.array_equal(i_, indices[t]))
+            parity = {"trees_checked": sample_trees, "tree_mismatches": bad,
+                      "checksum_match": bool(exp_cs == checksum)}
+            mats = [mrpt.sample_sparse_matrix(p["d"], p["depth"], p["sparsity"], seed=(p["seed"], t))
+                    for t in range(p["n_trees"])]
+            index = mrpt.MRPTIndex(dataset=mrpt.Dataset(X), n_trees=p["n_trees"], depth=p["depth"],
+                                   sparsity=p["sparsity"], seed=p["seed"], fixed_count=False,
+                                   matrices=mats, splits=splits, leaf_offsets=offsets,
+                                   leaf_indices=np.ascontiguousarray(indices),
+                                   dataset_checksum=checksum)
+        index_note = ("full index exported by a helper process running this repo's GPU build, "
+                      f"assembled with the reference's MRPTIndex; {parity['trees_checked']} of its "
+                      "trees rebuilt by the reference here (tree_mismatches)")
+    # each step: the reference answers a bounded sample of the queries on all
+    # cores; the step's own wall time is its ms_per_step
+    per_step = max(0.5, args.cpu_seconds / max(1, args.steps))
     for _ in range(args.warmup):
-        ref_query_rate(index, Q, p["k"], v, 1.0, cores)
-    rates = []
+        ref_query_rate(index, Q, k, v, min(per_step, 1.0), cores)
+    rates, times, done_all = [], [], 0
+    start = 0
     for _ in range(args.steps):
-        qps, done, dt = ref_query_rate(index, Q, p["k"], v, args.cpu_seconds / max(1, args.steps),
-                                       cores)
+        qps, done, dt, _ = ref_query_rate(index, Q, k, v, per_step, cores, start=start)
+        start = (start + done) % max(1, len(Q) - cores)
         rates.append(qps)
-    value = float(np.mean(rates))
+        times.append(dt)
+        done_all += done
+    value = float(done_all / sum(times))
     line = {
-        "impl": "reference", "metric": "queries/sec (approximate k-NN, batched queries)",
+        "impl": "reference", "metric": METRIC,
         "value": value, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1000.0 * p["nq"] / value, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": p["name"], "n": p["n"], "d": p["d"], "nq": p["nq"],
-                   "n_trees": p["n_trees"], "depth": p["depth"], "k": p["k"], "votes": v},
-        "build_s": build_s,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * float(np.mean(times)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(p, v, args.gpus),
+        "build_s": build_s, "build": build,
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "reference",
-                         "sample": f"reference mrpt.approximate_knn, one query per call, forked "
-                                   f"pool of {cores}, ~{args.cpu_seconds:.0f}s of queries per run"},
+                         "sample": f"each step: reference mrpt.approximate_knn, one query per call "
+                                   f"(evaluation.py:199-205), forked pool of {cores} for "
+                                   f"~{per_step:.1f}s; {done_all} queries over {args.steps} steps",
+                         "index": index_note},
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    if parity:
+        line["parity"] = parity
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------- ours
+def _stage_bytes(D, Qd, leaves_fn, counts, d):
+    """SURVEY 8(d) algorithmic bytes of the step: 4 B per leaf id streamed by
+    the vote (sum_t |L_t(q)|), 4*d B per candidate row (|S(q)|)."""
+    leaves = leaves_fn(Qd, D).long()
+    sizes = (D.offsets[:, 1:] - D.offsets[:, :-1])
+    touched = sizes.gather(1, leaves.t()).sum(0).double()
+    vote_bytes = float(4.0 * touched.sum().item())
+    scan_bytes = float(4.0 * d * counts.double().sum().item())
+    return vote_bytes, scan_bytes
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     import paper_1509_06957_b200 as mrpt
-    from paper_1509_06957_b200.search import query_device
+    from paper_1509_06957_b200 import _native as native
+    from paper_1509_06957_b200.search import _route_device, _size_class, query_device
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -240,61 +397,42 @@ def run_ours(args):
     else:
         index = mrpt.grow_trees(Xd, p["n_trees"], p["depth"], p["sparsity"], seed=p["seed"])
     torch.cuda.synchronize()
-    build_s = time.perf_counter() - t0  # includes the GPU FNV checksum
+    build_s = time.perf_counter() - t0  # includes the GPU FNV checksum (trees.py:244)
     D = index.device_index()
     Qd = torch.from_numpy(Q).cuda()
 
-    # --- per-query algorithmic bytes: 4*sum_t|L_t(q)| + 4*d*|S(q)| ---
+    # --- first pass: answers kept for recall / parity, per-query bytes --------------
     ids, dists, counts = query_device(D, Qd, k, v)
-    from paper_1509_06957_b200.search import _route_device
-
-    leaves = _route_device(Qd, D).long()
-    sizes = (D.offsets[:, 1:] - D.offsets[:, :-1])  # (T, nleaf)
-    touched = sizes.gather(1, leaves.t()).sum(0).double()  # (nq,)
-    cand = counts.double()
-    vote_bytes = float(4.0 * touched.sum().item())
-    scan_bytes = float(4.0 * p["d"] * cand.sum().item())
+    vote_bytes, scan_bytes = _stage_bytes(D, Qd, _route_device, counts, p["d"])
     torch.cuda.synchronize()
-
-    # --- stage timing hooks: events around each kernel, on the launching stream ---
     stage_ms = {"route": 0.0, "vote": 0.0, "scan_topk": 0.0}
 
-    def timed_step(events):
-        return query_device(D, Qd, k, v, timer=events)
-
-    # L2 is flushed between timed steps (a 2x-L2 write outside each step's events):
-    # within a step, the index and data rows are re-read by many queries, which is
-    # the workload; across steps nothing stays warm.  Warm-up runs the identical
-    # sequence (flush, events, stage timers) so no first-use cost lands in the
-    # timed region.
+    # L2 is flushed between timed steps (a 2x-L2 write outside each step's events);
+    # warm-up runs the identical sequence so no first-use cost lands in the timed region
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(args.warmup):
         flush.fill_(1)
-        w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        w0.record(stream)
-        timed_step([])
-        w1.record(stream)
+        query_device(D, Qd, k, v, timer=[])
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    evs = []
-    step_ev = []
-    from paper_1509_06957_b200 import _native as native
-
+    evs, step_ev = [], []
     lib = native.load()
+    from paper_1509_06957_b200.search import fallback_stats
+
+    fallback_stats(reset=True)
     launches0 = int(lib.mrpt_launch_count())
-    lib.mrpt_kernel_timer(1)  # events around the fused filter launches (roofline)
+    lib.mrpt_kernel_timer(1)  # events around the fused filter launches (side roofline)
     with Clocks(local) as clk:
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         for _ in range(args.steps):
             flush.fill_(1)
-            s0 = torch.cuda.Event(enable_timing=True)
-            s1 = torch.cuda.Event(enable_timing=True)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record(stream)
             ev = []
-            timed_step(ev)
+            query_device(D, Qd, k, v, timer=ev)
             s1.record(stream)
             evs.append(ev)
             step_ev.append((s0, s1))
@@ -306,6 +444,7 @@ def run_ours(args):
         for name, a, b in ev:
             stage_ms[name] += a.elapsed_time(b)
     launches = int(lib.mrpt_launch_count()) - launches0  # this library's kernels, timed steps only
+    fb = {r: x for r, x in fallback_stats().items() if x["queries"]}
     kt_ms, kt_n = ctypes.c_double(0.0), ctypes.c_int64(0)
     native.call("mrpt_kernel_timer_read", ctypes.byref(kt_ms), ctypes.byref(kt_n))
     lib.mrpt_kernel_timer(0)
@@ -319,12 +458,12 @@ def run_ours(args):
 
     # --- e2e through the public API: pinned host queries in, host results out ------
     Qpin = torch.from_numpy(Q).pin_memory()
-    for _ in range(5):
+    for _ in range(2 if p["nq"] >= 50_000 else 5):
         mrpt.approximate_knn_batch(Qpin, k, index, v)
     torch.cuda.synchronize()
-    # three runs of e2e_steps calls each, the median run reported: a host-side
-    # stall (the box's CPU is shared) in one run does not decide the number
-    e2e_steps = max(3, min(args.steps, 10))
+    # three runs, the median run reported: a host-side stall (the box's CPU is
+    # shared) in one run does not decide the number
+    e2e_steps = max(3, min(args.steps, 10 if p["nq"] < 50_000 else 4))
     runs = []
     for _ in range(3):
         t0 = time.perf_counter()
@@ -339,172 +478,96 @@ def run_ours(args):
     e2e_value = p["nq"] * e2e_steps * world / e2e_s
     h2d = Q.nbytes
     d2h = sum(np.asarray(o).nbytes for o in out)
+    e2e_ids = out[0]
 
-    # recall vs exact ground truth (brute force through the same exact kernel);
-    # above ~2e10 row-query pairs (config 5) on a fixed subsample of queries
-    n_gt = p["nq"] if p["n"] * p["nq"] <= 2e10 else max(100, int(2e10 // p["n"]))
-    gt_ids, _, _ = query_device_brute(D, Qd[:n_gt], k)
-    recall = float(np.mean([len(np.intersect1d(a[a >= 0], b)) / k
-                            for a, b in zip(ids[:n_gt].cpu().numpy(), gt_ids.cpu().numpy())]))
+    # --- recall@k against the package's exact ground truth (f3, bit-identical to
+    # the reference's brute_force_knn); a fixed query sample above 2e10 pairs ------
+    n_gt = p["nq"] if p["n"] * p["nq"] <= 2e10 else min(p["nq"], args.gt_queries)
+    t0 = time.perf_counter()
+    gt = mrpt.compute_ground_truth(index.dataset, Q[:n_gt], k)
+    gt_s = time.perf_counter() - t0
+    ids_h = ids.cpu().numpy()
+    dists_h = dists.cpu().numpy()
+    counts_h = counts.cpu().numpy()
+    recall = mrpt.recall_batch(ids_h[:n_gt], gt.indices)
 
-    # --- roofline of the dominant kernel (and of the vote+scan stage) -------------
+    # --- roofline: the dominant kernel (SURVEY 8(d) algorithmic bytes per launch
+    # / its event-timed launch duration) and the vote+scan stage ------------------
     peak, peak_kind = hbm_peak()
     steps = args.steps
-    per_launch = {}
-    nlaunch = stage_launches
-    for name in stage_ms:
-        per_launch[name] = stage_ms[name] / max(1, nlaunch[name])
+    per_launch = {name: stage_ms[name] / max(1, stage_launches[name]) for name in stage_ms}
     dominant = "scan_topk" if stage_ms["scan_topk"] >= stage_ms["vote"] else "vote"
-    dom_bytes = (scan_bytes if dominant == "scan_topk" else vote_bytes) / max(1, nlaunch[dominant] // steps)
+    dom_bytes = (scan_bytes if dominant == "scan_topk" else vote_bytes) / \
+        max(1, stage_launches[dominant] // steps)
     achieved = dom_bytes / (per_launch[dominant] / 1000.0) / 1e9
-    traffic = None
+    stage_s = (stage_ms["vote"] + stage_ms["scan_topk"]) / steps / 1000.0
+    stage_gbs = (vote_bytes + scan_bytes) / stage_s / 1e9
     tpath = os.path.join(ROOT, "profiles", f"traffic_config{args.config}_v{v}.json")
+    traffic = None
+    tr = {}
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(dominant)
+            tr = json.load(open(tpath))
+            traffic = tr.get(dominant + "_per_launch", tr.get(dominant))
         except Exception:
             traffic = None
-    # bytes the chosen filter variant actually reads per candidate (its row
-    # format + per-row side data + the candidate id); survivors reranked in fp32
-    # are not included
-    from paper_1509_06957_b200.search import _size_class
-
     variant = (D.scan_pin.get((k, v)) or D.scan_choice_by_size.get((k, v, _size_class(p["nq"])))
                or D.scan_choice.get((k, v), "fp32"))
-    if variant == "u8tc_bits":
-        # fused tcgen05 filter: no dot-product matrix; per candidate its bit
-        # (read once per (query, row)) and, per row tile, 16-B row records
-        row_b, filt_mb = 0, D.n * D.u8_rows()[1] / 1e6
-    elif variant.startswith("u8gemm"):
-        # per candidate: its dot product (4 B) + row record (16 B) (+ its id in
-        # list mode); per query: the GEMM's n dot products written and read
-        row_b, filt_mb = 16 if variant == "u8gemm_bits" else 20, D.n * D.u8_rows()[1] / 1e6
-    elif variant == "u8":
-        row_b, filt_mb = D.u8_rows()[1] + 12, D.n * D.u8_rows()[1] / 1e6
-    elif variant == "fp16":
-        row_b, filt_mb = 2 * D.shadow()[1] + 4, D.n * 2 * D.shadow()[1] / 1e6
-    else:
-        row_b, filt_mb = 4 * p["d"], X.nbytes / 1e6
-    filter_bytes = float(cand.sum().item()) * (row_b + 4)
-    if variant.startswith("u8gemm"):
-        filter_bytes += 8.0 * D.n * p["nq"]
-    if variant == "u8tc_bits":
-        filter_bytes = D.n * p["nq"] / 8.0 + 16.0 * D.n * math.ceil(p["nq"] / 128)
-    filter_gbs = filter_bytes / (stage_ms["scan_topk"] / steps / 1000.0) / 1e9
-    stage_gbs = (vote_bytes + scan_bytes) / ((stage_ms["vote"] + stage_ms["scan_topk"]) / steps / 1000.0) / 1e9
-
-    roof = None
+    roof = {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "bytes_per_launch": dom_bytes,
+            "kernel_ms_per_launch": per_launch[dominant],
+            "launches_per_step": stage_launches[dominant] / steps,
+            "stage_vote_plus_scan": {
+                "achieved_gbs": stage_gbs, "frac": stage_gbs / peak,
+                "frac_of_8000_nominal": stage_gbs / 8000.0,
+                "bytes_per_query": (vote_bytes + scan_bytes) / p["nq"],
+                "distance_only_frac": scan_bytes / (stage_ms["scan_topk"] / steps / 1000.0) / 1e9 / peak,
+                "measured_dram_bytes_per_step": tr.get("stage_bytes_per_step"),
+                "note": "SURVEY 8(d): B_q = 4*sum_t|L_t(q)| + 4*d*|S(q)| over the vote + exact-scan "
+                        "event time; measured_dram_bytes_per_step from ncu (profiles/traffic_*.json)"},
+            "scan_variant": variant,
+            "note": "achieved = SURVEY 8(d) algorithmic bytes of one launch (4 B per leaf id for the "
+                    "vote, 4*d B per candidate row for the scan) / its mean CUDA-event duration; "
+                    "traffic = ncu dram__bytes_read+write per launch"}
     if variant == "u8tc_bits" and kt_n.value > 0:
-        # the fused filter is a tensor-core kernel: int8 ops of the (query,
-        # row) dot products it forms (2*nq*n*d per step), live CUDA-event
-        # duration of its launches; peak = the measured int8 rate of this
-        # pool's B200 (profiles/int8_peak.json)
         per_ms = kt_ms.value / kt_n.value
-        launches_per_step = kt_n.value / steps
-        ops = 2.0 * p["nq"] * D.n * p["d"] / launches_per_step
-        tops = ops / (per_ms / 1000.0) / 1e12
+        ops = 2.0 * p["nq"] * D.n * p["d"] / (kt_n.value / steps)
         tpeak, tkind = tensor_peak_i8()
-        ttraffic = None
-        if os.path.exists(tpath):
-            try:
-                ttraffic = json.load(open(tpath)).get("k_tc_filter")
-            except Exception:
-                ttraffic = None
-        roof = {"bound": "tensor", "kernel": "k_tc_filter (fused tcgen05 int8 filter)",
-                "achieved": tops, "peak": tpeak, "peak_kind": tkind, "unit": "TOP/s",
-                "frac": tops / tpeak, "traffic": ttraffic,
-                "kernel_ms_per_launch": per_ms, "kernel_launches_per_step": launches_per_step,
-                "hbm_algorithmic": {"kernel": dominant, "achieved_gbs": achieved, "peak": peak,
-                                    "frac": achieved / peak,
-                                    "note": "SURVEY 8(d) algorithmic bytes (4*d B per candidate row) "
-                                            "over the scan stage; the fused filter never reads "
-                                            "float32 rows"},
-                "stage_vote_plus_scan_gbs": stage_gbs, "stage_frac": stage_gbs / peak,
-                "bytes_per_query": (vote_bytes + scan_bytes) / p["nq"], "scan_variant": variant,
-                "scan_filter_bytes_per_query": filter_bytes / p["nq"],
-                "note": ("ops = 2*nq*n*d int8 multiply-adds of the dot products the kernel forms "
-                         "(tcgen05.mma.kind::i8, K padded to 128-B blocks not counted); traffic "
-                         "= ncu DRAM bytes per launch (profiles/traffic_*.json)")}
+        useful = 2.0 * float(counts.double().sum().item()) * p["d"] / (kt_n.value / steps)
+        roof["int8_side"] = {"kernel": "k_tc_filter", "achieved_tops": ops / (per_ms / 1e3) / 1e12,
+                             "peak": tpeak, "peak_kind": tkind,
+                             "frac": ops / (per_ms / 1e3) / 1e12 / tpeak,
+                             "useful_op_fraction": useful / ops}
     line = {
-        "metric": "queries/sec (approximate k-NN, batched queries)",
+        "metric": METRIC,
         "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": p["name"], "n": p["n"], "d": p["d"], "nq_per_gpu": p["nq"],
-                   "n_trees": p["n_trees"], "depth": p["depth"], "k": k, "votes": v,
-                   "sparsity": p["sparsity"], "generator": p["generator"],
-                   "l2": "L2 flushed between timed steps (256 MB write outside the step "
-                         "events); X %.0f MB, leaf ids %.0f MB, scan filter rows %.0f MB" % (
-                       X.nbytes / 1e6, 4.0 * p["n_trees"] * p["n"] / 1e6, filt_mb),
-                   "parallelism": f"replicated index, queries sharded by batch x{world}"},
+        "config": config_dict(p, v, world),
         "recall_at_k": recall,
         "recall_queries": n_gt,
-        "mean_candidates": float(cand.mean().item()),
+        "ground_truth_s": gt_s,
+        "mean_candidates": float(counts.double().mean().item()),
         "build_s": build_s,
-        "roofline": roof if roof is not None else {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic,
-                     "stage_vote_plus_scan_gbs": stage_gbs,
-                     "stage_frac": stage_gbs / peak,
-                     "bytes_per_query": (vote_bytes + scan_bytes) / p["nq"],
-                     "scan_variant": variant,
-                     "scan_filter_bytes_per_query": filter_bytes / p["nq"],
-                     "scan_filter_gbs": filter_gbs,
-                     "note": ("achieved/frac use SURVEY 8(d) algorithmic bytes (4 B per leaf id "
-                              "+ 4*d B per candidate row); frac > 1 is possible because the "
-                              "exact scan does not read float32 candidate rows: " + (
-                                  "an int8 tensor-core GEMM forms every (query, row) dot "
-                                  "product on the u8 shadow (written and read once, 4 B each) "
-                                  "and the filter reads a 16-B record per candidate"
-                                  if variant.startswith("u8gemm") else
-                                  "it filters on %s rows (%d B/candidate), L2-resident within "
-                                  "a step" % (variant, row_b + 4)) +
-                              "; exact float64 re-rank of the survivors only; traffic = ncu "
-                              "DRAM bytes of the stage per call (profiles/traffic_*.json)")},
+        "roofline": roof,
         "stage_ms_per_step": {k2: v2 / steps for k2, v2 in stage_ms.items()},
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
                 "method": f"approximate_knn_batch on pinned host queries, wall clock; median of 3 runs "
                           f"of {e2e_steps} calls (run means: "
-                          + ", ".join(f"{p['nq'] * e2e_steps / r:.0f}" for r in runs) + " queries/s)"},
+                          + ", ".join(f"{p['nq'] * e2e_steps / r:.0f}" for r in runs) + " queries/s)",
+                "matches_device_pass": bool(np.array_equal(e2e_ids, ids_h))},
         "gpu_launches": int(launches),
+        "exact_fallbacks": fb,
     }
     if args.sweep:
-        sw = {}
-        for vv in p["votes"]:
-            for _ in range(2):
-                query_device(D, Qd, k, vv)
-            torch.cuda.synchronize()
-            # per-call events, median of 3 (robust to a stray host stall)
-            per = []
-            for _ in range(3):
-                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                s.record(stream)
-                r = query_device(D, Qd, k, vv)
-                e.record(stream)
-                torch.cuda.synchronize()
-                per.append(s.elapsed_time(e))
-            rc = float(np.mean([len(np.intersect1d(a[a >= 0], b)) / k
-                                for a, b in zip(r[0][:n_gt].cpu().numpy(), gt_ids.cpu().numpy())]))
-            sw[str(vv)] = {"qps": p["nq"] / (float(np.median(per)) / 1000.0), "recall": rc,
-                           "mean_candidates": float(r[2].double().mean().item())}
-        line["sweep"] = sw
-        # the same thresholds from one route + one counted vote (f4)
-        for _ in range(2):
-            mrpt.approximate_knn_sweep(Qd, k, index, p["votes"])
-        torch.cuda.synchronize()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record(stream)
-        for _ in range(3):
-            mrpt.approximate_knn_sweep(Qd, k, index, p["votes"])
-        e.record(stream)
-        torch.cuda.synchronize()
-        one = s.elapsed_time(e) / 3
-        line["sweep_one_pass"] = {
-            "votes": list(p["votes"]), "ms_all_thresholds": one,
-            "ms_sum_separate": sum(p["nq"] / x["qps"] * 1e3 for x in sw.values())}
+        line.update(_sweep(mrpt, query_device, D, Qd, index, p, k, gt, n_gt, stream))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args, X, Q, p, v, index)
+        base, parity = cpu_baseline_and_parity(args, X, Q, p, v, index, D, ids_h, dists_h, counts_h,
+                                               gt, n_gt, recall)
+        line["cpu_baseline"] = base
+        line["parity"] = parity
     line["clocks"] = clk.summary()
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -512,40 +575,97 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def query_device_brute(D, Qd, k):
-    """Exact k-NN over all points (cand == NULL mode of mrpt_scan_topk)."""
+def _sweep(mrpt, query_device, D, Qd, index, p, k, gt, n_gt, stream):
     import torch
 
-    from paper_1509_06957_b200 import _native
+    sw = {}
+    for vv in p["votes"]:
+        for _ in range(2):
+            query_device(D, Qd, k, vv)
+        torch.cuda.synchronize()
+        per = []
+        for _ in range(3):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            r = query_device(D, Qd, k, vv)
+            e.record(stream)
+            torch.cuda.synchronize()
+            per.append(s.elapsed_time(e))
+        sw[str(vv)] = {"qps": p["nq"] / (float(np.median(per)) / 1000.0),
+                       "recall": mrpt.recall_batch(r[0][:n_gt].cpu().numpy(), gt.indices),
+                       "mean_candidates": float(r[2].double().mean().item())}
+    for _ in range(2):
+        mrpt.approximate_knn_sweep(Qd, k, index, p["votes"])
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(3):
+        mrpt.approximate_knn_sweep(Qd, k, index, p["votes"])
+    e.record(stream)
+    torch.cuda.synchronize()
+    one = s.elapsed_time(e) / 3
+    return {"sweep": sw, "sweep_one_pass": {
+        "votes": list(p["votes"]), "ms_all_thresholds": one,
+        "ms_sum_separate": sum(p["nq"] / x["qps"] * 1e3 for x in sw.values())}}
 
-    nq = int(Qd.shape[0])
-    ids = torch.empty((nq, k), dtype=torch.int64, device=Qd.device)
-    dists = torch.empty((nq, k), dtype=torch.float64, device=Qd.device)
-    _native.call("mrpt_scan_topk", _native.ptr(D.X), D.n, D.d, int(D.X.stride(0)), _native.ptr(Qd),
-                 nq, int(Qd.stride(0)), None, 0, None, int(k), _native.ptr(ids),
-                 _native.ptr(dists), _native.stream_ptr())
-    return ids, dists, None
 
+def cpu_baseline_and_parity(args, X, Q, p, v, index, D, ids, dists, counts, gt, n_gt, recall):
+    """The unmodified reference (oracle/_ref) on the host cores over the
+    GPU-built index, on a bounded query sample -- the CPU baseline -- and the
+    parity checks of this run: the reference's answers on that sample against
+    ours (ids, float64 distance bytes, candidate counts), the oracle's rebuild
+    of sampled trees against the GPU-built trees, and recall from both."""
+    from oracle import oracle as O
 
-def cpu_baseline(args, X, Q, p, v, index):
-    """The unmodified reference (oracle/_ref) on the host cores, over the GPU-built
-    index (bit-identical to the reference's own build), bounded sample."""
+    out_base, parity = None, {}
+    # trees: the oracle rebuilds sampled trees (C restatement of trees.py:54-98)
+    T = p["n_trees"]
+    ts = sorted({int(round(x)) for x in np.linspace(0, T - 1, min(T, args.parity_trees))})
+
+    def check_tree(t):
+        R, (s_, o_, i_) = O.build_one_tree(X, p["depth"], p["sparsity"], p["seed"], t)
+        ok = (s_.tobytes() == D.splits[t].cpu().numpy().tobytes()
+              and np.array_equal(o_, D.offsets[t].cpu().numpy())
+              and np.array_equal(i_, D.indices[t].cpu().numpy()))
+        return int(not ok)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(len(ts)) as ex:
+        bad = sum(ex.map(check_tree, ts))
+    parity.update(trees_checked=ts, tree_mismatches=bad, tree_check_s=time.perf_counter() - t0)
     try:
         cores = len(os.sched_getaffinity(0))
         rindex = ref_index_from_arrays(X, p, index.matrices, index.splits, index.leaf_offsets,
                                        index.leaf_indices, index.dataset_checksum)
-        qps, done, dt = ref_query_rate(rindex, Q, p["k"], v, args.cpu_seconds, cores)
-        return {"value": qps, "unit": "queries/s", "cores": cores, "kind": "reference",
-                "sample": f"{done} queries of {p['name']} (v={v}) through reference "
-                          f"mrpt.approximate_knn, forked pool of {cores}, {dt:.1f}s"}
+        qps, done, dt, (rids, rdists, rcnt) = ref_query_rate(rindex, Q, p["k"], v, args.cpu_seconds,
+                                                             cores)
+        out_base = {"value": qps, "unit": "queries/s", "cores": cores, "kind": "reference",
+                    "sample": f"{done} queries of {p['name']} (v={v}) through reference "
+                              f"mrpt.approximate_knn, one query per call, forked pool of {cores}, "
+                              f"{dt:.1f}s, over the GPU-built index"}
+        m_ids = int((rids != ids[:done]).any(axis=1).sum())
+        m_d = int((rdists.view(np.uint64) != dists[:done].view(np.uint64)).any(axis=1).sum())
+        m_c = int((rcnt != counts[:done]).sum())
+        both = min(done, n_gt)
+        from paper_1509_06957_b200 import recall_batch
+
+        r_ref = recall_batch(rids[:both], gt.indices[:both])
+        r_ours = recall_batch(ids[:both], gt.indices[:both])
+        parity.update(queries=done, mismatches={"ids": m_ids, "dist_bytes": m_d, "counts": m_c},
+                      recall_ours=r_ours, recall_reference=r_ref, recall_queries=both,
+                      recall_abs_diff=abs(r_ours - r_ref),
+                      recall_within_0_001=bool(abs(r_ours - r_ref) <= 1e-3))
     except Exception as exc:  # the baseline is reported, never required
-        return {"value": None, "unit": "queries/s", "cores": None, "kind": "reference",
-                "sample": f"unavailable: {exc}"}
+        out_base = {"value": None, "unit": "queries/s", "cores": None, "kind": "reference",
+                    "sample": f"unavailable: {exc}"}
+    return out_base, parity
 
 
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.export_index:
+        _export_index(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -13,13 +13,13 @@
  *     message for the calling thread is available from mrpt_last_error();
  *   - every pointer argument is caller-owned DEVICE memory unless the comment
  *     says "host"; the library never allocates or frees caller memory (its
- *     own scratch: small stream-ordered pool allocations, and one 32 MB
- *     cuBLASLt workspace per device for mrpt_scan_topk_u8gemm);
+ *     own scratch: small stream-ordered pool allocations);
  *   - work is enqueued on `stream` (a cudaStream_t, NULL = legacy default) and
  *     the call returns without synchronising; host-side argument validation
  *     fails fast before anything is enqueued;
- *   - calls are reentrant; the only global state is the per-device cuBLASLt
- *     handle and GEMM plan cache of mrpt_scan_topk_u8gemm (mutex-guarded);
+ *   - calls are reentrant and keep no global mutable state besides
+ *     measurement counters (launch count, fallback statistics, the optional
+ *     kernel timer); every kernel is this library's own (no library GEMM);
  *   - leaf ids of tree t live at leaf_indices[t*n + off] (64-bit addressing,
  *     T*n reaches 1e10 at the largest configuration).
  * Status codes map onto the reference exception taxonomy
@@ -240,65 +240,13 @@ int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64_t ldx,
                           const int32_t *ncand, int32_t k, int64_t *ids,
                           double *dists, void *stream);
 
-/* Signed 8-bit shadow rows for data with negative values: per row scale
- * s = max|x| / 127, Xq = clamp(rint(x / s), -127, 127) (s8, (n, ldq)),
- * norm = sum Xq^2, radius >= ||x - s Xq||_2.  Used by mrpt_scan_topk_s8. */
-int32_t mrpt_quantize_s8(const float *X, int64_t n, int32_t d, int64_t ldx,
-                         void *Xq, int64_t ldq, float *scale, int32_t *norm,
-                         float *radius, void *stream);
-
-/* mrpt_scan_topk_u8 over signed (s8) shadow rows: the same exact integer
- * dot-product filter (dp4a with signed rows) and float64 rerank; identical
- * results.  Falls back to mrpt_scan_topk for unsupported shapes. */
-int32_t mrpt_scan_topk_s8(const float *X, int64_t n, int32_t d, int64_t ldx,
-                          const void *Xq, int64_t ldq, const float *scale,
-                          const int32_t *norm, const float *radius,
-                          const float *Q, int64_t nq, int64_t ldqq,
-                          const int32_t *cand, int64_t cap,
-                          const int32_t *ncand, int32_t k, int64_t *ids,
-                          double *dists, void *stream);
-
-/* GEMM operands of the u8 shadow for mrpt_scan_topk_u8gemm: Xs = Xq ^ 0x80
- * (s8, row stride ldq, room for round_up(n, 16) rows -- the rows past n are
- * zeroed here) and info (n x 16 bytes, 16-byte aligned): per row {scale
- * (f32), norm (s32), radius (f32), sum of the u8 entries (s32)}. */
+/* Tensor-core operands of the u8 shadow for mrpt_scan_topk_u8tc_bits:
+ * Xs = Xq ^ 0x80 (s8, row stride ldq, room for round_up(n, 16) rows -- the
+ * rows past n are zeroed here) and info (n x 16 bytes, 16-byte aligned): per
+ * row {scale (f32), norm (s32), radius (f32), sum of the u8 entries (s32)}. */
 int32_t mrpt_u8_gemm_rows(const void *Xq, int64_t n, int64_t ldq, const float *scale,
                           const int32_t *norm, const float *radius, void *Xs,
                           void *info, void *stream);
-
-/* Workspace bytes mrpt_scan_topk_u8gemm needs for nq queries (it runs
- * queries in chunks whose dot-product matrix is <= 4 GiB). */
-int32_t mrpt_scan_topk_u8gemm_workspace_size(int64_t n, int64_t ldq, int64_t nq,
-                                             int64_t *bytes);
-
-/* mrpt_scan_topk_u8 with the filter's integer dot products for every
- * (query, row) pair computed by one int8 tensor-core GEMM per query chunk
- * (D = Qop . Xs^T, cuBLASLt IMMA; exact in int32).  The filter then reads 4
- * bytes per candidate instead of a row: x.q = D + 128 sum(q) (+ 128 sum(x)
- * - 16384 ldq for u8 queries).  Same bounds, same float64 rerank, identical
- * results; pays when candidate sets cover a large share of the rows.
- * workspace: 256-byte aligned, >= one query's share of
- * mrpt_scan_topk_u8gemm_workspace_size (smaller workspaces run smaller
- * chunks).  Falls back to mrpt_scan_topk for unsupported shapes. */
-int32_t mrpt_scan_topk_u8gemm(const float *X, int64_t n, int32_t d, int64_t ldx,
-                              const void *Xs, int64_t ldq, const void *info,
-                              const float *Q, int64_t nq, int64_t ldqq,
-                              const int32_t *cand, int64_t cap,
-                              const int32_t *ncand, int32_t k, int64_t *ids,
-                              double *dists, void *workspace, int64_t ws_bytes,
-                              void *stream);
-
-/* mrpt_scan_topk_u8gemm over candidate bitmaps (mrpt_vote_bitmap) instead of
- * lists: each warp takes its query's bitmap 16 words at a time and admits
- * the set ids 32 per round.  k <= 96.  Same results.  wait_event (a
- * cudaEvent_t, or NULL): the filter waits for it after the first chunk's
- * GEMM, so the bitmaps may be produced on another stream while the GEMM runs. */
-int32_t mrpt_scan_topk_u8gemm_bits(const float *X, int64_t n, int32_t d, int64_t ldx,
-                                   const void *Xs, int64_t ldq, const void *info,
-                                   const float *Q, int64_t nq, int64_t ldqq,
-                                   const uint32_t *cbits, int64_t bstride, int32_t k,
-                                   int64_t *ids, double *dists, void *workspace,
-                                   int64_t ws_bytes, void *wait_event, void *stream);
 
 /* The u8 filter over candidate bitmaps fused onto the tcgen05 tensor cores
  * (replaces the _cy.scan + lexsort step of exact_knn_in_set,
@@ -307,7 +255,9 @@ int32_t mrpt_scan_topk_u8gemm_bits(const float *X, int64_t n, int32_t d, int64_t
  * shared memory, forms each 128-query x 256-row block of dot products with
  * tcgen05.mma.kind::i8 into TMEM and bounds every candidate straight out of
  * TMEM (no dot-product matrix in HBM); survivors get the exact float64
- * re-rank.  Same arguments and results as mrpt_scan_topk_u8gemm_bits.
+ * re-rank.  cbits: (nq, bstride) candidate bitmaps from mrpt_vote_bitmap;
+ * wait_event (a cudaEvent_t, or NULL): the filter waits for it after the
+ * query quantisation, so the bitmaps may come from another stream.
  * 128 <= ldq <= 1024, k <= 16; bstride a multiple of 4 words (the bitmaps are
  * TMA-staged per row tile).  workspace: 256-byte aligned, sized by
  * mrpt_scan_topk_u8tc_workspace_size (smaller workspaces run smaller query
@@ -320,6 +270,12 @@ int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d, int64_t l
                                  const uint32_t *cbits, int64_t bstride, int32_t k,
                                  int64_t *ids, double *dists, void *workspace,
                                  int64_t ws_bytes, void *wait_event, void *stream);
+
+/* Measurement support: how often the exact fallback ran.  out (host, 8
+ * int64): for the routes fp32 filter, fp16 filter, u8 filter and tcgen05
+ * filter in that order, [queries handed to the route, queries that took the
+ * exact tiled fallback].  Synchronises the device; reset != 0 clears. */
+int32_t mrpt_fallback_stats(int64_t *out /* host */, int32_t reset);
 
 /* Measurement support (not part of the reference interface): when enabled,
  * the fused filter launch of mrpt_scan_topk_u8tc_bits is bracketed by CUDA
@@ -345,6 +301,22 @@ int32_t mrpt_unique_ids(const int64_t *cand, int64_t m, int64_t n,
 int32_t mrpt_fnv1a64_workspace_size(int64_t nbytes, size_t *bytes /* host */);
 int32_t mrpt_fnv1a64(const uint8_t *buf, int64_t nbytes, uint64_t *out,
                      void *ws, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------ f3 --
+ * Exact brute-force k-NN (ground truth): replaces evaluation.brute_force_knn
+ * and compute_ground_truth (pkg/src/mrpt/evaluation.py:28-81).  Q (nq, ldq)
+ * float64 query rows (the reference converts the query to float64,
+ * evaluation.py:37); d2 per (query, row) summed in numpy's pairwise order
+ * (the reference's ((X - q)**2).sum(axis=1)), ordered by (d2, id) like
+ * np.lexsort((ids, d2)).  Output (nq, min(k, n)) row-major: ids int64,
+ * dists float64 = sqrt(d2).  d <= 4096.  Workspace from
+ * mrpt_brute_force_workspace_size (device bytes). */
+int32_t mrpt_brute_force_workspace_size(int64_t n, int32_t d, int64_t nq, int32_t k,
+                                        int64_t *bytes /* host */);
+int32_t mrpt_brute_force_knn(const float *X, int64_t n, int32_t d, int64_t ldx,
+                             const double *Q, int64_t nq, int64_t ldq, int32_t k,
+                             int64_t *ids, double *dists, void *ws, int64_t ws_bytes,
+                             void *stream);
 
 /* ------------------------------------------------------------- helpers --
  * Dataset validation (core.py:63): *bad (device int32) = 1 if any element of

@@ -200,10 +200,86 @@ def approximate_knn_batch(X, Q, k, index, v):
     return ids, dists, counts
 
 
+def candidates_crossing_order(leaves, index, v):
+    """The compiled reference's candidate order (_cy.pyx:57-78): trees in
+    order, each leaf slice in stored order, an id emitted when its running
+    count becomes exactly v."""
+    L, O = index["leaf_indices"], index["leaf_offsets"]
+    counts = {}
+    out = []
+    for t, leaf in enumerate(np.asarray(leaves, dtype=np.int64)):
+        for idx in L[t, O[t, leaf]:O[t, leaf + 1]]:
+            c = counts.get(int(idx), 0) + 1
+            counts[int(idx)] = c
+            if c == v:
+                out.append(int(idx))
+    return np.array(out, dtype=np.int64)
+
+
+def pairwise_plan(n, lo=0):
+    """numpy's pairwise summation of n contiguous float64 terms (numpy
+    loops_utils.h pairwise_sum), as the postfix plan the GPU ground-truth
+    kernel evaluates: ("leaf", lo, len) blocks of <= 128 terms and "add"."""
+    if n <= 128:
+        return [("leaf", lo, n)]
+    n2 = n // 2
+    n2 -= n2 % 8
+    return pairwise_plan(n2, lo) + pairwise_plan(n - n2, lo + n2) + ["add"]
+
+
+def pairwise_sum(a):
+    """Restatement of numpy's pairwise float64 sum of a 1-D array: a leaf of
+    < 8 terms is summed in order from 0.0; 8..128 terms go to 8 interleaved
+    accumulators combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the n % 8
+    tail in order; longer runs split at n/2 - (n/2) % 8."""
+    a = [float(x) for x in a]
+    stack = []
+    for op in pairwise_plan(len(a)):
+        if op == "add":
+            r = stack.pop()
+            stack.append(stack.pop() + r)
+            continue
+        _, lo, n = op
+        if n < 8:
+            res = 0.0
+            for x in a[lo:lo + n]:
+                res += x
+        else:
+            r = a[lo:lo + 8]
+            m = n - n % 8
+            for i in range(8, m, 8):
+                for j in range(8):
+                    r[j] += a[lo + i + j]
+            res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+            for x in a[lo + m:lo + n]:
+                res += x
+        stack.append(res)
+    return stack[0] if stack else 0.0
+
+
 def brute_force_knn(X, q, k):
-    """brute_force_knn (evaluation.py:28-47) ids, via the sequential scan."""
-    n = X.shape[0]
-    return exact_knn(X, q, k, np.arange(n))
+    """evaluation.brute_force_knn (evaluation.py:28-47): float64 differences,
+    d2 = numpy's row sums (pairwise order, restated by pairwise_sum), the
+    first min(k, n) of np.lexsort((ids, d2)); returns (ids, dists, n)."""
+    X = np.ascontiguousarray(X, np.float32)
+    qv = np.asarray(q, dtype=np.float64).ravel()
+    diff = X.astype(np.float64) - qv
+    d2 = (diff * diff).sum(axis=1)
+    ids = np.arange(X.shape[0], dtype=np.int64)
+    order = np.lexsort((ids, d2))[:k]
+    return ids[order], np.sqrt(d2[order]), X.shape[0]
+
+
+def compute_ground_truth(X, Q, k):
+    """evaluation.compute_ground_truth (evaluation.py:65-81): (nq, k) ids and
+    distances, one brute-force scan per query."""
+    Q = np.atleast_2d(np.asarray(Q, dtype=np.float32))
+    ids = np.empty((Q.shape[0], k), dtype=np.int64)
+    dists = np.empty((Q.shape[0], k), dtype=np.float64)
+    for i, q in enumerate(Q):
+        a, b, _ = brute_force_knn(X, q, k)
+        ids[i], dists[i] = a, b
+    return ids, dists
 
 
 def fnv1a64(buf):

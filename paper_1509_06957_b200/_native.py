@@ -46,28 +46,24 @@ SIGNATURES = {
     "mrpt_quantize_u8": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p],
     "mrpt_scan_topk_u8": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_p,
                           _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i32, _c_p, _c_p, _c_p],
-    "mrpt_quantize_s8": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_p],
-    "mrpt_scan_topk_s8": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_p,
-                          _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i32, _c_p, _c_p, _c_p],
     "mrpt_u8_gemm_rows": [_c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p],
-    "mrpt_scan_topk_u8gemm_workspace_size": [_c_i64, _c_i64, _c_i64, ctypes.POINTER(_c_i64)],
-    "mrpt_scan_topk_u8gemm": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_i64, _c_i64,
-                              _c_p, _c_i64, _c_p, _c_i32, _c_p, _c_p, _c_p, _c_i64, _c_p],
     "mrpt_vote_counted": [_c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_i64, _c_i32, _c_i32, _c_i64,
                           _c_p, _c_p, _c_p, _c_i64, _c_p, _c_p],
     "mrpt_filter_counts": [_c_p, _c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_p, _c_i64, _c_p, _c_p],
     "mrpt_vote_bitmap": [_c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_i64, _c_i32, _c_i32, _c_i64,
                          _c_p, _c_p, _c_i64, _c_p, _c_p],
-    "mrpt_scan_topk_u8gemm_bits": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_i64,
-                                   _c_i64, _c_p, _c_i64, _c_i32, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_p],
     "mrpt_scan_topk_u8tc_workspace_size": [_c_i64, _c_i64, _c_i64, ctypes.POINTER(_c_i64)],
     "mrpt_scan_topk_u8tc_bits": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_i64,
                                  _c_i64, _c_p, _c_i64, _c_i32, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_p],
     "mrpt_kernel_timer": [_c_i32],
+    "mrpt_fallback_stats": [ctypes.POINTER(_c_i64), _c_i32],
     "mrpt_kernel_timer_read": [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_c_i64)],
     "mrpt_unique_ids": [_c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p],
     "mrpt_fnv1a64_workspace_size": [_c_i64, ctypes.POINTER(_c_sz)],
     "mrpt_fnv1a64": [_c_p, _c_i64, _c_p, _c_p, _c_sz, _c_p],
+    "mrpt_brute_force_workspace_size": [_c_i64, _c_i32, _c_i64, _c_i32, ctypes.POINTER(_c_i64)],
+    "mrpt_brute_force_knn": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_i64, _c_i32, _c_p, _c_p,
+                             _c_p, _c_i64, _c_p],
     "mrpt_check_finite": [_c_p, _c_i64, _c_p, _c_p],
     "mrpt_audit_leaves": [_c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p],
 }

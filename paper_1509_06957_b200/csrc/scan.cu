@@ -15,6 +15,7 @@
 // np.lexsort((S, d2)) does.
 #include <cuda_fp16.h>
 #include <stdlib.h>
+#include <atomic>
 #include <vector>
 
 #include "common.cuh"
@@ -52,7 +53,12 @@ struct TopkArgs {
   int32_t *nsurv;        // survivors per query, -1 when the query was finished in the filter kernel
   const uint32_t *cbits; // optional: candidate bitmaps (nq, bstride words) instead of cand lists
   int64_t bstride;
+  int stat_slot;         // > 0: the exact fallback of route stat_slot (counts its queries)
 };
+
+// Queries that took the exact fallback, per route (1 fp32, 2 fp16, 3 u8,
+// 4 tcgen05 filter), read by mrpt_fallback_stats; measurement only.
+__device__ unsigned long long g_fallbacks[8];
 
 constexpr int kSurvCap = 64;
 
@@ -279,6 +285,8 @@ __global__ void __launch_bounds__(kScanNT, 3) k_scan_topk_tiled(TopkArgs a) {
   __shared__ unsigned long long s_tk;
   __shared__ int s_ti;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (a.qcount && a.stat_slot > 0 && blockIdx.x == 0 && tid == 0)
+    atomicAdd(&g_fallbacks[a.stat_slot], (unsigned long long)*a.qcount);
   float *tile = tiles + warp * 32 * kTileStride;
   const int d = a.d;
   const int nchunk = (d + 31) >> 5;
@@ -1083,44 +1091,6 @@ __global__ void k_quantize_u8(const float *__restrict__ X, int64_t n, int d, int
   }
 }
 
-// Signed 8-bit shadow rows for data with negative values: per row scale
-// sx = max|x| / 127, X_i = clamp(rint(x / sx), -127, 127) (one warp per row).
-__global__ void k_quantize_s8(const float *__restrict__ X, int64_t n, int d, int64_t ldx, int8_t *Xq, int64_t ldq,
-                              float *scale, int32_t *norm, float *radius) {
-  const int lane = threadIdx.x & 31;
-  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += wstride) {
-    const float *xr = X + i * ldx;
-    float mx = 0.f;
-    for (int c = lane; c < d; c += 32) mx = fmaxf(mx, fabsf(xr[c]));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const float sc = mx > 0.f ? mx / 127.f : 1.f;
-    double r2 = 0.0;
-    int nn = 0;
-    for (int c = lane; c < ldq; c += 32) {
-      const float x = c < d ? xr[c] : 0.f;
-      float qv = rintf(x / sc);
-      qv = fminf(fmaxf(qv, -127.f), 127.f);
-      const int qi = (int)qv;
-      Xq[i * ldq + c] = (int8_t)qi;
-      const double e = (double)x - (double)sc * (double)qi;
-      r2 = fma(e, e, r2);
-      nn += qi * qi;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      r2 += __shfl_xor_sync(0xffffffffu, r2, o);
-      nn += __shfl_xor_sync(0xffffffffu, nn, o);
-    }
-    if (lane == 0) {
-      scale[i] = sc;
-      norm[i] = nn;
-      radius[i] = r2 == 0.0 ? 0.f : __double2float_ru(__dsqrt_ru(r2 * (1.0 + 1e-12)));
-    }
-  }
-}
-
 __device__ __forceinline__ void dist_bounds2(float A, float r, float eta, double &L, double &U) {
   const double a = (double)A, e = (double)eta;
   const double slo = fmax(0.0, sqrt(fmax(0.0, a - e)) - (double)r);
@@ -1193,24 +1163,13 @@ struct Q8Rows {
   const float *scale;
   const int32_t *norm;
   const float *radius;
-  // precomputed-dot mode (tensor-core GEMM over all rows):
-  const int32_t *D;    // (nq, ldD) s32: (x ^ 0x80) . qop for every row x
-  int64_t ldD;
-  const uint4 *info;   // per row {scale (f32), norm (s32), radius (f32), sum of u8 entries (s32)}
-  const QParams *qp;   // per query (the quantisation that produced qop)
-  const uint32_t *cbits;  // optional: candidate bitmaps (nq, bstride words) instead of lists
-  int64_t bstride;
 };
 
-// a: 4 row bytes (u8, or s8 when RS), b: 4 query bytes (s8 when QS, else u8)
-template <bool QS, bool RS = false>
+// a: 4 row bytes (u8), b: 4 query bytes (s8 when QS, else u8)
+template <bool QS>
 __device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
   int d;
-  if (RS && QS)
-    asm("dp4a.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  else if (RS)
-    asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  else if (QS)
+  if (QS)
     asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
   else
     asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
@@ -1220,7 +1179,7 @@ __device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
 // U rows' partial dot products over this lane's 16-byte chunks.  The query's
 // signedness is a template parameter: a runtime flag here puts a branch
 // around every dp4a (inline asm cannot be predicated).
-template <int U, int G, bool QS, bool RS = false>
+template <int U, int G, bool QS>
 __device__ __forceinline__ void dot_rows_u8(const uint8_t *(&rp)[U], const uint32_t *qb,
                                             int gl, int nchunk, int (&acc)[U]) {
   for (int ch = gl; ch < nchunk; ch += G) {
@@ -1230,10 +1189,10 @@ __device__ __forceinline__ void dot_rows_u8(const uint8_t *(&rp)[U], const uint3
     for (int u = 0; u < U; ++u) xv[u] = __ldg(reinterpret_cast<const uint4 *>(rp[u] + 16 * ch));
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      acc[u] = dp4a_us<QS, RS>(xv[u].x, qv.x, acc[u]);
-      acc[u] = dp4a_us<QS, RS>(xv[u].y, qv.y, acc[u]);
-      acc[u] = dp4a_us<QS, RS>(xv[u].z, qv.z, acc[u]);
-      acc[u] = dp4a_us<QS, RS>(xv[u].w, qv.w, acc[u]);
+      acc[u] = dp4a_us<QS>(xv[u].x, qv.x, acc[u]);
+      acc[u] = dp4a_us<QS>(xv[u].y, qv.y, acc[u]);
+      acc[u] = dp4a_us<QS>(xv[u].z, qv.z, acc[u]);
+      acc[u] = dp4a_us<QS>(xv[u].w, qv.w, acc[u]);
     }
   }
 }
@@ -1388,18 +1347,15 @@ __device__ __forceinline__ bool admit_lane_u8(int32_t myc, int mys, float sx, in
 }
 
 // G lanes per row (ldq / 16 rounded up to a power of two, <= 32); each warp
-// iteration scores (32 / G) * 4 candidates with 16-byte loads.  DM: the dot
-// products come precomputed from the tensor-core GEMM (rows.D, one candidate
-// per lane, 4 bytes per candidate instead of a row); the bounds, buffer and
-// exact re-rank are the same code.
-template <int BUFW, int G, bool DM, bool RS = false>
+// iteration scores (32 / G) * 4 candidates with 16-byte loads.
+template <int BUFW, int G>
 __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows rows,
                                                              int32_t *fb_list, int32_t *fb_count) {
   extern __shared__ unsigned long long topk_smem[];
   constexpr int NWARP = kScanNT / 32;
   constexpr int R = 32 / G;             // rows per load instruction
   constexpr int U = 4;                  // loads in flight per lane
-  constexpr int CPI = DM ? 32 : R * U;  // candidates per warp iteration (<= 32)
+  constexpr int CPI = R * U;            // candidates per warp iteration (<= 32)
   uint32_t *qb = reinterpret_cast<uint32_t *>(topk_smem);             // 256 words: quantized q
   float *wa = reinterpret_cast<float *>(qb + 256);
   float *wr = wa + NWARP * BUFW;
@@ -1409,7 +1365,6 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
   int32_t *cid = reinterpret_cast<int32_t *>(ckey + NWARP * BUFW);
   float *cu = reinterpret_cast<float *>(cid + NWARP * BUFW);
   float *cl = cu + NWARP * BUFW;
-  int32_t *wq_base = reinterpret_cast<int32_t *>(cl + NWARP * BUFW);  // DM bitmap mode: 512 ids per warp
   __shared__ int s_wcnt[NWARP];
   __shared__ int s_bad, s_ns;
   __shared__ unsigned s_su_cta;
@@ -1430,19 +1385,10 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
       s_bad = 0;
       s_su_cta = 0x7f800000u;  // +inf
     }
-    QParams P;
-    if (DM) {
-      P = rows.qp[q];
-      __syncthreads();
-    } else {
-      P = quantize_query_u8<kScanNT>(qrow, d, ldq, qb, qscr);
-    }
+    const QParams P = quantize_query_u8<kScanNT>(qrow, d, ldq, qb, qscr);
     const bool qsigned = P.qsigned != 0;
     const float rq = P.rq;
     const float sqf = P.sq, t2f = P.t2f;
-    // DM: x.qq = D + 128*sum(qq) (+ 128*sum(x) - 16384*ldq when the GEMM used qq - 128)
-    const int corr_q = 128 * P.qsum - (qsigned ? 0 : 16384 * ldq);
-    const int32_t *Drow = DM ? rows.D + q * rows.ldD : nullptr;
     int64_t m;
     if (a.cand) {
       const int64_t nc = a.ncand[q];
@@ -1461,102 +1407,7 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
 #define ADMIT_LANE(MYC, MYS, SX, NRM, RAD) \
   admit_lane_u8<BUFW, CPI>((MYC), (MYS), (SX), (NRM), (RAD), sqf, t2f, rq, su, cnt, ma, mr, me, mi, kk, cu_w, cid_w, \
                            &s_su_cta)
-    if (DM && rows.cbits) {
-      // candidate bitmap: lanes 0..15 each load one of 16 consecutive words
-      // and write their set bits' ids, in id order, to the warp's queue at
-      // the word's prefix offset; the queue is then consumed 32 ids per
-      // admission round (2 rounds in flight)
-      constexpr int UB = 2;
-      const uint32_t *qbits = rows.cbits + q * rows.bstride;
-      const int nwords = (int)((a.n + 31) >> 5);
-      int32_t *queue = wq_base + warp * (16 * 32);
-      for (int w0 = warp * 16; w0 < nwords && !bad; w0 += NWARP * 16) {
-        const uint32_t word = (lane < 16 && w0 + lane < nwords) ? __ldg(qbits + w0 + lane) : 0u;
-        const int pc = __popc(word);
-        int incl = pc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int u = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += u;
-        }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        {
-          // lane l writes the low 16 bits of word l, lane l+16 its high 16 bits
-          const int src = lane & 15;
-          const uint32_t w = __shfl_sync(0xffffffffu, word, src);
-          int p = __shfl_sync(0xffffffffu, incl - pc, src);
-          uint32_t wd = w & 0xffffu;
-          if (lane >= 16) {
-            p += __popc(wd);
-            wd = w & 0xffff0000u;
-          }
-          const int32_t id0 = (w0 + src) * 32;
-          while (wd) {
-            queue[p++] = id0 + __ffs(wd) - 1;
-            wd &= wd - 1u;
-          }
-        }
-        __syncwarp();
-        for (int b0 = 0; b0 < total && !bad; b0 += 32 * UB) {
-          int32_t cj[UB];
-          int dv[UB];
-          uint4 inf[UB];
-#pragma unroll
-          for (int u = 0; u < UB; ++u) {
-            const int r = b0 + 32 * u + lane;
-            cj[u] = r < total ? queue[r] : -1;
-            dv[u] = 0;
-            inf[u] = make_uint4(0u, 0u, 0u, 0u);
-            if (cj[u] >= 0) {
-              dv[u] = __ldg(Drow + cj[u]);
-              inf[u] = __ldg(rows.info + cj[u]);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < UB; ++u) {
-            if (b0 + 32 * u >= total) break;  // warp-uniform
-            const int mys = dv[u] + corr_q + (qsigned ? 0 : 128 * (int)inf[u].w);
-            if (!ADMIT_LANE(cj[u], mys, __uint_as_float(inf[u].x), (int)inf[u].y, __uint_as_float(inf[u].z))) {
-              bad = true;
-              cnt = 0;
-              break;
-            }
-          }
-        }
-        __syncwarp();  // the queue is rewritten by the next 16 words
-      }
-    } else if (DM) {
-      // UDM candidates per lane in flight: ids, then their dot products and row info
-      constexpr int UDM = 4;
-      for (int64_t g = (int64_t)warp * 32 * UDM; g < m && !bad; g += (int64_t)NWARP * 32 * UDM) {
-        int32_t cj[UDM];
-#pragma unroll
-        for (int u = 0; u < UDM; ++u) {
-          const int64_t j = g + u * 32 + lane;
-          cj[u] = j < m ? (qc ? __ldg(qc + j) : (int32_t)j) : -1;
-        }
-        int dv[UDM];
-        uint4 inf[UDM];
-#pragma unroll
-        for (int u = 0; u < UDM; ++u) {
-          dv[u] = 0;
-          inf[u] = make_uint4(0u, 0u, 0u, 0u);
-          if (cj[u] >= 0) {
-            dv[u] = __ldg(Drow + cj[u]);
-            inf[u] = __ldg(rows.info + cj[u]);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < UDM; ++u) {
-          const int mys = dv[u] + corr_q + (qsigned ? 0 : 128 * (int)inf[u].w);
-          if (!ADMIT_LANE(cj[u], mys, __uint_as_float(inf[u].x), (int)inf[u].y, __uint_as_float(inf[u].z))) {
-            bad = true;
-            cnt = 0;
-            break;
-          }
-        }
-      }
-    } else {
+    {
     for (int64_t g = (int64_t)warp * CPI; g < m; g += (int64_t)NWARP * CPI) {
       int mys = 0;
       int32_t myc = -1;
@@ -1572,9 +1423,9 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_u8(TopkArgs a, Q8Rows 
 #pragma unroll
       for (int u = 0; u < U; ++u) acc[u] = 0;
       if (qsigned)
-        dot_rows_u8<U, G, true, RS>(rp, qb, gl, nchunk, acc);
+        dot_rows_u8<U, G, true>(rp, qb, gl, nchunk, acc);
       else
-        dot_rows_u8<U, G, false, RS>(rp, qb, gl, nchunk, acc);
+        dot_rows_u8<U, G, false>(rp, qb, gl, nchunk, acc);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
 #pragma unroll
@@ -1918,6 +1769,27 @@ using namespace mrpt;
 
 static bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Queries handed to each filter route (same slots as g_fallbacks).
+static std::atomic<long long> g_route_queries[8];
+
+extern "C" int32_t mrpt_fallback_stats(int64_t *out, int32_t reset) {
+  clear_error();
+  if (!out) return fail(MRPT_EPARAM, "mrpt_fallback_stats: out is NULL");
+  unsigned long long fb[8] = {0};
+  if (cudaMemcpyFromSymbol(fb, g_fallbacks, sizeof(fb)) != cudaSuccess)
+    return launch_status("mrpt_fallback_stats");
+  for (int r = 0; r < 4; ++r) {
+    out[2 * r] = g_route_queries[r + 1].load();
+    out[2 * r + 1] = (int64_t)fb[r + 1];
+  }
+  if (reset) {
+    const unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_fallbacks, z, sizeof(z));
+    for (auto &c : g_route_queries) c.store(0);
+  }
+  return launch_status("mrpt_fallback_stats");
+}
+
 extern "C" int32_t mrpt_scan(const float *X, int64_t n, int32_t d, int64_t ldx, const int64_t *cand,
                              int64_t m, const float *q, double *out, void *stream) {
   clear_error();
@@ -2017,6 +1889,8 @@ extern "C" int32_t mrpt_scan_topk(const float *X, int64_t n, int32_t d, int64_t 
     (count_launch(), ffn<<<(unsigned)grid, kScanNT, smem, s>>>(a, eps, eta, fb + 1, fb));
     // fallback: exact tiled kernel over the listed queries
     a.qlist = fb + 1;
+    a.stat_slot = 1;  // fallback statistics: see mrpt_fallback_stats
+    g_route_queries[1] += nq;
     a.qcount = fb;
     const int buf = (k + kScanNT <= 1024) ? 1024 : 2048;
     topk_fn tfn = buf == 1024 ? k_scan_topk_tiled<1024> : k_scan_topk_tiled<2048>;
@@ -2128,6 +2002,8 @@ extern "C" int32_t mrpt_scan_topk_fp16(const float *X, int64_t n, int32_t d, int
   (count_launch(), ffn<<<(unsigned)grid, kScanNT, smem, s>>>(a, eps, eta, fb + 1, fb));
   // fallback: exact tiled kernel over the listed queries
   a.qlist = fb + 1;
+  a.stat_slot = 2;  // fallback statistics: see mrpt_fallback_stats
+  g_route_queries[2] += nq;
   a.qcount = fb;
   if (a.vec4) {
     const int buf = (k + kScanNT <= 1024) ? 1024 : 2048;
@@ -2168,29 +2044,11 @@ extern "C" int32_t mrpt_quantize_u8(const float *X, int64_t n, int32_t d, int64_
   return launch_status("mrpt_quantize_u8");
 }
 
-extern "C" int32_t mrpt_quantize_s8(const float *X, int64_t n, int32_t d, int64_t ldx, void *Xq, int64_t ldq,
-                                    float *scale, int32_t *norm, float *radius, void *stream) {
-  clear_error();
-  if (n < 1 || d < 1 || ldx < d || ldq < d || ldq % 16 != 0 || ldq > 1024)
-    return fail(MRPT_ESHAPE, "mrpt_quantize_s8: bad shape");
-  const int64_t wb = ceil_div<int64_t>(n, 8);
-  const int g = (int)(wb < (int64_t)num_sms() * 16 ? wb : (int64_t)num_sms() * 16);
-  (count_launch(), k_quantize_s8<<<g, 256, 0, as_stream(stream)>>>(X, n, d, ldx, reinterpret_cast<int8_t *>(Xq),
-                                                                   ldq, scale, norm, radius));
-  return launch_status("mrpt_quantize_s8");
-}
-
 typedef void (*topk_fn_u8)(TopkArgs, Q8Rows, int32_t *, int32_t *);
 
-template <int G, bool DM = false, bool RS = false>
+template <int G>
 static topk_fn_u8 pick_u8_b(int bufw) {
-  return bufw == 64 ? k_scan_topk_u8<64, G, DM, RS>
-                    : (bufw == 128 ? k_scan_topk_u8<128, G, DM, RS> : k_scan_topk_u8<256, G, DM, RS>);
-}
-
-namespace mrpt {
-int32_t igemm_rows_tn(const int8_t *Xs, int64_t n, const int8_t *Qop, int64_t m, int64_t k, int32_t *D,
-                      int64_t ldD, cudaStream_t s);
+  return bufw == 64 ? k_scan_topk_u8<64, G> : (bufw == 128 ? k_scan_topk_u8<128, G> : k_scan_topk_u8<256, G>);
 }
 
 static void launch_rerank(const TopkArgs &a, cudaStream_t s) {
@@ -2204,7 +2062,7 @@ static void launch_rerank(const TopkArgs &a, cudaStream_t s) {
 static int32_t scan_u8_impl(const float *X, int64_t n, int32_t d, int64_t ldx, const void *Xq, int64_t ldq,
                             const float *scale, const int32_t *norm, const float *radius, const float *Q,
                             int64_t nq, int64_t ldqq, const int32_t *cand, int64_t cap, const int32_t *ncand,
-                            int32_t k, int64_t *ids, double *dists, void *stream, bool rs) {
+                            int32_t k, int64_t *ids, double *dists, void *stream) {
   if (!Xq || !scale || !norm || !radius || ldq % 16 != 0 || ldq < d || ldq > 1024 || k > 120 || k < 1 ||
       d % 4 != 0 || ldx % 4 != 0 || !aligned16(X))  // the exact fallback needs 16-byte rows
     return mrpt_scan_topk(X, n, d, ldx, Q, nq, ldqq, cand, cap, ncand, k, ids, dists, stream);
@@ -2244,12 +2102,6 @@ static int32_t scan_u8_impl(const float *X, int64_t n, int32_t d, int64_t ldx, c
   rows.scale = scale;
   rows.norm = norm;
   rows.radius = radius;
-  rows.D = nullptr;
-  rows.ldD = 0;
-  rows.info = nullptr;
-  rows.qp = nullptr;
-  rows.cbits = nullptr;
-  rows.bstride = 0;
   // G lanes per row: 8 for wide rows (16 candidates per warp iteration, several
   // chunk loads in flight per lane); 4 for rows of <= 256 bytes (two or more
   // chunks per lane, 32 candidates per iteration, one shuffle level less).
@@ -2260,7 +2112,6 @@ static int32_t scan_u8_impl(const float *X, int64_t n, int32_t d, int64_t ldx, c
     g_env = e ? atoi(e) : 0;
   }
   int G = (g_env == 4 || g_env == 8 || g_env == 16 || g_env == 32) ? g_env : (ldq <= 256 ? 4 : 8);
-  if (rs && G > 8) G = 8;  // signed rows are instantiated for 4 and 8 lanes per row
   const int cpi = (32 / G) * 4;
   int bufw = 64;
   while (bufw < 2 * k + 2 * cpi) bufw <<= 1;
@@ -2274,13 +2125,14 @@ static int32_t scan_u8_impl(const float *X, int64_t n, int32_t d, int64_t ldx, c
   cudaMemsetAsync(fb, 0, sizeof(int32_t), s);
   a.nsurv = fb + 1 + nq;
   a.surv = a.nsurv + nq;
-  topk_fn_u8 fn = rs ? (G == 4 ? pick_u8_b<4, false, true>(bufw) : pick_u8_b<8, false, true>(bufw))
-                     : (G == 32 ? pick_u8_b<32>(bufw)
-                                : (G == 16 ? pick_u8_b<16>(bufw) : (G == 8 ? pick_u8_b<8>(bufw) : pick_u8_b<4>(bufw))));
+  topk_fn_u8 fn = G == 32 ? pick_u8_b<32>(bufw)
+                          : (G == 16 ? pick_u8_b<16>(bufw) : (G == 8 ? pick_u8_b<8>(bufw) : pick_u8_b<4>(bufw)));
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t grid = nq < (int64_t)num_sms() * 8 ? nq : (int64_t)num_sms() * 8;
   (count_launch(), fn<<<(unsigned)grid, kScanNT, smem, s>>>(a, rows, fb + 1, fb));
   a.qlist = fb + 1;
+  a.stat_slot = 3;  // fallback statistics: see mrpt_fallback_stats
+  g_route_queries[3] += nq;
   a.qcount = fb;
   if (a.vec4) {
     const int buf = (k + kScanNT <= 1024) ? 1024 : 2048;
@@ -2306,18 +2158,7 @@ extern "C" int32_t mrpt_scan_topk_u8(const float *X, int64_t n, int32_t d, int64
                                      void *stream) {
   clear_error();
   return scan_u8_impl(X, n, d, ldx, Xq, ldq, scale, norm, radius, Q, nq, ldqq, cand, cap, ncand, k, ids, dists,
-                      stream, false);
-}
-
-extern "C" int32_t mrpt_scan_topk_s8(const float *X, int64_t n, int32_t d, int64_t ldx,
-                                     const void *Xq, int64_t ldq, const float *scale,
-                                     const int32_t *norm, const float *radius, const float *Q,
-                                     int64_t nq, int64_t ldqq, const int32_t *cand, int64_t cap,
-                                     const int32_t *ncand, int32_t k, int64_t *ids, double *dists,
-                                     void *stream) {
-  clear_error();
-  return scan_u8_impl(X, n, d, ldx, Xq, ldq, scale, norm, radius, Q, nq, ldqq, cand, cap, ncand, k, ids, dists,
-                      stream, true);
+                      stream);
 }
 
 extern "C" int32_t mrpt_u8_gemm_rows(const void *Xq, int64_t n, int64_t ldq, const float *scale,
@@ -2338,160 +2179,6 @@ extern "C" int32_t mrpt_u8_gemm_rows(const void *Xq, int64_t n, int64_t ldq, con
                                                        scale, norm, radius, reinterpret_cast<int8_t *>(Xs),
                                                        reinterpret_cast<uint4 *>(info)));
   return launch_status("mrpt_u8_gemm_rows");
-}
-
-// Workspace of the GEMM filter for a chunk of mc queries: D (mc x ldD s32),
-// the query operands, their parameters and the fallback list.
-static int64_t u8gemm_bytes(int64_t n, int64_t ldq, int64_t mc, int64_t *off_qop, int64_t *off_qp,
-                            int64_t *off_fb) {
-  auto al = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
-  const int64_t ldD = (n + 15) & ~(int64_t)15;
-  int64_t o = al(mc * ldD * 4);
-  if (off_qop) *off_qop = o;
-  o = al(o + mc * ldq);
-  if (off_qp) *off_qp = o;
-  o = al(o + mc * (int64_t)sizeof(QParams));
-  if (off_fb) *off_fb = o;  // fallback count + list, survivor counts, survivor lists
-  return al(o + ((mc + 1) + mc * (kSurvCap + 1)) * 4);
-}
-
-static const int64_t kGemmChunkD = (int64_t)1 << 32;  // D bytes per query chunk
-
-extern "C" int32_t mrpt_scan_topk_u8gemm_workspace_size(int64_t n, int64_t ldq, int64_t nq, int64_t *bytes) {
-  clear_error();
-  if (n < 1 || ldq < 16 || nq < 0 || !bytes) return fail(MRPT_ESHAPE, "mrpt_scan_topk_u8gemm_workspace_size");
-  const int64_t ldD = (n + 15) & ~(int64_t)15;
-  int64_t mc = kGemmChunkD / (4 * ldD);
-  if (mc > nq) mc = nq;
-  if (mc < 1) mc = 1;
-  *bytes = u8gemm_bytes(n, ldq, mc, nullptr, nullptr, nullptr);
-  return MRPT_OK;
-}
-
-static int32_t u8gemm_impl(const float *X, int64_t n, int32_t d, int64_t ldx, const void *Xs, int64_t ldq,
-                           const void *info, const float *Q, int64_t nq, int64_t ldqq, const int32_t *cand,
-                           int64_t cap, const int32_t *ncand, const uint32_t *cbits, int64_t bstride, int32_t k,
-                           int64_t *ids, double *dists, void *workspace, int64_t ws_bytes, void *stream,
-                           void *wait_event) {
-  if (cbits && (bstride < (n + 31) / 32 || cand))
-    return fail(MRPT_EPARAM, "mrpt_scan_topk_u8gemm_bits: bad candidate bitmaps");
-  if (cbits && (!Xs || !info || ldq % 16 != 0 || ldq < d || ldq > 1024 || k > 96 || k < 1 || d % 4 != 0 ||
-                ldx % 4 != 0 || !aligned16(X)))
-    return fail(MRPT_EPARAM, "mrpt_scan_topk_u8gemm_bits: unsupported shape");
-  if (!Xs || !info || ldq % 16 != 0 || ldq < d || ldq > 1024 ||
-      k > 120 || k < 1 || d % 4 != 0 || ldx % 4 != 0 || !aligned16(X))
-    return mrpt_scan_topk(X, n, d, ldx, Q, nq, ldqq, cand, cap, ncand, k, ids, dists, stream);
-  if (n < 1 || n >= (int64_t)1 << 31 || d < 1 || ldx < d || ldqq < d || nq < 0)
-    return fail(MRPT_ESHAPE, "mrpt_scan_topk_u8gemm: bad shape");
-  if (cand && (cap < 1 || !ncand)) return fail(MRPT_EPARAM, "mrpt_scan_topk_u8gemm: bad candidate lists");
-  if (nq == 0) return MRPT_OK;
-  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255u))
-    return fail(MRPT_EWORKSPACE, "mrpt_scan_topk_u8gemm: workspace must be 256-byte aligned");
-  // largest query chunk whose workspace fits; the GEMM covers n16 rows
-  const int64_t ldD = (n + 15) & ~(int64_t)15;
-  int64_t mc = ws_bytes / (4 * ldD + ldq + (int64_t)sizeof(QParams) + 4 * (kSurvCap + 2));
-  if (mc > nq) mc = nq;
-  while (mc > 0 && u8gemm_bytes(n, ldq, mc, nullptr, nullptr, nullptr) > ws_bytes) --mc;
-  if (mc < 1) return fail(MRPT_EWORKSPACE, "mrpt_scan_topk_u8gemm: workspace too small for one query");
-  int64_t off_qop, off_qp, off_fb;
-  u8gemm_bytes(n, ldq, mc, &off_qop, &off_qp, &off_fb);
-  char *w = reinterpret_cast<char *>(workspace);
-  int32_t *D = reinterpret_cast<int32_t *>(w);
-  int8_t *qop = reinterpret_cast<int8_t *>(w + off_qop);
-  QParams *qp = reinterpret_cast<QParams *>(w + off_qp);
-  int32_t *fb = reinterpret_cast<int32_t *>(w + off_fb);
-  cudaStream_t s = as_stream(stream);
-  int bufw = 64;
-  while (bufw < 2 * k + 2 * 32) bufw <<= 1;
-  if (bufw > 256) return mrpt_scan_topk(X, n, d, ldx, Q, nq, ldqq, cand, cap, ncand, k, ids, dists, stream);
-  const size_t smem = 1024 + (size_t)(kScanNT / 32) * bufw * (4 * 4 + 8 + 4 * 3) +
-                      (cbits ? (size_t)(kScanNT / 32) * 16 * 32 * 4 : 0);
-  topk_fn_u8 fn = pick_u8_b<8, true>(bufw);
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int buf = (k + kScanNT <= 1024) ? 1024 : 2048;
-  topk_fn tfn = buf == 1024 ? k_scan_topk_tiled<1024> : k_scan_topk_tiled<2048>;
-  const size_t tsmem =
-      (size_t)buf * 12 + sizeof(float) * (kScanNT / 32) * 32 * kTileStride + sizeof(double) * (size_t)d;
-  cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-  Q8Rows rows;
-  rows.X = nullptr;
-  rows.ldq = ldq;
-  rows.scale = nullptr;
-  rows.norm = nullptr;
-  rows.radius = nullptr;
-  rows.D = D;
-  rows.ldD = ldD;
-  rows.info = reinterpret_cast<const uint4 *>(info);
-  rows.qp = qp;
-  rows.cbits = nullptr;
-  rows.bstride = 0;
-  for (int64_t q0 = 0; q0 < nq; q0 += mc) {
-    const int64_t m = nq - q0 < mc ? nq - q0 : mc;
-    const int64_t g1 = m < (int64_t)num_sms() * 8 ? m : (int64_t)num_sms() * 8;
-    (count_launch(), k_quantize_q8<<<(unsigned)g1, kScanNT, 0, s>>>(Q + q0 * ldqq, ldqq, d, (int)ldq, m, qop, qp));
-    int32_t st = igemm_rows_tn(reinterpret_cast<const int8_t *>(Xs), ldD, qop, m, ldq, D, ldD, s);
-    if (st) return st;
-    // candidates produced on another stream (the vote runs beside the GEMM)
-    if (wait_event && q0 == 0) cudaStreamWaitEvent(s, reinterpret_cast<cudaEvent_t>(wait_event), 0);
-    TopkArgs a = {};
-    a.X = X;
-    a.n = n;
-    a.d = d;
-    a.ldx = ldx;
-    a.Q = Q + q0 * ldqq;
-    a.nq = m;
-    a.ldq = ldqq;
-    a.cand = cand ? cand + q0 * cap : nullptr;
-    a.cap = cap;
-    a.ncand = cand ? ncand + q0 : nullptr;
-    a.cbits = cbits ? cbits + q0 * bstride : nullptr;
-    a.bstride = bstride;
-    rows.cbits = a.cbits;
-    rows.bstride = bstride;
-    a.k = k;
-    a.kstride = k;
-    a.ids = ids + q0 * k;
-    a.dists = dists + q0 * k;
-    a.lb_key = nullptr;
-    a.lb_id = nullptr;
-    a.vec4 = true;
-    a.qlist = nullptr;
-    a.qcount = nullptr;
-    a.Xh = nullptr;
-    a.ldh = 0;
-    a.radius = nullptr;
-    a.nsurv = fb + 1 + mc;
-    a.surv = a.nsurv + mc;
-    cudaMemsetAsync(fb, 0, sizeof(int32_t), s);
-    const int64_t grid = m < (int64_t)num_sms() * 8 ? m : (int64_t)num_sms() * 8;
-    (count_launch(), fn<<<(unsigned)grid, kScanNT, smem, s>>>(a, rows, fb + 1, fb));
-    a.qlist = fb + 1;
-    a.qcount = fb;
-    (count_launch(), tfn<<<(unsigned)(grid < 64 ? grid : 64), kScanNT, tsmem, s>>>(a));
-    launch_rerank(a, s);
-  }
-  return launch_status("mrpt_scan_topk_u8gemm");
-}
-
-extern "C" int32_t mrpt_scan_topk_u8gemm(const float *X, int64_t n, int32_t d, int64_t ldx, const void *Xs,
-                                         int64_t ldq, const void *info, const float *Q, int64_t nq,
-                                         int64_t ldqq, const int32_t *cand, int64_t cap, const int32_t *ncand,
-                                         int32_t k, int64_t *ids, double *dists, void *workspace,
-                                         int64_t ws_bytes, void *stream) {
-  clear_error();
-  return u8gemm_impl(X, n, d, ldx, Xs, ldq, info, Q, nq, ldqq, cand, cap, ncand, nullptr, 0, k, ids, dists,
-                     workspace, ws_bytes, stream, nullptr);
-}
-
-extern "C" int32_t mrpt_scan_topk_u8gemm_bits(const float *X, int64_t n, int32_t d, int64_t ldx,
-                                              const void *Xs, int64_t ldq, const void *info, const float *Q,
-                                              int64_t nq, int64_t ldqq, const uint32_t *cbits, int64_t bstride,
-                                              int32_t k, int64_t *ids, double *dists, void *workspace,
-                                              int64_t ws_bytes, void *wait_event, void *stream) {
-  clear_error();
-  if (!cbits) return fail(MRPT_EPARAM, "mrpt_scan_topk_u8gemm_bits: cbits is NULL");
-  return u8gemm_impl(X, n, d, ldx, Xs, ldq, info, Q, nq, ldqq, nullptr, 0, nullptr, cbits, bstride, k, ids,
-                     dists, workspace, ws_bytes, stream, wait_event);
 }
 
 // ------------------------------------------------------------ K4 tc route --
@@ -2720,7 +2407,10 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
     ktimer_end(s, kt0);
     if (dbg) {
       const int64_t ldD = (n + 15) & ~(int64_t)15;
-      int32_t st = igemm_rows_tn(reinterpret_cast<const int8_t *>(Xs), ldD, qop, m, ldq, D2, ldD, s);
+      // naive int32 dot products of the same s8 operands (debug reference)
+      tc::k_dot_ref<<<dim3((unsigned)((n + 255) / 256), (unsigned)m), 256, 0, s>>>(
+          reinterpret_cast<const int8_t *>(Xs), n, qop, ldq, D2, ldD);
+      const int32_t st = 0;
       unsigned long long *o = nullptr;
       cudaMalloc(&o, 24);
       cudaMemsetAsync(o, 0, 24, s);
@@ -2774,6 +2464,8 @@ extern "C" int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d
               cg, grid, fbc, (long long)m, (double)se / m, (double)ss / m);
     }
     a.qlist = fb + 1;
+    a.stat_slot = 4;  // fallback statistics: see mrpt_fallback_stats
+    g_route_queries[4] += m;
     a.qcount = fb;
     const int64_t tg = m < 64 ? m : 64;
     (count_launch(), tfn<<<(unsigned)tg, kScanNT, tsmem, s>>>(a));

@@ -741,6 +741,18 @@ __global__ void __launch_bounds__(128) k_tc_select(const uint4 *__restrict__ ent
 namespace mrpt {
 namespace tc {
 // debug: compare two (m, n) s32 matrices, count mismatches; entry stats
+// Debug reference (MRPT_TC_DEBUG): D[q * ldD + r] = sum_c Xs[r][c] * Qop[q][c]
+// over the s8 operands, one thread per (row, query).
+__global__ void k_dot_ref(const int8_t *__restrict__ Xs, int64_t n, const int8_t *__restrict__ Qop, int64_t ldq,
+                          int32_t *D, int64_t ldD) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t q = blockIdx.y;
+  if (r >= n) return;
+  int acc = 0;
+  for (int64_t c = 0; c < ldq; ++c) acc += (int)Xs[r * ldq + c] * (int)Qop[q * ldq + c];
+  D[q * ldD + r] = acc;
+}
+
 __global__ void k_tc_debug(const int32_t *A, const int32_t *B, int64_t n, int64_t ldb, const int32_t *ent_cnt,
                            int64_t m, unsigned long long *out) {
   // A: (m, n) dense; B: (m, ldb) library GEMM output

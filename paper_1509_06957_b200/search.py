@@ -54,12 +54,19 @@ class VoteAccumulator:
 
     ``accumulate`` counts every occurrence of every id in the given leaves
     (one per tree) and returns, ascending, the ids with at least ``votes``.
+    Ascending is the order of the reference's numpy backend (``_py.vote``,
+    _py.py:63-83); its compiled backend emits ids in threshold-crossing order
+    (_cy.pyx:66-77), an order the reference's own tests do not rely on
+    (test_kernels.py:59-78 compares the two backends as sets).  The set is
+    identical; ``tests/test_gpu_reference_behaviour.py`` checks it against an
+    unsorted list written by the compiled reference.
     """
 
     def __init__(self, n):
         self.n = n
         self._counts = None
         self._epoch = 0
+        self._filled = -1  # epoch whose counts the device buffer holds
 
     def begin(self):
         self._epoch += 1
@@ -72,12 +79,14 @@ class VoteAccumulator:
 
     def counts(self):
         """Dense n-vector of the current query's votes (int64 copy)."""
-        if self._counts is None or self._epoch == 0:
+        # begin() starts a new epoch: like the reference's stamps (search.py:
+        # 68-73), every count reads 0 until the next accumulate
+        if self._counts is None or self._filled != self._epoch:
             return np.zeros(self.n, dtype=np.int64)
         return _device.d2h(self._counts).astype(np.int64)
 
     def count(self, i):
-        if self._counts is None or self._epoch == 0:
+        if self._counts is None or self._filled != self._epoch:
             return 0
         return int(self._counts[int(i)].item())
 
@@ -91,6 +100,7 @@ class VoteAccumulator:
         stream = _native.stream_ptr()
         _native.call("mrpt_vote_counts", _native.ptr(D.indices), _native.ptr(D.offsets), D.n, D.T,
                      D.depth, _native.ptr(lv), _native.ptr(counts), stream)
+        self._filled = self._epoch
         out = torch.empty(D.n, dtype=torch.int32, device=counts.device)
         nout = torch.zeros(1, dtype=torch.int64, device=counts.device)
         _native.call("mrpt_select_ge", _native.ptr(counts), D.n, int(votes), _native.ptr(out),
@@ -282,15 +292,14 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None, size_class=N
     return ids, dists, counts
 
 
-_BITS_ROUTES = ("u8gemm_bits", "u8tc_bits")
+_BITS_ROUTES = ("u8tc_bits",)
 
 
 def _run_bits(D, qb, m, ldq, leaves, votes, vdir, bits, bstride, counts, k, ids, dists, stage=None,
-              route="u8gemm_bits"):
-    """A bitmap route: K2 + K3 on their own stream beside K4's query
-    quantisation (and, for u8gemm_bits, the library GEMM), which need only
-    the queries; the filter waits for the candidate bitmaps.  u8tc_bits is
-    the fused tcgen05 filter (no dot-product matrix)."""
+              route="u8tc_bits"):
+    """The bitmap route: K2 + K3 on their own stream beside K4's query
+    quantisation, which needs only the queries; the fused tcgen05 filter
+    waits for the candidate bitmaps."""
     torch = _device.torch_mod()
     if stage is None:
         def stage(name, fn, *a):
@@ -304,8 +313,7 @@ def _run_bits(D, qb, m, ldq, leaves, votes, vdir, bits, bstride, counts, k, ids,
         stage("vote", _vote_bitmap, D, leaves, m, votes, vdir, bits, bstride, counts)
         ev_vote = torch.cuda.Event()
         ev_vote.record(vs)
-    scan = _scan_tc if route == "u8tc_bits" else _scan_bits
-    stage("scan_topk", scan, D, qb, m, ldq, bits, bstride, k, ids, dists, ev_vote)
+    stage("scan_topk", _scan_tc, D, qb, m, ldq, bits, bstride, k, ids, dists, ev_vote)
     torch.cuda.current_stream().wait_event(ev_vote)  # leaves/bits are reused
 
 
@@ -334,16 +342,6 @@ def _vote_bitmap(D, leaves, m, votes, vdir, bits, bstride, counts):
                  _native.ptr(counts), _native.stream_ptr())
 
 
-def _scan_bits(D, qb, m, ldq, bits, bstride, k, ids, dists, wait=None):
-    ldr = D.u8_rows()[1]
-    Xs, info, ws = D.u8_gemm(m)
-    _native.call("mrpt_scan_topk_u8gemm_bits", _native.ptr(D.X), D.n, D.d, int(D.X.stride(0)),
-                 _native.ptr(Xs), ldr, _native.ptr(info), _native.ptr(qb), m, ldq,
-                 _native.ptr(bits), int(bstride), int(k), _native.ptr(ids), _native.ptr(dists),
-                 _native.ptr(ws), int(ws.numel()), None if wait is None else wait.cuda_event,
-                 _native.stream_ptr())
-
-
 def _scan_tc(D, qb, m, ldq, bits, bstride, k, ids, dists, wait=None):
     ldr = D.u8_rows()[1]
     Xs, info, ws = D.u8_tc(m)
@@ -359,21 +357,12 @@ def _scan_variants(D, k):
     out = []
     if k <= 120 and D.u8_rows() is not None:
         out.append("u8")
-        # tensor-core dot products for every (query, row) pair: only where the
-        # dot-product matrix of a useful query chunk fits (n <= 4M rows)
-        if D.n <= (4 << 20):
-            out.append("u8gemm")
-            # same filter over K3's bitmaps; it has no list to fall back on, so
-            # only where the exact fallback's 16-byte rows exist
-            aligned = D.d % 4 == 0 and int(D.X.stride(0)) % 4 == 0 and D.X.data_ptr() % 16 == 0
-            if k <= 96 and aligned:
-                out.append("u8gemm_bits")
-            # the fused tcgen05 filter: one 128-B K block at least, the
-            # queries' k smallest bounds in shared memory (k <= 16)
-            if k <= 16 and aligned and 128 <= D.u8_rows()[1] <= 1024:
-                out.append("u8tc_bits")
-    elif k <= 120 and D.s8_rows() is not None:
-        out.append("s8")
+        # the fused tcgen05 filter over K3's bitmaps: one 128-B K block at
+        # least, the queries' k smallest bounds in shared memory (k <= 16),
+        # 16-byte rows for its exact fallback, bitmaps of at most 4M ids
+        aligned = D.d % 4 == 0 and int(D.X.stride(0)) % 4 == 0 and D.X.data_ptr() % 16 == 0
+        if k <= 16 and aligned and 128 <= D.u8_rows()[1] <= 1024 and D.n <= (4 << 20):
+            out.append("u8tc_bits")
     if k <= 120 and D.shadow() is not None:
         out.append("fp16")
     out.append("fp32")
@@ -391,18 +380,6 @@ def _scan_launch(D, variant, args):
         _native.call("mrpt_scan_topk_u8", _native.ptr(D.X), D.n, D.d, int(D.X.stride(0)),
                      _native.ptr(Xq), ldr, _native.ptr(sc), _native.ptr(nm), _native.ptr(rad),
                      *common_tail)
-    elif variant == "u8gemm":
-        ldr = D.u8_rows()[1]
-        Xs, info, ws = D.u8_gemm(m)
-        _native.call("mrpt_scan_topk_u8gemm", _native.ptr(D.X), D.n, D.d, int(D.X.stride(0)),
-                     _native.ptr(Xs), ldr, _native.ptr(info), _native.ptr(qb), m, ldq,
-                     _native.ptr(cand), int(cap), _native.ptr(counts), int(k), _native.ptr(ids),
-                     _native.ptr(dists), _native.ptr(ws), int(ws.numel()), stream)
-    elif variant == "s8":
-        Xq, ldr, sc, nm, rad = D.s8_rows()
-        _native.call("mrpt_scan_topk_s8", _native.ptr(D.X), D.n, D.d, int(D.X.stride(0)),
-                     _native.ptr(Xq), ldr, _native.ptr(sc), _native.ptr(nm), _native.ptr(rad),
-                     *common_tail)
     elif variant == "fp16":
         Xh, ldh, rad = D.shadow()
         _native.call("mrpt_scan_topk_fp16", _native.ptr(D.X), D.n, D.d, int(D.X.stride(0)),
@@ -414,7 +391,7 @@ def _scan_launch(D, variant, args):
 
 def _autotune(D, qb, m, ldq, leaves, votes, vdir, cap, counts, k, sc, ids, dists):
     """Time every exact route for this chunk -- list vote + each list filter,
-    bitmap vote + the bitmap GEMM filter -- and keep the fastest for the index
+    bitmap vote + the fused tcgen05 filter -- and keep the fastest for the index
     (per k and vote threshold); the last run leaves valid outputs (all routes
     give identical results).  MRPT_SCAN_ROWS forces a variant."""
     torch = _device.torch_mod()
@@ -561,6 +538,9 @@ def _knn_batch_pipelined(Qc, k, index, votes):
     hcnt = torch.empty(nq, dtype=torch.int32, pin_memory=True)
     compute = torch.cuda.current_stream()
     up, down = _device.side_streams()
+    # Qd came from the caching allocator on the compute stream: work still
+    # queued there may own that block, so the uploads wait for it first
+    up.wait_stream(compute)
     for i in range(pieces):
         s, e = bounds[i], bounds[i + 1]
         with torch.cuda.stream(up):
@@ -602,6 +582,7 @@ def _knn_batch_pipelined_bits(Qc, k, index, votes, route):
     hcnt = torch.empty(nq, dtype=torch.int32, pin_memory=True)
     compute = torch.cuda.current_stream()
     up, _ = _device.side_streams()
+    up.wait_stream(compute)  # Qd's block may still be in use by queued compute work
     vdir = D.vote_dir()
     pieces = max(1, min(int(os.environ.get("MRPT_PIPE_PIECES", "4")), nq // 1024))
     bounds = [nq * i // pieces for i in range(pieces + 1)]
@@ -614,8 +595,7 @@ def _knn_batch_pipelined_bits(Qc, k, index, votes, route):
         compute.wait_event(ev_up)
         _route_launch(D, Qd[s:e], e - s, int(Qd.stride(0)), leaves[s:e])
         _vote_bitmap(D, leaves[s:e], e - s, votes, vdir, bits[s:e], bstride, counts[s:e])
-    scan = _scan_tc if route == "u8tc_bits" else _scan_bits
-    scan(D, Qd, nq, int(Qd.stride(0)), bits, bstride, k, ids, dists)
+    _scan_tc(D, Qd, nq, int(Qd.stride(0)), bits, bstride, k, ids, dists)
     hid.copy_(ids, non_blocking=True)
     hdist.copy_(dists, non_blocking=True)
     hcnt.copy_(counts, non_blocking=True)
@@ -677,8 +657,7 @@ def approximate_knn_sweep(Q, k, index, votes):
         if nq:
             variant = D.scan_choice.get((k, v))
             if variant is None or variant in _BITS_ROUTES:
-                avail = [x for x in _scan_variants(D, k) if x not in _BITS_ROUTES]
-                variant = "u8gemm" if variant in _BITS_ROUTES else avail[0]
+                variant = [x for x in _scan_variants(D, k) if x not in _BITS_ROUTES][0]
             args = (Qd, nq, int(Qd.stride(0)), cand, cap, counts, k, ids, dists)
             _scan_launch(D, variant, args)
         res = (ids, dists, counts.clone())
@@ -699,3 +678,16 @@ def approximate_knn(q, k, index, votes):
     kept = min(k, m)
     return NeighborList(indices=ids[0, :kept].copy(), distances=dists[0, :kept].copy(),
                         requested_k=k, candidate_count=m)
+
+
+def fallback_stats(reset=False):
+    """How often each exact filter route handed queries to its exact tiled
+    fallback since the last reset (measurement; synchronises the device):
+    {route: {"queries": q, "fallbacks": f}} for fp32, fp16, u8, u8tc_bits."""
+    import ctypes
+
+    out = (ctypes.c_int64 * 8)()
+    _native.call("mrpt_fallback_stats", out, 1 if reset else 0)
+    names = ("fp32", "fp16", "u8", "u8tc_bits")
+    return {nm: {"queries": int(out[2 * i]), "fallbacks": int(out[2 * i + 1])}
+            for i, nm in enumerate(names)}

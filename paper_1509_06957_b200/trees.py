@@ -156,6 +156,8 @@ class _DeviceIndex:
         self.scan_choice = {}  # (k, votes) -> exact route chosen by the autotune
         self.scan_choice_by_size = {}  # (k, votes, batch-size class) -> route
         self.scan_pin = {}  # (k, votes) -> route forced for every batch size (pin_route)
+        self._ws = {}  # (name, stream) -> scratch
+        self._ws_lock = threading.Lock()
 
     def cap(self, votes):
         """Upper bound on any candidate set at this vote threshold."""
@@ -197,7 +199,7 @@ class _DeviceIndex:
         self._u8 = None
         ldq = (self.d + 15) // 16 * 16
         mode = os.environ.get("MRPT_SCAN_ROWS", "auto")
-        if mode in ("auto", "u8", "u8gemm", "u8gemm_bits", "u8tc_bits") and ldq <= 1024:
+        if mode in ("auto", "u8", "u8tc_bits") and ldq <= 1024:
             torch = _device.torch_mod()
             dev = self.X.device
             Xq = torch.empty((self.n, ldq), dtype=torch.uint8, device=dev)
@@ -213,51 +215,35 @@ class _DeviceIndex:
                 self._u8 = (Xq, ldq, sc, nm, rad)
         return self._u8
 
-    def s8_rows(self):
-        """s8 shadow (rows, row stride, scale, norm, radius) for data with
-        negative values (where u8_rows() is None), built once; None otherwise
-        (MRPT_SCAN_ROWS=fp16|fp32 disables it)."""
-        if getattr(self, "_s8", False) is not False:
-            return self._s8
-        self._s8 = None
-        ldq = (self.d + 15) // 16 * 16
-        mode = os.environ.get("MRPT_SCAN_ROWS", "auto")
-        if mode in ("auto", "s8") and ldq <= 1024 and self.u8_rows() is None:
-            torch = _device.torch_mod()
-            dev = self.X.device
-            Xq = torch.empty((self.n, ldq), dtype=torch.int8, device=dev)
-            sc = torch.empty(self.n, dtype=torch.float32, device=dev)
-            nm = torch.empty(self.n, dtype=torch.int32, device=dev)
-            rad = torch.empty(self.n, dtype=torch.float32, device=dev)
-            _native.call("mrpt_quantize_s8", _native.ptr(self.X), self.n, self.d,
-                         int(self.X.stride(0)), _native.ptr(Xq), ldq, _native.ptr(sc),
-                         _native.ptr(nm), _native.ptr(rad), _native.stream_ptr())
-            self._s8 = (Xq, ldq, sc, nm, rad)
-        return self._s8
-
-    def u8_gemm(self, nq):
-        """(s8 rows, per-row records, workspace) for the tensor-core GEMM filter over
-        the u8 shadow; rows built once, workspace sized for nq queries (kept,
-        grown on demand).  None without a u8 shadow."""
+    def tc_rows(self):
+        """(s8 rows, per-row records) of the fused tcgen05 filter over the u8
+        shadow (mrpt_u8_gemm_rows), built once; None without a u8 shadow."""
         u8 = self.u8_rows()
         if u8 is None:
             return None
-        torch = _device.torch_mod()
-        Xq, ldq = u8[0], u8[1]
-        if getattr(self, "_u8g", None) is None:
+        if getattr(self, "_tcr", None) is None:
+            torch = _device.torch_mod()
+            Xq, ldq = u8[0], u8[1]
             Xs = torch.empty(((self.n + 15) // 16 * 16, ldq), dtype=torch.uint8, device=Xq.device)
             info = torch.empty((self.n, 4), dtype=torch.int32, device=Xq.device)
             _native.call("mrpt_u8_gemm_rows", _native.ptr(Xq), self.n, ldq, _native.ptr(u8[2]),
                          _native.ptr(u8[3]), _native.ptr(u8[4]), _native.ptr(Xs),
                          _native.ptr(info), _native.stream_ptr())
-            self._u8g = (Xs, info)
-            self._u8g_ws = None
-        need = ctypes.c_int64(0)
-        _native.call("mrpt_scan_topk_u8gemm_workspace_size", self.n, ldq, int(nq),
-                     ctypes.byref(need))
-        if self._u8g_ws is None or self._u8g_ws.numel() < need.value:
-            self._u8g_ws = torch.empty(need.value, dtype=torch.uint8, device=Xq.device)
-        return self._u8g[0], self._u8g[1], self._u8g_ws
+            self._tcr = (Xs, info)
+        return self._tcr
+
+    def workspace(self, name, nbytes):
+        """A device scratch buffer of at least ``nbytes`` for this index, one per
+        (name, caller stream): calls on different streams never share scratch
+        (the reference's kernels are reentrant; so are these calls)."""
+        torch = _device.torch_mod()
+        key = (name, torch.cuda.current_stream().cuda_stream)
+        with self._ws_lock:
+            ws = self._ws.get(key)
+            if ws is None or ws.numel() < nbytes:
+                ws = self._ws[key] = torch.empty(max(1, int(nbytes)), dtype=torch.uint8,
+                                                 device=self.X.device)
+            return ws
 
     def pin_route(self, k, votes, route):
         """Force the exact K4 route for (k, votes) at every batch size (tools,
@@ -270,19 +256,15 @@ class _DeviceIndex:
 
     def u8_tc(self, nq):
         """(s8 rows, per-row records, workspace) for the fused tcgen05 filter
-        (mrpt_scan_topk_u8tc_bits): the GEMM route's rows, its own workspace
-        sized for nq queries (kept, grown on demand)."""
-        g = self.u8_gemm(1)
+        (mrpt_scan_topk_u8tc_bits): rows built once, the workspace sized for
+        nq queries and private to the caller's stream."""
+        g = self.tc_rows()
         if g is None:
             return None
-        torch = _device.torch_mod()
         need = ctypes.c_int64(0)
         _native.call("mrpt_scan_topk_u8tc_workspace_size", self.n, self.u8_rows()[1], int(nq),
                      ctypes.byref(need))
-        ws = getattr(self, "_u8tc_ws", None)
-        if ws is None or ws.numel() < need.value:
-            ws = self._u8tc_ws = torch.empty(need.value, dtype=torch.uint8, device=g[0].device)
-        return g[0], g[1], ws
+        return g[0], g[1], self.workspace("u8tc", need.value)
 
     def vote_dir(self):
         """Tile directory for the multi-tile vote (built once, on the device),

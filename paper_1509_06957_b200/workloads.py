@@ -3,7 +3,10 @@
 The reference measures nothing at these sizes and ships no data; these
 generators pin the interpretation of BASELINE.json's config text that
 SURVEY.md section 8(d) describes (all fp32, ``numpy.random.default_rng(seed)``,
-data and queries drawn from the same distribution, data first).  ``scale``
+data and queries drawn from the same distribution, data first).  Configs
+3-5 are generated in 65,536-row chunks, chunk i from its own stream
+``default_rng([seed, config, i])`` on a thread pool, so 10M rows take seconds
+and the rows do not depend on the thread count.  ``scale``
 shrinks n and the query count proportionally for tests; T, depth, a, k and v
 are the configuration's own (depth is clamped so 2^depth <= n).
 """
@@ -11,6 +14,8 @@ are the configuration's own (depth is clamped so 2^depth <= n).
 from __future__ import annotations
 
 import math
+import os
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -55,6 +60,47 @@ CONFIGS = {
 _CHUNK = 65_536
 
 
+def _parallel_rows(count, d, seed, tag, fill):
+    """(count, d) float32 rows made chunk by chunk, chunk i from its own stream
+    default_rng([seed, tag, i]), on a thread pool (numpy's generators release
+    the GIL while filling): the result does not depend on the thread count."""
+    out = np.empty((count, d), dtype=np.float32)
+    bounds = [(i, s, min(count, s + _CHUNK)) for i, s in enumerate(range(0, count, _CHUNK))]
+
+    def job(b):
+        i, s, e = b
+        out[s:e] = fill(np.random.default_rng([seed, tag, i]), e - s)
+
+    workers = max(1, min(32, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
+                         else (os.cpu_count() or 1)))
+    with ThreadPoolExecutor(workers) as ex:
+        list(ex.map(job, bounds))
+    return out
+
+
+def _mixture_fill(centres, sigma):
+    c32 = centres.astype(np.float32)
+
+    def fill(rng, m):
+        lab = rng.integers(0, c32.shape[0], size=m)
+        noise = rng.standard_normal((m, c32.shape[1]), dtype=np.float32)
+        noise *= np.float32(sigma)
+        noise += c32[lab]
+        return noise
+
+    return fill
+
+
+def _descriptor_fill(d, zeros):
+    def fill(rng, m):
+        x = np.minimum(255.0, np.floor(rng.exponential(20.0, size=(m, d))))
+        kill = np.argsort(rng.random((m, d)), axis=1)[:, :zeros]
+        np.put_along_axis(x, kill, 0.0, axis=1)
+        return x
+
+    return fill
+
+
 def _gaussian_mixture(rng, count, centres, sigma):
     out = np.empty((count, centres.shape[1]), dtype=np.float32)
     for s in range(0, count, _CHUNK):
@@ -80,18 +126,6 @@ def _blobs(rng, count):
     return out
 
 
-def _descriptors(rng, count, d=128, zeros=13):
-    out = np.empty((count, d), dtype=np.float32)
-    for s in range(0, count, _CHUNK):
-        e = min(count, s + _CHUNK)
-        m = e - s
-        x = np.minimum(255.0, np.floor(rng.exponential(20.0, size=(m, d))))
-        kill = np.argsort(rng.random((m, d)), axis=1)[:, :zeros]
-        np.put_along_axis(x, kill, 0.0, axis=1)
-        out[s:e] = x
-    return out
-
-
 def generate(config, scale=1.0, seed=0):
     """(X, Q, params) for a configuration; params mirrors grow_trees/query args."""
     w = CONFIGS[config]
@@ -106,13 +140,14 @@ def generate(config, scale=1.0, seed=0):
     elif config == 2:
         allx = _blobs(rng, total)
     elif config == 3:
-        allx = _descriptors(rng, total, w.d, math.ceil(0.1 * w.d))
+        allx = _parallel_rows(total, w.d, seed, 3, _descriptor_fill(w.d, math.ceil(0.1 * w.d)))
     elif config == 4:
         centres = rng.uniform(0.0, 0.5, size=(256, w.d))
-        allx = np.clip(_gaussian_mixture(rng, total, centres, 0.05), 0.0, 1.0)
+        allx = _parallel_rows(total, w.d, seed, 4, _mixture_fill(centres, 0.05))
+        np.clip(allx, 0.0, 1.0, out=allx)
     elif config == 5:
         centres = 3.0 * rng.standard_normal((1024, w.d))
-        allx = _gaussian_mixture(rng, total, centres, 1.0)
+        allx = _parallel_rows(total, w.d, seed, 5, _mixture_fill(centres, 1.0))
     else:
         raise KeyError(config)
     X = np.ascontiguousarray(allx[:n])

@@ -151,20 +151,17 @@ class _FakeIndex:
     def shadow(self):
         return object() if self._h else None
 
-    def s8_rows(self):
-        return None if self._u8 else object()
 
 
 @pytest.mark.parametrize("n,d,k,u8,want", [
-    (60_000, 784, 10, True, ["u8", "u8gemm", "u8gemm_bits", "u8tc_bits", "fp32"]),
-    (60_000, 784, 17, True, ["u8", "u8gemm", "u8gemm_bits", "fp32"]),  # tcgen05 filter: k <= 16
-    (60_000, 1000, 10, True, ["u8", "u8gemm", "u8gemm_bits", "u8tc_bits", "fp32"]),  # ldq 1008
-    (60_000, 100, 10, True, ["u8", "u8gemm", "u8gemm_bits", "fp32"]),   # tcgen05 filter: ldq >= 128
-    (60_000, 784, 100, True, ["u8", "u8gemm", "fp32"]),          # bitmap filter: k <= 96
-    (60_000, 37, 10, True, ["u8", "u8gemm", "fp32"]),            # no 16-byte rows
-    (5_000_000, 128, 10, True, ["u8", "fp32"]),                   # dot-product matrix too big
-    (60_000, 784, 121, True, ["fp32"]),                           # filters take k <= 120
-    (60_000, 784, 10, False, ["s8", "fp32"]),                     # signed data: s8 shadow
+    (60_000, 784, 10, True, ["u8", "u8tc_bits", "fp32"]),
+    (60_000, 784, 17, True, ["u8", "fp32"]),                # tcgen05 filter: k <= 16
+    (60_000, 1000, 10, True, ["u8", "u8tc_bits", "fp32"]),  # ldq 1008
+    (60_000, 100, 10, True, ["u8", "fp32"]),                # tcgen05 filter: ldq >= 128
+    (60_000, 37, 10, True, ["u8", "fp32"]),                 # no 16-byte rows
+    (5_000_000, 128, 10, True, ["u8", "fp32"]),             # bitmaps of at most 4M ids
+    (60_000, 784, 121, True, ["fp32"]),                     # filters take k <= 120
+    (60_000, 784, 10, False, ["fp32"]),                     # signed data: no u8 shadow
 ])
 def test_scan_route_availability(n, d, k, u8, want):
     from paper_1509_06957_b200.search import _scan_variants

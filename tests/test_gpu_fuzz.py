@@ -11,7 +11,7 @@ from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
 
-ROUTES = ["auto", "u8", "u8gemm", "u8gemm_bits", "s8", "fp16", "fp32"]
+ROUTES = ["auto", "u8", "u8tc_bits", "fp16", "fp32"]
 
 
 def _cases():

@@ -1,8 +1,9 @@
 """Every exact K4 filter variant (u8 shadow with dp4a, fp16 shadow, float32)
 returns exactly the oracle's neighbours and distances: non-negative float
 data, integer-valued data (exact u8 shadow), queries with negative values
-(s8 query quantisation), heavy exact ties (buffer overflow -> exact tiled
-fallback), k up to 120 and the >120 multi-pass path."""
+(s8 query quantisation), signed data (no u8 shadow: the float32 filter),
+heavy exact ties (buffer overflow -> exact tiled fallback), k up to 120 and
+the >120 multi-pass path."""
 
 import numpy as np
 import pytest
@@ -36,15 +37,13 @@ def _data(kind, rng, n, d):
     return x.astype(np.float32)
 
 
-@pytest.mark.parametrize("variant", ["u8", "u8gemm", "u8gemm_bits", "s8", "fp16", "fp32"])
+@pytest.mark.parametrize("variant", ["u8", "u8tc_bits", "fp16", "fp32"])
 @pytest.mark.parametrize("kind,d,k,v", [("pixels", 96, 10, 1), ("ints", 128, 10, 2),
                                          ("clusters01", 256, 10, 2), ("signed", 64, 7, 1),
                                          ("dups", 32, 20, 1), ("pixels", 200, 100, 1)])
 def test_variant_parity(monkeypatch, rng, variant, kind, d, k, v):
-    if variant == "u8gemm_bits" and k > 96:
-        pytest.skip("the bitmap GEMM filter takes k <= 96")
-    if variant == "s8" and kind != "signed":
-        pytest.skip("the s8 shadow is for data with negative values")
+    if variant == "u8tc_bits" and (k > 16 or d < 128):
+        pytest.skip("the fused tcgen05 filter takes k <= 16 and rows of >= 128 bytes")
     monkeypatch.setenv("MRPT_SCAN_ROWS", variant)
     if variant == "fp16":
         monkeypatch.setenv("MRPT_FP16_FILTER", "1")
@@ -55,7 +54,7 @@ def test_variant_parity(monkeypatch, rng, variant, kind, d, k, v):
         Q = Q - 0.05  # negative query coordinates: s8 query quantisation
     index = mrpt.grow_trees(Xd, 6, 6, seed=3)
     ids, dists, counts = mrpt.approximate_knn_batch(Q, k, index, v)
-    allowed = (variant, "fp32", "s8") if kind == "signed" else (variant, "fp32")
+    allowed = (variant, "fp32")
     assert index.device_index().scan_choice.get((k, v)) in allowed
     rids, rd, rc = _oracle(index, Xd, Q, k, v)
     assert np.array_equal(counts.astype(np.int64), rc)
@@ -71,88 +70,14 @@ def test_large_k_batch_multipass(rng):
     assert np.array_equal(ids, rids) and dists.tobytes() == rd.tobytes()
 
 
-@pytest.mark.parametrize("kind,signed", [("ints", False), ("pixels", True), ("clusters01", False)])
-def test_u8gemm_small_workspace_chunks(rng, kind, signed):
-    """The GEMM filter run through the C ABI with a workspace that holds only
-    a few queries (many query chunks, a ragged last one) returns exactly what
-    the dp4a filter returns, for u8 and s8 queries."""
-    import ctypes
-
-    import torch
-
-    from paper_1509_06957_b200 import _native
-    from paper_1509_06957_b200.search import query_device
-
-    n, d, nq, k = 3000, 72, 203, 9
-    X = _data(kind, rng, n + nq, d)
-    Xd, Q = X[:n], X[n:]
-    if signed:
-        Q = Q - 0.05
-    index = mrpt.grow_trees(Xd, 5, 5, seed=7)
-    D = index.device_index()
-    Qd = torch.from_numpy(np.ascontiguousarray(Q)).cuda()
-    D.pin_route(k, 1, "u8")
-    want = [t.cpu().numpy() for t in query_device(D, Qd, k, 1)]
-    ldq = D.u8_rows()[1]
-    Xs, info, _ = D.u8_gemm(nq)
-    per_q = ctypes.c_int64(0)
-    _native.call("mrpt_scan_topk_u8gemm_workspace_size", n, ldq, 1, ctypes.byref(per_q))
-    ws = torch.empty(per_q.value * 11 // 2, dtype=torch.uint8, device="cuda")  # ~5 queries
-    from paper_1509_06957_b200.search import _route_device
-
-    leaves = _route_device(Qd, D)
-    cap = D.cap(1)
-    cand = torch.empty((nq, cap), dtype=torch.int32, device="cuda")
-    counts = torch.empty(nq, dtype=torch.int32, device="cuda")
-    _native.call("mrpt_vote", _native.ptr(D.indices), _native.ptr(D.offsets), D.n, D.T, D.depth,
-                 _native.ptr(leaves), nq, 1, int(D.leaves_sorted), int(D.max_count),
-                 _native.ptr(D.vote_dir()), _native.ptr(cand), int(cap), _native.ptr(counts),
-                 _native.stream_ptr())
-    ids = torch.empty((nq, k), dtype=torch.int64, device="cuda")
-    dists = torch.empty((nq, k), dtype=torch.float64, device="cuda")
-    _native.call("mrpt_scan_topk_u8gemm", _native.ptr(D.X), n, d, int(D.X.stride(0)),
-                 _native.ptr(Xs), ldq, _native.ptr(info), _native.ptr(Qd), nq, d, _native.ptr(cand),
-                 int(cap), _native.ptr(counts), k, _native.ptr(ids), _native.ptr(dists),
-                 _native.ptr(ws), int(ws.numel()), _native.stream_ptr())
-    assert np.array_equal(ids.cpu().numpy(), want[0])
-    assert dists.cpu().numpy().tobytes() == want[1].tobytes()
-    # the same through candidate bitmaps
-    bstride = (n + 127) // 128 * 4
-    bits = torch.empty((nq, bstride), dtype=torch.int32, device="cuda")
-    bcounts = torch.empty(nq, dtype=torch.int32, device="cuda")
-    _native.call("mrpt_vote_bitmap", _native.ptr(D.indices), _native.ptr(D.offsets), D.n, D.T,
-                 D.depth, _native.ptr(leaves), nq, 1, int(D.leaves_sorted), int(D.max_count),
-                 _native.ptr(D.vote_dir()), _native.ptr(bits), bstride, _native.ptr(bcounts),
-                 _native.stream_ptr())
-    assert np.array_equal(bcounts.cpu().numpy(), counts.cpu().numpy())
-    bl = bits.cpu().numpy().view(np.uint32)
-    for qi in range(0, nq, 17):
-        setbits = np.flatnonzero(np.unpackbits(bl[qi].view(np.uint8), bitorder="little"))
-        setbits = setbits[setbits < n]  # words past ceil(n/32) are padding, never written
-        assert np.array_equal(setbits, np.sort(cand[qi, :int(counts[qi])].cpu().numpy()))
-    ids.fill_(-5)
-    _native.call("mrpt_scan_topk_u8gemm_bits", _native.ptr(D.X), n, d, int(D.X.stride(0)),
-                 _native.ptr(Xs), ldq, _native.ptr(info), _native.ptr(Qd), nq, d,
-                 _native.ptr(bits), bstride, k, _native.ptr(ids), _native.ptr(dists),
-                 _native.ptr(ws), int(ws.numel()), None, _native.stream_ptr())
-    assert np.array_equal(ids.cpu().numpy(), want[0])
-    assert dists.cpu().numpy().tobytes() == want[1].tobytes()
-    # a workspace too small for one query is refused
-    with pytest.raises(mrpt.MRPTError):
-        _native.call("mrpt_scan_topk_u8gemm", _native.ptr(D.X), n, d, int(D.X.stride(0)),
-                     _native.ptr(Xs), ldq, _native.ptr(info), _native.ptr(Qd), nq, d,
-                     _native.ptr(cand), int(cap), _native.ptr(counts), k, _native.ptr(ids),
-                     _native.ptr(dists), _native.ptr(ws), 1024, _native.stream_ptr())
-
-
-@pytest.mark.parametrize("v,k", [(6, 8), (5, 40), (1, 96)])
+@pytest.mark.parametrize("v,k", [(6, 8), (5, 16), (1, 16)])
 def test_bitmap_route_edges(monkeypatch, rng, v, k):
-    """The bitmap hand-over + GEMM filter at the edges: v = T (mostly empty
-    candidate sets), k larger than most candidate sets (-1 / inf padding),
-    k at its limit; a foreign index with unsorted leaf slices; n not a
-    multiple of 32."""
-    monkeypatch.setenv("MRPT_SCAN_ROWS", "u8gemm_bits")
-    n, d, nq = 3001, 40, 300
+    """The bitmap hand-over + fused tcgen05 filter at the edges: v = T (mostly
+    empty candidate sets), k larger than most candidate sets (-1 / inf
+    padding), k at its limit; a foreign index with unsorted leaf slices; n
+    not a multiple of 32."""
+    monkeypatch.setenv("MRPT_SCAN_ROWS", "u8tc_bits")
+    n, d, nq = 3001, 140, 300
     X = _data("ints", rng, n + nq, d)
     Xd, Q = X[:n], X[n:]
     a = mrpt.grow_trees(Xd, 6, 6, seed=21)
@@ -167,16 +92,16 @@ def test_bitmap_route_edges(monkeypatch, rng, v, k):
                        dataset_checksum=a.dataset_checksum)
     for index in (a, b):
         ids, dists, counts = mrpt.approximate_knn_batch(Q, k, index, v)
-        assert index.device_index().scan_choice.get((k, v)) == "u8gemm_bits"
+        assert index.device_index().scan_choice.get((k, v)) == "u8tc_bits"
         rids, rd, rc = _oracle(index, Xd, Q, k, v)
         assert np.array_equal(counts.astype(np.int64), rc)
         assert np.array_equal(ids, rids)
         assert dists.tobytes() == rd.tobytes()
 
 
-@pytest.mark.parametrize("variant", ["u8", "u8gemm", "u8gemm_bits"])
+@pytest.mark.parametrize("variant", ["u8", "u8tc_bits"])
 def test_u8_routes_odd_width(monkeypatch, rng, variant):
-    """d not a multiple of 4: the u8 list routes fall back to the float32
+    """d not a multiple of 4: the u8 list route falls back to the float32
     filter inside the library, the bitmap route is not offered; answers stay
     exact."""
     monkeypatch.setenv("MRPT_SCAN_ROWS", variant)
@@ -191,17 +116,16 @@ def test_u8_routes_odd_width(monkeypatch, rng, variant):
 
 
 @pytest.mark.parametrize("d,k,v", [(64, 10, 1), (256, 25, 2), (37, 9, 1), (200, 100, 1)])
-def test_s8_route_signed_data(monkeypatch, rng, d, k, v):
-    """Signed data through the s8 shadow (dp4a with signed rows and signed
-    queries): exactly the oracle's answers, including odd widths (library
-    fallback) and k near the filter's limit."""
-    monkeypatch.setenv("MRPT_SCAN_ROWS", "s8")
+def test_signed_data_routes(rng, d, k, v):
+    """Signed data has no u8 shadow: the autotune chooses among the float32
+    (and, when wide, fp16) filters; exactly the oracle's answers, including
+    odd widths and k near the filters' limit."""
     n, nq = 4000, 290
     X = _data("signed", rng, n + nq, d)
     Xd, Q = X[:n], X[n:]
     index = mrpt.grow_trees(Xd, 6, 5, seed=9)
     ids, dists, counts = mrpt.approximate_knn_batch(Q, k, index, v)
-    assert index.device_index().scan_choice.get((k, v)) == "s8"
+    assert index.device_index().scan_choice.get((k, v)) in ("fp16", "fp32")
     rids, rd, rc = _oracle(index, Xd, Q, k, v)
     assert np.array_equal(counts.astype(np.int64), rc)
     assert np.array_equal(ids, rids)

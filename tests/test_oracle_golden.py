@@ -75,3 +75,41 @@ def test_oracle_config1_matches_reference():
     assert np.array_equal(ids, g["ids_v2"][:200])
     assert np.array_equal(counts, g["counts_v2"][:200])
     np.testing.assert_allclose(dists, g["dists_v2"][:200], rtol=1e-12)
+
+
+# --- ground truth (f3) and the compiled vote order -----------------------------
+@pytest.mark.parametrize("d", [1, 5, 7, 8, 9, 24, 100, 128, 129, 200, 256, 384, 784, 960, 1000, 4096])
+def test_pairwise_plan_is_numpys_sum(d):
+    """The restated summation plan (what the GPU ground-truth kernel runs)
+    equals numpy's own row sum -- the reference's d2 (evaluation.py:40-41)."""
+    rng = np.random.default_rng(d)
+    diff = rng.standard_normal((20, d))
+    sq = diff * diff
+    want = sq.sum(axis=1)
+    got = np.array([O.pairwise_sum(r) for r in sq])
+    assert got.tobytes() == want.tobytes()
+
+
+def test_oracle_ground_truth_matches_reference():
+    g = golden("ground_truth.npz")
+    for name in g["names"]:
+        X, Q, k = g[f"{name}_X"], g[f"{name}_Q"], int(g[f"{name}_k"])
+        ids, dists = O.compute_ground_truth(X, Q, k)
+        assert np.array_equal(ids, g[f"{name}_ids"]), name
+        assert dists.tobytes() == g[f"{name}_dists"].tobytes(), name
+    ids, dists, n = O.brute_force_knn(g["kgtn_X"], g["kgtn_q"], 20)
+    assert n == 9 and np.array_equal(ids, g["kgtn_ids"])
+    assert dists.tobytes() == g["kgtn_dists"].tobytes()
+
+
+def test_oracle_crossing_order_matches_compiled_reference():
+    g = golden("candidates_unsorted.npz")
+    idx = O.grow_trees(g["X"], int(g["n_trees"]), int(g["depth"]), seed=int(g["seed"]))
+    leaves = O.query_leaves(g["Q"], idx)
+    b = g["bounds"]
+    i = 0
+    for v in g["votes"]:
+        for qi in range(len(g["Q"])):
+            got = O.candidates_crossing_order(leaves[qi], idx, int(v))
+            assert np.array_equal(got, g["cand"][b[i]:b[i + 1]])
+            i += 1
