@@ -302,6 +302,38 @@ int32_t mrpt_fnv1a64_workspace_size(int64_t nbytes, size_t *bytes /* host */);
 int32_t mrpt_fnv1a64(const uint8_t *buf, int64_t nbytes, uint64_t *out,
                      void *ws, size_t ws_bytes, void *stream);
 
+/* Streamed tiled vote (configs with many id tiles, T <= 1024): the same
+ * counts and the same candidate set as mrpt_vote (replaces
+ * VoteAccumulator.accumulate / _cy.vote, pkg/src/mrpt/search.py:75-86,
+ * _kernels/_cy.pyx:57-78) over a per-index layout built once:
+ * every ascending leaf slice is split into its parts per id tile, each part
+ * padded to a multiple of 4 entries, each entry pre-decoded into its
+ * tile-local counter address ((word << 5) | shift; 0xffffffff = padding).
+ *   _plan:   ntiles and the entries of qdir (T * 2^depth * (ntiles + 1) u16);
+ *            fails with MRPT_EPARAM where the layout does not apply.
+ *   _layout: qdir (quad offset of each tile's part within its leaf's padded
+ *            slice), qbase (T * 2^depth int32: the slice's first quad within
+ *            its tree row) and tree_quads (T int64: quads per tree row).
+ *   _fill:   qs (T * tstride quads of 4 uint32), tstride >= max tree_quads,
+ *            32 * tstride < 2^31.
+ *   mrpt_vote_stream: candidate lists like mrpt_vote (cand (nq, cap), ncand
+ *            may exceed cap; ids within one id tile in no particular order).
+ * Leaf slices must be ascending (as mrpt_build_levels writes them). */
+int32_t mrpt_vote_stream_plan(int64_t n, int32_t T, int32_t depth, int64_t max_count,
+                              int32_t *ntiles /* host */, int64_t *dir_entries /* host */);
+int32_t mrpt_vote_stream_layout(const int32_t *leaf_indices, const int64_t *leaf_offsets,
+                                int64_t n, int32_t T, int32_t depth, int64_t max_count,
+                                uint16_t *qdir, int32_t *qbase, int64_t *tree_quads,
+                                void *stream);
+int32_t mrpt_vote_stream_fill(const int32_t *leaf_indices, const int64_t *leaf_offsets,
+                              int64_t n, int32_t T, int32_t depth, int64_t max_count,
+                              const uint16_t *qdir, const int32_t *qbase, int64_t tstride,
+                              uint32_t *qs, void *stream);
+int32_t mrpt_vote_stream(const uint32_t *qs, int64_t tstride, const uint16_t *qdir,
+                         const int32_t *qbase, int64_t n, int32_t T, int32_t depth,
+                         int64_t max_count, const int32_t *leaves, int64_t nq, int32_t v,
+                         int32_t *cand, int64_t cap, int32_t *ncand, void *stream);
+
 /* ------------------------------------------------------------------ f3 --
  * Exact brute-force k-NN (ground truth): replaces evaluation.brute_force_knn
  * and compute_ground_truth (pkg/src/mrpt/evaluation.py:28-81).  Q (nq, ldq)

@@ -777,6 +777,264 @@ __global__ void __launch_bounds__(1024) k_bitmap_compact(const uint32_t *__restr
   if (threadIdx.x == 0) *nout = base;
 }
 
+// ---------------------------------------------------------------------------
+// Streamed tiled vote (configs 4-5: many id tiles, T <= 1024).  Built once
+// per index: for every leaf slice, its part in each id tile ("piece") is
+// stored padded to a multiple of 4 entries, pieces in tile order, and each
+// entry is pre-decoded into its tile-local counter address
+//     enc = (counter word << 5) | lane shift      (0xffffffff = padding)
+// so the vote reads every piece with aligned 16-byte loads and bumps a
+// counter with two bit operations instead of a division by the packing.
+// qdir[(t*L + leaf)*(ntiles+1) + w] = start (in 4-entry quads) of tile w's
+// piece within the leaf's padded slice; qbase[t*L + leaf] = the slice's first
+// quad within tree t's padded row (tree t's row starts at quad t * tstride).
+// The counts are identical to the plain vote's: every occurrence of every id
+// is counted once (_cy.pyx:66-77); only the memory layout differs.
+constexpr uint32_t kQuadPad = 0xffffffffu;
+
+template <int CW>
+__host__ __device__ __forceinline__ uint32_t quad_encode(int local) {
+  if (CW == 1) return ((uint32_t)(local >> 2) << 5) | (uint32_t)((local & 3) * 8);
+  if (CW == 3) return ((uint32_t)(local / 3) << 5) | (uint32_t)((local % 3) * 10);
+  if (CW == 2) return ((uint32_t)(local >> 1) << 5) | (uint32_t)((local & 1) * 16);
+  return (uint32_t)local << 5;
+}
+
+template <int CW>
+__device__ __forceinline__ int quad_decode(uint32_t word, uint32_t sh) {
+  if (CW == 1) return (int)(word * 4 + sh / 8);
+  if (CW == 3) return (int)(word * 3 + sh / 10);
+  if (CW == 2) return (int)(word * 2 + sh / 16);
+  return (int)word;
+}
+
+// qdir holds, after k_build_dir, the piece start POSITIONS within each leaf
+// slice (u16); this turns them into padded quad offsets in place and writes
+// each leaf's padded length (quads) to qlen.  One warp per leaf.
+__global__ void k_vstream_quads(uint16_t *qdir, int64_t nleaves, int ntiles, int32_t *qlen) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < nleaves; g += wstride) {
+    uint16_t *d = qdir + g * (ntiles + 1);
+    int carry = 0;
+    for (int w0 = 0; w0 < ntiles; w0 += 32) {
+      const int w = w0 + lane;
+      int q = 0;
+      if (w < ntiles) q = ((int)d[w + 1] - (int)d[w] + 3) >> 2;  // read before any write of this round
+      int incl = q;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      __syncwarp();
+      if (w < ntiles) d[w] = (uint16_t)(carry + incl - q);
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+      __syncwarp();
+    }
+    if (lane == 0) {
+      d[ntiles] = (uint16_t)carry;
+      qlen[g] = carry;
+    }
+  }
+}
+
+// Per tree: exclusive scan of the leaves' padded lengths -> qbase, total ->
+// tree_quads[t].  One CTA (1024 threads) per tree.
+__global__ void __launch_bounds__(1024) k_vstream_base(int32_t *qbase, int L, int64_t *tree_quads) {
+  __shared__ int wsum[33];
+  const int t = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int32_t *b = qbase + (int64_t)t * L;
+  long long carry = 0;
+  for (int f0 = 0; f0 < L; f0 += 1024) {
+    const int f = f0 + tid;
+    const int v = f < L ? b[f] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const int c = wsum[lane];
+      int x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += u;
+      }
+      wsum[lane] = x - c;
+      if (lane == 31) wsum[32] = x;
+    }
+    __syncthreads();
+    if (f < L) b[f] = (int32_t)(carry + wsum[warp] + incl - v);
+    carry += wsum[32];
+    __syncthreads();
+  }
+  if (tid == 0) tree_quads[t] = carry;
+}
+
+// Fill the padded, pre-decoded slices.  One warp per leaf; the slice is
+// ascending, so each tile's piece is one run.
+template <int CW>
+__global__ void k_vstream_fill(const int32_t *__restrict__ leaf_indices, const int64_t *__restrict__ leaf_offsets,
+                               int64_t n, int T, int L, int W, int ntiles, const uint16_t *__restrict__ qdir,
+                               const int32_t *__restrict__ qbase, int64_t tstride, uint32_t *qs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nleaves = (int64_t)T * L;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < nleaves; g += wstride) {
+    const int64_t t = g / L, leaf = g - t * L;
+    const int64_t *o = leaf_offsets + t * (L + 1);
+    const int64_t s = o[leaf], e = o[leaf + 1];
+    const int32_t *Lt = leaf_indices + t * n;
+    const uint16_t *d = qdir + g * (ntiles + 1);
+    uint32_t *out = qs + 4 * (t * tstride + qbase[g]);
+    int prev_tile = -1;
+    int64_t run_start = s;  // position where the current tile's run began
+    for (int64_t p0 = s; p0 < e; p0 += 32) {
+      const int64_t p = p0 + lane;
+      const bool in = p < e;
+      const int32_t id = in ? Lt[p] : 0;
+      const int tl = in ? id / W : 0x7fffffff;
+      int before = __shfl_up_sync(0xffffffffu, tl, 1);
+      if (lane == 0) before = prev_tile;
+      const bool first = in && tl != before;
+      // start of this lane's run: the last "first" at or before it, else carried
+      long long st = first ? (long long)p : -1;
+#pragma unroll
+      for (int o2 = 1; o2 < 32; o2 <<= 1) {
+        const long long u = __shfl_up_sync(0xffffffffu, st, o2);
+        if (lane >= o2 && u > st) st = u;
+      }
+      if (st < 0) st = run_start;
+      const int nxt = __shfl_down_sync(0xffffffffu, tl, 1);
+      if (in) {
+        const int local = id - tl * W;
+        const int64_t base = 4 * (int64_t)d[tl];
+        out[base + (p - st)] = quad_encode<CW>(local);
+        // the run's last element pads its piece to a multiple of 4
+        const bool last = p + 1 == e || (lane < 31 ? nxt != tl : Lt[p + 1] / W != tl);
+        if (last) {
+          const int64_t end = 4 * (int64_t)d[tl + 1];
+          for (int64_t z = base + (p - st) + 1; z < end; ++z) out[z] = kQuadPad;
+        }
+      }
+      prev_tile = __shfl_sync(0xffffffffu, tl, 31);
+      const long long last_st = __shfl_sync(0xffffffffu, st, 31);
+      run_start = last_st;
+    }
+  }
+}
+
+// The streamed vote: one CTA (1024 threads, one per SM) per query at a time;
+// warp w owns the contiguous tree range [w*T/32, (w+1)*T/32) (<= 32 trees,
+// one per lane).  Per id tile, the warp flattens its trees' pieces (quads)
+// into 32-quad windows: a lane finds the piece holding its quad from the
+// piece starts inside the window (__reduce_or_sync) and a 32-entry rank
+// table, loads the quad with one 16-byte load and bumps its 4 counters.  The
+// increment that lifts a count to v appends the id to the query's list
+// (the reference's `counts[idx] == v` emission, _cy.pyx:75-77; order within
+// a tile is not kept).  Counters are zeroed per tile; ncand may exceed cap
+// (only cap ids stored).
+template <int CW>
+__global__ void __launch_bounds__(1024, 1) k_vote_stream(VoteArgs a, const uint4 *__restrict__ qs,
+                                                         const int32_t *__restrict__ qbase, int64_t tstride) {
+  extern __shared__ uint4 vote_smem[];
+  uint32_t *cnt = reinterpret_cast<uint32_t *>(vote_smem);
+  const int cwords = (counter_words<CW>(a.W) + 3) & ~3;
+  constexpr int NW = 32;
+  __shared__ int32_t w_off[NW][32];
+  __shared__ int s_nc;
+  constexpr uint32_t MASK = CW == 1 ? 0xffu : (CW == 3 ? 0x3ffu : (CW == 2 ? 0xffffu : 0xffffffffu));
+  const uint32_t vm1 = (uint32_t)(a.v - 1);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t dstride = a.ntiles + 1;
+  const int t_lo = (int)(((int64_t)warp * a.T) / NW);
+  const int t_hi = (int)(((int64_t)(warp + 1) * a.T) / NW);
+  const int t = t_lo + lane;
+  const bool has = t < t_hi;
+  const uint4 *wbase = qs + (int64_t)t_lo * tstride;
+  uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
+  for (int64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
+    const uint16_t *dl = nullptr;
+    int32_t lbase = 0;
+    int dcur = 0, dnxt = 0;
+    if (has) {
+      const int64_t g = (int64_t)t * a.L + a.leaves[q * a.T + t];
+      dl = a.dir + g * dstride;
+      lbase = (int32_t)((int64_t)lane * tstride + qbase[g]);
+      dcur = dl[0];
+      dnxt = dl[1];
+    }
+    for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (tid == 0) s_nc = 0;
+    __syncthreads();
+    int32_t *qcand = a.cand + q * a.cap;
+    for (int tile = 0; tile < a.ntiles; ++tile) {
+      const int32_t lo = tile * a.W;
+      const int dnn = (has && tile + 2 <= a.ntiles) ? (int)__ldg(dl + tile + 2) : 0;
+      const int len = dnxt - dcur;  // this lane's quads in this tile
+      int incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      const int pre = incl - len;
+      const unsigned ne = __ballot_sync(0xffffffffu, len > 0);
+      if (len > 0) w_off[warp][__popc(ne & lanemask_lt())] = lbase + dcur - pre;
+      __syncwarp();
+      int before = 0;  // non-empty pieces starting before the current window
+      constexpr int UNR = 4;
+      for (int e0 = 0; e0 < total; e0 += 32 * UNR) {
+        uint4 val[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const int w0 = e0 + 32 * u;
+          const int rel = pre - w0;
+          const bool inwin = len > 0 && (unsigned)rel < 32u;
+          const unsigned starts = __reduce_or_sync(0xffffffffu, inwin ? (1u << rel) : 0u);
+          const int rank = before + __popc(starts & (0xffffffffu >> (31 - lane))) - 1;
+          before += __popc(starts);
+          const int e = w0 + lane;
+          val[u] = e < total ? __ldg(wbase + (w_off[warp][rank] + e))
+                             : make_uint4(kQuadPad, kQuadPad, kQuadPad, kQuadPad);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const uint32_t xs[4] = {val[u].x, val[u].y, val[u].z, val[u].w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint32_t x = xs[c];
+            if (x != kQuadPad) {
+              const uint32_t sh = x & 31u, wd = x >> 5;
+              const uint32_t old = atomicAdd(cnt + wd, 1u << sh);
+              if (((old >> sh) & MASK) == vm1) {
+                const int pos = atomicAdd(&s_nc, 1);
+                if (pos < a.cap) qcand[pos] = lo + quad_decode<CW>(wd, sh);
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();  // w_off is rewritten next tile
+      __syncthreads();
+      dcur = dnxt;
+      dnxt = dnn;
+      if (tile + 1 < a.ntiles) {
+        for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+      }
+    }
+    if (tid == 0) a.ncand[q] = s_nc;  // > cap means only cap ids were stored
+    __syncthreads();
+  }
+}
+
 }  // namespace mrpt
 
 using namespace mrpt;
@@ -791,6 +1049,10 @@ static const int kVoteSmemUnion = 222 * 1024;   // v == 1 bitmap over all ids + 
 static size_t vote_smem_bytes(int CW, int64_t W, int32_t T) {
   const int64_t words = CW == 1 ? W / 4 : (CW == 2 ? W / 2 : (CW == 3 ? (W + 2) / 3 : W));
   return (size_t)((words + 3) & ~3LL) * 4 + (size_t)W / 8 + (size_t)8 * T;
+}
+
+static int64_t counter_words_host(int CW, int64_t W) {
+  return CW == 1 ? W / 4 : (CW == 2 ? W / 2 : (CW == 3 ? (W + 2) / 3 : W));
 }
 
 static int vote_dir_threads() {
@@ -1062,4 +1324,110 @@ extern "C" int32_t mrpt_unique_ids(const int64_t *cand, int64_t m, int64_t n, ui
   }
   (count_launch(), k_bitmap_compact<<<1, 1024, 0, s>>>(bitmap, nwords, out, nout));
   return launch_status("mrpt_unique_ids");
+}
+
+// ------------------------------------------------------------ streamed vote --
+static const int kVoteSmemStream = 218 * 1024;  // counters only (the rank tables are static)
+
+static int32_t stream_geometry(int64_t n, int32_t T, int64_t max_count, int *CWo, int64_t *Wo, int *ntiles_o) {
+  if (T < 1 || T > 1024) return fail(MRPT_EPARAM, "streamed vote: needs 1 <= T <= 1024");
+  const int CW = max_count <= 255 ? 1 : (max_count <= 1023 ? 3 : (max_count <= 65535 ? 2 : 4));
+  const int per = CW == 1 ? 4 : (CW == 3 ? 3 : (CW == 2 ? 2 : 1));
+  const int64_t words = (kVoteSmemStream / 4) & ~3LL;
+  int64_t W = words * per;
+  if (W >= n) W = n;
+  *CWo = CW;
+  *Wo = W;
+  *ntiles_o = (int)ceil_div<int64_t>(n, W);
+  return MRPT_OK;
+}
+
+extern "C" int32_t mrpt_vote_stream_plan(int64_t n, int32_t T, int32_t depth, int64_t max_count,
+                                         int32_t *ntiles, int64_t *dir_entries) {
+  clear_error();
+  if (n < 1 || n >= (int64_t)1 << 31 || depth < 0 || depth > 30 || !ntiles || !dir_entries)
+    return fail(MRPT_ESHAPE, "mrpt_vote_stream_plan: bad arguments");
+  int CW, nt;
+  int64_t W;
+  const int32_t st = stream_geometry(n, T, max_count, &CW, &W, &nt);
+  if (st) return st;
+  *ntiles = nt;
+  *dir_entries = (int64_t)T * ((int64_t)1 << depth) * (nt + 1);
+  return MRPT_OK;
+}
+
+extern "C" int32_t mrpt_vote_stream_layout(const int32_t *leaf_indices, const int64_t *leaf_offsets, int64_t n,
+                                           int32_t T, int32_t depth, int64_t max_count, uint16_t *qdir,
+                                           int32_t *qbase, int64_t *tree_quads, void *stream) {
+  clear_error();
+  int CW, nt;
+  int64_t W;
+  const int32_t st = stream_geometry(n, T, max_count, &CW, &W, &nt);
+  if (st) return st;
+  cudaStream_t s = as_stream(stream);
+  const int64_t nleaves = (int64_t)T << depth;
+  const int64_t blocks = ceil_div<int64_t>(nleaves, 8);
+  const int grid = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
+  (count_launch(), k_build_dir<<<grid, 256, 0, s>>>(leaf_indices, leaf_offsets, n, T, 1 << depth, (int)W, nt, qdir));
+  (count_launch(), k_vstream_quads<<<grid, 256, 0, s>>>(qdir, nleaves, nt, qbase));
+  (count_launch(), k_vstream_base<<<T, 1024, 0, s>>>(qbase, 1 << depth, tree_quads));
+  return launch_status("mrpt_vote_stream_layout");
+}
+
+extern "C" int32_t mrpt_vote_stream_fill(const int32_t *leaf_indices, const int64_t *leaf_offsets, int64_t n,
+                                         int32_t T, int32_t depth, int64_t max_count, const uint16_t *qdir,
+                                         const int32_t *qbase, int64_t tstride, uint32_t *qs, void *stream) {
+  clear_error();
+  int CW, nt;
+  int64_t W;
+  const int32_t st = stream_geometry(n, T, max_count, &CW, &W, &nt);
+  if (st) return st;
+  if (tstride < 0 || 32 * tstride >= ((int64_t)1 << 31))
+    return fail(MRPT_EPARAM, "mrpt_vote_stream_fill: tree stride too large");
+  cudaStream_t s = as_stream(stream);
+  const int64_t nleaves = (int64_t)T << depth;
+  const int64_t blocks = ceil_div<int64_t>(nleaves, 8);
+  const int grid = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
+  auto fn = CW == 1 ? k_vstream_fill<1> : (CW == 3 ? k_vstream_fill<3> : (CW == 2 ? k_vstream_fill<2> : k_vstream_fill<4>));
+  (count_launch(), fn<<<grid, 256, 0, s>>>(leaf_indices, leaf_offsets, n, T, 1 << depth, (int)W, nt, qdir, qbase,
+                                           tstride, qs));
+  return launch_status("mrpt_vote_stream_fill");
+}
+
+extern "C" int32_t mrpt_vote_stream(const uint32_t *qs, int64_t tstride, const uint16_t *qdir, const int32_t *qbase,
+                                    int64_t n, int32_t T, int32_t depth, int64_t max_count, const int32_t *leaves,
+                                    int64_t nq, int32_t v, int32_t *cand, int64_t cap, int32_t *ncand,
+                                    void *stream) {
+  clear_error();
+  if (n < 1 || n >= (int64_t)1 << 31 || depth < 0 || depth > 30 || nq < 0)
+    return fail(MRPT_ESHAPE, "mrpt_vote_stream: bad shape");
+  if (v < 1 || v > max_count) return fail(MRPT_EPARAM, "mrpt_vote_stream: vote threshold out of range");
+  if (cap < 1) return fail(MRPT_EPARAM, "mrpt_vote_stream: cap must be >= 1");
+  if (32 * tstride >= ((int64_t)1 << 31)) return fail(MRPT_EPARAM, "mrpt_vote_stream: tree stride too large");
+  int CW, nt;
+  int64_t W;
+  const int32_t st = stream_geometry(n, T, max_count, &CW, &W, &nt);
+  if (st) return st;
+  if (nq == 0) return MRPT_OK;
+  VoteArgs a = {};
+  a.n = n;
+  a.T = T;
+  a.L = 1 << depth;
+  a.leaves = leaves;
+  a.nq = nq;
+  a.v = v;
+  a.cand = cand;
+  a.cap = cap;
+  a.ncand = ncand;
+  a.W = (int)W;
+  a.ntiles = nt;
+  a.dir = qdir;
+  const size_t smem = (size_t)((counter_words_host(CW, W) + 3) & ~3LL) * 4;
+  typedef void (*sfn_t)(VoteArgs, const uint4 *, const int32_t *, int64_t);
+  sfn_t fn = CW == 1 ? k_vote_stream<1> : (CW == 3 ? k_vote_stream<3> : (CW == 2 ? k_vote_stream<2> : k_vote_stream<4>));
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t grid = nq < (int64_t)num_sms() ? nq : (int64_t)num_sms();
+  cudaStream_t s = as_stream(stream);
+  (count_launch(), fn<<<(unsigned)grid, 1024, smem, s>>>(a, reinterpret_cast<const uint4 *>(qs), qbase, tstride));
+  return launch_status("mrpt_vote_stream");
 }

@@ -257,7 +257,6 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None, size_class=N
     if chunk is None:
         per_q = 4 * (D.T + (bstride if bits_mode else cap))
         chunk = max(1, min(nq, (1 << 30) // per_q))
-    vdir = D.vote_dir()
     m0 = min(chunk, nq)
     leaves = torch.empty((m0, D.T), dtype=torch.int32, device=dev)
     cand = None
@@ -266,14 +265,14 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None, size_class=N
         e = min(nq, s + chunk)
         qb = Qd[s:e]
         if bits_mode:
-            _run_bits(D, qb, e - s, int(Qd.stride(0)), leaves, votes, vdir, bits, bstride,
+            _run_bits(D, qb, e - s, int(Qd.stride(0)), leaves, votes, bits, bstride,
                       counts[s:e], k, ids[s:e], dists[s:e], stage, route=choice)
             continue
         stage("route", _route_launch, D, qb, e - s, int(Qd.stride(0)), leaves)
         if choice is None and e - s >= 256:
             # the autotune's last run leaves this chunk's outputs; the rest of
             # the batch runs the chosen route (its own chunking)
-            _autotune(D, qb, e - s, int(Qd.stride(0)), leaves, votes, vdir, cap, counts[s:e], k, sc,
+            _autotune(D, qb, e - s, int(Qd.stride(0)), leaves, votes, cap, counts[s:e], k, sc,
                       ids[s:e], dists[s:e])
             if e < nq:
                 query_device(D, Qd[e:], k, votes, out=(ids[e:], dists[e:], counts[e:]), timer=timer,
@@ -281,7 +280,7 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None, size_class=N
             return ids, dists, counts
         if cand is None:
             cand = torch.empty((m0, cap), dtype=torch.int32, device=dev)
-        stage("vote", _vote_list, D, leaves, e - s, votes, vdir, cand, cap, counts[s:e])
+        stage("vote", _vote_list, D, leaves, e - s, votes, cand, cap, counts[s:e])
         args = (qb, e - s, int(Qd.stride(0)), cand, cap, counts[s:e], k, ids[s:e], dists[s:e])
         variant = choice if choice is not None and choice not in _BITS_ROUTES else "fp32"
         if choice is None:  # small batch, no autotune: a forced list route still applies
@@ -295,7 +294,7 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None, size_class=N
 _BITS_ROUTES = ("u8tc_bits",)
 
 
-def _run_bits(D, qb, m, ldq, leaves, votes, vdir, bits, bstride, counts, k, ids, dists, stage=None,
+def _run_bits(D, qb, m, ldq, leaves, votes, bits, bstride, counts, k, ids, dists, stage=None,
               route="u8tc_bits"):
     """The bitmap route: K2 + K3 on their own stream beside K4's query
     quantisation, which needs only the queries; the fused tcgen05 filter
@@ -310,7 +309,7 @@ def _run_bits(D, qb, m, ldq, leaves, votes, vdir, bits, bstride, counts, k, ids,
     with torch.cuda.stream(vs):
         vs.wait_event(ev_start)
         stage("route", _route_launch, D, qb, m, ldq, leaves)
-        stage("vote", _vote_bitmap, D, leaves, m, votes, vdir, bits, bstride, counts)
+        stage("vote", _vote_bitmap, D, leaves, m, votes, bits, bstride, counts)
         ev_vote = torch.cuda.Event()
         ev_vote.record(vs)
     stage("scan_topk", _scan_tc, D, qb, m, ldq, bits, bstride, k, ids, dists, ev_vote)
@@ -328,17 +327,26 @@ def _route_launch(D, qb, m, ldq, leaves):
                  _native.ptr(leaves), _native.stream_ptr())
 
 
-def _vote_list(D, leaves, m, votes, vdir, cand, cap, counts):
+def _vote_list(D, leaves, m, votes, cand, cap, counts):
+    vs = D.vote_stream()
+    if vs is not None:
+        # the streamed tiled vote (padded, pre-decoded leaf slices)
+        qs, tstride, qdir, qbase = vs
+        _native.call("mrpt_vote_stream", _native.ptr(qs), int(tstride), _native.ptr(qdir),
+                     _native.ptr(qbase), D.n, D.T, D.depth, int(D.max_count), _native.ptr(leaves), m,
+                     int(votes), _native.ptr(cand), int(cap), _native.ptr(counts),
+                     _native.stream_ptr())
+        return
     _native.call("mrpt_vote", _native.ptr(D.indices), _native.ptr(D.offsets), D.n, D.T, D.depth,
                  _native.ptr(leaves), m, int(votes), int(D.leaves_sorted), int(D.max_count),
-                 _native.ptr(vdir), _native.ptr(cand), int(cap), _native.ptr(counts),
+                 _native.ptr(D.vote_dir()), _native.ptr(cand), int(cap), _native.ptr(counts),
                  _native.stream_ptr())
 
 
-def _vote_bitmap(D, leaves, m, votes, vdir, bits, bstride, counts):
+def _vote_bitmap(D, leaves, m, votes, bits, bstride, counts):
     _native.call("mrpt_vote_bitmap", _native.ptr(D.indices), _native.ptr(D.offsets), D.n, D.T,
                  D.depth, _native.ptr(leaves), m, int(votes), int(D.leaves_sorted),
-                 int(D.max_count), _native.ptr(vdir), _native.ptr(bits), int(bstride),
+                 int(D.max_count), _native.ptr(D.vote_dir()), _native.ptr(bits), int(bstride),
                  _native.ptr(counts), _native.stream_ptr())
 
 
@@ -389,7 +397,7 @@ def _scan_launch(D, variant, args):
                      *common_tail)
 
 
-def _autotune(D, qb, m, ldq, leaves, votes, vdir, cap, counts, k, sc, ids, dists):
+def _autotune(D, qb, m, ldq, leaves, votes, cap, counts, k, sc, ids, dists):
     """Time every exact route for this chunk -- list vote + each list filter,
     bitmap vote + the fused tcgen05 filter -- and keep the fastest for the index
     (per k and vote threshold); the last run leaves valid outputs (all routes
@@ -420,11 +428,11 @@ def _autotune(D, qb, m, ldq, leaves, votes, vdir, cap, counts, k, sc, ids, dists
         # then the filter
         bstride = _bstride(D)
         bits = torch.empty((m, bstride), dtype=torch.int32, device=dev)
-        times[route] = timed(_run_bits, D, qb, m, ldq, leaves, votes, vdir, bits, bstride,
+        times[route] = timed(_run_bits, D, qb, m, ldq, leaves, votes, bits, bstride,
                              counts, k, ids, dists, None, route)
     if list_vars:
         cand = torch.empty((m, cap), dtype=torch.int32, device=dev)
-        tv = tr + timed(_vote_list, D, leaves, m, votes, vdir, cand, cap, counts)
+        tv = tr + timed(_vote_list, D, leaves, m, votes, cand, cap, counts)
         args = (qb, m, ldq, cand, cap, counts, k, ids, dists)
         for v in list_vars:
             times[v] = tv + timed(_scan_launch, D, v, args)
@@ -583,7 +591,6 @@ def _knn_batch_pipelined_bits(Qc, k, index, votes, route):
     compute = torch.cuda.current_stream()
     up, _ = _device.side_streams()
     up.wait_stream(compute)  # Qd's block may still be in use by queued compute work
-    vdir = D.vote_dir()
     pieces = max(1, min(int(os.environ.get("MRPT_PIPE_PIECES", "4")), nq // 1024))
     bounds = [nq * i // pieces for i in range(pieces + 1)]
     for i in range(pieces):
@@ -594,7 +601,7 @@ def _knn_batch_pipelined_bits(Qc, k, index, votes, route):
             ev_up.record(up)
         compute.wait_event(ev_up)
         _route_launch(D, Qd[s:e], e - s, int(Qd.stride(0)), leaves[s:e])
-        _vote_bitmap(D, leaves[s:e], e - s, votes, vdir, bits[s:e], bstride, counts[s:e])
+        _vote_bitmap(D, leaves[s:e], e - s, votes, bits[s:e], bstride, counts[s:e])
     _scan_tc(D, Qd, nq, int(Qd.stride(0)), bits, bstride, k, ids, dists)
     hid.copy_(ids, non_blocking=True)
     hdist.copy_(dists, non_blocking=True)

@@ -28,7 +28,7 @@ from .core import (
     default_sparsity,
     sample_sparse_matrix,
 )
-from .exceptions import DepthError, IntegrityError, ParameterError
+from .exceptions import DepthError, IntegrityError, MRPTError, ParameterError
 
 __all__ = ["MRPTIndex", "RPTree", "build_tree", "grow_trees", "median_split"]
 
@@ -266,6 +266,51 @@ class _DeviceIndex:
                      ctypes.byref(need))
         return g[0], g[1], self.workspace("u8tc", need.value)
 
+    def vote_stream(self):
+        """The streamed-vote layout of this index (mrpt_vote_stream_layout /
+        _fill: every leaf slice's per-id-tile pieces padded to 16-byte quads of
+        pre-decoded counter addresses), built once on the device; None where
+        one id tile covers the index, the slices are not ascending (foreign
+        index), T > 1024, or it does not fit beside the index
+        (MRPT_VOTE_STREAM=0 disables it)."""
+        if getattr(self, "_vstream", False) is not False:
+            return self._vstream
+        self._vstream = None
+        if os.environ.get("MRPT_VOTE_STREAM", "1") == "0":
+            return None
+        if not self.leaves_sorted or self.max_leaf > 65535 or self.T > 1024:
+            return None
+        ntiles, entries = ctypes.c_int32(0), ctypes.c_int64(0)
+        try:
+            _native.call("mrpt_vote_stream_plan", self.n, self.T, self.depth, int(self.max_count),
+                         ctypes.byref(ntiles), ctypes.byref(entries))
+        except MRPTError:
+            return None
+        nleaf = 1 << self.depth
+        # padded lengths must fit the u16 quad directory
+        if ntiles.value <= 1 or self.max_leaf + 3 * ntiles.value >= 4 * 65535:
+            return None
+        torch = _device.torch_mod()
+        dev = self.indices.device
+        qdir = torch.empty(entries.value, dtype=torch.int16, device=dev)
+        qbase = torch.empty(self.T * nleaf, dtype=torch.int32, device=dev)
+        tq = torch.empty(self.T, dtype=torch.int64, device=dev)
+        _native.call("mrpt_vote_stream_layout", _native.ptr(self.indices), _native.ptr(self.offsets),
+                     self.n, self.T, self.depth, int(self.max_count), _native.ptr(qdir),
+                     _native.ptr(qbase), _native.ptr(tq), _native.stream_ptr())
+        tstride = int(tq.max().item())
+        tstride = (tstride + 1) // 2 * 2  # 32-byte aligned tree rows
+        nbytes = 16 * self.T * tstride
+        free = torch.cuda.mem_get_info(dev)[0]
+        if 32 * tstride >= (1 << 31) or nbytes > 0.8 * free:
+            return None
+        qs = torch.empty(nbytes // 4, dtype=torch.int32, device=dev)
+        _native.call("mrpt_vote_stream_fill", _native.ptr(self.indices), _native.ptr(self.offsets),
+                     self.n, self.T, self.depth, int(self.max_count), _native.ptr(qdir),
+                     _native.ptr(qbase), tstride, _native.ptr(qs), _native.stream_ptr())
+        self._vstream = (qs, tstride, qdir, qbase)
+        return self._vstream
+
     def vote_dir(self):
         """Tile directory for the multi-tile vote (built once, on the device),
         or None when one id tile covers the index or it cannot be used."""
@@ -495,6 +540,9 @@ def _finish_index(X, n_trees, depth, sparsity, seed, fixed_count, matrices, spli
     cp, rows, vals = _device.csc_device(matrices, pinned=True)
     dindex = _DeviceIndex(Xd, n_trees, depth, splits, offsets, indices, cp, rows, vals,
                           leaves_sorted=True, max_count=n_trees, max_leaf=max_leaf)
+    # the streamed-vote layout is part of the index the queries use: built
+    # here (billed to the build) wherever it applies
+    dindex.vote_stream()
     return MRPTIndex(dataset=X, n_trees=n_trees, depth=depth, sparsity=float(sparsity), seed=seed,
                      fixed_count=fixed_count, matrices=matrices, splits=splits,
                      leaf_offsets=offsets, leaf_indices=indices,

@@ -381,3 +381,90 @@ def test_vote_sweep_one_pass_matches_per_threshold(rng, n, T, depth, votes):
         assert np.array_equal(ids, rids)
         assert dists.tobytes() == rd.tobytes()
         assert np.array_equal(counts.astype(np.int64), rc)
+
+
+def _stream_lists(index, Q, v, cap=None):
+    """Raw K2 + streamed K3 output through the C ABI (mrpt_vote_stream)."""
+    import torch
+
+    from paper_1509_06957_b200 import _native
+    from paper_1509_06957_b200.search import _route_device
+
+    D = index.device_index()
+    vs = D.vote_stream()
+    assert vs is not None, "the streamed layout should apply here"
+    qs, tstride, qdir, qbase = vs
+    Qd = torch.from_numpy(np.ascontiguousarray(Q)).cuda()
+    leaves = _route_device(Qd, D)
+    cap = D.cap(v) if cap is None else cap
+    cand = torch.full((Q.shape[0], cap), -7, dtype=torch.int32, device="cuda")
+    counts = torch.empty(Q.shape[0], dtype=torch.int32, device="cuda")
+    _native.call("mrpt_vote_stream", _native.ptr(qs), int(tstride), _native.ptr(qdir),
+                 _native.ptr(qbase), D.n, D.T, D.depth, int(D.max_count), _native.ptr(leaves),
+                 Q.shape[0], int(v), _native.ptr(cand), int(cap), _native.ptr(counts),
+                 _native.stream_ptr())
+    c = counts.cpu().numpy()
+    return [row[:min(m, cap)] for row, m in zip(cand.cpu().numpy(), c)], c
+
+
+@pytest.mark.parametrize("T,depth,n,kind,votes", [
+    (12, 7, 500_000, "gauss", (1, 2, 12)),     # u8 counters, fewer trees than warps, 3 tiles
+    (300, 6, 400_000, "ints", (2, 9, 300)),    # 10-bit counters, heavy ties (unbalanced leaves)
+    (1000, 9, 400_000, "gauss", (3, 10)),      # 31-32 trees per warp
+    (1024, 5, 250_000, "gauss", (2, 40)),      # u16 counters (T = 1024 > 1023)
+    (40, 4, 170_001, "gauss", (1, 5)),         # ragged last tile of one id
+])
+def test_streamed_vote_matches_oracle(rng, T, depth, n, kind, votes):
+    """The streamed tiled vote (padded, pre-decoded leaf slices) gives the
+    oracle's candidate sets and counts, and the batch API over it the
+    oracle's neighbour ids and distances."""
+    if kind == "ints":
+        X = rng.integers(0, 4, size=(n + 40, 5)).astype(np.float32)
+    else:
+        X = gaussian(rng, n + 40, 5)
+    Xd, Q = X[:n], X[n:]
+    index = mrpt.grow_trees(Xd, T, depth, seed=8)
+    ref = dict(matrices=[(R.col_ptr, R.row_idx, R.values) for R in index.matrices],
+               splits=index.splits, leaf_offsets=index.leaf_offsets,
+               leaf_indices=index.leaf_indices, depth=depth)
+    leaves = O.query_leaves(Q, ref)
+    for v in votes:
+        got, gc = _stream_lists(index, Q, v)
+        for i in range(len(Q)):
+            want = O.candidates(leaves[i], ref, v)
+            assert gc[i] == len(want)
+            assert np.array_equal(np.sort(got[i]), want)
+        ids, dists, counts = mrpt.approximate_knn_batch(Q, 10, index, v)
+        rids, rd, rc = O.approximate_knn_batch(Xd, Q, 10, ref, v)
+        assert np.array_equal(counts.astype(np.int64), rc)
+        assert np.array_equal(ids, rids)
+        assert dists.tobytes() == rd.tobytes()
+
+
+def test_streamed_vote_layout_round_trip(rng):
+    """Decoding the streamed layout (quads -> ids, padding dropped) gives back
+    every leaf slice exactly: the layout is a lossless re-encoding."""
+    T, depth, n = 7, 6, 300_000
+    X = gaussian(rng, n, 4)
+    index = mrpt.grow_trees(X, T, depth, seed=2)
+    D = index.device_index()
+    qs, tstride, qdir, qbase = D.vote_stream()
+    qs = qs.cpu().numpy().view(np.uint32).reshape(T, tstride, 4)
+    qbase = qbase.cpu().numpy()
+    L = 1 << depth
+    nt = qdir.numel() // (T * L) - 1
+    qdir = qdir.cpu().numpy().view(np.uint16).reshape(T, L, nt + 1).astype(np.int64)
+    W = ((218 * 1024 // 4) & ~3) * 4  # u8 counters (T <= 255): 4 ids per counter word
+    assert nt == -(-n // W)
+    offs, li = index.leaf_offsets, index.leaf_indices
+    for t in range(T):
+        for f in range(L):
+            s0 = qbase[t * L + f]
+            ids = []
+            for w in range(nt):
+                quads = qs[t, s0 + qdir[t, f, w]: s0 + qdir[t, f, w + 1]].ravel()
+                assert len(quads) % 4 == 0
+                for e in quads:
+                    if e != 0xFFFFFFFF:
+                        ids.append(w * W + int(e >> 5) * 4 + int(e & 31) // 8)
+            assert np.array_equal(np.array(ids, dtype=np.int64), li[t, offs[t, f]:offs[t, f + 1]])
