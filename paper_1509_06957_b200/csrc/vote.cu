@@ -782,22 +782,30 @@ __global__ void __launch_bounds__(1024) k_bitmap_compact(const uint32_t *__restr
 // per index: for every leaf slice, its part in each id tile ("piece") is
 // stored padded to a multiple of 4 entries, pieces in tile order, and each
 // entry is pre-decoded into its tile-local counter address
-//     enc = (counter word << 5) | lane shift      (0xffffffff = padding)
 // so the vote reads every piece with aligned 16-byte loads and bumps a
-// counter with two bit operations instead of a division by the packing.
+// counter with two bit operations instead of a division by the packing:
+//     enc = (counter word << 7) | lane shift    (enc >> 5 = the word's byte offset)
+// Padding entries address one of 32 spare words past the counters (by slot,
+// so the lanes of a load rarely share one): they are bumped like any entry
+// (no per-entry test) and never emitted.
 // qdir[(t*L + leaf)*(ntiles+1) + w] = start (in 4-entry quads) of tile w's
 // piece within the leaf's padded slice; qbase[t*L + leaf] = the slice's first
 // quad within tree t's padded row (tree t's row starts at quad t * tstride).
 // The counts are identical to the plain vote's: every occurrence of every id
 // is counted once (_cy.pyx:66-77); only the memory layout differs.
-constexpr uint32_t kQuadPad = 0xffffffffu;
-
 template <int CW>
 __host__ __device__ __forceinline__ uint32_t quad_encode(int local) {
-  if (CW == 1) return ((uint32_t)(local >> 2) << 5) | (uint32_t)((local & 3) * 8);
-  if (CW == 3) return ((uint32_t)(local / 3) << 5) | (uint32_t)((local % 3) * 10);
-  if (CW == 2) return ((uint32_t)(local >> 1) << 5) | (uint32_t)((local & 1) * 16);
-  return (uint32_t)local << 5;
+  if (CW == 1) return ((uint32_t)(local >> 2) << 7) | (uint32_t)((local & 3) * 8);
+  if (CW == 3) return ((uint32_t)(local / 3) << 7) | (uint32_t)((local % 3) * 10);
+  if (CW == 2) return ((uint32_t)(local >> 1) << 7) | (uint32_t)((local & 1) * 16);
+  return (uint32_t)local << 7;
+}
+
+// The padding entry of a tile width for output slot z: spare word z % 32
+// after the counters (counter words rounded up to 4).
+template <int CW>
+__host__ __device__ __forceinline__ uint32_t quad_pad(int W, int64_t z = 0) {
+  return (uint32_t)(((counter_words<CW>(W) + 3) & ~3) + (int)(z & 31)) << 7;
 }
 
 template <int CW>
@@ -919,7 +927,7 @@ __global__ void k_vstream_fill(const int32_t *__restrict__ leaf_indices, const i
         const bool last = p + 1 == e || (lane < 31 ? nxt != tl : Lt[p + 1] / W != tl);
         if (last) {
           const int64_t end = 4 * (int64_t)d[tl + 1];
-          for (int64_t z = base + (p - st) + 1; z < end; ++z) out[z] = kQuadPad;
+          for (int64_t z = base + (p - st) + 1; z < end; ++z) out[z] = quad_pad<CW>(W, z);
         }
       }
       prev_tile = __shfl_sync(0xffffffffu, tl, 31);
@@ -939,102 +947,157 @@ __global__ void k_vstream_fill(const int32_t *__restrict__ leaf_indices, const i
 // (the reference's `counts[idx] == v` emission, _cy.pyx:75-77; order within
 // a tile is not kept).  Counters are zeroed per tile; ncand may exceed cap
 // (only cap ids stored).
-template <int CW>
+// Shared-memory atomic add at a 32-bit shared address; returns the old word.
+__device__ __forceinline__ uint32_t atom_add_shared(uint32_t saddr, uint32_t inc) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(saddr), "r"(inc) : "memory");
+  return old;
+}
+
+// Per-warp window source of the streamed vote: the warp's pieces of one id
+// tile flattened into 32-quad windows; next() returns this lane's quad of
+// the next window (padding past the end).  Windows must be taken in order.
+struct StreamWindows {
+  int pre, len, total, before, next_w;
+  __device__ __forceinline__ void begin(int len_, uint32_t lbase_minus, uint32_t *w_off_row) {
+    const int lane = threadIdx.x & 31;
+    len = len_;
+    int incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    total = __shfl_sync(0xffffffffu, incl, 31);
+    pre = incl - len;
+    const unsigned ne = __ballot_sync(0xffffffffu, len > 0);
+    __syncwarp();  // the previous tile's rank table has been read by every lane
+    if (len > 0) w_off_row[__popc(ne & lanemask_lt())] = lbase_minus - (uint32_t)pre;
+    __syncwarp();
+    before = 0;
+    next_w = 0;
+  }
+  __device__ __forceinline__ int windows() const { return (total + 31) >> 5; }
+  __device__ __forceinline__ uint4 next(unsigned long long wb, const uint32_t *w_off_row, uint4 padq) {
+    const int lane = threadIdx.x & 31;
+    const int w0 = 32 * next_w++;
+    const int rel = pre - w0;
+    const bool inwin = len > 0 && (unsigned)rel < 32u;
+    const unsigned starts = __reduce_or_sync(0xffffffffu, inwin ? (1u << rel) : 0u);
+    const int rank = before + __popc(starts & (0xffffffffu >> (31 - lane))) - 1;
+    before += __popc(starts);
+    const int e = w0 + lane;
+    return e < total ? __ldg(reinterpret_cast<const uint4 *>(wb) + (w_off_row[rank] + (uint32_t)e)) : padq;
+  }
+};
+
+// The streamed vote: one CTA (1024 threads, one per SM) per query at a time;
+// warp w owns the contiguous tree range [w*T/32, (w+1)*T/32) (<= 32 trees,
+// one per lane).  Per id tile, the warp flattens its trees' pieces (quads)
+// into 32-quad windows: a lane finds the piece holding its quad from the
+// piece starts inside the window (__reduce_or_sync) and a 32-entry rank
+// table, loads the quad with one 16-byte load and bumps its 4 counters.
+// Loads run P windows ahead of the bumps (a register ring), across tile
+// boundaries: the next tile's first windows are loaded before the barrier
+// that separates the tiles.  The increment that lifts a count to v appends
+// the id to the query's list (the reference's `counts[idx] == v` emission,
+// _cy.pyx:75-77; order within a tile is not kept).  ncand may exceed cap
+// (only cap ids stored).
+template <int CW, int P>
 __global__ void __launch_bounds__(1024, 1) k_vote_stream(VoteArgs a, const uint4 *__restrict__ qs,
                                                          const int32_t *__restrict__ qbase, int64_t tstride) {
   extern __shared__ uint4 vote_smem[];
   uint32_t *cnt = reinterpret_cast<uint32_t *>(vote_smem);
-  const int cwords = (counter_words<CW>(a.W) + 3) & ~3;
+  uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
+  asm volatile("" : "+r"(cnt_s));  // computed once, not re-derived per bump
+  const int cwords = (counter_words<CW>(a.W) + 3) & ~3;  // + 32 spare words (padding targets)
+  const uint32_t pad = quad_pad<CW>(a.W);
+  const uint32_t pad_word = pad >> 7;  // entries addressing words >= pad_word are padding
   constexpr int NW = 32;
-  __shared__ int32_t w_off[NW][32];
+  __shared__ uint32_t w_off[NW][32];
   __shared__ int s_nc;
   constexpr uint32_t MASK = CW == 1 ? 0xffu : (CW == 3 ? 0x3ffu : (CW == 2 ? 0xffffu : 0xffffffffu));
   const uint32_t vm1 = (uint32_t)(a.v - 1);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t nc_s = (uint32_t)__cvta_generic_to_shared(&s_nc);
+  asm volatile("" : "+r"(nc_s));
+  const int cap32 = a.cap < 0x7fffffff ? (int)a.cap : 0x7fffffff;
   const int64_t dstride = a.ntiles + 1;
   const int t_lo = (int)(((int64_t)warp * a.T) / NW);
   const int t_hi = (int)(((int64_t)(warp + 1) * a.T) / NW);
   const int t = t_lo + lane;
   const bool has = t < t_hi;
-  const uint4 *wbase = qs + (int64_t)t_lo * tstride;
+  // the warp's first tree row, kept in a register (opaque to the compiler,
+  // which would otherwise re-derive it from the kernel parameters per load)
+  unsigned long long wb = reinterpret_cast<unsigned long long>(qs + (int64_t)t_lo * tstride);
+  asm volatile("" : "+l"(wb));
+  uint32_t *woff = w_off[warp];
   uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
+  const uint4 padq = make_uint4(pad, pad, pad, pad);
   for (int64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
     const uint16_t *dl = nullptr;
-    int32_t lbase = 0;
-    int dcur = 0, dnxt = 0;
+    uint32_t lbase = 0;
+    int dcur = 0, dnxt = 0, dnn = 0;
     if (has) {
       const int64_t g = (int64_t)t * a.L + a.leaves[q * a.T + t];
       dl = a.dir + g * dstride;
-      lbase = (int32_t)((int64_t)lane * tstride + qbase[g]);
+      lbase = (uint32_t)((int64_t)lane * tstride + qbase[g]);
       dcur = dl[0];
       dnxt = dl[1];
+      dnn = a.ntiles >= 2 ? (int)__ldg(dl + 2) : 0;
     }
+    int32_t *qcand = a.cand + q * a.cap;
+    // tile 0's windows start loading before the counters are cleared
+    StreamWindows sw;
+    sw.begin(dnxt - dcur, lbase + (uint32_t)dcur, woff);
+    uint4 ring[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) ring[i] = i < sw.windows() ? sw.next(wb, woff, padq) : padq;
     for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(0u, 0u, 0u, 0u);
     if (tid == 0) s_nc = 0;
     __syncthreads();
-    int32_t *qcand = a.cand + q * a.cap;
     for (int tile = 0; tile < a.ntiles; ++tile) {
       const int32_t lo = tile * a.W;
-      const int dnn = (has && tile + 2 <= a.ntiles) ? (int)__ldg(dl + tile + 2) : 0;
-      const int len = dnxt - dcur;  // this lane's quads in this tile
-      int incl = len;
+      const int nwin = sw.windows();
+      for (int w0 = 0; w0 < nwin; w0 += P) {
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += u;
-      }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      const int pre = incl - len;
-      const unsigned ne = __ballot_sync(0xffffffffu, len > 0);
-      if (len > 0) w_off[warp][__popc(ne & lanemask_lt())] = lbase + dcur - pre;
-      __syncwarp();
-      int before = 0;  // non-empty pieces starting before the current window
-      constexpr int UNR = 4;
-      for (int e0 = 0; e0 < total; e0 += 32 * UNR) {
-        uint4 val[UNR];
+        for (int i = 0; i < P; ++i) {
+          if (w0 + i < nwin) {  // warp-uniform
+            const uint4 cur = ring[i];
+            if (w0 + i + P < nwin) ring[i] = sw.next(wb, woff, padq);
+            const uint32_t xs[4] = {cur.x, cur.y, cur.z, cur.w};
+            uint32_t old[4];
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-          const int w0 = e0 + 32 * u;
-          const int rel = pre - w0;
-          const bool inwin = len > 0 && (unsigned)rel < 32u;
-          const unsigned starts = __reduce_or_sync(0xffffffffu, inwin ? (1u << rel) : 0u);
-          const int rank = before + __popc(starts & (0xffffffffu >> (31 - lane))) - 1;
-          before += __popc(starts);
-          const int e = w0 + lane;
-          val[u] = e < total ? __ldg(wbase + (w_off[warp][rank] + e))
-                             : make_uint4(kQuadPad, kQuadPad, kQuadPad, kQuadPad);
-        }
+            for (int c = 0; c < 4; ++c) old[c] = atom_add_shared(cnt_s + (xs[c] >> 5), 1u << (xs[c] & 31u));
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-          const uint32_t xs[4] = {val[u].x, val[u].y, val[u].z, val[u].w};
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const uint32_t x = xs[c];
-            if (x != kQuadPad) {
-              const uint32_t sh = x & 31u, wd = x >> 5;
-              const uint32_t old = atomicAdd(cnt + wd, 1u << sh);
-              if (((old >> sh) & MASK) == vm1) {
-                const int pos = atomicAdd(&s_nc, 1);
-                if (pos < a.cap) qcand[pos] = lo + quad_decode<CW>(wd, sh);
+            for (int c = 0; c < 4; ++c) {
+              const uint32_t x = xs[c];
+              if (((old[c] >> (x & 31u)) & MASK) == vm1 && (x >> 7) < pad_word) {  // lifted a count to v
+                const int pos = (int)atom_add_shared(nc_s, 1u);
+                if (pos < cap32) qcand[pos] = lo + quad_decode<CW>(x >> 7, x & 31u);
               }
             }
           }
         }
       }
-      __syncwarp();  // w_off is rewritten next tile
-      __syncthreads();
-      dcur = dnxt;
-      dnxt = dnn;
+      // the next tile's windows start loading before the tile barrier
       if (tile + 1 < a.ntiles) {
+        dcur = dnxt;
+        dnxt = dnn;
+        dnn = (has && tile + 3 <= a.ntiles) ? (int)__ldg(dl + tile + 3) : 0;
+        sw.begin(dnxt - dcur, lbase + (uint32_t)dcur, woff);
+#pragma unroll
+        for (int i = 0; i < P; ++i) ring[i] = i < sw.windows() ? sw.next(wb, woff, padq) : padq;
+        __syncthreads();
         for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
       }
     }
+    __syncthreads();
     if (tid == 0) a.ncand[q] = s_nc;  // > cap means only cap ids were stored
     __syncthreads();
   }
 }
-
 }  // namespace mrpt
 
 using namespace mrpt;
@@ -1333,7 +1396,7 @@ static int32_t stream_geometry(int64_t n, int32_t T, int64_t max_count, int *CWo
   if (T < 1 || T > 1024) return fail(MRPT_EPARAM, "streamed vote: needs 1 <= T <= 1024");
   const int CW = max_count <= 255 ? 1 : (max_count <= 1023 ? 3 : (max_count <= 65535 ? 2 : 4));
   const int per = CW == 1 ? 4 : (CW == 3 ? 3 : (CW == 2 ? 2 : 1));
-  const int64_t words = (kVoteSmemStream / 4) & ~3LL;
+  const int64_t words = ((kVoteSmemStream - 128) / 4) & ~3LL;
   int64_t W = words * per;
   if (W >= n) W = n;
   *CWo = CW;
@@ -1422,9 +1485,17 @@ extern "C" int32_t mrpt_vote_stream(const uint32_t *qs, int64_t tstride, const u
   a.W = (int)W;
   a.ntiles = nt;
   a.dir = qdir;
-  const size_t smem = (size_t)((counter_words_host(CW, W) + 3) & ~3LL) * 4;
+  const size_t smem = (size_t)((counter_words_host(CW, W) + 3) & ~3LL) * 4 + 128;  // + 32 spare words
   typedef void (*sfn_t)(VoteArgs, const uint4 *, const int32_t *, int64_t);
-  sfn_t fn = CW == 1 ? k_vote_stream<1> : (CW == 3 ? k_vote_stream<3> : (CW == 2 ? k_vote_stream<2> : k_vote_stream<4>));
+  static int unr = -1;  // experiments: MRPT_VSTREAM_P (1, 2, 4): windows loaded ahead
+  if (unr < 0) {
+    const char *e1 = getenv("MRPT_VSTREAM_P");
+    unr = e1 ? atoi(e1) : 1;
+  }
+#define VS_PICK(C) \
+  (unr == 2 ? k_vote_stream<C, 2> : (unr == 4 ? k_vote_stream<C, 4> : k_vote_stream<C, 1>))
+  sfn_t fn = CW == 1 ? VS_PICK(1) : (CW == 3 ? VS_PICK(3) : (CW == 2 ? VS_PICK(2) : VS_PICK(4)));
+#undef VS_PICK
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t grid = nq < (int64_t)num_sms() ? nq : (int64_t)num_sms();
   cudaStream_t s = as_stream(stream);

@@ -1,0 +1,2 @@
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_vote_stream -c 1 -o gpurun_out/ncu_vote_stream_c5_p2 python tools/vote_ab.py --config 5 --nq 2000 --reps 1 > gpurun_out/ncu_vs2.log 2>&1
+tail -2 gpurun_out/ncu_vs2.log
