@@ -166,11 +166,7 @@ __global__ void k_level_plan(LevelArgs a) {
   const int t = (int)(seg >> a.lev), s = (int)(seg & (nseg - 1));
   const int64_t *B = a.bounds_in + (int64_t)t * a.bstride;
   const int64_t b = B[s], e = B[s + 1], m = e - b;
-  if (m <= kTinyMax) {
-    a.tiny_list[atomicAdd(&a.ctl->ntiny, 1)] = (int32_t)seg;
-  } else if (m <= kMidMax) {
-    a.mid_list[atomicAdd(&a.ctl->nmid, 1)] = (int32_t)seg;
-  } else {
+  if (m > kMidMax) {  // tiny / mid segments are found by k_seg_small itself
     const int slot = atomicAdd(&a.ctl->nbig, 1);
     const int nch = (int)ceil_div<int64_t>(m, kChunk);
     // chunk position within its tree; k_chunk_layout adds the tree's base so
@@ -248,7 +244,12 @@ __global__ void k_chunk_fill(LevelArgs a) {
   }
 }
 
-// One CTA per segment with m <= MAXM (keys and ids staged in smem).
+// One CTA per segment with m <= MAXM (keys and ids staged in smem).  CTAs
+// walk the segments in tree-major order (segment = t * 2^lev + s) and skip
+// those of the other size class, so the CTAs resident at any time gather
+// from one or two trees' projection columns, which then stay in L2 (an
+// atomically appended work list interleaves all trees of the batch and made
+// the gathers read DRAM ~13x the keys' bytes at config 5).
 template <int MAXM>
 __global__ void __launch_bounds__(kNT) k_seg_small(LevelArgs a, int which) {
   extern __shared__ uint32_t dyn_smem[];
@@ -259,14 +260,13 @@ __global__ void __launch_bounds__(kNT) k_seg_small(LevelArgs a, int which) {
   __shared__ int s_bin, s_below, s_cnt;
   __shared__ int wcnt[kNT / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int count = which == 0 ? a.ctl->ntiny : a.ctl->nmid;
-  const int32_t *list = which == 0 ? a.tiny_list : a.mid_list;
   const int nseg = 1 << a.lev;
-  for (int w = blockIdx.x; w < count; w += gridDim.x) {
-    const int seg = list[w];
-    const int t = seg >> a.lev, s = seg & (nseg - 1);
+  const int64_t total = (int64_t)a.Tb << a.lev;
+  for (int64_t seg = blockIdx.x; seg < total; seg += gridDim.x) {
+    const int t = (int)(seg >> a.lev), s = (int)(seg & (nseg - 1));
     const int64_t *B = a.bounds_in + (int64_t)t * a.bstride;
     const int64_t b = B[s], e = B[s + 1];
+    if (which == 0 ? (e - b > kTinyMax) : (e - b <= kTinyMax || e - b > kMidMax)) continue;  // CTA-uniform
     const int m = (int)(e - b);
     if (m == 0) {
       if (tid == 0) write_node(a, t, s, b, e, 0, 0.0f);

@@ -63,6 +63,62 @@ k_project_smem(const float *__restrict__ X, int64_t m, int d, int64_t ldx,
   }
 }
 
+// Float64 tile variant (the default where a warp's 32 consecutive points fit
+// in shared memory as float64): a CTA of 32 warps stages TP = 32 * PPT
+// points converted to float64 once (odd row stride in doubles: the 32 lanes
+// of a load hit 32 distinct bank pairs), every warp takes whole columns and
+// its lanes take consecutive points (lane + 32 j), so each CSC entry is one
+// warp-uniform 8-byte load (packed {row, value}) and each term one
+// conflict-free 8-byte shared load and one DFMA -- no per-term conversion.
+// Output stores are coalesced (32 consecutive points per column).
+template <int PPT>
+__global__ void __launch_bounds__(1024, 1)
+k_project_d64(const float *__restrict__ X, int64_t m, int d, int64_t ldx,
+              const int64_t *__restrict__ col_ptr, const int2 *__restrict__ ent, int ncols,
+              float *__restrict__ out, int64_t ors, int64_t ocs, int stride) {
+  extern __shared__ double xd[];
+  constexpr int TP = 32 * PPT;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t tile = blockIdx.x; tile * TP < m; tile += gridDim.x) {
+    const int64_t i0 = tile * TP;
+    const int here = (int)((m - i0) < TP ? (m - i0) : TP);
+    __syncthreads();
+    for (int r = warp; r < TP; r += nw) {
+      const float *src = X + (i0 + r) * ldx;
+      double *dst = xd + r * stride;
+      for (int c = lane; c < d; c += 32) dst[c] = r < here ? (double)__ldg(src + c) : 0.0;
+    }
+    __syncthreads();
+    const double *xb = xd + lane * stride;
+    for (int c = warp; c < ncols; c += nw) {
+      const int64_t s0 = __ldg(col_ptr + c), s1 = __ldg(col_ptr + c + 1);
+      double acc[PPT];
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) acc[j] = 0.0;
+#pragma unroll 4
+      for (int64_t s = s0; s < s1; ++s) {
+        const int2 e = __ldg(ent + s);
+        const double v = (double)__int_as_float(e.y);
+        const double *xr = xb + e.x;
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) acc[j] = __fma_rn(xr[j * 32 * stride], v, acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        const int p = lane + 32 * j;
+        if (p < here) out[(i0 + p) * ors + (int64_t)c * ocs] = __double2float_rn(acc[j]);
+      }
+    }
+  }
+}
+
+// {row, value bits} pairs of a CSC column set (one 8-byte load per entry).
+__global__ void k_pack_entries(const int32_t *__restrict__ rows, const float *__restrict__ vals, int64_t nnz,
+                               int2 *ent) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nnz; s += (int64_t)gridDim.x * blockDim.x)
+    ent[s] = make_int2(rows[s], __float_as_int(vals[s]));
+}
+
 // Fallback for rows too wide to stage (d beyond ~1.6K): one thread per
 // (point, column), coordinates read through the read-only path.
 __global__ void __launch_bounds__(256)
@@ -201,6 +257,39 @@ extern "C" int32_t mrpt_project(const float *X, int64_t m, int32_t d, int64_t ld
   cudaStream_t s = as_stream(stream);
   const int stride = (d & 1) ? d : d + 1;
   const int64_t row_bytes = (int64_t)stride * 4;
+  // float64 tile: as many 32-point groups as fit (PPT 1..6)
+  {
+    const char *pe = getenv("MRPT_PROJ_D64");  // experiments: 0 disables
+    int ppt = (int)((212 * 1024) / ((int64_t)stride * 8 * 32));
+    if (ppt > 6) ppt = 6;
+    if ((!pe || atoi(pe) != 0) && ppt >= 1 && ncols >= 32) {
+      int64_t nnz = 0;
+      cudaMemcpyAsync(&nnz, col_ptr + ncols, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+      if (cudaStreamSynchronize(s) != cudaSuccess) return launch_status("mrpt_project");
+      int2 *ent = nullptr;
+      keep_pool_warm();
+      if (cudaMallocAsync((void **)&ent, sizeof(int2) * (nnz > 0 ? nnz : 1), s) != cudaSuccess)
+        return fail(MRPT_ECUDA, "mrpt_project: scratch allocation failed");
+      if (nnz > 0) {
+        const int64_t pb = ceil_div<int64_t>(nnz, 256);
+        (count_launch(), k_pack_entries<<<(unsigned)(pb < 4096 ? pb : 4096), 256, 0, s>>>(rows, vals, nnz, ent));
+      }
+      const size_t smem = (size_t)32 * ppt * stride * 8;
+      void (*fn)(const float *, int64_t, int, int64_t, const int64_t *, const int2 *, int, float *, int64_t,
+                 int64_t, int) =
+          ppt >= 6 ? k_project_d64<6>
+                   : (ppt == 5 ? k_project_d64<5>
+                               : (ppt == 4 ? k_project_d64<4>
+                                           : (ppt == 3 ? k_project_d64<3> : (ppt == 2 ? k_project_d64<2> : k_project_d64<1>))));
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const int64_t tiles = ceil_div<int64_t>(m, 32 * ppt);
+      const int grid = (int)(tiles < (int64_t)num_sms() ? tiles : (int64_t)num_sms());
+      (count_launch(), fn<<<grid, 1024, smem, s>>>(X, m, d, ldx, col_ptr, ent, ncols, out, out_row_stride,
+                                                  out_col_stride, stride));
+      cudaFreeAsync(ent, s);
+      return launch_status("mrpt_project");
+    }
+  }
   // tile of 256, 128 or 64 points (point groups must be a power-of-two
   // multiple of the warp so every thread has a column group)
   int tp = 256;

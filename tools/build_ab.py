@@ -1,0 +1,37 @@
+"""Build-time A/B in one process: grow_trees on a configuration twice per
+variant (the first warms), variants chosen by environment settings given as
+NAME=VAL[,NAME=VAL] arguments; also checks the variants build identical trees.
+usage: python tools/build_ab.py CONFIG SCALE "MRPT_PROJ_D64=0" "MRPT_PROJ_D64=1" ..."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_1509_06957_b200 as mrpt  # noqa: E402
+from paper_1509_06957_b200 import workloads  # noqa: E402
+
+cfg, scale = int(sys.argv[1]), float(sys.argv[2])
+X, Q, p = workloads.generate(cfg, scale)
+Xd = torch.from_numpy(X).cuda()
+ref = None
+for spec in sys.argv[3:]:
+    for kv in spec.split(","):
+        k, v = kv.split("=")
+        os.environ[k] = v
+    ts = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        index = mrpt.grow_trees(Xd, p["n_trees"], p["depth"], p["sparsity"], seed=0)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    D = index.device_index()
+    sig = (D.splits.cpu().numpy().tobytes(), D.offsets.cpu().numpy().tobytes(),
+           D.indices[:: max(1, p["n_trees"] // 7)].cpu().numpy().tobytes())
+    same = ref is None or sig == ref
+    ref = ref or sig
+    print(f"config {cfg} scale {scale} [{spec}]: build {ts[-1]:.3f} s (first {ts[0]:.3f}) same={same}",
+          flush=True)
+    del index, D

@@ -8,11 +8,14 @@ rows = list(csv.reader(open(sys.argv[1])))
 hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 h = rows[hdr]
 ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+mi = h.index("Metric Name") if "Metric Name" in h else None
 agg = defaultdict(lambda: [0, 0.0])
 scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
          "second": 1e6, "s": 1e6}
 for r in rows[hdr + 1:]:
     if len(r) <= vi or not r[vi]:
+        continue
+    if mi is not None and r[mi] != "gpu__time_duration.sum":
         continue
     name = r[ki].split("(")[0].replace("void ", "")
     agg[name][0] += 1
