@@ -263,7 +263,7 @@ int32_t mrpt_u8_gemm_rows(const void *Xq, int64_t n, int64_t ldq, const float *s
  * mrpt_scan_topk_u8tc_workspace_size (smaller workspaces run smaller query
  * chunks). */
 int32_t mrpt_scan_topk_u8tc_workspace_size(int64_t n, int64_t ldq, int64_t nq,
-                                           int64_t *bytes);
+                                           int64_t *bytes /* host */);
 int32_t mrpt_scan_topk_u8tc_bits(const float *X, int64_t n, int32_t d, int64_t ldx,
                                  const void *Xs, int64_t ldq, const void *info,
                                  const float *Q, int64_t nq, int64_t ldqq,
@@ -283,7 +283,7 @@ int32_t mrpt_fallback_stats(int64_t *out /* host */, int32_t reset);
  * milliseconds and the number of bracketed launches.  Enabling (or
  * disabling) clears the record. */
 int32_t mrpt_kernel_timer(int32_t enable);
-int32_t mrpt_kernel_timer_read(double *ms, int64_t *launches);
+int32_t mrpt_kernel_timer_read(double *ms /* host */, int64_t *launches /* host */);
 
 /* Sorted de-duplication of arbitrary candidate ids (np.unique,
  * search.py:157) through an n-bit bitmap.  ids outside [0, n) set
