@@ -92,7 +92,8 @@ def config_dict(p, v, world):
             "l2": "device steps: L2 flushed between timed steps (256 MB write outside the step "
                   "events); inputs far above L2 (X %.0f MB, leaf ids %.0f MB)" % (
                       4.0 * p["n"] * p["d"] / 1e6, 4.0 * p["n_trees"] * p["n"] / 1e6),
-            "parallelism": f"replicated index, queries sharded by batch x{world}"}
+            "parallelism": (f"dp{world}: tree blocks built per rank and broadcast per batch; replicated "
+                            f"index; each rank answers its own {p['nq']}-query batch (weak scaling)")}
 
 
 class Clocks:

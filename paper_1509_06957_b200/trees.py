@@ -496,10 +496,11 @@ def _validate_grow(X, n_trees, depth, sparsity, seed, threads):
 
 
 def _grow_block(X, t_begin, t_end, depth, sparsity, seed, fixed_count, splits, offsets, indices,
-                batch_trees=None):
+                batch_trees=None, after_batch=None):
     """Build trees [t_begin, t_end) of an index (tree t from seed (seed, t)) into
     the device arrays ``splits/offsets/indices`` (rows 0 .. t_end-t_begin-1).
-    Returns the host matrices of those trees.  No host synchronisation."""
+    Returns the host matrices of those trees.  No host synchronisation.
+    ``after_batch(j)`` is called once the kernels of batch j are enqueued."""
     torch = _device.torch_mod()
     Xd = X.device()
     n, d = X.n, X.d
@@ -529,6 +530,8 @@ def _grow_block(X, t_begin, t_end, depth, sparsity, seed, fixed_count, splits, o
                      _native.ptr(splits[b0:]), _native.ptr(offsets[b0:]),
                      _native.ptr(indices[b0:]), _native.ptr(ws), sz.value, stream)
         del cp, rows, vals
+        if after_batch is not None:
+            after_batch(b0 // tb)
     return matrices
 
 
