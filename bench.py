@@ -443,7 +443,7 @@ def run_ours(args):
     elapsed_ms = sum(a.elapsed_time(b) for a, b in step_ev)
     for ev in evs:
         for name, a, b in ev:
-            stage_ms[name] += a.elapsed_time(b)
+            stage_ms[name] = stage_ms.get(name, 0.0) + a.elapsed_time(b)
     launches = int(lib.mrpt_launch_count()) - launches0  # this library's kernels, timed steps only
     fb = {r: x for r, x in fallback_stats().items() if x["queries"]}
     kt_ms, kt_n = ctypes.c_double(0.0), ctypes.c_int64(0)

@@ -334,6 +334,22 @@ int32_t mrpt_vote_stream(const uint32_t *qs, int64_t tstride, const uint16_t *qd
                          int64_t max_count, const int32_t *leaves, int64_t nq, int32_t v,
                          int32_t *cand, int64_t cap, int32_t *ncand, void *stream);
 
+/* Query ordering for a batch (no reference counterpart: the reference
+ * answers one query per call, search.py:175-184).  order (nq int32) lists
+ * the queries grouped by their leaf in tree 0 (leaves: (nq, T) int32 from
+ * mrpt_query_route); ws: 2^depth int32 scratch.  Processing the batch in
+ * this order lets concurrent CTAs share leaf slices and candidate rows in
+ * L2; answers do not depend on it. */
+int32_t mrpt_query_order(const int32_t *leaves, int64_t nq, int32_t T, int32_t depth,
+                         int32_t *order, int32_t *ws, void *stream);
+
+/* Row permutation of a (rows, words) array of 4-byte words (leading
+ * dimensions in words): scatter == 0 gathers dst[i] = src[idx[i]],
+ * scatter != 0 scatters dst[idx[i]] = src[i]. */
+int32_t mrpt_permute_rows(const void *src, int64_t src_ld, const int32_t *idx, int64_t rows,
+                          int64_t words, void *dst, int64_t dst_ld, int32_t scatter,
+                          void *stream);
+
 /* ------------------------------------------------------------------ f3 --
  * Exact brute-force k-NN (ground truth): replaces evaluation.brute_force_knn
  * and compute_ground_truth (pkg/src/mrpt/evaluation.py:28-81).  Q (nq, ldq)

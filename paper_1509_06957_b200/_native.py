@@ -71,6 +71,8 @@ SIGNATURES = {
     "mrpt_brute_force_workspace_size": [_c_i64, _c_i32, _c_i64, _c_i32, ctypes.POINTER(_c_i64)],
     "mrpt_brute_force_knn": [_c_p, _c_i64, _c_i32, _c_i64, _c_p, _c_i64, _c_i64, _c_i32, _c_p, _c_p,
                              _c_p, _c_i64, _c_p],
+    "mrpt_query_order": [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p],
+    "mrpt_permute_rows": [_c_p, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_i32, _c_p],
     "mrpt_check_finite": [_c_p, _c_i64, _c_p, _c_p],
     "mrpt_audit_leaves": [_c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p],
 }

@@ -39,6 +39,7 @@ struct VoteArgs {
   uint32_t *bits_out;    // optional: candidate bitmap per query instead of lists
   int64_t bstride;       // words per query in bits_out
   uint16_t *cnt_out;     // optional: each listed candidate's vote count (saturated), beside cand
+  int dbg;               // timing experiments only (MRPT_VOTE_DBG): 1 no bumps, 2 no per-tile clearing
 };
 
 // Vote count of tile-local id `local` in the packed counters (code cw).
@@ -954,6 +955,20 @@ __device__ __forceinline__ uint32_t atom_add_shared(uint32_t saddr, uint32_t inc
   return old;
 }
 
+// 16-byte load that bypasses L1 allocation and asks L2 to fetch the whole
+// 256-byte block around it from DRAM: a leaf slice stores its per-tile pieces
+// back to back, so the pieces of the next tiles arrive with this one and are
+// found in L2 later, and DRAM serves 256-byte bursts instead of scattered
+// 32-byte sectors (random small reads are bound by row activations, not by
+// bandwidth).
+__device__ __forceinline__ uint4 ld_quad_l2_256(const uint4 *p) {
+  uint4 v;
+  asm volatile("ld.global.cg.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
 // Per-warp window source of the streamed vote: the warp's pieces of one id
 // tile flattened into 32-quad windows; next() returns this lane's quad of
 // the next window (padding past the end).  Windows must be taken in order.
@@ -978,6 +993,7 @@ struct StreamWindows {
     next_w = 0;
   }
   __device__ __forceinline__ int windows() const { return (total + 31) >> 5; }
+  template <bool CG>
   __device__ __forceinline__ uint4 next(unsigned long long wb, const uint32_t *w_off_row, uint4 padq) {
     const int lane = threadIdx.x & 31;
     const int w0 = 32 * next_w++;
@@ -987,7 +1003,12 @@ struct StreamWindows {
     const int rank = before + __popc(starts & (0xffffffffu >> (31 - lane))) - 1;
     before += __popc(starts);
     const int e = w0 + lane;
-    return e < total ? __ldg(reinterpret_cast<const uint4 *>(wb) + (w_off_row[rank] + (uint32_t)e)) : padq;
+    // .cg: the quads are read once; with the counters taking most of the
+    // shared/L1 carve-out, allocating them in L1 only throttles the loads
+    if (e >= total) return padq;
+    const uint4 *src = reinterpret_cast<const uint4 *>(wb) + (w_off_row[rank] + (uint32_t)e);
+    if (CG) return ld_quad_l2_256(src);
+    return __ldg(src);
   }
 };
 
@@ -1003,7 +1024,7 @@ struct StreamWindows {
 // the id to the query's list (the reference's `counts[idx] == v` emission,
 // _cy.pyx:75-77; order within a tile is not kept).  ncand may exceed cap
 // (only cap ids stored).
-template <int CW, int P>
+template <int CW, int P, bool CG>
 __global__ void __launch_bounds__(1024, 1) k_vote_stream(VoteArgs a, const uint4 *__restrict__ qs,
                                                          const int32_t *__restrict__ qbase, int64_t tstride) {
   extern __shared__ uint4 vote_smem[];
@@ -1052,7 +1073,7 @@ __global__ void __launch_bounds__(1024, 1) k_vote_stream(VoteArgs a, const uint4
     sw.begin(dnxt - dcur, lbase + (uint32_t)dcur, woff);
     uint4 ring[P];
 #pragma unroll
-    for (int i = 0; i < P; ++i) ring[i] = i < sw.windows() ? sw.next(wb, woff, padq) : padq;
+    for (int i = 0; i < P; ++i) ring[i] = i < sw.windows() ? sw.template next<CG>(wb, woff, padq) : padq;
     for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(0u, 0u, 0u, 0u);
     if (tid == 0) s_nc = 0;
     __syncthreads();
@@ -1064,11 +1085,12 @@ __global__ void __launch_bounds__(1024, 1) k_vote_stream(VoteArgs a, const uint4
         for (int i = 0; i < P; ++i) {
           if (w0 + i < nwin) {  // warp-uniform
             const uint4 cur = ring[i];
-            if (w0 + i + P < nwin) ring[i] = sw.next(wb, woff, padq);
+            if (w0 + i + P < nwin) ring[i] = sw.template next<CG>(wb, woff, padq);
             const uint32_t xs[4] = {cur.x, cur.y, cur.z, cur.w};
             uint32_t old[4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) old[c] = atom_add_shared(cnt_s + (xs[c] >> 5), 1u << (xs[c] & 31u));
+            for (int c = 0; c < 4; ++c)
+              old[c] = (a.dbg & 1) ? xs[c] : atom_add_shared(cnt_s + (xs[c] >> 5), 1u << (xs[c] & 31u));
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               const uint32_t x = xs[c];
@@ -1087,9 +1109,10 @@ __global__ void __launch_bounds__(1024, 1) k_vote_stream(VoteArgs a, const uint4
         dnn = (has && tile + 3 <= a.ntiles) ? (int)__ldg(dl + tile + 3) : 0;
         sw.begin(dnxt - dcur, lbase + (uint32_t)dcur, woff);
 #pragma unroll
-        for (int i = 0; i < P; ++i) ring[i] = i < sw.windows() ? sw.next(wb, woff, padq) : padq;
+        for (int i = 0; i < P; ++i) ring[i] = i < sw.windows() ? sw.template next<CG>(wb, woff, padq) : padq;
         __syncthreads();
-        for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+        if (!(a.dbg & 2))
+          for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
       }
     }
@@ -1485,15 +1508,18 @@ extern "C" int32_t mrpt_vote_stream(const uint32_t *qs, int64_t tstride, const u
   a.W = (int)W;
   a.ntiles = nt;
   a.dir = qdir;
+  a.dbg = getenv("MRPT_VOTE_DBG") ? atoi(getenv("MRPT_VOTE_DBG")) : 0;
   const size_t smem = (size_t)((counter_words_host(CW, W) + 3) & ~3LL) * 4 + 128;  // + 32 spare words
   typedef void (*sfn_t)(VoteArgs, const uint4 *, const int32_t *, int64_t);
   static int unr = -1;  // experiments: MRPT_VSTREAM_P (1, 2, 4): windows loaded ahead
   if (unr < 0) {
     const char *e1 = getenv("MRPT_VSTREAM_P");
-    unr = e1 ? atoi(e1) : 1;
+    unr = e1 ? atoi(e1) : 1;  // 2 and 4 measured slower (364, 404 vs 357 ms at config 5)
   }
-#define VS_PICK(C) \
-  (unr == 2 ? k_vote_stream<C, 2> : (unr == 4 ? k_vote_stream<C, 4> : k_vote_stream<C, 1>))
+  static const bool cg = !(getenv("MRPT_VSTREAM_CG") && atoi(getenv("MRPT_VSTREAM_CG")) == 0);
+#define VS_PICK(C)                                                                              \
+  (cg ? (unr == 2 ? k_vote_stream<C, 2, true> : (unr == 4 ? k_vote_stream<C, 4, true> : k_vote_stream<C, 1, true>)) \
+      : (unr == 2 ? k_vote_stream<C, 2, false> : (unr == 4 ? k_vote_stream<C, 4, false> : k_vote_stream<C, 1, false>)))
   sfn_t fn = CW == 1 ? VS_PICK(1) : (CW == 3 ? VS_PICK(3) : (CW == 2 ? VS_PICK(2) : VS_PICK(4)));
 #undef VS_PICK
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -257,6 +257,10 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None, size_class=N
     if chunk is None:
         per_q = 4 * (D.T + (bstride if bits_mode else cap))
         chunk = max(1, min(nq, (1 << 30) // per_q))
+    if (not bits_mode and choice is not None and nq >= 2 * _ORDER_MIN
+            and os.environ.get("MRPT_QUERY_ORDER", "1") != "0" and D.vote_stream() is not None
+            and nq * D.T * 4 <= (2 << 30)):
+        return _query_device_ordered(D, Qd, k, votes, choice, cap, chunk, stage, (ids, dists, counts))
     m0 = min(chunk, nq)
     leaves = torch.empty((m0, D.T), dtype=torch.int32, device=dev)
     cand = None
@@ -292,6 +296,62 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None, size_class=N
 
 
 _BITS_ROUTES = ("u8tc_bits",)
+_ORDER_MIN = 4096  # queries: below this a batch is processed in its own order
+
+
+def _permute(src, idx, dst, scatter):
+    """dst[i] = src[idx[i]] (gather) or dst[idx[i]] = src[i] (scatter), rows of
+    4-byte words (mrpt_permute_rows)."""
+    words = src[0].numel() * src.element_size() // 4
+    _native.call("mrpt_permute_rows", _native.ptr(src), int(src.stride(0)) * src.element_size() // 4,
+                 _native.ptr(idx), int(idx.shape[0]), words, _native.ptr(dst),
+                 int(dst.stride(0)) * dst.element_size() // 4, 1 if scatter else 0,
+                 _native.stream_ptr())
+
+
+def _query_device_ordered(D, Qd, k, votes, variant, cap, chunk, stage, out):
+    """query_device for a large batch over a multi-tile index: route the whole
+    batch (K2), order the queries by their leaf in tree 0
+    (mrpt_query_order), gather the query rows and leaves into that order, run
+    K3 + K4 chunk by chunk on the ordered batch -- concurrent CTAs then share
+    leaf slices and candidate rows in L2 -- and scatter the answers back.
+    Identical results (queries are independent)."""
+    torch = _device.torch_mod()
+    nq = int(Qd.shape[0])
+    dev = Qd.device
+    leaves = torch.empty((nq, D.T), dtype=torch.int32, device=dev)
+    stage("route", _route_launch, D, Qd, nq, int(Qd.stride(0)), leaves)
+    order = torch.empty(nq, dtype=torch.int32, device=dev)
+    ws = D.workspace("qorder", 4 << D.depth)
+    Qp = torch.empty((nq, D.d), dtype=torch.float32, device=dev)
+    lp = torch.empty_like(leaves)
+
+    def reorder():
+        _native.call("mrpt_query_order", _native.ptr(leaves), nq, D.T, D.depth, _native.ptr(order),
+                     _native.ptr(ws), _native.stream_ptr())
+        _permute(Qd, order, Qp, False)
+        _permute(leaves, order, lp, False)
+
+    stage("reorder", reorder)
+    ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
+    dists = torch.empty((nq, k), dtype=torch.float64, device=dev)
+    counts = torch.empty(nq, dtype=torch.int32, device=dev)
+    m0 = min(chunk, nq)
+    cand = torch.empty((m0, cap), dtype=torch.int32, device=dev)
+    for s in range(0, nq, chunk):
+        e = min(nq, s + chunk)
+        stage("vote", _vote_list, D, lp[s:e], e - s, votes, cand, cap, counts[s:e])
+        args = (Qp[s:e], e - s, int(Qp.stride(0)), cand, cap, counts[s:e], k, ids[s:e], dists[s:e])
+        stage("scan_topk", _scan_launch, D, variant, args)
+    oids, odists, ocounts = out
+
+    def restore():
+        _permute(ids, order, oids, True)
+        _permute(dists, order, odists, True)
+        _permute(counts.view(nq, 1), order, ocounts.view(nq, 1), True)
+
+    stage("reorder", restore)
+    return oids, odists, ocounts
 
 
 def _run_bits(D, qb, m, ldq, leaves, votes, bits, bstride, counts, k, ids, dists, stage=None,
