@@ -847,13 +847,25 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_filter_h(TopkArgs a, d
     int cnt = 0;
     float su = __int_as_float(0x7f800000);  // sqrt(U_k), +inf until the first shrink
     bool bad = false;
-    for (int64_t g = (int64_t)warp * kFU; g < m; g += (int64_t)NWARP * kFU) {
+    // A warp takes 32 * kFU consecutive candidates at a time: one coalesced
+    // load puts lane l's kFU ids in registers, and each of the 32 iterations
+    // broadcasts its kFU ids by shuffle -- the rows of an iteration wait for
+    // one memory round trip instead of the id load and then the row load.
+    for (int64_t c0 = (int64_t)warp * (32 * kFU); c0 < m && !bad; c0 += (int64_t)NWARP * 32 * kFU) {
+      int32_t lane_ids[kFU];
+#pragma unroll
+      for (int u = 0; u < kFU; ++u) {
+        const int64_t j = c0 + (int64_t)kFU * lane + u;
+        lane_ids[u] = j < m ? (qc ? __ldg(qc + j) : (int32_t)j) : -1;
+      }
+      const int64_t left = m - c0;
+      const int nit = left >= 32 * kFU ? 32 : (int)((left + kFU - 1) / kFU);
+    for (int it = 0; it < nit; ++it) {
       int32_t cidv[kFU];
       const __half *row[kFU];
 #pragma unroll
       for (int u = 0; u < kFU; ++u) {
-        const int64_t j = g + u;
-        cidv[u] = j < m ? (qc ? __ldg(qc + j) : (int32_t)j) : -1;
+        cidv[u] = __shfl_sync(0xffffffffu, lane_ids[u], it);
         row[u] = a.Xh + (int64_t)(cidv[u] < 0 ? 0 : cidv[u]) * a.ldh;
       }
       const float myr = (lane < kFU && cidv[lane < kFU ? lane : 0] >= 0)
@@ -922,6 +934,7 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_filter_h(TopkArgs a, d
           break;
         }
       }
+    }
     }
     __syncwarp();
     if (lane == 0) {
