@@ -938,16 +938,6 @@ __global__ void k_vstream_fill(const int32_t *__restrict__ leaf_indices, const i
   }
 }
 
-// The streamed vote: one CTA (1024 threads, one per SM) per query at a time;
-// warp w owns the contiguous tree range [w*T/32, (w+1)*T/32) (<= 32 trees,
-// one per lane).  Per id tile, the warp flattens its trees' pieces (quads)
-// into 32-quad windows: a lane finds the piece holding its quad from the
-// piece starts inside the window (__reduce_or_sync) and a 32-entry rank
-// table, loads the quad with one 16-byte load and bumps its 4 counters.  The
-// increment that lifts a count to v appends the id to the query's list
-// (the reference's `counts[idx] == v` emission, _cy.pyx:75-77; order within
-// a tile is not kept).  Counters are zeroed per tile; ncand may exceed cap
-// (only cap ids stored).
 // Shared-memory atomic add at a 32-bit shared address; returns the old word.
 __device__ __forceinline__ uint32_t atom_add_shared(uint32_t saddr, uint32_t inc) {
   uint32_t old;
@@ -959,8 +949,9 @@ __device__ __forceinline__ uint32_t atom_add_shared(uint32_t saddr, uint32_t inc
 // 256-byte block around it from DRAM: a leaf slice stores its per-tile pieces
 // back to back, so the pieces of the next tiles arrive with this one and are
 // found in L2 later, and DRAM serves 256-byte bursts instead of scattered
-// 32-byte sectors (random small reads are bound by row activations, not by
-// bandwidth).
+// 32-byte sectors (HBM serves ~5.5G random accesses/s at any size up to
+// 512 bytes, tools/micro/rand_bw.cu: small scattered reads are bound by the
+// access rate, not by bandwidth).
 __device__ __forceinline__ uint4 ld_quad_l2_256(const uint4 *p) {
   uint4 v;
   asm volatile("ld.global.cg.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
