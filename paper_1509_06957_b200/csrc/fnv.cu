@@ -6,8 +6,9 @@
 // x = l ^ b, h' = (h - l + x) * P, so over a chunk of m bytes starting from
 // state h0 with low byte L the result is h0 * P^m + C(L), where C(L) only
 // depends on the chunk and L.  Three passes:
-//   A  per chunk, the 256 -> 256 low-byte permutation (one thread per L,
-//      two integer ops per byte, bytes broadcast from shared memory);
+//   A  per chunk, the 256 -> 256 low-byte permutation (128 starts walked,
+//      two per thread, 1.5 integer ops per start and byte, bytes broadcast
+//      from shared memory);
 //   S  a serial walk over the permutations gives each chunk's true L;
 //   B  one thread per chunk computes C(L) for that L only;
 // then h <- h * P^m + C_chunk composes the chunks in order.
@@ -17,45 +18,63 @@ namespace mrpt {
 
 constexpr unsigned long long kFnvOffset = 0xCBF29CE484222325ull;
 constexpr unsigned long long kFnvPrime = 0x100000001B3ull;
-constexpr int kFnvStage = 16384;  // bytes staged in smem per step (pass A)
+constexpr int kFnvStage = 4096;  // bytes staged in smem per step (pass A)
 constexpr int kStartBlock = 64;   // chunk tables staged per step of the serial walk
 
-// Pass A: the chunk's low-byte permutation, one thread per starting value.
-// Only the low 8 bits of l matter, so no masking inside the loop.
-__global__ void __launch_bounds__(256) k_fnv_perm(const uint8_t *__restrict__ buf, int64_t nbytes,
-                                                  int64_t chunk, uint8_t *perm) {
-  __shared__ uint32_t stage[kFnvStage / 4];
+// Pass A: the chunk's low-byte permutation.  Two facts cut the work 4x:
+//  * the top bit rides along: (l ^ 0x80) ^ b = (l ^ b) ^ 0x80, and since
+//    0xB3 is odd, ((x ^ 0x80) * 0xB3) & 0xFF = ((x * 0xB3) & 0xFF) ^ 0x80,
+//    so perm(L ^ 0x80) = perm(L) ^ 0x80 and only L < 128 is walked;
+//  * two starts share a 32-bit register as 16-bit lanes: per byte one PRMT
+//    (the byte into both lanes), one LOP3 ((l & 0x00FF00FF) ^ bb) and one
+//    IMAD (x * 0xB3: the low lane's product stays below 2^16).
+// 64 threads per chunk, each walking starts 2t and 2t+1.
+constexpr int kFnvThreads = 64;
+__global__ void __launch_bounds__(kFnvThreads) k_fnv_perm(const uint8_t *__restrict__ buf, int64_t nbytes,
+                                                          int64_t chunk, uint8_t *perm) {
+  __shared__ uint4 stage[kFnvStage / 16];
   const int64_t c = blockIdx.x;
   const int64_t b0 = c * chunk;
   const int64_t b1 = (b0 + chunk) < nbytes ? (b0 + chunk) : nbytes;
-  uint32_t l = threadIdx.x;
-  const bool al = ((reinterpret_cast<uintptr_t>(buf + b0) & 3u) == 0);
+  const uint32_t t = threadIdx.x;
+  uint32_t l = (2 * t) | ((2 * t + 1) << 16);
+  constexpr uint32_t M = 0x00FF00FFu;
+  const bool al = ((reinterpret_cast<uintptr_t>(buf + b0) & 15u) == 0);
   for (int64_t s0 = b0; s0 < b1; s0 += kFnvStage) {
     const int len = (int)((b1 - s0) < kFnvStage ? (b1 - s0) : kFnvStage);
     __syncthreads();
     if (al) {
-      const uint32_t *src = reinterpret_cast<const uint32_t *>(buf + s0);
-      for (int i = threadIdx.x; i < len / 4; i += blockDim.x) stage[i] = __ldg(src + i);
+      const uint4 *src = reinterpret_cast<const uint4 *>(buf + s0);
+      for (int i = t; i < len / 16; i += kFnvThreads) stage[i] = __ldg(src + i);
     } else {
       uint8_t *st8 = reinterpret_cast<uint8_t *>(stage);
-      for (int i = threadIdx.x; i < (len & ~3); i += blockDim.x) st8[i] = buf[s0 + i];
+      for (int i = t; i < (len & ~15); i += kFnvThreads) st8[i] = buf[s0 + i];
     }
     __syncthreads();
-    const int nw = len / 4;
-#pragma unroll 4
-    for (int i = 0; i < nw; ++i) {
-      uint32_t w = stage[i];
-      l = (l ^ w) * 0xB3u;
-      w >>= 8;
-      l = (l ^ w) * 0xB3u;
-      w >>= 8;
-      l = (l ^ w) * 0xB3u;
-      w >>= 8;
-      l = (l ^ w) * 0xB3u;
+    const int nv = len / 16;
+#pragma unroll 2
+    for (int i = 0; i < nv; ++i) {
+      const uint4 v = stage[i];
+      const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        l = ((l & M) ^ __byte_perm(ws[q], 0u, 0x4040u)) * 0xB3u;
+        l = ((l & M) ^ __byte_perm(ws[q], 0u, 0x4141u)) * 0xB3u;
+        l = ((l & M) ^ __byte_perm(ws[q], 0u, 0x4242u)) * 0xB3u;
+        l = ((l & M) ^ __byte_perm(ws[q], 0u, 0x4343u)) * 0xB3u;
+      }
     }
-    for (int j = nw * 4; j < len; ++j) l = (l ^ (uint32_t)buf[s0 + j]) * 0xB3u;
+    for (int j = nv * 16; j < len; ++j) {
+      const uint32_t b = buf[s0 + j];
+      l = ((l & M) ^ (b | (b << 16))) * 0xB3u;
+    }
   }
-  perm[c * 256 + threadIdx.x] = (uint8_t)(l & 0xffu);
+  const uint8_t p0 = (uint8_t)(l & 0xffu), p1 = (uint8_t)((l >> 16) & 0xffu);
+  uint8_t *pc = perm + c * 256;
+  pc[2 * t] = p0;
+  pc[2 * t + 1] = p1;
+  pc[2 * t + 128] = p0 ^ 0x80u;
+  pc[2 * t + 129] = p1 ^ 0x80u;
 }
 
 // Serial walk over the chunk permutations: the true low byte at each chunk
@@ -183,7 +202,7 @@ extern "C" int32_t mrpt_fnv1a64(const uint8_t *buf, int64_t nbytes, uint64_t *ou
   uint8_t *starts = perm + (size_t)nch * 256;
   unsigned long long *coff = reinterpret_cast<unsigned long long *>(
       (reinterpret_cast<uintptr_t>(starts + nch) + 15) & ~uintptr_t(15));
-  (count_launch(), k_fnv_perm<<<(unsigned)nch, 256, 0, s>>>(buf, nbytes, chunk, perm));
+  (count_launch(), k_fnv_perm<<<(unsigned)nch, kFnvThreads, 0, s>>>(buf, nbytes, chunk, perm));
   (count_launch(), k_fnv_starts<<<1, 256, 0, s>>>(perm, nch, starts));
   (count_launch(), k_fnv_offsets<<<(unsigned)ceil_div<int64_t>(nch, 128), 128, 0, s>>>(buf, nbytes, chunk, nch, starts,
                                                                       coff));

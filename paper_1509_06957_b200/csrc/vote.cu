@@ -965,6 +965,7 @@ __device__ __forceinline__ uint4 ld_quad_l2_256(const uint4 *p) {
 // the next window (padding past the end).  Windows must be taken in order.
 struct StreamWindows {
   int pre, len, total, before, next_w;
+  int pf;  // experiment: 1 prefetch the 1 KB region a quad opens, 2 the next one, 3 the next 2 KB
   __device__ __forceinline__ void begin(int len_, uint32_t lbase_minus, uint32_t *w_off_row) {
     const int lane = threadIdx.x & 31;
     len = len_;
@@ -998,6 +999,13 @@ struct StreamWindows {
     // shared/L1 carve-out, allocating them in L1 only throttles the loads
     if (e >= total) return padq;
     const uint4 *src = reinterpret_cast<const uint4 *>(wb) + (w_off_row[rank] + (uint32_t)e);
+    if (pf && (reinterpret_cast<uintptr_t>(src) & 1023u) == 0) {
+      const char *r = reinterpret_cast<const char *>(src) + (pf >= 2 ? 1024 : 0);
+      if (pf == 3)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], 2048;" ::"l"(r) : "memory");
+      else
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], 1024;" ::"l"(r) : "memory");
+    }
     if (CG) return ld_quad_l2_256(src);
     return __ldg(src);
   }
@@ -1061,6 +1069,7 @@ __global__ void __launch_bounds__(1024, 1) k_vote_stream(VoteArgs a, const uint4
     int32_t *qcand = a.cand + q * a.cap;
     // tile 0's windows start loading before the counters are cleared
     StreamWindows sw;
+    sw.pf = (a.dbg >> 2) & 3;
     sw.begin(dnxt - dcur, lbase + (uint32_t)dcur, woff);
     uint4 ring[P];
 #pragma unroll

@@ -135,6 +135,19 @@ def test_fnv_matches_oracle(rng, size):
     assert mrpt.fnv1a64(buf) == O.fnv1a64(buf.tobytes())
 
 
+@pytest.mark.parametrize("offset", [1, 3, 8])
+def test_fnv_unaligned_and_many_chunks(rng, offset):
+    """Device buffers not 16-byte aligned (staged byte-wise) and a size with
+    many chunks plus a ragged last one."""
+    import torch
+
+    from paper_1509_06957_b200.core import fnv1a64_device
+
+    buf = rng.integers(0, 256, size=40_000_013 + offset).astype(np.uint8)
+    t = torch.from_numpy(buf).cuda()[offset:]
+    assert fnv1a64_device(t) == O.fnv1a64(buf[offset:].tobytes())
+
+
 def test_fnv_golden_vectors():
     g = golden("fnv.npz")
     blob = g["blob"].tobytes()

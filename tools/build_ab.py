@@ -1,7 +1,9 @@
 """Build-time A/B in one process: grow_trees on a configuration twice per
 variant (the first warms), variants chosen by environment settings given as
 NAME=VAL[,NAME=VAL] arguments; also checks the variants build identical trees.
-usage: python tools/build_ab.py CONFIG SCALE "MRPT_PROJ_D64=0" "MRPT_PROJ_D64=1" ..."""
+usage: python tools/build_ab.py CONFIG SCALE "MRPT_PROJ_D64=0" "MRPT_PROJ_D64=1" ...
+(CACHED=1 in a spec: build from a Dataset whose checksum is already known,
+i.e. the build without the K6 checksum.)"""
 import os
 import sys
 import time
@@ -21,10 +23,15 @@ for spec in sys.argv[3:]:
         k, v = kv.split("=")
         os.environ[k] = v
     ts = []
+    src = Xd
+    if os.environ.get("CACHED") == "1":
+        from paper_1509_06957_b200.core import as_dataset
+        src = as_dataset(Xd)
+        src.checksum
     for _ in range(2):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        index = mrpt.grow_trees(Xd, p["n_trees"], p["depth"], p["sparsity"], seed=0)
+        index = mrpt.grow_trees(src, p["n_trees"], p["depth"], p["sparsity"], seed=0)
         torch.cuda.synchronize()
         ts.append(time.perf_counter() - t0)
     D = index.device_index()
