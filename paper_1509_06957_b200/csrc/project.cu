@@ -74,7 +74,7 @@ k_project_smem(const float *__restrict__ X, int64_t m, int d, int64_t ldx,
 template <int PPT>
 __global__ void __launch_bounds__(1024, 1)
 k_project_d64(const float *__restrict__ X, int64_t m, int d, int64_t ldx,
-              const int64_t *__restrict__ col_ptr, const int2 *__restrict__ ent, int ncols,
+              const int64_t *__restrict__ col_ptr, const int2 *__restrict__ ent, int64_t ent_cap, int ncols,
               float *__restrict__ out, int64_t ors, int64_t ocs, int stride) {
   extern __shared__ double xd[];
   constexpr int TP = 32 * PPT;
@@ -91,7 +91,8 @@ k_project_d64(const float *__restrict__ X, int64_t m, int d, int64_t ldx,
     __syncthreads();
     const double *xb = xd + lane * stride;
     for (int c = warp; c < ncols; c += nw) {
-      const int64_t s0 = __ldg(col_ptr + c), s1 = __ldg(col_ptr + c + 1);
+      const int64_t s0 = __ldg(col_ptr + c), s1r = __ldg(col_ptr + c + 1);
+      const int64_t s1 = s1r < ent_cap ? s1r : ent_cap;
       double acc[PPT];
 #pragma unroll
       for (int j = 0; j < PPT; ++j) acc[j] = 0.0;
@@ -113,8 +114,9 @@ k_project_d64(const float *__restrict__ X, int64_t m, int d, int64_t ldx,
 }
 
 // {row, value bits} pairs of a CSC column set (one 8-byte load per entry).
-__global__ void k_pack_entries(const int32_t *__restrict__ rows, const float *__restrict__ vals, int64_t nnz,
-                               int2 *ent) {
+__global__ void k_pack_entries(const int32_t *__restrict__ rows, const float *__restrict__ vals,
+                               const int64_t *__restrict__ nnz_ptr, int64_t cap, int2 *ent) {
+  const int64_t nnz = *nnz_ptr < cap ? *nnz_ptr : cap;  // cap: ncols * d (rows distinct per column)
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nnz; s += (int64_t)gridDim.x * blockDim.x)
     ent[s] = make_int2(rows[s], __float_as_int(vals[s]));
 }
@@ -263,20 +265,21 @@ extern "C" int32_t mrpt_project(const float *X, int64_t m, int32_t d, int64_t ld
     int ppt = (int)((212 * 1024) / ((int64_t)stride * 8 * 32));
     if (ppt > 6) ppt = 6;
     if ((!pe || atoi(pe) != 0) && ppt >= 1 && ncols >= 32) {
-      int64_t nnz = 0;
-      cudaMemcpyAsync(&nnz, col_ptr + ncols, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-      if (cudaStreamSynchronize(s) != cudaSuccess) return launch_status("mrpt_project");
+      // packed entries: sized by the bound d per column (no host read of
+      // col_ptr[ncols], so the call never synchronises)
+      const int64_t nnz_bound = (int64_t)ncols * d;
       int2 *ent = nullptr;
       keep_pool_warm();
-      if (cudaMallocAsync((void **)&ent, sizeof(int2) * (nnz > 0 ? nnz : 1), s) != cudaSuccess)
+      if (cudaMallocAsync((void **)&ent, sizeof(int2) * (size_t)nnz_bound, s) != cudaSuccess)
         return fail(MRPT_ECUDA, "mrpt_project: scratch allocation failed");
-      if (nnz > 0) {
-        const int64_t pb = ceil_div<int64_t>(nnz, 256);
-        (count_launch(), k_pack_entries<<<(unsigned)(pb < 4096 ? pb : 4096), 256, 0, s>>>(rows, vals, nnz, ent));
+      {
+        const int64_t pb = ceil_div<int64_t>(nnz_bound, 256);
+        (count_launch(), k_pack_entries<<<(unsigned)(pb < 4096 ? pb : 4096), 256, 0, s>>>(rows, vals,
+                                                                                          col_ptr + ncols, nnz_bound, ent));
       }
       const size_t smem = (size_t)32 * ppt * stride * 8;
-      void (*fn)(const float *, int64_t, int, int64_t, const int64_t *, const int2 *, int, float *, int64_t,
-                 int64_t, int) =
+      void (*fn)(const float *, int64_t, int, int64_t, const int64_t *, const int2 *, int64_t, int, float *,
+                 int64_t, int64_t, int) =
           ppt >= 6 ? k_project_d64<6>
                    : (ppt == 5 ? k_project_d64<5>
                                : (ppt == 4 ? k_project_d64<4>
@@ -284,8 +287,8 @@ extern "C" int32_t mrpt_project(const float *X, int64_t m, int32_t d, int64_t ld
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       const int64_t tiles = ceil_div<int64_t>(m, 32 * ppt);
       const int grid = (int)(tiles < (int64_t)num_sms() ? tiles : (int64_t)num_sms());
-      (count_launch(), fn<<<grid, 1024, smem, s>>>(X, m, d, ldx, col_ptr, ent, ncols, out, out_row_stride,
-                                                  out_col_stride, stride));
+      (count_launch(), fn<<<grid, 1024, smem, s>>>(X, m, d, ldx, col_ptr, ent, nnz_bound, ncols, out, out_row_stride,
+                                                out_col_stride, stride));
       cudaFreeAsync(ent, s);
       return launch_status("mrpt_project");
     }
