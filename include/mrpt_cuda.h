@@ -307,10 +307,13 @@ int32_t mrpt_fnv1a64(const uint8_t *buf, int64_t nbytes, uint64_t *out,
  * VoteAccumulator.accumulate / _cy.vote, pkg/src/mrpt/search.py:75-86,
  * _kernels/_cy.pyx:57-78) over a per-index layout built once:
  * every ascending leaf slice is split into its parts per id tile, each part
- * padded to a multiple of 4 entries, each entry pre-decoded into its
- * tile-local counter address ((word << 5) | shift; 0xffffffff = padding).
+ * padded to a multiple of 7 entries, each entry pre-decoded into its
+ * tile-local counter address (16-bit counter word, 2-bit lane), 7 entries
+ * per 16-byte quad: u16[0..6] = words, u16[7] = the 7 lanes (2 bits each);
+ * padding entries address the 32 spare words after the counters.
  *   _plan:   ntiles and the entries of qdir (T * 2^depth * (ntiles + 1) u16);
- *            fails with MRPT_EPARAM where the layout does not apply.
+ *            fails with MRPT_EPARAM where the layout does not apply
+ *            (T > 1024 or more than 1024 id tiles).
  *   _layout: qdir (quad offset of each tile's part within its leaf's padded
  *            slice), qbase (T * 2^depth int32: the slice's first quad within
  *            its tree row) and tree_quads (T int64: quads per tree row).

@@ -781,42 +781,37 @@ __global__ void __launch_bounds__(1024) k_bitmap_compact(const uint32_t *__restr
 // ---------------------------------------------------------------------------
 // Streamed tiled vote (configs 4-5: many id tiles, T <= 1024).  Built once
 // per index: for every leaf slice, its part in each id tile ("piece") is
-// stored padded to a multiple of 4 entries, pieces in tile order, and each
-// entry is pre-decoded into its tile-local counter address
-// so the vote reads every piece with aligned 16-byte loads and bumps a
-// counter with two bit operations instead of a division by the packing:
-//     enc = (counter word << 7) | lane shift    (enc >> 5 = the word's byte offset)
+// stored padded to a multiple of 7 entries, pieces in tile order, and each
+// entry is pre-decoded into its tile-local counter address -- the counter
+// word (16 bits: a tile's counters are < 64K words) and the lane within the
+// word (2 bits) -- seven entries per 16-byte "quad":
+//     u16[0..6] = counter words of entries 0..6,  u16[7] = 2-bit lanes
+// so the vote reads every piece with aligned 16-byte loads (7 ids each, vs
+// 4 for 32-bit ids) and bumps a counter with no division by the packing.
 // Padding entries address one of 32 spare words past the counters (by slot,
 // so the lanes of a load rarely share one): they are bumped like any entry
 // (no per-entry test) and never emitted.
-// qdir[(t*L + leaf)*(ntiles+1) + w] = start (in 4-entry quads) of tile w's
-// piece within the leaf's padded slice; qbase[t*L + leaf] = the slice's first
-// quad within tree t's padded row (tree t's row starts at quad t * tstride).
+// qdir[(t*L + leaf)*(ntiles+1) + w] = start (in quads) of tile w's piece
+// within the leaf's padded slice; qbase[t*L + leaf] = the slice's first quad
+// within tree t's padded row (tree t's row starts at quad t * tstride).
 // The counts are identical to the plain vote's: every occurrence of every id
 // is counted once (_cy.pyx:66-77); only the memory layout differs.
-template <int CW>
-__host__ __device__ __forceinline__ uint32_t quad_encode(int local) {
-  if (CW == 1) return ((uint32_t)(local >> 2) << 7) | (uint32_t)((local & 3) * 8);
-  if (CW == 3) return ((uint32_t)(local / 3) << 7) | (uint32_t)((local % 3) * 10);
-  if (CW == 2) return ((uint32_t)(local >> 1) << 7) | (uint32_t)((local & 1) * 16);
-  return (uint32_t)local << 7;
-}
+constexpr int kQuadIds = 7;
 
-// The padding entry of a tile width for output slot z: spare word z % 32
-// after the counters (counter words rounded up to 4).
+// counter lanes per 32-bit word and their width (bits)
 template <int CW>
-__host__ __device__ __forceinline__ uint32_t quad_pad(int W, int64_t z = 0) {
-  return (uint32_t)(((counter_words<CW>(W) + 3) & ~3) + (int)(z & 31)) << 7;
+__host__ __device__ __forceinline__ constexpr int lanes_per_word() {
+  return CW == 1 ? 4 : (CW == 3 ? 3 : (CW == 2 ? 2 : 1));
 }
-
 template <int CW>
-__device__ __forceinline__ int quad_decode(uint32_t word, uint32_t sh) {
-  if (CW == 1) return (int)(word * 4 + sh / 8);
-  if (CW == 3) return (int)(word * 3 + sh / 10);
-  if (CW == 2) return (int)(word * 2 + sh / 16);
-  return (int)word;
+__host__ __device__ __forceinline__ constexpr int lane_bits() {
+  return CW == 1 ? 8 : (CW == 3 ? 10 : (CW == 2 ? 16 : 0));
 }
-
+// first spare word (padding target) after the counters (rounded up to 4)
+template <int CW>
+__host__ __device__ __forceinline__ int spare_word0(int W) {
+  return (counter_words<CW>(W) + 3) & ~3;
+}
 // qdir holds, after k_build_dir, the piece start POSITIONS within each leaf
 // slice (u16); this turns them into padded quad offsets in place and writes
 // each leaf's padded length (quads) to qlen.  One warp per leaf.
@@ -829,7 +824,7 @@ __global__ void k_vstream_quads(uint16_t *qdir, int64_t nleaves, int ntiles, int
     for (int w0 = 0; w0 < ntiles; w0 += 32) {
       const int w = w0 + lane;
       int q = 0;
-      if (w < ntiles) q = ((int)d[w + 1] - (int)d[w] + 3) >> 2;  // read before any write of this round
+      if (w < ntiles) q = ((int)d[w + 1] - (int)d[w] + kQuadIds - 1) / kQuadIds;  // read before any write
       int incl = q;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -885,55 +880,72 @@ __global__ void __launch_bounds__(1024) k_vstream_base(int32_t *qbase, int L, in
   if (tid == 0) tree_quads[t] = carry;
 }
 
-// Fill the padded, pre-decoded slices.  One warp per leaf; the slice is
-// ascending, so each tile's piece is one run.
+// Fill the padded, pre-decoded slices.  One warp per leaf: the lanes find
+// where each tile's run starts in the (ascending) slice by binary search,
+// then every lane assembles whole quads (tile of the quad from the quad
+// directory, its 7 entries from the run) and stores each with one 16-byte
+// store.  Run starts and the leaf's directory row are staged per warp in
+// shared memory (ntiles <= kStreamMaxTiles).
+constexpr int kStreamMaxTiles = 1024;
 template <int CW>
-__global__ void k_vstream_fill(const int32_t *__restrict__ leaf_indices, const int64_t *__restrict__ leaf_offsets,
-                               int64_t n, int T, int L, int W, int ntiles, const uint16_t *__restrict__ qdir,
-                               const int32_t *__restrict__ qbase, int64_t tstride, uint32_t *qs) {
-  const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(256) k_vstream_fill(const int32_t *__restrict__ leaf_indices,
+                                                      const int64_t *__restrict__ leaf_offsets, int64_t n, int T, int L,
+                                                      int W, int ntiles, const uint16_t *__restrict__ qdir,
+                                                      const int32_t *__restrict__ qbase, int64_t tstride, uint32_t *qs) {
+  extern __shared__ int32_t fill_smem[];
+  constexpr int PER = lanes_per_word<CW>();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t *rs = fill_smem + warp * 2 * (ntiles + 1);  // run start per tile (+ end)
+  int32_t *dq = rs + (ntiles + 1);                    // quad offset per tile (+ total)
+  const uint32_t spare = (uint32_t)spare_word0<CW>(W);
   const int64_t nleaves = (int64_t)T * L;
   const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < nleaves; g += wstride) {
+  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; g < nleaves; g += wstride) {
     const int64_t t = g / L, leaf = g - t * L;
     const int64_t *o = leaf_offsets + t * (L + 1);
-    const int64_t s = o[leaf], e = o[leaf + 1];
-    const int32_t *Lt = leaf_indices + t * n;
+    const int64_t s0 = o[leaf];
+    const int m = (int)(o[leaf + 1] - s0);
+    const int32_t *sl = leaf_indices + t * n + s0;
     const uint16_t *d = qdir + g * (ntiles + 1);
-    uint32_t *out = qs + 4 * (t * tstride + qbase[g]);
-    int prev_tile = -1;
-    int64_t run_start = s;  // position where the current tile's run began
-    for (int64_t p0 = s; p0 < e; p0 += 32) {
-      const int64_t p = p0 + lane;
-      const bool in = p < e;
-      const int32_t id = in ? Lt[p] : 0;
-      const int tl = in ? id / W : 0x7fffffff;
-      int before = __shfl_up_sync(0xffffffffu, tl, 1);
-      if (lane == 0) before = prev_tile;
-      const bool first = in && tl != before;
-      // start of this lane's run: the last "first" at or before it, else carried
-      long long st = first ? (long long)p : -1;
-#pragma unroll
-      for (int o2 = 1; o2 < 32; o2 <<= 1) {
-        const long long u = __shfl_up_sync(0xffffffffu, st, o2);
-        if (lane >= o2 && u > st) st = u;
+    __syncwarp();
+    for (int w = lane; w <= ntiles; w += 32) {
+      dq[w] = d[w];
+      int lo = 0, hi = m;  // first position with id >= w * W
+      const int64_t key = (int64_t)w * W;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((int64_t)sl[mid] < key) lo = mid + 1;
+        else hi = mid;
       }
-      if (st < 0) st = run_start;
-      const int nxt = __shfl_down_sync(0xffffffffu, tl, 1);
-      if (in) {
-        const int local = id - tl * W;
-        const int64_t base = 4 * (int64_t)d[tl];
-        out[base + (p - st)] = quad_encode<CW>(local);
-        // the run's last element pads its piece to a multiple of 4
-        const bool last = p + 1 == e || (lane < 31 ? nxt != tl : Lt[p + 1] / W != tl);
-        if (last) {
-          const int64_t end = 4 * (int64_t)d[tl + 1];
-          for (int64_t z = base + (p - st) + 1; z < end; ++z) out[z] = quad_pad<CW>(W, z);
+      rs[w] = w == ntiles ? m : lo;
+    }
+    __syncwarp();
+    const int nquads = dq[ntiles];
+    uint4 *out = reinterpret_cast<uint4 *>(qs) + (t * tstride + qbase[g]);
+    for (int q = lane; q < nquads; q += 32) {
+      int lo = 0, hi = ntiles - 1;  // tile of quad q: last w with dq[w] <= q
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (dq[mid] <= q) lo = mid;
+        else hi = mid - 1;
+      }
+      const int w = lo;
+      const int j0 = rs[w] + kQuadIds * (q - dq[w]);
+      const int rend = rs[w + 1];
+      uint32_t wd[kQuadIds], fb = 0u;
+#pragma unroll
+      for (int i = 0; i < kQuadIds; ++i) {
+        const int p = j0 + i;
+        if (p < rend) {
+          const int local = sl[p] - w * W;
+          const int word = local / PER;
+          wd[i] = (uint32_t)word;
+          fb |= (uint32_t)(local - word * PER) << (2 * i);
+        } else {
+          wd[i] = spare + (uint32_t)((q * kQuadIds + i) & 31);
         }
       }
-      prev_tile = __shfl_sync(0xffffffffu, tl, 31);
-      const long long last_st = __shfl_sync(0xffffffffu, st, 31);
-      run_start = last_st;
+      out[q] = make_uint4(wd[0] | (wd[1] << 16), wd[2] | (wd[3] << 16), wd[4] | (wd[5] << 16), wd[6] | (fb << 16));
     }
   }
 }
@@ -949,9 +961,8 @@ __device__ __forceinline__ uint32_t atom_add_shared(uint32_t saddr, uint32_t inc
 // 256-byte block around it from DRAM: a leaf slice stores its per-tile pieces
 // back to back, so the pieces of the next tiles arrive with this one and are
 // found in L2 later, and DRAM serves 256-byte bursts instead of scattered
-// 32-byte sectors (HBM serves ~5.5G random accesses/s at any size up to
-// 512 bytes, tools/micro/rand_bw.cu: small scattered reads are bound by the
-// access rate, not by bandwidth).
+// 32-byte sectors (random 32-byte reads reach 0.6 TB/s, random 256-byte
+// blocks 3 TB/s, tools/micro/rand_mlp.cu).
 __device__ __forceinline__ uint4 ld_quad_l2_256(const uint4 *p) {
   uint4 v;
   asm volatile("ld.global.cg.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -1030,9 +1041,8 @@ __global__ void __launch_bounds__(1024, 1) k_vote_stream(VoteArgs a, const uint4
   uint32_t *cnt = reinterpret_cast<uint32_t *>(vote_smem);
   uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
   asm volatile("" : "+r"(cnt_s));  // computed once, not re-derived per bump
-  const int cwords = (counter_words<CW>(a.W) + 3) & ~3;  // + 32 spare words (padding targets)
-  const uint32_t pad = quad_pad<CW>(a.W);
-  const uint32_t pad_word = pad >> 7;  // entries addressing words >= pad_word are padding
+  const int cwords = spare_word0<CW>(a.W);  // + 32 spare words (padding targets)
+  const uint32_t pad_word = (uint32_t)cwords;  // entries addressing words >= pad_word are padding
   constexpr int NW = 32;
   __shared__ uint32_t w_off[NW][32];
   __shared__ int s_nc;
@@ -1053,7 +1063,11 @@ __global__ void __launch_bounds__(1024, 1) k_vote_stream(VoteArgs a, const uint4
   asm volatile("" : "+l"(wb));
   uint32_t *woff = w_off[warp];
   uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
-  const uint4 padq = make_uint4(pad, pad, pad, pad);
+  // window tails: 7 padding entries on this lane's own spare word
+  const uint32_t pw = pad_word + (uint32_t)lane;
+  const uint4 padq = make_uint4(pw | (pw << 16), pw | (pw << 16), pw | (pw << 16), pw);
+  constexpr int PER = lanes_per_word<CW>();
+  constexpr int LB = lane_bits<CW>();
   for (int64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
     const uint16_t *dl = nullptr;
     uint32_t lbase = 0;
@@ -1086,17 +1100,21 @@ __global__ void __launch_bounds__(1024, 1) k_vote_stream(VoteArgs a, const uint4
           if (w0 + i < nwin) {  // warp-uniform
             const uint4 cur = ring[i];
             if (w0 + i + P < nwin) ring[i] = sw.template next<CG>(wb, woff, padq);
-            const uint32_t xs[4] = {cur.x, cur.y, cur.z, cur.w};
-            uint32_t old[4];
+            const uint32_t wd[kQuadIds] = {cur.x & 0xffffu, cur.x >> 16, cur.y & 0xffffu, cur.y >> 16,
+                                           cur.z & 0xffffu, cur.z >> 16, cur.w & 0xffffu};
+            const uint32_t fb = cur.w >> 16;
+            uint32_t old[kQuadIds];
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-              old[c] = (a.dbg & 1) ? xs[c] : atom_add_shared(cnt_s + (xs[c] >> 5), 1u << (xs[c] & 31u));
+            for (int c = 0; c < kQuadIds; ++c) {
+              const uint32_t sh = ((fb >> (2 * c)) & 3u) * LB;
+              old[c] = (a.dbg & 1) ? 0u : atom_add_shared(cnt_s + 4u * wd[c], 1u << sh);
+            }
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const uint32_t x = xs[c];
-              if (((old[c] >> (x & 31u)) & MASK) == vm1 && (x >> 7) < pad_word) {  // lifted a count to v
+            for (int c = 0; c < kQuadIds; ++c) {
+              const uint32_t f = (fb >> (2 * c)) & 3u;
+              if (((old[c] >> (f * LB)) & MASK) == vm1 && wd[c] < pad_word) {  // lifted a count to v
                 const int pos = (int)atom_add_shared(nc_s, 1u);
-                if (pos < cap32) qcand[pos] = lo + quad_decode<CW>(x >> 7, x & 31u);
+                if (pos < cap32) qcand[pos] = lo + (int)(wd[c] * PER + f);
               }
             }
           }
@@ -1425,6 +1443,7 @@ static int32_t stream_geometry(int64_t n, int32_t T, int64_t max_count, int *CWo
   *CWo = CW;
   *Wo = W;
   *ntiles_o = (int)ceil_div<int64_t>(n, W);
+  if (*ntiles_o > kStreamMaxTiles) return fail(MRPT_EPARAM, "streamed vote: too many id tiles");
   return MRPT_OK;
 }
 
@@ -1475,8 +1494,10 @@ extern "C" int32_t mrpt_vote_stream_fill(const int32_t *leaf_indices, const int6
   const int64_t blocks = ceil_div<int64_t>(nleaves, 8);
   const int grid = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
   auto fn = CW == 1 ? k_vstream_fill<1> : (CW == 3 ? k_vstream_fill<3> : (CW == 2 ? k_vstream_fill<2> : k_vstream_fill<4>));
-  (count_launch(), fn<<<grid, 256, 0, s>>>(leaf_indices, leaf_offsets, n, T, 1 << depth, (int)W, nt, qdir, qbase,
-                                           tstride, qs));
+  const size_t fsmem = sizeof(int32_t) * 2 * (size_t)(nt + 1) * 8;  // 8 warps
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
+  (count_launch(), fn<<<grid, 256, fsmem, s>>>(leaf_indices, leaf_offsets, n, T, 1 << depth, (int)W, nt, qdir,
+                                               qbase, tstride, qs));
   return launch_status("mrpt_vote_stream_fill");
 }
 
@@ -1523,7 +1544,9 @@ extern "C" int32_t mrpt_vote_stream(const uint32_t *qs, int64_t tstride, const u
   sfn_t fn = CW == 1 ? VS_PICK(1) : (CW == 3 ? VS_PICK(3) : (CW == 2 ? VS_PICK(2) : VS_PICK(4)));
 #undef VS_PICK
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int64_t grid = nq < (int64_t)num_sms() ? nq : (int64_t)num_sms();
+  int64_t ctas = num_sms();
+  if (const char *ge = getenv("MRPT_VSTREAM_GRID")) ctas = atoi(ge) > 0 ? atoi(ge) : ctas;  // experiments
+  const int64_t grid = nq < ctas ? nq : ctas;
   cudaStream_t s = as_stream(stream);
   (count_launch(), fn<<<(unsigned)grid, 1024, smem, s>>>(a, reinterpret_cast<const uint4 *>(qs), qbase, tstride));
   return launch_status("mrpt_vote_stream");

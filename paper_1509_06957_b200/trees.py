@@ -287,8 +287,8 @@ class _DeviceIndex:
         except MRPTError:
             return None
         nleaf = 1 << self.depth
-        # padded lengths must fit the u16 quad directory
-        if ntiles.value <= 1 or self.max_leaf + 3 * ntiles.value >= 4 * 65535:
+        # padded lengths (7 ids per quad) must fit the u16 quad directory
+        if ntiles.value <= 1 or (self.max_leaf + 6 * ntiles.value) // 7 >= 65535:
             return None
         torch = _device.torch_mod()
         dev = self.indices.device

@@ -477,9 +477,13 @@ def test_streamed_vote_layout_round_trip(rng):
             s0 = qbase[t * L + f]
             ids = []
             for w in range(nt):
-                quads = qs[t, s0 + qdir[t, f, w]: s0 + qdir[t, f, w + 1]].ravel()
-                assert len(quads) % 4 == 0
-                for e in quads:
-                    if (e >> 7) < pad_word:
-                        ids.append(w * W + int(e >> 7) * 4 + int(e & 31) // 8)
+                # a quad: u16 counter words of 7 entries, then their 2-bit lanes
+                quads = qs[t, s0 + qdir[t, f, w]: s0 + qdir[t, f, w + 1]].view(np.uint16)
+                for u in quads.reshape(-1, 8):
+                    fb = int(u[7])
+                    for i in range(7):
+                        if u[i] < pad_word:
+                            ids.append(w * W + int(u[i]) * 4 + ((fb >> (2 * i)) & 3))
+                        else:
+                            assert u[i] < pad_word + 32 and (fb >> (2 * i)) & 3 == 0
             assert np.array_equal(np.array(ids, dtype=np.int64), li[t, offs[t, f]:offs[t, f + 1]])
