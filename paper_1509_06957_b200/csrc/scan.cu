@@ -868,8 +868,15 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_filter_h(TopkArgs a, d
         cidv[u] = __shfl_sync(0xffffffffu, lane_ids[u], it);
         row[u] = a.Xh + (int64_t)(cidv[u] < 0 ? 0 : cidv[u]) * a.ldh;
       }
-      const float myr = (lane < kFU && cidv[lane < kFU ? lane : 0] >= 0)
-                            ? __ldg(a.radius + cidv[lane < kFU ? lane : 0]) : 0.f;
+      // after the transposed reduction below, lanes 8u .. 8u+7 hold candidate
+      // u's value; lane 8u represents it
+      static_assert(kFU == 4, "transposed reduction is written for 4 candidates");
+      const int ci = (lane >> 3) & 3;
+      int32_t myid = cidv[0];
+#pragma unroll
+      for (int u = 1; u < kFU; ++u) myid = ci == u ? cidv[u] : myid;
+      const bool rep = (lane & 7) == 0;
+      const float myr = (rep && myid >= 0) ? __ldg(a.radius + myid) : 0.f;
       float acc[kFU];
 #pragma unroll
       for (int u = 0; u < kFU; ++u) acc[u] = 0.f;
@@ -902,20 +909,19 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_filter_h(TopkArgs a, d
           }
         }
       }
-#pragma unroll
-      for (int u = 0; u < kFU; ++u) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
-      }
-      float mine = acc[0];
-      int32_t myid = cidv[0];
-#pragma unroll
-      for (int u = 1; u < kFU; ++u)
-        if (lane == u) {
-          mine = acc[u];
-          myid = cidv[u];
-        }
-      const bool take = lane < kFU && myid >= 0 && admit(mine, myr, su, onepe);
+      // transposed warp reduction of the 4 sums (6 shuffles instead of 20):
+      // exchange halves across lane bit 4, then bit 3, then sum the rest.
+      // Any summation order is inside the eps bound (2 (ldh+16) u).
+      const bool b16 = lane & 16, b8 = lane & 8;
+      float k0 = b16 ? acc[2] : acc[0], k1 = b16 ? acc[3] : acc[1];
+      const float s0 = b16 ? acc[0] : acc[2], s1 = b16 ? acc[1] : acc[3];
+      k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+      k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+      float mine = (b8 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, b8 ? k0 : k1, 8);
+      mine += __shfl_xor_sync(0xffffffffu, mine, 4);
+      mine += __shfl_xor_sync(0xffffffffu, mine, 2);
+      mine += __shfl_xor_sync(0xffffffffu, mine, 1);
+      const bool take = rep && myid >= 0 && admit(mine, myr, su, onepe);
       const unsigned tm = __ballot_sync(0xffffffffu, take);
       if (take) {
         const int slot = cnt + __popc(tm & lanemask_lt());
