@@ -731,6 +731,29 @@ __global__ void k_quantize_fp16(const float *__restrict__ X, int64_t n, int d, i
   }
 }
 
+// Packed float32 pairs in one 64-bit register (sm_100 FADD2 / FFMA2).
+__device__ __forceinline__ unsigned long long f32x2_pack(float x, float y) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f32x2_sub(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f32x2_fma(unsigned long long a, unsigned long long b,
+                                                        unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ float f32x2_sum(unsigned long long a) {
+  float x, y;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(a));
+  return x + y;
+}
+
 // bounds of the reference distance E from the fp16-row filter value A and the
 // row radius r:  sqrt(E) in [sqrt(D) - r, sqrt(D) + r],  D = ||x~ - q||^2 with
 // |A - D| <= eps*D + eta (float32 arithmetic), E within 1e-12 relative of the
@@ -877,38 +900,37 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_filter_h(TopkArgs a, d
       for (int u = 1; u < kFU; ++u) myid = ci == u ? cidv[u] : myid;
       const bool rep = (lane & 7) == 0;
       const float myr = (rep && myid >= 0) ? __ldg(a.radius + myid) : 0.f;
-      float acc[kFU];
+      // packed float32 pairs (FADD2 / FFMA2: two lanes of arithmetic per
+      // instruction); even and odd coordinates accumulate separately
+      unsigned long long acc2[kFU];
 #pragma unroll
-      for (int u = 0; u < kFU; ++u) acc[u] = 0.f;
+      for (int u = 0; u < kFU; ++u) acc2[u] = 0ull;
 #pragma unroll
       for (int j = 0; j < kMaxJ; ++j) {
         const int c = j * 256 + 8 * lane;
         if (j < nj && c < dpad) {
           const float4 q0 = *reinterpret_cast<const float4 *>(qs + c);
           const float4 q1 = *reinterpret_cast<const float4 *>(qs + c + 4);
+          const unsigned long long qp[4] = {f32x2_pack(q0.x, q0.y), f32x2_pack(q0.z, q0.w),
+                                            f32x2_pack(q1.x, q1.y), f32x2_pack(q1.z, q1.w)};
           uint4 raw[kFU];
 #pragma unroll
           for (int u = 0; u < kFU; ++u) raw[u] = __ldg(reinterpret_cast<const uint4 *>(row[u] + c));
 #pragma unroll
           for (int u = 0; u < kFU; ++u) {
             const __half2 *h2 = reinterpret_cast<const __half2 *>(&raw[u]);
-            float2 f;
-            float t;
-            f = __half22float2(h2[0]);
-            t = f.x - q0.x; acc[u] = __fmaf_rn(t, t, acc[u]);
-            t = f.y - q0.y; acc[u] = __fmaf_rn(t, t, acc[u]);
-            f = __half22float2(h2[1]);
-            t = f.x - q0.z; acc[u] = __fmaf_rn(t, t, acc[u]);
-            t = f.y - q0.w; acc[u] = __fmaf_rn(t, t, acc[u]);
-            f = __half22float2(h2[2]);
-            t = f.x - q1.x; acc[u] = __fmaf_rn(t, t, acc[u]);
-            t = f.y - q1.y; acc[u] = __fmaf_rn(t, t, acc[u]);
-            f = __half22float2(h2[3]);
-            t = f.x - q1.z; acc[u] = __fmaf_rn(t, t, acc[u]);
-            t = f.y - q1.w; acc[u] = __fmaf_rn(t, t, acc[u]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __half22float2(h2[e]);
+              const unsigned long long t = f32x2_sub(f32x2_pack(f.x, f.y), qp[e]);
+              acc2[u] = f32x2_fma(t, t, acc2[u]);
+            }
           }
         }
       }
+      float acc[kFU];
+#pragma unroll
+      for (int u = 0; u < kFU; ++u) acc[u] = f32x2_sum(acc2[u]);
       // transposed warp reduction of the 4 sums (6 shuffles instead of 20):
       // exchange halves across lane bit 4, then bit 3, then sum the rest.
       // Any summation order is inside the eps bound (2 (ldh+16) u).
