@@ -497,17 +497,19 @@ __global__ void __launch_bounds__(kNT) k_big_scatter4(LevelArgs a) {
     int32_t *oout = a.order_out + (int64_t)g->t * a.n;
     const int64_t pa = p0 - (int64_t)(((uintptr_t)(kb + p0) >> 2) & 3);  // first group's position
     int64_t base_left = a.chunk_off[c];
-    for (int64_t r0 = pa; r0 < p1; r0 += (int64_t)SR * kNT * 4) {
-      uint4 kk[SR];
-      int4 id[SR];
-      int fl[SR], cl[SR], incl[SR];
+    // software pipelined: the next round's keys and ids are loaded before
+    // this round's ranks are published and its ids stored
+    uint4 kk[SR];
+    int4 id[SR];
 #pragma unroll
-      for (int j = 0; j < SR; ++j) {
-        const int64_t q = r0 + ((int64_t)j * kNT + threadIdx.x) * 4;  // group start position
-        const bool any = q < p1;
-        kk[j] = any ? __ldg(reinterpret_cast<const uint4 *>(kb + q)) : make_uint4(0u, 0u, 0u, 0u);
-        id[j] = any ? __ldg(reinterpret_cast<const int4 *>(oin + q)) : make_int4(0, 0, 0, 0);
-      }
+    for (int j = 0; j < SR; ++j) {
+      const int64_t q = pa + ((int64_t)j * kNT + threadIdx.x) * 4;  // group start position
+      const bool any = q < p1;
+      kk[j] = any ? __ldg(reinterpret_cast<const uint4 *>(kb + q)) : make_uint4(0u, 0u, 0u, 0u);
+      id[j] = any ? __ldg(reinterpret_cast<const int4 *>(oin + q)) : make_int4(0, 0, 0, 0);
+    }
+    for (int64_t r0 = pa; r0 < p1; r0 += (int64_t)SR * kNT * 4) {
+      int fl[SR], cl[SR], incl[SR];
 #pragma unroll
       for (int j = 0; j < SR; ++j) {
         const int64_t q = r0 + ((int64_t)j * kNT + threadIdx.x) * 4;
@@ -527,6 +529,17 @@ __global__ void __launch_bounds__(kNT) k_big_scatter4(LevelArgs a) {
         incl[j] = x;
         if (lane == 31) wcnt[j][warp] = x;
       }
+      int4 idc[SR];
+#pragma unroll
+      for (int j = 0; j < SR; ++j) idc[j] = id[j];
+      const int64_t rn = r0 + (int64_t)SR * kNT * 4;
+#pragma unroll
+      for (int j = 0; j < SR; ++j) {
+        const int64_t q = rn + ((int64_t)j * kNT + threadIdx.x) * 4;
+        const bool any = q < p1;
+        kk[j] = any ? __ldg(reinterpret_cast<const uint4 *>(kb + q)) : make_uint4(0u, 0u, 0u, 0u);
+        id[j] = any ? __ldg(reinterpret_cast<const int4 *>(oin + q)) : make_int4(0, 0, 0, 0);
+      }
       __syncthreads();
       int tot = 0;
 #pragma unroll
@@ -540,7 +553,7 @@ __global__ void __launch_bounds__(kNT) k_big_scatter4(LevelArgs a) {
         }
         const int64_t q = r0 + ((int64_t)j * kNT + threadIdx.x) * 4;
         int64_t lrank = base_left + bj + incl[j] - cl[j];
-        const int iv[4] = {id[j].x, id[j].y, id[j].z, id[j].w};
+        const int iv[4] = {idc[j].x, idc[j].y, idc[j].z, idc[j].w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int64_t p = q + e;
