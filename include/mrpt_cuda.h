@@ -337,6 +337,36 @@ int32_t mrpt_vote_stream(const uint32_t *qs, int64_t tstride, const uint16_t *qd
                          int64_t max_count, const int32_t *leaves, int64_t nq, int32_t v,
                          int32_t *cand, int64_t cap, int32_t *ncand, void *stream);
 
+/* Paired streamed vote (same counts and candidate sets as mrpt_vote_stream;
+ * replaces the same reference code, _cy.pyx:57-78 via search.py:130-172).
+ * The id tiles are taken two at a time: per leaf slice, super-piece j holds
+ * 32-byte pairs {quad k of tile 2j's piece, quad k of tile 2j+1's piece},
+ * so one load brings a quad of both tiles; the kernel bumps the first now
+ * and parks the second in tensor memory for the next tile.
+ *   _plan:   ntiles, pos_entries = T*2^depth*(ntiles+1) (u16 scratch of
+ *            _layout and _fill), dir_entries = T*2^depth*(ceil(ntiles/2)+1).
+ *   _layout: pos (scratch), pdir (pair offset of each super-piece within its
+ *            slice), pbase (T*2^depth int32: slice's first pair within its
+ *            tree row), tree_pairs (T int64: pairs per tree row).
+ *   _fill:   ps (T * pstride pairs of 8 uint32), pstride >= max tree_pairs,
+ *            64 * pstride < 2^31.
+ *   mrpt_vote_pair: candidate lists like mrpt_vote_stream. */
+int32_t mrpt_vote_pair_plan(int64_t n, int32_t T, int32_t depth, int64_t max_count,
+                            int32_t *ntiles /* host */, int64_t *pos_entries /* host */,
+                            int64_t *dir_entries /* host */);
+int32_t mrpt_vote_pair_layout(const int32_t *leaf_indices, const int64_t *leaf_offsets,
+                              int64_t n, int32_t T, int32_t depth, int64_t max_count,
+                              uint16_t *pos, uint16_t *pdir, int32_t *pbase, int64_t *tree_pairs,
+                              void *stream);
+int32_t mrpt_vote_pair_fill(const int32_t *leaf_indices, const int64_t *leaf_offsets,
+                            int64_t n, int32_t T, int32_t depth, int64_t max_count,
+                            const uint16_t *pos, const uint16_t *pdir, const int32_t *pbase,
+                            int64_t pstride, uint32_t *ps, void *stream);
+int32_t mrpt_vote_pair(const uint32_t *ps, int64_t pstride, const uint16_t *pdir,
+                       const int32_t *pbase, int64_t n, int32_t T, int32_t depth,
+                       int64_t max_count, const int32_t *leaves, int64_t nq, int32_t v,
+                       int32_t *cand, int64_t cap, int32_t *ncand, void *stream);
+
 /* Query ordering for a batch (no reference counterpart: the reference
  * answers one query per call, search.py:175-184).  order (nq int32) lists
  * the queries grouped by their leaf in tree 0 (leaves: (nq, T) int32 from

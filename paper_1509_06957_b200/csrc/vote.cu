@@ -1139,6 +1139,305 @@ __global__ void __launch_bounds__(1024, 1) k_vote_stream(VoteArgs a, const uint4
     __syncthreads();
   }
 }
+
+// ------------------------------------------------------ paired streamed vote --
+// Pair layout: the id tiles are taken two at a time ("super-tile" j = tiles
+// 2j and 2j+1).  Per leaf slice, super-piece j holds max(qa, qb) 32-byte
+// PAIRS, pair k = {quad k of tile 2j's piece, quad k of tile 2j+1's piece}
+// (the shorter side padded with padding quads), so one 32-byte load brings a
+// quad of both tiles and a query's slices are read with half as many
+// (twice as long) requests as with one piece per tile.
+// pdir[(t*L + leaf)*(nsup+1) + j] = first pair of super-piece j within the
+// slice; pbase[t*L + leaf] = the slice's first pair within tree t's row
+// (tree t's row starts at pair t * pstride).
+
+// Per leaf: super-piece lengths from the per-tile run starts (k_build_dir),
+// exclusive scan -> pdir, total -> plen.  One warp per leaf.
+__global__ void k_vpair_dir(const uint16_t *__restrict__ pos, uint16_t *pdir, int64_t nleaves, int ntiles,
+                            int nsup, int32_t *plen) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < nleaves; g += wstride) {
+    const uint16_t *p = pos + g * (ntiles + 1);
+    uint16_t *d = pdir + g * (nsup + 1);
+    int carry = 0;
+    for (int j0 = 0; j0 < nsup; j0 += 32) {
+      const int j = j0 + lane;
+      int len = 0;
+      if (j < nsup) {
+        const int qa = ((int)p[2 * j + 1] - (int)p[2 * j] + kQuadIds - 1) / kQuadIds;
+        const int qb = 2 * j + 1 < ntiles ? ((int)p[2 * j + 2] - (int)p[2 * j + 1] + kQuadIds - 1) / kQuadIds : 0;
+        len = qa > qb ? qa : qb;
+      }
+      int incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      if (j < nsup) d[j] = (uint16_t)(carry + incl - len);
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) {
+      d[nsup] = (uint16_t)carry;
+      plen[g] = carry;
+    }
+  }
+}
+
+// quad k of tile w's piece of a slice: 7 pre-decoded entries (padding past
+// the run end addresses spare words by position)
+template <int CW>
+__device__ __forceinline__ uint4 vpair_quad(const int32_t *sl, const int32_t *rs, int w, int ntiles, int k, int W,
+                                            uint32_t spare) {
+  constexpr int PER = lanes_per_word<CW>();
+  uint32_t wd[kQuadIds], fb = 0u;
+  const int j0 = w < ntiles ? rs[w] + kQuadIds * k : 0;
+  const int rend = w < ntiles ? rs[w + 1] : 0;
+#pragma unroll
+  for (int i = 0; i < kQuadIds; ++i) {
+    const int p = j0 + i;
+    if (p < rend) {
+      const int local = sl[p] - w * W;
+      const int word = local / PER;
+      wd[i] = (uint32_t)word;
+      fb |= (uint32_t)(local - word * PER) << (2 * i);
+    } else {
+      wd[i] = spare + (uint32_t)((k * kQuadIds + i) & 31);
+    }
+  }
+  return make_uint4(wd[0] | (wd[1] << 16), wd[2] | (wd[3] << 16), wd[4] | (wd[5] << 16), wd[6] | (fb << 16));
+}
+
+// Fill the pair layout.  One warp per leaf; run starts and the super-piece
+// directory row staged per warp in shared memory.
+template <int CW>
+__global__ void __launch_bounds__(256) k_vpair_fill(const int32_t *__restrict__ leaf_indices,
+                                                    const int64_t *__restrict__ leaf_offsets, int64_t n, int T, int L,
+                                                    int W, int ntiles, int nsup, const uint16_t *__restrict__ pos,
+                                                    const uint16_t *__restrict__ pdir,
+                                                    const int32_t *__restrict__ pbase, int64_t pstride, uint4 *out) {
+  extern __shared__ int32_t fill_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t *rs = fill_smem + warp * (ntiles + 1 + nsup + 1);  // run start per tile (+ end)
+  int32_t *dp = rs + (ntiles + 1);                           // pair offset per super-tile (+ total)
+  const uint32_t spare = (uint32_t)spare_word0<CW>(W);
+  const int64_t nleaves = (int64_t)T * L;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; g < nleaves; g += wstride) {
+    const int64_t t = g / L, leaf = g - t * L;
+    const int32_t *sl = leaf_indices + t * n + leaf_offsets[t * (L + 1) + leaf];
+    __syncwarp();
+    for (int w = lane; w <= ntiles; w += 32) rs[w] = pos[g * (ntiles + 1) + w];
+    for (int j = lane; j <= nsup; j += 32) dp[j] = pdir[g * (nsup + 1) + j];
+    __syncwarp();
+    const int npairs = dp[nsup];
+    uint4 *o = out + 2 * (t * pstride + pbase[g]);
+    for (int pp = lane; pp < npairs; pp += 32) {
+      int lo = 0, hi = nsup - 1;  // super-piece of pair pp: last j with dp[j] <= pp
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (dp[mid] <= pp) lo = mid;
+        else hi = mid - 1;
+      }
+      const int j = lo, k = pp - dp[j];
+      o[2 * pp] = vpair_quad<CW>(sl, rs, 2 * j, ntiles, k, W, spare);
+      o[2 * pp + 1] = vpair_quad<CW>(sl, rs, 2 * j + 1, ntiles, k, W, spare);
+    }
+  }
+}
+
+__device__ __forceinline__ void ld_pair_l2_256(const uint4 *p, uint4 &a, uint4 &b) {
+  asm volatile("ld.global.cg.L2::256B.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
+
+// Bump the 7 counters of one quad; the increment that lifts a count to v
+// appends the id (_cy.pyx:75-77).
+template <int CW>
+__device__ __forceinline__ void pair_bump(uint4 cur, uint32_t cnt_s, uint32_t nc_s, uint32_t pad_word, uint32_t vm1,
+                                          int32_t lo, int32_t *qcand, int cap32) {
+  constexpr uint32_t MASK = CW == 1 ? 0xffu : (CW == 3 ? 0x3ffu : (CW == 2 ? 0xffffu : 0xffffffffu));
+  constexpr int PER = lanes_per_word<CW>();
+  constexpr int LB = lane_bits<CW>();
+  const uint32_t wd[kQuadIds] = {cur.x & 0xffffu, cur.x >> 16, cur.y & 0xffffu, cur.y >> 16,
+                                 cur.z & 0xffffu, cur.z >> 16, cur.w & 0xffffu};
+  const uint32_t fb = cur.w >> 16;
+  uint32_t old[kQuadIds];
+#pragma unroll
+  for (int c = 0; c < kQuadIds; ++c) old[c] = atom_add_shared(cnt_s + 4u * wd[c], 1u << (((fb >> (2 * c)) & 3u) * LB));
+#pragma unroll
+  for (int c = 0; c < kQuadIds; ++c) {
+    const uint32_t f = (fb >> (2 * c)) & 3u;
+    if (((old[c] >> (f * LB)) & MASK) == vm1 && wd[c] < pad_word) {  // lifted a count to v
+      const int pos = (int)atom_add_shared(nc_s, 1u);
+      if (pos < cap32) qcand[pos] = lo + (int)(wd[c] * PER + f);
+    }
+  }
+}
+
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, uint4 v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint4 tmem_ld4(uint32_t taddr) {
+  uint4 v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(taddr)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return v;
+}
+
+constexpr int kPairSlots = 16;  // stashed windows per warp (4 TMEM columns each; 8 warps share a lane quarter)
+
+// The paired streamed vote: one CTA (1024 threads, one per SM) per query at
+// a time, warp w owning trees [w*T/32, (w+1)*T/32) (one per lane).  Per
+// super-tile the warp flattens its trees' super-pieces into 32-pair windows
+// (one pair per lane, one 32-byte load, loaded one window ahead of the
+// bumps).  Phase A bumps each pair's first quad into tile 2j's counters and
+// parks the second quad in tensor memory (the SM's 256 KB of TMEM, unused
+// otherwise: warp w's lanes own columns [64*(w/4), +64) of lane quarter w%4,
+// 16 windows of 4 columns); after the tile barrier and clearing, phase B
+// bumps the parked quads into tile 2j+1's counters.  Windows past the 16th
+// re-read their pair in phase B.  The counts are those of k_vote_stream.
+template <int CW>
+__global__ void __launch_bounds__(1024, 1) k_vote_pair(VoteArgs a, const uint4 *__restrict__ ps,
+                                                       const int32_t *__restrict__ pbase, int64_t pstride) {
+  extern __shared__ uint4 vote_smem[];
+  uint32_t *cnt = reinterpret_cast<uint32_t *>(vote_smem);
+  uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
+  asm volatile("" : "+r"(cnt_s));
+  const int cwords = spare_word0<CW>(a.W);
+  const uint32_t pad_word = (uint32_t)cwords;
+  constexpr int NW = 32;
+  __shared__ uint32_t w_off[NW][32];
+  __shared__ int s_nc;
+  __shared__ uint32_t s_tmem;
+  const uint32_t vm1 = (uint32_t)(a.v - 1);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t nc_s = (uint32_t)__cvta_generic_to_shared(&s_nc);
+  asm volatile("" : "+r"(nc_s));
+  const int cap32 = a.cap < 0x7fffffff ? (int)a.cap : 0x7fffffff;
+  const int nsup = (a.ntiles + 1) >> 1;
+  const int64_t dstride = nsup + 1;
+  const int t_lo = (int)(((int64_t)warp * a.T) / NW);
+  const int t_hi = (int)(((int64_t)(warp + 1) * a.T) / NW);
+  const int t = t_lo + lane;
+  const bool has = t < t_hi;
+  // pairs addressed as uint4 index 2*p from the warp's first tree row
+  unsigned long long wb = reinterpret_cast<unsigned long long>(ps + 2 * (int64_t)t_lo * pstride);
+  asm volatile("" : "+l"(wb));
+  uint32_t *woff = w_off[warp];
+  uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
+  const uint32_t pw = pad_word + (uint32_t)lane;
+  const uint4 padq = make_uint4(pw | (pw << 16), pw | (pw << 16), pw | (pw << 16), pw);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_tmem)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tslot = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+  for (int64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
+    const uint16_t *dl = nullptr;
+    uint32_t lbase = 0;
+    int dcur = 0, dnxt = 0, dnn = 0;
+    if (has) {
+      const int64_t g = (int64_t)t * a.L + a.leaves[q * a.T + t];
+      dl = a.dir + g * dstride;
+      lbase = (uint32_t)((int64_t)lane * pstride + pbase[g]);
+      dcur = dl[0];
+      dnxt = dl[1];
+      dnn = nsup >= 2 ? (int)__ldg(dl + 2) : 0;
+    }
+    int32_t *qcand = a.cand + q * a.cap;
+    StreamWindows sw;
+    sw.pf = 0;
+    sw.begin(dnxt - dcur, lbase + (uint32_t)dcur, woff);
+    // next pair of the flattened window sequence: its index (uint4 units / 2)
+    // or ~0 past the end
+    auto next_pair = [&](uint4 &A, uint4 &B) {
+      const int w0 = 32 * sw.next_w++;
+      const int rel = sw.pre - w0;
+      const bool inwin = sw.len > 0 && (unsigned)rel < 32u;
+      const unsigned starts = __reduce_or_sync(0xffffffffu, inwin ? (1u << rel) : 0u);
+      const int rank = sw.before + __popc(starts & (0xffffffffu >> (31 - lane))) - 1;
+      sw.before += __popc(starts);
+      const int e = w0 + lane;
+      if (e >= sw.total) {
+        A = padq;
+        B = padq;
+      } else {
+        ld_pair_l2_256(reinterpret_cast<const uint4 *>(wb) + 2 * (size_t)(woff[rank] + (uint32_t)e), A, B);
+      }
+    };
+    uint4 rA, rB;
+    if (sw.windows() > 0) next_pair(rA, rB);
+    for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (tid == 0) s_nc = 0;
+    __syncthreads();
+    for (int j = 0; j < nsup; ++j) {
+      const bool hasB = 2 * j + 1 < a.ntiles;
+      const int32_t loA = 2 * j * a.W, loB = loA + a.W;
+      const int nwin = sw.windows();
+      // phase A: tile 2j
+      for (int i = 0; i < nwin; ++i) {
+        const uint4 cA = rA, cB = rB;
+        if (i + 1 < nwin) next_pair(rA, rB);
+        if (hasB && i < kPairSlots) tmem_st4(tslot + 4u * (uint32_t)i, cB);
+        pair_bump<CW>(cA, cnt_s, nc_s, pad_word, vm1, loA, qcand, cap32);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      __syncthreads();
+      for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+      __syncthreads();
+      // phase B: tile 2j+1 from the parked quads (windows past the parked
+      // ones re-read from the stream)
+      if (hasB) {
+        const int nst = nwin < kPairSlots ? nwin : kPairSlots;
+        for (int i = 0; i < nst; ++i) pair_bump<CW>(tmem_ld4(tslot + 4u * (uint32_t)i), cnt_s, nc_s, pad_word, vm1, loB, qcand, cap32);
+        if (nwin > kPairSlots) {
+          sw.begin(dnxt - dcur, lbase + (uint32_t)dcur, woff);  // same super-tile again
+          for (int i = 0; i < nwin; ++i) {
+            uint4 xA, xB;
+            next_pair(xA, xB);
+            if (i >= kPairSlots) pair_bump<CW>(xB, cnt_s, nc_s, pad_word, vm1, loB, qcand, cap32);
+          }
+        }
+      }
+      // the next super-tile's first window starts loading before the barrier
+      if (j + 1 < nsup) {
+        dcur = dnxt;
+        dnxt = dnn;
+        dnn = (has && j + 3 <= nsup) ? (int)__ldg(dl + j + 3) : 0;
+        sw.begin(dnxt - dcur, lbase + (uint32_t)dcur, woff);
+        if (sw.windows() > 0) next_pair(rA, rB);
+      }
+      if (hasB) {
+        __syncthreads();
+        if (j + 1 < nsup)
+          for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+    if (tid == 0) a.ncand[q] = s_nc;  // > cap means only cap ids were stored
+    __syncthreads();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(512));
+  }
+}
 }  // namespace mrpt
 
 using namespace mrpt;
@@ -1550,4 +1849,98 @@ extern "C" int32_t mrpt_vote_stream(const uint32_t *qs, int64_t tstride, const u
   cudaStream_t s = as_stream(stream);
   (count_launch(), fn<<<(unsigned)grid, 1024, smem, s>>>(a, reinterpret_cast<const uint4 *>(qs), qbase, tstride));
   return launch_status("mrpt_vote_stream");
+}
+
+// ------------------------------------------------------- paired vote (host) --
+extern "C" int32_t mrpt_vote_pair_plan(int64_t n, int32_t T, int32_t depth, int64_t max_count, int32_t *ntiles,
+                                       int64_t *pos_entries, int64_t *dir_entries) {
+  clear_error();
+  if (n < 1 || n >= (int64_t)1 << 31 || depth < 0 || depth > 30 || !ntiles || !pos_entries || !dir_entries)
+    return fail(MRPT_ESHAPE, "mrpt_vote_pair_plan: bad arguments");
+  int CW, nt;
+  int64_t W;
+  const int32_t st = stream_geometry(n, T, max_count, &CW, &W, &nt);
+  if (st) return st;
+  *ntiles = nt;
+  *pos_entries = (int64_t)T * ((int64_t)1 << depth) * (nt + 1);
+  *dir_entries = (int64_t)T * ((int64_t)1 << depth) * ((nt + 1) / 2 + 1);
+  return MRPT_OK;
+}
+
+extern "C" int32_t mrpt_vote_pair_layout(const int32_t *leaf_indices, const int64_t *leaf_offsets, int64_t n,
+                                         int32_t T, int32_t depth, int64_t max_count, uint16_t *pos, uint16_t *pdir,
+                                         int32_t *pbase, int64_t *tree_pairs, void *stream) {
+  clear_error();
+  int CW, nt;
+  int64_t W;
+  const int32_t st = stream_geometry(n, T, max_count, &CW, &W, &nt);
+  if (st) return st;
+  cudaStream_t s = as_stream(stream);
+  const int64_t nleaves = (int64_t)T << depth;
+  const int64_t blocks = ceil_div<int64_t>(nleaves, 8);
+  const int grid = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
+  (count_launch(), k_build_dir<<<grid, 256, 0, s>>>(leaf_indices, leaf_offsets, n, T, 1 << depth, (int)W, nt, pos));
+  (count_launch(), k_vpair_dir<<<grid, 256, 0, s>>>(pos, pdir, nleaves, nt, (nt + 1) / 2, pbase));
+  (count_launch(), k_vstream_base<<<T, 1024, 0, s>>>(pbase, 1 << depth, tree_pairs));
+  return launch_status("mrpt_vote_pair_layout");
+}
+
+extern "C" int32_t mrpt_vote_pair_fill(const int32_t *leaf_indices, const int64_t *leaf_offsets, int64_t n, int32_t T,
+                                       int32_t depth, int64_t max_count, const uint16_t *pos, const uint16_t *pdir,
+                                       const int32_t *pbase, int64_t pstride, uint32_t *ps, void *stream) {
+  clear_error();
+  int CW, nt;
+  int64_t W;
+  const int32_t st = stream_geometry(n, T, max_count, &CW, &W, &nt);
+  if (st) return st;
+  if (pstride < 0 || 64 * pstride >= ((int64_t)1 << 31))
+    return fail(MRPT_EPARAM, "mrpt_vote_pair_fill: tree stride too large");
+  cudaStream_t s = as_stream(stream);
+  const int64_t nleaves = (int64_t)T << depth;
+  const int64_t blocks = ceil_div<int64_t>(nleaves, 8);
+  const int grid = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
+  const int nsup = (nt + 1) / 2;
+  auto fn = CW == 1 ? k_vpair_fill<1> : (CW == 3 ? k_vpair_fill<3> : (CW == 2 ? k_vpair_fill<2> : k_vpair_fill<4>));
+  const size_t fsmem = sizeof(int32_t) * (size_t)(nt + 1 + nsup + 1) * 8;  // 8 warps
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
+  (count_launch(), fn<<<grid, 256, fsmem, s>>>(leaf_indices, leaf_offsets, n, T, 1 << depth, (int)W, nt, nsup, pos,
+                                               pdir, pbase, pstride, reinterpret_cast<uint4 *>(ps)));
+  return launch_status("mrpt_vote_pair_fill");
+}
+
+extern "C" int32_t mrpt_vote_pair(const uint32_t *ps, int64_t pstride, const uint16_t *pdir, const int32_t *pbase,
+                                  int64_t n, int32_t T, int32_t depth, int64_t max_count, const int32_t *leaves,
+                                  int64_t nq, int32_t v, int32_t *cand, int64_t cap, int32_t *ncand, void *stream) {
+  clear_error();
+  if (n < 1 || n >= (int64_t)1 << 31 || depth < 0 || depth > 30 || nq < 0)
+    return fail(MRPT_ESHAPE, "mrpt_vote_pair: bad shape");
+  if (v < 1 || v > max_count) return fail(MRPT_EPARAM, "mrpt_vote_pair: vote threshold out of range");
+  if (cap < 1) return fail(MRPT_EPARAM, "mrpt_vote_pair: cap must be >= 1");
+  if (64 * pstride >= ((int64_t)1 << 31)) return fail(MRPT_EPARAM, "mrpt_vote_pair: tree stride too large");
+  int CW, nt;
+  int64_t W;
+  const int32_t st = stream_geometry(n, T, max_count, &CW, &W, &nt);
+  if (st) return st;
+  if (nq == 0) return MRPT_OK;
+  VoteArgs a = {};
+  a.n = n;
+  a.T = T;
+  a.L = 1 << depth;
+  a.leaves = leaves;
+  a.nq = nq;
+  a.v = v;
+  a.cand = cand;
+  a.cap = cap;
+  a.ncand = ncand;
+  a.W = (int)W;
+  a.ntiles = nt;
+  a.dir = pdir;
+  const size_t smem = (size_t)((counter_words_host(CW, W) + 3) & ~3LL) * 4 + 128;  // + 32 spare words
+  typedef void (*pfn_t)(VoteArgs, const uint4 *, const int32_t *, int64_t);
+  pfn_t fn = CW == 1 ? k_vote_pair<1> : (CW == 3 ? k_vote_pair<3> : (CW == 2 ? k_vote_pair<2> : k_vote_pair<4>));
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t grid = nq < (int64_t)num_sms() ? nq : (int64_t)num_sms();
+  (count_launch(), fn<<<(unsigned)grid, 1024, smem, as_stream(stream)>>>(a, reinterpret_cast<const uint4 *>(ps), pbase,
+                                                                         pstride));
+  return launch_status("mrpt_vote_pair");
 }

@@ -258,7 +258,7 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None, size_class=N
         per_q = 4 * (D.T + (bstride if bits_mode else cap))
         chunk = max(1, min(nq, (1 << 30) // per_q))
     if (not bits_mode and choice is not None and nq >= 2 * _ORDER_MIN
-            and os.environ.get("MRPT_QUERY_ORDER", "1") != "0" and D.vote_stream() is not None
+            and os.environ.get("MRPT_QUERY_ORDER", "1") != "0" and D.vote_layout() is not None
             and nq * D.T * 4 <= (2 << 30)):
         return _query_device_ordered(D, Qd, k, votes, choice, cap, chunk, stage, (ids, dists, counts))
     m0 = min(chunk, nq)
@@ -388,7 +388,16 @@ def _route_launch(D, qb, m, ldq, leaves):
 
 
 def _vote_list(D, leaves, m, votes, cand, cap, counts):
-    vs = D.vote_stream()
+    lay = D.vote_layout()
+    if lay == "pair":
+        # the paired streamed vote (two id tiles per load, second parked in TMEM)
+        ps, pstride, pdir, pbase = D.vote_pair()
+        _native.call("mrpt_vote_pair", _native.ptr(ps), int(pstride), _native.ptr(pdir),
+                     _native.ptr(pbase), D.n, D.T, D.depth, int(D.max_count), _native.ptr(leaves), m,
+                     int(votes), _native.ptr(cand), int(cap), _native.ptr(counts),
+                     _native.stream_ptr())
+        return
+    vs = D.vote_stream() if lay == "stream" else None
     if vs is not None:
         # the streamed tiled vote (padded, pre-decoded leaf slices)
         qs, tstride, qdir, qbase = vs

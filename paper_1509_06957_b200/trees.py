@@ -311,6 +311,60 @@ class _DeviceIndex:
         self._vstream = (qs, tstride, qdir, qbase)
         return self._vstream
 
+    def vote_pair(self):
+        """The paired streamed-vote layout of this index (mrpt_vote_pair_layout
+        / _fill: id tiles taken two at a time, every leaf slice stored as
+        32-byte pairs of pre-decoded quads, one of each tile), built once on
+        the device; None where the streamed layout would be None, or
+        MRPT_VOTE_PAIR=0."""
+        if getattr(self, "_vpair", False) is not False:
+            return self._vpair
+        self._vpair = None
+        if os.environ.get("MRPT_VOTE_STREAM", "1") == "0" or os.environ.get("MRPT_VOTE_PAIR", "1") == "0":
+            return None
+        if not self.leaves_sorted or self.max_leaf > 65535 or self.T > 1024:
+            return None
+        ntiles, pos_n, dir_n = ctypes.c_int32(0), ctypes.c_int64(0), ctypes.c_int64(0)
+        try:
+            _native.call("mrpt_vote_pair_plan", self.n, self.T, self.depth, int(self.max_count),
+                         ctypes.byref(ntiles), ctypes.byref(pos_n), ctypes.byref(dir_n))
+        except MRPTError:
+            return None
+        nleaf = 1 << self.depth
+        # padded lengths (7 ids per quad) must fit the u16 pair directory
+        if ntiles.value <= 1 or (self.max_leaf + 6 * ntiles.value) // 7 >= 65535:
+            return None
+        torch = _device.torch_mod()
+        dev = self.indices.device
+        pos = torch.empty(pos_n.value, dtype=torch.int16, device=dev)
+        pdir = torch.empty(dir_n.value, dtype=torch.int16, device=dev)
+        pbase = torch.empty(self.T * nleaf, dtype=torch.int32, device=dev)
+        tp = torch.empty(self.T, dtype=torch.int64, device=dev)
+        _native.call("mrpt_vote_pair_layout", _native.ptr(self.indices), _native.ptr(self.offsets),
+                     self.n, self.T, self.depth, int(self.max_count), _native.ptr(pos), _native.ptr(pdir),
+                     _native.ptr(pbase), _native.ptr(tp), _native.stream_ptr())
+        pstride = int(tp.max().item())
+        nbytes = 32 * self.T * pstride
+        free = torch.cuda.mem_get_info(dev)[0]
+        if 64 * pstride >= (1 << 31) or nbytes > 0.8 * free:
+            return None
+        ps = torch.empty(nbytes // 4, dtype=torch.int32, device=dev)
+        _native.call("mrpt_vote_pair_fill", _native.ptr(self.indices), _native.ptr(self.offsets),
+                     self.n, self.T, self.depth, int(self.max_count), _native.ptr(pos), _native.ptr(pdir),
+                     _native.ptr(pbase), pstride, _native.ptr(ps), _native.stream_ptr())
+        del pos  # stream-ordered: the allocator reuses it only after the fill
+        self._vpair = (ps, pstride, pdir, pbase)
+        return self._vpair
+
+    def vote_layout(self):
+        """Which list-vote layout queries use: "pair" (mrpt_vote_pair),
+        "stream" (mrpt_vote_stream) or None (mrpt_vote over leaf_indices)."""
+        if self.vote_pair() is not None:
+            return "pair"
+        if self.vote_stream() is not None:
+            return "stream"
+        return None
+
     def vote_dir(self):
         """Tile directory for the multi-tile vote (built once, on the device),
         or None when one id tile covers the index or it cannot be used."""
@@ -545,7 +599,7 @@ def _finish_index(X, n_trees, depth, sparsity, seed, fixed_count, matrices, spli
                           leaves_sorted=True, max_count=n_trees, max_leaf=max_leaf)
     # the streamed-vote layout is part of the index the queries use: built
     # here (billed to the build) wherever it applies
-    dindex.vote_stream()
+    dindex.vote_layout()
     return MRPTIndex(dataset=X, n_trees=n_trees, depth=depth, sparsity=float(sparsity), seed=seed,
                      fixed_count=fixed_count, matrices=matrices, splits=splits,
                      leaf_offsets=offsets, leaf_indices=indices,

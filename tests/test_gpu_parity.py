@@ -396,15 +396,16 @@ def test_vote_sweep_one_pass_matches_per_threshold(rng, n, T, depth, votes):
         assert np.array_equal(counts.astype(np.int64), rc)
 
 
-def _stream_lists(index, Q, v, cap=None):
-    """Raw K2 + streamed K3 output through the C ABI (mrpt_vote_stream)."""
+def _stream_lists(index, Q, v, cap=None, layout="stream"):
+    """Raw K2 + streamed K3 output through the C ABI (mrpt_vote_stream, or
+    mrpt_vote_pair over the paired layout)."""
     import torch
 
     from paper_1509_06957_b200 import _native
     from paper_1509_06957_b200.search import _route_device
 
     D = index.device_index()
-    vs = D.vote_stream()
+    vs = D.vote_pair() if layout == "pair" else D.vote_stream()
     assert vs is not None, "the streamed layout should apply here"
     qs, tstride, qdir, qbase = vs
     Qd = torch.from_numpy(np.ascontiguousarray(Q)).cuda()
@@ -412,10 +413,10 @@ def _stream_lists(index, Q, v, cap=None):
     cap = D.cap(v) if cap is None else cap
     cand = torch.full((Q.shape[0], cap), -7, dtype=torch.int32, device="cuda")
     counts = torch.empty(Q.shape[0], dtype=torch.int32, device="cuda")
-    _native.call("mrpt_vote_stream", _native.ptr(qs), int(tstride), _native.ptr(qdir),
-                 _native.ptr(qbase), D.n, D.T, D.depth, int(D.max_count), _native.ptr(leaves),
-                 Q.shape[0], int(v), _native.ptr(cand), int(cap), _native.ptr(counts),
-                 _native.stream_ptr())
+    _native.call("mrpt_vote_pair" if layout == "pair" else "mrpt_vote_stream", _native.ptr(qs),
+                 int(tstride), _native.ptr(qdir), _native.ptr(qbase), D.n, D.T, D.depth, int(D.max_count),
+                 _native.ptr(leaves), Q.shape[0], int(v), _native.ptr(cand), int(cap),
+                 _native.ptr(counts), _native.stream_ptr())
     c = counts.cpu().numpy()
     return [row[:min(m, cap)] for row, m in zip(cand.cpu().numpy(), c)], c
 
@@ -442,11 +443,12 @@ def test_streamed_vote_matches_oracle(rng, T, depth, n, kind, votes):
                leaf_indices=index.leaf_indices, depth=depth)
     leaves = O.query_leaves(Q, ref)
     for v in votes:
-        got, gc = _stream_lists(index, Q, v)
-        for i in range(len(Q)):
-            want = O.candidates(leaves[i], ref, v)
-            assert gc[i] == len(want)
-            assert np.array_equal(np.sort(got[i]), want)
+        for layout in ("stream", "pair"):
+            got, gc = _stream_lists(index, Q, v, layout=layout)
+            for i in range(len(Q)):
+                want = O.candidates(leaves[i], ref, v)
+                assert gc[i] == len(want)
+                assert np.array_equal(np.sort(got[i]), want)
         ids, dists, counts = mrpt.approximate_knn_batch(Q, 10, index, v)
         rids, rd, rc = O.approximate_knn_batch(Xd, Q, 10, ref, v)
         assert np.array_equal(counts.astype(np.int64), rc)
@@ -487,3 +489,42 @@ def test_streamed_vote_layout_round_trip(rng):
                         else:
                             assert u[i] < pad_word + 32 and (fb >> (2 * i)) & 3 == 0
             assert np.array_equal(np.array(ids, dtype=np.int64), li[t, offs[t, f]:offs[t, f + 1]])
+
+
+def test_paired_vote_layout_round_trip(rng):
+    """Decoding the paired layout (pairs -> the two tiles' quads -> ids,
+    padding dropped) gives back every leaf slice exactly, with an odd tile
+    count (the last super-tile's second quads are all padding)."""
+    T, depth, n = 5, 6, 2 * 223_104 + 17  # u8 counters: 223,104 ids per tile -> 3 tiles
+    X = gaussian(rng, n, 4)
+    index = mrpt.grow_trees(X, T, depth, seed=3)
+    D = index.device_index()
+    ps, pstride, pdir, pbase = D.vote_pair()
+    ps = ps.cpu().numpy().view(np.uint32).reshape(T, pstride, 2, 4)
+    pbase = pbase.cpu().numpy()
+    L = 1 << depth
+    words = ((218 * 1024 - 128) // 4) & ~3
+    W = words * 4
+    nt = -(-n // W)
+    nsup = (nt + 1) // 2
+    assert pdir.numel() == T * L * (nsup + 1)
+    pdir = pdir.cpu().numpy().view(np.uint16).reshape(T, L, nsup + 1).astype(np.int64)
+    pad_word = (W // 4 + 3) & ~3
+    offs, li = index.leaf_offsets, index.leaf_indices
+    for t in range(T):
+        for f in range(L):
+            s0 = pbase[t * L + f]
+            ids = []
+            for j in range(nsup):
+                pairs = ps[t, s0 + pdir[t, f, j]: s0 + pdir[t, f, j + 1]]
+                for side in (0, 1):
+                    w = 2 * j + side
+                    for u in pairs[:, side].copy().view(np.uint16).reshape(-1, 8):
+                        fb = int(u[7])
+                        for i in range(7):
+                            if u[i] < pad_word:
+                                assert w < nt
+                                ids.append(w * W + int(u[i]) * 4 + ((fb >> (2 * i)) & 3))
+                            else:
+                                assert u[i] < pad_word + 32 and (fb >> (2 * i)) & 3 == 0
+            assert np.array_equal(np.sort(np.array(ids, dtype=np.int64)), li[t, offs[t, f]:offs[t, f + 1]])
