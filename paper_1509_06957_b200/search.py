@@ -679,6 +679,9 @@ def _knn_batch_pipelined_bits(Qc, k, index, votes, route):
     return hid.numpy(), hdist.numpy(), hcnt.numpy()
 
 
+_SWEEP_SCRATCH_BYTES = 1 << 30  # leaves + candidates + counts of one sweep chunk
+
+
 def approximate_knn_sweep(Q, k, index, votes):
     """approximate_knn_batch for several vote thresholds from ONE route and
     ONE vote pass (the reference's sweeps loop queries and
@@ -706,38 +709,44 @@ def approximate_knn_sweep(Q, k, index, votes):
     dev = Qd.device
     _record_macs(nq * sum(R.nnz for R in index.matrices) * len(vs))
     cap0 = D.cap(vs[0])
-    leaves = torch.empty((max(1, nq), D.T), dtype=torch.int32, device=dev)
-    cand0 = torch.empty((max(1, nq), cap0), dtype=torch.int32, device=dev)
-    cnt0 = torch.empty((max(1, nq), cap0), dtype=torch.int16, device=dev)
-    n0 = torch.empty(max(1, nq), dtype=torch.int32, device=dev)
-    out = {}
-    if nq:
-        _route_launch(D, Qd, nq, int(Qd.stride(0)), leaves)
+    # query rows go through in chunks sized like query_device's (1 GiB of
+    # leaves + candidate + count scratch), so a batch that approximate_knn_batch
+    # answers never runs out of memory here
+    rows = max(1, min(max(1, nq), _SWEEP_SCRATCH_BYTES // (4 * D.T + 6 * cap0)))
+    leaves = torch.empty((rows, D.T), dtype=torch.int32, device=dev)
+    cand0 = torch.empty((rows, cap0), dtype=torch.int32, device=dev)
+    cnt0 = torch.empty((rows, cap0), dtype=torch.int16, device=dev)
+    n0 = torch.empty(rows, dtype=torch.int32, device=dev)
+    res = {v: (torch.empty((nq, k), dtype=torch.int64, device=dev),
+               torch.empty((nq, k), dtype=torch.float64, device=dev),
+               torch.empty(nq, dtype=torch.int32, device=dev)) for v in vs}
+    caps = {v: D.cap(v) for v in vs}
+    cands = {v: torch.empty((rows, caps[v]), dtype=torch.int32, device=dev) for v in vs[1:]}
+    for lo in range(0, nq, rows):
+        m = min(rows, nq - lo)
+        Qc = Qd[lo:lo + m]
+        _route_launch(D, Qc, m, int(Qd.stride(0)), leaves)
         _native.call("mrpt_vote_counted", _native.ptr(D.indices), _native.ptr(D.offsets), D.n, D.T,
-                     D.depth, _native.ptr(leaves), nq, vs[0], int(D.leaves_sorted),
+                     D.depth, _native.ptr(leaves), m, vs[0], int(D.leaves_sorted),
                      int(D.max_count), _native.ptr(D.vote_dir()), _native.ptr(cand0),
                      _native.ptr(cnt0), int(cap0), _native.ptr(n0), _native.stream_ptr())
-    for v in vs:
-        ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
-        dists = torch.empty((nq, k), dtype=torch.float64, device=dev)
-        if v == vs[0]:
-            cand, cap, counts = cand0, cap0, n0[:nq]
-        else:
-            cap = D.cap(v)
-            cand = torch.empty((max(1, nq), cap), dtype=torch.int32, device=dev)
-            counts = torch.empty(nq, dtype=torch.int32, device=dev)
-            if nq:
+        for v in vs:
+            ids, dists, counts_all = res[v]
+            counts = counts_all[lo:lo + m]
+            if v == vs[0]:
+                cand, cap = cand0, cap0
+                counts.copy_(n0[:m])
+            else:
+                cand, cap = cands[v], caps[v]
                 _native.call("mrpt_filter_counts", _native.ptr(cand0), _native.ptr(cnt0), int(cap0),
-                             _native.ptr(n0), nq, v, _native.ptr(cand), int(cap),
+                             _native.ptr(n0), m, v, _native.ptr(cand), int(cap),
                              _native.ptr(counts), _native.stream_ptr())
-        if nq:
             variant = D.scan_choice.get((k, v))
             if variant is None or variant in _BITS_ROUTES:
                 variant = [x for x in _scan_variants(D, k) if x not in _BITS_ROUTES][0]
-            args = (Qd, nq, int(Qd.stride(0)), cand, cap, counts, k, ids, dists)
+            args = (Qc, m, int(Qd.stride(0)), cand, cap, counts, k, ids[lo:lo + m], dists[lo:lo + m])
             _scan_launch(D, variant, args)
-        res = (ids, dists, counts.clone())
-        out[v] = res if on_device else tuple(_device.d2h(t) for t in res)
+    out = {v: (r if on_device else tuple(_device.d2h(t) for t in r)) for v, r in res.items()}
     return out
 
 

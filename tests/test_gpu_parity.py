@@ -396,6 +396,23 @@ def test_vote_sweep_one_pass_matches_per_threshold(rng, n, T, depth, votes):
         assert np.array_equal(counts.astype(np.int64), rc)
 
 
+def test_vote_sweep_in_query_chunks(rng, monkeypatch):
+    """A sweep whose scratch budget holds only 7 queries at a time gives the
+    same answers as the one-chunk sweep (40 queries: five full chunks + 5)."""
+    from paper_1509_06957_b200 import search
+
+    X = gaussian(rng, 20_040, 10)
+    Xd, Q = X[:20_000], X[20_000:]
+    index = mrpt.grow_trees(Xd, 12, 7, seed=17)
+    whole = mrpt.approximate_knn_sweep(Q, 7, index, (1, 2, 4))
+    D = index.device_index()
+    monkeypatch.setattr(search, "_SWEEP_SCRATCH_BYTES", 7 * (4 * D.T + 6 * D.cap(1)))
+    parts = mrpt.approximate_knn_sweep(Q, 7, index, (1, 2, 4))
+    for v in (1, 2, 4):
+        for a, b in zip(whole[v], parts[v]):
+            assert a.tobytes() == b.tobytes()
+
+
 def _stream_lists(index, Q, v, cap=None, layout="stream"):
     """Raw K2 + streamed K3 output through the C ABI (mrpt_vote_stream, or
     mrpt_vote_pair over the paired layout)."""
