@@ -11,9 +11,12 @@
 // m == 0 keeps split 0.0 and sends nothing left (trees.py:84-85).
 //
 // Segments are classified on the device every level (no host sync):
-//   tiny  (m <= 2048)          one CTA, keys+ids staged in 16 KB smem
-//   mid   (2048 < m <= 8192)   one CTA, 64 KB smem
-//   big   (m > 8192)           chunked over many CTAs: key gather pass,
+//   tiny  (m <= 2048)          one CTA of 128, keys+ids staged in 16 KB smem
+//   mid   (2048 < m <= 8192)   one CTA of 256, keys in 32 KB smem (ids re-read)
+//   large (8192 < m <= 23552)  one CTA of 1024, keys in 92 KB smem (ids are
+//                              re-read for the partition), segments taken
+//                              from a tree-major list
+//   big   (m > 23552)          chunked over many CTAs: key gather pass,
 //                              up to four 8-bit histogram passes with global
 //                              histograms, count / scan / stable scatter.
 // The radix select first strips the prefix shared by the segment's min and
@@ -24,6 +27,9 @@ namespace mrpt {
 
 constexpr int kTinyMax = 2048;
 constexpr int kMidMax = 8192;
+constexpr int kLargeMax = 47104;   // 184 KB of keys + 8 KB of buckets: one CTA per SM
+constexpr int kLargeMax2 = 23552;  // 92 KB of keys: two CTAs per SM
+constexpr int kLinList = 512;     // bucket members ranked by counting (else: radix select)
 constexpr int kChunk = 8192;  // elements per CTA work item in the big path
 constexpr int kNT = 256;      // threads per CTA for all build kernels
 
@@ -39,7 +45,7 @@ struct BigSeg {
 };
 
 struct LevelCtl {
-  int32_t ntiny, nmid, nbig, pad;
+  int32_t ntiny, nmid, nbig, nlarge;
   int64_t nchunks;
 };
 
@@ -63,6 +69,11 @@ struct LevelArgs {
   int32_t *chunk_left, *chunk_off;
   int32_t *tree_nch;   // (Tb) big-path chunks per tree this level
   int64_t *tree_base;  // (Tb) first chunk of each tree (tree-major chunk order)
+  int32_t *tree_nlg;   // (Tb) large segments per tree this level
+  int32_t *tree_lfill; // (Tb) large segments of the tree already listed
+  int64_t *tree_lbase; // (Tb) first list slot of each tree
+  int32_t *large_list; // tree-major list of this level's large segments
+  int large_max;       // upper size of the large class (kMidMax: no large class)
 };
 
 __device__ __forceinline__ void write_node(const LevelArgs &a, int t, int s, int64_t b, int64_t e,
@@ -166,7 +177,9 @@ __global__ void k_level_plan(LevelArgs a) {
   const int t = (int)(seg >> a.lev), s = (int)(seg & (nseg - 1));
   const int64_t *B = a.bounds_in + (int64_t)t * a.bstride;
   const int64_t b = B[s], e = B[s + 1], m = e - b;
-  if (m > kMidMax) {  // tiny / mid segments are found by k_seg_small itself
+  if (m > kMidMax && m <= a.large_max) {
+    atomicAdd(&a.tree_nlg[t], 1);  // listed tree-major by k_large_fill
+  } else if (m > a.large_max) {  // tiny / mid segments are found by k_seg_cta itself
     const int slot = atomicAdd(&a.ctl->nbig, 1);
     const int nch = (int)ceil_div<int64_t>(m, kChunk);
     // chunk position within its tree; k_chunk_layout adds the tree's base so
@@ -195,15 +208,14 @@ __global__ void k_level_plan(LevelArgs a) {
   }
 }
 
-// Tree-major chunk table: exclusive scan of the per-tree chunk counts (one
-// CTA), then one warp per big segment rebases its chunks and writes them.
-__global__ void __launch_bounds__(1024) k_chunk_layout(LevelArgs a) {
-  __shared__ int64_t wsum[33];
+// Exclusive scan of a per-tree count array by one CTA of 1024; returns the
+// total in every thread.
+__device__ __forceinline__ int64_t scan_trees(const int32_t *cnt, int64_t *base, int Tb, int64_t *wsum) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int64_t carry = 0;
-  for (int t0 = 0; t0 < a.Tb; t0 += 1024) {
+  for (int t0 = 0; t0 < Tb; t0 += 1024) {
     const int t = t0 + threadIdx.x;
-    const int64_t v = t < a.Tb ? a.tree_nch[t] : 0;
+    const int64_t v = t < Tb ? cnt[t] : 0;
     int64_t incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -224,11 +236,38 @@ __global__ void __launch_bounds__(1024) k_chunk_layout(LevelArgs a) {
       if (lane == 31) wsum[32] = x;
     }
     __syncthreads();
-    if (t < a.Tb) a.tree_base[t] = carry + wsum[warp] + incl - v;
+    if (t < Tb) base[t] = carry + wsum[warp] + incl - v;
     carry += wsum[32];
     __syncthreads();
   }
-  if (threadIdx.x == 0) a.ctl->nchunks = carry;
+  return carry;
+}
+
+// Tree-major tables: the big path's chunk table and the list of large
+// segments start, per tree, at the exclusive scan of the per-tree counts.
+__global__ void __launch_bounds__(1024) k_chunk_layout(LevelArgs a) {
+  __shared__ int64_t wsum[33];
+  const int64_t nch = scan_trees(a.tree_nch, a.tree_base, a.Tb, wsum);
+  const int64_t nlg = scan_trees(a.tree_nlg, a.tree_lbase, a.Tb, wsum);
+  if (threadIdx.x == 0) {
+    a.ctl->nchunks = nch;
+    a.ctl->nlarge = (int32_t)nlg;
+  }
+}
+
+// One thread per segment: large segments enter the list at their tree's base
+// (any order within a tree; what matters is that consecutive entries gather
+// from the same projection column).
+__global__ void k_large_fill(LevelArgs a) {
+  const int nseg = 1 << a.lev;
+  const int64_t total = (int64_t)a.Tb * nseg;
+  const int64_t seg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (seg >= total) return;
+  const int t = (int)(seg >> a.lev), s = (int)(seg & (nseg - 1));
+  const int64_t *B = a.bounds_in + (int64_t)t * a.bstride;
+  const int64_t m = B[s + 1] - B[s];
+  if (m > kMidMax && m <= a.large_max)
+    a.large_list[a.tree_lbase[t] + atomicAdd(&a.tree_lfill[t], 1)] = (int32_t)seg;
 }
 
 __global__ void k_chunk_fill(LevelArgs a) {
@@ -244,110 +283,250 @@ __global__ void k_chunk_fill(LevelArgs a) {
   }
 }
 
-// One CTA per segment with m <= MAXM (keys and ids staged in smem).  CTAs
-// walk the segments in tree-major order (segment = t * 2^lev + s) and skip
-// those of the other size class, so the CTAs resident at any time gather
-// from one or two trees' projection columns, which then stay in L2 (an
-// atomically appended work list interleaves all trees of the batch and made
-// the gathers read DRAM ~13x the keys' bytes at config 5).
-template <int MAXM>
-__global__ void __launch_bounds__(kNT) k_seg_small(LevelArgs a, int which) {
-  extern __shared__ uint32_t dyn_smem[];
-  uint32_t *keys = dyn_smem;                                      // MAXM
-  int32_t *ids = reinterpret_cast<int32_t *>(dyn_smem + MAXM);    // MAXM
-  __shared__ uint32_t hist[256];
-  __shared__ uint32_t red_mn[kNT / 32], red_mx[kNT / 32];
-  __shared__ int s_bin, s_below, s_cnt;
-  __shared__ int wcnt[kNT / 32];
+// One CTA per segment with m <= MAXM: keys (and, with IDS, the ids) staged in
+// shared memory, exact radix select there, stable partition by warp ranges.
+//  * load: every thread issues U id loads, then U projection gathers, before
+//    any key is stored (two memory round trips per U*NT elements);
+//  * partition: warp w owns a contiguous range of positions, counts its
+//    left-goers by ballots, one barrier publishes the warp totals, then every
+//    warp writes its range at its ranks (lanes consecutive: the left and the
+//    right runs are both coalesced).
+template <int MAXM, int NT, int NB, bool IDS>
+__device__ __forceinline__ void seg_cta(const LevelArgs &a, int t, int s, int64_t b, int64_t e,
+                                        uint32_t *keys, int32_t *ids, uint32_t *hist,
+                                        uint32_t *red, int *sh) {
+  constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nseg = 1 << a.lev;
-  const int64_t total = (int64_t)a.Tb << a.lev;
-  for (int64_t seg = blockIdx.x; seg < total; seg += gridDim.x) {
-    const int t = (int)(seg >> a.lev), s = (int)(seg & (nseg - 1));
-    const int64_t *B = a.bounds_in + (int64_t)t * a.bstride;
-    const int64_t b = B[s], e = B[s + 1];
-    if (which == 0 ? (e - b > kTinyMax) : (e - b <= kTinyMax || e - b > kMidMax)) continue;  // CTA-uniform
-    const int m = (int)(e - b);
-    if (m == 0) {
-      if (tid == 0) write_node(a, t, s, b, e, 0, 0.0f);
-      continue;
+  const int m = (int)(e - b);
+  const float *Pc = a.P + ((int64_t)t * a.depth + a.lev) * a.n;
+  const int32_t *oin = a.order_in + (int64_t)t * a.n + b;
+  int32_t *oout = a.order_out + (int64_t)t * a.n + b;
+  uint32_t mn = 0xffffffffu, mx = 0u;
+  constexpr int U = 8;
+  for (int i0 = tid; i0 < m; i0 += U * NT) {
+    int32_t id[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) id[j] = i0 + j * NT < m ? __ldg(oin + i0 + j * NT) : -1;
+    float v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) v[j] = id[j] >= 0 ? __ldg(Pc + id[j]) : 0.f;
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      if (id[j] >= 0) {
+        const uint32_t k = f2key(v[j]);
+        keys[i0 + j * NT] = k;
+        if (IDS) ids[i0 + j * NT] = id[j];
+        mn = k < mn ? k : mn;
+        mx = k > mx ? k : mx;
+      }
     }
-    const float *Pc = a.P + ((int64_t)t * a.depth + a.lev) * a.n;
-    const int32_t *oin = a.order_in + (int64_t)t * a.n + b;
-    int32_t *oout = a.order_out + (int64_t)t * a.n + b;
-    uint32_t mn = 0xffffffffu, mx = 0u;
-    for (int i = tid; i < m; i += kNT) {
-      const int32_t id = oin[i];
-      const uint32_t k = f2key(__ldg(Pc + id));
-      keys[i] = k;
-      ids[i] = id;
-      mn = k < mn ? k : mn;
-      mx = k > mx ? k : mx;
+  }
+  // block min / max (the barrier also publishes keys / ids)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint32_t x = __shfl_xor_sync(0xffffffffu, mn, o), y = __shfl_xor_sync(0xffffffffu, mx, o);
+    mn = x < mn ? x : mn;
+    mx = y > mx ? y : mx;
+  }
+  if (lane == 0) {
+    red[warp] = mn;
+    red[NW + warp] = mx;
+  }
+  __syncthreads();
+  {
+    uint32_t x = lane < NW ? red[lane] : 0xffffffffu, y = lane < NW ? red[NW + lane] : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint32_t x2 = __shfl_xor_sync(0xffffffffu, x, o), y2 = __shfl_xor_sync(0xffffffffu, y, o);
+      x = x2 < x ? x2 : x;
+      y = y2 > y ? y2 : y;
     }
-    block_minmax(mn, mx, red_mn, red_mx);  // includes the barrier publishing keys/ids
-    const int kth = (m + 1) / 2 - 1;
-    uint32_t K;
-    int nle;
-    if (mn == mx) {
-      K = mn;
-      nle = m;
-    } else {
-      int nb = __clz(mn ^ mx);
-      uint32_t prefix = nb ? (mn & (0xffffffffu << (32 - nb))) : 0u;
-      int krem = kth, cnt_last = 0;
-      while (nb < 32) {
-        const int w8 = (32 - nb) < 8 ? (32 - nb) : 8;
-        const int shift = 32 - nb - w8;
-        const uint32_t dmask = (1u << w8) - 1u;
-        hist[tid] = 0u;  // kNT == 256 bins
-        __syncthreads();
-        for (int i = tid; i < m; i += kNT) {
+    mn = x;
+    mx = y;
+  }
+  const int kth = (m + 1) / 2 - 1;
+  uint32_t K = mn;
+  int nle = m;
+  bool solved = mn == mx;
+  // Linear buckets first: bucket(v) = min(NB-1, int((v - vmin) * scale))
+  // is non-decreasing in v (rounded subtraction, multiplication by a positive
+  // constant and truncation all are), so the bucket holding rank kth holds
+  // the median, and its few members are ranked exactly by their keys.  The
+  // 8-bit digits of a float key put a whole segment into a handful of bins
+  // (sign and exponent bits), i.e. thousands of same-address shared atomics.
+  if (!solved) {
+    const float vmin = key2f(mn), span = key2f(mx) - vmin;
+    const float scale = (float)NB / span;
+    if (isfinite(span) && isfinite(scale)) {
+      constexpr int BPT = NB / NT;  // consecutive buckets per thread
+      for (int i = tid; i < NB; i += NT) hist[i] = 0u;
+      if (tid == 0) sh[3] = 0;
+      __syncthreads();
+      for (int i = tid; i < m; i += NT) {
+        const int bk = (int)((key2f(keys[i]) - vmin) * scale);
+        atomicAdd(&hist[bk < NB - 1 ? bk : NB - 1], 1u);
+      }
+      __syncthreads();
+      uint32_t hv[BPT];
+      int sum = 0;
+#pragma unroll
+      for (int j = 0; j < BPT; ++j) {
+        hv[j] = hist[tid * BPT + j];
+        sum += (int)hv[j];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+      }
+      int *wtot = sh + 4;
+      if (lane == 31) wtot[warp] = incl;
+      __syncthreads();
+      int wbase = lane < warp ? wtot[lane] : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) wbase += __shfl_xor_sync(0xffffffffu, wbase, o);
+      int excl = wbase + incl - sum;
+      if (excl <= kth && kth < excl + sum) {  // exactly one thread
+#pragma unroll
+        for (int j = 0; j < BPT; ++j) {
+          if (kth < excl + (int)hv[j]) {
+            sh[0] = tid * BPT + j;
+            sh[1] = excl;
+            sh[2] = (int)hv[j];
+            break;
+          }
+          excl += (int)hv[j];
+        }
+      }
+      __syncthreads();
+      const int bsel = sh[0], below = sh[1], cnt = sh[2];
+      if (cnt <= kLinList) {
+        uint32_t *list = hist;  // the counts are no longer needed
+        for (int i = tid; i < m; i += NT) {
           const uint32_t k = keys[i];
-          if (prefix_match(k, prefix, nb)) atomicAdd(&hist[(k >> shift) & dmask], 1u);
+          const int bk = (int)((key2f(k) - vmin) * scale);
+          if ((bk < NB - 1 ? bk : NB - 1) == bsel) list[atomicAdd(&sh[3], 1)] = k;
         }
         __syncthreads();
-        if (warp == 0) {
-          int bin, below, cnt;
-          warp_pick(hist, krem, bin, below, cnt);
-          if (lane == 0) {
-            s_bin = bin;
-            s_below = below;
-            s_cnt = cnt;
+        const int r = kth - below;
+        for (int j = tid; j < cnt; j += NT) {
+          const uint32_t kj = list[j];
+          int lt = 0, le = 0;
+          for (int i = 0; i < cnt; ++i) {
+            const uint32_t ki = list[i];
+            lt += ki < kj ? 1 : 0;
+            le += ki <= kj ? 1 : 0;
+          }
+          if (lt <= r && r < le) {  // every holder of the median value writes the same pair
+            sh[0] = (int)kj;
+            sh[1] = below + le;
           }
         }
         __syncthreads();
-        prefix |= (uint32_t)s_bin << shift;
-        krem -= s_below;
-        cnt_last = s_cnt;
-        nb += w8;
-        __syncthreads();
+        K = (uint32_t)sh[0];
+        nle = sh[1];
+        solved = true;
       }
-      K = prefix;
-      nle = kth - krem + cnt_last;
+      __syncthreads();  // sh / hist are rewritten below
     }
-    // stable partition: rounds of kNT elements, ballot ranks
-    int base_left = 0;
-    for (int r0 = 0; r0 < m; r0 += kNT) {
-      const int i = r0 + tid;
-      const bool valid = i < m;
-      const bool f = valid && keys[i] <= K;
-      const unsigned bal = __ballot_sync(0xffffffffu, f);
-      if (lane == 0) wcnt[warp] = __popc(bal);
+  }
+  if (!solved) {
+    int nb = __clz(mn ^ mx);
+    uint32_t prefix = nb ? (mn & (0xffffffffu << (32 - nb))) : 0u;
+    int krem = kth, cnt_last = 0;
+    while (nb < 32) {
+      const int w8 = (32 - nb) < 8 ? (32 - nb) : 8;
+      const int shift = 32 - nb - w8;
+      const uint32_t dmask = (1u << w8) - 1u;
+      if (tid < 256) hist[tid] = 0u;
       __syncthreads();
-      int before = 0, tot = 0;
+      for (int i = tid; i < m; i += NT) {
+        const uint32_t k = keys[i];
+        if (prefix_match(k, prefix, nb)) atomicAdd(&hist[(k >> shift) & dmask], 1u);
+      }
+      __syncthreads();
+      if (warp == 0) {
+        int bin, below, cnt;
+        warp_pick(hist, krem, bin, below, cnt);
+        if (lane == 0) {
+          sh[0] = bin;
+          sh[1] = below;
+          sh[2] = cnt;
+        }
+      }
+      __syncthreads();
+      prefix |= (uint32_t)sh[0] << shift;
+      krem -= sh[1];
+      cnt_last = sh[2];
+      nb += w8;
+    }
+    K = prefix;
+    nle = kth - krem + cnt_last;
+  }
+  // stable partition by warp ranges
+  int *wtot = sh + 4;
+  const int R = ((m + NW - 1) / NW + 31) & ~31;
+  const int r0 = warp * R;
+  const int r1 = r0 + R < m ? r0 + R : m;
+  int c = 0;
+  for (int i = r0 + lane; i - lane < r1; i += 32)  // warp-uniform trip count
+    c += __popc(__ballot_sync(0xffffffffu, i < r1 && keys[i] <= K));
+  if (lane == 0) wtot[warp] = c;
+  __syncthreads();
+  int base = lane < warp ? wtot[lane] : 0;  // NW <= 32
 #pragma unroll
-      for (int w2 = 0; w2 < kNT / 32; ++w2) {
-        const int c = wcnt[w2];
-        before += w2 < warp ? c : 0;
-        tot += c;
-      }
-      const int lrank = base_left + before + __popc(bal & lanemask_lt());
-      if (valid) oout[f ? lrank : nle + (i - lrank)] = ids[i];
-      base_left += tot;
-      __syncthreads();
+  for (int o = 16; o > 0; o >>= 1) base += __shfl_xor_sync(0xffffffffu, base, o);
+  constexpr int PU = IDS ? 1 : 4;  // id re-reads in flight per lane
+  for (int i0 = r0; i0 < r1; i0 += 32 * PU) {
+    int32_t idv[PU];
+#pragma unroll
+    for (int j = 0; j < PU; ++j) {
+      const int i = i0 + j * 32 + lane;
+      idv[j] = i < r1 ? (IDS ? ids[i] : __ldg(oin + i)) : 0;
     }
-    if (tid == 0) write_node(a, t, s, b, e, nle, key2f(K));
-    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < PU; ++j) {
+      const int i = i0 + j * 32 + lane;
+      const bool f = i < r1 && keys[i] <= K;
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      const int lrank = base + __popc(bal & lanemask_lt());
+      if (i < r1) oout[f ? lrank : nle + (i - lrank)] = idv[j];
+      base += __popc(bal);
+    }
+  }
+  if (tid == 0) write_node(a, t, s, b, e, nle, key2f(K));
+  __syncthreads();  // keys / hist / sh are reused by the CTA's next segment
+}
+
+// Flat mode (list == nullptr): CTA i looks at segment i = t * 2^lev + s and
+// returns unless its size lies in (lo, hi] -- in-order dispatch keeps the
+// resident CTAs within one or two trees, whose projection columns then stay
+// in L2 (an atomically appended work list interleaved all trees of the batch
+// and made the gathers read DRAM ~13x the keys' bytes at config 5).  List
+// mode: persistent CTAs stride over the tree-major list of large segments.
+template <int MAXM, int NT, int NB, bool IDS>
+__global__ void __launch_bounds__(NT) k_seg_cta(LevelArgs a, int lo, int hi, bool use_list) {
+  extern __shared__ uint32_t dyn_smem[];
+  uint32_t *keys = dyn_smem;                                                          // MAXM
+  int32_t *ids = reinterpret_cast<int32_t *>(dyn_smem + MAXM);                        // MAXM if IDS
+  __shared__ uint32_t hist[NB];
+  static_assert(NB % NT == 0 && NB >= kLinList && NB >= 256, "bucket table");
+  __shared__ uint32_t red[2 * NT / 32];
+  __shared__ int sh[4 + NT / 32];
+  const int nseg = 1 << a.lev;
+  const int64_t total = use_list ? (int64_t)a.ctl->nlarge : ((int64_t)a.Tb << a.lev);
+  for (int64_t w = blockIdx.x; w < total; w += gridDim.x) {
+    const int64_t seg = use_list ? (int64_t)a.large_list[w] : w;
+    const int t = (int)(seg >> a.lev), s = (int)(seg & (nseg - 1));
+    const int64_t *B = a.bounds_in + (int64_t)t * a.bstride;
+    const int64_t b = B[s], e = B[s + 1];
+    if (e - b <= lo || e - b > hi) continue;  // CTA-uniform
+    if (e == b) {
+      if (threadIdx.x == 0) write_node(a, t, s, b, e, 0, 0.0f);
+      continue;
+    }
+    seg_cta<MAXM, NT, NB, IDS>(a, t, s, b, e, keys, ids, hist, red, sh);
   }
 }
 
@@ -721,7 +900,7 @@ __global__ void __launch_bounds__(kNT) k_big_scatter(LevelArgs a) {
 
 // ---------------------------------------------------------------------------
 struct WsLayout {
-  size_t order_tmp, bounds_tmp, keys, ctl, tiny, mid, big, ghist, chunks, cleft, coff, tnch, tbase, total;
+  size_t order_tmp, bounds_tmp, keys, ctl, tiny, mid, big, ghist, chunks, cleft, coff, tnch, tbase, tlbase, llist, total;
 };
 
 static size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -732,6 +911,8 @@ static WsLayout layout(int64_t n, int Tb, int depth) {
   const int64_t max_level_segs = (int64_t)Tb * (depth > 0 ? (nleaf >> 1) : 1);
   int64_t big_per_tree = n / (kMidMax + 1);
   if (depth > 0 && big_per_tree > (nleaf >> 1)) big_per_tree = nleaf >> 1;
+  int64_t large_per_tree = n / (kMidMax + 1);
+  if (depth > 0 && large_per_tree > (nleaf >> 1)) large_per_tree = nleaf >> 1;
   const int64_t maxbig = (int64_t)Tb * big_per_tree + 1;
   const int64_t maxchunks = (int64_t)Tb * (n / kChunk + big_per_tree + 1) + 1;
   size_t off = 0;
@@ -746,8 +927,10 @@ static WsLayout layout(int64_t n, int Tb, int depth) {
   L.chunks = off; off = align_up(off + sizeof(int2) * (size_t)maxchunks);
   L.cleft = off; off = align_up(off + sizeof(int32_t) * (size_t)maxchunks);
   L.coff = off; off = align_up(off + sizeof(int32_t) * (size_t)maxchunks);
-  L.tnch = off; off = align_up(off + sizeof(int32_t) * (size_t)Tb);
+  L.tnch = off; off = align_up(off + sizeof(int32_t) * 3 * (size_t)Tb);  // tree_nch, tree_nlg, tree_lfill
   L.tbase = off; off = align_up(off + sizeof(int64_t) * (size_t)Tb);
+  L.tlbase = off; off = align_up(off + sizeof(int64_t) * (size_t)Tb);
+  L.llist = off; off = align_up(off + sizeof(int32_t) * ((size_t)Tb * large_per_tree + 1));
   L.total = off;
   return L;
 }
@@ -799,7 +982,14 @@ extern "C" int32_t mrpt_build_levels(const float *P, int64_t n, int32_t Tb, int3
     (count_launch(), k_build_init<<<grid, 256, 0, s>>>(obuf[0], bbuf[0], n, Tb, bstride));
   }
   const int sms = num_sms();
-  cudaFuncSetAttribute(k_seg_small<kMidMax>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMidMax * 8);
+  cudaFuncSetAttribute(k_seg_cta<kMidMax, 256, 1024, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMidMax * 4);
+  cudaFuncSetAttribute(k_seg_cta<kLargeMax, 1024, 2048, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLargeMax * 4);
+  cudaFuncSetAttribute(k_seg_cta<kLargeMax2, 1024, 2048, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLargeMax2 * 4);
+  const int large_max = [] {  // read per call: build_ab switches it between builds
+    const char *e = getenv("MRPT_BUILD_LARGE");  // experiments: 0 (no large class), 23552, 47104
+    const int v = e ? atoi(e) : kLargeMax;
+    return v >= kLargeMax ? kLargeMax : (v >= kLargeMax2 ? kLargeMax2 : kMidMax);
+  }();
   for (int lev = 0; lev < depth; ++lev) {
     LevelArgs a;
     a.P = P;
@@ -824,27 +1014,38 @@ extern "C" int32_t mrpt_build_levels(const float *P, int64_t n, int32_t Tb, int3
     a.chunk_left = reinterpret_cast<int32_t *>(w + L.cleft);
     a.chunk_off = reinterpret_cast<int32_t *>(w + L.coff);
     a.tree_nch = reinterpret_cast<int32_t *>(w + L.tnch);
+    a.tree_nlg = a.tree_nch + Tb;
+    a.tree_lfill = a.tree_nch + 2 * (size_t)Tb;
     a.tree_base = reinterpret_cast<int64_t *>(w + L.tbase);
+    a.tree_lbase = reinterpret_cast<int64_t *>(w + L.tlbase);
+    a.large_list = reinterpret_cast<int32_t *>(w + L.llist);
+    a.large_max = large_max;
     cudaMemsetAsync(a.ctl, 0, sizeof(LevelCtl), s);
-    cudaMemsetAsync(a.tree_nch, 0, sizeof(int32_t) * (size_t)Tb, s);
+    cudaMemsetAsync(a.tree_nch, 0, sizeof(int32_t) * 3 * (size_t)Tb, s);
     const int64_t nsegs = (int64_t)Tb << lev;
-    (count_launch(), k_level_plan<<<(unsigned)ceil_div<int64_t>(nsegs, 256), 256, 0, s>>>(a));
-    // expected per-segment size decides how many CTAs the small paths get
-    const int64_t est = n >> lev;
-    const int64_t tiny_grid = nsegs < (int64_t)sms * 8 ? nsegs : (int64_t)sms * 8;
-    // one CTA per segment for the same L2 locality of the projection gathers
-    static const bool small_flat = [] {
-      const char *e = getenv("MRPT_BUILD_SMALL_FLAT");  // "0": grid-stride loop
-      return !(e && atoi(e) == 0);
-    }();
+    const unsigned seg_blocks = (unsigned)ceil_div<int64_t>(nsegs, 256);
+    (count_launch(), k_level_plan<<<seg_blocks, 256, 0, s>>>(a));
+    (count_launch(), k_chunk_layout<<<1, 1024, 0, s>>>(a));
+    (count_launch(), k_large_fill<<<seg_blocks, 256, 0, s>>>(a));
+    // one CTA per segment (flat, in tree-major order) for the L2 locality of
+    // the projection gathers; large segments from their tree-major list
     const unsigned flat_grid = (unsigned)(nsegs < 0x7fffffff ? nsegs : 0x7fffffff);
-    (count_launch(), k_seg_small<kTinyMax><<<small_flat ? flat_grid
-                                                        : (unsigned)(est <= kTinyMax ? tiny_grid : (tiny_grid < sms ? tiny_grid : sms)),
-                             kNT, kTinyMax * 8, s>>>(a, 0));
-    const int64_t mid_grid = small_flat ? (int64_t)flat_grid : (nsegs < (int64_t)sms * 3 ? nsegs : (int64_t)sms * 3);
-    (count_launch(), k_seg_small<kMidMax><<<(unsigned)mid_grid, kNT, kMidMax * 8, s>>>(a, 1));
-    if (est > kMidMax || lev > 0) {
-      // the big path may have work whenever a segment can exceed kMidMax;
+    (count_launch(), k_seg_cta<kTinyMax, 128, 512, true><<<flat_grid, 128, kTinyMax * 8, s>>>(a, -1, kTinyMax, false));
+    (count_launch(), k_seg_cta<kMidMax, 256, 1024, false><<<flat_grid, 256, kMidMax * 4, s>>>(a, kTinyMax, kMidMax, false));
+    if (large_max > kMidMax) {
+      // a level has at most n * Tb / (kMidMax + 1) large segments
+      const int64_t bound = (int64_t)Tb * (n / (kMidMax + 1)) + 1;
+      const int64_t lg = bound < nsegs ? bound : nsegs;
+      if (large_max == kLargeMax)
+        (count_launch(), k_seg_cta<kLargeMax, 1024, 2048, false><<<(unsigned)(lg < sms ? lg : sms), 1024, kLargeMax * 4, s>>>(
+            a, kMidMax, kLargeMax, true));
+      else
+        (count_launch(), k_seg_cta<kLargeMax2, 1024, 2048, false><<<(unsigned)(lg < 2 * sms ? lg : 2 * sms), 1024, kLargeMax2 * 4, s>>>(
+            a, kMidMax, kLargeMax2, true));
+    }
+    const int64_t est = n >> lev;
+    if (est > large_max || lev > 0) {
+      // the big path may have work whenever a segment can exceed the large class;
       // after level 0 ties can make any segment large, so always launch.
       static const int big_per_sm = [] {
         // 8 resident 256-thread CTAs per SM for the streaming passes
@@ -854,7 +1055,6 @@ extern "C" int32_t mrpt_build_levels(const float *P, int64_t n, int32_t Tb, int3
         return v < 1 ? 1 : (v > 8 ? 8 : v);
       }();
       const int big_grid = sms * big_per_sm;
-      (count_launch(), k_chunk_layout<<<1, 1024, 0, s>>>(a));
       (count_launch(), k_chunk_fill<<<sms * 2, 256, 0, s>>>(a));
       // The gather P[t][lev][order[i]] re-reads a tree's projection column
       // once per segment; with one CTA per chunk (in-order dispatch keeps the

@@ -837,12 +837,14 @@ __global__ void __launch_bounds__(kScanNT, 4) k_scan_topk_filter_h(TopkArgs a, d
   constexpr int kMaxJ = 4;  // ldh <= 256 * kMaxJ halves
   float *qs = reinterpret_cast<float *>(topk_smem);                   // 256 * kMaxJ
   float *wa = qs + 256 * kMaxJ;                                        // NWARP*BUFW filter values
-  float *wr = wa + NWARP * BUFW;                                       // NWARP*BUFW radii
-  int32_t *wid = reinterpret_cast<int32_t *>(wr + NWARP * BUFW);      // NWARP*BUFW
-  unsigned long long *ckey = reinterpret_cast<unsigned long long *>(wid + NWARP * BUFW);  // NWARP*BUFW
-  int32_t *cid = reinterpret_cast<int32_t *>(ckey + NWARP * BUFW);    // NWARP*BUFW
-  float *cu = reinterpret_cast<float *>(cid + NWARP * BUFW);          // NWARP*BUFW
-  float *cl = cu + NWARP * BUFW;                                       // NWARP*BUFW
+  int32_t *wid = reinterpret_cast<int32_t *>(wa + NWARP * BUFW);      // NWARP*BUFW
+  int32_t *cid = wid + NWARP * BUFW;                                   // NWARP*BUFW
+  float *cl = reinterpret_cast<float *>(cid + NWARP * BUFW);          // NWARP*BUFW
+  float *wr = cl + NWARP * BUFW;                                       // NWARP*BUFW radii
+  float *cu = wr + NWARP * BUFW;                                       // NWARP*BUFW
+  // the rerank keys (8 bytes each) overlay the radii and the upper bounds,
+  // both dead by then: 52 KB per CTA at BUFW = 256, four CTAs per SM
+  unsigned long long *ckey = reinterpret_cast<unsigned long long *>(wr);  // NWARP*BUFW
   __shared__ int s_wcnt[NWARP];
   __shared__ int s_bad, s_ns;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -2027,7 +2029,7 @@ extern "C" int32_t mrpt_scan_topk_fp16(const float *X, int64_t n, int32_t d, int
   a.ldh = ldh;
   a.radius = radius;
   const int bufw = (2 * k + 16 <= 64) ? 64 : ((2 * k + 16 <= 128) ? 128 : 256);
-  const size_t smem = sizeof(float) * 256 * 4 + (size_t)(kScanNT / 32) * bufw * (4 + 4 + 4 + 8 + 4 + 4 + 4);
+  const size_t smem = sizeof(float) * 256 * 4 + (size_t)(kScanNT / 32) * bufw * (4 + 4 + 4 + 4 + 4 + 4);
   int32_t *fb = nullptr;
   keep_pool_warm();
   if (cudaMallocAsync((void **)&fb, sizeof(int32_t) * (nq + 1), s) != cudaSuccess)

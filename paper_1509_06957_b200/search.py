@@ -297,6 +297,7 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None, size_class=N
 
 _BITS_ROUTES = ("u8tc_bits",)
 _ORDER_MIN = 4096  # queries: below this a batch is processed in its own order
+_order_hook = None  # experiments (tools/order_ab.py): callable(leaves, Qd) -> int32 query order
 
 
 def _permute(src, idx, dst, scatter):
@@ -327,8 +328,11 @@ def _query_device_ordered(D, Qd, k, votes, variant, cap, chunk, stage, out):
     lp = torch.empty_like(leaves)
 
     def reorder():
-        _native.call("mrpt_query_order", _native.ptr(leaves), nq, D.T, D.depth, _native.ptr(order),
-                     _native.ptr(ws), _native.stream_ptr())
+        if _order_hook is not None:
+            order.copy_(_order_hook(leaves, Qd))
+        else:
+            _native.call("mrpt_query_order", _native.ptr(leaves), nq, D.T, D.depth, _native.ptr(order),
+                         _native.ptr(ws), _native.stream_ptr())
         _permute(Qd, order, Qp, False)
         _permute(leaves, order, lp, False)
 

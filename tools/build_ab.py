@@ -1,9 +1,10 @@
-"""Build-time A/B in one process: grow_trees on a configuration twice per
+"""Build-time A/B in one process (TB=n in a spec fixes the trees per batch): grow_trees on a configuration twice per
 variant (the first warms), variants chosen by environment settings given as
 NAME=VAL[,NAME=VAL] arguments; also checks the variants build identical trees.
 usage: python tools/build_ab.py CONFIG SCALE "MRPT_PROJ_D64=0" "MRPT_PROJ_D64=1" ...
 (CACHED=1 in a spec: build from a Dataset whose checksum is already known,
 i.e. the build without the K6 checksum.)"""
+import gc
 import os
 import sys
 import time
@@ -28,10 +29,14 @@ for spec in sys.argv[3:]:
         from paper_1509_06957_b200.core import as_dataset
         src = as_dataset(Xd)
         src.checksum
+    tb = int(os.environ.get("TB", "0")) or None  # trees per K1+K5 batch (else: from free memory)
     for _ in range(2):
+        index = D = None  # the previous index is freed first: the batch size depends on free memory
+        gc.collect()
+        torch.cuda.empty_cache()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        index = mrpt.grow_trees(src, p["n_trees"], p["depth"], p["sparsity"], seed=0)
+        index = mrpt.grow_trees(src, p["n_trees"], p["depth"], p["sparsity"], seed=0, batch_trees=tb)
         torch.cuda.synchronize()
         ts.append(time.perf_counter() - t0)
     D = index.device_index()
