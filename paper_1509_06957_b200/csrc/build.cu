@@ -283,44 +283,15 @@ __global__ void k_chunk_fill(LevelArgs a) {
   }
 }
 
-// One CTA per segment with m <= MAXM: keys (and, with IDS, the ids) staged in
-// shared memory, exact radix select there, stable partition by warp ranges.
-//  * load: every thread issues U id loads, then U projection gathers, before
-//    any key is stored (two memory round trips per U*NT elements);
-//  * partition: warp w owns a contiguous range of positions, counts its
-//    left-goers by ballots, one barrier publishes the warp totals, then every
-//    warp writes its range at its ranks (lanes consecutive: the left and the
-//    right runs are both coalesced).
-template <int MAXM, int NT, int NB, bool IDS>
-__device__ __forceinline__ void seg_cta(const LevelArgs &a, int t, int s, int64_t b, int64_t e,
-                                        uint32_t *keys, int32_t *ids, uint32_t *hist,
-                                        uint32_t *red, int *sh) {
+// Exact rank select over m keys staged in shared memory: K = the kth
+// smallest key (0-based), nle = the number of keys <= K; every thread gets
+// both.  mn / mx: the calling thread's partial min / max of the keys it
+// stored (the first barrier inside also publishes the keys).
+template <int NT, int NB>
+__device__ __forceinline__ void cta_select(const uint32_t *keys, int m, int kth, uint32_t mn, uint32_t mx,
+                                           uint32_t *hist, uint32_t *red, int *sh, uint32_t &Kout, int &nle_out) {
   constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int m = (int)(e - b);
-  const float *Pc = a.P + ((int64_t)t * a.depth + a.lev) * a.n;
-  const int32_t *oin = a.order_in + (int64_t)t * a.n + b;
-  int32_t *oout = a.order_out + (int64_t)t * a.n + b;
-  uint32_t mn = 0xffffffffu, mx = 0u;
-  constexpr int U = 8;
-  for (int i0 = tid; i0 < m; i0 += U * NT) {
-    int32_t id[U];
-#pragma unroll
-    for (int j = 0; j < U; ++j) id[j] = i0 + j * NT < m ? __ldg(oin + i0 + j * NT) : -1;
-    float v[U];
-#pragma unroll
-    for (int j = 0; j < U; ++j) v[j] = id[j] >= 0 ? __ldg(Pc + id[j]) : 0.f;
-#pragma unroll
-    for (int j = 0; j < U; ++j) {
-      if (id[j] >= 0) {
-        const uint32_t k = f2key(v[j]);
-        keys[i0 + j * NT] = k;
-        if (IDS) ids[i0 + j * NT] = id[j];
-        mn = k < mn ? k : mn;
-        mx = k > mx ? k : mx;
-      }
-    }
-  }
   // block min / max (the barrier also publishes keys / ids)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -344,7 +315,6 @@ __device__ __forceinline__ void seg_cta(const LevelArgs &a, int t, int s, int64_
     mn = x;
     mx = y;
   }
-  const int kth = (m + 1) / 2 - 1;
   uint32_t K = mn;
   int nle = m;
   bool solved = mn == mx;
@@ -464,6 +434,51 @@ __device__ __forceinline__ void seg_cta(const LevelArgs &a, int t, int s, int64_
     K = prefix;
     nle = kth - krem + cnt_last;
   }
+  Kout = K;
+  nle_out = nle;
+}
+
+// One CTA per segment with m <= MAXM: keys (and, with IDS, the ids) staged in
+// shared memory, exact radix select there, stable partition by warp ranges.
+//  * load: every thread issues U id loads, then U projection gathers, before
+//    any key is stored (two memory round trips per U*NT elements);
+//  * partition: warp w owns a contiguous range of positions, counts its
+//    left-goers by ballots, one barrier publishes the warp totals, then every
+//    warp writes its range at its ranks (lanes consecutive: the left and the
+//    right runs are both coalesced).
+template <int MAXM, int NT, int NB, bool IDS>
+__device__ __forceinline__ void seg_cta(const LevelArgs &a, int t, int s, int64_t b, int64_t e,
+                                        uint32_t *keys, int32_t *ids, uint32_t *hist,
+                                        uint32_t *red, int *sh) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int m = (int)(e - b);
+  const float *Pc = a.P + ((int64_t)t * a.depth + a.lev) * a.n;
+  const int32_t *oin = a.order_in + (int64_t)t * a.n + b;
+  int32_t *oout = a.order_out + (int64_t)t * a.n + b;
+  uint32_t mn = 0xffffffffu, mx = 0u;
+  constexpr int U = 8;
+  for (int i0 = tid; i0 < m; i0 += U * NT) {
+    int32_t id[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) id[j] = i0 + j * NT < m ? __ldg(oin + i0 + j * NT) : -1;
+    float v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) v[j] = id[j] >= 0 ? __ldg(Pc + id[j]) : 0.f;
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      if (id[j] >= 0) {
+        const uint32_t k = f2key(v[j]);
+        keys[i0 + j * NT] = k;
+        if (IDS) ids[i0 + j * NT] = id[j];
+        mn = k < mn ? k : mn;
+        mx = k > mx ? k : mx;
+      }
+    }
+  }
+  uint32_t K;
+  int nle;
+  cta_select<NT, NB>(keys, m, (m + 1) / 2 - 1, mn, mx, hist, red, sh, K, nle);
   // stable partition by warp ranges
   int *wtot = sh + 4;
   const int R = ((m + NW - 1) / NW + 31) & ~31;
@@ -529,6 +544,10 @@ __global__ void __launch_bounds__(NT) k_seg_cta(LevelArgs a, int lo, int hi, boo
     seg_cta<MAXM, NT, NB, IDS>(a, t, s, b, e, keys, ids, hist, red, sh);
   }
 }
+
+}  // namespace mrpt
+#include "build_top.cuh"
+namespace mrpt {
 
 // ---- big path -------------------------------------------------------------
 __global__ void __launch_bounds__(kNT) k_big_keys(LevelArgs a) {
@@ -900,10 +919,20 @@ __global__ void __launch_bounds__(kNT) k_big_scatter(LevelArgs a) {
 
 // ---------------------------------------------------------------------------
 struct WsLayout {
-  size_t order_tmp, bounds_tmp, keys, ctl, tiny, mid, big, ghist, chunks, cleft, coff, tnch, tbase, tlbase, llist, total;
+  size_t order_tmp, bounds_tmp, keys, ctl, tiny, mid, big, ghist, chunks, cleft, coff, tnch, tbase, tlbase, llist;
+  size_t tnode, tsize, tk, tinfo, tfill, thist, trange, ttable, total;
 };
 
 static size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
+
+// Levels taken by the top path (build_top.cuh): while the expected node size
+// exceeds the one-CTA classes, at most kTopMaxLev.
+static int top_levels(int64_t n, int depth) {
+  if (n <= kLargeMax) return 0;
+  int L = 0;
+  while (L < depth && L < kTopMaxLev && (n >> L) > kMidMax) ++L;
+  return L;
+}
 
 static WsLayout layout(int64_t n, int Tb, int depth) {
   WsLayout L;
@@ -931,6 +960,16 @@ static WsLayout layout(int64_t n, int Tb, int depth) {
   L.tbase = off; off = align_up(off + sizeof(int64_t) * (size_t)Tb);
   L.tlbase = off; off = align_up(off + sizeof(int64_t) * (size_t)Tb);
   L.llist = off; off = align_up(off + sizeof(int32_t) * ((size_t)Tb * large_per_tree + 1));
+  const int Lc = top_levels(n, depth);
+  const int64_t nrun = ceil_div<int64_t>(n, kTopBlk);
+  L.tnode = off; off = align_up(off + (Lc ? sizeof(uint16_t) * (size_t)Tb * n : 0));
+  L.tsize = off; off = align_up(off + (Lc ? sizeof(int32_t) * (size_t)Tb * 4 * kTopNodes : 0));
+  L.tk = off; off = align_up(off + (Lc ? sizeof(uint32_t) * (size_t)Tb * kTopNodes : 0));
+  L.tinfo = off; off = align_up(off + (Lc ? sizeof(int4) * (size_t)Tb * kTopNodes : 0));
+  L.tfill = off; off = align_up(off + (Lc ? sizeof(int32_t) * (size_t)Tb * kTopNodes : 0));
+  L.thist = off; off = align_up(off + (Lc ? sizeof(uint32_t) * (size_t)Tb * kTopBins : 0));
+  L.trange = off; off = align_up(off + (Lc ? sizeof(float2) * (size_t)Tb * depth : 0));
+  L.ttable = off; off = align_up(off + (Lc ? sizeof(int32_t) * (size_t)Tb * nrun * ((size_t)1 << kTopDigit) : 0));
   L.total = off;
   return L;
 }
@@ -975,13 +1014,76 @@ extern "C" int32_t mrpt_build_levels(const float *P, int64_t n, int32_t Tb, int3
   obuf[(depth + 1) & 1] = reinterpret_cast<int32_t *>(w + L.order_tmp);
   bbuf[depth & 1] = leaf_offsets;
   bbuf[(depth + 1) & 1] = reinterpret_cast<int64_t *>(w + L.bounds_tmp);
-  {
+  const int sms = num_sms();
+  int Lc = top_levels(n, depth);
+  if (const char *e = getenv("MRPT_BUILD_TOP"))  // experiments: "0" = every level through the permutation
+    if (atoi(e) == 0) Lc = 0;
+  if (Lc == 0) {
     const int64_t total = (int64_t)Tb * n;
     const int64_t blocks = ceil_div<int64_t>(total, 256);
     const int grid = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
     (count_launch(), k_build_init<<<grid, 256, 0, s>>>(obuf[0], bbuf[0], n, Tb, bstride));
+  } else {
+    TopArgs ta;
+    ta.P = P;
+    ta.n = n;
+    ta.depth = depth;
+    ta.Tb = Tb;
+    ta.Lc = Lc;
+    ta.node = reinterpret_cast<uint16_t *>(w + L.tnode);
+    ta.tsize = reinterpret_cast<int32_t *>(w + L.tsize);
+    ta.tK = reinterpret_cast<uint32_t *>(w + L.tk);
+    ta.tinfo = reinterpret_cast<int4 *>(w + L.tinfo);
+    ta.tfill = reinterpret_cast<int32_t *>(w + L.tfill);
+    ta.ghist = reinterpret_cast<uint32_t *>(w + L.thist);
+    ta.colrange = reinterpret_cast<float2 *>(w + L.trange);
+    ta.lists = reinterpret_cast<uint32_t *>(w + L.keys);  // the chunked path's key buffer is free here
+    ta.table = reinterpret_cast<int32_t *>(w + L.ttable);
+    ta.sid = obuf[(Lc + 1) & 1];                                  // the other order buffer, unused so far
+    ta.snode = reinterpret_cast<uint16_t *>(w + L.keys);         // after the last select the lists are dead
+    ta.nrun = ceil_div<int64_t>(n, kTopBlk);
+    ta.splits = splits;
+    ta.sstride = nleaf - 1;
+    ta.bounds = bbuf[Lc & 1];
+    ta.bstride = bstride;
+    ta.order = obuf[Lc & 1];
+    ta.lev = 0;
+    ta.NB = kTopMaxNB;
+    cudaFuncSetAttribute(k_top_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kTopBins * 4);
+    cudaFuncSetAttribute(k_top_select<kTopListLarge, 1024, 2048>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kTopListLarge * 4);
+    cudaFuncSetAttribute(k_top_collect, cudaFuncAttributeMaxDynamicSharedMemorySize, kTopBuf * 8);
+    const unsigned nchunk = (unsigned)ceil_div<int64_t>(n, kTopChunk);
+    (count_launch(), k_top_range<<<(unsigned)(Tb * depth), 256, 0, s>>>(ta));
+    (count_launch(), k_top_init<<<(unsigned)ceil_div<int64_t>((int64_t)Tb * kTopBins, 256), 256, 0, s>>>(ta));
+    for (int lev = 0; lev < Lc; ++lev) {
+      ta.lev = lev;
+      ta.NB = (kTopBins >> lev) < kTopMaxNB ? (kTopBins >> lev) : kTopMaxNB;
+      const dim3 gchunk(nchunk, (unsigned)Tb), gnode(1u << lev, (unsigned)Tb);
+      (count_launch(), k_top_hist<<<gchunk, 1024, (size_t)(ta.NB << lev) * 4, s>>>(ta));
+      (count_launch(), k_top_pick<<<(unsigned)Tb, 1024, 0, s>>>(ta));
+      (count_launch(), k_top_collect<<<gchunk, 1024, kTopBuf * 8, s>>>(ta));
+      (count_launch(), k_top_select<kTopListSmall, 256, 512><<<gnode, 256, kTopListSmall * 4, s>>>(ta, -1, kTopListSmall));
+      (count_launch(), k_top_select<kTopListLarge, 1024, 2048><<<gnode, 1024, kTopListLarge * 4, s>>>(
+          ta, kTopListSmall, kTopListLarge));
+      (count_launch(), k_top_select_huge<<<gnode, 1024, 0, s>>>(ta, kTopListLarge));
+    }
+    const dim3 grun((unsigned)ta.nrun, (unsigned)Tb);
+    const size_t gsmem = (size_t)kTopBlk * 6;
+    cudaFuncSetAttribute(k_top_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem);
+    cudaFuncSetAttribute(k_top_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem);
+    // stable grouping by node: low kTopDigit bits, then the rest
+    const int bitsA = Lc < kTopDigit ? Lc : kTopDigit, bitsB = Lc - bitsA;
+    (count_launch(), k_top_count<true><<<grun, 512, 0, s>>>(ta, 0, bitsA));
+    (count_launch(), k_top_scan<<<(unsigned)Tb, 1 << kTopDigit, 0, s>>>(ta, bitsA));
+    (count_launch(), k_top_bounds<<<(unsigned)Tb, 1024, 0, s>>>(ta));
+    (count_launch(), k_top_scatter<true><<<grun, 512, gsmem, s>>>(ta, 0, bitsA, bitsB == 0));
+    if (bitsB > 0) {
+      (count_launch(), k_top_count<false><<<grun, 512, 0, s>>>(ta, bitsA, bitsB));
+      (count_launch(), k_top_scan<<<(unsigned)Tb, 1 << kTopDigit, 0, s>>>(ta, bitsB));
+      (count_launch(), k_top_scatter<false><<<grun, 512, gsmem, s>>>(ta, bitsA, bitsB, 1));
+    }
   }
-  const int sms = num_sms();
   cudaFuncSetAttribute(k_seg_cta<kMidMax, 256, 1024, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMidMax * 4);
   cudaFuncSetAttribute(k_seg_cta<kLargeMax, 1024, 2048, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLargeMax * 4);
   cudaFuncSetAttribute(k_seg_cta<kLargeMax2, 1024, 2048, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLargeMax2 * 4);
@@ -990,7 +1092,7 @@ extern "C" int32_t mrpt_build_levels(const float *P, int64_t n, int32_t Tb, int3
     const int v = e ? atoi(e) : kLargeMax;
     return v >= kLargeMax ? kLargeMax : (v >= kLargeMax2 ? kLargeMax2 : kMidMax);
   }();
-  for (int lev = 0; lev < depth; ++lev) {
+  for (int lev = Lc; lev < depth; ++lev) {
     LevelArgs a;
     a.P = P;
     a.n = n;

@@ -520,8 +520,9 @@ def _resolve_threads(threads):
 
 def _batch_trees(n, d, depth, T, free_bytes):
     """Trees per K1+K5 batch: projections (depth*n*4) + keys + scratch order
-    (8n) per tree, within half of the free memory."""
-    per_tree = n * (4 * depth + 8) + 4096
+    (8n) + top-level scratch per tree, within half of the free memory."""
+    # + the top levels' node ids (2n) and per-run node tables (<= n/2) and fixed tables
+    per_tree = n * (4 * depth + 8) + 3 * n + (1 << 20)
     tb = max(1, int(0.5 * free_bytes) // per_tree)
     tb = min(tb, T, 128)
     while tb > 1 and tb * (1 << depth) >= (1 << 31):

@@ -105,12 +105,19 @@ def test_projection_bit_identical(rng, monkeypatch, n, d, depth, a, ppt):
     (60_000, 16, 2, 9, "ints"),          # heavy ties through the big path
     (40_000, 8, 2, 6, "ones"),           # all keys equal in a big segment
     (20_000, 32, 4, 12, "gauss"),        # tiny leaves (~5 points)
+    (100_000, 8, 2, 7, "ones"),          # top levels: one value, lists beyond shared memory
+    (120_001, 4, 2, 8, "tail"),          # top levels: bucket range sampled from a constant prefix
+    (150_000, 16, 2, 11, "ints"),        # top levels with heavy ties, then the per-segment kernels
+    (70_000, 6, 3, 5, "gauss"),          # every level on the top path
 ])
 def test_build_matches_oracle_large(rng, n, d, T, depth, gen):
     if gen == "gauss":
         X = gaussian(rng, n, d)
     elif gen == "ints":
         X = rng.integers(0, 3, size=(n, d)).astype(np.float32)
+    elif gen == "tail":
+        X = gaussian(rng, n, d)
+        X[:70_000] = 0.25
     else:
         X = np.ones((n, d), dtype=np.float32)
     index = mrpt.grow_trees(X, T, depth, seed=17)
