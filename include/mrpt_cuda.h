@@ -350,7 +350,23 @@ int32_t mrpt_vote_stream(const uint32_t *qs, int64_t tstride, const uint16_t *qd
  *            tree row), tree_pairs (T int64: pairs per tree row).
  *   _fill:   ps (T * pstride pairs of 8 uint32), pstride >= max tree_pairs,
  *            64 * pstride < 2^31.
- *   mrpt_vote_pair: candidate lists like mrpt_vote_stream. */
+ *   mrpt_vote_pair: candidate lists like mrpt_vote_stream.
+ * Counter width: where max_count > 255 and 8-bit counters need fewer pairs
+ * of id tiles than 10/16-bit ones (large n), the counters are 8 bits wide
+ * and SATURATE: a counter reaching 192 is pulled back by 64 by the
+ * increment that saw 192, so it never returns below v (v <= 128 required,
+ * see mrpt_vote_pair_max_votes; larger v is served by mrpt_vote) and each
+ * id reaching v votes is still listed exactly once (_cy.pyx:75-77).  An
+ * increment that would wrap a counter (it read 255) flags its query, which
+ * the same launch then redoes with check-before-increment bumps that cannot
+ * wrap -- results are exact either way; mrpt_vote_stats counts the redos.
+ * MRPT_VOTE_SAT=0 (environment, read per call; set before the layout is
+ * built) keeps 10/16-bit counters instead. */
+int32_t mrpt_vote_pair_max_votes(int64_t n, int32_t T, int64_t max_count,
+                                 int32_t *max_votes /* host */);
+/* out (host, 2 int64): queries voted with saturating counters, queries
+ * redone exactly after a counter wrapped.  Synchronises; reset != 0 clears. */
+int32_t mrpt_vote_stats(int64_t *out /* host */, int32_t reset);
 int32_t mrpt_vote_pair_plan(int64_t n, int32_t T, int32_t depth, int64_t max_count,
                             int32_t *ntiles /* host */, int64_t *pos_entries /* host */,
                             int64_t *dir_entries /* host */);

@@ -42,6 +42,8 @@ SIGNATURES = {
                               _c_p],
     "mrpt_vote_stream": [_c_p, _c_i64, _c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_i64, _c_p, _c_i64,
                          _c_i32, _c_p, _c_i64, _c_p, _c_p],
+    "mrpt_vote_pair_max_votes": [_c_i64, _c_i32, _c_i64, ctypes.POINTER(_c_i32)],
+    "mrpt_vote_stats": [ctypes.POINTER(_c_i64), _c_i32],
     "mrpt_vote_pair_plan": [_c_i64, _c_i32, _c_i32, _c_i64, ctypes.POINTER(_c_i32),
                             ctypes.POINTER(_c_i64), ctypes.POINTER(_c_i64)],
     "mrpt_vote_pair_layout": [_c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_p,

@@ -15,6 +15,7 @@
 // the order that lets concurrent queries sweep X through L2 together).
 // Groups of G lanes share one tree slice (G ~ mean slice length per tile)
 // and each lane keeps U loads in flight.
+#include <atomic>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -1255,9 +1256,24 @@ __device__ __forceinline__ void ld_pair_l2_256(const uint4 *p, uint4 &a, uint4 &
 
 // Bump the 7 counters of one quad; the increment that lifts a count to v
 // appends the id (_cy.pyx:75-77).
-template <int CW>
+// Saturating 8-bit counters (SAT): counts above 255 are possible (T up to
+// 1024) but only the crossing of v matters, so a counter that reaches
+// kSatTrig is pulled back by kSatSub -- by the one increment that saw exactly
+// kSatTrig -- and stays in [kSatTrig - kSatSub + 1, 255]: above v - 1 (v <=
+// kSatMaxV), so no id is listed twice.  Should increments outrun a pull-back
+// and wrap a counter, the increment that wraps it sees 255 and raises the
+// query's overflow flag; the query is then redone by vote_pair_careful.
+// Either way every id whose count reaches v is listed exactly once
+// (_cy.pyx:75-77).
+// Queries redone by vote_pair_careful (mrpt_vote_stats; measurement only).
+__device__ unsigned long long g_vote_sat_redos;
+
+constexpr uint32_t kSatTrig = 192, kSatSub = 64;
+constexpr int kSatMaxV = 128;
+
+template <int CW, bool SAT = false>
 __device__ __forceinline__ void pair_bump(uint4 cur, uint32_t cnt_s, uint32_t nc_s, uint32_t pad_word, uint32_t vm1,
-                                          int32_t lo, int32_t *qcand, int cap32) {
+                                          int32_t lo, int32_t *qcand, int cap32, uint32_t ovf_s = 0) {
   constexpr uint32_t MASK = CW == 1 ? 0xffu : (CW == 3 ? 0x3ffu : (CW == 2 ? 0xffffu : 0xffffffffu));
   constexpr int PER = lanes_per_word<CW>();
   constexpr int LB = lane_bits<CW>();
@@ -1265,16 +1281,102 @@ __device__ __forceinline__ void pair_bump(uint4 cur, uint32_t cnt_s, uint32_t nc
                                  cur.z & 0xffffu, cur.z >> 16, cur.w & 0xffffu};
   const uint32_t fb = cur.w >> 16;
   uint32_t old[kQuadIds];
+  // an all-padding quad (pieces pad at their end; window tails): its lane sits
+  // out, so the others' atomics meet fewer bank conflicts
+  if (wd[0] >= pad_word) return;
 #pragma unroll
   for (int c = 0; c < kQuadIds; ++c) old[c] = atom_add_shared(cnt_s + 4u * wd[c], 1u << (((fb >> (2 * c)) & 3u) * LB));
 #pragma unroll
   for (int c = 0; c < kQuadIds; ++c) {
     const uint32_t f = (fb >> (2 * c)) & 3u;
-    if (((old[c] >> (f * LB)) & MASK) == vm1 && wd[c] < pad_word) {  // lifted a count to v
+    const uint32_t fld = (old[c] >> (f * LB)) & MASK;
+    if (SAT) {
+      // Padding entries are not excluded up front: their spare words are
+      // pulled back like any counter, so they too sit below kSatTrig and
+      // this branch stays rare (tested for padding inside instead).
+      if (fld == vm1 || fld >= kSatTrig) {
+        if (fld == vm1) {
+          if (wd[c] < pad_word) {  // lifted a count to v
+            const int pos = (int)atom_add_shared(nc_s, 1u);
+            if (pos < cap32) qcand[pos] = lo + (int)(wd[c] * PER + f);
+          }
+        } else if (fld == kSatTrig) {
+          atom_add_shared(cnt_s + 4u * wd[c], 0u - (kSatSub << (f * LB)));
+        } else if (fld == MASK && wd[c] < pad_word) {
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(ovf_s), "r"(1u) : "memory");
+        }
+      }
+    } else if (fld == vm1 && wd[c] < pad_word) {  // lifted a count to v
       const int pos = (int)atom_add_shared(nc_s, 1u);
       if (pos < cap32) qcand[pos] = lo + (int)(wd[c] * PER + f);
     }
   }
+}
+
+// The exact redo of one query after a counter overflow of the saturating
+// vote (never seen on the benchmark configurations; MRPT_VOTE_DBG=8 forces
+// it for the tests).  Warp 0 alone bumps, every lane walking its own tree's
+// piece, and an increment is made only while the counter read just before is
+// below v: between that read and the increment at most the other 31 lanes
+// of the same instruction add to the counter, so it stays below v + 32 <= 160
+// and cannot wrap.  The other warps only help clearing.
+__device__ __noinline__ void vote_pair_careful(const VoteArgs &a, const uint4 *__restrict__ ps,
+                                               const int32_t *__restrict__ pbase, int64_t pstride, int64_t q,
+                                               uint32_t *cnt, int cwords, int *s_nc) {
+  constexpr int PER = 4;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nsup = (a.ntiles + 1) >> 1;
+  const int64_t dstride = nsup + 1;
+  const uint32_t pad_word = (uint32_t)cwords, v = (uint32_t)a.v;
+  const int cap32 = a.cap < 0x7fffffff ? (int)a.cap : 0x7fffffff;
+  int32_t *qcand = a.cand + q * a.cap;
+  uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
+  if (tid == 0) *s_nc = 0;
+  for (int w = 0; w < a.ntiles; ++w) {
+    __syncthreads();
+    for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
+    if (warp != 0) continue;
+    const int j = w >> 1, side = w & 1;
+    const int32_t lo = w * a.W;
+    for (int g = 0; g < 32; ++g) {
+      const int t_lo = (int)(((int64_t)g * a.T) / 32), t_hi = (int)(((int64_t)(g + 1) * a.T) / 32);
+      const int t = t_lo + lane;
+      int len = 0;
+      const uint4 *src = nullptr;
+      if (t < t_hi) {
+        const int64_t gl = (int64_t)t * a.L + a.leaves[q * a.T + t];
+        const uint16_t *dl = a.dir + gl * dstride;
+        const int start = dl[j];
+        len = (int)dl[j + 1] - start;
+        src = ps + 2 * ((int64_t)t * pstride + pbase[gl] + start) + side;
+      }
+      const int maxlen = __reduce_max_sync(0xffffffffu, len);
+      for (int p = 0; p < maxlen; ++p) {
+        uint4 cur = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0x0000ffffu);  // all padding
+        if (p < len) cur = __ldg(src + 2 * p);
+        const uint32_t wd[kQuadIds] = {cur.x & 0xffffu, cur.x >> 16, cur.y & 0xffffu, cur.y >> 16,
+                                       cur.z & 0xffffu, cur.z >> 16, cur.w & 0xffffu};
+        const uint32_t fb = cur.w >> 16;
+#pragma unroll 1
+        for (int c = 0; c < kQuadIds; ++c) {
+          __syncwarp();  // the previous round's increments are visible to every lane
+          const uint32_t sh = ((fb >> (2 * c)) & 3u) * 8u;
+          if (wd[c] < pad_word) {
+            volatile uint32_t *word = cnt + wd[c];
+            if (((*word >> sh) & 0xffu) < v) {
+              const uint32_t old = atomicAdd(const_cast<uint32_t *>(word), 1u << sh);
+              if (((old >> sh) & 0xffu) == v - 1u) {
+                const int pos = atomicAdd(s_nc, 1);
+                if (pos < cap32) qcand[pos] = lo + (int)(wd[c] * PER + (sh >> 3));
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
 }
 
 __device__ __forceinline__ void tmem_st4(uint32_t taddr, uint4 v) {
@@ -1304,7 +1406,7 @@ constexpr int kPairSlots = 16;  // stashed windows per warp (4 TMEM columns each
 // 16 windows of 4 columns); after the tile barrier and clearing, phase B
 // bumps the parked quads into tile 2j+1's counters.  Windows past the 16th
 // re-read their pair in phase B.  The counts are those of k_vote_stream.
-template <int CW>
+template <int CW, bool SAT = false>
 __global__ void __launch_bounds__(1024, 1) k_vote_pair(VoteArgs a, const uint4 *__restrict__ ps,
                                                        const int32_t *__restrict__ pbase, int64_t pstride) {
   extern __shared__ uint4 vote_smem[];
@@ -1316,11 +1418,13 @@ __global__ void __launch_bounds__(1024, 1) k_vote_pair(VoteArgs a, const uint4 *
   constexpr int NW = 32;
   __shared__ uint32_t w_off[NW][32];
   __shared__ int s_nc;
-  __shared__ uint32_t s_tmem;
+  __shared__ uint32_t s_tmem, s_ovf;
   const uint32_t vm1 = (uint32_t)(a.v - 1);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t nc_s = (uint32_t)__cvta_generic_to_shared(&s_nc);
   asm volatile("" : "+r"(nc_s));
+  uint32_t ovf_s = (uint32_t)__cvta_generic_to_shared(&s_ovf);
+  asm volatile("" : "+r"(ovf_s));
   const int cap32 = a.cap < 0x7fffffff ? (int)a.cap : 0x7fffffff;
   const int nsup = (a.ntiles + 1) >> 1;
   const int64_t dstride = nsup + 1;
@@ -1345,6 +1449,9 @@ __global__ void __launch_bounds__(1024, 1) k_vote_pair(VoteArgs a, const uint4 *
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tslot = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+  auto clear_counters = [&]() {
+    for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+  };
   for (int64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
     const uint16_t *dl = nullptr;
     uint32_t lbase = 0;
@@ -1380,8 +1487,11 @@ __global__ void __launch_bounds__(1024, 1) k_vote_pair(VoteArgs a, const uint4 *
     };
     uint4 rA, rB;
     if (sw.windows() > 0) next_pair(rA, rB);
-    for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(0u, 0u, 0u, 0u);
-    if (tid == 0) s_nc = 0;
+    clear_counters();
+    if (tid == 0) {
+      s_nc = 0;
+      s_ovf = (SAT && (a.dbg & 8)) ? 1u : 0u;
+    }
     __syncthreads();
     for (int j = 0; j < nsup; ++j) {
       const bool hasB = 2 * j + 1 < a.ntiles;
@@ -1392,23 +1502,23 @@ __global__ void __launch_bounds__(1024, 1) k_vote_pair(VoteArgs a, const uint4 *
         const uint4 cA = rA, cB = rB;
         if (i + 1 < nwin) next_pair(rA, rB);
         if (hasB && i < kPairSlots) tmem_st4(tslot + 4u * (uint32_t)i, cB);
-        pair_bump<CW>(cA, cnt_s, nc_s, pad_word, vm1, loA, qcand, cap32);
+        pair_bump<CW, SAT>(cA, cnt_s, nc_s, pad_word, vm1, loA, qcand, cap32, ovf_s);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       __syncthreads();
-      for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+      clear_counters();
       __syncthreads();
       // phase B: tile 2j+1 from the parked quads (windows past the parked
       // ones re-read from the stream)
       if (hasB) {
         const int nst = nwin < kPairSlots ? nwin : kPairSlots;
-        for (int i = 0; i < nst; ++i) pair_bump<CW>(tmem_ld4(tslot + 4u * (uint32_t)i), cnt_s, nc_s, pad_word, vm1, loB, qcand, cap32);
+        for (int i = 0; i < nst; ++i) pair_bump<CW, SAT>(tmem_ld4(tslot + 4u * (uint32_t)i), cnt_s, nc_s, pad_word, vm1, loB, qcand, cap32, ovf_s);
         if (nwin > kPairSlots) {
           sw.begin(dnxt - dcur, lbase + (uint32_t)dcur, woff);  // same super-tile again
           for (int i = 0; i < nwin; ++i) {
             uint4 xA, xB;
             next_pair(xA, xB);
-            if (i >= kPairSlots) pair_bump<CW>(xB, cnt_s, nc_s, pad_word, vm1, loB, qcand, cap32);
+            if (i >= kPairSlots) pair_bump<CW, SAT>(xB, cnt_s, nc_s, pad_word, vm1, loB, qcand, cap32, ovf_s);
           }
         }
       }
@@ -1423,11 +1533,15 @@ __global__ void __launch_bounds__(1024, 1) k_vote_pair(VoteArgs a, const uint4 *
       if (hasB) {
         __syncthreads();
         if (j + 1 < nsup)
-          for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+          clear_counters();
         __syncthreads();
       }
     }
     __syncthreads();
+    if (SAT && s_ovf) {  // CTA-uniform: a counter wrapped, redo the query exactly
+      if (tid == 0) atomicAdd(&g_vote_sat_redos, 1ull);
+      vote_pair_careful(a, ps, pbase, pstride, q, cnt, cwords, &s_nc);
+    }
     if (tid == 0) a.ncand[q] = s_nc;  // > cap means only cap ids were stored
     __syncthreads();
   }
@@ -1732,9 +1846,25 @@ extern "C" int32_t mrpt_unique_ids(const int64_t *cand, int64_t m, int64_t n, ui
 // ------------------------------------------------------------ streamed vote --
 static const int kVoteSmemStream = 218 * 1024;  // counters only (the rank tables are static)
 
-static int32_t stream_geometry(int64_t n, int32_t T, int64_t max_count, int *CWo, int64_t *Wo, int *ntiles_o) {
+// sat_ok (the paired vote): counts above 255 still use 8-bit counters, which
+// then saturate instead of counting on (k_vote_pair, SAT) -- a quarter fewer
+// id tiles than 10-bit counters.  MRPT_VOTE_SAT=0 keeps the wide counters.
+static bool vote_sat_enabled() {
+  const char *e = getenv("MRPT_VOTE_SAT");
+  return !(e && e[0] == '0');
+}
+
+static int32_t stream_geometry(int64_t n, int32_t T, int64_t max_count, int *CWo, int64_t *Wo, int *ntiles_o,
+                               bool sat_ok = false, bool *sat_o = nullptr) {
   if (T < 1 || T > 1024) return fail(MRPT_EPARAM, "streamed vote: needs 1 <= T <= 1024");
-  const int CW = max_count <= 255 ? 1 : (max_count <= 1023 ? 3 : (max_count <= 65535 ? 2 : 4));
+  int CW = max_count <= 255 ? 1 : (max_count <= 1023 ? 3 : (max_count <= 65535 ? 2 : 4));
+  const int64_t words0 = ((kVoteSmemStream - 128) / 4) & ~3LL;
+  // saturating 8-bit counters only where they save super-tiles (pairs of id tiles)
+  const int64_t nsup_wide = (ceil_div<int64_t>(n, words0 * (CW == 3 ? 3 : (CW == 2 ? 2 : 1))) + 1) / 2;
+  const int64_t nsup_sat = (ceil_div<int64_t>(n, words0 * 4) + 1) / 2;
+  const bool sat = sat_ok && CW != 1 && vote_sat_enabled() && nsup_sat < nsup_wide;
+  if (sat) CW = 1;
+  if (sat_o) *sat_o = sat;
   const int per = CW == 1 ? 4 : (CW == 3 ? 3 : (CW == 2 ? 2 : 1));
   const int64_t words = ((kVoteSmemStream - 128) / 4) & ~3LL;
   int64_t W = words * per;
@@ -1852,6 +1982,37 @@ extern "C" int32_t mrpt_vote_stream(const uint32_t *qs, int64_t tstride, const u
 }
 
 // ------------------------------------------------------- paired vote (host) --
+// Queries voted with saturating counters (host count; redone ones: g_vote_sat_redos).
+static std::atomic<long long> g_vote_sat_queries{0};
+
+extern "C" int32_t mrpt_vote_pair_max_votes(int64_t n, int32_t T, int64_t max_count, int32_t *max_votes) {
+  clear_error();
+  if (!max_votes) return fail(MRPT_EPARAM, "mrpt_vote_pair_max_votes: NULL output");
+  int CW, nt;
+  int64_t W;
+  bool sat = false;
+  const int32_t st = stream_geometry(n, T, max_count, &CW, &W, &nt, true, &sat);
+  if (st) return st;
+  *max_votes = sat ? kSatMaxV : (int32_t)(max_count < 0x7fffffff ? max_count : 0x7fffffff);
+  return MRPT_OK;
+}
+
+extern "C" int32_t mrpt_vote_stats(int64_t *out, int32_t reset) {
+  clear_error();
+  if (!out) return fail(MRPT_EPARAM, "mrpt_vote_stats: out is NULL");
+  unsigned long long redo = 0;
+  if (cudaMemcpyFromSymbol(&redo, g_vote_sat_redos, sizeof(redo)) != cudaSuccess)
+    return launch_status("mrpt_vote_stats");
+  out[0] = g_vote_sat_queries.load();
+  out[1] = (int64_t)redo;
+  if (reset) {
+    const unsigned long long z = 0;
+    cudaMemcpyToSymbol(g_vote_sat_redos, &z, sizeof(z));
+    g_vote_sat_queries.store(0);
+  }
+  return launch_status("mrpt_vote_stats");
+}
+
 extern "C" int32_t mrpt_vote_pair_plan(int64_t n, int32_t T, int32_t depth, int64_t max_count, int32_t *ntiles,
                                        int64_t *pos_entries, int64_t *dir_entries) {
   clear_error();
@@ -1859,7 +2020,8 @@ extern "C" int32_t mrpt_vote_pair_plan(int64_t n, int32_t T, int32_t depth, int6
     return fail(MRPT_ESHAPE, "mrpt_vote_pair_plan: bad arguments");
   int CW, nt;
   int64_t W;
-  const int32_t st = stream_geometry(n, T, max_count, &CW, &W, &nt);
+  bool sat = false;
+  const int32_t st = stream_geometry(n, T, max_count, &CW, &W, &nt, true, &sat);
   if (st) return st;
   *ntiles = nt;
   *pos_entries = (int64_t)T * ((int64_t)1 << depth) * (nt + 1);
@@ -1873,7 +2035,8 @@ extern "C" int32_t mrpt_vote_pair_layout(const int32_t *leaf_indices, const int6
   clear_error();
   int CW, nt;
   int64_t W;
-  const int32_t st = stream_geometry(n, T, max_count, &CW, &W, &nt);
+  bool sat = false;
+  const int32_t st = stream_geometry(n, T, max_count, &CW, &W, &nt, true, &sat);
   if (st) return st;
   cudaStream_t s = as_stream(stream);
   const int64_t nleaves = (int64_t)T << depth;
@@ -1891,7 +2054,8 @@ extern "C" int32_t mrpt_vote_pair_fill(const int32_t *leaf_indices, const int64_
   clear_error();
   int CW, nt;
   int64_t W;
-  const int32_t st = stream_geometry(n, T, max_count, &CW, &W, &nt);
+  bool sat = false;
+  const int32_t st = stream_geometry(n, T, max_count, &CW, &W, &nt, true, &sat);
   if (st) return st;
   if (pstride < 0 || 64 * pstride >= ((int64_t)1 << 31))
     return fail(MRPT_EPARAM, "mrpt_vote_pair_fill: tree stride too large");
@@ -1919,8 +2083,11 @@ extern "C" int32_t mrpt_vote_pair(const uint32_t *ps, int64_t pstride, const uin
   if (64 * pstride >= ((int64_t)1 << 31)) return fail(MRPT_EPARAM, "mrpt_vote_pair: tree stride too large");
   int CW, nt;
   int64_t W;
-  const int32_t st = stream_geometry(n, T, max_count, &CW, &W, &nt);
+  bool sat = false;
+  const int32_t st = stream_geometry(n, T, max_count, &CW, &W, &nt, true, &sat);
   if (st) return st;
+  if (sat && v > kSatMaxV)
+    return fail(MRPT_EPARAM, "mrpt_vote_pair: saturating counters need v <= 128 (see mrpt_vote_pair_max_votes)");
   if (nq == 0) return MRPT_OK;
   VoteArgs a = {};
   a.n = n;
@@ -1935,9 +2102,12 @@ extern "C" int32_t mrpt_vote_pair(const uint32_t *ps, int64_t pstride, const uin
   a.W = (int)W;
   a.ntiles = nt;
   a.dir = pdir;
+  a.dbg = getenv("MRPT_VOTE_DBG") ? atoi(getenv("MRPT_VOTE_DBG")) : 0;
   const size_t smem = (size_t)((counter_words_host(CW, W) + 3) & ~3LL) * 4 + 128;  // + 32 spare words
   typedef void (*pfn_t)(VoteArgs, const uint4 *, const int32_t *, int64_t);
-  pfn_t fn = CW == 1 ? k_vote_pair<1> : (CW == 3 ? k_vote_pair<3> : (CW == 2 ? k_vote_pair<2> : k_vote_pair<4>));
+  pfn_t fn = sat ? k_vote_pair<1, true>
+                 : (CW == 1 ? k_vote_pair<1> : (CW == 3 ? k_vote_pair<3> : (CW == 2 ? k_vote_pair<2> : k_vote_pair<4>)));
+  if (sat) g_vote_sat_queries += nq;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t grid = nq < (int64_t)num_sms() ? nq : (int64_t)num_sms();
   (count_launch(), fn<<<(unsigned)grid, 1024, smem, as_stream(stream)>>>(a, reinterpret_cast<const uint4 *>(ps), pbase,

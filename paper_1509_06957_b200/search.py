@@ -393,8 +393,10 @@ def _route_launch(D, qb, m, ldq, leaves):
 
 def _vote_list(D, leaves, m, votes, cand, cap, counts):
     lay = D.vote_layout()
-    if lay == "pair":
-        # the paired streamed vote (two id tiles per load, second parked in TMEM)
+    if lay == "pair" and votes <= D.pair_max_votes():
+        # the paired streamed vote (two id tiles per load, second parked in TMEM;
+        # saturating 8-bit counters when T > 255, which bound the threshold --
+        # larger thresholds take mrpt_vote below)
         ps, pstride, pdir, pbase = D.vote_pair()
         _native.call("mrpt_vote_pair", _native.ptr(ps), int(pstride), _native.ptr(pdir),
                      _native.ptr(pbase), D.n, D.T, D.depth, int(D.max_count), _native.ptr(leaves), m,
@@ -767,6 +769,17 @@ def approximate_knn(q, k, index, votes):
     kept = min(k, m)
     return NeighborList(indices=ids[0, :kept].copy(), distances=dists[0, :kept].copy(),
                         requested_k=k, candidate_count=m)
+
+
+def vote_stats(reset=False):
+    """Saturating paired vote (8-bit counters with T > 255): queries voted
+    and queries redone exactly after a counter wrapped, since the last reset
+    (measurement; synchronises the device)."""
+    import ctypes
+
+    out = (ctypes.c_int64 * 2)()
+    _native.call("mrpt_vote_stats", out, 1 if reset else 0)
+    return {"queries": int(out[0]), "redone": int(out[1])}
 
 
 def fallback_stats(reset=False):

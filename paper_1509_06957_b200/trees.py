@@ -356,6 +356,13 @@ class _DeviceIndex:
         self._vpair = (ps, pstride, pdir, pbase)
         return self._vpair
 
+    def pair_max_votes(self):
+        """Largest vote threshold mrpt_vote_pair serves on this index (128
+        where it votes with saturating 8-bit counters: T > 255 and large n)."""
+        mv = ctypes.c_int32(0)
+        _native.call("mrpt_vote_pair_max_votes", self.n, self.T, int(self.max_count), ctypes.byref(mv))
+        return mv.value
+
     def vote_layout(self):
         """Which list-vote layout queries use: "pair" (mrpt_vote_pair),
         "stream" (mrpt_vote_stream) or None (mrpt_vote over leaf_indices)."""

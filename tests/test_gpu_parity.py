@@ -466,8 +466,14 @@ def test_streamed_vote_matches_oracle(rng, T, depth, n, kind, votes):
                splits=index.splits, leaf_offsets=index.leaf_offsets,
                leaf_indices=index.leaf_indices, depth=depth)
     leaves = O.query_leaves(Q, ref)
+    pair_max = index.device_index().pair_max_votes()
+    assert pair_max == (128 if T > 255 else T)  # T > 255 here: saturating u8 counters (fewer tile pairs)
     for v in votes:
         for layout in ("stream", "pair"):
+            if layout == "pair" and v > pair_max:
+                with pytest.raises(mrpt.ParameterError):
+                    _stream_lists(index, Q, v, layout=layout)
+                continue  # approximate_knn_batch below serves it with mrpt_vote
             got, gc = _stream_lists(index, Q, v, layout=layout)
             for i in range(len(Q)):
                 want = O.candidates(leaves[i], ref, v)
@@ -478,6 +484,44 @@ def test_streamed_vote_matches_oracle(rng, T, depth, n, kind, votes):
         assert np.array_equal(counts.astype(np.int64), rc)
         assert np.array_equal(ids, rids)
         assert dists.tobytes() == rd.tobytes()
+
+
+@pytest.mark.parametrize("T,depth,n,dim,votes", [
+    (1000, 9, 400_000, 5, (3, 10, 128)),   # counts far above 255: every hot id is pulled back several times
+    (300, 5, 350_000, 5, (1, 7)),          # 2 tiles of 8-bit counters (3 of 10-bit ones), big leaves
+])
+def test_saturating_pair_vote_and_its_exact_redo(rng, monkeypatch, T, depth, n, dim, votes):
+    """T > 255 with 8-bit counters: the saturating paired vote lists exactly
+    the oracle's candidates (counts reach hundreds, so the pull-back runs all
+    the time), and so does the check-before-increment redo that a wrapped
+    counter would trigger (forced here for every query by MRPT_VOTE_DBG=8)."""
+    from paper_1509_06957_b200.search import vote_stats
+
+    X = gaussian(rng, n + 24, dim)
+    Xd, Q = X[:n], np.concatenate([X[n:], X[:8]])  # 8 queries are data points
+    index = mrpt.grow_trees(Xd, T, depth, seed=5)
+    ref = dict(matrices=[(R.col_ptr, R.row_idx, R.values) for R in index.matrices],
+               splits=index.splits, leaf_offsets=index.leaf_offsets,
+               leaf_indices=index.leaf_indices, depth=depth)
+    leaves = O.query_leaves(Q, ref)
+    want = {v: [O.candidates(leaves[i], ref, v) for i in range(len(Q))] for v in votes}
+    top = max(int(np.bincount(np.concatenate([index.leaf_indices[t, index.leaf_offsets[t, f]:index.leaf_offsets[t, f + 1]]
+                                              for t, f in enumerate(leaves[-1])])).max()), 0)
+    assert top > 255, "the case should count past 8 bits"
+    for forced in (False, True):
+        if forced:
+            monkeypatch.setenv("MRPT_VOTE_DBG", "8")
+        vote_stats(reset=True)
+        for v in votes:
+            got, gc = _stream_lists(index, Q, v, layout="pair")
+            for i in range(len(Q)):
+                assert gc[i] == len(want[v][i])
+                assert np.array_equal(np.sort(got[i]), want[v][i])
+        st = vote_stats()
+        assert st["queries"] == len(votes) * len(Q)
+        print(f"T={T} forced={forced}: saturating vote {st}")
+        if forced:
+            assert st["redone"] == len(votes) * len(Q)
 
 
 def test_streamed_vote_layout_round_trip(rng):

@@ -1,6 +1,7 @@
 """A/B of the list-vote kernels on one configuration, in one process: the
 streamed vote (mrpt_vote_stream, one piece per id tile) against the paired
-vote (mrpt_vote_pair, two tiles per 32-byte load, second parked in TMEM).
+vote (mrpt_vote_pair, two tiles per 32-byte load, second parked in TMEM;
+"pairw" = the same with wide counters).
 Queries in the batch order the product uses (tree-0 leaf).  Candidate counts
 and sorted candidate sets must be identical; prints CUDA-event times.
 
@@ -45,8 +46,18 @@ sizes = D.offsets[:, 1:] - D.offsets[:, :-1]
 touched = float(sizes.gather(1, leaves.long().t()).sum().item())
 res, ref = {}, None
 for name in args.variants.split(","):
-    fn = "mrpt_vote_pair" if name == "pair" else "mrpt_vote_stream"
-    buf, stride, dr, base = D.vote_pair() if name == "pair" else D.vote_stream()
+    # pairw: the paired vote with wide (10/16-bit) counters instead of the
+    # saturating 8-bit ones (MRPT_VOTE_SAT=0; the layout is rebuilt)
+    # pair8: plain 8-bit counters whatever T (timing only: the counts may wrap)
+    sat = "0" if name == "pairw" else "1"
+    mc = 255 if name == "pair8" else p["n_trees"]
+    if name.startswith("pair") and (os.environ.get("MRPT_VOTE_SAT", "1") != sat or D.max_count != mc):
+        os.environ["MRPT_VOTE_SAT"] = sat
+        D.max_count = mc
+        D._vpair = False
+        torch.cuda.empty_cache()
+    fn = "mrpt_vote_pair" if name.startswith("pair") else "mrpt_vote_stream"
+    buf, stride, dr, base = D.vote_pair() if name.startswith("pair") else D.vote_stream()
     cand = torch.empty((nq, cap), dtype=torch.int32, device="cuda") if nq * cap * 4 < (8 << 30) else None
     cbuf = torch.empty((chunk, cap), dtype=torch.int32, device="cuda")
     counts = torch.empty(nq, dtype=torch.int32, device="cuda")
@@ -82,7 +93,8 @@ for name in args.variants.split(","):
         ref = (c, digest)
     res[name] = {"layout_gb": round(buf.numel() * 4 / 1e9, 2), "ms": round(ms, 3),
                  "ms_per_100k": round(ms * 1e5 / nq, 2), "leaf_id_gbs": round(4 * touched / (ms / 1e3) / 1e9, 1),
-                 "same_counts": bool(np.array_equal(c, ref[0])), "same_sets": digest == ref[1]}
+                 "same_counts": bool(np.array_equal(c, ref[0])), "same_sets": digest == ref[1],
+                 "sat": mrpt.search.vote_stats(reset=True)}
     del cand
 print(json.dumps({"config": args.config, "scale": args.scale, "nq": nq, "v": v,
                   "leaf_id_bytes_per_query": 4 * touched / nq, **res}))
