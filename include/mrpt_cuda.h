@@ -353,10 +353,12 @@ int32_t mrpt_vote_stream(const uint32_t *qs, int64_t tstride, const uint16_t *qd
  *   mrpt_vote_pair: candidate lists like mrpt_vote_stream.
  * Counter width: where max_count > 255 and 8-bit counters need fewer pairs
  * of id tiles than 10/16-bit ones (large n), the counters are 8 bits wide
- * and SATURATE: a counter reaching 192 is pulled back by 64 by the
- * increment that saw 192, so it never returns below v (v <= 128 required,
- * see mrpt_vote_pair_max_votes; larger v is served by mrpt_vote) and each
- * id reaching v votes is still listed exactly once (_cy.pyx:75-77).  An
+ * and SATURATE: they start at 128 - v (so the increment lifting a count to v
+ * is the one that reads 127) and a counter reaching 192 is pulled back by 64
+ * by the increment that read 191, so it never returns to 127 (v <= 128
+ * required, see mrpt_vote_pair_max_votes; larger v is served by mrpt_vote)
+ * and each id reaching v votes is still listed exactly once
+ * (_cy.pyx:75-77).  An
  * increment that would wrap a counter (it read 255) flags its query, which
  * the same launch then redoes with check-before-increment bumps that cannot
  * wrap -- results are exact either way; mrpt_vote_stats counts the redos.

@@ -6,6 +6,7 @@
 // product is exact in float64 (24+24 < 53 mantissa bits), so one fused
 // multiply-add per term rounds exactly like the reference's separate
 // multiply and add -- the chain below is bit-identical to _cy.project.
+#include <stdint.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -108,6 +109,183 @@ k_project_d64(const float *__restrict__ X, int64_t m, int d, int64_t ldx,
       for (int j = 0; j < PPT; ++j) {
         const int p = lane + 32 * j;
         if (p < here) out[(i0 + p) * ors + (int64_t)c * ocs] = __double2float_rn(acc[j]);
+      }
+    }
+  }
+}
+
+// Packed float64 tile (PPT = 3 or 5; the default where it fits).  K1 is
+// bound by the shared-memory return path (a warp's 8-byte load returns 256
+// bytes = 2 cycles per DFMA), so the tile keeps fewer bytes per coordinate.
+// (double)x of a float has at most 23 explicit mantissa bits: its high word
+// plus the top 3 bits of its low word are the whole value.  Per (coordinate,
+// lane) the tile stores the PPT high words of points lane + 32 j and one word
+// holding the PPT 3-bit fields -- 16 bytes for 3 points, 24 bytes for 5
+// (5.3 / 4.8 bytes per term instead of 8) -- and a term rebuilds its float64
+// with one or two integer operations before the same DFMA.  The value is the
+// exact float64 the plain tile holds, so the chain is bit-identical.
+template <int J>
+__device__ __forceinline__ uint32_t h32_lo(uint32_t w) {
+  // fields: j=0 bits 0-2, j=1 bits 13-15 (byte 1 otherwise zero), j=2 bits
+  // 21-23 (byte 2 otherwise zero), j=3 bits 29-31, j=4 bits 3-5
+  if (J == 0) return w << 29;
+  if (J == 1) return __byte_perm(w, 0u, 0x1444);
+  if (J == 2) return __byte_perm(w, 0u, 0x2444);
+  if (J == 3) return w & 0xE0000000u;
+  return (w << 26) & 0xE0000000u;
+}
+__device__ __forceinline__ uint32_t h32_field(int j, double x) {
+  const uint32_t l = (uint32_t)__double2loint(x) >> 29;
+  return l << (j == 0 ? 0 : (j == 1 ? 13 : (j == 2 ? 21 : (j == 3 ? 29 : 3))));
+}
+
+// Stage TP = 32 * PPT rows of X (rows i0 .. i0 + here) into the packed tile:
+// a warp takes 4 coordinates at a time, its lanes the points lane + 32 j.
+template <int PPT>
+__device__ __forceinline__ void h32_stage(const float *__restrict__ X, int64_t ldx, int d, int64_t i0, int here,
+                                          uint4 *A, uint2 *B) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int g = warp; 4 * g < d; g += nw) {
+    float4 x[PPT];
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      const int p = lane + 32 * j;
+      x[j] = p < here ? __ldg(reinterpret_cast<const float4 *>(X + (i0 + p) * ldx) + g)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      uint32_t hi[PPT], w = 0u;
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        const float f = u == 0 ? x[j].x : (u == 1 ? x[j].y : (u == 2 ? x[j].z : x[j].w));
+        const double xd = (double)f;
+        hi[j] = (uint32_t)__double2hiint(xd);
+        w |= h32_field(j, xd);
+      }
+      const int at = (4 * g + u) * 32 + lane;
+      A[at] = make_uint4(hi[0], hi[1], hi[2], w);
+      if (PPT == 5) B[at] = make_uint2(hi[PPT - 2], hi[PPT - 1]);
+    }
+  }
+}
+
+// One column's chain for the lane's PPT points: acc[j] = fma(x_j[row], value,
+// acc[j]) over the column's entries in stored order.  Al / Bl: the tile
+// regions offset by the lane.
+template <int PPT>
+__device__ __forceinline__ void h32_column(const uint4 *Al, const uint2 *Bl, const int2 *__restrict__ ent, int64_t s0,
+                                           int64_t s1, double (&acc)[PPT]) {
+#pragma unroll 4
+  for (int64_t s = s0; s < s1; ++s) {
+    const int2 e = __ldg(ent + s);
+    const double v = (double)__int_as_float(e.y);
+    const uint4 a = Al[e.x * 32];
+    acc[0] = __fma_rn(__hiloint2double((int)a.x, (int)h32_lo<0>(a.w)), v, acc[0]);
+    acc[1] = __fma_rn(__hiloint2double((int)a.y, (int)h32_lo<1>(a.w)), v, acc[1]);
+    acc[2] = __fma_rn(__hiloint2double((int)a.z, (int)h32_lo<2>(a.w)), v, acc[2]);
+    if (PPT == 5) {
+      const uint2 b = Bl[e.x * 32];
+      acc[PPT - 2] = __fma_rn(__hiloint2double((int)b.x, (int)h32_lo<3>(a.w)), v, acc[PPT - 2]);
+      acc[PPT - 1] = __fma_rn(__hiloint2double((int)b.y, (int)h32_lo<4>(a.w)), v, acc[PPT - 1]);
+    }
+  }
+}
+
+template <int PPT>
+__global__ void __launch_bounds__(1024, 1)
+k_project_h32(const float *__restrict__ X, int64_t m, int d, int64_t ldx,
+              const int64_t *__restrict__ col_ptr, const int2 *__restrict__ ent, int64_t ent_cap, int ncols,
+              float *__restrict__ out, int64_t ors, int64_t ocs) {
+  static_assert(PPT == 3 || PPT == 5, "packed tile: 3 or 5 points per lane");
+  extern __shared__ uint4 h32_smem[];
+  constexpr int TP = 32 * PPT;
+  uint4 *A = h32_smem;                                      // [d][32]: hi0, hi1, hi2, fields
+  uint2 *B = reinterpret_cast<uint2 *>(h32_smem + 32 * d);  // [d][32]: hi3, hi4 (PPT == 5)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t tile = blockIdx.x; tile * TP < m; tile += gridDim.x) {
+    const int64_t i0 = tile * TP;
+    const int here = (int)((m - i0) < TP ? (m - i0) : TP);
+    __syncthreads();
+    h32_stage<PPT>(X, ldx, d, i0, here, A, B);
+    __syncthreads();
+    const uint4 *Al = A + lane;
+    const uint2 *Bl = B + lane;
+    for (int c = warp; c < ncols; c += nw) {
+      const int64_t s0 = __ldg(col_ptr + c), s1r = __ldg(col_ptr + c + 1);
+      const int64_t s1 = s1r < ent_cap ? s1r : ent_cap;
+      double acc[PPT];
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) acc[j] = 0.0;
+      h32_column<PPT>(Al, Bl, ent, s0, s1, acc);
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        const int p = lane + 32 * j;
+        if (p < here) out[(i0 + p) * ors + (int64_t)c * ocs] = __double2float_rn(acc[j]);
+      }
+    }
+  }
+}
+
+// K2 on the packed tile (batched queries): a CTA stages 32 * PPT query rows
+// like K1 and its warps take whole trees of its share [part T/S, (part+1)
+// T/S): per level the column's chain for the lane's PPT queries (the K1
+// chain: warp-uniform entries, conflict-free tile loads), then the descent
+// _cy.route: node = 2*node + 1 + (p > split[node]).  Against k_query_route
+// (thread = tree, query coordinates gathered at per-lane rows: bank
+// conflicts on every term) the shared-memory return path carries 4.8 bytes
+// per term without conflicts.
+template <int PPT>
+__global__ void __launch_bounds__(1024, 1)
+k_query_route_h32(const float *__restrict__ Q, int64_t nq, int d, int64_t ldq,
+                  const int64_t *__restrict__ col_ptr, const int2 *__restrict__ ent, int64_t ent_cap,
+                  const float *__restrict__ splits, int T, int depth, int32_t *__restrict__ leaves, int S) {
+  static_assert(PPT == 3 || PPT == 5, "packed tile: 3 or 5 points per lane");
+  extern __shared__ uint4 h32_smem[];
+  constexpr int TP = 32 * PPT;
+  uint4 *A = h32_smem;
+  uint2 *B = reinterpret_cast<uint2 *>(h32_smem + 32 * d);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int32_t nint = (int32_t)(((int64_t)1 << depth) - 1);
+  const int64_t items = ((nq + TP - 1) / TP) * S;
+  int64_t staged = -1;
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int64_t tile = item / S;
+    const int part = (int)(item - tile * S);
+    const int64_t i0 = tile * TP;
+    const int here = (int)((nq - i0) < TP ? (nq - i0) : TP);
+    if (tile != staged) {  // CTA-uniform
+      __syncthreads();
+      h32_stage<PPT>(Q, ldq, d, i0, here, A, B);
+      __syncthreads();
+      staged = tile;
+    }
+    const uint4 *Al = A + lane;
+    const uint2 *Bl = B + lane;
+    const int t0 = (int)(((int64_t)part * T) / S), t1 = (int)(((int64_t)(part + 1) * T) / S);
+    for (int t = t0 + warp; t < t1; t += nw) {
+      const float *tsplit = splits + (int64_t)t * nint;
+      int32_t node[PPT];
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) node[j] = 0;
+      for (int lev = 0; lev < depth; ++lev) {
+        const int64_t c = (int64_t)t * depth + lev;
+        const int64_t s0 = __ldg(col_ptr + c), s1r = __ldg(col_ptr + c + 1);
+        const int64_t s1 = s1r < ent_cap ? s1r : ent_cap;
+        double acc[PPT];
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) acc[j] = 0.0;
+        h32_column<PPT>(Al, Bl, ent, s0, s1, acc);
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          const float p = __double2float_rn(acc[j]);
+          node[j] = 2 * node[j] + 1 + (p > __ldg(tsplit + node[j]) ? 1 : 0);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        const int p = lane + 32 * j;
+        if (p < here) leaves[(i0 + p) * T + t] = node[j] - nint;
       }
     }
   }
@@ -277,6 +455,25 @@ extern "C" int32_t mrpt_project(const float *X, int64_t m, int32_t d, int64_t ld
         (count_launch(), k_pack_entries<<<(unsigned)(pb < 4096 ? pb : 4096), 256, 0, s>>>(rows, vals,
                                                                                           col_ptr + ncols, nnz_bound, ent));
       }
+      // packed tile (k_project_h32): 5 points per lane in 24 bytes per
+      // coordinate, or 3 in 16, where the rows are 16-byte loadable
+      {
+        const char *ph = getenv("MRPT_PROJ_H32");  // experiments: 0 disables
+        const bool vec = d % 4 == 0 && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+        const int hp = (int64_t)d * 32 * 24 <= 224 * 1024 ? 5 : ((int64_t)d * 32 * 16 <= 224 * 1024 ? 3 : 0);
+        if ((!ph || atoi(ph) != 0) && vec && hp) {
+          const size_t hsmem = (size_t)d * 32 * (hp == 5 ? 24 : 16);
+          void (*hf)(const float *, int64_t, int, int64_t, const int64_t *, const int2 *, int64_t, int, float *,
+                     int64_t, int64_t) = hp == 5 ? k_project_h32<5> : k_project_h32<3>;
+          cudaFuncSetAttribute(hf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
+          const int64_t htiles = ceil_div<int64_t>(m, 32 * hp);
+          const int hgrid = (int)(htiles < (int64_t)num_sms() ? htiles : (int64_t)num_sms());
+          (count_launch(), hf<<<hgrid, 1024, hsmem, s>>>(X, m, d, ldx, col_ptr, ent, nnz_bound, ncols, out,
+                                                       out_row_stride, out_col_stride));
+          cudaFreeAsync(ent, s);
+          return launch_status("mrpt_project");
+        }
+      }
       const size_t smem = (size_t)32 * ppt * stride * 8;
       void (*fn)(const float *, int64_t, int, int64_t, const int64_t *, const int2 *, int64_t, int, float *,
                  int64_t, int64_t, int) =
@@ -384,6 +581,38 @@ extern "C" int32_t mrpt_query_route(const float *Q, int64_t nq, int32_t d, int64
     return fail(MRPT_ESHAPE, "mrpt_query_route: bad shape");
   if (nq == 0) return MRPT_OK;
   cudaStream_t s = as_stream(stream);
+  // batched queries on the packed tile (k_query_route_h32)
+  {
+    const char *ph = getenv("MRPT_ROUTE_H32");  // experiments: 0 disables, 1 forces for any batch size
+    const bool vec = d % 4 == 0 && ldq % 4 == 0 && (reinterpret_cast<uintptr_t>(Q) & 15) == 0;
+    const int hp = (int64_t)d * 32 * 24 <= 224 * 1024 ? 5 : ((int64_t)d * 32 * 16 <= 224 * 1024 ? 3 : 0);
+    const bool want = ph ? atoi(ph) != 0 : nq >= 1024;
+    if (want && vec && hp && depth <= 30) {
+      const int64_t ncols = (int64_t)T * depth, nnz_bound = ncols * d;
+      int2 *ent = nullptr;
+      keep_pool_warm();
+      if (cudaMallocAsync((void **)&ent, sizeof(int2) * (size_t)nnz_bound, s) != cudaSuccess)
+        return fail(MRPT_ECUDA, "mrpt_query_route: scratch allocation failed");
+      const int64_t pb = ceil_div<int64_t>(nnz_bound, 256);
+      (count_launch(), k_pack_entries<<<(unsigned)(pb < 4096 ? pb : 4096), 256, 0, s>>>(rows, vals, col_ptr + ncols,
+                                                                                        nnz_bound, ent));
+      const size_t hsmem = (size_t)d * 32 * (hp == 5 ? 24 : 16);
+      void (*hf)(const float *, int64_t, int, int64_t, const int64_t *, const int2 *, int64_t, const float *, int,
+                 int, int32_t *, int) = hp == 5 ? k_query_route_h32<5> : k_query_route_h32<3>;
+      cudaFuncSetAttribute(hf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
+      const int64_t tiles = ceil_div<int64_t>(nq, 32 * hp);
+      // tree shares per tile so that every SM gets ~10 work items or more
+      int64_t S = ceil_div<int64_t>(10 * (int64_t)num_sms(), tiles);
+      S = S < 1 ? 1 : (S > 8 ? 8 : S);
+      if (S > T / 32) S = T / 32 > 0 ? T / 32 : 1;
+      const int64_t items = tiles * S;
+      const int grid = (int)(items < (int64_t)num_sms() ? items : (int64_t)num_sms());
+      (count_launch(), hf<<<grid, 1024, hsmem, s>>>(Q, nq, d, ldq, col_ptr, ent, nnz_bound, splits, T, depth, leaves,
+                                                    (int)S));
+      cudaFreeAsync(ent, s);
+      return launch_status("mrpt_query_route");
+    }
+  }
   const char *qe = getenv("MRPT_ROUTE_QB");
   const int qbs = qe ? atoi(qe) : 8;
   // 8 queries per thread (8 independent float64 chains per CSC entry load);

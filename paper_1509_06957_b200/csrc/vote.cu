@@ -1255,20 +1255,26 @@ __device__ __forceinline__ void ld_pair_l2_256(const uint4 *p, uint4 &a, uint4 &
 }
 
 // Bump the 7 counters of one quad; the increment that lifts a count to v
-// appends the id (_cy.pyx:75-77).
+// appends the id (_cy.pyx:75-77).  The returned counts are tested into one
+// predicate per quad (events are rare per id), and only a quad holding an
+// event walks its 7 entries again.
 // Saturating 8-bit counters (SAT): counts above 255 are possible (T up to
-// 1024) but only the crossing of v matters, so a counter that reaches
-// kSatTrig is pulled back by kSatSub -- by the one increment that saw exactly
-// kSatTrig -- and stays in [kSatTrig - kSatSub + 1, 255]: above v - 1 (v <=
-// kSatMaxV), so no id is listed twice.  Should increments outrun a pull-back
-// and wrap a counter, the increment that wraps it sees 255 and raises the
-// query's overflow flag; the query is then redone by vote_pair_careful.
-// Either way every id whose count reaches v is listed exactly once
-// (_cy.pyx:75-77).
+// 1024) but only the crossing of v matters.  The counters are BIASED: they
+// are cleared to kSatCross + 1 - v (v <= kSatMaxV = 128), so the increment
+// that lifts a count to v is the one that reads kSatCross = 127, and a
+// counter that reaches 192 is pulled back by 64 -- by the one increment that
+// read 191 -- so it cycles in [128, 192]: above kSatCross, no id is listed
+// twice.  Every event value (63: nothing, 127: crossing, 191: pull-back, 255:
+// about to wrap) has its low six bits set, so the test per id is one masked
+// compare, the same cost as the plain counters'.  Should increments outrun a
+// pull-back and wrap a counter, the increment that wraps it reads 255 and
+// raises the query's overflow flag; the query is then redone by
+// vote_pair_careful.  Either way every id whose count reaches v is listed
+// exactly once (_cy.pyx:75-77).
 // Queries redone by vote_pair_careful (mrpt_vote_stats; measurement only).
 __device__ unsigned long long g_vote_sat_redos;
 
-constexpr uint32_t kSatTrig = 192, kSatSub = 64;
+constexpr uint32_t kSatCross = 127, kSatPull = 191, kSatSub = 64;
 constexpr int kSatMaxV = 128;
 
 template <int CW, bool SAT = false>
@@ -1286,27 +1292,34 @@ __device__ __forceinline__ void pair_bump(uint4 cur, uint32_t cnt_s, uint32_t nc
   if (wd[0] >= pad_word) return;
 #pragma unroll
   for (int c = 0; c < kQuadIds; ++c) old[c] = atom_add_shared(cnt_s + 4u * wd[c], 1u << (((fb >> (2 * c)) & 3u) * LB));
+  // per-id event predicates, kept for the second walk
+  bool ev[kQuadIds], any = false;
 #pragma unroll
   for (int c = 0; c < kQuadIds; ++c) {
+    const uint32_t fld = (old[c] >> (((fb >> (2 * c)) & 3u) * LB)) & MASK;
+    ev[c] = SAT ? ((fld & 63u) == 63u) : (fld == vm1);
+    any |= ev[c];
+  }
+  if (!any) return;
+#pragma unroll
+  for (int c = 0; c < kQuadIds; ++c) {
+    if (!ev[c]) continue;
     const uint32_t f = (fb >> (2 * c)) & 3u;
-    const uint32_t fld = (old[c] >> (f * LB)) & MASK;
     if (SAT) {
       // Padding entries are not excluded up front: their spare words are
-      // pulled back like any counter, so they too sit below kSatTrig and
-      // this branch stays rare (tested for padding inside instead).
-      if (fld == vm1 || fld >= kSatTrig) {
-        if (fld == vm1) {
-          if (wd[c] < pad_word) {  // lifted a count to v
-            const int pos = (int)atom_add_shared(nc_s, 1u);
-            if (pos < cap32) qcand[pos] = lo + (int)(wd[c] * PER + f);
-          }
-        } else if (fld == kSatTrig) {
-          atom_add_shared(cnt_s + 4u * wd[c], 0u - (kSatSub << (f * LB)));
-        } else if (fld == MASK && wd[c] < pad_word) {
-          asm volatile("st.shared.u32 [%0], %1;" ::"r"(ovf_s), "r"(1u) : "memory");
+      // pulled back like any counter (tested for padding inside instead).
+      const uint32_t fld = (old[c] >> (f * LB)) & MASK;
+      if (fld == kSatCross) {
+        if (wd[c] < pad_word) {  // lifted a count to v
+          const int pos = (int)atom_add_shared(nc_s, 1u);
+          if (pos < cap32) qcand[pos] = lo + (int)(wd[c] * PER + f);
         }
+      } else if (fld == kSatPull) {
+        atom_add_shared(cnt_s + 4u * wd[c], 0u - (kSatSub << (f * LB)));
+      } else if (fld == MASK && wd[c] < pad_word) {
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(ovf_s), "r"(1u) : "memory");
       }
-    } else if (fld == vm1 && wd[c] < pad_word) {  // lifted a count to v
+    } else if (wd[c] < pad_word) {  // lifted a count to v
       const int pos = (int)atom_add_shared(nc_s, 1u);
       if (pos < cap32) qcand[pos] = lo + (int)(wd[c] * PER + f);
     }
@@ -1320,7 +1333,16 @@ __device__ __forceinline__ void pair_bump(uint4 cur, uint32_t cnt_s, uint32_t nc
 // below v: between that read and the increment at most the other 31 lanes
 // of the same instruction add to the counter, so it stays below v + 32 <= 160
 // and cannot wrap.  The other warps only help clearing.
-__device__ __noinline__ void vote_pair_careful(const VoteArgs &a, const uint4 *__restrict__ ps,
+// (The kernel's VoteArgs fields come by value: a reference would force the
+// kernel's copy of its parameter struct onto the local-memory stack.)
+struct CarefulArgs {
+  int ntiles, W, T, L, v;
+  int64_t cap;
+  const int32_t *leaves;
+  const uint16_t *dir;
+  int32_t *cand;
+};
+__device__ __noinline__ void vote_pair_careful(CarefulArgs a, const uint4 *__restrict__ ps,
                                                const int32_t *__restrict__ pbase, int64_t pstride, int64_t q,
                                                uint32_t *cnt, int cwords, int *s_nc) {
   constexpr int PER = 4;
@@ -1449,8 +1471,10 @@ __global__ void __launch_bounds__(1024, 1) k_vote_pair(VoteArgs a, const uint4 *
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tslot = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+  // SAT: counters start at kSatCross + 1 - v (see pair_bump)
+  const uint32_t c0 = SAT ? (kSatCross - vm1) * 0x01010101u : 0u;
   auto clear_counters = [&]() {
-    for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(c0, c0, c0, c0);
   };
   for (int64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
     const uint16_t *dl = nullptr;
@@ -1540,7 +1564,10 @@ __global__ void __launch_bounds__(1024, 1) k_vote_pair(VoteArgs a, const uint4 *
     __syncthreads();
     if (SAT && s_ovf) {  // CTA-uniform: a counter wrapped, redo the query exactly
       if (tid == 0) atomicAdd(&g_vote_sat_redos, 1ull);
-      vote_pair_careful(a, ps, pbase, pstride, q, cnt, cwords, &s_nc);
+      CarefulArgs ca;
+      ca.ntiles = a.ntiles, ca.W = a.W, ca.T = a.T, ca.L = a.L, ca.v = a.v, ca.cap = a.cap;
+      ca.leaves = a.leaves, ca.dir = a.dir, ca.cand = a.cand;
+      vote_pair_careful(ca, ps, pbase, pstride, q, cnt, cwords, &s_nc);
     }
     if (tid == 0) a.ncand[q] = s_nc;  // > cap means only cap ids were stored
     __syncthreads();

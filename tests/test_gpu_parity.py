@@ -100,6 +100,65 @@ def test_projection_bit_identical(rng, monkeypatch, n, d, depth, a, ppt):
         assert mrpt.project_query(X[i], R).tobytes() == ref[i].tobytes()
 
 
+@pytest.mark.parametrize("h32", ["1", "0"])
+@pytest.mark.parametrize("n,d,ncols,a", [
+    (777, 256, 40, 1 / 16),    # packed tile, 5 points per lane (24 bytes per coordinate), ragged last tile
+    (1000, 128, 64, 0.09),     # packed tile at a small d
+    (500, 300, 33, 0.05),      # d beyond the 5-point tile: 3 points per lane (16 bytes)
+    (333, 440, 35, 0.03),      # the largest 3-point tile rows
+    (161, 784, 32, 1 / 28),    # d beyond the packed tiles: plain float64 tile
+    (321, 48, 50, 0.25),
+])
+def test_projection_column_batches_bit_identical(rng, monkeypatch, n, d, ncols, a, h32):
+    """K1 on >= 32 columns at once (the build's batches: the float64-tile
+    kernels, packed and plain) is bit-identical to _cy.project, including
+    zeros, negative zeros, denormals and the largest finite floats."""
+    monkeypatch.setenv("MRPT_PROJ_H32", h32)
+    X = gaussian(rng, n, d)
+    X[::7, ::5] = 0.0
+    X[1::11, 3::9] = -0.0
+    X[2::13, 1::6] = np.float32(1e-41)      # denormal
+    X[3::17, 2::8] = np.float32(-3e-45)     # smallest denormals
+    X[4::19, ::10] = np.finfo(np.float32).max
+    X[5::23, 4::12] = np.finfo(np.float32).tiny
+    R = mrpt.sample_sparse_matrix(d, ncols, a, seed=(5, 2))
+    P = mrpt.project_dataset(X, R)
+    ref = O.project(X, R.col_ptr, R.row_idx, R.values)
+    assert P.tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("d,T,depth,nq", [
+    (256, 70, 9, 1500),    # 5 queries per lane, several tree shares per tile, ragged last tile
+    (128, 33, 6, 161),     # forced on a small batch: two tiles, the second of one query
+    (400, 40, 7, 1100),    # 3 queries per lane
+    (64, 3, 5, 2000),      # fewer trees than warps
+])
+def test_batched_route_on_packed_tile_matches_oracle(rng, monkeypatch, d, T, depth, nq):
+    """K2 on the packed tile (the batched route of >= 1024 queries) gives the
+    oracle's leaves, and the same leaves as the thread-per-tree kernel."""
+    import torch
+
+    from paper_1509_06957_b200.search import _route_device
+
+    X = gaussian(rng, 3000 + nq, d)
+    Xd, Q = X[:3000], X[3000:].copy()
+    Q[::9, ::4] = 0.0
+    Q[1::7, 1::5] = np.float32(2e-42)
+    index = mrpt.grow_trees(Xd, T, depth, seed=4)
+    ref = dict(matrices=[(R.col_ptr, R.row_idx, R.values) for R in index.matrices],
+               splits=index.splits, leaf_offsets=index.leaf_offsets,
+               leaf_indices=index.leaf_indices, depth=depth)
+    want = np.asarray(O.query_leaves(Q, ref))
+    D = index.device_index()
+    Qd = torch.from_numpy(Q).cuda()
+    got = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("MRPT_ROUTE_H32", mode)
+        got[mode] = _route_device(Qd, D).cpu().numpy()
+    assert np.array_equal(got["1"], want)
+    assert np.array_equal(got["0"], want)
+
+
 @pytest.mark.parametrize("n,d,T,depth,gen", [
     (100_000, 64, 3, 10, "gauss"),       # big-path segments (> 8192) at the top levels
     (60_000, 16, 2, 9, "ints"),          # heavy ties through the big path
