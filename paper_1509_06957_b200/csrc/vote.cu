@@ -1277,6 +1277,18 @@ __device__ unsigned long long g_vote_sat_redos;
 constexpr uint32_t kSatCross = 127, kSatPull = 191, kSatSub = 64;
 constexpr int kSatMaxV = 128;
 
+// Append one id to the query's candidate list.  nc_lane is the list counter's
+// shared address made lane-dependent on purpose (see k_vote_pair): with a
+// provably uniform address ptxas wraps the atomic in an 11-instruction
+// warp-aggregation sequence, which loses when one or two lanes emit; qcand is
+// kept opaque so its 64-bit base is not recomputed per emission.
+__device__ __forceinline__ void pair_emit(uint32_t nc_lane, int32_t *qcand, int cap32, int32_t id) {
+  const int pos = (int)atom_add_shared(nc_lane, 1u);
+  if (pos < cap32)
+    asm volatile("{ .reg .u64 a; mad.wide.u32 a, %1, 4, %0; st.global.u32 [a], %2; }" ::"l"(qcand), "r"(pos), "r"(id)
+                 : "memory");
+}
+
 template <int CW, bool SAT = false>
 __device__ __forceinline__ void pair_bump(uint4 cur, uint32_t cnt_s, uint32_t nc_s, uint32_t pad_word, uint32_t vm1,
                                           int32_t lo, int32_t *qcand, int cap32, uint32_t ovf_s = 0) {
@@ -1310,18 +1322,14 @@ __device__ __forceinline__ void pair_bump(uint4 cur, uint32_t cnt_s, uint32_t nc
       // pulled back like any counter (tested for padding inside instead).
       const uint32_t fld = (old[c] >> (f * LB)) & MASK;
       if (fld == kSatCross) {
-        if (wd[c] < pad_word) {  // lifted a count to v
-          const int pos = (int)atom_add_shared(nc_s, 1u);
-          if (pos < cap32) qcand[pos] = lo + (int)(wd[c] * PER + f);
-        }
+        if (wd[c] < pad_word) pair_emit(nc_s, qcand, cap32, lo + (int)(wd[c] * PER + f));  // lifted a count to v
       } else if (fld == kSatPull) {
         atom_add_shared(cnt_s + 4u * wd[c], 0u - (kSatSub << (f * LB)));
       } else if (fld == MASK && wd[c] < pad_word) {
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(ovf_s), "r"(1u) : "memory");
       }
-    } else if (wd[c] < pad_word) {  // lifted a count to v
-      const int pos = (int)atom_add_shared(nc_s, 1u);
-      if (pos < cap32) qcand[pos] = lo + (int)(wd[c] * PER + f);
+    } else if (wd[c] < pad_word) {
+      pair_emit(nc_s, qcand, cap32, lo + (int)(wd[c] * PER + f));  // lifted a count to v
     }
   }
 }
@@ -1333,16 +1341,9 @@ __device__ __forceinline__ void pair_bump(uint4 cur, uint32_t cnt_s, uint32_t nc
 // below v: between that read and the increment at most the other 31 lanes
 // of the same instruction add to the counter, so it stays below v + 32 <= 160
 // and cannot wrap.  The other warps only help clearing.
-// (The kernel's VoteArgs fields come by value: a reference would force the
-// kernel's copy of its parameter struct onto the local-memory stack.)
-struct CarefulArgs {
-  int ntiles, W, T, L, v;
-  int64_t cap;
-  const int32_t *leaves;
-  const uint16_t *dir;
-  int32_t *cand;
-};
-__device__ __noinline__ void vote_pair_careful(CarefulArgs a, const uint4 *__restrict__ ps,
+// It runs in its own kernel (k_vote_pair_redo) over the queries the main
+// kernel listed, so the main kernel carries no call and no stack frame.
+__device__ __forceinline__ void vote_pair_careful(const VoteArgs &a, const uint4 *__restrict__ ps,
                                                const int32_t *__restrict__ pbase, int64_t pstride, int64_t q,
                                                uint32_t *cnt, int cwords, int *s_nc) {
   constexpr int PER = 4;
@@ -1430,7 +1431,8 @@ constexpr int kPairSlots = 16;  // stashed windows per warp (4 TMEM columns each
 // re-read their pair in phase B.  The counts are those of k_vote_stream.
 template <int CW, bool SAT = false>
 __global__ void __launch_bounds__(1024, 1) k_vote_pair(VoteArgs a, const uint4 *__restrict__ ps,
-                                                       const int32_t *__restrict__ pbase, int64_t pstride) {
+                                                       const int32_t *__restrict__ pbase, int64_t pstride,
+                                                       int32_t *redo /* SAT: count, then queries */) {
   extern __shared__ uint4 vote_smem[];
   uint32_t *cnt = reinterpret_cast<uint32_t *>(vote_smem);
   uint32_t cnt_s = (uint32_t)__cvta_generic_to_shared(cnt);
@@ -1443,7 +1445,10 @@ __global__ void __launch_bounds__(1024, 1) k_vote_pair(VoteArgs a, const uint4 *
   __shared__ uint32_t s_tmem, s_ovf;
   const uint32_t vm1 = (uint32_t)(a.v - 1);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint32_t nc_s = (uint32_t)__cvta_generic_to_shared(&s_nc);
+  // + 0 in a form ptxas cannot fold: the address stays per-lane (pair_emit)
+  uint32_t lm_eq;
+  asm volatile("mov.u32 %0, %%lanemask_eq;" : "=r"(lm_eq));
+  uint32_t nc_s = (uint32_t)__cvta_generic_to_shared(&s_nc) + (uint32_t)(__popc(lm_eq) - 1);
   asm volatile("" : "+r"(nc_s));
   uint32_t ovf_s = (uint32_t)__cvta_generic_to_shared(&s_ovf);
   asm volatile("" : "+r"(ovf_s));
@@ -1489,6 +1494,7 @@ __global__ void __launch_bounds__(1024, 1) k_vote_pair(VoteArgs a, const uint4 *
       dnn = nsup >= 2 ? (int)__ldg(dl + 2) : 0;
     }
     int32_t *qcand = a.cand + q * a.cap;
+    asm volatile("" : "+l"(qcand));
     StreamWindows sw;
     sw.pf = 0;
     sw.begin(dnxt - dcur, lbase + (uint32_t)dcur, woff);
@@ -1562,14 +1568,11 @@ __global__ void __launch_bounds__(1024, 1) k_vote_pair(VoteArgs a, const uint4 *
       }
     }
     __syncthreads();
-    if (SAT && s_ovf) {  // CTA-uniform: a counter wrapped, redo the query exactly
-      if (tid == 0) atomicAdd(&g_vote_sat_redos, 1ull);
-      CarefulArgs ca;
-      ca.ntiles = a.ntiles, ca.W = a.W, ca.T = a.T, ca.L = a.L, ca.v = a.v, ca.cap = a.cap;
-      ca.leaves = a.leaves, ca.dir = a.dir, ca.cand = a.cand;
-      vote_pair_careful(ca, ps, pbase, pstride, q, cnt, cwords, &s_nc);
+    if (tid == 0) {
+      a.ncand[q] = s_nc;  // > cap means only cap ids were stored
+      // a counter wrapped: the query is listed for the exact redo kernel
+      if (SAT && s_ovf) redo[1 + atomicAdd(redo, 1)] = (int32_t)q;
     }
-    if (tid == 0) a.ncand[q] = s_nc;  // > cap means only cap ids were stored
     __syncthreads();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1577,6 +1580,24 @@ __global__ void __launch_bounds__(1024, 1) k_vote_pair(VoteArgs a, const uint4 *
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(512));
+  }
+}
+
+// The queries the saturating vote listed (a counter wrapped), redone exactly.
+__global__ void __launch_bounds__(1024, 1) k_vote_pair_redo(VoteArgs a, const uint4 *__restrict__ ps,
+                                                            const int32_t *__restrict__ pbase, int64_t pstride,
+                                                            const int32_t *__restrict__ redo) {
+  extern __shared__ uint4 vote_smem[];
+  uint32_t *cnt = reinterpret_cast<uint32_t *>(vote_smem);
+  __shared__ int s_nc;
+  const int cwords = spare_word0<1>(a.W);
+  const int m = redo[0];
+  for (int i = blockIdx.x; i < m; i += gridDim.x) {
+    const int64_t q = redo[1 + i];
+    if (threadIdx.x == 0) atomicAdd(&g_vote_sat_redos, 1ull);
+    vote_pair_careful(a, ps, pbase, pstride, q, cnt, cwords, &s_nc);
+    if (threadIdx.x == 0) a.ncand[q] = s_nc;
+    __syncthreads();
   }
 }
 }  // namespace mrpt
@@ -2131,13 +2152,27 @@ extern "C" int32_t mrpt_vote_pair(const uint32_t *ps, int64_t pstride, const uin
   a.dir = pdir;
   a.dbg = getenv("MRPT_VOTE_DBG") ? atoi(getenv("MRPT_VOTE_DBG")) : 0;
   const size_t smem = (size_t)((counter_words_host(CW, W) + 3) & ~3LL) * 4 + 128;  // + 32 spare words
-  typedef void (*pfn_t)(VoteArgs, const uint4 *, const int32_t *, int64_t);
+  typedef void (*pfn_t)(VoteArgs, const uint4 *, const int32_t *, int64_t, int32_t *);
   pfn_t fn = sat ? k_vote_pair<1, true>
                  : (CW == 1 ? k_vote_pair<1> : (CW == 3 ? k_vote_pair<3> : (CW == 2 ? k_vote_pair<2> : k_vote_pair<4>)));
-  if (sat) g_vote_sat_queries += nq;
+  cudaStream_t s = as_stream(stream);
+  int32_t *redo = nullptr;
+  if (sat) {  // the list of queries to redo exactly (count first)
+    if (nq >= (int64_t)1 << 31) return fail(MRPT_ESHAPE, "mrpt_vote_pair: too many queries in one call");
+    g_vote_sat_queries += nq;
+    keep_pool_warm();
+    if (cudaMallocAsync((void **)&redo, sizeof(int32_t) * (size_t)(nq + 1), s) != cudaSuccess)
+      return fail(MRPT_ECUDA, "mrpt_vote_pair: scratch allocation failed");
+    cudaMemsetAsync(redo, 0, sizeof(int32_t), s);
+  }
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t grid = nq < (int64_t)num_sms() ? nq : (int64_t)num_sms();
-  (count_launch(), fn<<<(unsigned)grid, 1024, smem, as_stream(stream)>>>(a, reinterpret_cast<const uint4 *>(ps), pbase,
-                                                                         pstride));
+  (count_launch(), fn<<<(unsigned)grid, 1024, smem, s>>>(a, reinterpret_cast<const uint4 *>(ps), pbase, pstride, redo));
+  if (sat) {
+    cudaFuncSetAttribute(k_vote_pair_redo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    (count_launch(), k_vote_pair_redo<<<(unsigned)grid, 1024, smem, s>>>(a, reinterpret_cast<const uint4 *>(ps), pbase,
+                                                                          pstride, redo));
+    cudaFreeAsync(redo, s);
+  }
   return launch_status("mrpt_vote_pair");
 }
