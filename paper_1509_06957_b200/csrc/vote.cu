@@ -1466,6 +1466,15 @@ __global__ void __launch_bounds__(1024, 1) k_vote_pair(VoteArgs a, const uint4 *
   uint4 *c4 = reinterpret_cast<uint4 *>(cnt);
   const uint32_t pw = pad_word + (uint32_t)lane;
   const uint4 padq = make_uint4(pw | (pw << 16), pw | (pw << 16), pw | (pw << 16), pw);
+  // SAT: counters start at kSatCross + 1 - v (see pair_bump).  The clear
+  // value comes back from shared memory as one register quad per clear (ptxas
+  // otherwise copies it into a fresh quad for every 16-byte store); written
+  // here, before the barrier below.
+  __shared__ uint4 s_cz;
+  if (SAT && tid == 32) {
+    const uint32_t c0 = (kSatCross - vm1) * 0x01010101u;
+    s_cz = make_uint4(c0, c0, c0, c0);
+  }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(&s_tmem)),
@@ -1476,10 +1485,13 @@ __global__ void __launch_bounds__(1024, 1) k_vote_pair(VoteArgs a, const uint4 *
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tslot = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
-  // SAT: counters start at kSatCross + 1 - v (see pair_bump)
-  const uint32_t c0 = SAT ? (kSatCross - vm1) * 0x01010101u : 0u;
   auto clear_counters = [&]() {
-    for (int i = tid; i < cwords / 4; i += 1024) c4[i] = make_uint4(c0, c0, c0, c0);
+    uint4 cz = make_uint4(0u, 0u, 0u, 0u);
+    if (SAT)
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(cz.x), "=r"(cz.y), "=r"(cz.z), "=r"(cz.w)
+                   : "r"((uint32_t)__cvta_generic_to_shared(&s_cz)));
+    for (int i = tid; i < cwords / 4; i += 1024) c4[i] = cz;
   };
   for (int64_t q = blockIdx.x; q < a.nq; q += gridDim.x) {
     const uint16_t *dl = nullptr;
