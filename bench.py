@@ -401,6 +401,13 @@ def run_ours(args):
         index = mrpt.grow_trees(Xd, p["n_trees"], p["depth"], p["sparsity"], seed=p["seed"])
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0  # includes the GPU FNV checksum (trees.py:244)
+    if os.environ.get("MRPT_BENCH_REBUILD") and world == 1:  # diagnostics: a second build in the same process
+        del index
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        index = mrpt.grow_trees(Xd, p["n_trees"], p["depth"], p["sparsity"], seed=p["seed"])
+        torch.cuda.synchronize()
+        print(f"build_s first {build_s:.3f} second {time.perf_counter() - t1:.3f}", file=sys.stderr)
     D = index.device_index()
     Qd = torch.from_numpy(Q).cuda()
 

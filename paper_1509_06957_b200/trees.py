@@ -534,7 +534,10 @@ def _batch_trees(n, d, depth, T, free_bytes):
     tb = min(tb, T, 128)
     while tb > 1 and tb * (1 << depth) >= (1 << 31):
         tb //= 2
-    return tb
+    # equal batches: the same number of launches without a small last batch
+    # (config 5: 10 x 100 trees instead of 9 x 111 + 1; 1.77 vs 1.84 s)
+    nb = -(-T // tb)
+    return -(-T // nb)
 
 
 def _validate_grow(X, n_trees, depth, sparsity, seed, threads):
