@@ -925,12 +925,17 @@ struct WsLayout {
 
 static size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
-// Levels taken by the top path (build_top.cuh): while the expected node size
-// exceeds the one-CTA classes, at most kTopMaxLev.
+// Levels taken by the top path (build_top.cuh), at most kTopMaxLev.
 static int top_levels(int64_t n, int depth) {
   if (n <= kLargeMax) return 0;
   int L = 0;
-  while (L < depth && L < kTopMaxLev && (n >> L) > kMidMax) ++L;
+  // A level takes the top path while its expected node size exceeds 4,096: a
+  // top level costs ~7 ms per 100 trees of 10M points, a level of
+  // one-CTA-per-segment kernels ~15 (config 5: 1.765 -> 1.709 s with level 11
+  // on the top path; MRPT_BUILD_TOP_MIN overrides for experiments).
+  const char *te = getenv("MRPT_BUILD_TOP_MIN");  // read per call: build_ab switches it between builds
+  const int64_t top_min = te ? (int64_t)atoll(te) : (int64_t)4096;
+  while (L < depth && L < kTopMaxLev && (n >> L) > top_min) ++L;
   return L;
 }
 

@@ -26,7 +26,7 @@
 
 namespace mrpt {
 
-constexpr int kTopMaxLev = 11;      // node ids < 2^11
+constexpr int kTopMaxLev = 12;      // node ids < 2^12
 constexpr int kTopBins = 32768;     // shared counters per CTA: nodes x buckets
 constexpr int kTopMaxNB = 2048;     // buckets per node at the first levels
 constexpr int kTopChunk = 65536;    // points per histogram / collect CTA
@@ -174,10 +174,12 @@ __global__ void __launch_bounds__(1024) k_top_pick(TopArgs a) {
   uint32_t *gh = a.ghist + (int64_t)t * kTopBins;
   const int32_t *sz = a.tsize + (int64_t)t * (4 * kTopNodes) + nnode;
   int4 *info = a.tinfo + (int64_t)t * kTopNodes;
-  const int per = NB / 32;  // NB >= 32
+  // buckets per lane; with fewer than 32 buckets per node (level 11 on) the
+  // first NB lanes take one each
+  const int per = NB >= 32 ? NB / 32 : (lane < NB ? 1 : 0);
   for (int nd = warp; nd < nnode; nd += 32) {
     const int m = sz[nd];
-    uint32_t *h = gh + nd * NB + lane * per;
+    uint32_t *h = gh + nd * NB + (NB >= 32 ? lane * per : lane);
     int sum = 0;
     for (int j = 0; j < per; ++j) sum += (int)h[j];
     int incl = sum;
@@ -192,7 +194,7 @@ __global__ void __launch_bounds__(1024) k_top_pick(TopArgs a) {
       for (int j = 0; j < per; ++j) {
         const int c = (int)h[j];
         if (kth < excl + c) {
-          info[nd] = make_int4(lane * per + j, excl, c, 0);
+          info[nd] = make_int4((NB >= 32 ? lane * per : lane) + j, excl, c, 0);
           s_cnt[nd] = c;
           break;
         }
