@@ -1078,7 +1078,8 @@ extern "C" int32_t mrpt_build_levels(const float *P, int64_t n, int32_t Tb, int3
     cudaFuncSetAttribute(k_top_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem);
     cudaFuncSetAttribute(k_top_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem);
     // stable grouping by node: low kTopDigit bits, then the rest
-    const int bitsA = Lc < kTopDigit ? Lc : kTopDigit, bitsB = Lc - bitsA;
+    // (6 + up to 6 bits; 7 + 6 for 13 levels)
+    const int bitsA = Lc <= 6 ? Lc : (Lc <= 12 ? 6 : kTopDigit), bitsB = Lc - bitsA;
     (count_launch(), k_top_count<true><<<grun, 512, 0, s>>>(ta, 0, bitsA));
     (count_launch(), k_top_scan<<<(unsigned)Tb, 1 << kTopDigit, 0, s>>>(ta, bitsA));
     (count_launch(), k_top_bounds<<<(unsigned)Tb, 1024, 0, s>>>(ta));

@@ -26,12 +26,12 @@
 
 namespace mrpt {
 
-constexpr int kTopMaxLev = 12;      // node ids < 2^12
+constexpr int kTopMaxLev = 13;      // node ids < 2^13
 constexpr int kTopBins = 32768;     // shared counters per CTA: nodes x buckets
 constexpr int kTopMaxNB = 2048;     // buckets per node at the first levels
 constexpr int kTopChunk = 65536;    // points per histogram / collect CTA
 constexpr int kTopBuf = 16384;      // staged list members per collect CTA
-constexpr int kTopDigit = 6;        // bits per pass of the final grouping
+constexpr int kTopDigit = 7;        // bits per pass of the final grouping (at most)
 constexpr int kTopNodes = 1 << (kTopMaxLev - 1);  // nodes of the last top level
 constexpr int kTopListSmall = 4096;
 constexpr int kTopListLarge = 47104;
@@ -237,7 +237,8 @@ __global__ void __launch_bounds__(1024) k_top_pick(TopArgs a) {
 __global__ void __launch_bounds__(1024, 1) k_top_collect(TopArgs a) {
   extern __shared__ uint32_t top_smem[];
   uint2 *buf = reinterpret_cast<uint2 *>(top_smem);  // kTopBuf x (node | rank << 16, key)
-  __shared__ int s_bsel[kTopNodes], s_loff[kTopNodes], s_cnt[kTopNodes], s_gb[kTopNodes];
+  __shared__ int s_cnt[kTopNodes], s_gb[kTopNodes];
+  __shared__ int16_t s_bsel[kTopNodes];  // selected bucket (< kTopMaxNB) or -1; list offsets stay in tinfo
   __shared__ int s_n;
   const int t = blockIdx.y, lev = a.lev, NB = a.NB;
   const int lane = threadIdx.x & 31;
@@ -247,8 +248,7 @@ __global__ void __launch_bounds__(1024, 1) k_top_collect(TopArgs a) {
   const int4 *info = a.tinfo + (int64_t)t * kTopNodes;
   for (int i = threadIdx.x; i < nnode; i += 1024) {
     const int4 f = info[i];
-    s_bsel[i] = f.z > 0 ? f.x : -1;
-    s_loff[i] = f.w;
+    s_bsel[i] = (int16_t)(f.z > 0 ? f.x : -1);
     s_cnt[i] = 0;
   }
   if (threadIdx.x == 0) s_n = 0;
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(1024, 1) k_top_collect(TopArgs a) {
     }
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      const bool hit = me[j] >= 0 && top_bucket(v[j], cr.x, sc, NB) == s_bsel[me[j]];
+      const bool hit = me[j] >= 0 && top_bucket(v[j], cr.x, sc, NB) == (int)s_bsel[me[j]];
       const unsigned bal = __ballot_sync(0xffffffffu, hit);
       if (bal) {
         int base = 0;
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(1024, 1) k_top_collect(TopArgs a) {
       for (int i = threadIdx.x; i < nnode; i += 1024) {
         const int c = s_cnt[i];
         if (c) {
-          s_gb[i] = s_loff[i] + atomicAdd(fill + i, c);
+          s_gb[i] = info[i].w + atomicAdd(fill + i, c);
           s_cnt[i] = 0;
         }
       }
@@ -510,20 +510,19 @@ __global__ void __launch_bounds__(512) k_top_scatter(TopArgs a, int shift, int b
     gbase[threadIdx.x] = a.table[((int64_t)t * a.nrun + blockIdx.x) * nb + threadIdx.x];
   }
   __syncthreads();
-  if (warp == 0) {  // exclusive scan of the totals over the digits (nb <= 64)
-    const int c0 = lane < nb ? lbase[lane] : 0, c1 = lane + 32 < nb ? lbase[lane + 32] : 0;
-    int i0 = c0, i1 = c1;
+  if (warp == 0) {  // exclusive scan of the totals over the digits (nb <= 2^kTopDigit)
+    int carry = 0;
+    for (int b0 = 0; b0 < nb; b0 += 32) {
+      const int c = b0 + lane < nb ? lbase[b0 + lane] : 0;
+      int inc = c;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int u0 = __shfl_up_sync(0xffffffffu, i0, o), u1 = __shfl_up_sync(0xffffffffu, i1, o);
-      if (lane >= o) {
-        i0 += u0;
-        i1 += u1;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
       }
+      if (b0 + lane < nb) lbase[b0 + lane] = carry + inc - c;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
     }
-    const int tot0 = __shfl_sync(0xffffffffu, i0, 31);
-    if (lane < nb) lbase[lane] = i0 - c0;
-    if (lane + 32 < nb) lbase[lane + 32] = tot0 + i1 - c1;
   }
   __syncthreads();
 #pragma unroll
