@@ -16,6 +16,18 @@ def device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_SMS = {}
+
+
+def sm_count():
+    """Streaming multiprocessors of the current device."""
+    torch = torch_mod()
+    dev = torch.cuda.current_device()
+    if dev not in _SMS:
+        _SMS[dev] = int(torch.cuda.get_device_properties(dev).multi_processor_count)
+    return _SMS[dev]
+
+
 def is_tensor(x):
     try:
         import torch

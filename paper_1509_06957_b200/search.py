@@ -222,6 +222,11 @@ def _check_batch_args(k, index, votes):
         raise ParameterError(f"vote threshold must lie in [1, {index.n_trees}], got {votes}")
 
 
+def _chunk_bytes():
+    """Scratch (leaves + candidate lists) of one query chunk of a batch."""
+    return int(os.environ.get("MRPT_CHUNK_BYTES", 1 << 30))
+
+
 def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None, size_class=None):
     """K2 -> K3 -> K4 over a device query block; returns device tensors
     (ids (nq,k) int64, dists (nq,k) float64, candidate_count (nq,) int32).
@@ -256,7 +261,12 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None, size_class=N
     bits_mode = choice in _BITS_ROUTES
     if chunk is None:
         per_q = 4 * (D.T + (bstride if bits_mode else cap))
-        chunk = max(1, min(nq, (1 << 30) // per_q))
+        chunk = max(1, min(nq, _chunk_bytes() // per_q))
+        # whole waves: the vote runs one CTA per SM and the filters up to four,
+        # each CTA striding over the chunk's queries
+        wave = 4 * _device.sm_count()
+        if chunk > wave and os.environ.get("MRPT_CHUNK_WAVES", "1") != "0":
+            chunk -= chunk % wave
     if (not bits_mode and choice is not None and nq >= 2 * _ORDER_MIN
             and os.environ.get("MRPT_QUERY_ORDER", "1") != "0" and D.vote_layout() is not None
             and nq * D.T * 4 <= (2 << 30)):
