@@ -287,33 +287,12 @@ __global__ void __launch_bounds__(1024, 1) k_top_collect(TopArgs a) {
   for (int64_t i0 = p0 + threadIdx.x; i0 - threadIdx.x < p1; i0 += (int64_t)U * 1024) {  // CTA-uniform trips
     float v[U];
     int me[U];
-    if ((a.n & 3) == 0) {
-      // element j = 4 g + c: the c-th of 4 consecutive points of group g
-      // (16-byte projection loads, 8-byte node-id loads; any order of a
-      // round's elements is fine -- the lists are unordered)
-      const int64_t r0 = i0 - threadIdx.x;  // the round's first point
 #pragma unroll
-      for (int g = 0; g < U / 4; ++g) {
-        const int64_t i = r0 + (int64_t)g * 4096 + 4 * (int64_t)threadIdx.x;
-        const bool in = i < p1;  // p1 is a multiple of 4
-        float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        ushort4 n4 = make_ushort4(0, 0, 0, 0);
-        if (in) {
-          v4 = __ldg(reinterpret_cast<const float4 *>(Pc + i));
-          if (lev >= 1) n4 = *reinterpret_cast<const ushort4 *>(nd + i);
-        }
-        v[4 * g] = v4.x, v[4 * g + 1] = v4.y, v[4 * g + 2] = v4.z, v[4 * g + 3] = v4.w;
-        me[4 * g] = in ? (int)n4.x : -1, me[4 * g + 1] = in ? (int)n4.y : -1;
-        me[4 * g + 2] = in ? (int)n4.z : -1, me[4 * g + 3] = in ? (int)n4.w : -1;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < U; ++j) {
-        const int64_t i = i0 + (int64_t)j * 1024;
-        const bool in = i < p1;
-        v[j] = in ? __ldg(Pc + i) : 0.f;
-        me[j] = in ? (lev >= 1 ? (int)nd[i] : 0) : -1;
-      }
+    for (int j = 0; j < U; ++j) {
+      const int64_t i = i0 + (int64_t)j * 1024;
+      const bool in = i < p1;
+      v[j] = in ? __ldg(Pc + i) : 0.f;
+      me[j] = in ? (lev >= 1 ? (int)nd[i] : 0) : -1;
     }
 #pragma unroll
     for (int j = 0; j < U; ++j) {
