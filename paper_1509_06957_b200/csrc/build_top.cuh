@@ -277,6 +277,15 @@ __global__ void __launch_bounds__(1024, 1) k_top_collect(TopArgs a) {
   }
   if (threadIdx.x == 0) s_n = 0;
   __syncthreads();
+  // shared addresses as 32-bit values, kept opaque; the slot counter's one is
+  // made lane-dependent (+ 0 ptxas cannot fold) so that its atomic stays a
+  // plain per-lane atomic
+  uint32_t bsel_s = (uint32_t)__cvta_generic_to_shared(s_bsel), cnt_s = (uint32_t)__cvta_generic_to_shared(s_cnt);
+  uint32_t buf_s = (uint32_t)__cvta_generic_to_shared(buf);
+  uint32_t lm_eq;
+  asm volatile("mov.u32 %0, %%lanemask_eq;" : "=r"(lm_eq));
+  uint32_t sn_lane = (uint32_t)__cvta_generic_to_shared(&s_n) + (uint32_t)(__popc(lm_eq) - 1);
+  asm volatile("" : "+r"(bsel_s), "+r"(cnt_s), "+r"(buf_s), "+r"(sn_lane));
   const float *Pc = a.P + ((int64_t)t * a.depth + lev) * a.n;
   const uint16_t *nd = a.node + (int64_t)t * a.n;
   const float2 cr = a.colrange[(int64_t)t * a.depth + lev];
@@ -287,24 +296,46 @@ __global__ void __launch_bounds__(1024, 1) k_top_collect(TopArgs a) {
   for (int64_t i0 = p0 + threadIdx.x; i0 - threadIdx.x < p1; i0 += (int64_t)U * 1024) {  // CTA-uniform trips
     float v[U];
     int me[U];
+    if (i0 - threadIdx.x + (int64_t)U * 1024 <= p1) {  // a whole round (CTA-uniform): no per-element range checks
 #pragma unroll
-    for (int j = 0; j < U; ++j) {
-      const int64_t i = i0 + (int64_t)j * 1024;
-      const bool in = i < p1;
-      v[j] = in ? __ldg(Pc + i) : 0.f;
-      me[j] = in ? (lev >= 1 ? (int)nd[i] : 0) : -1;
+      for (int j = 0; j < U; ++j) {
+        v[j] = __ldg(Pc + i0 + j * 1024);
+        me[j] = lev >= 1 ? (int)nd[i0 + j * 1024] : 0;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int64_t i = i0 + (int64_t)j * 1024;
+        const bool in = i < p1;
+        v[j] = in ? __ldg(Pc + i) : 0.f;
+        me[j] = in ? (lev >= 1 ? (int)nd[i] : 0) : -1;
+      }
     }
+    // (32-bit shared addresses and PTX atomics: through generic pointers the
+    // compiler rebuilds the shared window base per access and wraps the
+    // leader's reservation in a second warp aggregation -- 73 instructions
+    // per element where most elements of a deep level are hits)
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      const bool hit = me[j] >= 0 && top_bucket(v[j], cr.x, sc, NB) == (int)s_bsel[me[j]];
+      bool hit = false;
+      if (me[j] >= 0) {
+        int16_t bs;
+        asm volatile("ld.shared.s16 %0, [%1];" : "=h"(bs) : "r"(bsel_s + 2u * (uint32_t)me[j]));
+        hit = top_bucket(v[j], cr.x, sc, NB) == (int)bs;
+      }
       const unsigned bal = __ballot_sync(0xffffffffu, hit);
       if (bal) {
-        int base = 0;
-        if (lane == __ffs(bal) - 1) base = atomicAdd(&s_n, __popc(bal));
-        base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
+        const int leader = __ffs(bal) - 1;
+        uint32_t base = 0;
+        if (lane == leader)
+          asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(base) : "r"(sn_lane), "r"((uint32_t)__popc(bal)) : "memory");
+        base = __shfl_sync(0xffffffffu, base, leader);
         if (hit) {
-          const int lr = atomicAdd(&s_cnt[me[j]], 1);
-          buf[base + __popc(bal & lanemask_lt())] = make_uint2((uint32_t)me[j] | ((uint32_t)lr << 16), f2key(v[j]));
+          uint32_t lr;
+          asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(lr) : "r"(cnt_s + 4u * (uint32_t)me[j]), "r"(1u) : "memory");
+          const uint32_t at = buf_s + 8u * (base + (uint32_t)__popc(bal & lanemask_lt()));
+          asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(at), "r"((uint32_t)me[j] | (lr << 16)), "r"(f2key(v[j]))
+                       : "memory");
         }
       }
     }
