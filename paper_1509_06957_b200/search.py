@@ -265,8 +265,8 @@ def query_device(D, Qd, k, votes, chunk=None, out=None, timer=None, size_class=N
         # whole waves: the vote runs one CTA per SM and the filters up to four,
         # each CTA striding over the chunk's queries
         wave = 4 * _device.sm_count()
-        if chunk > wave and os.environ.get("MRPT_CHUNK_WAVES", "1") != "0":
-            chunk -= chunk % wave
+        if wave < chunk < nq and os.environ.get("MRPT_CHUNK_WAVES", "1") != "0":
+            chunk -= chunk % wave  # (a batch that fits one chunk stays one chunk)
     if (not bits_mode and choice is not None and nq >= 2 * _ORDER_MIN
             and os.environ.get("MRPT_QUERY_ORDER", "1") != "0" and D.vote_layout() is not None
             and nq * D.T * 4 <= (2 << 30)):
