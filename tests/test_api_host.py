@@ -167,3 +167,20 @@ def test_scan_route_availability(n, d, k, u8, want):
     from paper_1509_06957_b200.search import _scan_variants
 
     assert _scan_variants(_FakeIndex(n, d, u8), k) == want
+
+
+def test_build_batches_are_equal_sized():
+    """Trees per K1+K5 batch: as many as memory allows, but in equal batches
+    (no small last batch): config 5's 1000 trees go as 10 x 100, not 9 x 111 + 1."""
+    from paper_1509_06957_b200.trees import _batch_trees
+
+    n, d, depth, T = 10_000_000, 256, 13, 1000
+    per_tree = n * (4 * depth + 8) + 3 * n + (1 << 20)
+    tb = _batch_trees(n, d, depth, T, free_bytes=2 * 111 * per_tree)
+    assert tb == 100
+    assert _batch_trees(n, d, depth, 7, free_bytes=2 * 111 * per_tree) == 7
+    assert _batch_trees(n, d, depth, T, free_bytes=per_tree) == 1
+    for free_trees in (3, 17, 64, 200):
+        tb = _batch_trees(n, d, depth, T, free_bytes=2 * free_trees * per_tree)
+        nb = -(-T // tb)
+        assert tb <= min(free_trees, 128) and nb * tb - T < nb  # batches differ by at most one tree
