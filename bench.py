@@ -333,6 +333,14 @@ def run_reference(args):
         times.append(dt)
         done_all += done
     value = float(done_all / sum(times))
+    # the single-thread figure SURVEY 8(d) asks for beside the all-core one:
+    # the same call, one query after the other in this process, ~2 s
+    t0 = time.perf_counter()
+    n1 = 0
+    while time.perf_counter() - t0 < 2.0 and n1 < len(Q):
+        mrpt.approximate_knn(Q[n1], k, index, v)
+        n1 += 1
+    single = {"value": n1 / (time.perf_counter() - t0), "unit": "queries/s", "cores": 1, "queries": n1}
     line = {
         "impl": "reference", "metric": METRIC,
         "value": value, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
@@ -344,7 +352,7 @@ def run_reference(args):
                          "sample": f"each step: reference mrpt.approximate_knn, one query per call "
                                    f"(evaluation.py:199-205), forked pool of {cores} for "
                                    f"~{per_step:.1f}s; {done_all} queries over {args.steps} steps",
-                         "index": index_note},
+                         "index": index_note, "single_thread": single},
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
